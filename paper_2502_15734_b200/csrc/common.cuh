@@ -1,0 +1,73 @@
+// Shared device helpers for the cachecraft_b200 kernels (sm_100a).
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/cachecraft_b200.h"
+
+namespace ccb {
+
+// ---- error plumbing (thread-local last message, see cc_last_error) --------
+void set_error(const std::string& msg);
+int fail(int code, const std::string& msg);
+int check_launch(const char* what);
+
+#define CCB_REQUIRE(cond, msg) \
+  do {                         \
+    if (!(cond)) return ::ccb::fail(CC_E_ARG, msg); \
+  } while (0)
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// ---- scalar conversions --------------------------------------------------
+template <typename T> struct Acc { using type = float; };
+template <> struct Acc<double> { using type = double; };
+
+__device__ __forceinline__ float to_f(float x) { return x; }
+__device__ __forceinline__ double to_f(double x) { return x; }
+__device__ __forceinline__ float to_f(__nv_bfloat16 x) { return __bfloat162float(x); }
+
+template <typename T> __device__ __forceinline__ T from_f(float x);
+template <> __device__ __forceinline__ float from_f<float>(float x) { return x; }
+template <> __device__ __forceinline__ double from_f<double>(float x) { return x; }
+template <> __device__ __forceinline__ __nv_bfloat16 from_f<__nv_bfloat16>(float x) { return __float2bfloat16_rn(x); }
+template <typename T> __device__ __forceinline__ T from_d(double x);
+template <> __device__ __forceinline__ float from_d<float>(double x) { return (float)x; }
+template <> __device__ __forceinline__ double from_d<double>(double x) { return x; }
+template <> __device__ __forceinline__ __nv_bfloat16 from_d<__nv_bfloat16>(double x) { return __float2bfloat16_rn((float)x); }
+
+// cos/sin pair type of the RoPE table: double2 in fp64 mode, float2 otherwise
+template <typename T> struct CS { using type = float2; };
+template <> struct CS<double> { using type = double2; };
+
+__device__ __forceinline__ float gelu_tanh(float x) {
+  const float k0 = 0.7978845608028654f;  // sqrt(2/pi)
+  return 0.5f * x * (1.f + tanhf(k0 * (x + 0.044715f * x * x * x)));
+}
+__device__ __forceinline__ double gelu_tanh(double x) {
+  const double k0 = 0.7978845608028654;
+  return 0.5 * x * (1.0 + tanh(k0 * (x + 0.044715 * x * x * x)));
+}
+__device__ __forceinline__ float silu(float x) { return x / (1.f + __expf(-x)); }
+__device__ __forceinline__ double silu(double x) { return x / (1.0 + exp(-x)); }
+
+// ---- dtype dispatch -------------------------------------------------------
+#define CCB_DISPATCH_DTYPE(dtype, T, ...)                         \
+  [&]() -> int {                                                  \
+    switch (dtype) {                                              \
+      case CC_F64: { using T = double; return __VA_ARGS__(); }    \
+      case CC_F32: { using T = float; return __VA_ARGS__(); }     \
+      case CC_BF16: { using T = __nv_bfloat16; return __VA_ARGS__(); } \
+      default: return ::ccb::fail(CC_E_ARG, "unknown dtype");     \
+    }                                                             \
+  }()
+
+inline size_t dtype_size(int dtype) { return dtype == CC_F64 ? 8 : (dtype == CC_F32 ? 4 : 2); }
+
+int num_sms();
+
+}  // namespace ccb

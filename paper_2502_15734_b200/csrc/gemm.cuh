@@ -1,0 +1,10 @@
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace ccb {
+int gemm_tc_bf16(const void* A, int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc, int M, int N, int K,
+                 int epi, cudaStream_t st);
+int gemm_simt(const void* A, int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc, int M, int N, int K,
+              int epi, int dtype, cudaStream_t st);
+}  // namespace ccb

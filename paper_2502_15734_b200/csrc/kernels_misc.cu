@@ -1,0 +1,616 @@
+// Memory-bound kernels of the fix-up prefill path:
+//   K1  gather + RoPE of cached chunk K/V      (model.py:387-393, :404; rpe.py:34-44)
+//   K3e RoPE + scatter of fresh Q/K/V rows       (model.py:399-404)
+//   K2  RMSNorm                                  (model.py:121-122)
+//   K7  logits + greedy argmax                   (model.py:94-95, :455)
+//   K8b chunk statistics reduction               (harness.py:331-354, stats.py:68-106)
+//   K9  per-chunk top-k selection                (planner.py:17-34)
+//   K10 extract fresh chunk rows into pool blocks (model.py:487-492, store.py:30-53)
+// plus the RoPE table, embedding rows and an L2 flush helper.
+#include <float.h>
+#include <math.h>
+
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace ccb {
+
+template <typename T, int N>
+struct alignas(sizeof(T) * N) Vec {
+  T v[N];
+};
+
+// pick the widest vector (<=16 B) whose element count divides `n`
+template <typename T>
+inline int pick_vec(int n) {
+  int v = 16 / (int)sizeof(T);
+  while (v > 1 && (n % v) != 0) v /= 2;
+  return v;
+}
+
+#define CCB_DISPATCH_VEC(vec, V, ...)                  \
+  [&]() -> int {                                       \
+    switch (vec) {                                     \
+      case 8: { constexpr int V = 8; return __VA_ARGS__(); } \
+      case 4: { constexpr int V = 4; return __VA_ARGS__(); } \
+      case 2: { constexpr int V = 2; return __VA_ARGS__(); } \
+      default: { constexpr int V = 1; return __VA_ARGS__(); } \
+    }                                                  \
+  }()
+
+// ---------------------------------------------------------------------------
+// RoPE table: (cos, sin) of pos * inv_freq[j], angles in fp64 (rpe.py:34-37)
+// ---------------------------------------------------------------------------
+template <typename C>
+__global__ void rope_table_kernel(C* table, const double* inv_freq, int max_pos, int half) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (int64_t)max_pos * half) return;
+  int p = (int)(i / half), j = (int)(i % half);
+  double ang = (double)p * inv_freq[j];
+  double s, c;
+  sincos(ang, &s, &c);
+  C out;
+  out.x = c;
+  out.y = s;
+  table[i] = out;
+}
+
+// apply_rpe / remove_rpe in float64 (rpe.py:19-44)
+__global__ void rope_apply_f64_kernel(const double* __restrict__ x, double* __restrict__ y,
+                                      const int64_t* __restrict__ pos, int n, int width, int dh,
+                                      const double* __restrict__ inv_freq, double sign) {
+  int half = dh / 2;
+  int64_t total = (int64_t)n * (width / 2);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int r = (int)(i / (width / 2));
+    int rem = (int)(i % (width / 2));
+    int h = rem / half, j = rem % half;
+    double ang = sign * (double)pos[r] * inv_freq[j];
+    double s, c;
+    sincos(ang, &s, &c);
+    const double* row = x + (int64_t)r * width + h * dh;
+    double a = row[j], b = row[j + half];
+    double* out = y + (int64_t)r * width + h * dh;
+    out[j] = a * c - b * s;
+    out[j + half] = a * s + b * c;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K1: gather + RoPE.  One CTA per (gather item, layer).  Each CTA moves one
+// 16-row pool block: K rows -> kv_k (copy) and k_rot (rotated at the slot's
+// position), V rows -> kv_v.  Vectorised 16-byte accesses; pairs (j, j+half)
+// of a head are loaded together so the rotation needs no shuffles.
+// ---------------------------------------------------------------------------
+template <typename T, int V>
+__global__ void __launch_bounds__(256) gather_rope_kernel(
+    const T* __restrict__ pool, int64_t pool_layer_stride, int64_t pool_block_stride,
+    const cc_gather_item* __restrict__ items, int l0, const int32_t* __restrict__ slot_pos,
+    const int32_t* __restrict__ active_until, const typename CS<T>::type* __restrict__ table,
+    T* __restrict__ kv_k, T* __restrict__ kv_v, T* __restrict__ k_rot, int64_t req_layer_stride,
+    int kvw, int dh) {
+  using A = typename Acc<T>::type;
+  using VT = Vec<T, V>;
+  const cc_gather_item it = items[blockIdx.x];
+  const int l = l0 + blockIdx.y;
+  const int half = dh / 2;
+  const int hv = half / V;           // vectors per half-head
+  const int nh = kvw / dh;           // kv heads
+  const T* src = pool + (int64_t)l * pool_layer_stride + (int64_t)it.src_block * pool_block_stride;
+  const T* srcK = src;
+  const T* srcV = src + 16 * (int64_t)kvw;
+  const int64_t lofs = (int64_t)l * req_layer_stride;
+  // K: rotate pairs
+  const int k_units = it.n_rows * nh * hv;
+  for (int u = threadIdx.x; u < k_units; u += blockDim.x) {
+    int r = u / (nh * hv);
+    int rem = u % (nh * hv);
+    int h = rem / hv, jv = rem % hv;
+    int slot = it.dst_slot + r;
+    if (active_until[slot] > l) continue;
+    int64_t off = (int64_t)r * kvw + h * dh + jv * V;
+    VT x = *reinterpret_cast<const VT*>(srcK + off);
+    VT y = *reinterpret_cast<const VT*>(srcK + off + half);
+    int64_t doff = lofs + (int64_t)slot * kvw + h * dh + jv * V;
+    *reinterpret_cast<VT*>(kv_k + doff) = x;
+    *reinterpret_cast<VT*>(kv_k + doff + half) = y;
+    const typename CS<T>::type* cs = table + (int64_t)slot_pos[slot] * half + jv * V;
+    VT xr, yr;
+#pragma unroll
+    for (int e = 0; e < V; ++e) {
+      A c = (A)cs[e].x, s = (A)cs[e].y;
+      A a = (A)to_f(x.v[e]), b = (A)to_f(y.v[e]);
+      if constexpr (sizeof(A) == 8) {
+        xr.v[e] = from_d<T>(a * c - b * s);
+        yr.v[e] = from_d<T>(a * s + b * c);
+      } else {
+        xr.v[e] = from_f<T>(a * c - b * s);
+        yr.v[e] = from_f<T>(a * s + b * c);
+      }
+    }
+    *reinterpret_cast<VT*>(k_rot + doff) = xr;
+    *reinterpret_cast<VT*>(k_rot + doff + half) = yr;
+  }
+  // V: copy
+  const int vpr = kvw / V;
+  const int v_units = it.n_rows * vpr;
+  for (int u = threadIdx.x; u < v_units; u += blockDim.x) {
+    int r = u / vpr, c = u % vpr;
+    int slot = it.dst_slot + r;
+    if (active_until[slot] > l) continue;
+    VT x = *reinterpret_cast<const VT*>(srcV + (int64_t)r * kvw + c * V);
+    *reinterpret_cast<VT*>(kv_v + lofs + (int64_t)slot * kvw + c * V) = x;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Fresh rows after the QKV GEMM: rotate q and k, scatter k/v into the
+// request KV (position-free k, rotated k for attention).  One CTA per row.
+// ---------------------------------------------------------------------------
+template <typename T, int V>
+__global__ void __launch_bounds__(128) rope_scatter_kernel(
+    const T* __restrict__ qkv, int64_t ld, const int32_t* __restrict__ row_slot,
+    const int32_t* __restrict__ row_pos, const typename CS<T>::type* __restrict__ table,
+    T* __restrict__ q_rot, T* __restrict__ kv_k, T* __restrict__ kv_v, T* __restrict__ k_rot,
+    int Hq, int Hkv, int dh) {
+  using A = typename Acc<T>::type;
+  using VT = Vec<T, V>;
+  const int r = blockIdx.x;
+  const int half = dh / 2, hv = half / V;
+  const int slot = row_slot[r];
+  const typename CS<T>::type* cs_row = table + (int64_t)row_pos[r] * half;
+  const T* row = qkv + (int64_t)r * ld;
+  const int kvw = Hkv * dh;
+  const int rot_units = (Hq + Hkv) * hv;
+  for (int u = threadIdx.x; u < rot_units; u += blockDim.x) {
+    int h = u / hv, jv = u % hv;
+    bool is_q = h < Hq;
+    int64_t off = (int64_t)h * dh + jv * V;  // q heads then k heads are contiguous in the row
+    VT x = *reinterpret_cast<const VT*>(row + off);
+    VT y = *reinterpret_cast<const VT*>(row + off + half);
+    VT xr, yr;
+#pragma unroll
+    for (int e = 0; e < V; ++e) {
+      A c = (A)cs_row[jv * V + e].x, s = (A)cs_row[jv * V + e].y;
+      A a = (A)to_f(x.v[e]), b = (A)to_f(y.v[e]);
+      if constexpr (sizeof(A) == 8) {
+        xr.v[e] = from_d<T>(a * c - b * s);
+        yr.v[e] = from_d<T>(a * s + b * c);
+      } else {
+        xr.v[e] = from_f<T>(a * c - b * s);
+        yr.v[e] = from_f<T>(a * s + b * c);
+      }
+    }
+    if (is_q) {
+      T* dst = q_rot + (int64_t)r * Hq * dh + off;
+      *reinterpret_cast<VT*>(dst) = xr;
+      *reinterpret_cast<VT*>(dst + half) = yr;
+    } else {
+      int64_t koff = (int64_t)slot * kvw + (h - Hq) * dh + jv * V;
+      *reinterpret_cast<VT*>(kv_k + koff) = x;
+      *reinterpret_cast<VT*>(kv_k + koff + half) = y;
+      *reinterpret_cast<VT*>(k_rot + koff) = xr;
+      *reinterpret_cast<VT*>(k_rot + koff + half) = yr;
+    }
+  }
+  const T* vrow = row + (int64_t)(Hq + Hkv) * dh;
+  for (int c = threadIdx.x; c < kvw / V; c += blockDim.x) {
+    *reinterpret_cast<VT*>(kv_v + (int64_t)slot * kvw + c * V) =
+        *reinterpret_cast<const VT*>(vrow + c * V);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// embedding rows and RMSNorm
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void embed_kernel(const T* __restrict__ embed, const int32_t* __restrict__ tok,
+                             typename Acc<T>::type* __restrict__ hidden, int d) {
+  using A = typename Acc<T>::type;
+  const T* src = embed + (int64_t)tok[blockIdx.x] * d;
+  A* dst = hidden + (int64_t)blockIdx.x * d;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) dst[i] = (A)to_f(src[i]);
+}
+
+template <typename A>
+__device__ __forceinline__ A block_sum(A v, A* red) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) red[w] = v;
+  __syncthreads();
+  A t = 0;
+  if (threadIdx.x < 32) {
+    t = (lane < (int)(blockDim.x >> 5)) ? red[lane] : (A)0;
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (lane == 0) red[0] = t;
+  }
+  __syncthreads();
+  t = red[0];
+  __syncthreads();
+  return t;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) rmsnorm_kernel(const typename Acc<T>::type* __restrict__ h,
+                                                      T* __restrict__ out, const float* __restrict__ w,
+                                                      int d, double eps) {
+  using A = typename Acc<T>::type;
+  __shared__ A red[32];
+  const A* x = h + (int64_t)blockIdx.x * d;
+  A ss = 0;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) ss += x[i] * x[i];
+  ss = block_sum<A>(ss, red);
+  A inv = (A)1 / sqrt(ss / (A)d + (A)eps);
+  T* y = out + (int64_t)blockIdx.x * d;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) {
+    A v = x[i] * inv;
+    if (w) v *= (A)w[i];
+    if constexpr (sizeof(A) == 8) y[i] = from_d<T>(v); else y[i] = from_f<T>(v);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K7 logits (GEMV over the unembedding, bandwidth-bound) + argmax
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(256) logits_kernel(const typename Acc<T>::type* __restrict__ hrows,
+                                                     const float* __restrict__ w, double eps,
+                                                     const T* __restrict__ U, typename Acc<T>::type* __restrict__ logits,
+                                                     int m, int d, int vocab) {
+  using A = typename Acc<T>::type;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  A* xs = reinterpret_cast<A*>(smem_raw);  // [m][d] normed rows
+  __shared__ A red[32];
+  for (int r = 0; r < m; ++r) {
+    const A* x = hrows + (int64_t)r * d;
+    A ss = 0;
+    for (int i = threadIdx.x; i < d; i += blockDim.x) ss += x[i] * x[i];
+    ss = block_sum<A>(ss, red);
+    A inv = (A)1 / sqrt(ss / (A)d + (A)eps);
+    for (int i = threadIdx.x; i < d; i += blockDim.x) xs[r * d + i] = x[i] * inv * (w ? (A)w[i] : (A)1);
+  }
+  __syncthreads();
+  const int warps = blockDim.x >> 5, lane = threadIdx.x & 31;
+  for (int v = blockIdx.x * warps + (threadIdx.x >> 5); v < vocab; v += gridDim.x * warps) {
+    const T* u = U + (int64_t)v * d;
+    for (int r = 0; r < m; ++r) {
+      A acc = 0;
+      for (int i = lane; i < d; i += 32) acc += (A)to_f(u[i]) * xs[r * d + i];
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (lane == 0) logits[(int64_t)r * vocab + v] = acc;
+    }
+  }
+}
+
+template <typename A>
+__global__ void __launch_bounds__(1024) argmax_kernel(const A* __restrict__ logits, int32_t* __restrict__ out, int vocab) {
+  __shared__ A bv[32];
+  __shared__ int bi[32];
+  const A* x = logits + (int64_t)blockIdx.x * vocab;
+  A best = -INFINITY;
+  int idx = 0x7fffffff;
+  for (int i = threadIdx.x; i < vocab; i += blockDim.x) {
+    A v = x[i];
+    if (v > best || (v == best && i < idx)) { best = v; idx = i; }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    A ov = __shfl_xor_sync(0xffffffffu, best, o);
+    int oi = __shfl_xor_sync(0xffffffffu, idx, o);
+    if (ov > best || (ov == best && oi < idx)) { best = ov; idx = oi; }
+  }
+  int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) { bv[w] = best; bi[w] = idx; }
+  __syncthreads();
+  if (w == 0) {
+    best = lane < (int)(blockDim.x >> 5) ? bv[lane] : (A)-INFINITY;
+    idx = lane < (int)(blockDim.x >> 5) ? bi[lane] : 0x7fffffff;
+    for (int o = 16; o > 0; o >>= 1) {
+      A ov = __shfl_xor_sync(0xffffffffu, best, o);
+      int oi = __shfl_xor_sync(0xffffffffu, idx, o);
+      if (ov > best || (ov == best && oi < idx)) { best = ov; idx = oi; }
+    }
+    if (lane == 0) out[blockIdx.x] = idx;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K9 top-k: bitonic sort of (score desc, index asc) in shared memory, then an
+// ordered compaction of the selected indices (ascending output).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ bool precedes(double sa, int ia, double sb, int ib) {
+  return sa > sb || (sa == sb && ia < ib);
+}
+
+__global__ void __launch_bounds__(1024) topk_kernel(const double* __restrict__ scores,
+                                                    const int32_t* __restrict__ off,
+                                                    const int32_t* __restrict__ count,
+                                                    const int32_t* __restrict__ off_out,
+                                                    int32_t* __restrict__ out, int P) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* ks = reinterpret_cast<double*>(smem_raw);
+  int* ki = reinterpret_cast<int*>(ks + P);
+  unsigned char* sel = reinterpret_cast<unsigned char*>(ki + P);
+  __shared__ int warp_tot[32];
+  const int c = blockIdx.x;
+  const int base = off[c], n = off[c + 1] - off[c], k = count[c];
+  for (int i = threadIdx.x; i < P; i += blockDim.x) {
+    ks[i] = i < n ? scores[base + i] : -INFINITY;
+    ki[i] = i < n ? i : 0x7fffffff;
+    sel[i] = 0;
+  }
+  __syncthreads();
+  for (int size = 2; size <= P; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = threadIdx.x; i < P; i += blockDim.x) {
+        int j = i ^ stride;
+        if (j > i) {
+          bool up = (i & size) == 0;  // ascending in "precedes" order
+          bool swap = up ? precedes(ks[j], ki[j], ks[i], ki[i]) : precedes(ks[i], ki[i], ks[j], ki[j]);
+          if (swap) {
+            double ts = ks[i]; ks[i] = ks[j]; ks[j] = ts;
+            int ti = ki[i]; ki[i] = ki[j]; ki[j] = ti;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int i = threadIdx.x; i < k; i += blockDim.x) sel[ki[i]] = 1;
+  __syncthreads();
+  // ordered compaction: each thread owns a contiguous range of indices
+  const int per = (n + blockDim.x - 1) / blockDim.x;
+  const int lo = threadIdx.x * per, hi = min(n, lo + per);
+  int cnt = 0;
+  for (int i = lo; i < hi; ++i) cnt += sel[i];
+  // exclusive block scan of cnt
+  int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int incl = cnt;
+  for (int o = 1; o < 32; o <<= 1) {
+    int t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  if (lane == 31) warp_tot[w] = incl;
+  __syncthreads();
+  if (w == 0) {
+    int t = lane < (int)(blockDim.x >> 5) ? warp_tot[lane] : 0;
+    for (int o = 1; o < 32; o <<= 1) {
+      int u = __shfl_up_sync(0xffffffffu, t, o);
+      if (lane >= o) t += u;
+    }
+    warp_tot[lane] = t;  // inclusive totals per warp
+  }
+  __syncthreads();
+  int pos = incl - cnt + (w > 0 ? warp_tot[w - 1] : 0);
+  int32_t* o = out + off_out[c];
+  for (int i = lo; i < hi; ++i)
+    if (sel[i]) o[pos++] = i;
+}
+
+// ---------------------------------------------------------------------------
+// K8b chunk statistics from per-row segment masses (deterministic: each
+// output element is summed by one thread in row order)
+// ---------------------------------------------------------------------------
+__global__ void chunk_stats_kernel(const double* __restrict__ mass, int L, int n_rows, int n_seg,
+                                   const int32_t* __restrict__ row0, const int32_t* __restrict__ len,
+                                   const int32_t* __restrict__ seg_of, const int32_t* __restrict__ token_off,
+                                   double* __restrict__ inter, double* __restrict__ intra,
+                                   double* __restrict__ token) {
+  const int c = blockIdx.x;
+  const int r0 = row0[c], nr = len[c], sg = seg_of[c];
+  const int W = n_seg + 1;
+  // inter [c][l][j]
+  for (int t = threadIdx.x; t < L * n_seg; t += blockDim.x) {
+    int l = t / n_seg, j = t % n_seg;
+    double s = 0;
+    if (j < sg)
+      for (int r = 0; r < nr; ++r) s += mass[((int64_t)l * n_rows + r0 + r) * W + j];
+    inter[((int64_t)c * L + l) * n_seg + j] = s;
+  }
+  for (int l = threadIdx.x; l < L; l += blockDim.x) {
+    double s = 0;
+    for (int r = 0; r < nr; ++r) {
+      const double* m = mass + ((int64_t)l * n_rows + r0 + r) * W;
+      s += m[sg] - m[n_seg];
+    }
+    intra[(int64_t)c * L + l] = s;
+  }
+  for (int t = threadIdx.x; t < nr; t += blockDim.x) {
+    double s = 0;
+    for (int l = 0; l < L; ++l) {
+      const double* m = mass + ((int64_t)l * n_rows + r0 + t) * W;
+      double sl = 0;
+      for (int j = 0; j < sg; ++j) sl += m[j];
+      s += sl;
+    }
+    token[token_off[c] + t] = s;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K10: request rows -> fresh pool blocks (zero-padded to 16 rows)
+// ---------------------------------------------------------------------------
+template <typename T, int V>
+__global__ void __launch_bounds__(256) extract_kernel(const T* __restrict__ kv_k, const T* __restrict__ kv_v,
+                                                      int64_t req_layer_stride, int start, int n_rows,
+                                                      const int32_t* __restrict__ blocks, T* __restrict__ pool,
+                                                      int64_t pool_layer_stride, int64_t pool_block_stride, int kvw) {
+  using VT = Vec<T, V>;
+  const int b = blockIdx.x, l = blockIdx.y;
+  T* dst = pool + (int64_t)l * pool_layer_stride + (int64_t)blocks[b] * pool_block_stride;
+  const int vpr = kvw / V;
+  for (int u = threadIdx.x; u < 2 * 16 * vpr; u += blockDim.x) {
+    int kv = u / (16 * vpr);
+    int rem = u % (16 * vpr);
+    int r = rem / vpr, cidx = rem % vpr;
+    int row = b * 16 + r;
+    VT x;
+    if (row < n_rows) {
+      const T* src = (kv ? kv_v : kv_k) + (int64_t)l * req_layer_stride + (int64_t)(start + row) * kvw + cidx * V;
+      x = *reinterpret_cast<const VT*>(src);
+    } else {
+#pragma unroll
+      for (int e = 0; e < V; ++e) x.v[e] = from_f<T>(0.f);
+    }
+    *reinterpret_cast<VT*>(dst + (int64_t)kv * 16 * kvw + (int64_t)r * kvw + cidx * V) = x;
+  }
+}
+
+__global__ void flush_kernel(int4* p, size_t n, int seed) {
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    p[i] = make_int4(seed, (int)i, seed, (int)i);
+}
+
+}  // namespace ccb
+
+using namespace ccb;
+
+extern "C" {
+
+int cc_rope_table(void* table, const double* inv_freq, int max_pos, int half, int dtype, void* stream) {
+  CCB_REQUIRE(table && inv_freq && max_pos > 0 && half > 0, "rope_table: bad arguments");
+  int64_t total = (int64_t)max_pos * half;
+  int grid = (int)((total + 255) / 256);
+  if (dtype == CC_F64)
+    rope_table_kernel<double2><<<grid, 256, 0, as_stream(stream)>>>((double2*)table, inv_freq, max_pos, half);
+  else
+    rope_table_kernel<float2><<<grid, 256, 0, as_stream(stream)>>>((float2*)table, inv_freq, max_pos, half);
+  return check_launch("rope_table");
+}
+
+int cc_rope_apply_f64(const double* x, double* y, const int64_t* positions, int n, int width, int d_head,
+                      const double* inv_freq, int sign, void* stream) {
+  CCB_REQUIRE(d_head > 0 && d_head % 2 == 0 && width % d_head == 0, "rope_apply: bad head width");
+  if (n == 0) return 0;
+  int64_t total = (int64_t)n * (width / 2);
+  int grid = (int)std::min<int64_t>((total + 255) / 256, 65535);
+  rope_apply_f64_kernel<<<grid, 256, 0, as_stream(stream)>>>(x, y, positions, n, width, d_head, inv_freq,
+                                                             sign >= 0 ? 1.0 : -1.0);
+  return check_launch("rope_apply_f64");
+}
+
+int cc_gather_rope_kv(const void* pool, int64_t pool_layer_stride, int64_t pool_block_stride,
+                      const cc_gather_item* items, int n_items, int l0, int l1, const int32_t* slot_pos,
+                      const int32_t* active_until, const void* rope_table, void* kv_k, void* kv_v, void* k_rot,
+                      int64_t req_layer_stride, int kv_width, int d_head, int dtype, void* stream) {
+  CCB_REQUIRE(d_head > 0 && d_head % 2 == 0 && kv_width % d_head == 0, "gather_rope_kv: bad head width");
+  CCB_REQUIRE(l1 >= l0 && l0 >= 0, "gather_rope_kv: bad layer range");
+  if (n_items == 0 || l1 == l0) return 0;
+  CCB_REQUIRE(n_items <= 0x7fffffff && (l1 - l0) <= 65535, "gather_rope_kv: grid too large");
+  return CCB_DISPATCH_DTYPE(dtype, T, [&] {
+    int vec = std::min(pick_vec<T>(d_head / 2), pick_vec<T>(kv_width));
+    return CCB_DISPATCH_VEC(vec, V, [&] {
+      dim3 grid(n_items, l1 - l0);
+      gather_rope_kernel<T, V><<<grid, 256, 0, as_stream(stream)>>>(
+          (const T*)pool, pool_layer_stride, pool_block_stride, items, l0, slot_pos, active_until,
+          (const typename CS<T>::type*)rope_table, (T*)kv_k, (T*)kv_v, (T*)k_rot, req_layer_stride, kv_width,
+          d_head);
+      return check_launch("gather_rope_kv");
+    });
+  });
+}
+
+int cc_rope_scatter_qkv(const void* qkv, int64_t ld_qkv, int n_rows, const int32_t* row_slot, const int32_t* row_pos,
+                        const void* rope_table, void* q_rot, void* kv_k, void* kv_v, void* k_rot, int n_heads,
+                        int n_kv_heads, int d_head, int dtype, void* stream) {
+  CCB_REQUIRE(d_head > 0 && d_head % 2 == 0, "rope_scatter: bad head width");
+  if (n_rows == 0) return 0;
+  return CCB_DISPATCH_DTYPE(dtype, T, [&] {
+    int vec = std::min(pick_vec<T>(d_head / 2), pick_vec<T>((int)ld_qkv));
+    return CCB_DISPATCH_VEC(vec, V, [&] {
+      rope_scatter_kernel<T, V><<<n_rows, 128, 0, as_stream(stream)>>>(
+          (const T*)qkv, ld_qkv, row_slot, row_pos, (const typename CS<T>::type*)rope_table, (T*)q_rot,
+          (T*)kv_k, (T*)kv_v, (T*)k_rot, n_heads, n_kv_heads, d_head);
+      return check_launch("rope_scatter_qkv");
+    });
+  });
+}
+
+int cc_embed_rows(const void* embed, const int32_t* tokens, void* hidden, int n_rows, int d, int dtype, void* stream) {
+  if (n_rows == 0) return 0;
+  return CCB_DISPATCH_DTYPE(dtype, T, [&] {
+    embed_kernel<T><<<n_rows, 256, 0, as_stream(stream)>>>((const T*)embed, tokens,
+                                                          (typename Acc<T>::type*)hidden, d);
+    return check_launch("embed_rows");
+  });
+}
+
+int cc_rmsnorm(const void* hidden, void* out, const float* weight, int n_rows, int d, double eps, int dtype,
+               void* stream) {
+  if (n_rows == 0) return 0;
+  return CCB_DISPATCH_DTYPE(dtype, T, [&] {
+    rmsnorm_kernel<T><<<n_rows, 256, 0, as_stream(stream)>>>((const typename Acc<T>::type*)hidden, (T*)out,
+                                                            weight, d, eps);
+    return check_launch("rmsnorm");
+  });
+}
+
+int cc_logits_argmax(const void* hidden_rows, const float* norm_w, double eps, const void* unembed, void* logits,
+                     int32_t* argmax, int m, int d, int vocab, int dtype, void* stream) {
+  CCB_REQUIRE(m >= 1 && m <= 8, "logits_argmax: 1..8 rows");
+  return CCB_DISPATCH_DTYPE(dtype, T, [&] {
+    using A = typename Acc<T>::type;
+    size_t smem = (size_t)m * d * sizeof(A);
+    CCB_REQUIRE(smem <= 200 * 1024, "logits_argmax: rows too wide");
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(logits_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int grid = std::min((vocab + 7) / 8, num_sms() * 8);
+    logits_kernel<T><<<grid, 256, smem, as_stream(stream)>>>((const A*)hidden_rows, norm_w, eps,
+                                                            (const T*)unembed, (A*)logits, m, d, vocab);
+    int rc = check_launch("logits");
+    if (rc) return rc;
+    if (argmax) {
+      argmax_kernel<A><<<m, 1024, 0, as_stream(stream)>>>((const A*)logits, argmax, vocab);
+      return check_launch("argmax");
+    }
+    return 0;
+  });
+}
+
+int cc_topk_select(const double* scores, const int32_t* off, const int32_t* count, const int32_t* off_out,
+                   int32_t* out, int n_chunks, int max_len, void* stream) {
+  CCB_REQUIRE(max_len <= 8192, "topk_select: chunk longer than 8192 tokens");
+  if (n_chunks == 0) return 0;
+  int P = 1;
+  while (P < std::max(max_len, 1)) P <<= 1;
+  size_t smem = (size_t)P * (sizeof(double) + sizeof(int) + 1);
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  topk_kernel<<<n_chunks, 1024, smem, as_stream(stream)>>>(scores, off, count, off_out, out, P);
+  return check_launch("topk_select");
+}
+
+int cc_chunk_stats(const double* mass, int L, int n_rows, int n_seg, const int32_t* row0, const int32_t* len,
+                   const int32_t* seg_of, const int32_t* token_off, int n_chunks, double* inter, double* intra,
+                   double* token, void* stream) {
+  if (n_chunks == 0) return 0;
+  chunk_stats_kernel<<<n_chunks, 256, 0, as_stream(stream)>>>(mass, L, n_rows, n_seg, row0, len, seg_of,
+                                                              token_off, inter, intra, token);
+  return check_launch("chunk_stats");
+}
+
+int cc_extract_to_pool(const void* kv_k, const void* kv_v, int64_t req_layer_stride, int L, int start, int n_rows,
+                       const int32_t* blocks, int n_blocks, void* pool, int64_t pool_layer_stride,
+                       int64_t pool_block_stride, int kv_width, int dtype, void* stream) {
+  CCB_REQUIRE(n_blocks * 16 >= n_rows, "extract_to_pool: not enough blocks");
+  if (n_blocks == 0) return 0;
+  return CCB_DISPATCH_DTYPE(dtype, T, [&] {
+    int vec = pick_vec<T>(kv_width);
+    return CCB_DISPATCH_VEC(vec, V, [&] {
+      dim3 grid(n_blocks, L);
+      extract_kernel<T, V><<<grid, 256, 0, as_stream(stream)>>>((const T*)kv_k, (const T*)kv_v, req_layer_stride,
+                                                               start, n_rows, blocks, (T*)pool, pool_layer_stride,
+                                                               pool_block_stride, kv_width);
+      return check_launch("extract_to_pool");
+    });
+  });
+}
+
+int cc_flush_l2(void* scratch, size_t bytes, void* stream) {
+  size_t n = bytes / sizeof(int4);
+  flush_kernel<<<num_sms() * 4, 512, 0, as_stream(stream)>>>((int4*)scratch, n, 7);
+  return check_launch("flush_l2");
+}
+
+}  // extern "C"

@@ -1,0 +1,428 @@
+"""Device execution of the chunk-cache fix-up prefill (model.py:348-442).
+
+Data layout in HBM for one request (n slots, L layers, kvw = Hkv * dh):
+  * ``hidden`` [n_rows, d] f32 (f64 in fp64 mode): residual stream of the
+    rows whose Q/K/V are ever recomputed, ordered by (-depth, slot) so the
+    rows active at layer l are always the prefix ``hidden[:n_act[l]]``.
+  * ``kv_k`` / ``kv_v`` [L, n, kvw]: the returned position-free KV (cached
+    rows copied from the pool, active rows freshly computed = cache repair).
+  * ``k_rot`` [L, n, kvw]: keys rotated at their slot position for attention.
+Per layer: RMSNorm -> QKV GEMM -> RoPE/scatter -> attention -> o_proj GEMM
+(+residual) -> RMSNorm -> gate/up GEMM (+SwiGLU or GELU) -> down GEMM
+(+residual).  One K1 launch gathers+rotates every cached block for all
+layers before the loop.  Every tensor op is a CUDA kernel from
+libcc_b200.so; torch only allocates memory and provides the stream.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _native as N
+from .errors import PlanError, ShapeError
+from .model import BLOCK, FULL_DEPTH, AttentionRecord, ChunkCache, KVCache, Model, PrefillResult, _Payload
+
+_GATHER_DT = np.dtype([("src_block", "<i4"), ("dst_slot", "<i4"), ("n_rows", "<i4"), ("pad", "<i4")])
+
+
+class DevicePlan:
+    """Host-resolved index arrays of one request, uploaded in a single copy."""
+
+    def __init__(self, model: Model, token_ids, positions, is_pad, mask, depth, seg_slots, seg_caches, question_span):
+        import torch
+
+        cfg = model.config
+        L = cfg.n_layers
+        n = int(token_ids.size)
+        self.n = n
+        depth_eff = np.where(depth == FULL_DEPTH, L, depth).astype(np.int64)
+        rows = np.flatnonzero(mask)
+        order = np.argsort(-depth_eff[rows], kind="stable")
+        rows = rows[order]
+        self.rows = rows  # slot of each hidden row, (-depth, slot) order
+        self.n_rows = int(rows.size)
+        rd = depth_eff[rows]
+        self.n_act = [int(np.count_nonzero(rd > l)) for l in range(L)]
+        active_until = np.where(mask, depth_eff, 0).astype(np.int32)
+        key_pos = np.where(is_pad, 0, positions).astype(np.int32)
+        self.max_pos = int(key_pos.max()) + 1 if n else 1
+        items = []
+        for (start, _), payload in zip(seg_slots, seg_caches):
+            if payload is None:
+                continue
+            for b in range(len(payload.blocks)):
+                nr = min(BLOCK, payload.n_slots - BLOCK * b)
+                if nr > 0:
+                    items.append((int(payload.blocks[b]), start + BLOCK * b, nr, 0))
+        self.items = np.array(items, dtype=_GATHER_DT)
+        self.n_items = len(items)
+        self.n_cached_rows = int(sum(it[2] for it in items))
+        # pack every int32 array into one host buffer -> one H2D copy
+        parts = {
+            "row_slot": rows.astype(np.int32),
+            "row_pos": positions[rows].astype(np.int32),
+            "row_tok": token_ids[rows].astype(np.int32),
+            "slot_pos": key_pos,
+            "active_until": active_until,
+            "items": self.items.view(np.int32).reshape(-1),
+        }
+        self.stats_segments = None
+        self.stats_rows = np.zeros(0, np.int32)
+        offs, cur = {}, 0
+        for k, a in parts.items():
+            offs[k] = (cur, a.size)
+            cur += -(-max(a.size, 1) // 4) * 4  # keep 16-byte alignment
+        host = np.zeros(cur, np.int32)
+        for k, a in parts.items():
+            o, s = offs[k]
+            host[o:o + s] = a
+        pad_bytes = -(-n // 16) * 16
+        host_pad = np.zeros(pad_bytes, np.uint8)
+        host_pad[:n] = is_pad
+        self.h2d_bytes = host.nbytes + host_pad.nbytes
+        pin = torch.from_numpy(host).pin_memory()
+        dev = pin.to(model.device, non_blocking=True)
+        pin_pad = torch.from_numpy(host_pad).pin_memory()
+        self.key_pad = pin_pad.to(model.device, non_blocking=True)
+        self.has_pad = bool(is_pad.any())
+        self._keep = (pin, pin_pad)
+        self.d = {k: dev[o:o + s] for k, (o, s) in offs.items()}
+
+
+class LazyAttention:
+    """Device operands kept per layer to materialise softmax weights."""
+
+    def __init__(self, model, plan, k_rot):
+        self.model, self.plan, self.k_rot = model, plan, k_rot
+        self.q = {}
+        self.lse = {}
+
+    def materialize(self, layer: int) -> np.ndarray:
+        import torch
+
+        cfg = self.model.config
+        n_l = self.plan.n_act[layer]
+        H = cfg.n_heads
+        if n_l == 0:
+            return np.zeros((H, 0, self.plan.n))
+        probs = torch.empty((H, n_l, self.plan.n), dtype=self.model.hidden_dtype, device=self.model.device)
+        N.call("cc_attention_probs", N.ptr(self.q[layer]), N.ptr(self.k_rot[layer]), N.ptr(self.plan.d["row_slot"]),
+               N.ptr(self.plan.key_pad) if self.plan.has_pad else None, N.ptr(self.lse[layer]), N.ptr(probs), n_l,
+               self.plan.n, H, cfg.kv_heads(), cfg.head_dim(), self.model.dtype_code, N.stream_ptr())
+        order = np.argsort(self.plan.rows[:n_l], kind="stable")
+        return probs.double().cpu().numpy()[:, order]
+
+    def materialize_all(self) -> list:
+        if not self.q:
+            raise PlanError("attention weights were not recorded; call prefill(..., record_attention=True)")
+        return [self.materialize(l) for l in range(self.model.config.n_layers)]
+
+
+def _workspace(model: Model, plan: DevicePlan):
+    import torch
+
+    cfg = model.config
+    L, n, nr = cfg.n_layers, plan.n, max(plan.n_rows, 1)
+    T, Hd = model.torch_dtype, model.hidden_dtype
+    d, q, kv, ff = cfg.d_model, cfg.q_width(), cfg.kv_width(), cfg.ff_dim()
+    dev = model.device
+    e = torch.empty
+    return {
+        "hidden": e((nr, d), dtype=Hd, device=dev),
+        "kv_k": e((L, n, kv), dtype=T, device=dev),
+        "kv_v": e((L, n, kv), dtype=T, device=dev),
+        "k_rot": e((L, n, kv), dtype=T, device=dev),
+        "xn": e((nr, d), dtype=T, device=dev),
+        "qkv": e((nr, q + 2 * kv), dtype=T, device=dev),
+        "q_rot": e((nr, q), dtype=T, device=dev),
+        "ctx": e((nr, q), dtype=T, device=dev),
+        "act": e((nr, ff), dtype=T, device=dev),
+        "lse": e((nr, cfg.n_heads), dtype=Hd, device=dev),
+    }
+
+
+def _record_default(model: Model, plan: DevicePlan) -> bool:
+    cfg = model.config
+    bytes_q = sum(plan.n_act) * cfg.q_width() * model.torch_dtype.itemsize
+    return plan.n <= 8192 and bytes_q <= (256 << 20)
+
+
+def execute(model: Model, plan: DevicePlan, ws: dict, *, record=False, record_values=False, stats=False,
+            gemm_impl=0, attn_impl=0):
+    """Launch the per-layer pipeline on the current stream.  Returns the
+    LazyAttention (if recording), value trace list and stats masses."""
+    import torch
+
+    cfg = model.config
+    L, n = cfg.n_layers, plan.n
+    H, Hkv, dh, d = cfg.n_heads, cfg.kv_heads(), cfg.head_dim(), cfg.d_model
+    qw, kvw, ff = cfg.q_width(), cfg.kv_width(), cfg.ff_dim()
+    dt = model.dtype_code
+    s = N.stream_ptr()
+    P = N.ptr
+    D = plan.d
+    pool = model.pool
+    rope = model.rope_table(plan.max_pos)
+    hidden, kv_k, kv_v, k_rot = ws["hidden"], ws["kv_k"], ws["kv_v"], ws["k_rot"]
+    xn, qkv, q_rot, ctx, act, lse = ws["xn"], ws["qkv"], ws["q_rot"], ws["ctx"], ws["act"], ws["lse"]
+    if plan.n_rows:
+        N.call("cc_embed_rows", P(model.w["embed"]), P(D["row_tok"]), P(hidden), plan.n_rows, d, dt, s)
+    if plan.n_items:
+        N.call("cc_gather_rope_kv", P(pool.storage), pool.layer_stride, pool.block_stride, P(D["items"]),
+               plan.n_items, 0, L, P(D["slot_pos"]), P(D["active_until"]), P(rope), P(kv_k), P(kv_v), P(k_rot),
+               n * kvw, kvw, dh, dt, s)
+    lazy = LazyAttention(model, plan, k_rot) if record else None
+    vtrace = [] if record_values else None
+    n_stats = plan.stats_rows.size if stats else 0
+    n_seg = len(plan.stats_segments) if (stats and plan.stats_segments) else 0
+    mass = torch.zeros((L, max(n_stats, 1), n_seg + 1), dtype=torch.float64, device=model.device) if n_stats else None
+    key_pad = P(plan.key_pad) if plan.has_pad else None
+    eps = cfg.rms_eps
+    for l in range(L):
+        lw = model.w["layers"][l]
+        n_l = plan.n_act[l]
+        if n_l == 0:
+            if record_values:
+                vtrace.append((kv_v[l], None))
+            continue
+        N.call("cc_rmsnorm", P(hidden), P(xn), P(lw.get("attn_norm")), n_l, d, eps, dt, s)
+        N.call("cc_gemm", P(xn), d, P(lw["w_qkv"]), d, P(qkv), qw + 2 * kvw, n_l, qw + 2 * kvw, d, N.EPI_STORE, dt,
+               gemm_impl, s)
+        N.call("cc_rope_scatter_qkv", P(qkv), qw + 2 * kvw, n_l, P(D["row_slot"]), P(D["row_pos"]), P(rope), P(q_rot),
+               P(kv_k[l]), P(kv_v[l]), P(k_rot[l]), H, Hkv, dh, dt, s)
+        N.call("cc_attention", P(q_rot), P(k_rot[l]), P(kv_v[l]), P(D["row_slot"]), key_pad, P(ctx), P(lse), n_l, n,
+               H, Hkv, dh, dt, attn_impl, s)
+        if n_stats:
+            N.call("cc_segment_mass", P(q_rot), P(k_rot[l]), P(D["row_slot"]), key_pad, P(lse), P(D["seg_lo"]),
+                   P(D["seg_hi"]), n_seg, P(D["stats_rows"]), n_stats, P(mass[l]), n, H, Hkv, dh, dt, s)
+        if record:
+            lazy.q[l] = q_rot[:n_l].clone()
+            lazy.lse[l] = lse[:n_l].clone()
+        if record_values:
+            vtrace.append((kv_v[l], ctx[:n_l].clone()))
+        N.call("cc_gemm", P(ctx), qw, P(lw["w_o"]), qw, P(hidden), d, n_l, d, qw, N.EPI_RESID_ADD, dt, gemm_impl, s)
+        N.call("cc_rmsnorm", P(hidden), P(xn), P(lw.get("mlp_norm")), n_l, d, eps, dt, s)
+        if cfg.mlp == "swiglu":
+            N.call("cc_gemm", P(xn), d, P(lw["w_gu"]), d, P(act), ff, n_l, 2 * ff, d, N.EPI_SWIGLU, dt, gemm_impl, s)
+        else:
+            N.call("cc_gemm", P(xn), d, P(lw["w_up"]), d, P(act), ff, n_l, ff, d, N.EPI_GELU, dt, gemm_impl, s)
+        N.call("cc_gemm", P(act), ff, P(lw["w_down"]), ff, P(hidden), d, n_l, d, ff, N.EPI_RESID_ADD, dt, gemm_impl, s)
+    return lazy, vtrace, mass
+
+
+def _payloads(model: Model, request):
+    cfg = model.config
+    out = []
+    for seg in request.segments:
+        c = seg.cache
+        if c is None:
+            out.append(None)
+            continue
+        if c.n_layers != cfg.n_layers:
+            raise PlanError(f"injected cache has {c.n_layers} layers, model has {cfg.n_layers}")
+        if c.width != cfg.kv_width():
+            raise ShapeError("injected cache width != kv width (d_model for MHA)")
+        out.append(c.device_payload(model))
+    return out
+
+
+def run_prefill(model: Model, request, record_values: bool = False, record_attention="auto", stats="auto",
+                first_token: bool = False, gemm_impl: int = 0, attn_impl: int = 0) -> PrefillResult:
+    import torch
+
+    N.require_cuda()
+    cfg = model.config
+    payloads = _payloads(model, request)
+    fresh = [i for i, seg in enumerate(request.segments) if seg.cache is None]
+    if stats == "auto":
+        stats = bool(fresh)
+    stats_segments = None
+    if stats:
+        stats_segments = list(request.segment_slots)
+        if request.question_span[1] > request.question_span[0]:
+            stats_segments.append(tuple(request.question_span))
+        # only fully recomputed spans can carry stats rows (stats.py:55-65)
+        ok = request.recompute_mask & (np.where(request.recompute_depth == FULL_DEPTH, cfg.n_layers,
+                                                 request.recompute_depth) >= cfg.n_layers)
+        stats_rows_spans = [(lo, hi) for (lo, hi) in stats_segments if hi > lo and ok[lo:hi].all()]
+    plan = DevicePlan(model, request.token_ids, request.positions, request.is_pad, request.recompute_mask,
+                      request.recompute_depth, request.segment_slots, payloads, request.question_span)
+    if stats:
+        plan.stats_segments = stats_segments
+        _attach_stats_rows(model, plan, stats_rows_spans)
+    if record_attention == "auto":
+        record_attention = _record_default(model, plan)
+    ws = _workspace(model, plan)
+    lazy, vtrace, mass = execute(model, plan, ws, record=bool(record_attention), record_values=record_values,
+                                 stats=bool(stats), gemm_impl=gemm_impl, attn_impl=attn_impl)
+    extras = {"plan": plan, "ws": ws, "mass": mass, "stats_spans": stats_rows_spans if stats else None}
+    q0, q1 = request.question_span
+    if first_token and q1 > q0:
+        r = int(np.flatnonzero(plan.rows == q1 - 1)[0])
+        if plan.n_act[-1] <= r:
+            raise PlanError("the question's last row is not computed through every layer")
+        logits, tok = _logits_rows(model, ws["hidden"][r:r + 1])
+        extras["logits_last"] = logits
+        extras["first_token_dev"] = tok
+        extras["first_token"] = int(tok.item())
+    L = cfg.n_layers
+    attn = AttentionRecord(query_slots=[np.sort(plan.rows[:plan.n_act[l]]) for l in range(L)], _lazy=lazy)
+    if lazy is None:
+        attn._lazy = LazyAttention(model, plan, ws["k_rot"])
+    depth_eff = np.where(request.recompute_depth == FULL_DEPTH, L, request.recompute_depth)
+
+    def hidden_fn():
+        out = torch.zeros((plan.n, cfg.d_model), dtype=torch.float64, device=model.device)
+        if plan.n_rows:
+            idx = torch.from_numpy(plan.rows.astype(np.int64)).to(model.device)
+            out[idx] = ws["hidden"][: plan.n_rows].double()
+        return out.cpu().numpy()
+
+    res = PrefillResult(
+        kv=KVCache(positions=request.positions.copy(), valid=~request.is_pad, _dev=(ws["kv_k"], ws["kv_v"])),
+        attn=attn,
+        question_span=request.question_span,
+        computed=request.recompute_mask & (depth_eff >= L),
+        active_per_layer=list(plan.n_act),
+        positions=request.positions.copy(),
+        hidden_fn=hidden_fn,
+        extras=extras,
+    )
+    res.model = model
+    res.request = request
+    if record_values:
+        res.value_trace = _ValueTrace(vtrace, plan)
+    return res
+
+
+def _attach_stats_rows(model, plan: DevicePlan, spans):
+    """Stats rows (row indices in hidden order) for the given slot spans."""
+    import torch
+
+    pos_in_rows = np.full(plan.n, -1, np.int64)
+    pos_in_rows[plan.rows] = np.arange(plan.rows.size)
+    rows = [pos_in_rows[lo:hi] for lo, hi in spans]
+    sr = np.concatenate(rows).astype(np.int32) if rows else np.zeros(0, np.int32)
+    plan.stats_rows = sr
+    plan.stats_row_spans = spans
+    segs = plan.stats_segments
+    host = np.concatenate([sr, np.array([a for a, _ in segs], np.int32), np.array([b for _, b in segs], np.int32)])
+    dev = torch.from_numpy(host).to(model.device)
+    plan.d["stats_rows"] = dev[: sr.size]
+    plan.d["seg_lo"] = dev[sr.size: sr.size + len(segs)]
+    plan.d["seg_hi"] = dev[sr.size + len(segs):]
+
+
+class _ValueTrace(list):
+    """Per-layer (V [n, kvw], pre-projection ctx [n_act, q_width]) as numpy,
+    ctx rows in ascending slot order (model.py:421-426)."""
+
+    def __init__(self, raw, plan):
+        out = []
+        for l, (v, c) in enumerate(raw):
+            vv = v.double().cpu().numpy()
+            if c is None:
+                out.append((vv, np.zeros((0, v.shape[-1]))))
+                continue
+            order = np.argsort(plan.rows[: c.shape[0]], kind="stable")
+            out.append((vv, c.double().cpu().numpy()[order]))
+        super().__init__(out)
+
+
+def _logits_rows(model: Model, rows_dev):
+    import torch
+
+    cfg = model.config
+    m = rows_dev.shape[0]
+    logits = torch.empty((m, cfg.vocab_size), dtype=model.hidden_dtype, device=model.device)
+    tok = torch.empty((m,), dtype=torch.int32, device=model.device)
+    N.call("cc_logits_argmax", N.ptr(rows_dev.contiguous()), N.ptr(model.w.get("final_norm")), cfg.rms_eps,
+           N.ptr(model.w["unembed_t"]), N.ptr(logits), N.ptr(tok), m, cfg.d_model, cfg.vocab_size, model.dtype_code,
+           N.stream_ptr())
+    return logits, tok
+
+
+def logits_device(model: Model, hidden_rows):
+    """Model.logits on the GPU (model.py:94-95): returns (logits, argmax)."""
+    import torch
+
+    N.require_cuda()
+    h = np.atleast_2d(np.asarray(hidden_rows, dtype=np.float64))
+    if h.shape[1] != model.config.d_model:
+        raise ShapeError("hidden rows width != d_model")
+    outs, toks = [], []
+    for i in range(0, h.shape[0], 8):
+        rows = torch.from_numpy(h[i:i + 8]).to(model.device, model.hidden_dtype)
+        lg, tk = _logits_rows(model, rows)
+        outs.append(lg.double().cpu().numpy())
+        toks.append(tk.cpu().numpy())
+    return np.concatenate(outs), np.concatenate(toks)
+
+
+def extract_rows(result: PrefillResult, start: int, stop: int, source_prefix=()) -> ChunkCache:
+    """K10: request KV rows [start, stop) -> fresh pool blocks of a new cache."""
+    model = result.model
+    cfg = model.config
+    kv_k, kv_v = result.kv._dev if result.kv._dev is not None else (None, None)
+    n = stop - start
+    if n <= 0:
+        raise PlanError("empty row range")
+    if kv_k is None:
+        keys, values = result.kv.slice_rows(start, stop)
+        return ChunkCache(keys=keys, values=values, n_tokens=n, source_prefix=source_prefix)
+    pool = model.pool
+    nb = -(-n // BLOCK)
+    blocks = pool.alloc(nb)
+    import torch
+
+    bdev = torch.from_numpy(blocks).to(model.device)
+    N.call("cc_extract_to_pool", N.ptr(kv_k), N.ptr(kv_v), kv_k.stride(0), cfg.n_layers, start, n, N.ptr(bdev), nb,
+           N.ptr(pool.storage), pool.layer_stride, pool.block_stride, cfg.kv_width(), model.dtype_code, N.stream_ptr())
+    return ChunkCache(n_tokens=n, source_prefix=source_prefix, _payload=_Payload(pool, blocks, n))
+
+
+def run_decode(model: Model, kv: KVCache, last_hidden, max_steps: int) -> list:
+    """Greedy decode (model.py:445-484): token from logits(last row), then
+    one engine step per token over the whole existing KV (a cache segment of
+    every previous slot, nothing recomputed) plus the new token."""
+    import torch
+
+    if max_steps <= 0:
+        return []
+    cfg = model.config
+    out = []
+    tok = int(logits_device(model, last_hidden)[1][0])
+    valid = kv.valid.copy()
+    positions = kv.positions.copy()
+    keys = [np.asarray(k) for k in kv.keys]
+    values = [np.asarray(v) for v in kv.values]
+    next_pos = int(positions[valid].max()) + 1
+    for step in range(max_steps):
+        out.append(tok)
+        n_prev = positions.size
+        cache = ChunkCache(keys=keys, values=values, n_tokens=n_prev)
+        payload = cache.device_payload(model)
+        token_ids = np.zeros(n_prev + 1, np.int64)
+        token_ids[-1] = tok
+        pos = np.concatenate([np.where(valid, positions, 0), [next_pos]]).astype(np.int64)
+        pad = np.concatenate([~valid, [False]])
+        mask = np.zeros(n_prev + 1, bool)
+        mask[-1] = True
+        depth = np.zeros(n_prev + 1, np.int64)
+        depth[-1] = FULL_DEPTH
+        plan = DevicePlan(model, token_ids, pos, pad, mask, depth, [(0, n_prev)], [payload], (n_prev, n_prev + 1))
+        ws = _workspace(model, plan)
+        execute(model, plan, ws)
+        new_k = ws["kv_k"][:, n_prev].double().cpu().numpy()
+        new_v = ws["kv_v"][:, n_prev].double().cpu().numpy()
+        rows = [(new_k[l][None, :], new_v[l][None, :]) for l in range(cfg.n_layers)]
+        kv.append_token(rows, next_pos)
+        keys = kv.keys
+        values = kv.values
+        valid = kv.valid.copy()
+        positions = kv.positions.copy()
+        next_pos += 1
+        if step + 1 < max_steps:
+            _, t = _logits_rows(model, ws["hidden"][0:1])
+            tok = int(t.item())
+    return out

@@ -1,0 +1,208 @@
+"""Kernel-level parity on the B200 (through the C ABI): each CUDA kernel
+against the oracle / a plain torch fp32 reference of the same op."""
+import json
+import math
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from ccb_helpers import golden_path, load_json  # noqa: E402
+
+from oracle import cachecraft_oracle as O  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def N():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_2502_15734_b200 import _native
+
+    _native.lib()
+    return _native
+
+
+def test_rope_apply_matches_reference_fixture(N):
+    import paper_2502_15734_b200 as cc
+
+    g = np.load(golden_path("rope.npz"))
+    x, pos = g["x"], g["pos"]
+    np.testing.assert_allclose(cc.apply_rpe(x, pos), g["apply_full"], atol=1e-12, rtol=0)
+    np.testing.assert_allclose(cc.apply_rpe(x, pos, d_head=8), g["apply_h8"], atol=1e-12, rtol=0)
+    np.testing.assert_allclose(cc.remove_rpe(x, pos, d_head=8), g["remove_h8"], atol=1e-12, rtol=0)
+    np.testing.assert_allclose(cc.apply_rpe(x, pos, base=500000.0, d_head=16), g["apply_h16_b5e5"], atol=1e-12)
+    np.testing.assert_array_equal(cc.apply_rpe(x[:3], np.zeros(3)), x[:3])  # position 0 is identity
+
+
+def test_topk_select_bit_exact_on_reference_vectors(N):
+    import paper_2502_15734_b200 as cc
+
+    for case in load_json("select.json"):
+        assert cc.select_tokens(case["scores"], case["cfo"]).tolist() == case["selected"]
+
+
+def test_topk_select_random_ties_and_batches(N):
+    from paper_2502_15734_b200.planner import recompute_count, select_tokens_batched
+
+    r = np.random.default_rng(0)
+    scores, counts = [], []
+    for n in (1, 3, 16, 100, 128, 512, 1000, 1024, 4096):
+        s = np.round(r.standard_normal(n), 1)  # heavy ties
+        c = float(r.uniform())
+        scores.append(s)
+        counts.append(recompute_count(n, c))
+    got = select_tokens_batched(scores, counts)
+    for s, k, gsel in zip(scores, counts, got):
+        want = np.sort(np.argsort(-s, kind="stable")[:k])
+        np.testing.assert_array_equal(gsel, want)
+
+
+def _gemm(N, A, B, epi, dtype, impl, C=None):
+    M, K = A.shape
+    Nn = B.shape[0]
+    if C is None:
+        n_out = Nn // 2 if epi == N.EPI_SWIGLU else Nn
+        C = torch.zeros((M, n_out), dtype=A.dtype, device="cuda")
+    N.call("cc_gemm", N.ptr(A), K, N.ptr(B), K, N.ptr(C), C.shape[1], M, Nn, K, epi, dtype, impl, N.stream_ptr())
+    torch.cuda.synchronize()
+    return C
+
+
+@pytest.mark.parametrize("M", [1, 77, 128, 130, 802])
+@pytest.mark.parametrize("NK", [(256, 64), (768, 256), (512, 4096)])
+def test_gemm_tcgen05_store_matches_fp32_reference(N, M, NK):
+    Nn, K = NK
+    g = torch.Generator(device="cuda").manual_seed(M * 7 + Nn)
+    A = torch.randn((M, K), generator=g, device="cuda").bfloat16()
+    B = (torch.randn((Nn, K), generator=g, device="cuda") / math.sqrt(K)).bfloat16()
+    ref = A.float() @ B.float().T
+    tc = _gemm(N, A, B, N.EPI_STORE, N.BF16, 1)
+    simt = _gemm(N, A, B, N.EPI_STORE, N.BF16, 2)
+    torch.testing.assert_close(tc.float(), ref, atol=2e-2, rtol=1e-2)
+    torch.testing.assert_close(simt.float(), ref, atol=2e-2, rtol=1e-2)
+
+
+@pytest.mark.parametrize("epi", ["resid", "swiglu", "gelu"])
+def test_gemm_tcgen05_epilogues(N, epi):
+    M, Nn, K = 300, 1024, 512
+    g = torch.Generator(device="cuda").manual_seed(3)
+    A = torch.randn((M, K), generator=g, device="cuda").bfloat16()
+    B = (torch.randn((Nn, K), generator=g, device="cuda") / math.sqrt(K)).bfloat16()
+    acc = A.float() @ B.float().T
+    if epi == "resid":
+        H0 = torch.randn((M, Nn), generator=g, device="cuda")
+        H = H0.clone()
+        _gemm(N, A, B, N.EPI_RESID_ADD, N.BF16, 1, C=H)
+        torch.testing.assert_close(H, H0 + acc, atol=1e-3, rtol=1e-3)
+    elif epi == "swiglu":
+        out = _gemm(N, A, B, N.EPI_SWIGLU, N.BF16, 1)
+        a4 = acc.reshape(M, Nn // 128, 2, 64)
+        ref = (torch.nn.functional.silu(a4[:, :, 0]) * a4[:, :, 1]).reshape(M, Nn // 2)
+        torch.testing.assert_close(out.float(), ref, atol=2e-2, rtol=2e-2)
+        out2 = _gemm(N, A, B, N.EPI_SWIGLU, N.BF16, 2)
+        torch.testing.assert_close(out2.float(), ref, atol=2e-2, rtol=2e-2)
+    else:
+        out = _gemm(N, A, B, N.EPI_GELU, N.BF16, 1)
+        ref = torch.nn.functional.gelu(acc, approximate="tanh")
+        torch.testing.assert_close(out.float(), ref, atol=2e-2, rtol=2e-2)
+
+
+def test_gemm_tcgen05_m_invariance(N):
+    """A row's result does not depend on how many rows are active."""
+    K, Nn = 1024, 512
+    g = torch.Generator(device="cuda").manual_seed(5)
+    A = torch.randn((700, K), generator=g, device="cuda").bfloat16()
+    B = (torch.randn((Nn, K), generator=g, device="cuda") / 32).bfloat16()
+    full = _gemm(N, A, B, N.EPI_STORE, N.BF16, 1)
+    part = _gemm(N, A[:37].contiguous(), B, N.EPI_STORE, N.BF16, 1)
+    assert torch.equal(full[:37], part)
+
+
+def _attn_ref(q, k, v, q_slot, pad, Hq, Hkv):
+    """plain torch fp32 reference of model.py:406-416 for scattered rows"""
+    n = k.shape[0]
+    dh = q.shape[-1]
+    G = Hq // Hkv
+    kk = k.float().repeat_interleave(G, dim=1)  # [n, Hq, dh]
+    vv = v.float().repeat_interleave(G, dim=1)
+    s = torch.einsum("qhd,khd->hqk", q.float(), kk) / math.sqrt(dh)
+    j = torch.arange(n, device=q.device)
+    ok = (j[None, :] <= q_slot[:, None].long()) & (pad[None, :] == 0)
+    s = s.masked_fill(~ok[None], float("-inf"))
+    p = torch.softmax(s, dim=-1)
+    return torch.einsum("hqk,khd->qhd", p, vv).reshape(q.shape[0], Hq * dh), torch.logsumexp(s, dim=-1).T
+
+
+@pytest.mark.parametrize("Hq,Hkv,dh", [(32, 8, 128), (4, 4, 64), (8, 1, 128), (16, 2, 64)])
+def test_attention_mma_scattered_rows(N, Hq, Hkv, dh):
+    n = 700
+    g = torch.Generator(device="cuda").manual_seed(Hq + dh)
+    rows = torch.sort(torch.randperm(n, generator=g, device="cuda")[:150]).values.int()
+    q = torch.randn((rows.numel(), Hq, dh), generator=g, device="cuda").bfloat16()
+    k = torch.randn((n, Hkv, dh), generator=g, device="cuda").bfloat16()
+    v = torch.randn((n, Hkv, dh), generator=g, device="cuda").bfloat16()
+    pad = torch.zeros(n, dtype=torch.uint8, device="cuda")
+    pad[100:112] = 1
+    pad[400:405] = 1
+    rows = rows[pad[rows.long()] == 0].contiguous()
+    q = q[: rows.numel()].contiguous()
+    ctx = torch.empty((rows.numel(), Hq * dh), dtype=torch.bfloat16, device="cuda")
+    lse = torch.empty((rows.numel(), Hq), dtype=torch.float32, device="cuda")
+    for impl in (1, 2):
+        N.call("cc_attention", N.ptr(q), N.ptr(k), N.ptr(v), N.ptr(rows), N.ptr(pad), N.ptr(ctx), N.ptr(lse),
+               rows.numel(), n, Hq, Hkv, dh, N.BF16, impl, N.stream_ptr())
+        torch.cuda.synchronize()
+        ref, ref_lse = _attn_ref(q, k, v, rows, pad, Hq, Hkv)
+        torch.testing.assert_close(ctx.float(), ref, atol=3e-2, rtol=3e-2)
+        torch.testing.assert_close(lse, ref_lse, atol=2e-3, rtol=1e-3)
+
+
+def test_gather_rope_matches_torch(N):
+    """K1 against a torch reference: copy position-free rows, rotate keys."""
+    L, kvw, dh = 3, 256, 128
+    nb_pool = 12
+    pool = torch.randn((L, nb_pool, 2, 16, kvw), device="cuda").bfloat16()
+    n = 70
+    items = np.array([(3, 0, 16, 0), (7, 16, 16, 0), (1, 32, 10, 0), (5, 50, 16, 0)], dtype=np.int32)
+    slot_pos = torch.arange(n, dtype=torch.int32, device="cuda") + 5
+    active = torch.zeros(n, dtype=torch.int32, device="cuda")
+    active[20] = 2  # slot 20 recomputed through layer 1: skipped at layers 0, 1
+    half = dh // 2
+    inv = torch.from_numpy(500000.0 ** (-2.0 * np.arange(half) / dh)).cuda()
+    tab = torch.empty((256, half, 2), dtype=torch.float32, device="cuda")
+    N.call("cc_rope_table", N.ptr(tab), N.ptr(inv), 256, half, N.BF16, N.stream_ptr())
+    kv_k = torch.zeros((L, n, kvw), dtype=torch.bfloat16, device="cuda")
+    kv_v = torch.zeros_like(kv_k)
+    k_rot = torch.zeros_like(kv_k)
+    it = torch.from_numpy(items.reshape(-1)).cuda()
+    N.call("cc_gather_rope_kv", N.ptr(pool), pool.stride(0), pool.stride(1), N.ptr(it), len(items), 0, L,
+           N.ptr(slot_pos), N.ptr(active), N.ptr(tab), N.ptr(kv_k), N.ptr(kv_v), N.ptr(k_rot), n * kvw, kvw, dh,
+           N.BF16, N.stream_ptr())
+    torch.cuda.synchronize()
+    for (blk, dst, nr, _) in items:
+        for l in range(L):
+            for r in range(nr):
+                s = dst + r
+                if l < int(active[s]):
+                    assert torch.all(kv_k[l, s] == 0)
+                    continue
+                assert torch.equal(kv_k[l, s], pool[l, blk, 0, r])
+                assert torch.equal(kv_v[l, s], pool[l, blk, 1, r])
+                x = pool[l, blk, 0, r].double().numpy(force=True).reshape(1, kvw)
+                want = O.rope(x, [int(slot_pos[s])], 500000.0, dh)[0]
+                np.testing.assert_allclose(k_rot[l, s].double().numpy(force=True), want, atol=2e-2, rtol=1e-2)
+
+
+def test_logits_argmax_first_max_wins(N):
+    d, vocab = 64, 1000
+    U = torch.zeros((vocab, d), dtype=torch.float32, device="cuda")
+    U[17, 0] = 1.0
+    U[900, 0] = 1.0  # tie -> first index
+    h = torch.ones((1, d), dtype=torch.float32, device="cuda")
+    logits = torch.empty((1, vocab), dtype=torch.float32, device="cuda")
+    tok = torch.empty((1,), dtype=torch.int32, device="cuda")
+    N.call("cc_logits_argmax", N.ptr(h), None, 1e-6, N.ptr(U), N.ptr(logits), N.ptr(tok), 1, d, vocab, N.F32,
+           N.stream_ptr())
+    assert int(tok.item()) == 17
