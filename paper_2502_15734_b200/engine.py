@@ -57,6 +57,14 @@ class DevicePlan:
         self.items = np.array(items, dtype=_GATHER_DT)
         self.n_items = len(items)
         self.n_cached_rows = int(sum(it[2] for it in items))
+        cached = np.zeros(n, bool)
+        for (src, dst, nr, _) in items:
+            cached[dst:dst + nr] = True
+        self.cached_active = [int(np.count_nonzero(cached & (active_until > l))) for l in range(L)]
+        # keys visible per active row (slot <= own slot, not pad) -> attention FLOPs
+        nonpad_before = np.cumsum(~np.asarray(is_pad, bool))
+        vis = nonpad_before[rows] if rows.size else np.zeros(0, np.int64)
+        self.attn_keys = [int(vis[: self.n_act[l]].sum()) for l in range(L)]
         # pack every int32 array into one host buffer -> one H2D copy
         parts = {
             "row_slot": rows.astype(np.int32),
@@ -147,8 +155,61 @@ def _record_default(model: Model, plan: DevicePlan) -> bool:
     return plan.n <= 8192 and bytes_q <= (256 << 20)
 
 
+class KernelTimer:
+    """CUDA events around each launch family on the launching stream (bench
+    instrumentation: per-kernel average durations inside the timed region)."""
+
+    def __init__(self):
+        self.events = {}
+        self.flops = {}
+        self.bytes = {}
+
+    def span(self, name, flops=0.0, nbytes=0.0):
+        import torch
+
+        t = self
+
+        class _Span:
+            def __enter__(self_inner):
+                self_inner.a = torch.cuda.Event(enable_timing=True)
+                self_inner.a.record()
+
+            def __exit__(self_inner, *exc):
+                b = torch.cuda.Event(enable_timing=True)
+                b.record()
+                t.events.setdefault(name, []).append((self_inner.a, b))
+                t.flops[name] = t.flops.get(name, 0.0) + flops
+                t.bytes[name] = t.bytes.get(name, 0.0) + nbytes
+
+        return _Span()
+
+    def summary(self):
+        out = {}
+        for k, ev in self.events.items():
+            ms = sum(a.elapsed_time(b) for a, b in ev)
+            out[k] = {"launches": len(ev), "ms_total": ms, "flops": self.flops[k], "bytes": self.bytes[k]}
+        return out
+
+
+class _NoTimer:
+    class _Null:
+        def __enter__(self):
+            return None
+
+        def __exit__(self, *exc):
+            return False
+
+    _n = _Null()
+
+    def span(self, name, flops=0.0, nbytes=0.0):
+        return self._n
+
+
+_NOTIMER = _NoTimer()
+
+
 def execute(model: Model, plan: DevicePlan, ws: dict, *, record=False, record_values=False, stats=False,
-            gemm_impl=0, attn_impl=0):
+            gemm_impl=0, attn_impl=0, timer=None):
     """Launch the per-layer pipeline on the current stream.  Returns the
     LazyAttention (if recording), value trace list and stats masses."""
     import torch
@@ -167,10 +228,15 @@ def execute(model: Model, plan: DevicePlan, ws: dict, *, record=False, record_va
     xn, qkv, q_rot, ctx, act, lse = ws["xn"], ws["qkv"], ws["q_rot"], ws["ctx"], ws["act"], ws["lse"]
     if plan.n_rows:
         N.call("cc_embed_rows", P(model.w["embed"]), P(D["row_tok"]), P(hidden), plan.n_rows, d, dt, s)
+    tm = _NOTIMER if timer is None else timer
+    esz = model.torch_dtype.itemsize
     if plan.n_items:
-        N.call("cc_gather_rope_kv", P(pool.storage), pool.layer_stride, pool.block_stride, P(D["items"]),
-               plan.n_items, 0, L, P(D["slot_pos"]), P(D["active_until"]), P(rope), P(kv_k), P(kv_v), P(k_rot),
-               n * kvw, kvw, dh, dt, s)
+        # algorithmic bytes: read K,V block rows, write kv_k, kv_v, k_rot (rows not recomputed at that layer)
+        moved = sum(plan.n_cached_rows - plan.cached_active[l] for l in range(L)) * kvw * esz * 5
+        with tm.span("gather_rope", nbytes=moved):
+            N.call("cc_gather_rope_kv", P(pool.storage), pool.layer_stride, pool.block_stride, P(D["items"]),
+                   plan.n_items, 0, L, P(D["slot_pos"]), P(D["active_until"]), P(rope), P(kv_k), P(kv_v), P(k_rot),
+                   n * kvw, kvw, dh, dt, s)
     lazy = LazyAttention(model, plan, k_rot) if record else None
     vtrace = [] if record_values else None
     n_stats = plan.stats_rows.size if stats else 0
@@ -186,12 +252,14 @@ def execute(model: Model, plan: DevicePlan, ws: dict, *, record=False, record_va
                 vtrace.append((kv_v[l], None))
             continue
         N.call("cc_rmsnorm", P(hidden), P(xn), P(lw.get("attn_norm")), n_l, d, eps, dt, s)
-        N.call("cc_gemm", P(xn), d, P(lw["w_qkv"]), d, P(qkv), qw + 2 * kvw, n_l, qw + 2 * kvw, d, N.EPI_STORE, dt,
-               gemm_impl, s)
+        with tm.span("gemm", flops=2.0 * n_l * (qw + 2 * kvw) * d):
+            N.call("cc_gemm", P(xn), d, P(lw["w_qkv"]), d, P(qkv), qw + 2 * kvw, n_l, qw + 2 * kvw, d, N.EPI_STORE,
+                   dt, gemm_impl, s)
         N.call("cc_rope_scatter_qkv", P(qkv), qw + 2 * kvw, n_l, P(D["row_slot"]), P(D["row_pos"]), P(rope), P(q_rot),
                P(kv_k[l]), P(kv_v[l]), P(k_rot[l]), H, Hkv, dh, dt, s)
-        N.call("cc_attention", P(q_rot), P(k_rot[l]), P(kv_v[l]), P(D["row_slot"]), key_pad, P(ctx), P(lse), n_l, n,
-               H, Hkv, dh, dt, attn_impl, s)
+        with tm.span("attention", flops=4.0 * H * dh * plan.attn_keys[l]):
+            N.call("cc_attention", P(q_rot), P(k_rot[l]), P(kv_v[l]), P(D["row_slot"]), key_pad, P(ctx), P(lse), n_l,
+                   n, H, Hkv, dh, dt, attn_impl, s)
         if n_stats:
             N.call("cc_segment_mass", P(q_rot), P(k_rot[l]), P(D["row_slot"]), key_pad, P(lse), P(D["seg_lo"]),
                    P(D["seg_hi"]), n_seg, P(D["stats_rows"]), n_stats, P(mass[l]), n, H, Hkv, dh, dt, s)
@@ -200,13 +268,20 @@ def execute(model: Model, plan: DevicePlan, ws: dict, *, record=False, record_va
             lazy.lse[l] = lse[:n_l].clone()
         if record_values:
             vtrace.append((kv_v[l], ctx[:n_l].clone()))
-        N.call("cc_gemm", P(ctx), qw, P(lw["w_o"]), qw, P(hidden), d, n_l, d, qw, N.EPI_RESID_ADD, dt, gemm_impl, s)
+        with tm.span("gemm", flops=2.0 * n_l * qw * d):
+            N.call("cc_gemm", P(ctx), qw, P(lw["w_o"]), qw, P(hidden), d, n_l, d, qw, N.EPI_RESID_ADD, dt, gemm_impl,
+                   s)
         N.call("cc_rmsnorm", P(hidden), P(xn), P(lw.get("mlp_norm")), n_l, d, eps, dt, s)
         if cfg.mlp == "swiglu":
-            N.call("cc_gemm", P(xn), d, P(lw["w_gu"]), d, P(act), ff, n_l, 2 * ff, d, N.EPI_SWIGLU, dt, gemm_impl, s)
+            with tm.span("gemm", flops=2.0 * n_l * 2 * ff * d):
+                N.call("cc_gemm", P(xn), d, P(lw["w_gu"]), d, P(act), ff, n_l, 2 * ff, d, N.EPI_SWIGLU, dt,
+                       gemm_impl, s)
         else:
-            N.call("cc_gemm", P(xn), d, P(lw["w_up"]), d, P(act), ff, n_l, ff, d, N.EPI_GELU, dt, gemm_impl, s)
-        N.call("cc_gemm", P(act), ff, P(lw["w_down"]), ff, P(hidden), d, n_l, d, ff, N.EPI_RESID_ADD, dt, gemm_impl, s)
+            with tm.span("gemm", flops=2.0 * n_l * ff * d):
+                N.call("cc_gemm", P(xn), d, P(lw["w_up"]), d, P(act), ff, n_l, ff, d, N.EPI_GELU, dt, gemm_impl, s)
+        with tm.span("gemm", flops=2.0 * n_l * ff * d):
+            N.call("cc_gemm", P(act), ff, P(lw["w_down"]), ff, P(hidden), d, n_l, d, ff, N.EPI_RESID_ADD, dt,
+                   gemm_impl, s)
     return lazy, vtrace, mass
 
 
