@@ -5,6 +5,8 @@
 namespace ccb {
 int attention_mma_bf16(const void* q, const void* k, const void* v, const int32_t* q_slot, const uint8_t* key_pad,
                        void* ctx, float* lse, int n_q, int n_keys, int Hq, int Hkv, int dh, cudaStream_t st);
+int attention_tc_bf16(const void* q, const void* k, const void* v, const int32_t* q_slot, const uint8_t* key_pad,
+                      void* ctx, float* lse, int n_q, int n_keys, int Hq, int Hkv, int dh, cudaStream_t st);
 int attention_simt(const void* q, const void* k, const void* v, const int32_t* q_slot, const uint8_t* key_pad,
                    void* ctx, void* lse, int n_q, int n_keys, int Hq, int Hkv, int dh, int dtype, cudaStream_t st);
 }  // namespace ccb

@@ -176,10 +176,16 @@ int cc_attention(const void* q, const void* k_rot, const void* v, const int32_t*
   CCB_REQUIRE(d_head > 0 && d_head <= 256, "attention: bad d_head");
   if (n_q == 0) return 0;
   cudaStream_t st = as_stream(stream);
-  if (dtype == CC_BF16 && impl != 2) {
+  // impl: 0 auto (tcgen05 -> mma.sync -> SIMT), 1 tcgen05 only, 3 mma.sync only, 2 SIMT
+  if (dtype == CC_BF16 && (impl == 0 || impl == 1)) {
+    int rc = attention_tc_bf16(q, k_rot, v, q_slot, key_pad, ctx, (float*)lse, n_q, n_keys, n_heads, n_kv_heads,
+                               d_head, st);
+    if (rc != CC_E_UNSUP || impl == 1) return rc;
+  }
+  if (dtype == CC_BF16 && (impl == 0 || impl == 3)) {
     int rc = attention_mma_bf16(q, k_rot, v, q_slot, key_pad, ctx, (float*)lse, n_q, n_keys, n_heads, n_kv_heads,
                                 d_head, st);
-    if (rc != CC_E_UNSUP || impl == 1) return rc;
+    if (rc != CC_E_UNSUP || impl == 3) return rc;
   }
   return attention_simt(q, k_rot, v, q_slot, key_pad, ctx, lse, n_q, n_keys, n_heads, n_kv_heads, d_head, dtype, st);
 }

@@ -1,0 +1,428 @@
+// K4 on the 5th-generation tensor cores: flash-style attention of the
+// recomputed (scattered) query rows over all request keys (model.py:406-416)
+// with S and O accumulators in TMEM.
+//
+// CTA = 128 "M-rows" = R query rows x G heads of one GQA group (G = Hq/Hkv,
+// R = 128/G), so one K/V tile in shared memory serves the whole group.
+//   warp 0     TMA: Q once (3-D map), K/V tiles of 128 keys (2-stage ring)
+//   warp 1     MMA issuer: S_i = Q K_i^T (M128 N128 K16 x dh/16) into one of
+//              two TMEM S buffers, O += P_i V_i (A = P from smem, B = V
+//              MN-major) into the TMEM O accumulator
+//   warps 2-5  softmax / correction / epilogue: thread = M-row = TMEM lane.
+//              Reads its S row (tcgen05.ld), applies the causal+pad mask
+//              (key j visible iff j <= q_slot[row] and !pad[j]), online
+//              softmax in fp32 (exp2), rescales its own O row in TMEM when
+//              the running max grows, writes its P row (bf16, 128B-swizzled)
+//              to smem for the PV MMA.
+// The PV MMA of tile i overlaps the S MMA of tile i+1 and the softmax of
+// tile i+1 (double-buffered S).
+#include <math.h>
+
+#include <mutex>
+#include <unordered_map>
+
+#include "attention.cuh"
+#include "common.cuh"
+#include "sm100.cuh"
+
+namespace ccb {
+
+namespace {
+
+using namespace sm100;
+
+constexpr int AT_BN = 128;      // keys per tile
+constexpr int AT_STAGES = 2;    // K/V ring depth
+constexpr int AT_THREADS = 192;
+
+// MN-major operand (B = V: N = head dim contiguous, K = keys), 128B swizzle:
+// 64-element atoms along N at `lbo` bytes, 8-key groups at 1024 B.
+__device__ __forceinline__ uint64_t desc_sw128_mn(const void* smem_tile, uint32_t lbo_bytes) {
+  uint64_t addr = smem_u32(smem_tile);
+  return ((addr >> 4) & 0x3FFFull) | ((uint64_t)((lbo_bytes >> 4) & 0x3FFF) << 16) | (64ull << 32) | (1ull << 46) |
+         (2ull << 61);
+}
+
+__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, bool b_mn_major) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | (b_mn_major ? (1u << 16) : 0u) | ((uint32_t)(N >> 3) << 17) |
+         ((uint32_t)(M >> 4) << 24);
+}
+
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
+      "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
+      "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31]));
+}
+__device__ __forceinline__ float ex2_fast(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+template <int DH>
+struct AtSmem {
+  static constexpr int ATOMS = DH / 64;              // 64-element (128 B) column atoms
+  static constexpr int Q_BYTES = 128 * DH * 2;       // 128 M-rows
+  static constexpr int KV_BYTES = AT_BN * DH * 2;    // one K (or V) tile
+  static constexpr int P_BYTES = 128 * AT_BN * 2;    // P tile, 2 atoms of 64 keys
+  static constexpr int Q_OFF = 0;
+  static constexpr int K_OFF = Q_OFF + Q_BYTES;
+  static constexpr int V_OFF = K_OFF + AT_STAGES * KV_BYTES;
+  static constexpr int P_OFF = V_OFF + AT_STAGES * KV_BYTES;
+  static constexpr int BAR_OFF = P_OFF + P_BYTES;
+  static constexpr size_t TOTAL = 1024 + BAR_OFF + 256;
+};
+
+template <int DH>
+__global__ void __launch_bounds__(AT_THREADS, 1)
+    attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                   const __grid_constant__ CUtensorMap tmV, const int32_t* __restrict__ q_slot,
+                   const uint8_t* __restrict__ key_pad, __nv_bfloat16* __restrict__ ctx, float* __restrict__ lse,
+                   int n_q, int n_keys, int Hq, int G, float scale_log2) {
+  using SM = AtSmem<DH>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = base + SM::Q_OFF;
+  uint8_t* sK = base + SM::K_OFF;
+  uint8_t* sV = base + SM::V_OFF;
+  uint8_t* sP = base + SM::P_OFF;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(base + SM::BAR_OFF);
+  uint64_t* q_full = bars + 0;
+  uint64_t* k_full = bars + 1;                 // [AT_STAGES]
+  uint64_t* v_full = k_full + AT_STAGES;       // [AT_STAGES]
+  uint64_t* kv_empty = v_full + AT_STAGES;     // [AT_STAGES]
+  uint64_t* s_full = kv_empty + AT_STAGES;     // [2]
+  uint64_t* s_empty = s_full + 2;              // [2]
+  uint64_t* p_full = s_empty + 2;
+  uint64_t* p_empty = p_full + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(p_empty + 1);
+  __shared__ int s_kmax;
+  __shared__ uint32_t padw[8];
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = blockIdx.y;
+  const int R = 128 / G;
+  const int row0 = blockIdx.x * R;
+
+  if (threadIdx.x == 0) s_kmax = -1;
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmQ);
+    tma_prefetch(&tmK);
+    tma_prefetch(&tmV);
+    mbar_init(q_full, 1);
+    for (int s = 0; s < AT_STAGES; ++s) {
+      mbar_init(&k_full[s], 1);
+      mbar_init(&v_full[s], 1);
+      mbar_init(&kv_empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&s_full[b], 1);
+      mbar_init(&s_empty[b], 128);
+    }
+    mbar_init(p_full, 128);
+    mbar_init(p_empty, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<512>(tmem_slot);
+  __syncthreads();
+  // per-CTA key range: max causal limit over valid rows
+  if (threadIdx.x < 128) {
+    int r = row0 + threadIdx.x / G;
+    if (r < n_q) atomicMax(&s_kmax, q_slot[r]);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int kmax = s_kmax;
+  const int n_tiles = kmax < 0 ? 0 : kmax / AT_BN + 1;
+  const uint32_t t_s0 = tmem, t_o = tmem + 256;
+
+  if (warp == 0) {
+    if (lane == 0 && n_tiles > 0) {
+      mbar_expect_tx(q_full, SM::Q_BYTES);
+#pragma unroll
+      for (int a = 0; a < SM::ATOMS; ++a) tma_load_3d(sQ + a * 128 * 128, &tmQ, q_full, a * 64, g * G, row0);
+      for (int i = 0; i < n_tiles; ++i) {
+        const int st = i % AT_STAGES;
+        const uint32_t ph = (i / AT_STAGES) & 1;
+        mbar_wait(&kv_empty[st], ph ^ 1);
+        mbar_expect_tx(&k_full[st], SM::KV_BYTES);
+#pragma unroll
+        for (int a = 0; a < SM::ATOMS; ++a)
+          tma_load_2d(sK + st * SM::KV_BYTES + a * AT_BN * 128, &tmK, &k_full[st], g * DH + a * 64, i * AT_BN);
+        mbar_expect_tx(&v_full[st], SM::KV_BYTES);
+#pragma unroll
+        for (int a = 0; a < SM::ATOMS; ++a)
+          tma_load_2d(sV + st * SM::KV_BYTES + a * AT_BN * 128, &tmV, &v_full[st], g * DH + a * 64, i * AT_BN);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && n_tiles > 0) {
+      constexpr uint32_t id_s = idesc_bf16(128, AT_BN, false);
+      constexpr uint32_t id_o = idesc_bf16(128, DH, true);
+      mbar_wait(q_full, 0);
+      auto issue_s = [&](int i) {
+        const int st = i % AT_STAGES, b = i & 1;
+        mbar_wait(&k_full[st], (i / AT_STAGES) & 1);
+        mbar_wait(&s_empty[b], ((i >> 1) & 1) ^ 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < DH / 16; ++kk) {
+          const int a = kk >> 2, w = kk & 3;
+          uint64_t ad = desc_sw128(sQ + a * 128 * 128) + 2 * w;
+          uint64_t bd = desc_sw128(sK + st * SM::KV_BYTES + a * AT_BN * 128) + 2 * w;
+          mma_bf16(t_s0 + b * AT_BN, ad, bd, id_s, kk > 0);
+        }
+        mma_commit(&s_full[b]);
+      };
+      issue_s(0);
+      for (int i = 0; i < n_tiles; ++i) {
+        if (i + 1 < n_tiles) issue_s(i + 1);
+        const int st = i % AT_STAGES;
+        mbar_wait(p_full, i & 1);
+        mbar_wait(&v_full[st], (i / AT_STAGES) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < AT_BN / 16; ++kk) {
+          uint64_t ad = desc_sw128(sP + (kk >> 2) * 128 * 128) + 2 * (kk & 3);
+          uint64_t bd = desc_sw128_mn(sV + st * SM::KV_BYTES + kk * 16 * 128, AT_BN * 128);
+          mma_bf16(t_o, ad, bd, id_o, (i > 0 || kk > 0) ? 1u : 0u);
+        }
+        mma_commit(p_empty);
+        mma_commit(&kv_empty[st]);
+      }
+    }
+  } else {
+    // ---- softmax / correction / epilogue: one thread per M-row -------------
+    const int q4 = warp & 3;
+    const int m = q4 * 32 + lane;
+    const int row = row0 + m / G;
+    const int head = g * G + m % G;
+    const int lim = row < n_q ? q_slot[row] : -1;
+    const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
+    float m_run = -INFINITY, l_run = 0.f;
+    uint8_t* prow = sP + m * 128;  // row m inside each 64-key atom (+ atom * 16 KiB)
+    constexpr float kRescaleLog2 = 8.f;  // lazy rescale: keep the stale max while p <= 2^8
+    for (int i = 0; i < n_tiles; ++i) {
+      const int b = i & 1;
+      mbar_wait(&s_full[b], (i >> 1) & 1);
+      tc_fence_after();
+      float s[AT_BN];
+      {
+        uint32_t r0[32], r1[32], r2[32], r3[32];
+        const uint32_t ta = t_s0 + b * AT_BN + lane_off;
+        tmem_ld32(ta, r0);
+        tmem_ld32(ta + 32, r1);
+        tmem_ld32(ta + 64, r2);
+        tmem_ld32(ta + 96, r3);
+        tmem_ld_wait();
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+          s[e] = __uint_as_float(r0[e]);
+          s[32 + e] = __uint_as_float(r1[e]);
+          s[64 + e] = __uint_as_float(r2[e]);
+          s[96 + e] = __uint_as_float(r3[e]);
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&s_empty[b]);
+      const int j0 = i * AT_BN;
+      // keys j0 + c visible iff c <= lim_rel (causal + bounds) and not a pad
+      const int lim_rel = min(lim, n_keys - 1) - j0;
+      if (key_pad != nullptr) {
+        // 128-bit pad mask of this tile, built by the 128 softmax threads
+        const int jm = j0 + m;
+        const unsigned word = __ballot_sync(0xffffffffu, jm >= n_keys || key_pad[jm] != 0);
+        if (lane == 0) padw[(i & 1) * 4 + q4] = word;
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        uint32_t pw[4];
+#pragma unroll
+        for (int w = 0; w < 4; ++w) pw[w] = padw[(i & 1) * 4 + w];
+#pragma unroll
+        for (int c = 0; c < AT_BN; ++c)
+          s[c] = (c <= lim_rel && !((pw[c >> 5] >> (c & 31)) & 1u)) ? s[c] : -INFINITY;
+      } else if (lim_rel < AT_BN - 1) {
+#pragma unroll
+        for (int c = 0; c < AT_BN; ++c) s[c] = (c <= lim_rel) ? s[c] : -INFINITY;
+      }
+      float mx[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) mx[e] = s[e];
+#pragma unroll
+      for (int c = 8; c < AT_BN; ++c) mx[c & 7] = fmaxf(mx[c & 7], s[c]);
+      const float tmax = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])), fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
+      bool grow = false;
+      float alpha = 1.f;
+      if (i > 0) {
+        mbar_wait(p_empty, (i - 1) & 1);  // PV_{i-1} done: O current, P buffer free
+        tc_fence_after();
+        grow = (m_run != -INFINITY) && ((tmax - m_run) * scale_log2 > kRescaleLog2);
+        if (grow) {
+          alpha = ex2_fast((m_run - tmax) * scale_log2);
+          l_run *= alpha;
+          m_run = tmax;
+        }
+      }
+      if (m_run == -INFINITY) m_run = tmax;  // first visible keys: nothing accumulated yet
+      const float base_l2 = (m_run == -INFINITY) ? 0.f : m_run * scale_log2;
+      float ps[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int a = 0; a < 2; ++a) {
+        uint8_t* patom = prow + a * 128 * 128;
+#pragma unroll
+        for (int ch = 0; ch < 8; ++ch) {
+          uint32_t pk[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int c = a * 64 + ch * 8 + e * 2;
+            const float p0 = ex2_fast(fmaf(s[c], scale_log2, -base_l2));
+            const float p1 = ex2_fast(fmaf(s[c + 1], scale_log2, -base_l2));
+            ps[(2 * e) & 7] += p0;
+            ps[(2 * e + 1) & 7] += p1;
+            __nv_bfloat162 h = __floats2bfloat162_rn(p0, p1);
+            pk[e] = *reinterpret_cast<uint32_t*>(&h);
+          }
+          *reinterpret_cast<uint4*>(patom + ((ch ^ (m & 7)) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        }
+      }
+      l_run += ((ps[0] + ps[1]) + (ps[2] + ps[3])) + ((ps[4] + ps[5]) + (ps[6] + ps[7]));
+      // O *= alpha for rows whose max grew past the lazy threshold.  tcgen05.ld/st
+      // are warp-collective (.sync.aligned): the whole warp joins, alpha = 1
+      // for rows that keep their max.
+      if (__any_sync(0xffffffffu, grow)) {
+#pragma unroll 1
+        for (int c = 0; c < DH / 32; ++c) {
+          uint32_t r[32];
+          tmem_ld32(t_o + c * 32 + lane_off, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int e = 0; e < 32; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) * alpha);
+          tmem_st32(t_o + c * 32 + lane_off, r);
+        }
+        tmem_st_wait();
+      }
+      fence_async_smem();
+      tc_fence_before();
+      mbar_arrive(p_full);
+    }
+    // epilogue
+    if (n_tiles > 0) {
+      mbar_wait(p_empty, (n_tiles - 1) & 1);
+      tc_fence_after();
+    }
+    const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
+    __nv_bfloat16* out = ctx + ((int64_t)row * Hq + head) * DH;
+#pragma unroll 1
+    for (int c = 0; c < DH / 32; ++c) {
+      uint32_t r[32];
+      tmem_ld32(t_o + c * 32 + lane_off, r);
+      tmem_ld_wait();
+      if (row < n_q && n_tiles > 0) {
+        uint4 pk[4];
+        uint32_t* pw = reinterpret_cast<uint32_t*>(pk);
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          __nv_bfloat162 h = __floats2bfloat162_rn(__uint_as_float(r[2 * e]) * inv, __uint_as_float(r[2 * e + 1]) * inv);
+          pw[e] = *reinterpret_cast<uint32_t*>(&h);
+        }
+        uint4* o4 = reinterpret_cast<uint4*>(out + c * 32);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) o4[e] = pk[e];
+      }
+    }
+    if (row < n_q)
+      lse[(int64_t)row * Hq + head] = l_run > 0.f ? (m_run * scale_log2 + log2f(l_run)) * 0.6931471805599453f : -INFINITY;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+int encode(CUtensorMap* m, int rank, const void* p, const cuuint64_t* dims, const cuuint64_t* strides,
+           const cuuint32_t* box) {
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) return fail(CC_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(p), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(CC_E_CUDA, "attention_tc: tensor map encode failed " + std::to_string((int)r));
+  return CC_OK;
+}
+
+template <int DH>
+int launch(const void* q, const void* k, const void* v, const int32_t* q_slot, const uint8_t* key_pad, void* ctx,
+           float* lse, int n_q, int n_keys, int Hq, int Hkv, cudaStream_t st) {
+  const int G = Hq / Hkv;
+  const int R = 128 / G;
+  CUtensorMap mq, mk, mv;
+  {
+    cuuint64_t dims[3] = {(cuuint64_t)DH, (cuuint64_t)Hq, (cuuint64_t)n_q};
+    cuuint64_t strides[2] = {(cuuint64_t)DH * 2, (cuuint64_t)Hq * DH * 2};
+    cuuint32_t box[3] = {64, (cuuint32_t)G, (cuuint32_t)R};
+    int rc = encode(&mq, 3, q, dims, strides, box);
+    if (rc) return rc;
+  }
+  {
+    cuuint64_t dims[2] = {(cuuint64_t)Hkv * DH, (cuuint64_t)n_keys};
+    cuuint64_t strides[1] = {(cuuint64_t)Hkv * DH * 2};
+    cuuint32_t box[2] = {64, (cuuint32_t)AT_BN};
+    int rc = encode(&mk, 2, k, dims, strides, box);
+    if (rc) return rc;
+    rc = encode(&mv, 2, v, dims, strides, box);
+    if (rc) return rc;
+  }
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(attn_tc_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)AtSmem<DH>::TOTAL);
+    attr = true;
+  }
+  dim3 grid((n_q + R - 1) / R, Hkv);
+  const float scale_log2 = 1.4426950408889634f / sqrtf((float)DH);
+  attn_tc_kernel<DH><<<grid, AT_THREADS, AtSmem<DH>::TOTAL, st>>>(mq, mk, mv, q_slot, key_pad, (__nv_bfloat16*)ctx,
+                                                                  lse, n_q, n_keys, Hq, G, scale_log2);
+  return check_launch("attention_tc");
+}
+
+}  // namespace
+
+int attention_tc_bf16(const void* q, const void* k, const void* v, const int32_t* q_slot, const uint8_t* key_pad,
+                      void* ctx, float* lse, int n_q, int n_keys, int Hq, int Hkv, int dh, cudaStream_t st) {
+  const int G = Hq / Hkv;
+  if (G < 1 || G > 128 || (128 % G) != 0) return fail(CC_E_UNSUP, "attention_tc: GQA group must divide 128");
+  if ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(k) | reinterpret_cast<uintptr_t>(v)) & 15)
+    return fail(CC_E_UNSUP, "attention_tc: pointers must be 16-byte aligned");
+  if (dh == 128) return launch<128>(q, k, v, q_slot, key_pad, ctx, lse, n_q, n_keys, Hq, Hkv, st);
+  if (dh == 64) return launch<64>(q, k, v, q_slot, key_pad, ctx, lse, n_q, n_keys, Hq, Hkv, st);
+  return fail(CC_E_UNSUP, "attention_tc: d_head must be 64 or 128");
+}
+
+}  // namespace ccb

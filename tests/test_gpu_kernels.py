@@ -135,9 +135,10 @@ def _attn_ref(q, k, v, q_slot, pad, Hq, Hkv):
     return torch.einsum("hqk,khd->qhd", p, vv).reshape(q.shape[0], Hq * dh), torch.logsumexp(s, dim=-1).T
 
 
-@pytest.mark.parametrize("Hq,Hkv,dh", [(32, 8, 128), (4, 4, 64), (8, 1, 128), (16, 2, 64)])
-def test_attention_mma_scattered_rows(N, Hq, Hkv, dh):
-    n = 700
+@pytest.mark.parametrize("Hq,Hkv,dh,n", [(32, 8, 128, 700), (4, 4, 64, 700), (8, 1, 128, 700), (16, 2, 64, 700),
+                                          (32, 8, 128, 2100), (64, 8, 128, 300)])
+def test_attention_scattered_rows(N, Hq, Hkv, dh, n):
+    """impl 1 = tcgen05/TMEM kernel, 3 = mma.sync kernel, 2 = SIMT."""
     g = torch.Generator(device="cuda").manual_seed(Hq + dh)
     rows = torch.sort(torch.randperm(n, generator=g, device="cuda")[:150]).values.int()
     q = torch.randn((rows.numel(), Hq, dh), generator=g, device="cuda").bfloat16()
@@ -150,7 +151,8 @@ def test_attention_mma_scattered_rows(N, Hq, Hkv, dh):
     q = q[: rows.numel()].contiguous()
     ctx = torch.empty((rows.numel(), Hq * dh), dtype=torch.bfloat16, device="cuda")
     lse = torch.empty((rows.numel(), Hq), dtype=torch.float32, device="cuda")
-    for impl in (1, 2):
+    for impl in (1, 3, 2):
+        ctx.zero_()
         N.call("cc_attention", N.ptr(q), N.ptr(k), N.ptr(v), N.ptr(rows), N.ptr(pad), N.ptr(ctx), N.ptr(lse),
                rows.numel(), n, Hq, Hkv, dh, N.BF16, impl, N.stream_ptr())
         torch.cuda.synchronize()
