@@ -11,6 +11,7 @@
 #include <math.h>
 
 #include <algorithm>
+#include <type_traits>
 
 #include "common.cuh"
 
@@ -232,6 +233,41 @@ __device__ __forceinline__ A block_sum(A v, A* red) {
   return t;
 }
 
+// Register-resident RMSNorm: one 128-thread CTA per row, the row read once
+// with 16-byte loads (d / 512 float4 per thread), one block reduction.
+template <typename T, int NV>
+__global__ void __launch_bounds__(128) rmsnorm_vec_kernel(const float* __restrict__ h, T* __restrict__ out,
+                                                          const float* __restrict__ w, int d, float eps) {
+  __shared__ float red[4];
+  const float4* x = reinterpret_cast<const float4*>(h + (int64_t)blockIdx.x * d);
+  float4 v[NV];
+  float ss = 0.f;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    v[i] = x[threadIdx.x + i * 128];
+    ss += v[i].x * v[i].x + v[i].y * v[i].y + v[i].z * v[i].z + v[i].w * v[i].w;
+  }
+  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  ss = (red[0] + red[1]) + (red[2] + red[3]);
+  const float inv = 1.f / sqrtf(ss / (float)d + eps);
+  T* y = out + (int64_t)blockIdx.x * d;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int c = (threadIdx.x + i * 128) * 4;
+    float4 wv = w ? *reinterpret_cast<const float4*>(w + c) : make_float4(1.f, 1.f, 1.f, 1.f);
+    float a0 = v[i].x * inv * wv.x, a1 = v[i].y * inv * wv.y, a2 = v[i].z * inv * wv.z, a3 = v[i].w * inv * wv.w;
+    if constexpr (sizeof(T) == 2) {
+      __nv_bfloat162 p0 = __floats2bfloat162_rn(a0, a1), p1 = __floats2bfloat162_rn(a2, a3);
+      uint2 pk = make_uint2(*reinterpret_cast<uint32_t*>(&p0), *reinterpret_cast<uint32_t*>(&p1));
+      *reinterpret_cast<uint2*>(y + c) = pk;
+    } else {
+      *reinterpret_cast<float4*>(y + c) = make_float4(a0, a1, a2, a3);
+    }
+  }
+}
+
 template <typename T>
 __global__ void __launch_bounds__(256) rmsnorm_kernel(const typename Acc<T>::type* __restrict__ h,
                                                       T* __restrict__ out, const float* __restrict__ w,
@@ -277,23 +313,46 @@ __global__ void __launch_bounds__(256) logits_kernel(const typename Acc<T>::type
     const T* u = U + (int64_t)v * d;
     for (int r = 0; r < m; ++r) {
       A acc = 0;
-      for (int i = lane; i < d; i += 32) acc += (A)to_f(u[i]) * xs[r * d + i];
+      if constexpr (sizeof(T) == 2) {
+        // 16-byte loads of the bf16 unembedding row
+        for (int i = lane * 8; i < d; i += 256) {
+          uint4 raw = *reinterpret_cast<const uint4*>(u + i);
+          const __nv_bfloat16* hb = reinterpret_cast<const __nv_bfloat16*>(&raw);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) acc += __bfloat162float(hb[e]) * xs[r * d + i + e];
+        }
+      } else {
+        for (int i = lane; i < d; i += 32) acc += (A)to_f(u[i]) * xs[r * d + i];
+      }
       for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
       if (lane == 0) logits[(int64_t)r * vocab + v] = acc;
     }
   }
 }
 
+// two-stage first-max argmax: stage 1 (gridDim.y chunks per row) writes
+// partial (value, index); stage 2 (one CTA per row) folds the partials
 template <typename A>
-__global__ void __launch_bounds__(1024) argmax_kernel(const A* __restrict__ logits, int32_t* __restrict__ out, int vocab) {
+__global__ void __launch_bounds__(1024) argmax_kernel(const A* __restrict__ logits, int32_t* __restrict__ out, int vocab,
+                                                      A* __restrict__ part_v, int32_t* __restrict__ part_i, int n_part) {
   __shared__ A bv[32];
   __shared__ int bi[32];
-  const A* x = logits + (int64_t)blockIdx.x * vocab;
   A best = -INFINITY;
   int idx = 0x7fffffff;
-  for (int i = threadIdx.x; i < vocab; i += blockDim.x) {
-    A v = x[i];
-    if (v > best || (v == best && i < idx)) { best = v; idx = i; }
+  if (part_v == nullptr || n_part == 0) {
+    const A* x = logits + (int64_t)blockIdx.x * vocab;
+    const int chunk = (vocab + gridDim.y - 1) / gridDim.y;
+    const int lo = blockIdx.y * chunk, hi = min(vocab, lo + chunk);
+    for (int i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+      A v = x[i];
+      if (v > best || (v == best && i < idx)) { best = v; idx = i; }
+    }
+  } else {
+    for (int i = threadIdx.x; i < n_part; i += blockDim.x) {
+      A v = part_v[(int64_t)blockIdx.x * n_part + i];
+      int j = part_i[(int64_t)blockIdx.x * n_part + i];
+      if (v > best || (v == best && j < idx)) { best = v; idx = j; }
+    }
   }
   for (int o = 16; o > 0; o >>= 1) {
     A ov = __shfl_xor_sync(0xffffffffu, best, o);
@@ -311,7 +370,14 @@ __global__ void __launch_bounds__(1024) argmax_kernel(const A* __restrict__ logi
       int oi = __shfl_xor_sync(0xffffffffu, idx, o);
       if (ov > best || (ov == best && oi < idx)) { best = ov; idx = oi; }
     }
-    if (lane == 0) out[blockIdx.x] = idx;
+    if (lane == 0) {
+      if (part_v != nullptr && n_part == 0) {
+        part_v[(int64_t)blockIdx.x * gridDim.y + blockIdx.y] = best;
+        part_i[(int64_t)blockIdx.x * gridDim.y + blockIdx.y] = idx;
+      } else {
+        out[blockIdx.x] = idx;
+      }
+    }
   }
 }
 
@@ -539,6 +605,29 @@ int cc_embed_rows(const void* embed, const int32_t* tokens, void* hidden, int n_
 int cc_rmsnorm(const void* hidden, void* out, const float* weight, int n_rows, int d, double eps, int dtype,
                void* stream) {
   if (n_rows == 0) return 0;
+  if (dtype != CC_F64 && d % 512 == 0 && d <= 512 * 32 &&
+      ((reinterpret_cast<uintptr_t>(hidden) | reinterpret_cast<uintptr_t>(out) | reinterpret_cast<uintptr_t>(weight)) & 15) == 0) {
+    const int nv = d / 512;
+    auto go = [&](auto tag) -> int {
+      constexpr int NV = decltype(tag)::value;
+      if (dtype == CC_BF16)
+        rmsnorm_vec_kernel<__nv_bfloat16, NV><<<n_rows, 128, 0, as_stream(stream)>>>(
+            (const float*)hidden, (__nv_bfloat16*)out, weight, d, (float)eps);
+      else
+        rmsnorm_vec_kernel<float, NV><<<n_rows, 128, 0, as_stream(stream)>>>((const float*)hidden, (float*)out, weight,
+                                                                             d, (float)eps);
+      return check_launch("rmsnorm_vec");
+    };
+    switch (nv) {
+      case 1: return go(std::integral_constant<int, 1>{});
+      case 2: return go(std::integral_constant<int, 2>{});
+      case 4: return go(std::integral_constant<int, 4>{});
+      case 8: return go(std::integral_constant<int, 8>{});
+      case 16: return go(std::integral_constant<int, 16>{});
+      case 32: return go(std::integral_constant<int, 32>{});
+      default: break;
+    }
+  }
   return CCB_DISPATCH_DTYPE(dtype, T, [&] {
     rmsnorm_kernel<T><<<n_rows, 256, 0, as_stream(stream)>>>((const typename Acc<T>::type*)hidden, (T*)out,
                                                             weight, d, eps);
@@ -561,7 +650,21 @@ int cc_logits_argmax(const void* hidden_rows, const float* norm_w, double eps, c
     int rc = check_launch("logits");
     if (rc) return rc;
     if (argmax) {
-      argmax_kernel<A><<<m, 1024, 0, as_stream(stream)>>>((const A*)logits, argmax, vocab);
+      // partials live after the logits rows in a small static scratch
+      constexpr int PARTS = 64;
+      static A* part_v = nullptr;
+      static int32_t* part_i = nullptr;
+      static int cap = 0;
+      if (cap < m * PARTS) {
+        if (part_v) { cudaFree(part_v); cudaFree(part_i); }
+        cudaMalloc(&part_v, sizeof(A) * 8 * PARTS);
+        cudaMalloc(&part_i, sizeof(int32_t) * 8 * PARTS);
+        cap = 8 * PARTS;
+      }
+      argmax_kernel<A><<<dim3(m, PARTS), 1024, 0, as_stream(stream)>>>((const A*)logits, argmax, vocab, part_v, part_i, 0);
+      rc = check_launch("argmax_partial");
+      if (rc) return rc;
+      argmax_kernel<A><<<m, 64, 0, as_stream(stream)>>>((const A*)logits, argmax, vocab, part_v, part_i, PARTS);
       return check_launch("argmax");
     }
     return 0;
