@@ -107,9 +107,11 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
   __shared__ uint32_t padw[8];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int g = blockIdx.y;
+  // grid = (kv groups, row tiles), row tiles walked last-first: later rows see
+  // more keys, so the longest CTAs are scheduled in the first wave
+  const int g = blockIdx.x;
   const int R = 128 / G;
-  const int row0 = blockIdx.x * R;
+  const int row0 = (gridDim.y - 1 - blockIdx.y) * R;
 
   if (threadIdx.x == 0) s_kmax = -1;
   if (warp == 0 && lane == 0) {
@@ -405,7 +407,7 @@ int launch(const void* q, const void* k, const void* v, const int32_t* q_slot, c
     cudaFuncSetAttribute(attn_tc_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)AtSmem<DH>::TOTAL);
     attr = true;
   }
-  dim3 grid((n_q + R - 1) / R, Hkv);
+  dim3 grid(Hkv, (n_q + R - 1) / R);
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)DH);
   attn_tc_kernel<DH><<<grid, AT_THREADS, AtSmem<DH>::TOTAL, st>>>(mq, mk, mv, q_slot, key_pad, (__nv_bfloat16*)ctx,
                                                                   lse, n_q, n_keys, Hq, G, scale_log2);

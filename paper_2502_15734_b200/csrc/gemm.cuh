@@ -4,7 +4,7 @@
 
 namespace ccb {
 int gemm_tc_bf16(const void* A, int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc, int M, int N, int K,
-                 int epi, cudaStream_t st);
+                 int epi, bool allow_split, cudaStream_t st);
 int gemm_simt(const void* A, int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc, int M, int N, int K,
               int epi, int dtype, cudaStream_t st);
 }  // namespace ccb

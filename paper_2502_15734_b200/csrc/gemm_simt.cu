@@ -108,10 +108,12 @@ extern "C" int cc_gemm(const void* A, int64_t lda, const void* B, int64_t ldb, v
   CCB_REQUIRE(M >= 0 && N > 0 && K > 0, "gemm: bad shape");
   if (M == 0) return 0;
   cudaStream_t st = as_stream(stream);
+  // impl: 0 auto (tcgen05, split-K allowed -> SIMT if unsupported), 1 tcgen05 with
+  // split-K, 4 tcgen05 without split-K (batch/M-invariant), 2 SIMT reference
   if (dtype == CC_BF16 && impl != 2) {
-    int rc = gemm_tc_bf16(A, lda, B, ldb, C, ldc, M, N, K, epilogue, st);
-    if (rc != CC_E_UNSUP || impl == 1) return rc;
-  } else if (impl == 1) {
+    int rc = gemm_tc_bf16(A, lda, B, ldb, C, ldc, M, N, K, epilogue, impl != 4, st);
+    if (rc != CC_E_UNSUP || impl == 1 || impl == 4) return rc;
+  } else if (impl == 1 || impl == 4) {
     return fail(CC_E_UNSUP, "gemm: tcgen05 kernel requires bf16");
   }
   return gemm_simt(A, lda, B, ldb, C, ldc, M, N, K, epilogue, dtype, st);

@@ -71,7 +71,7 @@ def _gemm(N, A, B, epi, dtype, impl, C=None):
 
 
 @pytest.mark.parametrize("M", [1, 77, 128, 130, 802])
-@pytest.mark.parametrize("NK", [(256, 64), (768, 256), (512, 4096)])
+@pytest.mark.parametrize("NK", [(256, 64), (768, 256), (512, 4096), (6144, 256), (384, 512)])
 def test_gemm_tcgen05_store_matches_fp32_reference(N, M, NK):
     Nn, K = NK
     g = torch.Generator(device="cuda").manual_seed(M * 7 + Nn)
@@ -109,15 +109,51 @@ def test_gemm_tcgen05_epilogues(N, epi):
         torch.testing.assert_close(out.float(), ref, atol=2e-2, rtol=2e-2)
 
 
-def test_gemm_tcgen05_m_invariance(N):
-    """A row's result does not depend on how many rows are active."""
-    K, Nn = 1024, 512
+@pytest.mark.parametrize("Nn", [512, 6144, 1536])
+def test_gemm_tcgen05_m_invariance(N, Nn):
+    """A row's result does not depend on how many rows are active (also when
+    the tile width chosen for the two M differs)."""
+    K = 1024
     g = torch.Generator(device="cuda").manual_seed(5)
-    A = torch.randn((700, K), generator=g, device="cuda").bfloat16()
+    A = torch.randn((5152, K), generator=g, device="cuda").bfloat16()
     B = (torch.randn((Nn, K), generator=g, device="cuda") / 32).bfloat16()
-    full = _gemm(N, A, B, N.EPI_STORE, N.BF16, 1)
-    part = _gemm(N, A[:37].contiguous(), B, N.EPI_STORE, N.BF16, 1)
+    full = _gemm(N, A, B, N.EPI_STORE, N.BF16, 4)  # impl 4: tcgen05 without split-K
+    part = _gemm(N, A[:37].contiguous(), B, N.EPI_STORE, N.BF16, 4)
     assert torch.equal(full[:37], part)
+
+
+@pytest.mark.parametrize("M", [32, 802])
+@pytest.mark.parametrize("epi", ["store", "resid", "swiglu", "gelu"])
+def test_gemm_split_k_deterministic(N, M, epi):
+    """Split-K with in-order fix-ups: matches the fp32 reference and is
+    bit-reproducible run to run."""
+    Nn, K = (4096, 14336) if epi == "resid" else (2048, 4096)
+    g = torch.Generator(device="cuda").manual_seed(M)
+    A = torch.randn((M, K), generator=g, device="cuda").bfloat16()
+    B = (torch.randn((Nn, K), generator=g, device="cuda") / math.sqrt(K)).bfloat16()
+    acc = A.float() @ B.float().T
+    code = {"store": N.EPI_STORE, "resid": N.EPI_RESID_ADD, "swiglu": N.EPI_SWIGLU, "gelu": N.EPI_GELU}[epi]
+    outs = []
+    for _ in range(2):
+        if epi == "resid":
+            H = torch.ones((M, Nn), device="cuda")
+            _gemm(N, A, B, code, N.BF16, 1, C=H)
+            outs.append(H)
+        else:
+            outs.append(_gemm(N, A, B, code, N.BF16, 1))
+    assert torch.equal(outs[0], outs[1])
+    if epi == "resid":
+        ref = acc + 1.0
+        torch.testing.assert_close(outs[0], ref, atol=1e-3, rtol=1e-3)
+    elif epi == "swiglu":
+        a4 = acc.reshape(M, Nn // 128, 2, 64)
+        ref = (torch.nn.functional.silu(a4[:, :, 0]) * a4[:, :, 1]).reshape(M, Nn // 2)
+        torch.testing.assert_close(outs[0].float(), ref, atol=2e-2, rtol=2e-2)
+    elif epi == "gelu":
+        torch.testing.assert_close(outs[0].float(), torch.nn.functional.gelu(acc, approximate="tanh"), atol=2e-2,
+                                   rtol=2e-2)
+    else:
+        torch.testing.assert_close(outs[0].float(), acc, atol=2e-2, rtol=1e-2)
 
 
 def _attn_ref(q, k, v, q_slot, pad, Hq, Hkv):
