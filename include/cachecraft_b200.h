@@ -172,6 +172,10 @@ CC_API int cc_extract_to_pool(const void* kv_k, const void* kv_v, int64_t req_la
                        int64_t pool_layer_stride, int64_t pool_block_stride, int kv_width, int dtype,
                        void* stream);
 
+/* dst[i] += src[i] over n f32 elements (the residual add after a tensor-
+ * parallel all-reduce of the o_proj / down_proj partial outputs). */
+CC_API int cc_add_f32(float* dst, const float* src, int64_t n, void* stream);
+
 /* L2 flush helper for benchmarks: writes `bytes` of scratch. */
 CC_API int cc_flush_l2(void* scratch, size_t bytes, void* stream);
 

@@ -213,7 +213,7 @@ def layout(segments, question) -> dict:
 # --------------------------------------------------------------------------
 
 
-def prefill(w: dict, cfg: OracleConfig, lay: dict, caches, keep_weights=True, layers=None) -> dict:
+def prefill(w: dict, cfg: OracleConfig, lay: dict, caches, keep_weights=True, layers=None, tp=None) -> dict:
     """Partial prefill with injected position-free caches.
 
     ``caches`` is a list aligned with the segments: None for fresh text, else
@@ -224,10 +224,22 @@ def prefill(w: dict, cfg: OracleConfig, lay: dict, caches, keep_weights=True, la
     position (0 at pads); a query sees the non-pad keys at positions <= its
     own; the residual MLP follows.  ``layers`` optionally limits the run to
     the first ``layers`` layers (bench CPU-baseline sampling).
+
+    ``tp`` (test of the multi-GPU partition) = {"q": slice, "kv": slice,
+    "ff": slice, "allreduce": fn}: this call computes one tensor-parallel
+    rank — its query/kv head columns and MLP columns — and ``allreduce``
+    sums the o_proj and down_proj partial outputs over the ranks before the
+    residual adds (the only two reductions of a layer, model.py:417, :419).
     """
     L = cfg.n_layers if layers is None else layers
     H, Hkv, dh = cfg.n_heads, cfg.hkv, cfg.dh
+    qc, kc, fc = (slice(None), slice(None), slice(None)) if tp is None else (tp["q"], tp["kv"], tp["ff"])
+    if tp is not None:
+        H = (qc.stop - qc.start) // dh
+        Hkv = (kc.stop - kc.start) // dh
+    kvw = Hkv * dh
     group = H // Hkv
+    reduce = (lambda a: a) if tp is None else tp["allreduce"]
     n = lay["token_ids"].size
     d = cfg.d_model
     mask, pos, pad = lay["mask"], lay["positions"], lay["is_pad"]
@@ -241,19 +253,19 @@ def prefill(w: dict, cfg: OracleConfig, lay: dict, caches, keep_weights=True, la
         lw = w["layers"][l]
         rows = np.flatnonzero(mask & (depth > l))
         active.append(int(rows.size))
-        K = np.zeros((n, cfg.kv_width))
-        V = np.zeros((n, cfg.kv_width))
+        K = np.zeros((n, kvw))
+        V = np.zeros((n, kvw))
         for (start, _), c in zip(lay["segment_slots"], caches):
             if c is not None:
                 ns = c[0][l].shape[0]
-                K[start : start + ns] = c[0][l]
-                V[start : start + ns] = c[1][l]
+                K[start : start + ns] = c[0][l][:, kc] if c[0][l].shape[1] != kvw else c[0][l]
+                V[start : start + ns] = c[1][l][:, kc] if c[1][l].shape[1] != kvw else c[1][l]
         if rows.size:
             x = hidden[rows]
             xn = rmsnorm(x, cfg.rms_eps, lw["attn_norm"] if nw else None)
-            q = xn @ lw["wq"]
-            K[rows] = xn @ lw["wk"]
-            V[rows] = xn @ lw["wv"]
+            q = xn @ lw["wq"][:, qc]
+            K[rows] = xn @ lw["wk"][:, kc]
+            V[rows] = xn @ lw["wv"][:, kc]
             qr = rope(q, pos[rows], cfg.rpe_base, dh).reshape(rows.size, H, dh)
             kr = rope(K, key_pos, cfg.rpe_base, dh).reshape(n, Hkv, dh)
             vv = V.reshape(n, Hkv, dh)
@@ -267,14 +279,14 @@ def prefill(w: dict, cfg: OracleConfig, lay: dict, caches, keep_weights=True, la
             p = np.exp(s)
             p /= p.sum(axis=2, keepdims=True)
             ctx = np.matmul(p, vv_h).transpose(1, 0, 2).reshape(rows.size, H * dh)
-            hidden[rows] = x + ctx @ lw["wo"]
+            hidden[rows] = x + reduce(ctx @ lw["wo"][qc, :])
             x2 = hidden[rows]
             xn2 = rmsnorm(x2, cfg.rms_eps, lw["mlp_norm"] if nw else None)
             if cfg.mlp == "swiglu":
-                ff = silu(xn2 @ lw["w_gate"]) * (xn2 @ lw["w_up"])
+                ff = silu(xn2 @ lw["w_gate"][:, fc]) * (xn2 @ lw["w_up"][:, fc])
             else:
-                ff = gelu_tanh(xn2 @ lw["w_up"])
-            hidden[rows] = x2 + ff @ lw["w_down"]
+                ff = gelu_tanh(xn2 @ lw["w_up"][:, fc])
+            hidden[rows] = x2 + reduce(ff @ lw["w_down"][fc, :])
             attn_w.append(p if keep_weights else None)
         else:
             attn_w.append(np.zeros((H, 0, n)) if keep_weights else None)

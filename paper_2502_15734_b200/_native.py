@@ -45,13 +45,15 @@ _SIGS = {
     "cc_topk_select": ([_vp, _vp, _vp, _vp, _vp, _i32, _i32, _vp], _i32),
     "cc_logits_argmax": ([_vp, _vp, _f64, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _vp], _i32),
     "cc_extract_to_pool": ([_vp, _vp, _i64, _i32, _i32, _i32, _vp, _i32, _vp, _i64, _i64, _i32, _i32, _vp], _i32),
+    "cc_add_f32": ([_vp, _vp, _i64, _vp], _i32),
     "cc_flush_l2": ([_vp, _sz, _vp], _i32),
 }
 
 _lib = None
 _lock = threading.Lock()
-# per-entry-point launch counters (the bench reports how many native kernels ran)
+# per-entry-point call counters and the number of kernels those calls launched
 calls: dict[str, int] = {}
+kernels_launched = 0
 
 
 def library_loaded() -> bool:
@@ -92,9 +94,12 @@ def check(rc: int, what: str):
 
 def call(name: str, *args):
     """Invoke a native entry point, count it and map its status."""
+    global kernels_launched
     fn = getattr(lib(), name)
     rc = fn(*args)
     calls[name] = calls.get(name, 0) + 1
+    # cc_logits_argmax with an argmax output runs GEMV + two argmax stages
+    kernels_launched += 3 if (name == "cc_logits_argmax" and args[5] is not None) else 1
     check(rc, name)
     return rc
 

@@ -69,5 +69,6 @@ __device__ __forceinline__ double silu(double x) { return x / (1.0 + exp(-x)); }
 inline size_t dtype_size(int dtype) { return dtype == CC_F64 ? 8 : (dtype == CC_F32 ? 4 : 2); }
 
 int num_sms();
+void* stream_scratch(cudaStream_t st, int tag, size_t bytes);
 
 }  // namespace ccb

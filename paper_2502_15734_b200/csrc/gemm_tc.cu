@@ -358,11 +358,20 @@ struct SplitScratch {
   int epoch = 0;
 };
 
-SplitScratch& scratch() {
-  static SplitScratch s[16];
+// one split-K scratch per (device, stream): concurrent GEMMs on different
+// streams (e.g. tensor-parallel ranks sharing a process) never share it
+SplitScratch& scratch(cudaStream_t st) {
+  static std::mutex mu;
+  static std::unordered_map<uint64_t, SplitScratch*> by_key;
   int dev = 0;
   cudaGetDevice(&dev);
-  return s[dev & 15];
+  const uint64_t key = (reinterpret_cast<uint64_t>(st) << 4) ^ (uint64_t)dev;
+  std::lock_guard<std::mutex> g(mu);
+  auto it = by_key.find(key);
+  if (it != by_key.end()) return *it->second;
+  SplitScratch* sc = new SplitScratch();
+  by_key.emplace(key, sc);
+  return *sc;
 }
 
 template <int EPI, int BN>
@@ -379,7 +388,7 @@ int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, void* C, int64_t ldc
   const int tiles = ((M + TC_BM - 1) / TC_BM) * (N / BN);
   const int units = tiles * splits;
   const int grid = units < num_sms() ? units : num_sms();
-  SplitScratch& sc = scratch();
+  SplitScratch& sc = scratch(st);
   if (splits > 1) {
     if (sc.flag_elems < tiles) {
       if (sc.flags) cudaFree(sc.flags);

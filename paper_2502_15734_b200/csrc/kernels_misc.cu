@@ -523,6 +523,14 @@ __global__ void __launch_bounds__(256) extract_kernel(const T* __restrict__ kv_k
   }
 }
 
+__global__ void add_f32_kernel(float4* __restrict__ dst, const float4* __restrict__ src, int64_t n4) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+    float4 a = dst[i], b = src[i];
+    a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
+    dst[i] = a;
+  }
+}
+
 __global__ void flush_kernel(int4* p, size_t n, int seed) {
   for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
     p[i] = make_int4(seed, (int)i, seed, (int)i);
@@ -652,15 +660,10 @@ int cc_logits_argmax(const void* hidden_rows, const float* norm_w, double eps, c
     if (argmax) {
       // partials live after the logits rows in a small static scratch
       constexpr int PARTS = 64;
-      static A* part_v = nullptr;
-      static int32_t* part_i = nullptr;
-      static int cap = 0;
-      if (cap < m * PARTS) {
-        if (part_v) { cudaFree(part_v); cudaFree(part_i); }
-        cudaMalloc(&part_v, sizeof(A) * 8 * PARTS);
-        cudaMalloc(&part_i, sizeof(int32_t) * 8 * PARTS);
-        cap = 8 * PARTS;
-      }
+      uint8_t* scratch = (uint8_t*)stream_scratch(as_stream(stream), 1, (sizeof(A) + sizeof(int32_t)) * 8 * PARTS);
+      if (!scratch) return fail(CC_E_CUDA, "logits_argmax: scratch allocation failed");
+      A* part_v = reinterpret_cast<A*>(scratch);
+      int32_t* part_i = reinterpret_cast<int32_t*>(scratch + sizeof(A) * 8 * PARTS);
       argmax_kernel<A><<<dim3(m, PARTS), 1024, 0, as_stream(stream)>>>((const A*)logits, argmax, vocab, part_v, part_i, 0);
       rc = check_launch("argmax_partial");
       if (rc) return rc;
@@ -708,6 +711,16 @@ int cc_extract_to_pool(const void* kv_k, const void* kv_v, int64_t req_layer_str
       return check_launch("extract_to_pool");
     });
   });
+}
+
+int cc_add_f32(float* dst, const float* src, int64_t n, void* stream) {
+  CCB_REQUIRE(n % 4 == 0 && ((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 15) == 0,
+              "add_f32: needs 16-byte aligned buffers of a multiple of 4 floats");
+  if (n == 0) return 0;
+  const int64_t n4 = n / 4;
+  const int grid = (int)std::min<int64_t>((n4 + 255) / 256, (int64_t)num_sms() * 8);
+  add_f32_kernel<<<grid, 256, 0, as_stream(stream)>>>((float4*)dst, (const float4*)src, n4);
+  return check_launch("add_f32");
 }
 
 int cc_flush_l2(void* scratch, size_t bytes, void* stream) {

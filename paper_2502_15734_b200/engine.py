@@ -108,7 +108,7 @@ class LazyAttention:
     def materialize(self, layer: int) -> np.ndarray:
         import torch
 
-        cfg = self.model.config
+        cfg = self.model.kcfg
         n_l = self.plan.n_act[layer]
         H = cfg.n_heads
         if n_l == 0:
@@ -129,13 +129,15 @@ class LazyAttention:
 def _workspace(model: Model, plan: DevicePlan):
     import torch
 
-    cfg = model.config
+    cfg = model.kcfg
     L, n, nr = cfg.n_layers, plan.n, max(plan.n_rows, 1)
     T, Hd = model.torch_dtype, model.hidden_dtype
     d, q, kv, ff = cfg.d_model, cfg.q_width(), cfg.kv_width(), cfg.ff_dim()
     dev = model.device
     e = torch.empty
+    tp = model.tp is not None and model.tp.world > 1
     return {
+        "partial": e((nr, d), dtype=Hd, device=dev) if tp else None,
         "hidden": e((nr, d), dtype=Hd, device=dev),
         "kv_k": e((L, n, kv), dtype=T, device=dev),
         "kv_v": e((L, n, kv), dtype=T, device=dev),
@@ -150,7 +152,7 @@ def _workspace(model: Model, plan: DevicePlan):
 
 
 def _record_default(model: Model, plan: DevicePlan) -> bool:
-    cfg = model.config
+    cfg = model.kcfg
     bytes_q = sum(plan.n_act) * cfg.q_width() * model.torch_dtype.itemsize
     return plan.n <= 8192 and bytes_q <= (256 << 20)
 
@@ -211,10 +213,14 @@ _NOTIMER = _NoTimer()
 def execute(model: Model, plan: DevicePlan, ws: dict, *, record=False, record_values=False, stats=False,
             gemm_impl=0, attn_impl=0, timer=None):
     """Launch the per-layer pipeline on the current stream.  Returns the
-    LazyAttention (if recording), value trace list and stats masses."""
+    LazyAttention (if recording), value trace list and stats masses.
+    Under tensor parallelism (model.tp) the o_proj and down_proj GEMMs write
+    rank-partial outputs that are all-reduced before the residual add."""
     import torch
 
-    cfg = model.config
+    cfg = model.kcfg
+    tp = model.tp if (model.tp is not None and model.tp.world > 1) else None
+    part = ws.get("partial")
     L, n = cfg.n_layers, plan.n
     H, Hkv, dh, d = cfg.n_heads, cfg.kv_heads(), cfg.head_dim(), cfg.d_model
     qw, kvw, ff = cfg.q_width(), cfg.kv_width(), cfg.ff_dim()
@@ -269,8 +275,11 @@ def execute(model: Model, plan: DevicePlan, ws: dict, *, record=False, record_va
         if record_values:
             vtrace.append((kv_v[l], ctx[:n_l].clone()))
         with tm.span("gemm", flops=2.0 * n_l * qw * d):
-            N.call("cc_gemm", P(ctx), qw, P(lw["w_o"]), qw, P(hidden), d, n_l, d, qw, N.EPI_RESID_ADD, dt, gemm_impl,
-                   s)
+            if tp is None:
+                N.call("cc_gemm", P(ctx), qw, P(lw["w_o"]), qw, P(hidden), d, n_l, d, qw, N.EPI_RESID_ADD, dt,
+                       gemm_impl, s)
+            else:
+                _tp_partial_gemm(model, tp, ctx, qw, lw["w_o"], hidden, part, n_l, d, qw, dt, gemm_impl, s)
         N.call("cc_rmsnorm", P(hidden), P(xn), P(lw.get("mlp_norm")), n_l, d, eps, dt, s)
         if cfg.mlp == "swiglu":
             with tm.span("gemm", flops=2.0 * n_l * 2 * ff * d):
@@ -280,13 +289,36 @@ def execute(model: Model, plan: DevicePlan, ws: dict, *, record=False, record_va
             with tm.span("gemm", flops=2.0 * n_l * ff * d):
                 N.call("cc_gemm", P(xn), d, P(lw["w_up"]), d, P(act), ff, n_l, ff, d, N.EPI_GELU, dt, gemm_impl, s)
         with tm.span("gemm", flops=2.0 * n_l * ff * d):
-            N.call("cc_gemm", P(act), ff, P(lw["w_down"]), ff, P(hidden), d, n_l, d, ff, N.EPI_RESID_ADD, dt,
-                   gemm_impl, s)
+            if tp is None:
+                N.call("cc_gemm", P(act), ff, P(lw["w_down"]), ff, P(hidden), d, n_l, d, ff, N.EPI_RESID_ADD, dt,
+                       gemm_impl, s)
+            else:
+                _tp_partial_gemm(model, tp, act, ff, lw["w_down"], hidden, part, n_l, d, ff, dt, gemm_impl, s)
+    if tp is not None and mass is not None:
+        # K8a divides by the rank's own heads: global head mean = sum over ranks / world
+        mass.mul_(1.0 / tp.world)
+        tp.allreduce_(mass)
     return lazy, vtrace, mass
 
 
+def _tp_partial_gemm(model, tp, a, lda, w, hidden, part, n_l, d, k, dt, gemm_impl, s):
+    """Row-parallel projection: partial = a_local @ W_local^T on this rank,
+    summed over the TP group (NCCL all-reduce), then hidden += sum."""
+    P = N.ptr
+    if dt == N.F64:
+        part[:n_l].zero_()
+        N.call("cc_gemm", P(a), lda, P(w), lda, P(part), d, n_l, d, k, N.EPI_RESID_ADD, dt, gemm_impl, s)
+        tp.allreduce_(part[:n_l])
+        hidden[:n_l].add_(part[:n_l])
+        return
+    part[:n_l].zero_()
+    N.call("cc_gemm", P(a), lda, P(w), lda, P(part), d, n_l, d, k, N.EPI_RESID_ADD, dt, gemm_impl, s)
+    tp.allreduce_(part[:n_l])
+    N.call("cc_add_f32", P(hidden), P(part), n_l * d, s)
+
+
 def _payloads(model: Model, request):
-    cfg = model.config
+    cfg = model.kcfg
     out = []
     for seg in request.segments:
         c = seg.cache
@@ -295,7 +327,7 @@ def _payloads(model: Model, request):
             continue
         if c.n_layers != cfg.n_layers:
             raise PlanError(f"injected cache has {c.n_layers} layers, model has {cfg.n_layers}")
-        if c.width != cfg.kv_width():
+        if c.width != cfg.kv_width() and c.width != model.config.kv_width():
             raise ShapeError("injected cache width != kv width (d_model for MHA)")
         out.append(c.device_payload(model))
     return out
@@ -306,7 +338,7 @@ def run_prefill(model: Model, request, record_values: bool = False, record_atten
     import torch
 
     N.require_cuda()
-    cfg = model.config
+    cfg = model.kcfg
     payloads = _payloads(model, request)
     fresh = [i for i, seg in enumerate(request.segments) if seg.cache is None]
     if stats == "auto":
@@ -437,7 +469,7 @@ def logits_device(model: Model, hidden_rows):
 def extract_rows(result: PrefillResult, start: int, stop: int, source_prefix=()) -> ChunkCache:
     """K10: request KV rows [start, stop) -> fresh pool blocks of a new cache."""
     model = result.model
-    cfg = model.config
+    cfg = model.kcfg
     kv_k, kv_v = result.kv._dev if result.kv._dev is not None else (None, None)
     n = stop - start
     if n <= 0:

@@ -136,7 +136,7 @@ class KVPool:
     def __init__(self, model: "Model", n_blocks: int = 256):
         import torch
 
-        cfg = model.config
+        cfg = model.kcfg
         self.L, self.kvw = cfg.n_layers, cfg.kv_width()
         self.torch_dtype = model.torch_dtype
         self.storage = torch.zeros((self.L, n_blocks, 2, BLOCK, self.kvw), dtype=self.torch_dtype, device=model.device)
@@ -213,10 +213,17 @@ class _Payload:
 class Model:
     """Weights resident on the GPU (K-major [out, in] layout) + the KV pool."""
 
-    def __init__(self, config: ModelConfig, weights: dict, device, host_weights: dict | None = None):
+    def __init__(self, config: ModelConfig, weights: dict, device, host_weights: dict | None = None, tp=None):
         import torch
 
         self.config = config
+        self.tp = tp  # parallel.TPContext or None
+        if tp is not None and tp.world > 1:
+            from .parallel import local_config
+
+            self.kcfg = local_config(config, tp.slices)  # rank-local head / MLP shape for the kernels
+        else:
+            self.kcfg = config
         self.device = device
         self.w = weights
         self.dtype_code = _DTYPES[config.dtype]
@@ -322,23 +329,42 @@ def _draw_host(config: ModelConfig) -> dict:
     return {"embed": embed, "unembed": unembed, "layers": layers}
 
 
-def build_model(config: ModelConfig, device=None, host_draw: bool | None = None) -> Model:
+def build_model(config: ModelConfig, device=None, host_draw: bool | None = None, tp=None) -> Model:
     """Fill all weights from a seeded stream (model.py:98-118) and place them
     on the GPU.  Small models use the reference's numpy stream exactly (so
     fp64 mode reproduces the reference weights bit for bit); large
     (Llama-shaped) models are drawn on the device with a seeded torch
-    generator, N(0,1)/sqrt(fan_in), norms = 1."""
+    generator, N(0,1)/sqrt(fan_in), norms = 1.
+
+    ``tp`` (a ``parallel.TPContext``) builds one tensor-parallel rank: its
+    slice of the host-drawn weights (so ranks compose exactly into the full
+    model), or for device-drawn (large) models its own seeded shard."""
     import torch
 
     config.validate()
     N.require_cuda()
     dev = torch.device("cuda") if device is None else torch.device(device)
     tdt = {"fp64": torch.float64, "fp32": torch.float32, "bf16": torch.bfloat16}[config.dtype]
-    d, q, kv, ff = config.d_model, config.q_width(), config.kv_width(), config.ff_dim()
+    sl = tp.slices if (tp is not None and tp.world > 1) else None
+    kc = config
+    if sl is not None:
+        from .parallel import local_config, shard_layer_weights
+
+        kc = local_config(config, sl)
+    d, q, kv, ff = kc.d_model, kc.q_width(), kc.kv_width(), kc.ff_dim()
     if host_draw is None:
         host_draw = config.n_params() <= 64_000_000
     host = _draw_host(config) if host_draw else None
-    gen = None if host_draw else torch.Generator(device=dev).manual_seed(config.seed)
+    if host is not None and sl is not None:
+        full = host
+        host = {"embed": full["embed"], "unembed": full["unembed"], "layers": []}
+        for hl in full["layers"]:
+            sh = shard_layer_weights({"wq": hl.wq, "wk": hl.wk, "wv": hl.wv, "wo": hl.wo, "w_up": hl.w_up,
+                                      "w_down": hl.w_down, "w_gate": hl.w_gate}, config, sl)
+            host["layers"].append(LayerWeights(wq=sh["wq"], wk=sh["wk"], wv=sh["wv"], wo=sh["wo"], w_up=sh["w_up"],
+                                               w_down=sh["w_down"], w_gate=sh.get("w_gate")))
+    seed = config.seed if sl is None else config.seed * 1000003 + sl.rank
+    gen = None if host_draw else torch.Generator(device=dev).manual_seed(seed)
 
     def dev_normal(r, c, fan):
         t = torch.randn((r, c), generator=gen, device=dev, dtype=torch.float32)
@@ -383,9 +409,9 @@ def build_model(config: ModelConfig, device=None, host_draw: bool | None = None)
     if config.norm_weight:
         w["final_norm"] = torch.ones(d, dtype=torch.float32, device=dev)
     host_view = None
-    if host is not None and config.dtype == "fp64":
+    if host is not None and config.dtype == "fp64" and sl is None:
         host_view = host
-    return Model(config, w, dev, host_view)
+    return Model(config, w, dev, host_view, tp=tp)
 
 
 # ---------------------------------------------------------------------------
@@ -485,6 +511,10 @@ class ChunkCache:
         if p is not None and p.pool is model.pool:
             return p
         keys, values = self.keys, self.values
+        if model.tp is not None and model.tp.world > 1 and keys[0].shape[1] == model.config.kv_width():
+            cols = model.tp.slices.kv_cols(model.config.head_dim())
+            keys = [np.asarray(k)[:, cols] for k in keys]
+            values = [np.asarray(v)[:, cols] for v in values]
         n = keys[0].shape[0]
         nb = max(1, -(-n // BLOCK))
         pool = model.pool

@@ -1,0 +1,95 @@
+"""Tensor-parallel engine on one B200: two TP ranks (separate shard models
+and CUDA streams) run concurrently in threads; their all-reduce is a
+barrier + device sum.  The composed result must equal the unsharded model
+(and the oracle), i.e. the sharded kernels + the two all-reduces per layer
+reproduce model.py:348-442."""
+import threading
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle import cachecraft_oracle as O  # noqa: E402
+
+
+class ThreadGroup:
+    def __init__(self, world):
+        self.world = world
+        self.bar = threading.Barrier(world)
+        self.buf = [None] * world
+
+    def allreduce_for(self, rank):
+        def ar(t):
+            torch.cuda.current_stream().synchronize()
+            self.buf[rank] = t
+            self.bar.wait()
+            if rank == 0:
+                total = sum(b.clone() for b in self.buf)
+                for b in self.buf:
+                    b.copy_(total)
+                torch.cuda.synchronize()
+            self.bar.wait()
+            return t
+        return ar
+
+
+@pytest.mark.parametrize("dtype,tol", [("fp64", 1e-9), ("bf16", 5e-2)])
+def test_two_rank_tensor_parallel_matches_unsharded(dtype, tol):
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import paper_2502_15734_b200 as cc
+    from paper_2502_15734_b200 import parallel
+
+    kw = dict(n_layers=2, n_heads=8, d_model=512, d_head=64, vocab_size=512, rpe_base=500000.0, seed=3,
+              n_kv_heads=2, d_ff=1024, mlp="swiglu", norm_weight=True, rms_eps=1e-5)
+    cfg = cc.ModelConfig(dtype=dtype, **kw)
+    r = np.random.default_rng(2)
+    chunks = [r.integers(0, 512, n) for n in (64, 48)]
+    q = r.integers(0, 512, 16)
+    masks = [r.uniform(size=c.size) < 0.25 for c in chunks]
+    # creation caches from the oracle (full width); each rank uploads its kv slice
+    ocfg = O.OracleConfig(**kw)
+    w = O.draw_weights(ocfg)
+    lay0 = O.layout([{"tokens": c} for c in chunks], [])
+    o0 = O.prefill(w, ocfg, lay0, [None] * 2)
+    ocaches = [([k[s:e] for k in o0["keys"]], [v[s:e] for v in o0["values"]]) for s, e in lay0["segment_slots"]]
+    lay = O.layout([{"tokens": c, "n_slots": c.size, "recompute": m} for c, m in zip(chunks, masks)], q)
+    ref = O.prefill(w, ocfg, lay, ocaches)
+
+    group = ThreadGroup(2)
+    results = [None, None]
+    errors = []
+
+    def rank_main(rank):
+        try:
+            stream = torch.cuda.Stream()
+            with torch.cuda.stream(stream):
+                sl = parallel.tp_slices(cfg.n_heads, cfg.kv_heads(), cfg.ff_dim(), rank, 2)
+                tp = parallel.TPContext(sl, allreduce=group.allreduce_for(rank))
+                model = cc.build_model(cfg, tp=tp)
+                segs = [cc.Segment(tokens=c, cache=cc.ChunkCache(keys=k, values=v, n_tokens=c.size), recompute=m)
+                        for c, (k, v), m in zip(chunks, ocaches, masks)]
+                res = cc.prefill(model, cc.build_request(segs, q), first_token=True, record_attention=False)
+                stream.synchronize()
+                results[rank] = (res.hidden, [res.kv.keys[l] for l in range(2)], res.first_token)
+        except Exception as e:  # pragma: no cover - surfaced below
+            errors.append(e)
+            group.bar.abort()
+
+    th = [threading.Thread(target=rank_main, args=(k,)) for k in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=300)
+    assert not errors, errors
+    for rank in range(2):
+        h, keys, tok = results[rank]
+        err = np.linalg.norm(h - ref["hidden"]) / np.linalg.norm(ref["hidden"])
+        assert err < tol, (rank, err)
+        assert tok == O.greedy_token(w, ocfg, ref)
+    for l in range(2):
+        k = np.concatenate([results[0][1][l], results[1][1][l]], axis=1)
+        err = np.linalg.norm(k - ref["keys"][l]) / np.linalg.norm(ref["keys"][l])
+        assert err < tol
