@@ -35,6 +35,17 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "prefill tokens/sec at 15% recompute (Llama-3-8B shapes, 10x512+32)"
+WORKLOADS = {
+    "8b": "config2: Llama-3-8B shapes, 1 request of 10x512 reused chunks + 32-token question, 15% recompute per "
+          "chunk (K9 top-k of variant token scores)",
+    "8b-32k": "config5: Llama-3-8B shapes, 32k prompt of 64x512 reused chunks + 32, 15% recompute",
+    "70b": "config4: Llama-3-70B shapes, 16x1024 reused chunks + 32, 15% recompute, head-sharded TP{world}",
+}
+MODELS = {
+    "8b": "Llama-3-8B-shaped (L=32,d=4096,Hq=32,Hkv=8,dh=128,ff=14336,vocab=128256)",
+    "8b-32k": "Llama-3-8B-shaped (L=32,d=4096,Hq=32,Hkv=8,dh=128,ff=14336,vocab=128256)",
+    "70b": "Llama-3-70B-shaped (L=80,d=8192,Hq=64,Hkv=8,dh=128,ff=28672,vocab=128256)",
+}
 UNIT = "tokens/s"
 
 
@@ -53,7 +64,17 @@ def parse():
     p.add_argument("--no-baselines", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--cpu-layers", type=int, default=2, help="layers in the bounded CPU-oracle sample")
-    return p.parse_args()
+    p.add_argument("--config", default="8b", choices=["8b", "8b-32k", "70b"],
+                   help="8b = BASELINE config 2 (default); 8b-32k = config 5 (64x512+32); "
+                        "70b = config 4 (Llama-3-70B shapes, 16x1024+32, tensor parallel over the ranks)")
+    a = p.parse_args()
+    if a.config == "8b-32k":
+        a.chunks = 64
+    elif a.config == "70b":
+        a.chunks, a.chunk_len = 16, 1024
+        if a.layers == 32:
+            a.layers = 80
+    return a
 
 
 # ---------------------------------------------------------------------------
@@ -161,9 +182,20 @@ def make_workload(args, rank):
 
     import paper_2502_15734_b200 as cc
 
-    cfg = cc.ModelConfig.llama3_8b(n_layers=args.layers, dtype="bf16", seed=0)
-    model = cc.build_model(cfg)
-    r = np.random.default_rng(1000 + rank)
+    tp = None
+    if getattr(args, "config", "8b") == "70b":
+        from paper_2502_15734_b200 import parallel
+
+        cfg = cc.ModelConfig.llama3_70b(n_layers=args.layers, dtype="bf16", seed=0)
+        world = int(os.environ.get("WORLD_SIZE", "1"))
+        if world > 1:
+            tp = parallel.TPContext(parallel.tp_slices(cfg.n_heads, cfg.kv_heads(), cfg.ff_dim(), rank, world))
+        model = cc.build_model(cfg, tp=tp)
+        r = np.random.default_rng(1000)  # every TP rank serves the same request
+    else:
+        cfg = cc.ModelConfig.llama3_8b(n_layers=args.layers, dtype="bf16", seed=0)
+        model = cc.build_model(cfg)
+        r = np.random.default_rng(1000 + rank)
     chunks = [r.integers(0, cfg.vocab_size, args.chunk_len) for _ in range(args.chunks)]
     question = r.integers(0, cfg.vocab_size, args.question)
     store = cc.VariantStore(cc.StoreConfig(max_chunks=max(100, args.chunks), variants_per_chunk=5))
@@ -459,7 +491,8 @@ def main():
     clocks = clk.summary()
     ms_step = statistics.mean(ms)
     ms_max = allreduce_max(ms_step, world)
-    value = n_prompt * world / (ms_max / 1e3)
+    tp_mode = args.config == "70b" and world > 1
+    value = n_prompt * (1 if tp_mode else world) / (ms_max / 1e3)
     summ = timer.summary()
 
     # ---- e2e: public API with host buffers ----------------------------------
@@ -479,7 +512,7 @@ def main():
             d2h = 4 + sum(4 * len(cp.recompute) for cp in p.chunks if cp.recompute is not None)
         del res
     e2e_mean = allreduce_max(statistics.mean(e2e_ms), world)
-    e2e_value = n_prompt * world / (e2e_mean / 1e3)
+    e2e_value = n_prompt * (1 if tp_mode else world) / (e2e_mean / 1e3)
     ttft_p50 = statistics.median(e2e_ms)
 
     # ---- baselines on the same GPU --------------------------------------------
@@ -496,6 +529,7 @@ def main():
         del wsp
         baselines["prefix_cache_60pct_ours"] = {"tokens_per_s": round(n_prompt / (statistics.mean(msp) / 1e3), 1),
                                                 "ms_per_step": round(statistics.mean(msp), 3)}
+    if not args.no_baselines and not tp_mode:
         toks = torch.from_numpy(np.concatenate(chunks + [question]).astype(np.int64)).cuda()
         run, attn_name = torch_reference_full(model, toks)
         for _ in range(2):
@@ -526,7 +560,7 @@ def main():
             del ws_
 
     cpu = None
-    if rank == 0 and not args.no_cpu:
+    if rank == 0 and not args.no_cpu and args.config == "8b":
         v, cores, dt, desc = cpu_baseline(args, req, n_prompt)
         cpu = {"value": round(v, 3), "unit": UNIT, "cores": cores, "kind": "port", "sample": desc}
 
@@ -537,16 +571,18 @@ def main():
                            roofline_obj("attention", summ, peaks, "tensor")) if k]
     share = {k: round(v["ms_total"] / (sum(ms[: args.steps]) or 1), 4) for k, v in summ.items()}
     line = {
-        "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": round(ms_max, 4), "higher_is_better": True, "scaling": "weak",
+        "metric": METRIC if args.config == "8b" else METRIC.replace("Llama-3-8B shapes, 10x512+32", {
+            "8b-32k": "Llama-3-8B shapes, 64x512+32", "70b": "Llama-3-70B shapes, 16x1024+32"}[args.config]),
+        "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms_max, 4), "higher_is_better": True,
+        "scaling": "strong" if tp_mode else "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init weights, random token chunks)",
-        "config": {"workload": "config2: Llama-3-8B shapes, 1 request of 10x512 reused chunks + 32-token question, "
-                               "15% recompute per chunk (K9 top-k of variant token scores)",
-                   "model": "Llama-3-8B-shaped (L=32,d=4096,Hq=32,Hkv=8,dh=128,ff=14336,vocab=128256)",
+        "config": {"workload": WORKLOADS[args.config].format(world=world),
+                   "model": MODELS[args.config],
                    "layers": args.layers, "chunks": args.chunks, "chunk_len": args.chunk_len,
                    "question": args.question, "recompute_ratio": args.ratio, "prompt_tokens": n_prompt,
-                   "recomputed_rows": n_recomputed, "parallelism": f"request-sharded x{world}",
-                   "l2": "inputs larger than L2 (16 GB weights streamed per step)"},
+                   "recomputed_rows": n_recomputed, "parallelism": f"tensor-parallel x{world}" if tp_mode else f"request-sharded x{world}",
+                   "l2": "inputs larger than L2 (%s GB of weights streamed per step)" % ("140" if args.config == "70b" else "16")},
         "ttft_ms": {"p50_e2e": round(ttft_p50, 3), "device_mean": round(ms_step, 3)},
         "e2e": {"value": round(e2e_value, 1), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h), "path": "build_plan -> plan_to_request -> prefill(first_token=True)"},
