@@ -208,9 +208,13 @@ int cc_attention_probs(const void* q, const void* k_rot, const int32_t* q_slot, 
 int cc_segment_mass(const void* q, const void* k_rot, const int32_t* q_slot, const uint8_t* key_pad, const void* lse,
                     const int32_t* seg_lo, const int32_t* seg_hi, int n_seg, const int32_t* rows, int n_rows,
                     double* mass, int n_keys, int n_heads, int n_kv_heads, int d_head, int dtype, void* stream) {
-  (void)n_keys;
   if (n_rows == 0) return 0;
   CCB_REQUIRE(d_head <= 256, "segment_mass: d_head must be <= 256");
+  if (dtype == CC_BF16) {
+    int rc = segment_mass_tc_bf16(q, k_rot, q_slot, key_pad, (const float*)lse, seg_lo, seg_hi, n_seg, rows, n_rows,
+                                  mass, n_keys, n_heads, n_kv_heads, d_head, as_stream(stream));
+    if (rc != CC_E_UNSUP) return rc;
+  }
   return CCB_DISPATCH_DTYPE(dtype, T, [&] {
     using A = typename Acc<T>::type;
     segment_mass_kernel<T><<<n_rows, 256, 0, as_stream(stream)>>>((const T*)q, (const T*)k_rot, q_slot, key_pad,

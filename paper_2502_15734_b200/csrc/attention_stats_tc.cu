@@ -1,0 +1,310 @@
+// K8a on the tensor cores: head-mean attention mass of selected query rows
+// onto key segments (stats.py:68-106, harness.py:331-354) without
+// materialising the softmax weights.  Given the row's log-sum-exp from the
+// attention kernel, p = exp(s - lse) is recomputed tile by tile:
+//   warp 0     TMA K tiles (128 keys, 2-stage ring)
+//   warp 1     tcgen05.mma S = Q K^T into one of two TMEM buffers
+//   warps 2-5  load the CTA's Q rows (gathered by index, written 128B-swizzled
+//              into smem), then per tile: tcgen05.ld S, p = exp2(s*c - lse*log2e)
+//              masked by the causal limit and pads, accumulated per key segment
+//              with a warp-uniform run-length walk over the tile's segment map.
+// Partial sums per (row, kv group) are folded over the G heads of the CTA in
+// fixed order; a second kernel folds the kv groups in fixed order and divides
+// by Hq.  No atomics: run-to-run bit-identical.
+#include <math.h>
+
+#include "attention.cuh"
+#include "common.cuh"
+#include "sm100.cuh"
+
+namespace ccb {
+
+namespace {
+
+using namespace sm100;
+
+constexpr int ST_BN = 128;
+constexpr int ST_STAGES = 2;
+constexpr int ST_MAXSEG = 128;  // n_seg + 1 (diagonal) <= 128
+
+__host__ __device__ constexpr uint32_t idesc_s(int M, int N) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+__device__ __forceinline__ float ex2f(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+template <int DH>
+struct StSmem {
+  static constexpr int Q_BYTES = 128 * DH * 2;
+  static constexpr int K_BYTES = ST_BN * DH * 2;
+  static constexpr int Q_OFF = 0;
+  static constexpr int K_OFF = Q_BYTES;
+  static constexpr int ACC_OFF = K_OFF + ST_STAGES * K_BYTES;            // float [128][ST_MAXSEG]
+  static constexpr int SEG_OFF = ACC_OFF + 128 * (ST_MAXSEG + 1) * 4;     // int [2][ST_BN]
+  static constexpr int BAR_OFF = SEG_OFF + 2 * ST_BN * 4;
+  static constexpr size_t TOTAL = 1024 + BAR_OFF + 256;
+};
+
+template <int DH>
+__global__ void __launch_bounds__(192, 1)
+    attn_stats_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __nv_bfloat16* __restrict__ q,
+                         const int32_t* __restrict__ rows, int n_rows, const int32_t* __restrict__ q_slot,
+                         const uint8_t* __restrict__ key_pad, const float* __restrict__ lse,
+                         const int32_t* __restrict__ seg_lo, const int32_t* __restrict__ seg_hi, int n_seg,
+                         float* __restrict__ part, int n_keys, int Hq, int Hkv, int G, float scale_log2) {
+  using SM = StSmem<DH>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = base + SM::Q_OFF;
+  uint8_t* sK = base + SM::K_OFF;
+  float* acc = reinterpret_cast<float*>(base + SM::ACC_OFF);
+  int* segmap = reinterpret_cast<int*>(base + SM::SEG_OFF);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(base + SM::BAR_OFF);
+  uint64_t* q_full = bars;
+  uint64_t* k_full = bars + 1;
+  uint64_t* k_empty = k_full + ST_STAGES;
+  uint64_t* s_full = k_empty + ST_STAGES;
+  uint64_t* s_empty = s_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_empty + 2);
+  __shared__ int s_kmax;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = blockIdx.x;
+  const int R = 128 / G;
+  const int r0 = blockIdx.y * R;  // first stats row of this CTA
+  const int W = n_seg + 1;
+
+  if (threadIdx.x == 0) s_kmax = -1;
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmK);
+    mbar_init(q_full, 128);
+    for (int s = 0; s < ST_STAGES; ++s) {
+      mbar_init(&k_full[s], 1);
+      mbar_init(&k_empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&s_full[b], 1);
+      mbar_init(&s_empty[b], 128);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<256>(tmem_slot);
+  __syncthreads();
+  if (threadIdx.x < 128) {
+    const int sr = r0 + threadIdx.x / G;
+    if (sr < n_rows) atomicMax(&s_kmax, q_slot[rows[sr]]);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int kmax = s_kmax;
+  const int n_tiles = kmax < 0 ? 0 : kmax / ST_BN + 1;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int i = 0; i < n_tiles; ++i) {
+        const int st = i % ST_STAGES;
+        mbar_wait(&k_empty[st], ((i / ST_STAGES) & 1) ^ 1);
+        mbar_expect_tx(&k_full[st], SM::K_BYTES);
+#pragma unroll
+        for (int a = 0; a < DH / 64; ++a)
+          tma_load_2d(sK + st * SM::K_BYTES + a * ST_BN * 128, &tmK, &k_full[st], g * DH + a * 64, i * ST_BN);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && n_tiles > 0) {
+      constexpr uint32_t id = idesc_s(128, ST_BN);
+      mbar_wait(q_full, 0);
+      for (int i = 0; i < n_tiles; ++i) {
+        const int st = i % ST_STAGES, b = i & 1;
+        mbar_wait(&k_full[st], (i / ST_STAGES) & 1);
+        mbar_wait(&s_empty[b], ((i >> 1) & 1) ^ 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < DH / 16; ++kk) {
+          const int a = kk >> 2, w = kk & 3;
+          uint64_t ad = desc_sw128(sQ + a * 128 * 128) + 2 * w;
+          uint64_t bd = desc_sw128(sK + st * SM::K_BYTES + a * ST_BN * 128) + 2 * w;
+          mma_bf16(tmem + b * ST_BN, ad, bd, id, kk > 0);
+        }
+        mma_commit(&s_full[b]);
+        mma_commit(&k_empty[st]);
+      }
+    }
+  } else {
+    const int q4 = warp & 3;
+    const int m = q4 * 32 + lane;
+    const int et = threadIdx.x - 64;
+    const int sr = r0 + m / G;
+    const int head = g * G + m % G;
+    const bool valid = sr < n_rows;
+    const int qrow = valid ? rows[sr] : 0;
+    const int lim = valid ? q_slot[qrow] : -1;
+    const float base_l2 = valid ? lse[(int64_t)qrow * Hq + head] * 1.4426950408889634f : 0.f;
+    // gather this M-row's q (dh bf16) into the 128B-swizzled K-major tile
+    {
+      const uint4* src = reinterpret_cast<const uint4*>(q + ((int64_t)qrow * Hq + head) * DH);
+#pragma unroll
+      for (int ch = 0; ch < DH / 8; ++ch) {
+        uint4 v = valid ? src[ch] : make_uint4(0, 0, 0, 0);
+        const int a = ch >> 3, c16 = ch & 7;
+        *reinterpret_cast<uint4*>(sQ + a * 128 * 128 + m * 128 + ((c16 ^ (m & 7)) << 4)) = v;
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_arrive(q_full);
+    }
+    float* my = acc + m * (ST_MAXSEG + 1);  // padded stride: no bank conflicts
+    for (int sg = 0; sg < W; ++sg) my[sg] = 0.f;
+    float diag = 0.f;
+    for (int i = 0; i < n_tiles; ++i) {
+      const int b = i & 1;
+      const int j0 = i * ST_BN;
+      // segment id of each key of the tile (-1 outside every segment)
+      {
+        const int j = j0 + et;
+        int sid = -1;
+        for (int sg = 0; sg < n_seg; ++sg)
+          if (j >= seg_lo[sg] && j < seg_hi[sg]) { sid = sg; break; }
+        if (j >= n_keys || (key_pad != nullptr && key_pad[j])) sid = -1;
+        segmap[b * ST_BN + et] = sid;
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      mbar_wait(&s_full[b], (i >> 1) & 1);
+      tc_fence_after();
+      float s[ST_BN];
+      {
+        uint32_t ra[32], rb[32], rc[32], rd[32];
+        const uint32_t ta = tmem + b * ST_BN + ((uint32_t)(q4 * 32) << 16);
+        tmem_ld32(ta, ra);
+        tmem_ld32(ta + 32, rb);
+        tmem_ld32(ta + 64, rc);
+        tmem_ld32(ta + 96, rd);
+        tmem_ld_wait();
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+          s[e] = __uint_as_float(ra[e]);
+          s[32 + e] = __uint_as_float(rb[e]);
+          s[64 + e] = __uint_as_float(rc[e]);
+          s[96 + e] = __uint_as_float(rd[e]);
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&s_empty[b]);
+      const int lim_rel = lim - j0;
+      int cur = segmap[b * ST_BN];
+      float run = 0.f;
+#pragma unroll
+      for (int c = 0; c < ST_BN; ++c) {
+        const int sid = segmap[b * ST_BN + c];  // warp-uniform (same column for every lane)
+        if (sid != cur) {
+          if (cur >= 0) my[cur] += run;
+          run = 0.f;
+          cur = sid;
+        }
+        const float p = (c <= lim_rel && sid >= 0) ? ex2f(fmaf(s[c], scale_log2, -base_l2)) : 0.f;
+        run += p;
+        if (c == lim_rel) diag += p;
+      }
+      if (cur >= 0) my[cur] += run;
+    }
+    my[n_seg] = diag;
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+    // fold the G heads of each row in fixed order -> part[sr][g][W]
+    for (int t = et; t < R * W; t += 128) {
+      const int rr = t / W, sg = t % W;
+      if (r0 + rr < n_rows) {
+        float v = 0.f;
+        for (int h = 0; h < G; ++h) v += acc[(rr * G + h) * (ST_MAXSEG + 1) + sg];
+        part[((int64_t)(r0 + rr) * Hkv + g) * W + sg] = v;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<256>(tmem);
+  }
+}
+
+__global__ void seg_mass_fold_kernel(const float* __restrict__ part, double* __restrict__ mass, int n_rows, int Hkv,
+                                     int W, int Hq) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (int64_t)n_rows * W) return;
+  const int r = (int)(t / W), sg = (int)(t % W);
+  double v = 0.0;
+  for (int g = 0; g < Hkv; ++g) v += (double)part[((int64_t)r * Hkv + g) * W + sg];
+  mass[t] = v / Hq;
+}
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+template <int DH>
+int launch(const void* q, const void* k, const int32_t* q_slot, const uint8_t* key_pad, const float* lse,
+           const int32_t* seg_lo, const int32_t* seg_hi, int n_seg, const int32_t* rows, int n_rows, double* mass,
+           int n_keys, int Hq, int Hkv, cudaStream_t st) {
+  static EncodeTiledFn enc = nullptr;
+  if (!enc) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult qr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &qr) != cudaSuccess ||
+        qr != cudaDriverEntryPointSuccess)
+      return fail(CC_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+    enc = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  CUtensorMap mk;
+  cuuint64_t dims[2] = {(cuuint64_t)Hkv * DH, (cuuint64_t)n_keys};
+  cuuint64_t strides[1] = {(cuuint64_t)Hkv * DH * 2};
+  cuuint32_t box[2] = {64, (cuuint32_t)ST_BN};
+  cuuint32_t estr[2] = {1, 1};
+  if (enc(&mk, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(k), dims, strides, box, estr,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return fail(CC_E_CUDA, "segment_mass_tc: tensor map encode failed");
+  const int G = Hq / Hkv, R = 128 / G, W = n_seg + 1;
+  float* part = (float*)stream_scratch(st, 2, sizeof(float) * (size_t)n_rows * Hkv * W);
+  if (!part) return fail(CC_E_CUDA, "segment_mass_tc: scratch allocation failed");
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(attn_stats_tc_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)StSmem<DH>::TOTAL);
+    attr = true;
+  }
+  dim3 grid(Hkv, (n_rows + R - 1) / R);
+  const float scale_log2 = 1.4426950408889634f / sqrtf((float)DH);
+  attn_stats_tc_kernel<DH><<<grid, 192, StSmem<DH>::TOTAL, st>>>(mk, (const __nv_bfloat16*)q, rows, n_rows, q_slot,
+                                                                   key_pad, lse, seg_lo, seg_hi, n_seg, part, n_keys,
+                                                                   Hq, Hkv, G, scale_log2);
+  int rc = check_launch("segment_mass_tc");
+  if (rc) return rc;
+  const int64_t total = (int64_t)n_rows * W;
+  seg_mass_fold_kernel<<<(int)((total + 255) / 256), 256, 0, st>>>(part, mass, n_rows, Hkv, W, Hq);
+  return check_launch("segment_mass_fold");
+}
+
+}  // namespace
+
+int segment_mass_tc_bf16(const void* q, const void* k, const int32_t* q_slot, const uint8_t* key_pad,
+                         const float* lse, const int32_t* seg_lo, const int32_t* seg_hi, int n_seg,
+                         const int32_t* rows, int n_rows, double* mass, int n_keys, int Hq, int Hkv, int dh,
+                         cudaStream_t st) {
+  const int G = Hq / Hkv;
+  if (G < 1 || G > 128 || (128 % G) != 0) return fail(CC_E_UNSUP, "segment_mass_tc: GQA group must divide 128");
+  if (n_seg + 1 > ST_MAXSEG) return fail(CC_E_UNSUP, "segment_mass_tc: too many segments");
+  if ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(k)) & 15)
+    return fail(CC_E_UNSUP, "segment_mass_tc: pointers must be 16-byte aligned");
+  if (dh == 128)
+    return launch<128>(q, k, q_slot, key_pad, lse, seg_lo, seg_hi, n_seg, rows, n_rows, mass, n_keys, Hq, Hkv, st);
+  if (dh == 64)
+    return launch<64>(q, k, q_slot, key_pad, lse, seg_lo, seg_hi, n_seg, rows, n_rows, mass, n_keys, Hq, Hkv, st);
+  return fail(CC_E_UNSUP, "segment_mass_tc: d_head must be 64 or 128");
+}
+
+}  // namespace ccb

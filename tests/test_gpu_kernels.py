@@ -244,3 +244,47 @@ def test_logits_argmax_first_max_wins(N):
     N.call("cc_logits_argmax", N.ptr(h), None, 1e-6, N.ptr(U), N.ptr(logits), N.ptr(tok), 1, d, vocab, N.F32,
            N.stream_ptr())
     assert int(tok.item()) == 17
+
+
+@pytest.mark.parametrize("Hq,Hkv,dh", [(32, 8, 128), (4, 4, 64)])
+def test_segment_mass_tensor_core_matches_simt(N, Hq, Hkv, dh):
+    """K8a: the tcgen05 segment-mass kernel against the SIMT reference (fp64
+    sums of the same softmax) and against torch fp32 probabilities."""
+    n, nq = 900, 300
+    g = torch.Generator(device="cuda").manual_seed(Hq)
+    q_slot = torch.sort(torch.randperm(n, generator=g, device="cuda")[:nq]).values.int().contiguous()
+    q = torch.randn((nq, Hq, dh), generator=g, device="cuda").bfloat16()
+    k = torch.randn((n, Hkv, dh), generator=g, device="cuda").bfloat16()
+    v = torch.randn((n, Hkv, dh), generator=g, device="cuda").bfloat16()
+    pad = torch.zeros(n, dtype=torch.uint8, device="cuda")
+    pad[250:256] = 1
+    keep = pad[q_slot.long()] == 0
+    q_slot, q = q_slot[keep].contiguous(), q[keep].contiguous()
+    nq = q_slot.numel()
+    ctx = torch.empty((nq, Hq * dh), dtype=torch.bfloat16, device="cuda")
+    lse = torch.empty((nq, Hq), dtype=torch.float32, device="cuda")
+    N.call("cc_attention", N.ptr(q), N.ptr(k), N.ptr(v), N.ptr(q_slot), N.ptr(pad), N.ptr(ctx), N.ptr(lse), nq, n, Hq,
+           Hkv, dh, N.BF16, 0, N.stream_ptr())
+    bounds = [0, 100, 250, 400, 401, 700, 900]
+    lo = torch.tensor(bounds[:-1], dtype=torch.int32, device="cuda")
+    hi = torch.tensor(bounds[1:], dtype=torch.int32, device="cuda")
+    rows = torch.arange(0, nq, 3, dtype=torch.int32, device="cuda")
+    n_seg = len(bounds) - 1
+    out = {}
+    for name, dt in (("tc", N.BF16), ("simt", N.F32)):
+        mass = torch.zeros((rows.numel(), n_seg + 1), dtype=torch.float64, device="cuda")
+        qq, kk = (q, k) if dt == N.BF16 else (q.float(), k.float())
+        ll = lse if dt == N.BF16 else lse.float()
+        N.call("cc_segment_mass", N.ptr(qq), N.ptr(kk), N.ptr(q_slot), N.ptr(pad), N.ptr(ll), N.ptr(lo), N.ptr(hi),
+               n_seg, N.ptr(rows), rows.numel(), N.ptr(mass), n, Hq, Hkv, dh, dt, N.stream_ptr())
+        torch.cuda.synchronize()
+        out[name] = mass
+    torch.testing.assert_close(out["tc"], out["simt"], atol=2e-3, rtol=2e-3)
+    # rows of the softmax sum to one: segments cover every visible key
+    torch.testing.assert_close(out["tc"][:, :n_seg].sum(dim=1), torch.ones(rows.numel(), dtype=torch.float64,
+                                                                          device="cuda"), atol=3e-3, rtol=0)
+    again = torch.zeros_like(out["tc"])
+    N.call("cc_segment_mass", N.ptr(q), N.ptr(k), N.ptr(q_slot), N.ptr(pad), N.ptr(lse), N.ptr(lo), N.ptr(hi), n_seg,
+           N.ptr(rows), rows.numel(), N.ptr(again), n, Hq, Hkv, dh, N.BF16, N.stream_ptr())
+    torch.cuda.synchronize()
+    assert torch.equal(again, out["tc"])  # deterministic
