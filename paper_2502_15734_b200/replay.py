@@ -1,0 +1,319 @@
+"""Trace synthesis and GPU replay of the chunk-cache pipeline (
+cachecraft/harness.py:67-144, :324-591).
+
+``replay_gpu`` drives the hot path request by request exactly like the
+reference's ``replay``: plan (host decisions + K9 selection on the GPU) ->
+partial prefill (device engine, K8 statistics when a chunk misses) ->
+optional focused-chunk early termination (Algorithm 1 on the device's
+question->chunk masses, then the reference's second pass) -> store update
+(new variants from MISS chunks via K10 extraction, f_r touch for HITs).  The
+baseline policies run for real on the GPU: ``full_recompute`` (plain
+prefill), ``full_cache_naive`` (latest variant, nothing recomputed) and
+``exact_prefix`` (prefix caching: the longest chunk-boundary prefix seen
+before is reused verbatim from an HBM prefix registry, the rest computed).
+The tier simulator (simulated TTFT) is out of scope; TTFT here is measured.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import math
+import time
+from collections import OrderedDict
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .errors import ArgumentError
+from .model import Segment, build_request, extract_chunk_cache, plain_request, prefill
+from .planner import HIT, MISS, ChunkPlan, InferencePlan, apply_early_termination, build_plan, plan_to_request, \
+    predict_focused
+from .scoring import cci
+from .stats import creation_stats, question_stream
+from .store import chunk_hash
+
+POLICIES = ("cachecraft", "full_recompute", "full_cache_naive", "exact_prefix")
+
+
+@dataclass
+class TraceRecord:
+    request_id: int
+    chunk_ids: list
+    question: np.ndarray
+    arrival_s: float
+
+
+@dataclass
+class Trace:
+    records: list
+    corpus: dict
+
+    def __len__(self) -> int:
+        return len(self.records)
+
+
+def gen_synthetic(n_chunks: int, zipf_s: float, k: int, n_requests: int, chunk_len_range=(16, 64), seed: int = 0,
+                  question_len_range=(8, 16), vocab_size: int = 256, arrival_rate: float = 2.0) -> Trace:
+    """Zipf-popularity trace, same draw order as harness.py:84-106 (so a seed
+    gives the reference's trace): corpus lengths/tokens, then per request k
+    distinct chunks, a question and an exponential inter-arrival gap."""
+    if k > n_chunks:
+        raise ArgumentError(f"k ({k}) cannot exceed the corpus size ({n_chunks})")
+    if n_chunks < 1 or n_requests < 0:
+        raise ArgumentError("corpus and request counts must be non-negative")
+    g = np.random.default_rng(seed)
+    lo, hi = chunk_len_range
+    corpus = {}
+    for cid in range(n_chunks):
+        length = int(g.integers(lo, hi + 1))
+        corpus[cid] = g.integers(0, vocab_size, size=length)
+    pop = (1.0 / np.arange(1, n_chunks + 1)) ** zipf_s
+    pop /= pop.sum()
+    qlo, qhi = question_len_range
+    t = 0.0
+    recs = []
+    for rid in range(n_requests):
+        pick = g.choice(n_chunks, size=k, replace=False, p=pop)
+        q = g.integers(0, vocab_size, size=int(g.integers(qlo, qhi + 1)))
+        t += float(g.exponential(1.0 / arrival_rate))
+        recs.append(TraceRecord(request_id=rid, chunk_ids=[int(c) for c in pick], question=q, arrival_s=t))
+    return Trace(records=recs, corpus=corpus)
+
+
+def top_share(trace: Trace, top_fraction: float = 0.05) -> float:
+    """Fraction of retrievals landing on the most popular chunks (harness.py:110-122)."""
+    counts: dict = {}
+    for rec in trace.records:
+        for cid in rec.chunk_ids:
+            counts[cid] = counts.get(cid, 0) + 1
+    total = sum(counts.values())
+    if total == 0:
+        return 0.0
+    n_top = max(1, int(math.ceil(top_fraction * len(trace.corpus))))
+    return sum(sorted(counts.values(), reverse=True)[:n_top]) / total
+
+
+def fit_zipf_skew(n_chunks: int, k: int, n_requests: int, target_share: float = 0.6, seed: int = 0,
+                  iterations: int = 18, **gen_kwargs) -> float:
+    """Bisect the Zipf exponent in [0, 4] until the top-5% share meets the
+    target (harness.py:125-144)."""
+    lo, hi = 0.0, 4.0
+    for _ in range(iterations):
+        mid = (lo + hi) / 2
+        if top_share(gen_synthetic(n_chunks, mid, k, n_requests, seed=seed, **gen_kwargs)) < target_share:
+            lo = mid
+        else:
+            hi = mid
+    return (lo + hi) / 2
+
+
+@dataclass
+class RequestMetrics:
+    request_id: int
+    k: int
+    hits: int
+    tokens_total: int
+    tokens_computed: int
+    token_layers: int
+    mean_cfo: float
+    tokens_hit_total: int
+    tokens_hit_recomputed: int
+    deviation: float
+    ttft_ms: float
+    first_token: int | None = None
+
+
+@dataclass
+class GpuReport:
+    policy: str
+    warmup: int
+    requests: list = field(default_factory=list)
+
+    def steady(self) -> list:
+        return self.requests[self.warmup:]
+
+    def aggregate(self) -> dict:
+        rows = self.steady()
+        if not rows:
+            return {"n_requests": 0}
+        tot = sum(r.tokens_total for r in rows)
+        comp = sum(r.tokens_computed for r in rows)
+        wall = sum(r.ttft_ms for r in rows) / 1e3
+        ht = sum(r.tokens_hit_total for r in rows)
+        return {
+            "n_requests": len(rows),
+            "tokens_total": tot,
+            "tokens_computed": comp,
+            "recompute_fraction": comp / tot if tot else 0.0,
+            "hit_rate": sum(r.hits for r in rows) / max(1, sum(r.k for r in rows)),
+            "hit_recompute_fraction": sum(r.tokens_hit_recomputed for r in rows) / ht if ht else 0.0,
+            "mean_cfo": float(np.mean([r.mean_cfo for r in rows])),
+            "mean_deviation": float(np.mean([r.deviation for r in rows])),
+            "prompt_tokens_per_s": tot / wall if wall else 0.0,
+            "ttft_p50_ms": float(np.median([r.ttft_ms for r in rows])),
+            "ttft_p99_ms": float(np.percentile([r.ttft_ms for r in rows], 99)),
+        }
+
+
+def _deviation(hidden_q, oracle_q) -> float:
+    """harness.py:364-370: mean per-token L2 distance over the question span."""
+    if hidden_q.shape[0] == 0:
+        return 0.0
+    return float(np.linalg.norm(hidden_q - oracle_q, axis=1).mean())
+
+
+def _naive_plan(chunk_tokens, hashes, question, store, alpha) -> InferencePlan:
+    """Latest variant of every cached chunk, nothing recomputed (harness.py:373-396)."""
+    out = []
+    for toks, cid in zip(chunk_tokens, hashes):
+        vs = store.lookup(cid)
+        if vs:
+            v = max(vs, key=lambda x: (x.created_at, x.variant_id))
+            out.append(ChunkPlan(chunk_id=cid, status=HIT, tokens=toks, n_tokens=toks.size, n_slots=v.cache.n_slots,
+                                 variant_id=v.variant_id, cfo=0.0, recompute=np.empty(0, dtype=np.int64),
+                                 cache=v.cache))
+        else:
+            out.append(ChunkPlan(chunk_id=cid, status=MISS, tokens=toks, n_tokens=toks.size, n_slots=toks.size))
+    return InferencePlan(chunks=out, question=question, alpha=alpha)
+
+
+def _execute_planned(model, plan, hashes, store, use_focus, first_token):
+    """harness.py:399-451 on the device engine."""
+    n_layers = model.config.n_layers
+    has_miss = any(cp.status == MISS for cp in plan.chunks)
+    can_terminate = use_focus and len(plan.chunks) >= 3 and any(
+        cp.status == HIT and cp.recompute is not None and cp.recompute.size for cp in plan.chunks)
+    request = plan_to_request(plan)
+    result = prefill(model, request, stats=has_miss or can_terminate, record_attention=False,
+                     first_token=first_token)
+    if can_terminate:
+        focus = predict_focused(question_stream(result), plan.focus_window)
+        unfocused = set(range(len(plan.chunks))) - set(focus.focused)
+        rerun = focus.cutoff_layer < n_layers and any(
+            plan.chunks[i].status == HIT and plan.chunks[i].recompute is not None and plan.chunks[i].recompute.size
+            for i in unfocused)
+        if rerun:
+            plan = apply_early_termination(plan, focus)
+            request = plan_to_request(plan)
+            result = prefill(model, request, stats=has_miss, record_attention=False, first_token=first_token)
+    miss_idx = [i for i, cp in enumerate(plan.chunks) if cp.status == MISS]
+    stats = creation_stats(result, hashes, miss_idx) if miss_idx else {}
+    for i, cp in enumerate(plan.chunks):
+        if cp.status == MISS:
+            prefix, a_bar, b_bar, scores = stats[i]
+            s0, s1 = request.segment_slots[i]
+            cache = extract_chunk_cache(result, s0, s1, source_prefix=prefix.chunk_ids)
+            store.insert(cp.chunk_id, prefix=prefix, a_bar=a_bar, b_bar=b_bar, cci=cci(a_bar, b_bar),
+                         token_scores=scores, cache=cache)
+        else:
+            store.touch(cp.variant_id, cp.cfo)
+    return result, plan, request
+
+
+def _prefix_keys(chunk_tokens):
+    """Running content hashes of every chunk-boundary prefix (harness.py:454-461)."""
+    h = hashlib.blake2b(digest_size=16)
+    keys = []
+    for toks in chunk_tokens:
+        h.update(np.asarray(toks, dtype=np.int64).tobytes())
+        keys.append(h.copy().hexdigest())
+    return keys
+
+
+class PrefixRegistry:
+    """GPU prefix cache for the exact_prefix baseline: prefix key -> the
+    chunk cache computed in exactly that prefix context (LRU-bounded)."""
+
+    def __init__(self, capacity: int = 512):
+        self.capacity = capacity
+        self._m: OrderedDict = OrderedDict()
+
+    def get(self, key):
+        c = self._m.get(key)
+        if c is not None:
+            self._m.move_to_end(key)
+        return c
+
+    def put(self, key, cache):
+        self._m[key] = cache
+        self._m.move_to_end(key)
+        while len(self._m) > self.capacity:
+            self._m.popitem(last=False)
+
+
+def replay_gpu(trace: Trace, model, store=None, alpha: float = 1.0, policy: str = "cachecraft", warmup: int = 20,
+               focus_window: int = 3, use_focus: bool = True, cfo_override: float | None = None,
+               measure_deviation: bool = True, first_token: bool = True, registry: PrefixRegistry | None = None,
+               records=None) -> GpuReport:
+    """Replay (a shard of) a trace under one policy on the GPU.  ``records``
+    restricts the run to this rank's requests (``parallel.shard_requests``)."""
+    import torch
+
+    if policy not in POLICIES:
+        raise ArgumentError(f"unknown policy {policy!r}; expected one of {POLICIES}")
+    L = model.config.n_layers
+    report = GpuReport(policy=policy, warmup=warmup)
+    registry = registry if registry is not None else PrefixRegistry()
+    for rec in (trace.records if records is None else records):
+        chunk_tokens = [np.asarray(trace.corpus[c], dtype=np.int64) for c in rec.chunk_ids]
+        question = np.asarray(rec.question, dtype=np.int64)
+        k = len(chunk_tokens)
+        total = sum(t.size for t in chunk_tokens) + question.size
+        hashes = [chunk_hash(t) for t in chunk_tokens]
+        oracle_q = None
+        if measure_deviation and policy != "full_recompute":
+            full = prefill(model, build_request([Segment(tokens=t) for t in chunk_tokens], question), stats=False,
+                           record_attention=False)
+            oracle_q = full.hidden[slice(*full.question_span)]
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        tok = None
+        if policy == "full_recompute":
+            res = prefill(model, plain_request(*chunk_tokens, question), stats=False, record_attention=False,
+                          first_token=first_token)
+            tok = res.first_token
+            torch.cuda.synchronize()
+            ttft = (time.perf_counter() - t0) * 1e3
+            report.requests.append(RequestMetrics(rec.request_id, k, 0, total, total, total * L, 1.0, 0, 0, 0.0,
+                                                  ttft, tok))
+            continue
+        if policy == "exact_prefix":
+            keys = _prefix_keys(chunk_tokens)
+            hits = 0
+            while hits < k and registry.get(keys[hits]) is not None:
+                hits += 1
+            segs = [Segment(tokens=t, cache=registry.get(keys[i])) if i < hits else Segment(tokens=t)
+                    for i, t in enumerate(chunk_tokens)]
+            req = build_request(segs, question)
+            res = prefill(model, req, stats=False, record_attention=False, first_token=first_token)
+            tok = res.first_token
+            torch.cuda.synchronize()
+            ttft = (time.perf_counter() - t0) * 1e3
+            for i in range(hits, k):
+                registry.put(keys[i], extract_chunk_cache(res, *req.segment_slots[i]))
+            reused = sum(t.size for t in chunk_tokens[:hits])
+            dev = _deviation(res.hidden[slice(*res.question_span)], oracle_q) if oracle_q is not None else 0.0
+            report.requests.append(RequestMetrics(rec.request_id, k, hits, total, total - reused,
+                                                  sum(res.active_per_layer), (k - hits) / k if k else 1.0, reused, 0,
+                                                  dev, ttft, tok))
+            continue
+        if policy == "cachecraft":
+            plan = build_plan(chunk_tokens, question, store, alpha, focus_window, cfo_override=cfo_override)
+        else:
+            plan = _naive_plan(chunk_tokens, hashes, question, store, alpha)
+        res, plan, req = _execute_planned(model, plan, hashes, store,
+                                          use_focus=(policy == "cachecraft" and use_focus), first_token=first_token)
+        tok = res.first_token
+        torch.cuda.synchronize()
+        ttft = (time.perf_counter() - t0) * 1e3
+        cfos = [cp.cfo if cp.status == HIT else 1.0 for cp in plan.chunks]
+        dev = _deviation(res.hidden[slice(*res.question_span)], oracle_q) if oracle_q is not None else 0.0
+        report.requests.append(RequestMetrics(
+            request_id=rec.request_id, k=k, hits=plan.hit_count, tokens_total=total,
+            tokens_computed=plan.tokens_recomputed(), token_layers=sum(res.active_per_layer),
+            mean_cfo=float(np.mean(cfos)) if cfos else 1.0,
+            tokens_hit_total=sum(cp.n_tokens for cp in plan.chunks if cp.status == HIT),
+            tokens_hit_recomputed=sum(int(cp.recompute.size) for cp in plan.chunks
+                                      if cp.status == HIT and cp.recompute is not None),
+            deviation=dev, ttft_ms=ttft, first_token=tok))
+    return report

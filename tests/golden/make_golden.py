@@ -258,7 +258,7 @@ def gen_plan():
                         "census": store.census()})
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and not os.environ.get("GEN_ONLY"):
     gen_rope()
     gen_select()
     gen_scoring()
@@ -268,4 +268,32 @@ if __name__ == "__main__":
     gen_stats()
     gen_config1()
     gen_plan()
+    gen_replay()
     print("golden fixtures written to", HERE)
+
+
+def gen_replay():
+    """harness.py:67-144 trace synthesis + harness.py:464-591 replay at a tiny
+    config (no early termination): per-request decisions to reproduce."""
+    from cachecraft.harness import top_share
+
+    tr = cc.gen_synthetic(12, 1.2, 3, 14, chunk_len_range=(16, 40), seed=3, question_len_range=(4, 8))
+    skew = cc.fit_zipf_skew(60, 5, 40, target_share=0.6, seed=3, iterations=10)
+    out = {"trace": [{"id": r.request_id, "chunks": list(map(int, r.chunk_ids)), "q": [int(t) for t in r.question],
+                      "arrival": r.arrival_s} for r in tr.records],
+           "corpus": {str(k): [int(t) for t in v] for k, v in tr.corpus.items()},
+           "skew": skew, "top_share": top_share(tr)}
+    cfg = cc.ModelConfig(n_layers=2, n_heads=4, d_model=64)
+    for name, policy, focus in (("cachecraft", "cachecraft", False), ("full_cache_naive", "full_cache_naive", False),
+                                 ("cachecraft_focus", "cachecraft", True)):
+        mcfg = cc.ModelConfig(n_layers=6, n_heads=4, d_model=64) if focus else cfg
+        rep = cc.replay(tr, model_cfg=mcfg, store_cfg=cc.StoreConfig(max_chunks=5, variants_per_chunk=3), alpha=1.0,
+                        policy=policy, warmup=0, use_focus=focus, focus_window=2)
+        out[name] = [{"hits": m.hits, "tokens_computed": m.tokens_computed, "token_layers": m.token_layers,
+                        "mean_cfo": m.mean_cfo, "deviation": m.deviation, "hit_recomputed": m.tokens_hit_recomputed}
+                       for m in rep.requests]
+    _json("replay.json", out)
+
+
+if __name__ == "__main__" and os.environ.get("GEN_ONLY") == "replay":
+    gen_replay()
