@@ -42,7 +42,11 @@ class DevicePlan:
         self.rows = rows  # slot of each hidden row, (-depth, slot) order
         self.n_rows = int(rows.size)
         rd = depth_eff[rows]
+        self.row_depth = rd.copy()
         self.n_act = [int(np.count_nonzero(rd > l)) for l in range(L)]
+        self.row_pos = positions[rows].astype(np.int32)
+        self.row_tok = token_ids[rows].astype(np.int32)
+        self.active_until_h = np.where(mask, depth_eff, 0).astype(np.int32)
         active_until = np.where(mask, depth_eff, 0).astype(np.int32)
         key_pos = np.where(is_pad, 0, positions).astype(np.int32)
         self.max_pos = int(key_pos.max()) + 1 if n else 1
@@ -210,8 +214,73 @@ class _NoTimer:
 _NOTIMER = _NoTimer()
 
 
+class OnlineFocus:
+    """Single-pass focused-chunk early termination (reference:
+    harness.py:406-428 runs prefill twice).  After each layer the question
+    rows' head-mean mass per chunk (K8a) feeds Algorithm 1 (planner.
+    FocusTracker); when it fires with cutoff L* < L, the recompute rows of the
+    unfocused cached chunks stop at layer L* — the same depths the reference's
+    second pass uses, so the layers it recomputes are identical."""
+
+    def __init__(self, request, window: int, n_layers: int):
+        from .planner import FocusTracker
+
+        self.k = len(request.segments)
+        self.tracker = FocusTracker(self.k, window, n_layers)
+        self.n_layers = n_layers
+        self.request = request
+        self.result = None
+        self.cut = False
+        self.q_span = tuple(request.question_span)
+
+    def cut_slots(self, focused) -> np.ndarray:
+        out = []
+        for i, (seg, (s0, _)) in enumerate(zip(self.request.segments, self.request.segment_slots)):
+            if seg.cache is None or i in focused or seg.recompute is None:
+                continue
+            idx = np.flatnonzero(np.asarray(seg.recompute, dtype=bool))
+            if idx.size:
+                out.append(s0 + idx)
+        return np.concatenate(out) if out else np.zeros(0, np.int64)
+
+
+def _apply_cut(model, plan, ws, slots, new_depth):
+    """Deactivate hidden rows of ``slots`` from layer ``new_depth`` on: permute
+    rows so the active ones stay a prefix, refresh the device index arrays and
+    re-gather the stale cached K/V of those slots for the remaining layers."""
+    import torch
+
+    L = model.config.n_layers
+    is_cut = np.isin(plan.rows, slots)
+    plan.row_depth = np.where(is_cut, np.minimum(plan.row_depth, new_depth), plan.row_depth)
+    perm = np.argsort(-plan.row_depth, kind="stable")
+    plan.rows, plan.row_depth = plan.rows[perm], plan.row_depth[perm]
+    plan.row_pos, plan.row_tok = plan.row_pos[perm], plan.row_tok[perm]
+    plan.n_act = [int(np.count_nonzero(plan.row_depth > l)) for l in range(L)]
+    dev = model.device
+    h = ws["hidden"]
+    idx = torch.from_numpy(perm.astype(np.int64)).to(dev)
+    h[: plan.n_rows].copy_(h[: plan.n_rows].index_select(0, idx))
+    plan.d["row_slot"].copy_(torch.from_numpy(plan.rows.astype(np.int32)).to(dev))
+    plan.d["row_pos"].copy_(torch.from_numpy(plan.row_pos).to(dev))
+    plan.active_until_h[slots] = np.minimum(plan.active_until_h[slots], new_depth)
+    plan.d["active_until"].copy_(torch.from_numpy(plan.active_until_h).to(dev))
+    if getattr(plan, "stats_row_spans", None):
+        _attach_stats_rows(model, plan, plan.stats_row_spans)
+    # stale rows of the cut slots for layers >= new_depth (K1 on the affected blocks only)
+    touched = [it for it in plan.items if np.any((slots >= it["dst_slot"]) & (slots < it["dst_slot"] + it["n_rows"]))]
+    if touched and new_depth < L:
+        items = torch.from_numpy(np.array(touched, dtype=_GATHER_DT).view(np.int32).reshape(-1).copy()).to(dev)
+        cfg = model.kcfg
+        pool = model.pool
+        N.call("cc_gather_rope_kv", N.ptr(pool.storage), pool.layer_stride, pool.block_stride, N.ptr(items),
+               len(touched), new_depth, L, N.ptr(plan.d["slot_pos"]), N.ptr(plan.d["active_until"]),
+               N.ptr(model.rope_table(plan.max_pos)), N.ptr(ws["kv_k"]), N.ptr(ws["kv_v"]), N.ptr(ws["k_rot"]),
+               plan.n * cfg.kv_width(), cfg.kv_width(), cfg.head_dim(), model.dtype_code, N.stream_ptr())
+
+
 def execute(model: Model, plan: DevicePlan, ws: dict, *, record=False, record_values=False, stats=False,
-            gemm_impl=0, attn_impl=0, timer=None):
+            gemm_impl=0, attn_impl=0, timer=None, focus: OnlineFocus | None = None):
     """Launch the per-layer pipeline on the current stream.  Returns the
     LazyAttention (if recording), value trace list and stats masses.
     Under tensor parallelism (model.tp) the o_proj and down_proj GEMMs write
@@ -269,6 +338,22 @@ def execute(model: Model, plan: DevicePlan, ws: dict, *, record=False, record_va
         if n_stats:
             N.call("cc_segment_mass", P(q_rot), P(k_rot[l]), P(D["row_slot"]), key_pad, P(lse), P(D["seg_lo"]),
                    P(D["seg_hi"]), n_seg, P(D["stats_rows"]), n_stats, P(mass[l]), n, H, Hkv, dh, dt, s)
+        pending_cut = None
+        if focus is not None and focus.result is None and n_stats:
+            # question rows are the last stats span; their mass onto each chunk span
+            q0, q1 = focus.q_span
+            nq = q1 - q0
+            row = mass[l, n_stats - nq:n_stats, : focus.k].sum(dim=0)
+            if tp is not None:  # K8a saw this rank's heads only
+                row = row / tp.world
+                tp.allreduce_(row)
+            res = focus.tracker.push(row.cpu().numpy())
+            if res is not None:
+                focus.result = res
+                if res.cutoff_layer < L:
+                    slots = focus.cut_slots(set(res.focused))
+                    if slots.size:
+                        pending_cut = (slots, res.cutoff_layer)
         if record:
             lazy.q[l] = q_rot[:n_l].clone()
             lazy.lse[l] = lse[:n_l].clone()
@@ -294,6 +379,11 @@ def execute(model: Model, plan: DevicePlan, ws: dict, *, record=False, record_va
                        gemm_impl, s)
             else:
                 _tp_partial_gemm(model, tp, act, ff, lw["w_down"], hidden, part, n_l, d, ff, dt, gemm_impl, s)
+        if pending_cut is not None:
+            _apply_cut(model, plan, ws, pending_cut[0], pending_cut[1])
+            focus.cut = True
+            if n_stats:
+                n_stats = plan.stats_rows.size
     if tp is not None and mass is not None:
         # K8a divides by the rank's own heads: global head mean = sum over ranks / world
         mass.mul_(1.0 / tp.world)
@@ -334,13 +424,21 @@ def _payloads(model: Model, request):
 
 
 def run_prefill(model: Model, request, record_values: bool = False, record_attention="auto", stats="auto",
-                first_token: bool = False, gemm_impl: int = 0, attn_impl: int = 0) -> PrefillResult:
+                first_token: bool = False, gemm_impl: int = 0, attn_impl: int = 0,
+                focus_window: int | None = None) -> PrefillResult:
     import torch
 
     N.require_cuda()
     cfg = model.kcfg
     payloads = _payloads(model, request)
     fresh = [i for i, seg in enumerate(request.segments) if seg.cache is None]
+    q0, q1 = request.question_span
+    focus = None
+    if focus_window is not None and len(request.segments) >= 3 and q1 > q0 and any(
+            seg.cache is not None and seg.recompute is not None and np.asarray(seg.recompute).any()
+            for seg in request.segments):
+        focus = OnlineFocus(request, focus_window, cfg.n_layers)
+        stats = True
     if stats == "auto":
         stats = bool(fresh)
     stats_segments = None
@@ -361,9 +459,9 @@ def run_prefill(model: Model, request, record_values: bool = False, record_atten
         record_attention = _record_default(model, plan)
     ws = _workspace(model, plan)
     lazy, vtrace, mass = execute(model, plan, ws, record=bool(record_attention), record_values=record_values,
-                                 stats=bool(stats), gemm_impl=gemm_impl, attn_impl=attn_impl)
-    extras = {"plan": plan, "ws": ws, "mass": mass, "stats_spans": stats_rows_spans if stats else None}
-    q0, q1 = request.question_span
+                                 stats=bool(stats), gemm_impl=gemm_impl, attn_impl=attn_impl, focus=focus)
+    extras = {"plan": plan, "ws": ws, "mass": mass, "stats_spans": stats_rows_spans if stats else None,
+              "focus": None if focus is None else focus.result, "focus_cut": bool(focus is not None and focus.cut)}
     if first_token and q1 > q0:
         r = int(np.flatnonzero(plan.rows == q1 - 1)[0])
         if plan.n_act[-1] <= r:
@@ -377,6 +475,9 @@ def run_prefill(model: Model, request, record_values: bool = False, record_atten
     if lazy is None:
         attn._lazy = LazyAttention(model, plan, ws["k_rot"])
     depth_eff = np.where(request.recompute_depth == FULL_DEPTH, L, request.recompute_depth)
+    if focus is not None and focus.cut:
+        depth_eff = depth_eff.copy()
+        depth_eff[plan.rows] = plan.row_depth
 
     def hidden_fn():
         out = torch.zeros((plan.n, cfg.d_model), dtype=torch.float64, device=model.device)

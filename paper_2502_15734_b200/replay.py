@@ -177,25 +177,33 @@ def _naive_plan(chunk_tokens, hashes, question, store, alpha) -> InferencePlan:
     return InferencePlan(chunks=out, question=question, alpha=alpha)
 
 
-def _execute_planned(model, plan, hashes, store, use_focus, first_token):
-    """harness.py:399-451 on the device engine."""
+def _execute_planned(model, plan, hashes, store, use_focus, first_token, two_pass=False):
+    """harness.py:399-451 on the device engine.  Early termination runs online
+    in the single prefill (engine.OnlineFocus) unless ``two_pass`` asks for the
+    reference's run-predict-rerun sequence."""
     n_layers = model.config.n_layers
     has_miss = any(cp.status == MISS for cp in plan.chunks)
     can_terminate = use_focus and len(plan.chunks) >= 3 and any(
         cp.status == HIT and cp.recompute is not None and cp.recompute.size for cp in plan.chunks)
     request = plan_to_request(plan)
-    result = prefill(model, request, stats=has_miss or can_terminate, record_attention=False,
-                     first_token=first_token)
-    if can_terminate:
-        focus = predict_focused(question_stream(result), plan.focus_window)
-        unfocused = set(range(len(plan.chunks))) - set(focus.focused)
-        rerun = focus.cutoff_layer < n_layers and any(
-            plan.chunks[i].status == HIT and plan.chunks[i].recompute is not None and plan.chunks[i].recompute.size
-            for i in unfocused)
-        if rerun:
-            plan = apply_early_termination(plan, focus)
-            request = plan_to_request(plan)
-            result = prefill(model, request, stats=has_miss, record_attention=False, first_token=first_token)
+    if can_terminate and not two_pass:
+        result = prefill(model, request, stats=True, record_attention=False, first_token=first_token,
+                         focus_window=plan.focus_window)
+        if result.extras.get("focus_cut"):
+            plan = apply_early_termination(plan, result.extras["focus"])
+    else:
+        result = prefill(model, request, stats=has_miss or can_terminate, record_attention=False,
+                         first_token=first_token)
+        if can_terminate:
+            focus = predict_focused(question_stream(result), plan.focus_window)
+            unfocused = set(range(len(plan.chunks))) - set(focus.focused)
+            rerun = focus.cutoff_layer < n_layers and any(
+                plan.chunks[i].status == HIT and plan.chunks[i].recompute is not None
+                and plan.chunks[i].recompute.size for i in unfocused)
+            if rerun:
+                plan = apply_early_termination(plan, focus)
+                request = plan_to_request(plan)
+                result = prefill(model, request, stats=has_miss, record_attention=False, first_token=first_token)
     miss_idx = [i for i, cp in enumerate(plan.chunks) if cp.status == MISS]
     stats = creation_stats(result, hashes, miss_idx) if miss_idx else {}
     for i, cp in enumerate(plan.chunks):
@@ -244,7 +252,7 @@ class PrefixRegistry:
 def replay_gpu(trace: Trace, model, store=None, alpha: float = 1.0, policy: str = "cachecraft", warmup: int = 20,
                focus_window: int = 3, use_focus: bool = True, cfo_override: float | None = None,
                measure_deviation: bool = True, first_token: bool = True, registry: PrefixRegistry | None = None,
-               records=None) -> GpuReport:
+               records=None, two_pass: bool = False) -> GpuReport:
     """Replay (a shard of) a trace under one policy on the GPU.  ``records``
     restricts the run to this rank's requests (``parallel.shard_requests``)."""
     import torch
@@ -302,7 +310,8 @@ def replay_gpu(trace: Trace, model, store=None, alpha: float = 1.0, policy: str 
         else:
             plan = _naive_plan(chunk_tokens, hashes, question, store, alpha)
         res, plan, req = _execute_planned(model, plan, hashes, store,
-                                          use_focus=(policy == "cachecraft" and use_focus), first_token=first_token)
+                                          use_focus=(policy == "cachecraft" and use_focus), first_token=first_token,
+                                          two_pass=two_pass)
         tok = res.first_token
         torch.cuda.synchronize()
         ttft = (time.perf_counter() - t0) * 1e3

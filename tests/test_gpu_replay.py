@@ -11,12 +11,13 @@ pytestmark = pytest.mark.gpu
 from ccb_helpers import load_json  # noqa: E402
 
 
-@pytest.mark.parametrize("name,policy,focus,layers", [
-    ("cachecraft", "cachecraft", False, 2),
-    ("full_cache_naive", "full_cache_naive", False, 2),
-    ("cachecraft_focus", "cachecraft", True, 6),
+@pytest.mark.parametrize("name,policy,focus,layers,two_pass", [
+    ("cachecraft", "cachecraft", False, 2, False),
+    ("full_cache_naive", "full_cache_naive", False, 2, False),
+    ("cachecraft_focus", "cachecraft", True, 6, True),   # the reference's two-pass early termination
+    ("cachecraft_focus", "cachecraft", True, 6, False),  # single-pass online early termination (f1)
 ])
-def test_replay_decisions_match_reference(name, policy, focus, layers):
+def test_replay_decisions_match_reference(name, policy, focus, layers, two_pass):
     if not torch.cuda.is_available():
         pytest.skip("no GPU")
     import paper_2502_15734_b200 as cc
@@ -26,7 +27,8 @@ def test_replay_decisions_match_reference(name, policy, focus, layers):
     tr = replay.gen_synthetic(12, 1.2, 3, 14, chunk_len_range=(16, 40), seed=3, question_len_range=(4, 8))
     model = cc.build_model(cc.ModelConfig(n_layers=layers, n_heads=4, d_model=64))
     store = cc.VariantStore(cc.StoreConfig(max_chunks=5, variants_per_chunk=3))
-    rep = replay.replay_gpu(tr, model, store, alpha=1.0, policy=policy, warmup=0, use_focus=focus, focus_window=2)
+    rep = replay.replay_gpu(tr, model, store, alpha=1.0, policy=policy, warmup=0, use_focus=focus, focus_window=2,
+                            two_pass=two_pass)
     want = g[name]
     got = [(m.hits, m.tokens_computed, m.token_layers, m.tokens_hit_recomputed) for m in rep.requests]
     assert got == [(w["hits"], w["tokens_computed"], w["token_layers"], w["hit_recomputed"]) for w in want]
