@@ -44,7 +44,7 @@ struct StSmem {
   static constexpr int Q_OFF = 0;
   static constexpr int K_OFF = Q_BYTES;
   static constexpr int ACC_OFF = K_OFF + ST_STAGES * K_BYTES;            // float [128][ST_MAXSEG]
-  static constexpr int SEG_OFF = ACC_OFF + 128 * (ST_MAXSEG + 1) * 4;     // int [2][ST_BN]
+  static constexpr int SEG_OFF = ACC_OFF + 128 * (ST_MAXSEG + 1) * 4;     // int seg_lo[128], seg_hi[128]
   static constexpr int BAR_OFF = SEG_OFF + 2 * ST_BN * 4;
   static constexpr size_t TOTAL = 1024 + BAR_OFF + 256;
 };
@@ -71,6 +71,7 @@ __global__ void __launch_bounds__(192, 1)
   uint64_t* s_empty = s_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_empty + 2);
   __shared__ int s_kmax;
+  __shared__ uint32_t padw[8];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = blockIdx.x;
@@ -160,23 +161,31 @@ __global__ void __launch_bounds__(192, 1)
     }
     float* my = acc + m * (ST_MAXSEG + 1);  // padded stride: no bank conflicts
     for (int sg = 0; sg < W; ++sg) my[sg] = 0.f;
+    // segment bounds in shared memory (segments are sorted, disjoint slot ranges)
+    int* s_lo = segmap;
+    int* s_hi = segmap + ST_MAXSEG;
+    for (int sg = et; sg < n_seg; sg += 128) {
+      s_lo[sg] = seg_lo[sg];
+      s_hi[sg] = seg_hi[sg];
+    }
+    asm volatile("bar.sync 1, 128;" ::: "memory");
     float diag = 0.f;
     for (int i = 0; i < n_tiles; ++i) {
       const int b = i & 1;
       const int j0 = i * ST_BN;
-      // segment id of each key of the tile (-1 outside every segment)
-      {
-        const int j = j0 + et;
-        int sid = -1;
-        for (int sg = 0; sg < n_seg; ++sg)
-          if (j >= seg_lo[sg] && j < seg_hi[sg]) { sid = sg; break; }
-        if (j >= n_keys || (key_pad != nullptr && key_pad[j])) sid = -1;
-        segmap[b * ST_BN + et] = sid;
+      uint32_t pw[4] = {0u, 0u, 0u, 0u};
+      if (key_pad != nullptr) {
+        // 128-bit pad mask of the tile, built by the 128 threads (double-buffered)
+        const int jm = j0 + m;  // word q4 of the mask covers keys [32*q4, 32*q4+32)
+        const unsigned word = __ballot_sync(0xffffffffu, jm >= n_keys || key_pad[jm] != 0);
+        if (lane == 0) padw[(b << 2) + q4] = word;
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+#pragma unroll
+        for (int w = 0; w < 4; ++w) pw[w] = padw[(b << 2) + w];
       }
-      asm volatile("bar.sync 1, 128;" ::: "memory");
       mbar_wait(&s_full[b], (i >> 1) & 1);
       tc_fence_after();
-      float s[ST_BN];
+      float p[ST_BN];
       {
         uint32_t ra[32], rb[32], rc[32], rd[32];
         const uint32_t ta = tmem + b * ST_BN + ((uint32_t)(q4 * 32) << 16);
@@ -187,30 +196,34 @@ __global__ void __launch_bounds__(192, 1)
         tmem_ld_wait();
 #pragma unroll
         for (int e = 0; e < 32; ++e) {
-          s[e] = __uint_as_float(ra[e]);
-          s[32 + e] = __uint_as_float(rb[e]);
-          s[64 + e] = __uint_as_float(rc[e]);
-          s[96 + e] = __uint_as_float(rd[e]);
+          p[e] = __uint_as_float(ra[e]);
+          p[32 + e] = __uint_as_float(rb[e]);
+          p[64 + e] = __uint_as_float(rc[e]);
+          p[96 + e] = __uint_as_float(rd[e]);
         }
       }
       tc_fence_before();
       mbar_arrive(&s_empty[b]);
       const int lim_rel = lim - j0;
-      int cur = segmap[b * ST_BN];
-      float run = 0.f;
+      // all probabilities first (independent -> full ILP); masked keys give 0
 #pragma unroll
       for (int c = 0; c < ST_BN; ++c) {
-        const int sid = segmap[b * ST_BN + c];  // warp-uniform (same column for every lane)
-        if (sid != cur) {
-          if (cur >= 0) my[cur] += run;
-          run = 0.f;
-          cur = sid;
-        }
-        const float p = (c <= lim_rel && sid >= 0) ? ex2f(fmaf(s[c], scale_log2, -base_l2)) : 0.f;
-        run += p;
-        if (c == lim_rel) diag += p;
+        const bool vis = (c <= lim_rel) && !((pw[c >> 5] >> (c & 31)) & 1u);
+        p[c] = vis ? ex2f(fmaf(p[c], scale_log2, -base_l2)) : 0.f;
       }
-      if (cur >= 0) my[cur] += run;
+      if (lim_rel >= 0 && lim_rel < ST_BN) {
+#pragma unroll
+        for (int c = 0; c < ST_BN; ++c) diag += (c == lim_rel) ? p[c] : 0.f;
+      }
+      // each segment overlapping the tile: predicated 8-way-ILP sum over its columns
+      for (int sg = 0; sg < n_seg; ++sg) {
+        const int lo = s_lo[sg] - j0, hi = s_hi[sg] - j0;  // warp-uniform
+        if (hi <= 0 || lo >= ST_BN) continue;
+        float a8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int c = 0; c < ST_BN; ++c) a8[c & 7] += (c >= lo && c < hi) ? p[c] : 0.f;
+        my[sg] += ((a8[0] + a8[1]) + (a8[2] + a8[3])) + ((a8[4] + a8[5]) + (a8[6] + a8[7]));
+      }
     }
     my[n_seg] = diag;
     asm volatile("bar.sync 1, 128;" ::: "memory");

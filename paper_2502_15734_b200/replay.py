@@ -261,6 +261,12 @@ def replay_gpu(trace: Trace, model, store=None, alpha: float = 1.0, policy: str 
         raise ArgumentError(f"unknown policy {policy!r}; expected one of {POLICIES}")
     L = model.config.n_layers
     report = GpuReport(policy=policy, warmup=warmup)
+    if store is not None:
+        # size the HBM pool for the store's N*M variants up front (growth copies the pool)
+        longest = max(len(t) for t in trace.corpus.values())
+        need = (store.config.capacity + 64) * -(-longest // 16)
+        if model.pool.n_blocks < need:
+            model.pool.reserve(need)
     registry = registry if registry is not None else PrefixRegistry()
     for rec in (trace.records if records is None else records):
         chunk_tokens = [np.asarray(trace.corpus[c], dtype=np.int64) for c in rec.chunk_ids]
