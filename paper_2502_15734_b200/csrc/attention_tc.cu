@@ -33,7 +33,7 @@ using namespace sm100;
 
 constexpr int AT_BN = 128;      // keys per tile
 constexpr int AT_STAGES = 2;    // K/V ring depth
-constexpr int AT_THREADS = 192;
+constexpr int AT_THREADS = 320;  // TMA warp, MMA warp, 2 x 4 softmax warps
 
 // MN-major operand (B = V: N = head dim contiguous, K = keys), 128B swizzle:
 // 64-element atoms along N at `lbo` bytes, 8-key groups at 1024 B.
@@ -63,6 +63,23 @@ __device__ __forceinline__ float ex2_fast(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+// 2^x on the FMA/ALU pipes (x <= 0): round-to-nearest split x = n + f,
+// f in [-1/2, 1/2], cubic Taylor for 2^f (rel. error < 5e-4, below the bf16
+// rounding of P), n added to the exponent; x < -125 (masked) gives 0
+__device__ __forceinline__ float ex2_poly(float x) {
+  const float xc = fmaxf(x, -125.f);
+  const float t = xc + 12582912.f;  // 1.5 * 2^23: rounds xc to an integer in the low mantissa bits
+  const float n = t - 12582912.f;
+  const float f = xc - n;
+  float p = fmaf(f, fmaf(f, fmaf(f, 0.05550410866f, 0.2402265070f), 0.6931471806f), 1.f);
+  const int e = __float_as_int(t) << 23;  // n in the exponent field (two's complement wraps correctly)
+  p = __int_as_float(__float_as_int(p) + e);
+  return x < -125.f ? 0.f : p;
+}
+__device__ __forceinline__ void st_shared_v4(uint32_t addr, const uint32_t (&v)[4]) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3])
+               : "memory");
+}
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
@@ -71,13 +88,16 @@ struct AtSmem {
   static constexpr int ATOMS = DH / 64;              // 64-element (128 B) column atoms
   static constexpr int Q_BYTES = 128 * DH * 2;       // 128 M-rows
   static constexpr int KV_BYTES = AT_BN * DH * 2;    // one K (or V) tile
-  static constexpr int P_BYTES = 128 * AT_BN * 2;    // P tile, 2 atoms of 64 keys
+  static constexpr int P_BYTES = 128 * AT_BN * 2;    // one P tile, 2 atoms of 64 keys (x2 buffers)
   static constexpr int Q_OFF = 0;
   static constexpr int K_OFF = Q_OFF + Q_BYTES;
   static constexpr int V_OFF = K_OFF + AT_STAGES * KV_BYTES;
   static constexpr int P_OFF = V_OFF + AT_STAGES * KV_BYTES;
-  static constexpr int BAR_OFF = P_OFF + P_BYTES;
-  static constexpr size_t TOTAL = 1024 + BAR_OFF + 256;
+  static constexpr int BAR_OFF = P_OFF + 2 * P_BYTES;
+  static constexpr int X_OFF = BAR_OFF + 256;        // [2 parities][2 halves][128 rows] f32 exchange
+  // no alignment slack: the kernel holds no static shared memory, so the
+  // dynamic window starts 1 KiB aligned (checked at run time)
+  static constexpr size_t TOTAL = X_OFF + 4 * 128 * 4;
 };
 
 template <int DH>
@@ -88,7 +108,8 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
                    int n_q, int n_keys, int Hq, int G, float scale_log2) {
   using SM = AtSmem<DH>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* base = smem_raw;
+  if (smem_u32(smem_raw) & 1023) __trap();  // 128B-swizzled TMA / UMMA tiles need 1 KiB alignment
   uint8_t* sQ = base + SM::Q_OFF;
   uint8_t* sK = base + SM::K_OFF;
   uint8_t* sV = base + SM::V_OFF;
@@ -97,14 +118,16 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
   uint64_t* q_full = bars + 0;
   uint64_t* k_full = bars + 1;                 // [AT_STAGES]
   uint64_t* v_full = k_full + AT_STAGES;       // [AT_STAGES]
-  uint64_t* kv_empty = v_full + AT_STAGES;     // [AT_STAGES]
-  uint64_t* s_full = kv_empty + AT_STAGES;     // [2]
+  uint64_t* k_empty = v_full + AT_STAGES;      // [AT_STAGES]
+  uint64_t* v_empty = k_empty + AT_STAGES;     // [AT_STAGES]
+  uint64_t* s_full = v_empty + AT_STAGES;      // [2]
   uint64_t* s_empty = s_full + 2;              // [2]
-  uint64_t* p_full = s_empty + 2;
-  uint64_t* p_empty = p_full + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(p_empty + 1);
-  __shared__ int s_kmax;
-  __shared__ uint32_t padw[8];
+  uint64_t* p_full = s_empty + 2;              // [2]
+  uint64_t* p_empty = p_full + 2;              // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(p_empty + 2);
+  int& s_kmax = *reinterpret_cast<int*>(tmem_slot + 1);
+  uint32_t* padw = tmem_slot + 2;                                  // [2 parities][4 words]
+  float* xmax = reinterpret_cast<float*>(base + SM::X_OFF);       // row maxima / sums of the pair
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // grid = (kv groups, row tiles), row tiles walked last-first: later rows see
@@ -122,14 +145,17 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
     for (int s = 0; s < AT_STAGES; ++s) {
       mbar_init(&k_full[s], 1);
       mbar_init(&v_full[s], 1);
-      mbar_init(&kv_empty[s], 1);
+      mbar_init(&k_empty[s], 1);
+      mbar_init(&v_empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&s_full[b], 1);
-      mbar_init(&s_empty[b], 128);
+      mbar_init(&s_empty[b], 256);
     }
-    mbar_init(p_full, 128);
-    mbar_init(p_empty, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&p_full[b], 256);
+      mbar_init(&p_empty[b], 1);
+    }
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<512>(tmem_slot);
@@ -152,14 +178,22 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
       mbar_expect_tx(q_full, SM::Q_BYTES);
 #pragma unroll
       for (int a = 0; a < SM::ATOMS; ++a) tma_load_3d(sQ + a * 128 * 128, &tmQ, q_full, a * 64, g * G, row0);
-      for (int i = 0; i < n_tiles; ++i) {
+      // K runs one tile ahead of V: K_{i+1}'s slot frees when S_{i-1} is done
+      // (early), V_i's when PV_{i-2} is done, so neither S nor PV waits on a
+      // load issued after the previous PV
+      auto load_k = [&](int i) {
         const int st = i % AT_STAGES;
-        const uint32_t ph = (i / AT_STAGES) & 1;
-        mbar_wait(&kv_empty[st], ph ^ 1);
+        mbar_wait(&k_empty[st], ((i / AT_STAGES) & 1) ^ 1);
         mbar_expect_tx(&k_full[st], SM::KV_BYTES);
 #pragma unroll
         for (int a = 0; a < SM::ATOMS; ++a)
           tma_load_2d(sK + st * SM::KV_BYTES + a * AT_BN * 128, &tmK, &k_full[st], g * DH + a * 64, i * AT_BN);
+      };
+      load_k(0);
+      for (int i = 0; i < n_tiles; ++i) {
+        if (i + 1 < n_tiles) load_k(i + 1);
+        const int st = i % AT_STAGES;
+        mbar_wait(&v_empty[st], ((i / AT_STAGES) & 1) ^ 1);
         mbar_expect_tx(&v_full[st], SM::KV_BYTES);
 #pragma unroll
         for (int a = 0; a < SM::ATOMS; ++a)
@@ -184,88 +218,94 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
           mma_bf16(t_s0 + b * AT_BN, ad, bd, id_s, kk > 0);
         }
         mma_commit(&s_full[b]);
+        mma_commit(&k_empty[st]);
       };
       issue_s(0);
       for (int i = 0; i < n_tiles; ++i) {
         if (i + 1 < n_tiles) issue_s(i + 1);
-        const int st = i % AT_STAGES;
-        mbar_wait(p_full, i & 1);
+        const int st = i % AT_STAGES, pb = i & 1;
+        mbar_wait(&p_full[pb], (i >> 1) & 1);
         mbar_wait(&v_full[st], (i / AT_STAGES) & 1);
         tc_fence_after();
+        const uint8_t* sPb = sP + pb * SM::P_BYTES;
 #pragma unroll
         for (int kk = 0; kk < AT_BN / 16; ++kk) {
-          uint64_t ad = desc_sw128(sP + (kk >> 2) * 128 * 128) + 2 * (kk & 3);
+          uint64_t ad = desc_sw128(sPb + (kk >> 2) * 128 * 128) + 2 * (kk & 3);
           uint64_t bd = desc_sw128_mn(sV + st * SM::KV_BYTES + kk * 16 * 128, AT_BN * 128);
           mma_bf16(t_o, ad, bd, id_o, (i > 0 || kk > 0) ? 1u : 0u);
         }
-        mma_commit(p_empty);
-        mma_commit(&kv_empty[st]);
+        mma_commit(&p_empty[pb]);
+        mma_commit(&v_empty[st]);
       }
     }
   } else {
-    // ---- softmax / correction / epilogue: one thread per M-row -------------
-    const int q4 = warp & 3;
+    // ---- softmax / correction / epilogue --------------------------------------
+    // Two softmax warpgroups (warps 2-5, 6-9): thread = (M-row m, key half h);
+    // half h owns S columns [64h, 64h+64), P atom h and O columns
+    // [DH/2 h, DH/2 (h+1)).  Per tile the pair exchanges its row max through
+    // smem (one named barrier per TMEM lane quarter); the running sums stay
+    // per half and are added once at the end.
+    const int q4 = warp & 3;               // TMEM lane quarter
+    const int h = (warp - 2) >> 2;         // key / output-column half
     const int m = q4 * 32 + lane;
     const int row = row0 + m / G;
     const int head = g * G + m % G;
     const int lim = row < n_q ? q_slot[row] : -1;
     const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
     float m_run = -INFINITY, l_run = 0.f;
-    uint8_t* prow = sP + m * 128;  // row m inside each 64-key atom (+ atom * 16 KiB)
+    const uint32_t patom_s = smem_u32(sP + m * 128) + h * 128 * 128;  // row m of P atom h
     constexpr float kRescaleLog2 = 8.f;  // lazy rescale: keep the stale max while p <= 2^8
+    auto pair_bar = [&]() { asm volatile("bar.sync %0, 64;" ::"r"(2 + q4) : "memory"); };
     for (int i = 0; i < n_tiles; ++i) {
       const int b = i & 1;
       mbar_wait(&s_full[b], (i >> 1) & 1);
       tc_fence_after();
-      float s[AT_BN];
+      float s[64];
       {
-        uint32_t r0[32], r1[32], r2[32], r3[32];
-        const uint32_t ta = t_s0 + b * AT_BN + lane_off;
+        uint32_t r0[32], r1[32];
+        const uint32_t ta = t_s0 + b * AT_BN + h * 64 + lane_off;
         tmem_ld32(ta, r0);
         tmem_ld32(ta + 32, r1);
-        tmem_ld32(ta + 64, r2);
-        tmem_ld32(ta + 96, r3);
         tmem_ld_wait();
 #pragma unroll
         for (int e = 0; e < 32; ++e) {
           s[e] = __uint_as_float(r0[e]);
           s[32 + e] = __uint_as_float(r1[e]);
-          s[64 + e] = __uint_as_float(r2[e]);
-          s[96 + e] = __uint_as_float(r3[e]);
         }
       }
       tc_fence_before();
       mbar_arrive(&s_empty[b]);
       const int j0 = i * AT_BN;
-      // keys j0 + c visible iff c <= lim_rel (causal + bounds) and not a pad
-      const int lim_rel = min(lim, n_keys - 1) - j0;
+      // keys j0 + 64h + c visible iff c <= lim_rel (causal + bounds) and not a pad
+      const int lim_rel = min(lim, n_keys - 1) - j0 - 64 * h;
       if (key_pad != nullptr) {
-        // 128-bit pad mask of this tile, built by the 128 softmax threads
-        const int jm = j0 + m;
-        const unsigned word = __ballot_sync(0xffffffffu, jm >= n_keys || key_pad[jm] != 0);
-        if (lane == 0) padw[(i & 1) * 4 + q4] = word;
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        uint32_t pw[4];
+        // 128-bit pad mask of this tile, built by the first warpgroup
+        if (h == 0) {
+          const int jm = j0 + m;
+          const unsigned word = __ballot_sync(0xffffffffu, jm >= n_keys || key_pad[jm] != 0);
+          if (lane == 0) padw[(i & 1) * 4 + q4] = word;
+        }
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+        const uint32_t pw0 = padw[(i & 1) * 4 + 2 * h], pw1 = padw[(i & 1) * 4 + 2 * h + 1];
 #pragma unroll
-        for (int w = 0; w < 4; ++w) pw[w] = padw[(i & 1) * 4 + w];
+        for (int c = 0; c < 64; ++c)
+          s[c] = (c <= lim_rel && !((((c < 32) ? pw0 : pw1) >> (c & 31)) & 1u)) ? s[c] : -INFINITY;
+      } else if (lim_rel < 63) {
 #pragma unroll
-        for (int c = 0; c < AT_BN; ++c)
-          s[c] = (c <= lim_rel && !((pw[c >> 5] >> (c & 31)) & 1u)) ? s[c] : -INFINITY;
-      } else if (lim_rel < AT_BN - 1) {
-#pragma unroll
-        for (int c = 0; c < AT_BN; ++c) s[c] = (c <= lim_rel) ? s[c] : -INFINITY;
+        for (int c = 0; c < 64; ++c) s[c] = (c <= lim_rel) ? s[c] : -INFINITY;
       }
       float mx[8];
 #pragma unroll
       for (int e = 0; e < 8; ++e) mx[e] = s[e];
 #pragma unroll
-      for (int c = 8; c < AT_BN; ++c) mx[c & 7] = fmaxf(mx[c & 7], s[c]);
-      const float tmax = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])), fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
+      for (int c = 8; c < 64; ++c) mx[c & 7] = fmaxf(mx[c & 7], s[c]);
+      float tmax = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])), fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
+      xmax[((i & 1) * 2 + h) * 128 + m] = tmax;
+      pair_bar();
+      tmax = fmaxf(tmax, xmax[((i & 1) * 2 + (h ^ 1)) * 128 + m]);
       bool grow = false;
       float alpha = 1.f;
       if (i > 0) {
-        mbar_wait(p_empty, (i - 1) & 1);  // PV_{i-1} done: O current, P buffer free
-        tc_fence_after();
         grow = (m_run != -INFINITY) && ((tmax - m_run) * scale_log2 > kRescaleLog2);
         if (grow) {
           alpha = ex2_fast((m_run - tmax) * scale_log2);
@@ -273,75 +313,88 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
           m_run = tmax;
         }
       }
+      const int pb = i & 1;
+      if (i >= 2) {
+        mbar_wait(&p_empty[pb], ((i - 2) >> 1) & 1);  // PV_{i-2} done: P buffer pb free
+        tc_fence_after();
+      }
       if (m_run == -INFINITY) m_run = tmax;  // first visible keys: nothing accumulated yet
       const float base_l2 = (m_run == -INFINITY) ? 0.f : m_run * scale_log2;
       float ps[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      const uint32_t patom = patom_s + pb * SM::P_BYTES;
 #pragma unroll
-      for (int a = 0; a < 2; ++a) {
-        uint8_t* patom = prow + a * 128 * 128;
+      for (int ch = 0; ch < 8; ++ch) {
+        uint32_t pk[4];
 #pragma unroll
-        for (int ch = 0; ch < 8; ++ch) {
-          uint32_t pk[4];
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const int c = a * 64 + ch * 8 + e * 2;
-            const float p0 = ex2_fast(fmaf(s[c], scale_log2, -base_l2));
-            const float p1 = ex2_fast(fmaf(s[c + 1], scale_log2, -base_l2));
-            ps[(2 * e) & 7] += p0;
-            ps[(2 * e + 1) & 7] += p1;
-            __nv_bfloat162 h = __floats2bfloat162_rn(p0, p1);
-            pk[e] = *reinterpret_cast<uint32_t*>(&h);
-          }
-          *reinterpret_cast<uint4*>(patom + ((ch ^ (m & 7)) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        for (int e = 0; e < 4; ++e) {
+          const int c = ch * 8 + e * 2;
+          // a quarter of the exponentials on the FMA pipe (the MUFU pipe
+          // alone would take as long as the two MMAs of a tile)
+          const bool poly = (ch & 3) == 3;
+          const float x0 = fmaf(s[c], scale_log2, -base_l2), x1 = fmaf(s[c + 1], scale_log2, -base_l2);
+          const float p0 = poly ? ex2_poly(x0) : ex2_fast(x0);
+          const float p1 = poly ? ex2_poly(x1) : ex2_fast(x1);
+          ps[(2 * e) & 7] += p0;
+          ps[(2 * e + 1) & 7] += p1;
+          __nv_bfloat162 hv = __floats2bfloat162_rn(p0, p1);
+          pk[e] = *reinterpret_cast<uint32_t*>(&hv);
         }
+        st_shared_v4(patom + ((ch ^ (m & 7)) << 4), pk);
       }
       l_run += ((ps[0] + ps[1]) + (ps[2] + ps[3])) + ((ps[4] + ps[5]) + (ps[6] + ps[7]));
-      // O *= alpha for rows whose max grew past the lazy threshold.  tcgen05.ld/st
-      // are warp-collective (.sync.aligned): the whole warp joins, alpha = 1
-      // for rows that keep their max.
+      // O *= alpha (this half's columns) for rows whose max grew past the lazy
+      // threshold.  tcgen05.ld/st are warp-collective: the whole warp joins,
+      // alpha = 1 for rows that keep their max.
       if (__any_sync(0xffffffffu, grow)) {
+        mbar_wait(&p_empty[(i - 1) & 1], ((i - 1) >> 1) & 1);  // PV_{i-1} done: O current
+        tc_fence_after();
 #pragma unroll 1
-        for (int c = 0; c < DH / 32; ++c) {
+        for (int c = 0; c < DH / 64; ++c) {
+          const uint32_t to = t_o + h * (DH / 2) + c * 32 + lane_off;
           uint32_t r[32];
-          tmem_ld32(t_o + c * 32 + lane_off, r);
+          tmem_ld32(to, r);
           tmem_ld_wait();
 #pragma unroll
           for (int e = 0; e < 32; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) * alpha);
-          tmem_st32(t_o + c * 32 + lane_off, r);
+          tmem_st32(to, r);
         }
         tmem_st_wait();
       }
       fence_async_smem();
       tc_fence_before();
-      mbar_arrive(p_full);
+      mbar_arrive(&p_full[pb]);
     }
-    // epilogue
+    // epilogue: total row sum = both halves
+    // (slot parity n_tiles & 1 was last read before the previous pair barrier)
+    xmax[((n_tiles & 1) * 2 + h) * 128 + m] = l_run;
+    pair_bar();
+    const float l_tot = l_run + xmax[((n_tiles & 1) * 2 + (h ^ 1)) * 128 + m];
     if (n_tiles > 0) {
-      mbar_wait(p_empty, (n_tiles - 1) & 1);
+      mbar_wait(&p_empty[(n_tiles - 1) & 1], ((n_tiles - 1) >> 1) & 1);
       tc_fence_after();
     }
-    const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
-    __nv_bfloat16* out = ctx + ((int64_t)row * Hq + head) * DH;
+    const float inv = l_tot > 0.f ? 1.f / l_tot : 0.f;
+    __nv_bfloat16* out = ctx + ((int64_t)row * Hq + head) * DH + h * (DH / 2);
 #pragma unroll 1
-    for (int c = 0; c < DH / 32; ++c) {
+    for (int c = 0; c < DH / 64; ++c) {
       uint32_t r[32];
-      tmem_ld32(t_o + c * 32 + lane_off, r);
+      tmem_ld32(t_o + h * (DH / 2) + c * 32 + lane_off, r);
       tmem_ld_wait();
       if (row < n_q && n_tiles > 0) {
         uint4 pk[4];
         uint32_t* pw = reinterpret_cast<uint32_t*>(pk);
 #pragma unroll
         for (int e = 0; e < 16; ++e) {
-          __nv_bfloat162 h = __floats2bfloat162_rn(__uint_as_float(r[2 * e]) * inv, __uint_as_float(r[2 * e + 1]) * inv);
-          pw[e] = *reinterpret_cast<uint32_t*>(&h);
+          __nv_bfloat162 hv = __floats2bfloat162_rn(__uint_as_float(r[2 * e]) * inv, __uint_as_float(r[2 * e + 1]) * inv);
+          pw[e] = *reinterpret_cast<uint32_t*>(&hv);
         }
         uint4* o4 = reinterpret_cast<uint4*>(out + c * 32);
 #pragma unroll
         for (int e = 0; e < 4; ++e) o4[e] = pk[e];
       }
     }
-    if (row < n_q)
-      lse[(int64_t)row * Hq + head] = l_run > 0.f ? (m_run * scale_log2 + log2f(l_run)) * 0.6931471805599453f : -INFINITY;
+    if (row < n_q && h == 0)
+      lse[(int64_t)row * Hq + head] = l_tot > 0.f ? (m_run * scale_log2 + log2f(l_tot)) * 0.6931471805599453f : -INFINITY;
   }
   tc_fence_before();
   __syncthreads();

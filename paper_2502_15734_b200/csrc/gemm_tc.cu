@@ -8,7 +8,9 @@
 //   warps 2-5  epilogue (tcgen05.ld 32 lanes x 32 cols -> registers -> global)
 // Two TMEM accumulators (2 x 256 columns) let tile i's epilogue overlap tile
 // i+1's MMAs.  Tiles are walked M-fastest so the CTAs of one wave share the
-// weight tile through L2.  No split-K: a row's result is independent of M.
+// weight tile through L2.  Wave quantisation (M ~ 800 gives 112-224 tiles on
+// 148 SMs) is removed by a stream-K tail with deterministic fixed-order folds;
+// impl 4 (no split) keeps a row's result independent of M.
 #include <cuda.h>
 
 #include <cstdio>
@@ -34,18 +36,103 @@ struct TcCfg {
   static constexpr int B_BYTES = BN * TC_BK * 2;
   static constexpr int STAGES = (200 * 1024) / (TC_A_BYTES + B_BYTES) > 6 ? 6 : (200 * 1024) / (TC_A_BYTES + B_BYTES);
   static constexpr int TMEM_COLS = 2 * BN <= 256 ? 256 : 512;
-  static constexpr size_t SMEM = 1024 + STAGES * (TC_A_BYTES + B_BYTES) + 256;
+  static constexpr size_t SMEM = 1024 + STAGES * (TC_A_BYTES + B_BYTES) + 256 + 4 * 4096;
 };
 
 using namespace sm100;
 
-// Work unit u in [0, num_tiles * splits): split s = u / num_tiles, tile
-// t = u % num_tiles (split-major, so a unit only ever waits on a smaller unit
-// index: with a persistent grid of co-resident CTAs this cannot deadlock).
-// Split s covers k-blocks [kb_begin(s), kb_begin(s+1)).
-__device__ __forceinline__ int kb_begin(int s, int splits, int num_kb) {
-  const int q = num_kb / splits, r = num_kb % splits;
-  return s * q + (s < r ? s : r);
+// Work schedule (persistent grid of G co-resident CTAs):
+//   tiles [0, t_dp)      data-parallel: CTA c takes tiles c, c + G, ... whole
+//   tiles [t_dp, tiles)  stream-K: their k-blocks, linearised tile-major, are
+//                        cut into G equal contiguous ranges, one per CTA
+// A stream-K tile is covered by CTAs c_lo..c_hi.  Every CTA but c_lo meets
+// the tile at the START of its range (its only non-final fragment): it parks
+// its fp32 partial in its own workspace slot and stamps flags[c].  c_lo meets
+// the tile at the END of its range, waits for the stamps of c_lo+1..c_hi and
+// folds their slots onto its accumulator in that fixed order (deterministic,
+// and a CTA only ever waits on work other CTAs do first: no deadlock).
+struct Unit {
+  int tile, k0, k1, order, nfrag;
+};
+
+struct UnitIter {
+  int nkb, t_dp, G, c, dp_next;
+  long long W, g, g_end;
+  __device__ UnitIter(int nkb_, int t_dp_, long long W_, int G_, int c_)
+      : nkb(nkb_), t_dp(t_dp_), G(G_), c(c_), dp_next(c_), W(W_) {
+    g = W > 0 ? (long long)c * W / G : 0;
+    g_end = W > 0 ? (long long)(c + 1) * W / G : 0;
+  }
+  __device__ int cta_of(long long x) const { return (int)(((x + 1) * G - 1) / W); }
+  __device__ bool next(Unit& u) {
+    if (dp_next < t_dp) {
+      u.tile = dp_next; u.k0 = 0; u.k1 = nkb; u.order = 0; u.nfrag = 1;
+      dp_next += G;
+      return true;
+    }
+    if (g >= g_end) return false;
+    const int t = (int)(g / nkb);
+    const long long tb = (long long)t * nkb, te = tb + nkb;
+    const long long e = te < g_end ? te : g_end;
+    u.tile = t_dp + t;
+    u.k0 = (int)(g - tb);
+    u.k1 = (int)(e - tb);
+    const int c_lo = cta_of(tb), c_hi = cta_of(te - 1);
+    u.order = c_hi - c;
+    u.nfrag = c_hi - c_lo + 1;
+    g = e;
+    return true;
+  }
+};
+
+__device__ __forceinline__ long long globaltimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// 32x32 fp32 transpose through a per-warp 4 KiB smem slab (16-byte units
+// XOR-swizzled by row: conflict-free both ways).  In: r = this lane's row
+// (32 columns).  Out: v[i] = row (lane >> 3) + 4 i, columns (lane & 7) * 4 .. +3.
+__device__ __forceinline__ void transpose32(uint32_t stg, const uint32_t (&r)[32], int lane, float4 (&v)[8]) {
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(stg + (lane * 8 + (j ^ (lane & 7))) * 16),
+                 "r"(r[4 * j]), "r"(r[4 * j + 1]), "r"(r[4 * j + 2]), "r"(r[4 * j + 3])
+                 : "memory");
+  __syncwarp();
+  const int c4 = lane & 7;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int rr = (lane >> 3) + 4 * i;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v[i].x), "=f"(v[i].y), "=f"(v[i].z), "=f"(v[i].w)
+                 : "r"(stg + (rr * 8 + (c4 ^ (rr & 7))) * 16)
+                 : "memory");
+  }
+  __syncwarp();
+}
+
+// fp32 fold of v with a global slab (row stride ld_rows4 = 4 rows, in
+// floats) through L2 (.cg: written by other CTAs).  All loads are issued
+// before any store: __ldcg/__stcg are volatile asm and would otherwise
+// serialise on the L2 round trip.
+__device__ __forceinline__ void fold8(float* p, int64_t ld_rows4, const bool (&ok)[8], float4 (&v)[8], bool add,
+                                      bool store) {
+  if (add) {
+    float4 w[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      if (ok[i]) w[i] = __ldcg(reinterpret_cast<const float4*>(p + i * ld_rows4));
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      if (ok[i]) { v[i].x += w[i].x; v[i].y += w[i].y; v[i].z += w[i].z; v[i].w += w[i].w; }
+  }
+  if (store) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      if (ok[i]) __stcg(reinterpret_cast<float4*>(p + i * ld_rows4), v[i]);
+  }
 }
 
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
@@ -62,9 +149,8 @@ __device__ __forceinline__ void st_release(int* p, int v) {
 template <int EPI, int TC_BN, bool SPLIT>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, void* C,
-                   int64_t ldc, int M, int N, int K, int splits_arg, float* __restrict__ ws, int* __restrict__ flags,
-                   int epoch) {
-  const int splits = SPLIT ? splits_arg : 1;
+                   int64_t ldc, int M, int N, int K, int t_dp, long long W, float* __restrict__ ws,
+                   int* __restrict__ flags, int epoch, long long* __restrict__ trace) {
   constexpr int TC_B_BYTES = TcCfg<TC_BN>::B_BYTES;
   constexpr int TC_STAGES = TcCfg<TC_BN>::STAGES;
   constexpr int TMEM_COLS = TcCfg<TC_BN>::TMEM_COLS;
@@ -77,12 +163,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   uint64_t* tfull = empty + TC_STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  // per-epilogue-warp 4 KiB transpose slabs, after the barriers (1 KiB aligned)
+  float4* stg_base = reinterpret_cast<float4*>(sB + TC_STAGES * TC_B_BYTES + 256);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int num_m = (M + TC_BM - 1) / TC_BM;
   const int num_tiles = num_m * (N / TC_BN);
   const int num_kb = K / TC_BK;
-  const int num_units = num_tiles * splits;
+  if (!SPLIT) { t_dp = num_tiles; W = 0; }
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
@@ -107,11 +195,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
-        const int sp = u / num_tiles, tile = u % num_tiles;
-        const int mt = tile % num_m, nt = tile / num_m;
-        const int k0 = kb_begin(sp, splits, num_kb), k1 = kb_begin(sp + 1, splits, num_kb);
-        for (int kb = k0; kb < k1; ++kb) {
+      UnitIter it(num_kb, t_dp, W, gridDim.x, blockIdx.x);
+      Unit w;
+      while (it.next(w)) {
+        const int mt = w.tile % num_m, nt = w.tile / num_m;
+        for (int kb = w.k0; kb < w.k1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_expect_tx(&full[stage], TC_A_BYTES + TC_B_BYTES);
           tma_load_2d(sA + stage * TC_A_BYTES, &tmA, &full[stage], kb * TC_BK, mt * TC_BM);
@@ -127,9 +215,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
-        const int sp = u / num_tiles;
-        const int k0 = kb_begin(sp, splits, num_kb), k1 = kb_begin(sp + 1, splits, num_kb);
+      UnitIter it(num_kb, t_dp, W, gridDim.x, blockIdx.x);
+      Unit w;
+      while (it.next(w)) {
+        const int k0 = w.k0, k1 = w.k1;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * TC_BN;
@@ -151,121 +240,125 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   } else {
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const int et = threadIdx.x - 64;  // 0..127 within the epilogue warps
+    const uint32_t stg = smem_u32(stg_base + (warp - 2) * 256);
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
-      const int sp = u / num_tiles, tile = u % num_tiles;
+    UnitIter it(num_kb, t_dp, W, gridDim.x, blockIdx.x);
+    Unit w;
+    int ui = 0;
+    while (it.next(w)) {
+      const int tile = w.tile, sp = w.order;
       const int mt = tile % num_m, nt = tile / num_m;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
+      long long* tr = (trace != nullptr && et == 0 && ui < 8) ? trace + ((int64_t)blockIdx.x * 8 + ui) * 8 : nullptr;
+      if (tr) { tr[0] = tile; tr[1] = sp; tr[2] = w.nfrag; tr[3] = w.k1 - w.k0; tr[4] = globaltimer(); }
       const int row = mt * TC_BM + q * 32 + lane;
       const uint32_t t0 = tmem_base + acc * TC_BN + ((uint32_t)(q * 32) << 16);
       const int n0 = nt * TC_BN;
-      // split-K: partial sums are folded in split order (deterministic)
-      constexpr bool split = SPLIT;
-      const bool last = sp == splits - 1;
-      if (SPLIT && sp > 0) {
-        if (et == 0)
-          while (ld_acquire(&flags[tile]) != epoch * 64 + sp) __nanosleep(64);
+      // stream-K: non-final fragments park partials; the final one folds them
+      const bool split = SPLIT && w.nfrag > 1;
+      const bool last = sp == w.nfrag - 1;  // c_lo: applies the epilogue
+      const int c_hi = blockIdx.x + sp;
+      if (split && last) {
+        for (int j = et; j < c_hi - (int)blockIdx.x; j += 128)
+          while (ld_acquire(&flags[blockIdx.x + 1 + j]) != epoch) __nanosleep(32);
         epi_bar();
       }
-      float* wrow = ws + (int64_t)row * N + n0;  // fp32 workspace row (non-residual splits)
+      if (tr) tr[5] = globaltimer();
+      // this CTA's partial slot [128][TC_BN] fp32 (non-final) / slot of CTA j (final)
+      auto slot = [&](int cta, int col) -> float* {
+        return ws + (int64_t)cta * (TC_BM * TC_BN) + (int64_t)(q * 32 + (lane >> 3)) * TC_BN + col + (lane & 7) * 4;
+      };
+      auto fold_in = [&](float4 (&v)[8], int col, const bool (&okr)[8]) {
+        for (int j = blockIdx.x + 1; j <= c_hi; ++j) fold8(slot(j, col), 4 * TC_BN, okr, v, true, false);
+      };
+      // Coalesced epilogue: each 32x32 fp32 chunk (thread = row after
+      // tcgen05.ld) is transposed through a 4 KiB swizzled smem slab so that
+      // a warp instruction covers 4 rows x 128 B; lane -> (row rb + 4 i,
+      // cols c4*4 .. +3), i = 0..7.
+      const int rb = mt * TC_BM + q * 32 + (lane >> 3);
+      const int c4 = lane & 7;
+      bool ok[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) ok[i] = rb + 4 * i < M;
       if constexpr (EPI == CC_EPI_SWIGLU && TC_BN == 256) {
         // tile columns: [gate 64 | up 64 | gate 64 | up 64] -> 128 outputs
 #pragma unroll 1
         for (int g = 0; g < 4; ++g) {
           const int gc = (g >> 1) * 128 + (g & 1) * 32;
-          uint32_t rg[32], ru[32];
-          tmem_ld32(t0 + gc, rg);
-          tmem_ld32(t0 + gc + 64, ru);
-          tmem_ld_wait();
-          if (row < M) {
-            if (split) {
-              float4* wg = reinterpret_cast<float4*>(wrow + gc);
-              float4* wu = reinterpret_cast<float4*>(wrow + gc + 64);
+          float4 vg[8], vu[8];
+          {
+            uint32_t r[32];
+            tmem_ld32(t0 + gc, r);
+            tmem_ld_wait();
+            transpose32(stg, r, lane, vg);
+            tmem_ld32(t0 + gc + 64, r);
+            tmem_ld_wait();
+            transpose32(stg, r, lane, vu);
+          }
+          if (split && !last) {
+            fold8(slot(blockIdx.x, gc), 4 * TC_BN, ok, vg, false, true);
+            fold8(slot(blockIdx.x, gc + 64), 4 * TC_BN, ok, vu, false, true);
+          } else if (split) {
+            fold_in(vg, gc, ok);
+            fold_in(vu, gc + 64, ok);
+          }
+          if (last) {
+            __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(C) + (int64_t)rb * ldc + n0 / 2 + (g >> 1) * 64 +
+                                 (g & 1) * 32 + c4 * 4;
 #pragma unroll
-              for (int i = 0; i < 8; ++i) {
-                float4 a = make_float4(__uint_as_float(rg[4 * i]), __uint_as_float(rg[4 * i + 1]),
-                                       __uint_as_float(rg[4 * i + 2]), __uint_as_float(rg[4 * i + 3]));
-                float4 b = make_float4(__uint_as_float(ru[4 * i]), __uint_as_float(ru[4 * i + 1]),
-                                       __uint_as_float(ru[4 * i + 2]), __uint_as_float(ru[4 * i + 3]));
-                if (sp > 0) {
-                  float4 pa = __ldcg(wg + i), pb = __ldcg(wu + i);
-                  a.x += pa.x; a.y += pa.y; a.z += pa.z; a.w += pa.w;
-                  b.x += pb.x; b.y += pb.y; b.z += pb.z; b.w += pb.w;
-                }
-                if (!last) { __stcg(wg + i, a); __stcg(wu + i, b); }
-                rg[4 * i] = __float_as_uint(a.x); rg[4 * i + 1] = __float_as_uint(a.y);
-                rg[4 * i + 2] = __float_as_uint(a.z); rg[4 * i + 3] = __float_as_uint(a.w);
-                ru[4 * i] = __float_as_uint(b.x); ru[4 * i + 1] = __float_as_uint(b.y);
-                ru[4 * i + 2] = __float_as_uint(b.z); ru[4 * i + 3] = __float_as_uint(b.w);
-              }
-            }
-            if (last) {
-              __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(C) + (int64_t)row * ldc + n0 / 2 + (g >> 1) * 64 + (g & 1) * 32;
-              uint4 pk[4];
-              uint32_t* pw = reinterpret_cast<uint32_t*>(pk);
-#pragma unroll
-              for (int i = 0; i < 16; ++i) {
-                float a0 = __uint_as_float(rg[2 * i]), a1 = __uint_as_float(rg[2 * i + 1]);
-                float u0 = __uint_as_float(ru[2 * i]), u1 = __uint_as_float(ru[2 * i + 1]);
-                __nv_bfloat162 h = __floats2bfloat162_rn(silu(a0) * u0, silu(a1) * u1);
-                pw[i] = *reinterpret_cast<uint32_t*>(&h);
-              }
-              uint4* o4 = reinterpret_cast<uint4*>(out);
-#pragma unroll
-              for (int i = 0; i < 4; ++i) o4[i] = pk[i];
+            for (int i = 0; i < 8; ++i) {
+              if (!ok[i]) continue;
+              __nv_bfloat162 h0 = __floats2bfloat162_rn(silu(vg[i].x) * vu[i].x, silu(vg[i].y) * vu[i].y);
+              __nv_bfloat162 h1 = __floats2bfloat162_rn(silu(vg[i].z) * vu[i].z, silu(vg[i].w) * vu[i].w);
+              *reinterpret_cast<uint2*>(out + (int64_t)4 * i * ldc) =
+                  make_uint2(*reinterpret_cast<uint32_t*>(&h0), *reinterpret_cast<uint32_t*>(&h1));
             }
           }
         }
       } else {
 #pragma unroll 1
         for (int c = 0; c < TC_BN / 32; ++c) {
-          uint32_t r[32];
-          tmem_ld32(t0 + c * 32, r);
-          tmem_ld_wait();
-          if (row < M) {
-            const int64_t o = (int64_t)row * ldc + n0 + c * 32;
-            if constexpr (EPI == CC_EPI_RESID_ADD) {
-              float4* h = reinterpret_cast<float4*>(reinterpret_cast<float*>(C) + o);
+          float4 v[8];
+          {
+            uint32_t r[32];
+            tmem_ld32(t0 + c * 32, r);
+            tmem_ld_wait();
+            transpose32(stg, r, lane, v);
+          }
+          const int col = n0 + c * 32 + c4 * 4;
+          if constexpr (EPI == CC_EPI_RESID_ADD) {
+            float* h = reinterpret_cast<float*>(C) + (int64_t)rb * ldc + col;
+            if (split && !last) {
+              fold8(slot(blockIdx.x, c * 32), 4 * TC_BN, ok, v, false, true);
+            } else {
+              if (split) fold_in(v, c * 32, ok);
+              float4 cv[8];
+#pragma unroll
+              for (int i = 0; i < 8; ++i)
+                if (ok[i]) cv[i] = *reinterpret_cast<const float4*>(h + (int64_t)4 * i * ldc);
+#pragma unroll
+              for (int i = 0; i < 8; ++i)
+                if (ok[i])
+                  *reinterpret_cast<float4*>(h + (int64_t)4 * i * ldc) =
+                      make_float4(cv[i].x + v[i].x, cv[i].y + v[i].y, cv[i].z + v[i].z, cv[i].w + v[i].w);
+            }
+          } else {
+            if (split && !last) fold8(slot(blockIdx.x, c * 32), 4 * TC_BN, ok, v, false, true);
+            else if (split) fold_in(v, c * 32, ok);
+            if (last) {
+              __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(C) + (int64_t)rb * ldc + col;
 #pragma unroll
               for (int i = 0; i < 8; ++i) {
-                float4 v = split ? __ldcg(h + i) : h[i];
-                v.x += __uint_as_float(r[4 * i]);
-                v.y += __uint_as_float(r[4 * i + 1]);
-                v.z += __uint_as_float(r[4 * i + 2]);
-                v.w += __uint_as_float(r[4 * i + 3]);
-                if (split) __stcg(h + i, v); else h[i] = v;
-              }
-            } else {
-              if (split) {
-                float4* w4 = reinterpret_cast<float4*>(wrow + c * 32);
-#pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                  float4 a = make_float4(__uint_as_float(r[4 * i]), __uint_as_float(r[4 * i + 1]),
-                                         __uint_as_float(r[4 * i + 2]), __uint_as_float(r[4 * i + 3]));
-                  if (sp > 0) {
-                    float4 p = __ldcg(w4 + i);
-                    a.x += p.x; a.y += p.y; a.z += p.z; a.w += p.w;
-                  }
-                  if (!last) __stcg(w4 + i, a);
-                  r[4 * i] = __float_as_uint(a.x); r[4 * i + 1] = __float_as_uint(a.y);
-                  r[4 * i + 2] = __float_as_uint(a.z); r[4 * i + 3] = __float_as_uint(a.w);
+                if (!ok[i]) continue;
+                float4 x = v[i];
+                if constexpr (EPI == CC_EPI_GELU) {
+                  x.x = gelu_tanh(x.x); x.y = gelu_tanh(x.y); x.z = gelu_tanh(x.z); x.w = gelu_tanh(x.w);
                 }
-              }
-              if (last) {
-                uint4 pk[4];
-                uint32_t* pw = reinterpret_cast<uint32_t*>(pk);
-#pragma unroll
-                for (int i = 0; i < 16; ++i) {
-                  float a0 = __uint_as_float(r[2 * i]), a1 = __uint_as_float(r[2 * i + 1]);
-                  if constexpr (EPI == CC_EPI_GELU) { a0 = gelu_tanh(a0); a1 = gelu_tanh(a1); }
-                  __nv_bfloat162 h = __floats2bfloat162_rn(a0, a1);
-                  pw[i] = *reinterpret_cast<uint32_t*>(&h);
-                }
-                uint4* o4 = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(C) + o);
-#pragma unroll
-                for (int i = 0; i < 4; ++i) o4[i] = pk[i];
+                __nv_bfloat162 h0 = __floats2bfloat162_rn(x.x, x.y), h1 = __floats2bfloat162_rn(x.z, x.w);
+                *reinterpret_cast<uint2*>(out + (int64_t)4 * i * ldc) =
+                    make_uint2(*reinterpret_cast<uint32_t*>(&h0), *reinterpret_cast<uint32_t*>(&h1));
               }
             }
           }
@@ -273,11 +366,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       }
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
-      if (SPLIT && !last) {
+      if (split && !last) {
         __threadfence();
         epi_bar();
-        if (et == 0) st_release(&flags[tile], epoch * 64 + sp + 1);
+        if (et == 0) st_release(&flags[blockIdx.x], epoch);
       }
+      if (tr) tr[6] = globaltimer();
+      ++ui;
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
   }
@@ -374,9 +469,20 @@ SplitScratch& scratch(cudaStream_t st) {
   return *sc;
 }
 
+long long* g_trace = nullptr;  // debug: per-CTA unit timeline (cc_gemm_set_trace)
+
+// Tiling plan: tile width, how many tiles run data-parallel, the stream-K
+// k-block total and the persistent grid.
+struct Tiling {
+  int bn = 0;
+  int t_dp = 0;
+  long long W = 0;  // stream-K k-blocks (0: pure data-parallel)
+  int grid = 0;
+};
+
 template <int EPI, int BN>
-int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, void* C, int64_t ldc, int M, int N, int K, int splits,
-              cudaStream_t st) {
+int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, void* C, int64_t ldc, int M, int N, int K,
+              const Tiling& tl, cudaStream_t st) {
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(gemm_tc_kernel<EPI, BN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -386,63 +492,102 @@ int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, void* C, int64_t ldc
     attr_set = true;
   }
   const int tiles = ((M + TC_BM - 1) / TC_BM) * (N / BN);
-  const int units = tiles * splits;
-  const int grid = units < num_sms() ? units : num_sms();
   SplitScratch& sc = scratch(st);
-  if (splits > 1) {
-    if (sc.flag_elems < tiles) {
+  if (tl.W > 0) {
+    if (sc.flag_elems < tl.grid) {
       if (sc.flags) cudaFree(sc.flags);
-      sc.flag_elems = tiles < 4096 ? 4096 : tiles;
+      sc.flag_elems = 1024;
       if (cudaMalloc(&sc.flags, sizeof(int) * sc.flag_elems) != cudaSuccess) return fail(CC_E_CUDA, "gemm_tc: flags");
       cudaMemset(sc.flags, 0xff, sizeof(int) * sc.flag_elems);
     }
-    const size_t need = EPI == CC_EPI_RESID_ADD ? 0 : (size_t)((M + TC_BM - 1) / TC_BM) * TC_BM * N;
+    const size_t need = (size_t)tl.grid * TC_BM * BN;  // one partial slot per CTA
     if (sc.ws_elems < need) {
       if (sc.ws) cudaFree(sc.ws);
       sc.ws_elems = need;
       if (cudaMalloc(&sc.ws, sizeof(float) * need) != cudaSuccess) return fail(CC_E_CUDA, "gemm_tc: workspace");
     }
-    sc.epoch = (sc.epoch + 1) & 0x00ffffff;
+    sc.epoch = (sc.epoch + 1) & 0x3fffffff;
+    gemm_tc_kernel<EPI, BN, true><<<tl.grid, TC_THREADS, TcCfg<BN>::SMEM, st>>>(ma, mb, C, ldc, M, N, K, tl.t_dp,
+                                                                               tl.W, sc.ws, sc.flags, sc.epoch, g_trace);
+  } else {
+    gemm_tc_kernel<EPI, BN, false><<<tl.grid, TC_THREADS, TcCfg<BN>::SMEM, st>>>(ma, mb, C, ldc, M, N, K, tiles, 0,
+                                                                                nullptr, nullptr, 0, g_trace);
   }
-  if (splits > 1)
-    gemm_tc_kernel<EPI, BN, true><<<grid, TC_THREADS, TcCfg<BN>::SMEM, st>>>(ma, mb, C, ldc, M, N, K, splits, sc.ws,
-                                                                            sc.flags, sc.epoch);
-  else
-    gemm_tc_kernel<EPI, BN, false><<<grid, TC_THREADS, TcCfg<BN>::SMEM, st>>>(ma, mb, C, ldc, M, N, K, 1, nullptr,
-                                                                             nullptr, 0);
   return check_launch("gemm_tc");
 }
 
-// (BN, split-K) minimising the modelled time: persistent rounds x k-blocks per
-// unit x per-k-block cost of the tile width + a fixed-up epilogue per split
-void pick_tiling(int M, int N, int K, int epi, bool allow_split, int* bn_out, int* splits_out) {
-  const int m_tiles = (M + TC_BM - 1) / TC_BM;
-  const int sms = num_sms();
-  const int num_kb = K / TC_BK;
+// relative time of one k-block of a 128xBN tile (measured, BN = 256 / 192 / 128)
+constexpr double kKbCost[3] = {1.0, 0.75 / 0.97, 0.5 / 0.88};
+// exposed cost of a CTA's final stream-K fold (read the partials, in 128x256 k-blocks)
+constexpr double kFoldCost = 4.0;
+
+Tiling plan_dp(int M, int N, int bn) {
+  Tiling t;
+  const int tiles = ((M + TC_BM - 1) / TC_BM) * (N / bn);
+  t.bn = bn;
+  t.t_dp = tiles;
+  t.grid = tiles < num_sms() ? tiles : num_sms();
+  return t;
+}
+
+// hybrid: whole waves data-parallel, the last [G, 2G) tiles (or all, when
+// fewer) stream-K; >= 4 k-blocks per CTA and <= ~3 fragments per tile (the
+// final fragment folds the others' slots one after another)
+Tiling plan_sk(int M, int N, int K, int bn) {
+  Tiling t;
+  const int sms = num_sms(), nkb = K / TC_BK;
+  const int tiles = ((M + TC_BM - 1) / TC_BM) * (N / bn);
+  const int full = tiles / sms;
+  t.bn = bn;
+  t.t_dp = full >= 2 ? (full - 1) * sms : 0;
+  t.W = (long long)(tiles - t.t_dp) * nkb;
+  long long g = t.W / 4;
+  if (g > 3LL * (tiles - t.t_dp)) g = 3LL * (tiles - t.t_dp);
+  t.grid = (int)(g < sms ? (g > 0 ? g : 1) : sms);
+  if (t.t_dp > 0) t.grid = sms;  // (the stream-K part then has >= sms tiles)
+  return t;
+}
+
+double model_time(const Tiling& t, int M, int N, int K) {
+  const int nkb = K / TC_BK;
+  const int ci = t.bn == 256 ? 0 : (t.bn == 192 ? 1 : 2);
+  const int tiles = ((M + TC_BM - 1) / TC_BM) * (N / t.bn);
+  if (t.W == 0) return (double)((tiles + t.grid - 1) / t.grid) * nkb * kKbCost[ci];
+  const double per = (double)((t.W + t.grid - 1) / t.grid);
+  const bool splits = (t.W / t.grid) % nkb != 0 || t.W / t.grid < nkb;
+  return ((double)(t.t_dp / t.grid) * nkb + per) * kKbCost[ci] + (splits ? kFoldCost * t.bn / 256.0 : 0.0);
+}
+
+// the tiling minimising the modelled time.  Stream-K is considered where it
+// measured faster: small M (fewer than half a wave of tiles: weight
+// streaming) and long K with several waves (M ~ 5k down_proj).  At M ~ 800
+// the data-parallel schedule wins: stream-K's scattered k offsets defeat the
+// L2 sharing of the weight tiles across a wave's M tiles.
+Tiling pick_tiling(int M, int N, int K, int epi, bool allow_split) {
   const int cand[3] = {256, 192, 128};
-  const double kb_cost[3] = {1.0, 0.75 / 0.97, 0.5 / 0.88};  // relative time of one k-block of a 128xBN tile
-  double best = 1e30;
-  *bn_out = 0;
-  *splits_out = 1;
+  const int sms = num_sms(), nkb = K / TC_BK;
+  Tiling best;
+  double best_t = 1e30;
   for (int i = 0; i < 3; ++i) {
     const int bn = cand[i];
     if (N % bn) continue;
     if (epi == CC_EPI_SWIGLU && bn != 256) continue;
-    const int tiles = m_tiles * (N / bn);
-    // split-K only pays when most SMs would idle (small M: weight streaming);
-    // the in-order fix-ups cost more than wave quantisation at larger M
-    const int max_s = (allow_split && 2 * tiles <= sms) ? (num_kb < 16 ? num_kb : 16) : 1;
-    for (int s = 1; s <= max_s; ++s) {
-      if (s > 1 && num_kb / s < 4) break;  // keep >= 4 k-blocks per split unit
-      const int rounds = (tiles * s + sms - 1) / sms;
-      const double t = rounds * ((double)(num_kb + s - 1) / s) * kb_cost[i] + (s > 1 ? 6.0 * s : 0.0);
-      if (t < best - 1e-9) { best = t; *bn_out = bn; *splits_out = s; }
+    Tiling dp = plan_dp(M, N, bn);
+    double t = model_time(dp, M, N, K);
+    if (t < best_t - 1e-9) { best_t = t; best = dp; }
+    const int tiles = dp.t_dp;
+    if (allow_split && (2 * tiles <= sms || (tiles >= 2 * sms && nkb >= 128))) {
+      Tiling sk = plan_sk(M, N, K, bn);
+      double ts = model_time(sk, M, N, K);
+      if (ts < 0.97 * best_t) { best_t = ts; best = sk; }
     }
   }
+  return best;
 }
 
-// CCB_GEMM_FORCE="bn,splits" pins the tiling (experiments / tests)
-bool forced_tiling(int N, int epi, int* bn, int* splits) {
+// CCB_GEMM_FORCE="bn,mode" pins the tiling (experiments / tests): mode 0
+// data-parallel, 1 stream-K hybrid
+bool forced_tiling(int M, int N, int K, int epi, Tiling* out) {
   static int fb = -1, fs = -1;
   static bool init = false;
   if (!init) {
@@ -450,29 +595,29 @@ bool forced_tiling(int N, int epi, int* bn, int* splits) {
     if (const char* e = getenv("CCB_GEMM_FORCE")) sscanf(e, "%d,%d", &fb, &fs);
   }
   if (fb <= 0 || N % fb || (epi == CC_EPI_SWIGLU && fb != 256)) return false;
-  *bn = fb;
-  *splits = fs > 0 ? fs : 1;
+  *out = fs == 1 ? plan_sk(M, N, K, fb) : plan_dp(M, N, fb);
   return true;
 }
 
 template <int EPI>
 int launch_epi(const void* A, int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc, int M, int N, int K,
                bool allow_split, cudaStream_t st) {
-  int bn, splits;
-  if (!forced_tiling(N, EPI, &bn, &splits)) pick_tiling(M, N, K, EPI, allow_split, &bn, &splits);
-  if (splits > K / TC_BK) splits = K / TC_BK;
-  if (bn == 0) return fail(CC_E_UNSUP, "gemm_tc: N must be a multiple of 128 (SwiGLU: 256)");
+  Tiling tl;
+  if (!forced_tiling(M, N, K, EPI, &tl)) tl = pick_tiling(M, N, K, EPI, allow_split);
+  if (tl.bn == 0) return fail(CC_E_UNSUP, "gemm_tc: N must be a multiple of 128 (SwiGLU: 256)");
   CUtensorMap ma, mb;
   int rc = make_map(&ma, A, M, K, lda, TC_BM);
   if (rc) return rc;
-  rc = make_map(&mb, B, N, K, ldb, bn);
+  rc = make_map(&mb, B, N, K, ldb, tl.bn);
   if (rc) return rc;
-  if (bn == 256) return launch_tc<EPI, 256>(ma, mb, C, ldc, M, N, K, splits, st);
-  if (bn == 192) return launch_tc<EPI, 192>(ma, mb, C, ldc, M, N, K, splits, st);
-  return launch_tc<EPI, 128>(ma, mb, C, ldc, M, N, K, splits, st);
+  if (tl.bn == 256) return launch_tc<EPI, 256>(ma, mb, C, ldc, M, N, K, tl, st);
+  if (tl.bn == 192) return launch_tc<EPI, 192>(ma, mb, C, ldc, M, N, K, tl, st);
+  return launch_tc<EPI, 128>(ma, mb, C, ldc, M, N, K, tl, st);
 }
 
 }  // namespace
+
+void gemm_tc_set_trace(void* p) { g_trace = reinterpret_cast<long long*>(p); }
 
 int gemm_tc_bf16(const void* A, int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc, int M, int N, int K,
                  int epi, bool allow_split, cudaStream_t st) {
@@ -490,3 +635,6 @@ int gemm_tc_bf16(const void* A, int64_t lda, const void* B, int64_t ldb, void* C
 }
 
 }  // namespace ccb
+
+// debug hook (not part of the ABI): per-CTA epilogue timeline of the next GEMMs
+extern "C" __attribute__((visibility("default"))) void cc_debug_gemm_trace(void* p) { ccb::gemm_tc_set_trace(p); }

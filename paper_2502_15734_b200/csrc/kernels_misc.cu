@@ -309,23 +309,56 @@ __global__ void __launch_bounds__(256) logits_kernel(const typename Acc<T>::type
   }
   __syncthreads();
   const int warps = blockDim.x >> 5, lane = threadIdx.x & 31;
+  // one warp per vocab row: the row is streamed ONCE (16-byte no-allocate
+  // loads, 4 in flight per lane) and dotted with all m normed rows
   for (int v = blockIdx.x * warps + (threadIdx.x >> 5); v < vocab; v += gridDim.x * warps) {
     const T* u = U + (int64_t)v * d;
-    for (int r = 0; r < m; ++r) {
-      A acc = 0;
-      if constexpr (sizeof(T) == 2) {
-        // 16-byte loads of the bf16 unembedding row
-        for (int i = lane * 8; i < d; i += 256) {
-          uint4 raw = *reinterpret_cast<const uint4*>(u + i);
-          const __nv_bfloat16* hb = reinterpret_cast<const __nv_bfloat16*>(&raw);
+    A acc[8];
 #pragma unroll
-          for (int e = 0; e < 8; ++e) acc += __bfloat162float(hb[e]) * xs[r * d + i + e];
+    for (int r = 0; r < 8; ++r) acc[r] = 0;
+    if constexpr (sizeof(T) == 2) {
+      auto ld = [&](int i) {
+        uint4 raw;
+        asm("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+            : "=r"(raw.x), "=r"(raw.y), "=r"(raw.z), "=r"(raw.w)
+            : "l"(u + i));
+        return raw;
+      };
+      auto dot = [&](const uint4& raw, int i) {
+        const __nv_bfloat16* hb = reinterpret_cast<const __nv_bfloat16*>(&raw);
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+          if (r < m) {
+            const A* x = xs + r * d + i;
+#pragma unroll
+            for (int e = 0; e < 8; ++e) acc[r] += __bfloat162float(hb[e]) * x[e];
+          }
         }
-      } else {
-        for (int i = lane; i < d; i += 32) acc += (A)to_f(u[i]) * xs[r * d + i];
+      };
+      int i = lane * 8;
+      for (; i + 3 * 256 < d; i += 4 * 256) {  // 4 independent 16-byte loads in flight
+        uint4 raw[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) raw[j] = ld(i + j * 256);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dot(raw[j], i + j * 256);
       }
-      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-      if (lane == 0) logits[(int64_t)r * vocab + v] = acc;
+      for (; i < d; i += 256) dot(ld(i), i);
+    } else {
+      for (int i = lane; i < d; i += 32) {
+        const A uv = (A)to_f(u[i]);
+#pragma unroll
+        for (int r = 0; r < 8; ++r)
+          if (r < m) acc[r] += uv * xs[r * d + i];
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      if (r < m) {
+        A a = acc[r];
+        for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+        if (lane == 0) logits[(int64_t)r * vocab + v] = a;
+      }
     }
   }
 }
