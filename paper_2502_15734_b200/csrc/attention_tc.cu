@@ -17,6 +17,7 @@
 // The PV MMA of tile i overlaps the S MMA of tile i+1 and the softmax of
 // tile i+1 (double-buffered S).
 #include <math.h>
+#include <stdlib.h>
 
 #include <mutex>
 #include <unordered_map>
@@ -32,7 +33,11 @@ namespace {
 using namespace sm100;
 
 constexpr int AT_BN = 128;      // keys per tile
-constexpr int AT_STAGES = 2;    // K/V ring depth
+// P (softmax output, bf16) lives in TMEM and feeds the PV MMA as its A
+// operand (tcgen05.mma ... [a-tmem]); this frees the smem P buffers and 64 KiB
+// of smem traffic per tile, so the K/V ring gets a third stage.
+constexpr bool kPTmem = true;
+constexpr int AT_STAGES = kPTmem ? 3 : 2;    // K/V ring depth
 constexpr int AT_THREADS = 320;  // TMA warp, MMA warp, 2 x 4 softmax warps
 
 // MN-major operand (B = V: N = head dim contiguous, K = keys), 128B swizzle:
@@ -83,6 +88,17 @@ __device__ __forceinline__ void st_shared_v4(uint32_t addr, const uint32_t (&v)[
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
+// mbarrier wait that adds its stall cycles to acc when tracing (debug)
+__device__ __forceinline__ void twait(uint64_t* bar, uint32_t parity, bool tracing, long long& acc) {
+  if (tracing) {
+    const long long t0 = clock64();
+    mbar_wait(bar, parity);
+    acc += clock64() - t0;
+  } else {
+    mbar_wait(bar, parity);
+  }
+}
+
 template <int DH>
 struct AtSmem {
   static constexpr int ATOMS = DH / 64;              // 64-element (128 B) column atoms
@@ -93,7 +109,7 @@ struct AtSmem {
   static constexpr int K_OFF = Q_OFF + Q_BYTES;
   static constexpr int V_OFF = K_OFF + AT_STAGES * KV_BYTES;
   static constexpr int P_OFF = V_OFF + AT_STAGES * KV_BYTES;
-  static constexpr int BAR_OFF = P_OFF + 2 * P_BYTES;
+  static constexpr int BAR_OFF = P_OFF + (kPTmem ? 0 : 2 * P_BYTES);
   static constexpr int X_OFF = BAR_OFF + 256;        // [2 parities][2 halves][128 rows] f32 exchange
   // no alignment slack: the kernel holds no static shared memory, so the
   // dynamic window starts 1 KiB aligned (checked at run time)
@@ -105,7 +121,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                    const __grid_constant__ CUtensorMap tmV, const int32_t* __restrict__ q_slot,
                    const uint8_t* __restrict__ key_pad, __nv_bfloat16* __restrict__ ctx, float* __restrict__ lse,
-                   int n_q, int n_keys, int Hq, int G, float scale_log2) {
+                   int n_q, int n_keys, int Hq, int G, float scale_log2, long long* __restrict__ trace) {
   using SM = AtSmem<DH>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* base = smem_raw;
@@ -171,7 +187,11 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
   const uint32_t tmem = *tmem_slot;
   const int kmax = s_kmax;
   const int n_tiles = kmax < 0 ? 0 : kmax / AT_BN + 1;
-  const uint32_t t_s0 = tmem, t_o = tmem + 256;
+  const uint32_t t_s0 = tmem, t_o = tmem + 256, t_p = tmem + 384;  // S0 S1 | O | P0 P1
+  const bool tracing = trace != nullptr;
+  long long w0 = 0, w1 = 0, w2 = 0, w3 = 0, t_loop = 0;  // per-role stall cycles (trace only)
+  long long t_begin = 0;
+  if (trace != nullptr && threadIdx.x == 64) asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_begin));
 
   if (warp == 0) {
     if (lane == 0 && n_tiles > 0) {
@@ -183,7 +203,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
       // load issued after the previous PV
       auto load_k = [&](int i) {
         const int st = i % AT_STAGES;
-        mbar_wait(&k_empty[st], ((i / AT_STAGES) & 1) ^ 1);
+        twait(&k_empty[st], ((i / AT_STAGES) & 1) ^ 1, tracing, w0);
         mbar_expect_tx(&k_full[st], SM::KV_BYTES);
 #pragma unroll
         for (int a = 0; a < SM::ATOMS; ++a)
@@ -193,7 +213,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
       for (int i = 0; i < n_tiles; ++i) {
         if (i + 1 < n_tiles) load_k(i + 1);
         const int st = i % AT_STAGES;
-        mbar_wait(&v_empty[st], ((i / AT_STAGES) & 1) ^ 1);
+        twait(&v_empty[st], ((i / AT_STAGES) & 1) ^ 1, tracing, w1);
         mbar_expect_tx(&v_full[st], SM::KV_BYTES);
 #pragma unroll
         for (int a = 0; a < SM::ATOMS; ++a)
@@ -207,8 +227,8 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
       mbar_wait(q_full, 0);
       auto issue_s = [&](int i) {
         const int st = i % AT_STAGES, b = i & 1;
-        mbar_wait(&k_full[st], (i / AT_STAGES) & 1);
-        mbar_wait(&s_empty[b], ((i >> 1) & 1) ^ 1);
+        twait(&k_full[st], (i / AT_STAGES) & 1, tracing, w0);
+        twait(&s_empty[b], ((i >> 1) & 1) ^ 1, tracing, w1);
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < DH / 16; ++kk) {
@@ -224,15 +244,20 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
       for (int i = 0; i < n_tiles; ++i) {
         if (i + 1 < n_tiles) issue_s(i + 1);
         const int st = i % AT_STAGES, pb = i & 1;
-        mbar_wait(&p_full[pb], (i >> 1) & 1);
-        mbar_wait(&v_full[st], (i / AT_STAGES) & 1);
+        twait(&p_full[pb], (i >> 1) & 1, tracing, w2);
+        twait(&v_full[st], (i / AT_STAGES) & 1, tracing, w3);
         tc_fence_after();
         const uint8_t* sPb = sP + pb * SM::P_BYTES;
 #pragma unroll
         for (int kk = 0; kk < AT_BN / 16; ++kk) {
-          uint64_t ad = desc_sw128(sPb + (kk >> 2) * 128 * 128) + 2 * (kk & 3);
           uint64_t bd = desc_sw128_mn(sV + st * SM::KV_BYTES + kk * 16 * 128, AT_BN * 128);
-          mma_bf16(t_o, ad, bd, id_o, (i > 0 || kk > 0) ? 1u : 0u);
+          if constexpr (kPTmem) {
+            // A = P in TMEM: row = lane, 2 bf16 keys per 32-bit column, 16 keys = 8 columns
+            mma_bf16_ts(t_o, t_p + pb * (AT_BN / 2) + kk * 8, bd, id_o, (i > 0 || kk > 0) ? 1u : 0u);
+          } else {
+            uint64_t ad = desc_sw128(sPb + (kk >> 2) * 128 * 128) + 2 * (kk & 3);
+            mma_bf16(t_o, ad, bd, id_o, (i > 0 || kk > 0) ? 1u : 0u);
+          }
         }
         mma_commit(&p_empty[pb]);
         mma_commit(&v_empty[st]);
@@ -258,7 +283,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
     auto pair_bar = [&]() { asm volatile("bar.sync %0, 64;" ::"r"(2 + q4) : "memory"); };
     for (int i = 0; i < n_tiles; ++i) {
       const int b = i & 1;
-      mbar_wait(&s_full[b], (i >> 1) & 1);
+      twait(&s_full[b], (i >> 1) & 1, tracing, w0);
       tc_fence_after();
       float s[64];
       {
@@ -315,13 +340,14 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
       }
       const int pb = i & 1;
       if (i >= 2) {
-        mbar_wait(&p_empty[pb], ((i - 2) >> 1) & 1);  // PV_{i-2} done: P buffer pb free
+        twait(&p_empty[pb], ((i - 2) >> 1) & 1, tracing, w1);  // PV_{i-2} done: P buffer pb free
         tc_fence_after();
       }
       if (m_run == -INFINITY) m_run = tmax;  // first visible keys: nothing accumulated yet
       const float base_l2 = (m_run == -INFINITY) ? 0.f : m_run * scale_log2;
       float ps[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
       const uint32_t patom = patom_s + pb * SM::P_BYTES;
+      uint32_t pt[32];  // this half's 64 keys of P, packed bf16x2 (TMEM P)
 #pragma unroll
       for (int ch = 0; ch < 8; ++ch) {
         uint32_t pk[4];
@@ -339,14 +365,20 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
           __nv_bfloat162 hv = __floats2bfloat162_rn(p0, p1);
           pk[e] = *reinterpret_cast<uint32_t*>(&hv);
         }
-        st_shared_v4(patom + ((ch ^ (m & 7)) << 4), pk);
+        if constexpr (kPTmem) {
+#pragma unroll
+          for (int e = 0; e < 4; ++e) pt[ch * 4 + e] = pk[e];
+        } else {
+          st_shared_v4(patom + ((ch ^ (m & 7)) << 4), pk);
+        }
       }
+      if constexpr (kPTmem) tmem_st32(t_p + pb * (AT_BN / 2) + h * 32 + lane_off, pt);
       l_run += ((ps[0] + ps[1]) + (ps[2] + ps[3])) + ((ps[4] + ps[5]) + (ps[6] + ps[7]));
       // O *= alpha (this half's columns) for rows whose max grew past the lazy
       // threshold.  tcgen05.ld/st are warp-collective: the whole warp joins,
       // alpha = 1 for rows that keep their max.
       if (__any_sync(0xffffffffu, grow)) {
-        mbar_wait(&p_empty[(i - 1) & 1], ((i - 1) >> 1) & 1);  // PV_{i-1} done: O current
+        twait(&p_empty[(i - 1) & 1], ((i - 1) >> 1) & 1, tracing, w2);  // PV_{i-1} done: O current
         tc_fence_after();
 #pragma unroll 1
         for (int c = 0; c < DH / 64; ++c) {
@@ -360,7 +392,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
         }
         tmem_st_wait();
       }
-      fence_async_smem();
+      if constexpr (kPTmem) tmem_st_wait(); else fence_async_smem();
       tc_fence_before();
       mbar_arrive(&p_full[pb]);
     }
@@ -396,6 +428,21 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
     if (row < n_q && h == 0)
       lse[(int64_t)row * Hq + head] = l_tot > 0.f ? (m_run * scale_log2 + log2f(l_tot)) * 0.6931471805599453f : -INFINITY;
   }
+  if (tracing) {
+    long long* tr = trace + 16 * ((int64_t)blockIdx.y * gridDim.x + blockIdx.x);
+    if (threadIdx.x == 64) {
+      long long t_end;
+      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_end));
+      int smid;
+      asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+      tr[0] = n_tiles; tr[1] = t_begin; tr[2] = t_end; tr[3] = smid;
+      tr[4] = w0; tr[5] = w1; tr[6] = w2; tr[7] = w3;  // softmax: s_full, p_empty(i-2), p_empty(grow)
+    } else if (threadIdx.x == 32) {
+      tr[8] = w0; tr[9] = w1; tr[10] = w2; tr[11] = w3;  // mma: k_full, s_empty, p_full, v_full
+    } else if (threadIdx.x == 0) {
+      tr[12] = w0; tr[13] = w1;  // tma: k_empty, v_empty
+    }
+  }
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {
@@ -403,6 +450,8 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
     tmem_dealloc<512>(tmem);
   }
 }
+
+long long* g_attn_trace = nullptr;  // debug: per-CTA (n_tiles, start, end, sm, stalls)
 
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -463,7 +512,7 @@ int launch(const void* q, const void* k, const void* v, const int32_t* q_slot, c
   dim3 grid(Hkv, (n_q + R - 1) / R);
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)DH);
   attn_tc_kernel<DH><<<grid, AT_THREADS, AtSmem<DH>::TOTAL, st>>>(mq, mk, mv, q_slot, key_pad, (__nv_bfloat16*)ctx,
-                                                                  lse, n_q, n_keys, Hq, G, scale_log2);
+                                                                  lse, n_q, n_keys, Hq, G, scale_log2, g_attn_trace);
   return check_launch("attention_tc");
 }
 
@@ -481,3 +530,8 @@ int attention_tc_bf16(const void* q, const void* k, const void* v, const int32_t
 }
 
 }  // namespace ccb
+
+// debug hook (not part of the ABI): per-CTA timeline of the next attention launches
+extern "C" __attribute__((visibility("default"))) void cc_debug_attn_trace(void* p) {
+  ccb::g_attn_trace = reinterpret_cast<long long*>(p);
+}
