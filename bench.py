@@ -63,6 +63,8 @@ def parse():
     p.add_argument("--sweep", action="store_true", help="also report the recompute-ratio sweep 0..50%%")
     p.add_argument("--no-baselines", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--decode-steps", type=int, default=32,
+                   help="greedy decode tokens timed after the fix-up (SURVEY f3); 0 skips")
     p.add_argument("--cpu-layers", type=int, default=2, help="layers in the bounded CPU-oracle sample")
     p.add_argument("--requests", type=int, default=60, help="zipf: trace length (per rank before sharding x world)")
     p.add_argument("--config", default="8b", choices=["8b", "8b-32k", "70b", "zipf"],
@@ -355,6 +357,47 @@ def torch_reference_full(model, tokens):
     return run, attn_name
 
 
+def time_decode(cc, model, req, steps, peaks):
+    """Greedy decode of `steps` tokens continuing the fix-up prefill
+    (engine.DecodeSession: per-token GEMVs + split-KV attention, no host
+    round trip), device-timed with CUDA events on the launching stream.
+    Roofline: HBM — every token streams all weights once plus the KV of
+    every layer (bf16)."""
+    import torch
+
+    from paper_2502_15734_b200 import engine
+
+    res = cc.prefill(model, req, record_attention=False, stats=False)
+    q1 = req.question_span[1] - 1
+    h = torch.from_numpy(np.asarray(res.hidden[q1], np.float64).reshape(1, -1)).to(model.device, model.hidden_dtype)
+    warm = engine.DecodeSession(model, res.kv, 4)
+    warm.run(h)
+    torch.cuda.synchronize()
+    sess = engine.DecodeSession(model, res.kv, steps)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    sess.run(h)
+    b.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b)
+    toks = sess.tokens[:steps].cpu().numpy().tolist()
+    cfg = model.kcfg
+    w_bytes = sum(t.numel() * t.element_size() for lw in model.w["layers"] for t in lw.values() if t is not None)
+    w_bytes += model.w["unembed_t"].numel() * model.w["unembed_t"].element_size()
+    n0 = res.kv.n_slots
+    kv_bytes = sum(2 * (n0 + i + 1) * cfg.kv_width() * 2 * cfg.n_layers for i in range(steps)) / steps
+    per_tok = (w_bytes + kv_bytes)
+    ms_tok = ms / steps
+    gbs = per_tok / (ms_tok / 1e3) / 1e9
+    peak = peaks.get("hbm_gbs") or peaks.get("hbm_copy_gbs") or 6536.4
+    return {"tokens": steps, "tokens_per_s": round(steps / (ms / 1e3), 1), "ms_per_token": round(ms_tok, 4),
+            "context_tokens": n0, "first_tokens": toks[:4],
+            "roofline": {"bound": "hbm", "achieved": round(gbs, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(gbs / peak, 4),
+                         "bytes_per_token": int(per_tok), "note": "all weights + the KV of every layer per token"}}
+
+
 def cpu_baseline(args, req_fix, n_prompt):
     """Oracle port (numpy float64) on the host cores: a bounded sample of
     the same fix-up request — `cpu_layers` full-width Llama-3-8B layers over
@@ -402,6 +445,18 @@ def cpu_baseline(args, req_fix, n_prompt):
 # ---------------------------------------------------------------------------
 
 
+def _traffic(name):
+    """DRAM bytes (read + write) per launch of `name` from the committed ncu
+    capture summary (profiles/traffic.json, written by tools/traffic_json.py
+    from an ncu launch list of one config-2 step); None if absent."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            t = json.load(fh)
+        return t["kernels"][name]["dram_bytes_per_launch"]
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def roofline_obj(name, summ, peaks, bound):
     s = summ.get(name)
     if not s or s["ms_total"] <= 0:
@@ -411,13 +466,14 @@ def roofline_obj(name, summ, peaks, bound):
         ach = s["flops"] / sec / 1e12
         peak = peaks.get("bf16_tflops_sustained") or 1407.5
         return {"kernel": name, "bound": "tensor", "achieved": round(ach, 1), "peak": peak, "unit": "TFLOP/s",
-                "frac": round(ach / peak, 4), "traffic": None, "launches": s["launches"],
+                "frac": round(ach / peak, 4), "traffic": _traffic(name), "launches": s["launches"],
                 "avg_launch_us": round(s["ms_total"] * 1e3 / s["launches"], 2),
                 "peak_source": "measured sustained (MEASURED_PEAKS.json)"}
     ach = s["bytes"] / sec / 1e9
     peak = peaks.get("hbm_gbs") or 6536.4
     return {"kernel": name, "bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
-            "frac": round(ach / peak, 4), "traffic": None, "launches": s["launches"],
+            "frac": round(ach / peak, 4), "traffic": _traffic(name), "launches": s["launches"],
+            "algorithmic_bytes_per_launch": int(s["bytes"] / s["launches"]),
             "avg_launch_us": round(s["ms_total"] * 1e3 / s["launches"], 2),
             "peak_source": "measured copy bandwidth (MEASURED_PEAKS.json)"}
 
@@ -587,6 +643,11 @@ def main():
     e2e_value = n_prompt * (1 if tp_mode else world) / (e2e_mean / 1e3)
     ttft_p50 = statistics.median(e2e_ms)
 
+    # ---- decode continuation on the repaired KV (f3) ------------------------
+    decode = None
+    if args.decode_steps > 0 and not tp_mode:
+        decode = time_decode(cc, model, req, args.decode_steps, peaks)
+
     # ---- baselines on the same GPU --------------------------------------------
     baselines = {}
     if not args.no_baselines:
@@ -668,6 +729,8 @@ def main():
     }
     if sweep:
         line["recompute_sweep"] = sweep
+    if decode:
+        line["decode"] = decode
     print(json.dumps(line), flush=True)
 
 

@@ -176,6 +176,30 @@ CC_API int cc_extract_to_pool(const void* kv_k, const void* kv_v, int64_t req_la
  * parallel all-reduce of the o_proj / down_proj partial outputs). */
 CC_API int cc_add_f32(float* dst, const float* src, int64_t n, void* stream);
 
+/* ---- decode continuation (model.py:445-484) ---------------------------- */
+
+/* Weight-streaming projection for 1..4 rows (the per-token QKV / o / MLP
+ * products of decode, model.py:461-476): C[M,N] (+)= epi(A[M,K] W[N,K]^T),
+ * bf16 A/W, same epilogues and C types as cc_gemm (which routes bf16 M <= 4
+ * here when impl == 0).  CC_E_UNSUP unless K % 8 == 0, 16-byte aligned rows
+ * and M*K*2 <= 96 KiB. */
+CC_API int cc_gemv(const void* A, int64_t lda, const void* W, int64_t ldw, void* C, int64_t ldc, int M, int N,
+                   int K, int epilogue, void* stream);
+
+/* Attention of ONE new query row over all n_keys keys (model.py:467-474: the
+ * decode token sees every valid key incl. its own), bf16, d_head 128,
+ * split-KV over 128-key chunks with a fixed-order combine (deterministic).
+ * q [Hq*dh] rotated; k_rot/v [n_keys][Hkv*dh]; key_pad[j] != 0 masks key j
+ * (kv.valid false).  Writes ctx [Hq*dh] and lse [Hq] (as cc_attention). */
+CC_API int cc_decode_attention(const void* q, const void* k_rot, const void* v, const uint8_t* key_pad, void* ctx,
+                               float* lse, int n_keys, int n_heads, int n_kv_heads, int d_head, void* stream);
+
+/* y[r] = RoPE(x[r], positions[r % n]) for n_rows rows of `width` (= heads x
+ * d_head) (rpe.py:19-44 apply_rpe; decode rotates the stored position-free
+ * keys at their positions, model.py:467-468).  x == y allowed. */
+CC_API int cc_rope_rows(const void* x, void* y, int64_t n_rows, int n, int width, const int32_t* positions,
+                        const void* rope_table, int d_head, int dtype, void* stream);
+
 /* L2 flush helper for benchmarks: writes `bytes` of scratch. */
 CC_API int cc_flush_l2(void* scratch, size_t bytes, void* stream);
 

@@ -319,6 +319,68 @@ def greedy_token(w: dict, cfg: OracleConfig, result: dict) -> int:
     return int(np.argmax(logits(w, cfg, result["hidden"][q1 - 1])[0]))
 
 
+def decode(w: dict, cfg: OracleConfig, keys, values, positions, valid, last_hidden, max_steps: int):
+    """Greedy decode (model.py:445-484): token = argmax(logits(hidden_row));
+    embed it; per layer the new row's q/k/v from the normed state, ALL keys
+    (stored position-free, pads at position 0, :466) rotated at their
+    positions, q at next_pos, pads masked, residual MLP; the new K/V row is
+    appended (:481 append_token).  Returns (tokens, keys, values) with the
+    per-layer K/V extended by max_steps rows."""
+    H, Hkv, dh, d = cfg.n_heads, cfg.hkv, cfg.dh, cfg.d_model
+    group = H // Hkv
+    nw = cfg.norm_weight
+    keys = [np.asarray(k, dtype=np.float64) for k in keys]
+    values = [np.asarray(v, dtype=np.float64) for v in values]
+    positions = np.asarray(positions, dtype=np.int64)
+    valid = np.asarray(valid, dtype=bool)
+    out = []
+    if max_steps <= 0:
+        return out, keys, values
+    hidden_row = np.asarray(last_hidden, dtype=np.float64).reshape(1, d)
+    next_pos = int(positions[valid].max()) + 1
+    for _ in range(max_steps):
+        token = int(np.argmax(logits(w, cfg, hidden_row)[0]))
+        out.append(token)
+        x = w["embed"][token][None, :]
+        new_rows = []
+        for l in range(cfg.n_layers):
+            lw = w["layers"][l]
+            xn = rmsnorm(x, cfg.rms_eps, lw["attn_norm"] if nw else None)
+            q = xn @ lw["wq"]
+            k_new = xn @ lw["wk"]
+            v_new = xn @ lw["wv"]
+            K = np.vstack([keys[l], k_new])
+            V = np.vstack([values[l], v_new])
+            key_pos = np.append(np.where(valid, positions, 0), next_pos)
+            kr = rope(K, key_pos, cfg.rpe_base, dh).reshape(-1, Hkv, dh)
+            qr = rope(q, [next_pos], cfg.rpe_base, dh).reshape(H, dh)
+            kr_h = np.repeat(kr.transpose(1, 0, 2), group, axis=0)  # [H, n, dh]
+            vv_h = np.repeat(V.reshape(-1, Hkv, dh).transpose(1, 0, 2), group, axis=0)
+            sc = np.einsum("hd,hkd->hk", qr, kr_h) / np.sqrt(dh)
+            ok = np.append(valid, True)
+            sc[:, ~ok] = -np.inf
+            sc -= sc.max(axis=1, keepdims=True)
+            p = np.exp(sc)
+            p /= p.sum(axis=1, keepdims=True)
+            ctx = np.einsum("hk,hkd->hd", p, vv_h).reshape(1, H * dh)
+            x = x + ctx @ lw["wo"]
+            xn2 = rmsnorm(x, cfg.rms_eps, lw["mlp_norm"] if nw else None)
+            if cfg.mlp == "swiglu":
+                ff = silu(xn2 @ lw["w_gate"]) * (xn2 @ lw["w_up"])
+            else:
+                ff = gelu_tanh(xn2 @ lw["w_up"])
+            x = x + ff @ lw["w_down"]
+            new_rows.append((k_new, v_new))
+        for l, (k_row, v_row) in enumerate(new_rows):
+            keys[l] = np.vstack([keys[l], k_row])
+            values[l] = np.vstack([values[l], v_row])
+        positions = np.append(positions, next_pos)
+        valid = np.append(valid, True)
+        next_pos += 1
+        hidden_row = x
+    return out, keys, values
+
+
 # --------------------------------------------------------------------------
 # selection and scoring  (planner.py:17-34, scoring.py:45-111)
 # --------------------------------------------------------------------------

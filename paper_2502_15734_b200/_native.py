@@ -47,6 +47,9 @@ _SIGS = {
     "cc_extract_to_pool": ([_vp, _vp, _i64, _i32, _i32, _i32, _vp, _i32, _vp, _i64, _i64, _i32, _i32, _vp], _i32),
     "cc_add_f32": ([_vp, _vp, _i64, _vp], _i32),
     "cc_flush_l2": ([_vp, _sz, _vp], _i32),
+    "cc_gemv": ([_vp, _i64, _vp, _i64, _vp, _i64, _i32, _i32, _i32, _i32, _vp], _i32),
+    "cc_decode_attention": ([_vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _vp], _i32),
+    "cc_rope_rows": ([_vp, _vp, _i64, _i32, _i32, _vp, _vp, _i32, _i32, _vp], _i32),
 }
 
 _lib = None
@@ -98,8 +101,10 @@ def call(name: str, *args):
     fn = getattr(lib(), name)
     rc = fn(*args)
     calls[name] = calls.get(name, 0) + 1
-    # cc_logits_argmax with an argmax output runs GEMV + two argmax stages
-    kernels_launched += 3 if (name == "cc_logits_argmax" and args[5] is not None) else 1
+    # cc_logits_argmax with an argmax output runs GEMV + two argmax stages;
+    # cc_decode_attention runs the split-KV partials + the combine
+    kernels_launched += 3 if (name == "cc_logits_argmax" and args[5] is not None) else (
+        2 if name == "cc_decode_attention" else 1)
     check(rc, name)
     return rc
 

@@ -108,8 +108,11 @@ extern "C" int cc_gemm(const void* A, int64_t lda, const void* B, int64_t ldb, v
   CCB_REQUIRE(M >= 0 && N > 0 && K > 0, "gemm: bad shape");
   if (M == 0) return 0;
   cudaStream_t st = as_stream(stream);
-  // impl: 0 auto (tcgen05, split-K allowed -> SIMT if unsupported), 1 tcgen05 with
-  // split-K, 4 tcgen05 without split-K (batch/M-invariant), 2 SIMT reference
+  // impl: 0 auto (bf16: <= 4 rows -> weight-streaming GEMV, else tcgen05 with
+  // stream-K allowed; SIMT if unsupported), 1 tcgen05 with stream-K, 4 tcgen05
+  // without split (batch/M-invariant), 2 SIMT reference
+  if (dtype == CC_BF16 && impl == 0 && gemv_eligible(M, N, K, epilogue, A, lda, B, ldb))
+    return gemv_bf16(A, lda, B, ldb, C, ldc, M, N, K, epilogue, st);
   if (dtype == CC_BF16 && impl != 2) {
     int rc = gemm_tc_bf16(A, lda, B, ldb, C, ldc, M, N, K, epilogue, impl != 4, st);
     if (rc != CC_E_UNSUP || impl == 1 || impl == 4) return rc;

@@ -589,48 +589,159 @@ def extract_rows(result: PrefillResult, start: int, stop: int, source_prefix=())
     return ChunkCache(n_tokens=n, source_prefix=source_prefix, _payload=_Payload(pool, blocks, n))
 
 
+class DecodeSession:
+    """Greedy decode on the device (model.py:445-484).
+
+    The request KV is copied once into capacity buffers [L][n0 + max_steps]
+    (position-free ``kv_k``/``kv_v`` + ``k_rot`` rotated at the key positions,
+    pads at position 0 as in the reference, :466); every step then runs the
+    per-layer pipeline for the single new row entirely on the stream: the
+    token id never leaves the device (argmax -> embedding), the new K/V row is
+    scattered in place (cc_rope_scatter_qkv), attention is the split-KV
+    cc_decode_attention (bf16) and the projections are weight-streaming
+    GEMVs (cc_gemm routes M = 1 there).  Tokens are read back once."""
+
+    def __init__(self, model: Model, kv: KVCache, max_steps: int):
+        import torch
+
+        cfg = model.kcfg
+        self.model, self.kv, self.steps = model, kv, int(max_steps)
+        L, kvw = cfg.n_layers, cfg.kv_width()
+        dev, T = model.device, model.torch_dtype
+        n0 = kv.n_slots
+        cap = n0 + self.steps
+        self.n0, self.cap = n0, cap
+        valid = np.asarray(kv.valid, bool)
+        positions = np.asarray(kv.positions, np.int64)
+        if not valid.any():
+            raise PlanError("decode needs at least one valid KV row")
+        self.next_pos = int(positions[valid].max()) + 1
+        key_pos = np.where(valid, positions, 0)
+        pos_all = np.concatenate([key_pos, self.next_pos + np.arange(self.steps)]).astype(np.int32)
+        slots = (n0 + np.arange(self.steps)).astype(np.int32)
+        pad = np.zeros(-(-cap // 16) * 16, np.uint8)
+        pad[:n0] = ~valid
+        self.has_pad = bool((~valid).any())
+        self.kv_k = torch.empty((L, cap, kvw), dtype=T, device=dev)
+        self.kv_v = torch.empty((L, cap, kvw), dtype=T, device=dev)
+        self.k_rot = torch.empty((L, cap, kvw), dtype=T, device=dev)
+        if n0:
+            if kv._dev is not None:
+                self.kv_k[:, :n0].copy_(kv._dev[0][:, :n0])
+                self.kv_v[:, :n0].copy_(kv._dev[1][:, :n0])
+            else:
+                self.kv_k[:, :n0].copy_(torch.from_numpy(np.stack(kv.keys)).to(dev, T))
+                self.kv_v[:, :n0].copy_(torch.from_numpy(np.stack(kv.values)).to(dev, T))
+        self.pos = torch.from_numpy(pos_all).to(dev)
+        self.slots = torch.from_numpy(slots).to(dev)
+        self.pad = torch.from_numpy(pad).to(dev)
+        self.rope = model.rope_table(self.next_pos + self.steps)
+        if n0:
+            N.call("cc_rope_rows", N.ptr(self.kv_k), N.ptr(self.k_rot), L * cap, cap, kvw, N.ptr(self.pos),
+                   N.ptr(self.rope), cfg.head_dim(), model.dtype_code, N.stream_ptr())
+        d, q, ff = cfg.d_model, cfg.q_width(), cfg.ff_dim()
+        Hd = model.hidden_dtype
+        e = torch.empty
+        self.hidden = e((1, d), dtype=Hd, device=dev)
+        self.part = e((1, d), dtype=Hd, device=dev) if (model.tp is not None and model.tp.world > 1) else None
+        self.xn = e((1, d), dtype=T, device=dev)
+        self.qkv = e((1, q + 2 * kvw), dtype=T, device=dev)
+        self.q_rot = e((1, q), dtype=T, device=dev)
+        self.ctx = e((1, q), dtype=T, device=dev)
+        self.act = e((1, ff), dtype=T, device=dev)
+        self.lse = e((1, cfg.n_heads), dtype=Hd, device=dev)
+        self.tokens = torch.zeros((self.steps + 1,), dtype=torch.int32, device=dev)
+        self.logits = e((1, model.config.vocab_size), dtype=Hd, device=dev)
+        self.launches = 0
+
+    def _argmax(self, rows, out_idx: int):
+        m = self.model
+        cfg = m.config
+        N.call("cc_logits_argmax", N.ptr(rows), N.ptr(m.w.get("final_norm")), cfg.rms_eps, N.ptr(m.w["unembed_t"]),
+               N.ptr(self.logits), N.ptr(self.tokens[out_idx:out_idx + 1]), 1, cfg.d_model, cfg.vocab_size,
+               m.dtype_code, N.stream_ptr())
+        self.launches += 3 if m.dtype_code != N.F64 else 1
+
+    def _layers(self, step: int):
+        m = self.model
+        cfg = m.kcfg
+        tp = m.tp if (m.tp is not None and m.tp.world > 1) else None
+        P, s, dt = N.ptr, N.stream_ptr(), m.dtype_code
+        H, Hkv, dh, d = cfg.n_heads, cfg.kv_heads(), cfg.head_dim(), cfg.d_model
+        qw, kvw, ff = cfg.q_width(), cfg.kv_width(), cfg.ff_dim()
+        slot = self.n0 + step
+        row_slot = self.slots[step:step + 1]
+        row_pos = self.pos[slot:slot + 1]
+        pad = P(self.pad) if self.has_pad else None
+        hid = self.hidden
+        N.call("cc_embed_rows", P(m.w["embed"]), P(self.tokens[step:step + 1]), P(hid), 1, d, dt, s)
+        fast_attn = dt == N.BF16 and dh == 128 and H // Hkv in (1, 2, 4, 8)
+        for l in range(cfg.n_layers):
+            lw = m.w["layers"][l]
+            N.call("cc_rmsnorm", P(hid), P(self.xn), P(lw.get("attn_norm")), 1, d, cfg.rms_eps, dt, s)
+            N.call("cc_gemm", P(self.xn), d, P(lw["w_qkv"]), d, P(self.qkv), qw + 2 * kvw, 1, qw + 2 * kvw, d,
+                   N.EPI_STORE, dt, 0, s)
+            N.call("cc_rope_scatter_qkv", P(self.qkv), qw + 2 * kvw, 1, P(row_slot), P(row_pos), P(self.rope),
+                   P(self.q_rot), P(self.kv_k[l]), P(self.kv_v[l]), P(self.k_rot[l]), H, Hkv, dh, dt, s)
+            if fast_attn:
+                N.call("cc_decode_attention", P(self.q_rot), P(self.k_rot[l]), P(self.kv_v[l]), pad, P(self.ctx),
+                       P(self.lse), slot + 1, H, Hkv, dh, s)
+            else:
+                N.call("cc_attention", P(self.q_rot), P(self.k_rot[l]), P(self.kv_v[l]), P(row_slot), pad,
+                       P(self.ctx), P(self.lse), 1, slot + 1, H, Hkv, dh, dt, 0, s)
+            if tp is None:
+                N.call("cc_gemm", P(self.ctx), qw, P(lw["w_o"]), qw, P(hid), d, 1, d, qw, N.EPI_RESID_ADD, dt, 0, s)
+            else:
+                _tp_partial_gemm(m, tp, self.ctx, qw, lw["w_o"], hid, self.part, 1, d, qw, dt, 0, s)
+            N.call("cc_rmsnorm", P(hid), P(self.xn), P(lw.get("mlp_norm")), 1, d, cfg.rms_eps, dt, s)
+            if cfg.mlp == "swiglu":
+                N.call("cc_gemm", P(self.xn), d, P(lw["w_gu"]), d, P(self.act), ff, 1, 2 * ff, d, N.EPI_SWIGLU, dt,
+                       0, s)
+            else:
+                N.call("cc_gemm", P(self.xn), d, P(lw["w_up"]), d, P(self.act), ff, 1, ff, d, N.EPI_GELU, dt, 0, s)
+            if tp is None:
+                N.call("cc_gemm", P(self.act), ff, P(lw["w_down"]), ff, P(hid), d, 1, d, ff, N.EPI_RESID_ADD, dt,
+                       0, s)
+            else:
+                _tp_partial_gemm(m, tp, self.act, ff, lw["w_down"], hid, self.part, 1, d, ff, dt, 0, s)
+        self.launches += 1 + cfg.n_layers * (8 if fast_attn else 8) + (cfg.n_layers if fast_attn else 0)
+
+    def run(self, last_hidden_dev) -> None:
+        """Enqueue all steps (no host synchronisation)."""
+        self._argmax(last_hidden_dev, 0)
+        for step in range(self.steps):
+            self._layers(step)
+            if step + 1 < self.steps:
+                self._argmax(self.hidden, step + 1)
+
+    def finish(self) -> list:
+        """Read the tokens back and extend the caller's KVCache in place
+        (kv.append_token semantics: position-free rows, positions next_pos..)."""
+        toks = [int(t) for t in self.tokens[: self.steps].cpu().numpy()]
+        kv = self.kv
+        new_pos = self.next_pos + np.arange(self.steps)
+        kv._keys = None
+        kv._values = None
+        kv._dev = (self.kv_k, self.kv_v)
+        kv.positions = np.concatenate([np.asarray(kv.positions, np.int64), new_pos])
+        kv.valid = np.concatenate([np.asarray(kv.valid, bool), np.ones(self.steps, bool)])
+        return toks
+
+
 def run_decode(model: Model, kv: KVCache, last_hidden, max_steps: int) -> list:
-    """Greedy decode (model.py:445-484): token from logits(last row), then
-    one engine step per token over the whole existing KV (a cache segment of
-    every previous slot, nothing recomputed) plus the new token."""
+    """Greedy decode (model.py:445-484) on the device: see DecodeSession."""
     import torch
 
     if max_steps <= 0:
         return []
-    cfg = model.config
-    out = []
-    tok = int(logits_device(model, last_hidden)[1][0])
-    valid = kv.valid.copy()
-    positions = kv.positions.copy()
-    keys = [np.asarray(k) for k in kv.keys]
-    values = [np.asarray(v) for v in kv.values]
-    next_pos = int(positions[valid].max()) + 1
-    for step in range(max_steps):
-        out.append(tok)
-        n_prev = positions.size
-        cache = ChunkCache(keys=keys, values=values, n_tokens=n_prev)
-        payload = cache.device_payload(model)
-        token_ids = np.zeros(n_prev + 1, np.int64)
-        token_ids[-1] = tok
-        pos = np.concatenate([np.where(valid, positions, 0), [next_pos]]).astype(np.int64)
-        pad = np.concatenate([~valid, [False]])
-        mask = np.zeros(n_prev + 1, bool)
-        mask[-1] = True
-        depth = np.zeros(n_prev + 1, np.int64)
-        depth[-1] = FULL_DEPTH
-        plan = DevicePlan(model, token_ids, pos, pad, mask, depth, [(0, n_prev)], [payload], (n_prev, n_prev + 1))
-        ws = _workspace(model, plan)
-        execute(model, plan, ws)
-        new_k = ws["kv_k"][:, n_prev].double().cpu().numpy()
-        new_v = ws["kv_v"][:, n_prev].double().cpu().numpy()
-        rows = [(new_k[l][None, :], new_v[l][None, :]) for l in range(cfg.n_layers)]
-        kv.append_token(rows, next_pos)
-        keys = kv.keys
-        values = kv.values
-        valid = kv.valid.copy()
-        positions = kv.positions.copy()
-        next_pos += 1
-        if step + 1 < max_steps:
-            _, t = _logits_rows(model, ws["hidden"][0:1])
-            tok = int(t.item())
-    return out
+    N.require_cuda()
+    sess = DecodeSession(model, kv, max_steps)
+    if isinstance(last_hidden, torch.Tensor):
+        h = last_hidden.reshape(1, -1).to(model.device, model.hidden_dtype)
+    else:
+        h = torch.from_numpy(np.asarray(last_hidden, dtype=np.float64).reshape(1, -1)).to(model.device,
+                                                                                      model.hidden_dtype)
+    if h.shape[1] != model.config.d_model:
+        raise ShapeError("last_hidden width != d_model")
+    sess.run(h.contiguous())
+    return sess.finish()

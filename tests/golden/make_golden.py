@@ -258,17 +258,6 @@ def gen_plan():
                         "census": store.census()})
 
 
-if __name__ == "__main__" and not os.environ.get("GEN_ONLY"):
-    gen_rope()
-    gen_select()
-    gen_scoring()
-    gen_hash()
-    gen_weights()
-    gen_toy_prefill()
-    gen_stats()
-    gen_config1()
-    gen_plan()
-    gen_replay()
     print("golden fixtures written to", HERE)
 
 
@@ -295,5 +284,38 @@ def gen_replay():
     _json("replay.json", out)
 
 
-if __name__ == "__main__" and os.environ.get("GEN_ONLY") == "replay":
-    gen_replay()
+
+
+def gen_decode():
+    # model.py:445-484 greedy decode continuing the toy fix-up prefill of
+    # gen_toy_prefill (its KV holds pad rows: kv.valid False, position 0)
+    model = cc.build_model(cc.ModelConfig())
+    r = np.random.default_rng(1234)
+    chunks = [r.integers(0, 256, n) for n in (32, 32, 26)]
+    q = r.integers(0, 256, 12)
+    req0 = cc.plain_request(*chunks, [])
+    res0 = cc.prefill(model, req0)
+    caches = [cc.extract_chunk_cache(res0, s, e) for s, e in req0.segment_slots]
+    padded, _ = cc.pad_to_blocks(caches[2])
+    segs = [cc.Segment(tokens=chunks[0], cache=caches[0], recompute=np.eye(32, dtype=bool)[7]),
+            cc.Segment(tokens=chunks[1], cache=caches[1]), cc.Segment(tokens=chunks[2], cache=padded)]
+    req = cc.build_request(segs, q)
+    res = cc.prefill(model, req)
+    kv = res.kv.copy()
+    n0 = kv.positions.size
+    last = res.hidden[req.question_span[1] - 1]
+    toks = cc.decode(model, kv, last, 6)
+    out = {"c0": chunks[0], "c1": chunks[1], "c2": chunks[2], "question": q, "tokens": np.array(toks),
+           "n0": np.array(n0), "positions": kv.positions, "valid": kv.valid, "last_hidden": last}
+    for l in range(4):
+        out[f"k{l}"], out[f"v{l}"] = kv.keys[l], kv.values[l]
+    _save("decode_toy.npz", **out)
+
+
+if __name__ == "__main__":
+    only = os.environ.get("GEN_ONLY")
+    gens = [gen_rope, gen_select, gen_scoring, gen_hash, gen_weights, gen_toy_prefill, gen_stats, gen_config1,
+            gen_plan, gen_replay, gen_decode]
+    for g in gens:
+        if not only or g.__name__ == "gen_" + only:
+            g()

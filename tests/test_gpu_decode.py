@@ -1,0 +1,188 @@
+"""Device greedy decode (model.py:445-484) and its kernels
+against the reference fixture and the CPU oracle.
+
+Tolerances as for prefill: fp64 ~1e-9 absolute vs the reference; fp32 1e-3
+relative; bf16 relative Frobenius < 5e-2 on the appended K/V plus identical
+greedy tokens.  Kernel tests compare with a plain torch fp32 reference."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from ccb_helpers import golden_path  # noqa: E402
+
+from oracle import cachecraft_oracle as O  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def cc():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import paper_2502_15734_b200 as cc
+
+    cc._native.lib()
+    return cc
+
+
+def rel(a, b):
+    a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
+
+
+def _toy_fixup(cc, g, dtype):
+    model = cc.build_model(cc.ModelConfig(dtype=dtype))
+    chunks = [g["c0"], g["c1"], g["c2"]]
+    req0 = cc.plain_request(*chunks, [])
+    res0 = cc.prefill(model, req0)
+    caches = [cc.extract_chunk_cache(res0, s, e) for s, e in req0.segment_slots]
+    padded, _ = cc.pad_to_blocks(caches[2])
+    segs = [cc.Segment(tokens=chunks[0], cache=caches[0], recompute=np.eye(32, dtype=bool)[7]),
+            cc.Segment(tokens=chunks[1], cache=caches[1]), cc.Segment(tokens=chunks[2], cache=padded)]
+    req = cc.build_request(segs, g["question"])
+    return model, req, cc.prefill(model, req)
+
+
+@pytest.mark.parametrize("dtype,tol", [("fp64", 1e-9), ("fp32", 1e-3), ("bf16", 5e-2)])
+def test_decode_continues_padded_fixup_like_reference(cc, dtype, tol):
+    g = np.load(golden_path("decode_toy.npz"))
+    model, req, res = _toy_fixup(cc, g, dtype)
+    kv = res.kv
+    n0 = int(g["n0"])
+    assert kv.n_slots == n0
+    toks = cc.decode(model, kv, res.hidden[req.question_span[1] - 1], 6)
+    assert toks == g["tokens"].tolist()
+    # kv extended in place (model.py:481): positions, validity, appended rows
+    np.testing.assert_array_equal(kv.positions, g["positions"])
+    np.testing.assert_array_equal(kv.valid, g["valid"])
+    for l in range(4):
+        if dtype == "fp64":
+            np.testing.assert_allclose(kv.keys[l], g[f"k{l}"], atol=tol, rtol=0)
+            np.testing.assert_allclose(kv.values[l], g[f"v{l}"], atol=tol, rtol=0)
+        else:
+            assert rel(kv.keys[l][n0:], g[f"k{l}"][n0:]) < tol
+            assert rel(kv.values[l][n0:], g[f"v{l}"][n0:]) < tol
+
+
+def test_decode_zero_steps_and_chaining(cc):
+    g = np.load(golden_path("decode_toy.npz"))
+    model, req, res = _toy_fixup(cc, g, "fp64")
+    kv = res.kv
+    assert cc.decode(model, kv, res.hidden[req.question_span[1] - 1], 0) == []
+    assert kv.n_slots == int(g["n0"])
+    # two decode calls of 3 == one of 6 (the second continues from the extended KV)
+    first = cc.decode(model, kv, res.hidden[req.question_span[1] - 1], 3)
+    assert first == g["tokens"][:3].tolist()
+    assert kv.n_slots == int(g["n0"]) + 3
+
+
+@pytest.mark.parametrize("dtype,tol", [("fp64", 1e-9), ("bf16", 5e-2)])
+def test_decode_llama_shaped_vs_oracle(cc, dtype, tol):
+    """GQA 8/2, d_head 128 (bf16: GEMV projections + split-KV decode attention),
+    SwiGLU, norm weights, theta 5e5."""
+    kw = dict(n_layers=2, n_heads=8, d_model=512, d_head=128, vocab_size=512, rpe_base=500000.0, seed=6,
+              n_kv_heads=2, d_ff=1024, mlp="swiglu", norm_weight=True, rms_eps=1e-5)
+    model = cc.build_model(cc.ModelConfig(dtype=dtype, **kw))
+    ocfg = O.OracleConfig(**kw)
+    w = O.draw_weights(ocfg)
+    r = np.random.default_rng(21)
+    chunks = [r.integers(0, 512, n) for n in (96, 200, 64)]
+    q = r.integers(0, 512, 24)
+    res = cc.prefill(model, cc.plain_request(*chunks, q))
+    lay = O.layout([{"tokens": c} for c in chunks], q)
+    ref = O.prefill(w, ocfg, lay, [None] * 3)
+    last = ref["question_span"][1] - 1
+    n0 = res.kv.n_slots
+    want, k2, v2 = O.decode(w, ocfg, ref["keys"], ref["values"], ref["positions"], ~lay["is_pad"], ref["hidden"][last],
+                            5)
+    kv = res.kv
+    got = cc.decode(model, kv, res.hidden[last], 5)
+    assert got == want
+    for l in range(2):
+        if dtype == "fp64":
+            np.testing.assert_allclose(kv.keys[l][n0:], k2[l][n0:], atol=tol)
+        else:
+            assert rel(kv.keys[l][n0:], k2[l][n0:]) < tol
+            assert rel(kv.values[l][n0:], v2[l][n0:]) < tol
+
+
+# ---------------------------------------------------------------------------
+# kernels
+# ---------------------------------------------------------------------------
+
+
+@pytest.mark.parametrize("M", [1, 3])
+@pytest.mark.parametrize("epi", ["store", "resid", "swiglu", "gelu"])
+def test_gemv_epilogues_vs_torch(cc, M, epi):
+    N = cc._native
+    Nn, K = (1536, 4096) if epi != "resid" else (1024, 14336)
+    g = torch.Generator(device="cuda").manual_seed(3)
+    A = torch.randn((M, K), generator=g, device="cuda").bfloat16()
+    W = (torch.randn((Nn, K), generator=g, device="cuda") / K ** 0.5).bfloat16()
+    acc = A.float() @ W.float().T
+    code = {"store": N.EPI_STORE, "resid": N.EPI_RESID_ADD, "swiglu": N.EPI_SWIGLU, "gelu": N.EPI_GELU}[epi]
+    if epi == "resid":
+        C = torch.ones((M, Nn), device="cuda")
+        ref = acc + 1.0
+    elif epi == "swiglu":
+        C = torch.empty((M, Nn // 2), device="cuda", dtype=torch.bfloat16)
+        a4 = acc.reshape(M, Nn // 128, 2, 64)
+        ref = (torch.nn.functional.silu(a4[:, :, 0]) * a4[:, :, 1]).reshape(M, Nn // 2)
+    else:
+        C = torch.empty((M, Nn), device="cuda", dtype=torch.bfloat16)
+        ref = torch.nn.functional.gelu(acc, approximate="tanh") if epi == "gelu" else acc
+    N.call("cc_gemv", N.ptr(A), K, N.ptr(W), K, N.ptr(C), C.shape[1], M, Nn, K, code, N.stream_ptr())
+    torch.testing.assert_close(C.float(), ref, atol=2e-2, rtol=2e-2)
+    # cc_gemm(impl 0) routes bf16 M <= 4 here: identical bits
+    C2 = torch.ones_like(C) if epi == "resid" else torch.empty_like(C)
+    N.call("cc_gemm", N.ptr(A), K, N.ptr(W), K, N.ptr(C2), C.shape[1], M, Nn, K, code, N.BF16, 0, N.stream_ptr())
+    assert torch.equal(C, C2)
+
+
+@pytest.mark.parametrize("n_keys,G,pads", [(1, 4, False), (300, 4, True), (5153, 4, False), (777, 1, True)])
+def test_decode_attention_vs_torch(cc, n_keys, G, pads):
+    N = cc._native
+    Hkv, dh = 2, 128
+    Hq = Hkv * G
+    g = torch.Generator(device="cuda").manual_seed(n_keys)
+    q = torch.randn((Hq * dh,), generator=g, device="cuda").bfloat16()
+    k = torch.randn((n_keys, Hkv * dh), generator=g, device="cuda").bfloat16()
+    v = torch.randn((n_keys, Hkv * dh), generator=g, device="cuda").bfloat16()
+    pad = torch.zeros((-(-n_keys // 16) * 16,), dtype=torch.uint8, device="cuda")
+    if pads and n_keys > 20:
+        pad[5:17] = 1
+    ctx = torch.empty((Hq * dh,), device="cuda", dtype=torch.bfloat16)
+    lse = torch.empty((Hq,), device="cuda")
+    N.call("cc_decode_attention", N.ptr(q), N.ptr(k), N.ptr(v), N.ptr(pad) if pads else None, N.ptr(ctx), N.ptr(lse),
+           n_keys, Hq, Hkv, dh, N.stream_ptr())
+    qh = q.float().reshape(Hq, dh)
+    kh = k.float().reshape(n_keys, Hkv, dh).repeat_interleave(G, dim=1).transpose(0, 1)  # [Hq, n, dh]
+    vh = v.float().reshape(n_keys, Hkv, dh).repeat_interleave(G, dim=1).transpose(0, 1)
+    s = torch.einsum("hd,hnd->hn", qh, kh) / dh ** 0.5
+    if pads:
+        s[:, pad[:n_keys].bool()] = -float("inf")
+    p = torch.softmax(s, dim=1)
+    ref = torch.einsum("hn,hnd->hd", p, vh).reshape(-1)
+    torch.testing.assert_close(ctx.float(), ref, atol=2e-2, rtol=2e-2)
+    torch.testing.assert_close(lse, torch.logsumexp(s, dim=1), atol=1e-3, rtol=1e-4)
+    # deterministic
+    ctx2 = torch.empty_like(ctx)
+    N.call("cc_decode_attention", N.ptr(q), N.ptr(k), N.ptr(v), N.ptr(pad) if pads else None, N.ptr(ctx2), N.ptr(lse),
+           n_keys, Hq, Hkv, dh, N.stream_ptr())
+    assert torch.equal(ctx, ctx2)
+
+
+def test_rope_rows_matches_oracle(cc):
+    N = cc._native
+    model = cc.build_model(cc.ModelConfig(dtype="fp64"))
+    L, n, width, dh = 3, 37, 64, 16
+    r = np.random.default_rng(2)
+    x = r.standard_normal((L, n, width))
+    pos = r.integers(0, 300, n).astype(np.int32)
+    xd = torch.from_numpy(x).cuda()
+    y = torch.empty_like(xd)
+    pd = torch.from_numpy(pos).cuda()
+    table = model.rope_table(400)
+    N.call("cc_rope_rows", N.ptr(xd), N.ptr(y), L * n, n, width, N.ptr(pd), N.ptr(table), dh, N.F64, N.stream_ptr())
+    want = np.stack([O.rope(x[l], pos, model.config.rpe_base, dh) for l in range(L)])
+    np.testing.assert_allclose(y.cpu().numpy(), want, atol=1e-12)
