@@ -63,6 +63,7 @@ def parse():
     p.add_argument("--sweep", action="store_true", help="also report the recompute-ratio sweep 0..50%%")
     p.add_argument("--no-baselines", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--tiers", type=int, default=1, help="time the host-tier (f2) variant of the fix-up; 0 skips")
     p.add_argument("--decode-steps", type=int, default=32,
                    help="greedy decode tokens timed after the fix-up (SURVEY f3); 0 skips")
     p.add_argument("--cpu-layers", type=int, default=2, help="layers in the bounded CPU-oracle sample")
@@ -357,6 +358,55 @@ def torch_reference_full(model, tokens):
     return run, attn_name
 
 
+def time_tiers(cc, model, req, steps, n_prompt):
+    """f2: the same fix-up with every HIT chunk-cache in the pinned-host tier.
+    Layer-wise preload (copy engine, L_p + 1 slot HBM ring, tiers.py) vs
+    loading everything first (serial) vs all-HBM; device-timed."""
+    import torch
+
+    from paper_2502_15734_b200 import engine, tiers
+
+    rate = tiers.calibrate_h2d(model)
+    tp = tiers.TieredPool(model)
+    segs = []
+    for seg in req.segments:
+        if seg.cache is None:
+            segs.append(seg)
+            continue
+        c = seg.cache.copy()
+        tp.move(c, tiers.HOST)
+        segs.append(cc.Segment(tokens=seg.tokens, cache=c, recompute=seg.recompute,
+                               recompute_depth=seg.recompute_depth))
+    hreq = cc.build_request(segs, req.question)
+    payloads = engine._payloads(model, hreq)
+    dplan = engine.DevicePlan(model, hreq.token_ids, hreq.positions, hreq.is_pad, hreq.recompute_mask,
+                              hreq.recompute_depth, hreq.segment_slots, payloads, hreq.question_span)
+    ws = engine._workspace(model, dplan)
+    ms, _ = time_device(model, dplan, ws, hreq, steps, 2, 1)
+    depth = engine._HostPreload(model, dplan).depth
+    torch.cuda.synchronize()
+    host_bytes = sum(p.nbytes() for p, _ in dplan.host_payloads)
+    # serial: copy all host slabs to HBM first, then the all-HBM step
+    dst = torch.empty(host_bytes, dtype=torch.uint8, device=model.device)
+    flat = [p.data.view(torch.uint8).reshape(-1) for p, _ in dplan.host_payloads]
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    o = 0
+    for f in flat:
+        dst[o:o + f.numel()].copy_(f, non_blocking=True)
+        o += f.numel()
+    b.record()
+    torch.cuda.synchronize()
+    load_ms = a.elapsed_time(b)
+    del ws, dst
+    return {"workload": "config2 with all 10 HIT chunk-caches in pinned host memory",
+            "layerwise_preload_ms": round(statistics.mean(ms), 3),
+            "tokens_per_s": round(n_prompt / (statistics.mean(ms) / 1e3), 1),
+            "preload_depth_Lp": depth, "host_bytes": int(host_bytes),
+            "h2d_gbs_calibrated": round(rate / 1e9, 1),
+            "serial_load_ms": round(load_ms, 3)}
+
+
 def time_decode(cc, model, req, steps, peaks):
     """Greedy decode of `steps` tokens continuing the fix-up prefill
     (engine.DecodeSession: per-token GEMVs + split-KV attention, no host
@@ -648,6 +698,12 @@ def main():
     if args.decode_steps > 0 and not tp_mode:
         decode = time_decode(cc, model, req, args.decode_steps, peaks)
 
+    tiers_leg = None
+    if args.tiers and not tp_mode:
+        tiers_leg = time_tiers(cc, model, req, max(3, args.steps // 2), n_prompt)
+        tiers_leg["all_hbm_ms"] = round(ms_step, 3)
+        tiers_leg["serial_ms"] = round(tiers_leg["serial_load_ms"] + ms_step, 3)
+
     # ---- baselines on the same GPU --------------------------------------------
     baselines = {}
     if not args.no_baselines:
@@ -731,6 +787,8 @@ def main():
         line["recompute_sweep"] = sweep
     if decode:
         line["decode"] = decode
+    if tiers_leg:
+        line["tiers"] = tiers_leg
     print(json.dumps(line), flush=True)
 
 

@@ -140,9 +140,12 @@ __global__ void __launch_bounds__(DA_KEYS) decode_attn_partial(const __nv_bfloat
   for (int h = 0; h < G; ++h) sc[h] = 0.f;
   if (valid) {
     const uint4* kr = reinterpret_cast<const uint4*>(K + (int64_t)j * kvw + g * DA_DH);
-#pragma unroll 4
+    uint4 kv16[DA_DH / 8];
+#pragma unroll
+    for (int u = 0; u < DA_DH / 8; ++u) kv16[u] = kr[u];  // 16 independent 16-byte loads
+#pragma unroll
     for (int u = 0; u < DA_DH / 8; ++u) {
-      const uint4 kk = kr[u];
+      const uint4 kk = kv16[u];
       const __nv_bfloat162* kb = reinterpret_cast<const __nv_bfloat162*>(&kk);
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
@@ -178,22 +181,52 @@ __global__ void __launch_bounds__(DA_KEYS) decode_attn_partial(const __nv_bfloat
     if (lane == 0) ml_s[h] = make_float2(m, l);
   }
   __syncthreads();
-  // P.V: thread t = output column t
-  float o[G];
+  // P.V: thread t = (column group cg = t & 15: 8 columns, key group kg = t >> 4:
+  // keys kg, kg + 8, ...) -> 16 independent 16-byte V loads per thread; the 8
+  // key-group partials are folded through smem in a fixed order
+  const int cg = t & 15, kg = t >> 4;
+  float o[G][8];
 #pragma unroll
-  for (int h = 0; h < G; ++h) o[h] = 0.f;
+  for (int h = 0; h < G; ++h)
+#pragma unroll
+    for (int e = 0; e < 8; ++e) o[h][e] = 0.f;
   const int jn = min(DA_KEYS, n_keys - c * DA_KEYS);
-  const __nv_bfloat16* vcol = V + (int64_t)c * DA_KEYS * kvw + g * DA_DH + t;
-#pragma unroll 4
-  for (int jj = 0; jj < jn; ++jj) {
-    const float vv = __bfloat162float(vcol[(int64_t)jj * kvw]);
+  const __nv_bfloat16* vbase = V + (int64_t)c * DA_KEYS * kvw + g * DA_DH + cg * 8;
+  uint4 vv[DA_KEYS / 8];
 #pragma unroll
-    for (int h = 0; h < G; ++h) o[h] = fmaf(ps[h][jj], vv, o[h]);
+  for (int u = 0; u < DA_KEYS / 8; ++u) {
+    const int jj = kg + 8 * u;
+    vv[u] = jj < jn ? *reinterpret_cast<const uint4*>(vbase + (int64_t)jj * kvw) : make_uint4(0, 0, 0, 0);
   }
 #pragma unroll
+  for (int u = 0; u < DA_KEYS / 8; ++u) {
+    const int jj = kg + 8 * u;
+    const __nv_bfloat162* vb = reinterpret_cast<const __nv_bfloat162*>(&vv[u]);
+#pragma unroll
+    for (int h = 0; h < G; ++h) {
+      const float p = ps[h][jj];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 vf = __bfloat1622float2(vb[e]);
+        o[h][2 * e] = fmaf(p, vf.x, o[h][2 * e]);
+        o[h][2 * e + 1] = fmaf(p, vf.y, o[h][2 * e + 1]);
+      }
+    }
+  }
+  __syncthreads();  // ps no longer needed: reuse as [8 key groups][G][128] partials? (too small) -> red below
+  __shared__ float red[8][G][DA_DH];
+#pragma unroll
+  for (int h = 0; h < G; ++h)
+#pragma unroll
+    for (int e = 0; e < 8; ++e) red[kg][h][cg * 8 + e] = o[h][e];
+  __syncthreads();
+#pragma unroll
   for (int h = 0; h < G; ++h) {
+    float acc = 0.f;
+#pragma unroll
+    for (int k2 = 0; k2 < 8; ++k2) acc += red[k2][h][t];
     const int head = g * G + h;
-    part_o[((int64_t)c * Hq + head) * DA_DH + t] = o[h];
+    part_o[((int64_t)c * Hq + head) * DA_DH + t] = acc;
     if (t == 0) part_ml[(int64_t)c * Hq + head] = ml_s[h];
   }
 }

@@ -213,11 +213,23 @@ class _Payload:
 class Model:
     """Weights resident on the GPU (K-major [out, in] layout) + the KV pool."""
 
+    def copy_stream(self):
+        """Side stream of the layer-wise host-tier preload (created once)."""
+        import torch
+
+        if self._copy_stream is None:
+            self._copy_stream = torch.cuda.Stream(device=self.device)
+        return self._copy_stream
+
     def __init__(self, config: ModelConfig, weights: dict, device, host_weights: dict | None = None, tp=None):
         import torch
 
         self.config = config
         self.tp = tp  # parallel.TPContext or None
+        # host -> HBM copy-engine rate used for the preload depth (tiers.py);
+        # tiers.calibrate_h2d measures it on this box
+        self.h2d_bytes_per_s = 50e9
+        self._copy_stream = None
         if tp is not None and tp.world > 1:
             from .parallel import local_config
 
@@ -445,11 +457,17 @@ class ChunkCache:
         if self._keys is None and _payload is None:
             raise ShapeError("ChunkCache needs keys/values or a device payload")
 
-    # reference fields materialise lazily from HBM
+    # reference fields materialise lazily from HBM (or the host / disk tier)
+    def _rows(self, kv: int):
+        p = self._payload
+        if getattr(p, "tier", None) == "disk":
+            p = self._payload = p.load()
+        return p.all_rows(kv)
+
     @property
     def keys(self) -> list:
         if self._keys is None:
-            self._keys = _host_layers(self._payload.all_rows(0))
+            self._keys = _host_layers(self._rows(0))
         return self._keys
 
     @keys.setter
@@ -460,7 +478,7 @@ class ChunkCache:
     @property
     def values(self) -> list:
         if self._values is None:
-            self._values = _host_layers(self._payload.all_rows(1))
+            self._values = _host_layers(self._rows(1))
         return self._values
 
     @values.setter
@@ -481,13 +499,13 @@ class ChunkCache:
     @property
     def n_layers(self) -> int:
         if self._payload is not None:
-            return self._payload.pool.L
+            return self._payload.pool.L if hasattr(self._payload, "pool") else self._payload.L
         return len(self._keys)
 
     @property
     def width(self) -> int:
         if self._payload is not None:
-            return self._payload.pool.kvw
+            return self._payload.pool.kvw if hasattr(self._payload, "pool") else self._payload.kvw
         return self._keys[0].shape[1]
 
     def copy(self) -> "ChunkCache":
@@ -508,8 +526,14 @@ class ChunkCache:
         import torch
 
         p = self._payload
-        if p is not None and p.pool is model.pool:
+        if p is not None and getattr(p, "pool", None) is model.pool:
             return p
+        tier = getattr(p, "tier", None)
+        if tier == "disk":  # asynchronous read started by tiers.TieredPool.prefetch (or now)
+            p = self._payload = p.load()
+            tier = "host"
+        if tier == "host" and p.L == model.kcfg.n_layers and p.kvw == model.kcfg.kv_width():
+            return p  # gathered layer by layer through the copy engine (engine.execute)
         keys, values = self.keys, self.values
         if model.tp is not None and model.tp.world > 1 and keys[0].shape[1] == model.config.kv_width():
             cols = model.tp.slices.kv_cols(model.config.head_dim())

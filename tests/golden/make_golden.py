@@ -312,10 +312,45 @@ def gen_decode():
     _save("decode_toy.npz", **out)
 
 
+def gen_tiers():
+    # tiers.py:62-71 preload_depth and :209-261 place_and_migrate
+    # (tests/test_tiers.py idioms: f_r bands, byte budgets, spill)
+    from cachecraft import tiers as T
+
+    depth = []
+    for L in (1, 2, 5, 32, 80):
+        for tp, tl in ((1.0, 2.0), (2.0, 1.0), (1.0, 1.0), (0.3, 0.9), (0.49, 0.38), (1e-3, 5.0)):
+            depth.append({"L": L, "tp": tp, "tl": tl, "depth": T.preload_depth(L, tp, tl)})
+    store = cc.VariantStore(cc.StoreConfig(max_chunks=8, variants_per_chunk=3))
+    r = np.random.default_rng(17)
+    vids = []
+    for i in range(12):
+        n = int(r.integers(8, 40))
+        keys = [np.zeros((n, 8)) for _ in range(2)]
+        cache = cc.ChunkCache(keys=keys, values=[k.copy() for k in keys], n_tokens=n)
+        vid = store.insert(f"c{i % 7}", prefix=cc.PrefixContext((f"p{i}",), (1.0,)), a_bar=0.1, b_bar=0.1,
+                           cci=0.5, token_scores=np.zeros(n), cache=cache)
+        vids.append(vid)
+        for _ in range(int(r.integers(0, 4))):
+            store.touch(vid, float(r.uniform(0.05, 1.0)))
+    variants = list(store._by_id.values())
+    meta = [{"variant_id": v.variant_id, "f_r": v.f_r, "created_at": v.created_at, "bytes": v.payload_bytes()}
+            for v in variants]
+    cases = []
+    for fracs, caps in (((0.25, 0.5, None), (None, None, None)), ((0.5, None), (20000, None)),
+                        ((0.2, 0.3, None), (6000, 30000, None))):
+        tiers = tuple(T.Tier(name=nm, bandwidth=bw, capacity_bytes=cp, placement_fraction=fr)
+                      for nm, bw, cp, fr in zip(("hbm", "host", "disk"), (3e12, 5e10, 5e9), caps, fracs))
+        cfg = T.TierConfig(tiers=tiers, n_layers=4, t_prefill_layer=1e-3)
+        cases.append({"fractions": list(fracs), "capacities": list(caps),
+                      "placement": {str(k): v for k, v in T.place_and_migrate(variants, cfg).items()}})
+    _json("tiers.json", {"depth": depth, "variants": meta, "placement": cases})
+
+
 if __name__ == "__main__":
     only = os.environ.get("GEN_ONLY")
     gens = [gen_rope, gen_select, gen_scoring, gen_hash, gen_weights, gen_toy_prefill, gen_stats, gen_config1,
-            gen_plan, gen_replay, gen_decode]
+            gen_plan, gen_replay, gen_decode, gen_tiers]
     for g in gens:
         if not only or g.__name__ == "gen_" + only:
             g()
