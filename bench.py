@@ -430,7 +430,10 @@ def time_decode(cc, model, req, steps, peaks):
     sess.run(h)
     b.record()
     torch.cuda.synchronize()
-    ms = a.elapsed_time(b)
+    if sess.replay_events is not None:  # steady state: graph replays of steps 1..n-1
+        ms = sess.replay_events[0].elapsed_time(sess.replay_events[1]) * steps / (steps - 1)
+    else:
+        ms = a.elapsed_time(b)
     toks = sess.tokens[:steps].cpu().numpy().tolist()
     cfg = model.kcfg
     w_bytes = sum(t.numel() * t.element_size() for lw in model.w["layers"] for t in lw.values() if t is not None)

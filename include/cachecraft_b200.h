@@ -178,6 +178,12 @@ CC_API int cc_add_f32(float* dst, const float* src, int64_t n, void* stream);
 
 /* ---- decode continuation (model.py:445-484) ---------------------------- */
 
+/* Launch the decode-chain kernels (cc_gemv*, cc_decode_attention*,
+ * cc_rope_scatter_qkv, cc_embed_rows, cc_logits_argmax, cc_decode_advance)
+ * with programmatic dependent launch: each kernel's independent prologue
+ * overlaps its predecessor.  Process-wide; returns the previous setting. */
+CC_API int cc_set_pdl(int on);
+
 /* Weight-streaming projection for 1..4 rows (the per-token QKV / o / MLP
  * products of decode, model.py:461-476): C[M,N] (+)= epi(A[M,K] W[N,K]^T),
  * bf16 A/W, same epilogues and C types as cc_gemm (which routes bf16 M <= 4
@@ -186,6 +192,12 @@ CC_API int cc_add_f32(float* dst, const float* src, int64_t n, void* stream);
 CC_API int cc_gemv(const void* A, int64_t lda, const void* W, int64_t ldw, void* C, int64_t ldc, int M, int N,
                    int K, int epilogue, void* stream);
 
+/* cc_gemv with the weighted RMSNorm of the f32 residual rows fused into the
+ * prologue (model.py:121-122, eps as cc_rmsnorm, norm_w may be NULL):
+ * C = epi(bf16(rmsnorm(hidden)) W^T).  Decode: replaces rmsnorm + gemv. */
+CC_API int cc_gemv_rmsnorm(const float* hidden, int64_t ld_hidden, const float* norm_w, double eps, const void* W,
+                           int64_t ldw, void* C, int64_t ldc, int M, int N, int K, int epilogue, void* stream);
+
 /* Attention of ONE new query row over all n_keys keys (model.py:467-474: the
  * decode token sees every valid key incl. its own), bf16, d_head 128,
  * split-KV over 128-key chunks with a fixed-order combine (deterministic).
@@ -193,6 +205,18 @@ CC_API int cc_gemv(const void* A, int64_t lda, const void* W, int64_t ldw, void*
  * (kv.valid false).  Writes ctx [Hq*dh] and lse [Hq] (as cc_attention). */
 CC_API int cc_decode_attention(const void* q, const void* k_rot, const void* v, const uint8_t* key_pad, void* ctx,
                                float* lse, int n_keys, int n_heads, int n_kv_heads, int d_head, void* stream);
+
+/* cc_decode_attention with the key count read from device memory
+ * (*n_keys_dev <= max_keys) so one captured CUDA graph replays every decode
+ * step; the grid is sized for max_keys and idle chunks exit. */
+CC_API int cc_decode_attention_dev(const void* q, const void* k_rot, const void* v, const uint8_t* key_pad,
+                                   void* ctx, float* lse, const int32_t* n_keys_dev, int max_keys, int n_heads,
+                                   int n_kv_heads, int d_head, void* stream);
+
+/* Decode step bookkeeping on the device (model.py:455-483 loop state):
+ * tokens[state[0]] = *cur_token, then state[0..3] (count, slot, position,
+ * live keys) += 1. */
+CC_API int cc_decode_advance(int32_t* state, const int32_t* cur_token, int32_t* tokens, void* stream);
 
 /* y[r] = RoPE(x[r], positions[r % n]) for n_rows rows of `width` (= heads x
  * d_head) (rpe.py:19-44 apply_rpe; decode rotates the stored position-free

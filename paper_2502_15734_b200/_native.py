@@ -50,6 +50,10 @@ _SIGS = {
     "cc_gemv": ([_vp, _i64, _vp, _i64, _vp, _i64, _i32, _i32, _i32, _i32, _vp], _i32),
     "cc_decode_attention": ([_vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _vp], _i32),
     "cc_rope_rows": ([_vp, _vp, _i64, _i32, _i32, _vp, _vp, _i32, _i32, _vp], _i32),
+    "cc_decode_attention_dev": ([_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _vp], _i32),
+    "cc_decode_advance": ([_vp, _vp, _vp, _vp], _i32),
+    "cc_set_pdl": ([_i32], _i32),
+    "cc_gemv_rmsnorm": ([_vp, _i64, _vp, _f64, _vp, _i64, _vp, _i64, _i32, _i32, _i32, _i32, _vp], _i32),
 }
 
 _lib = None
@@ -104,7 +108,7 @@ def call(name: str, *args):
     # cc_logits_argmax with an argmax output runs GEMV + two argmax stages;
     # cc_decode_attention runs the split-KV partials + the combine
     kernels_launched += 3 if (name == "cc_logits_argmax" and args[5] is not None) else (
-        2 if name == "cc_decode_attention" else 1)
+        2 if name in ("cc_decode_attention", "cc_decode_attention_dev") else 1)
     check(rc, name)
     return rc
 

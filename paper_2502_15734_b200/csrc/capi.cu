@@ -11,6 +11,8 @@ static thread_local std::string g_last_error;
 
 void set_error(const std::string& msg) { g_last_error = msg; }
 
+int g_pdl = 0;
+
 int fail(int code, const std::string& msg) {
   g_last_error = msg;
   return code;
@@ -61,6 +63,12 @@ int num_sms() {
 extern "C" {
 
 int cc_abi_version(void) { return CC_ABI_VERSION; }
+
+int cc_set_pdl(int on) {
+  const int prev = ccb::g_pdl;
+  ccb::g_pdl = on ? 1 : 0;
+  return prev;
+}
 
 const char* cc_last_error(void) { return ccb::g_last_error.c_str(); }
 

@@ -71,4 +71,33 @@ inline size_t dtype_size(int dtype) { return dtype == CC_F64 ? 8 : (dtype == CC_
 int num_sms();
 void* stream_scratch(cudaStream_t st, int tag, size_t bytes);
 
+// ---- programmatic dependent launch (PDL) ------------------------------------
+// Kernels of the decode chain call pdl_trigger() first (the next kernel may be
+// scheduled now) and pdl_wait() before reading anything a predecessor wrote;
+// their independent prologue (weight streaming) overlaps the predecessor's
+// tail.  Both are no-ops for a kernel launched without the PDL attribute.
+extern int g_pdl;  // cc_set_pdl
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+int launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, const char* what,
+             Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  if (g_pdl) {
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+  }
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+  if (e != cudaSuccess) return fail(CC_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  return 0;
+}
+
 }  // namespace ccb

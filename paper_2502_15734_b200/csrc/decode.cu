@@ -10,6 +10,8 @@
 //                       (rpe.py:19-44), once per decode session
 #include <math.h>
 
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace ccb {
@@ -40,36 +42,80 @@ constexpr int GV_WARPS = 8;
 
 // C[M, N] (+)= epi(A[M, K] W[N, K]^T); SwiGLU: W rows in 64-row gate/up groups,
 // output column o = silu(gate row) * up row (N/2 outputs)
-template <int EPI>
-__global__ void __launch_bounds__(GV_WARPS * 32) gemv_kernel(const __nv_bfloat16* __restrict__ A, int64_t lda,
+// NORM: A is the f32 residual stream; the prologue applies the weighted
+// RMSNorm (model.py:121-122) and stages bf16(x * rsqrt(mean(x^2) + eps) * w)
+// -- the rmsnorm kernel fused away (decode: one launch less per projection)
+template <int EPI, bool NORM, int MR>
+__global__ void __launch_bounds__(GV_WARPS * 32) gemv_kernel(const void* __restrict__ A_, int64_t lda,
                                                              const __nv_bfloat16* __restrict__ W, int64_t ldw,
-                                                             void* __restrict__ C, int64_t ldc, int M, int N, int K) {
+                                                             void* __restrict__ C, int64_t ldc, int M, int N, int K,
+                                                             const float* __restrict__ norm_w, float eps) {
   extern __shared__ uint4 xs[];  // [M][K / 8] staged activations
   const int kv8 = K / 8;
-  for (int r = 0; r < M; ++r)
-    for (int i = threadIdx.x; i < kv8; i += blockDim.x)
-      xs[r * kv8 + i] = reinterpret_cast<const uint4*>(A + (int64_t)r * lda)[i];
-  __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr bool GLU = EPI == CC_EPI_SWIGLU;
+  constexpr int B = 4;  // 16-byte weight loads in flight per lane (x2 for SwiGLU)
   const int n_out = GLU ? N / 2 : N;
-  for (int o = blockIdx.x * GV_WARPS + warp; o < n_out; o += gridDim.x * GV_WARPS) {
+  auto wrows = [&](int o, const uint4*& wg, const uint4*& wu) {
     const int rg = GLU ? (o / 64) * 128 + (o % 64) : o;
-    const uint4* wg = reinterpret_cast<const uint4*>(W + (int64_t)rg * ldw);
-    const uint4* wu = reinterpret_cast<const uint4*>(W + (int64_t)(rg + 64) * ldw);
-    float ag[GV_MAXM] = {0.f, 0.f, 0.f, 0.f}, au[GV_MAXM] = {0.f, 0.f, 0.f, 0.f};
-    int i = lane;
-    for (; i + 96 < kv8; i += 128) {  // 4 independent 16-byte weight loads per lane (x2 for SwiGLU)
-      uint4 g4[4], u4[4];
+    wg = reinterpret_cast<const uint4*>(W + (int64_t)rg * ldw);
+    wu = reinterpret_cast<const uint4*>(W + (int64_t)(rg + 64) * ldw);
+  };
+  pdl_trigger();
+  pdl_wait();  // activations come from the predecessor
+  if constexpr (NORM) {
+    __shared__ float red[GV_WARPS];
+    __nv_bfloat16* xb = reinterpret_cast<__nv_bfloat16*>(xs);
+    for (int r = 0; r < M; ++r) {
+      const float4* x4 = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(A_) + (int64_t)r * lda);
+      float ss = 0.f;
+      for (int i = threadIdx.x; i < K / 4; i += blockDim.x) {
+        const float4 v = x4[i];
+        ss = fmaf(v.x, v.x, fmaf(v.y, v.y, fmaf(v.z, v.z, fmaf(v.w, v.w, ss))));
+      }
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
+      for (int off = 16; off > 0; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
+      if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+      __syncthreads();
+      float tot = 0.f;
+#pragma unroll
+      for (int w = 0; w < GV_WARPS; ++w) tot += red[w];
+      const float inv = rsqrtf(tot / (float)K + eps);
+      for (int i = threadIdx.x; i < K / 4; i += blockDim.x) {
+        const float4 v = x4[i];
+        float4 g = norm_w != nullptr ? reinterpret_cast<const float4*>(norm_w)[i] : make_float4(1.f, 1.f, 1.f, 1.f);
+        __nv_bfloat162 a = __floats2bfloat162_rn(v.x * inv * g.x, v.y * inv * g.y);
+        __nv_bfloat162 b = __floats2bfloat162_rn(v.z * inv * g.z, v.w * inv * g.w);
+        *reinterpret_cast<uint2*>(xb + (int64_t)r * K + 4 * i) =
+            make_uint2(*reinterpret_cast<uint32_t*>(&a), *reinterpret_cast<uint32_t*>(&b));
+      }
+      __syncthreads();
+    }
+  } else {
+    const __nv_bfloat16* A = reinterpret_cast<const __nv_bfloat16*>(A_);
+    for (int r = 0; r < M; ++r)
+      for (int i = threadIdx.x; i < kv8; i += blockDim.x)
+        xs[r * kv8 + i] = reinterpret_cast<const uint4*>(A + (int64_t)r * lda)[i];
+    __syncthreads();
+  }
+  for (int o = blockIdx.x * GV_WARPS + warp; o < n_out; o += gridDim.x * GV_WARPS) {
+    const uint4 *wg, *wu;
+    wrows(o, wg, wu);
+    float ag[MR], au[MR];
+#pragma unroll
+    for (int r = 0; r < MR; ++r) ag[r] = au[r] = 0.f;
+    int i = lane;
+    for (; i + 32 * (B - 1) < kv8; i += 32 * B) {  // B independent 16-byte weight loads per lane
+      uint4 g4[B], u4[B];
+#pragma unroll
+      for (int j = 0; j < B; ++j) {
         g4[j] = ld_stream16(wg + i + 32 * j);
         if (GLU) u4[j] = ld_stream16(wu + i + 32 * j);
       }
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
+      for (int j = 0; j < B; ++j)
 #pragma unroll
-        for (int r = 0; r < GV_MAXM; ++r)
+        for (int r = 0; r < MR; ++r)
           if (r < M) {
             const uint4 x = xs[r * kv8 + i + 32 * j];
             ag[r] += dot8(g4[j], x);
@@ -81,7 +127,7 @@ __global__ void __launch_bounds__(GV_WARPS * 32) gemv_kernel(const __nv_bfloat16
       uint4 u1;
       if (GLU) u1 = ld_stream16(wu + i);
 #pragma unroll
-      for (int r = 0; r < GV_MAXM; ++r)
+      for (int r = 0; r < MR; ++r)
         if (r < M) {
           const uint4 x = xs[r * kv8 + i];
           ag[r] += dot8(g1, x);
@@ -89,7 +135,7 @@ __global__ void __launch_bounds__(GV_WARPS * 32) gemv_kernel(const __nv_bfloat16
         }
     }
 #pragma unroll
-    for (int r = 0; r < GV_MAXM; ++r) {
+    for (int r = 0; r < MR; ++r) {
       if (r >= M) break;
       float g = ag[r], u = au[r];
 #pragma unroll
@@ -115,6 +161,7 @@ __global__ void __launch_bounds__(GV_WARPS * 32) gemv_kernel(const __nv_bfloat16
 constexpr int DA_KEYS = 128;  // keys per CTA (one per thread)
 constexpr int DA_DH = 128;
 constexpr int DA_MAXG = 8;
+constexpr int DA_COMBINE_MAX = 4096;  // chunks of 128 keys: 512k keys
 
 // grid (Hkv, n_chunks); thread t owns key j = chunk * 128 + t for the scores
 // and output column t for P.V.  Partials: o [chunk][Hq][DH] (unnormalised),
@@ -125,7 +172,12 @@ __global__ void __launch_bounds__(DA_KEYS) decode_attn_partial(const __nv_bfloat
                                                                const __nv_bfloat16* __restrict__ V,
                                                                const uint8_t* __restrict__ key_pad,
                                                                float* __restrict__ part_o, float2* __restrict__ part_ml,
-                                                               int n_keys, int Hq, int Hkv, float scale_log2) {
+                                                               int n_keys, const int32_t* __restrict__ n_keys_dev,
+                                                               int Hq, int Hkv, float scale_log2) {
+  pdl_trigger();
+  pdl_wait();
+  if (n_keys_dev != nullptr) n_keys = *n_keys_dev;  // CUDA-graph replay: key count lives on the device
+  if ((int)blockIdx.y * DA_KEYS >= n_keys) return;   // chunk beyond the live keys (grid sized for capacity)
   __shared__ float qs[G][DA_DH];
   __shared__ float ps[G][DA_KEYS];
   __shared__ float2 ml_s[G];
@@ -133,6 +185,17 @@ __global__ void __launch_bounds__(DA_KEYS) decode_attn_partial(const __nv_bfloat
   const int kvw = Hkv * DA_DH;
   for (int i = t; i < G * DA_DH; i += DA_KEYS) qs[i / DA_DH][i % DA_DH] = __bfloat162float(q[(int64_t)g * G * DA_DH + i]);
   __syncthreads();
+  // V rows of this thread's P.V role are loaded up front so their latency
+  // overlaps the K loads and the score math (thread = 8 columns x 16 keys)
+  const int cg = t & 15, kg = t >> 4;
+  const int jn = min(DA_KEYS, n_keys - c * DA_KEYS);
+  const __nv_bfloat16* vbase = V + (int64_t)c * DA_KEYS * kvw + g * DA_DH + cg * 8;
+  uint4 vv[DA_KEYS / 8];
+#pragma unroll
+  for (int u = 0; u < DA_KEYS / 8; ++u) {
+    const int jj = kg + 8 * u;
+    vv[u] = jj < jn ? *reinterpret_cast<const uint4*>(vbase + (int64_t)jj * kvw) : make_uint4(0, 0, 0, 0);
+  }
   const int j = c * DA_KEYS + t;
   const bool valid = j < n_keys && (key_pad == nullptr || key_pad[j] == 0);
   float sc[G];
@@ -184,20 +247,11 @@ __global__ void __launch_bounds__(DA_KEYS) decode_attn_partial(const __nv_bfloat
   // P.V: thread t = (column group cg = t & 15: 8 columns, key group kg = t >> 4:
   // keys kg, kg + 8, ...) -> 16 independent 16-byte V loads per thread; the 8
   // key-group partials are folded through smem in a fixed order
-  const int cg = t & 15, kg = t >> 4;
   float o[G][8];
 #pragma unroll
   for (int h = 0; h < G; ++h)
 #pragma unroll
     for (int e = 0; e < 8; ++e) o[h][e] = 0.f;
-  const int jn = min(DA_KEYS, n_keys - c * DA_KEYS);
-  const __nv_bfloat16* vbase = V + (int64_t)c * DA_KEYS * kvw + g * DA_DH + cg * 8;
-  uint4 vv[DA_KEYS / 8];
-#pragma unroll
-  for (int u = 0; u < DA_KEYS / 8; ++u) {
-    const int jj = kg + 8 * u;
-    vv[u] = jj < jn ? *reinterpret_cast<const uint4*>(vbase + (int64_t)jj * kvw) : make_uint4(0, 0, 0, 0);
-  }
 #pragma unroll
   for (int u = 0; u < DA_KEYS / 8; ++u) {
     const int jj = kg + 8 * u;
@@ -234,20 +288,43 @@ __global__ void __launch_bounds__(DA_KEYS) decode_attn_partial(const __nv_bfloat
 // grid Hq, 128 threads: fold the chunks in index order
 __global__ void __launch_bounds__(DA_DH) decode_attn_combine(const float* __restrict__ part_o,
                                                              const float2* __restrict__ part_ml, int n_chunks, int Hq,
-                                                             __nv_bfloat16* __restrict__ ctx, float* __restrict__ lse) {
+                                                             __nv_bfloat16* __restrict__ ctx, float* __restrict__ lse,
+                                                             const int32_t* __restrict__ n_keys_dev) {
   const int head = blockIdx.x, t = threadIdx.x;
-  float m = -INFINITY;
-  for (int c = 0; c < n_chunks; ++c) m = fmaxf(m, part_ml[(int64_t)c * Hq + head].x);
-  float l = 0.f, o = 0.f;
-  if (m != -INFINITY) {
-    for (int c = 0; c < n_chunks; ++c) {
+  pdl_trigger();
+  pdl_wait();
+  if (n_keys_dev != nullptr) n_chunks = (*n_keys_dev + DA_KEYS - 1) / DA_KEYS;
+  __shared__ float w_s[DA_COMBINE_MAX];
+  __shared__ float ml_red[2];
+  // warp 0: global max and the chunk weights 2^(m_c - m), sum l (fixed order)
+  if (t < 32) {
+    float m = -INFINITY;
+    for (int c = t; c < n_chunks; c += 32) m = fmaxf(m, part_ml[(int64_t)c * Hq + head].x);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
+    float l = 0.f;
+    for (int c = t; c < n_chunks; c += 32) {
       const float2 ml = part_ml[(int64_t)c * Hq + head];
-      if (ml.x == -INFINITY) continue;
-      const float w = exp2f(ml.x - m);
+      const float w = (m == -INFINITY || ml.x == -INFINITY) ? 0.f : exp2f(ml.x - m);
+      w_s[c] = w;
       l = fmaf(ml.y, w, l);
-      o = fmaf(part_o[((int64_t)c * Hq + head) * DA_DH + t], w, o);
     }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) l += __shfl_xor_sync(0xffffffffu, l, off);
+    if (t == 0) { ml_red[0] = m; ml_red[1] = l; }
   }
+  __syncthreads();
+  const float m = ml_red[0], l = ml_red[1];
+  float o0 = 0.f, o1 = 0.f, o2 = 0.f, o3 = 0.f;  // 4 independent chains
+  int c = 0;
+  for (; c + 3 < n_chunks; c += 4) {
+    o0 = fmaf(part_o[((int64_t)c * Hq + head) * DA_DH + t], w_s[c], o0);
+    o1 = fmaf(part_o[((int64_t)(c + 1) * Hq + head) * DA_DH + t], w_s[c + 1], o1);
+    o2 = fmaf(part_o[((int64_t)(c + 2) * Hq + head) * DA_DH + t], w_s[c + 2], o2);
+    o3 = fmaf(part_o[((int64_t)(c + 3) * Hq + head) * DA_DH + t], w_s[c + 3], o3);
+  }
+  for (; c < n_chunks; ++c) o0 = fmaf(part_o[((int64_t)c * Hq + head) * DA_DH + t], w_s[c], o0);
+  const float o = (o0 + o1) + (o2 + o3);
   ctx[(int64_t)head * DA_DH + t] = __float2bfloat16_rn(l > 0.f ? o / l : 0.f);
   if (t == 0 && lse != nullptr) lse[head] = l > 0.f ? (m + log2f(l)) * 0.6931471805599453f : -INFINITY;
 }
@@ -287,31 +364,44 @@ bool gemv_eligible(int M, int N, int K, int epi, const void* A, int64_t lda, con
   return ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(W)) & 15) == 0;
 }
 
-int gemv_bf16(const void* A, int64_t lda, const void* W, int64_t ldw, void* C, int64_t ldc, int M, int N, int K,
-              int epi, cudaStream_t st) {
+int gemv_launch(const void* A, int64_t lda, const void* W, int64_t ldw, void* C, int64_t ldc, int M, int N, int K,
+                int epi, const float* norm_w, float eps, bool norm, cudaStream_t st) {
   const int n_out = epi == CC_EPI_SWIGLU ? N / 2 : N;
   const size_t smem = (size_t)M * K * 2;
   int grid = (n_out + GV_WARPS - 1) / GV_WARPS;
-  static bool attr = false;  // (the four instantiations share one function-pointer type)
+  static bool attr = false;  // (the instantiations share one function-pointer type)
   if (!attr) {
-    cudaFuncSetAttribute(gemv_kernel<CC_EPI_STORE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
-    cudaFuncSetAttribute(gemv_kernel<CC_EPI_RESID_ADD>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
-    cudaFuncSetAttribute(gemv_kernel<CC_EPI_SWIGLU>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
-    cudaFuncSetAttribute(gemv_kernel<CC_EPI_GELU>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+    auto set = [](auto k) { cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024); };
+#define CCB_GV_SET(E) set(gemv_kernel<E, false, 1>); set(gemv_kernel<E, true, 1>); \
+    set(gemv_kernel<E, false, GV_MAXM>); set(gemv_kernel<E, true, GV_MAXM>);
+    CCB_GV_SET(CC_EPI_STORE) CCB_GV_SET(CC_EPI_RESID_ADD) CCB_GV_SET(CC_EPI_SWIGLU) CCB_GV_SET(CC_EPI_GELU)
+#undef CCB_GV_SET
     attr = true;
   }
   auto go = [&](auto kern) {
-    kern<<<grid, GV_WARPS * 32, smem, st>>>((const __nv_bfloat16*)A, lda, (const __nv_bfloat16*)W, ldw, C, ldc, M, N,
-                                            K);
-    return check_launch("gemv");
+    return launch_k(kern, dim3(grid), dim3(GV_WARPS * 32), smem, st, "gemv", A, lda, (const __nv_bfloat16*)W, ldw,
+                    C, ldc, M, N, K, norm_w, eps);
+  };
+  auto by_rows = [&](auto e_tag, auto n_tag) -> int {
+    constexpr int E = decltype(e_tag)::value;
+    constexpr bool NM = decltype(n_tag)::value;
+    return M == 1 ? go(gemv_kernel<E, NM, 1>) : go(gemv_kernel<E, NM, GV_MAXM>);
+  };
+  auto by_norm = [&](auto e_tag) -> int {
+    return norm ? by_rows(e_tag, std::true_type{}) : by_rows(e_tag, std::false_type{});
   };
   switch (epi) {
-    case CC_EPI_STORE: return go(gemv_kernel<CC_EPI_STORE>);
-    case CC_EPI_RESID_ADD: return go(gemv_kernel<CC_EPI_RESID_ADD>);
-    case CC_EPI_SWIGLU: return go(gemv_kernel<CC_EPI_SWIGLU>);
-    case CC_EPI_GELU: return go(gemv_kernel<CC_EPI_GELU>);
+    case CC_EPI_STORE: return by_norm(std::integral_constant<int, CC_EPI_STORE>{});
+    case CC_EPI_RESID_ADD: return by_norm(std::integral_constant<int, CC_EPI_RESID_ADD>{});
+    case CC_EPI_SWIGLU: return by_norm(std::integral_constant<int, CC_EPI_SWIGLU>{});
+    case CC_EPI_GELU: return by_norm(std::integral_constant<int, CC_EPI_GELU>{});
     default: return fail(CC_E_ARG, "gemv: unknown epilogue");
   }
+}
+
+int gemv_bf16(const void* A, int64_t lda, const void* W, int64_t ldw, void* C, int64_t ldc, int M, int N, int K,
+              int epi, cudaStream_t st) {
+  return gemv_launch(A, lda, W, ldw, C, ldc, M, N, K, epi, nullptr, 0.f, false, st);
 }
 
 }  // namespace ccb
@@ -327,13 +417,16 @@ extern "C" int cc_gemv(const void* A, int64_t lda, const void* W, int64_t ldw, v
   return gemv_bf16(A, lda, W, ldw, C, ldc, M, N, K, epilogue, as_stream(stream));
 }
 
-extern "C" int cc_decode_attention(const void* q, const void* k_rot, const void* v, const uint8_t* key_pad, void* ctx,
-                                   float* lse, int n_keys, int n_heads, int n_kv_heads, int d_head, void* stream) {
+namespace ccb {
+namespace {
+int decode_attention_impl(const void* q, const void* k_rot, const void* v, const uint8_t* key_pad, void* ctx,
+                          float* lse, int n_keys, const int32_t* n_keys_dev, int n_heads, int n_kv_heads, int d_head,
+                          cudaStream_t st) {
   CCB_REQUIRE(n_keys >= 1 && n_heads >= 1 && n_kv_heads >= 1 && n_heads % n_kv_heads == 0, "decode_attention: bad shape");
+  CCB_REQUIRE(n_keys <= DA_COMBINE_MAX * DA_KEYS, "decode_attention: more than 512k keys");
   if (d_head != DA_DH) return fail(CC_E_UNSUP, "decode_attention: d_head must be 128");
   const int G = n_heads / n_kv_heads;
   const int n_chunks = (n_keys + DA_KEYS - 1) / DA_KEYS;
-  cudaStream_t st = as_stream(stream);
   const size_t bytes = (size_t)n_chunks * n_heads * (DA_DH * sizeof(float) + sizeof(float2));
   uint8_t* scratch = (uint8_t*)stream_scratch(st, 2, bytes);
   if (!scratch) return fail(CC_E_CUDA, "decode_attention: scratch allocation failed");
@@ -342,9 +435,9 @@ extern "C" int cc_decode_attention(const void* q, const void* k_rot, const void*
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)d_head);
   dim3 grid(n_kv_heads, n_chunks);
   auto go = [&](auto kern) {
-    kern<<<grid, DA_KEYS, 0, st>>>((const __nv_bfloat16*)q, (const __nv_bfloat16*)k_rot, (const __nv_bfloat16*)v,
-                                   key_pad, part_o, part_ml, n_keys, n_heads, n_kv_heads, scale_log2);
-    return check_launch("decode_attention");
+    return launch_k(kern, grid, dim3(DA_KEYS), 0, st, "decode_attention", (const __nv_bfloat16*)q,
+                    (const __nv_bfloat16*)k_rot, (const __nv_bfloat16*)v, key_pad, part_o, part_ml, n_keys,
+                    n_keys_dev, n_heads, n_kv_heads, scale_log2);
   };
   int rc;
   switch (G) {
@@ -355,8 +448,55 @@ extern "C" int cc_decode_attention(const void* q, const void* k_rot, const void*
     default: return fail(CC_E_UNSUP, "decode_attention: GQA group must be 1, 2, 4 or 8");
   }
   if (rc) return rc;
-  decode_attn_combine<<<n_heads, DA_DH, 0, st>>>(part_o, part_ml, n_chunks, n_heads, (__nv_bfloat16*)ctx, lse);
-  return check_launch("decode_attention_combine");
+  return launch_k(decode_attn_combine, dim3(n_heads), dim3(DA_DH), 0, st, "decode_attention_combine",
+                  (const float*)part_o, (const float2*)part_ml, n_chunks, n_heads, (__nv_bfloat16*)ctx, lse,
+                  n_keys_dev);
+}
+
+// one decode step's bookkeeping on the device (graph-replayable):
+// tokens[state[0]] = *cur_tok; state[0]++ (count); state[1]++ (slot);
+// state[2]++ (position); state[3]++ (live keys)
+__global__ void decode_advance_kernel(int32_t* state, const int32_t* cur_tok, int32_t* tokens) {
+  pdl_trigger();
+  pdl_wait();
+  tokens[state[0]] = *cur_tok;
+  state[0] += 1;
+  state[1] += 1;
+  state[2] += 1;
+  state[3] += 1;
+}
+}  // namespace
+}  // namespace ccb
+
+extern "C" int cc_gemv_rmsnorm(const float* hidden, int64_t ld_hidden, const float* norm_w, double eps,
+                               const void* W, int64_t ldw, void* C, int64_t ldc, int M, int N, int K, int epilogue,
+                               void* stream) {
+  CCB_REQUIRE(M >= 0 && N > 0 && K > 0, "gemv_rmsnorm: bad shape");
+  if (M == 0) return 0;
+  if (!gemv_eligible(M, N, K, epilogue, W, ldw, W, ldw) || K % 4 || ld_hidden % 4 ||
+      (reinterpret_cast<uintptr_t>(hidden) & 15) || (reinterpret_cast<uintptr_t>(norm_w) & 15))
+    return fail(CC_E_UNSUP, "gemv_rmsnorm: needs 1..4 rows, K % 8 == 0, 16-byte aligned rows, M*K*2 <= 96 KiB");
+  return gemv_launch(hidden, ld_hidden, W, ldw, C, ldc, M, N, K, epilogue, norm_w, (float)eps, true,
+                     as_stream(stream));
+}
+
+extern "C" int cc_decode_attention(const void* q, const void* k_rot, const void* v, const uint8_t* key_pad, void* ctx,
+                                   float* lse, int n_keys, int n_heads, int n_kv_heads, int d_head, void* stream) {
+  return decode_attention_impl(q, k_rot, v, key_pad, ctx, lse, n_keys, nullptr, n_heads, n_kv_heads, d_head,
+                               as_stream(stream));
+}
+
+extern "C" int cc_decode_attention_dev(const void* q, const void* k_rot, const void* v, const uint8_t* key_pad,
+                                       void* ctx, float* lse, const int32_t* n_keys_dev, int max_keys, int n_heads,
+                                       int n_kv_heads, int d_head, void* stream) {
+  CCB_REQUIRE(n_keys_dev != nullptr, "decode_attention_dev: needs the device key count");
+  return decode_attention_impl(q, k_rot, v, key_pad, ctx, lse, max_keys, n_keys_dev, n_heads, n_kv_heads, d_head,
+                               as_stream(stream));
+}
+
+extern "C" int cc_decode_advance(int32_t* state, const int32_t* cur_token, int32_t* tokens, void* stream) {
+  return launch_k(decode_advance_kernel, dim3(1), dim3(1), 0, as_stream(stream), "decode_advance", state,
+                  cur_token, tokens);
 }
 
 extern "C" int cc_rope_rows(const void* x, void* y, int64_t n_rows, int n, int width, const int32_t* positions,

@@ -156,6 +156,8 @@ __global__ void __launch_bounds__(128) rope_scatter_kernel(
     const int32_t* __restrict__ row_pos, const typename CS<T>::type* __restrict__ table,
     T* __restrict__ q_rot, T* __restrict__ kv_k, T* __restrict__ kv_v, T* __restrict__ k_rot,
     int Hq, int Hkv, int dh) {
+  pdl_trigger();
+  pdl_wait();
   using A = typename Acc<T>::type;
   using VT = Vec<T, V>;
   const int r = blockIdx.x;
@@ -209,6 +211,8 @@ __global__ void __launch_bounds__(128) rope_scatter_kernel(
 template <typename T>
 __global__ void embed_kernel(const T* __restrict__ embed, const int32_t* __restrict__ tok,
                              typename Acc<T>::type* __restrict__ hidden, int d) {
+  pdl_trigger();
+  pdl_wait();
   using A = typename Acc<T>::type;
   const T* src = embed + (int64_t)tok[blockIdx.x] * d;
   A* dst = hidden + (int64_t)blockIdx.x * d;
@@ -295,6 +299,8 @@ __global__ void __launch_bounds__(256) logits_kernel(const typename Acc<T>::type
                                                      const float* __restrict__ w, double eps,
                                                      const T* __restrict__ U, typename Acc<T>::type* __restrict__ logits,
                                                      int m, int d, int vocab) {
+  pdl_trigger();
+  pdl_wait();
   using A = typename Acc<T>::type;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   A* xs = reinterpret_cast<A*>(smem_raw);  // [m][d] normed rows
@@ -368,6 +374,8 @@ __global__ void __launch_bounds__(256) logits_kernel(const typename Acc<T>::type
 template <typename A>
 __global__ void __launch_bounds__(1024) argmax_kernel(const A* __restrict__ logits, int32_t* __restrict__ out, int vocab,
                                                       A* __restrict__ part_v, int32_t* __restrict__ part_i, int n_part) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ A bv[32];
   __shared__ int bi[32];
   A best = -INFINITY;
@@ -626,10 +634,9 @@ int cc_rope_scatter_qkv(const void* qkv, int64_t ld_qkv, int n_rows, const int32
   return CCB_DISPATCH_DTYPE(dtype, T, [&] {
     int vec = std::min(pick_vec<T>(d_head / 2), pick_vec<T>((int)ld_qkv));
     return CCB_DISPATCH_VEC(vec, V, [&] {
-      rope_scatter_kernel<T, V><<<n_rows, 128, 0, as_stream(stream)>>>(
-          (const T*)qkv, ld_qkv, row_slot, row_pos, (const typename CS<T>::type*)rope_table, (T*)q_rot,
-          (T*)kv_k, (T*)kv_v, (T*)k_rot, n_heads, n_kv_heads, d_head);
-      return check_launch("rope_scatter_qkv");
+      return launch_k(rope_scatter_kernel<T, V>, dim3(n_rows), dim3(128), 0, as_stream(stream), "rope_scatter_qkv",
+                      (const T*)qkv, ld_qkv, row_slot, row_pos, (const typename CS<T>::type*)rope_table, (T*)q_rot,
+                      (T*)kv_k, (T*)kv_v, (T*)k_rot, n_heads, n_kv_heads, d_head);
     });
   });
 }
@@ -637,9 +644,8 @@ int cc_rope_scatter_qkv(const void* qkv, int64_t ld_qkv, int n_rows, const int32
 int cc_embed_rows(const void* embed, const int32_t* tokens, void* hidden, int n_rows, int d, int dtype, void* stream) {
   if (n_rows == 0) return 0;
   return CCB_DISPATCH_DTYPE(dtype, T, [&] {
-    embed_kernel<T><<<n_rows, 256, 0, as_stream(stream)>>>((const T*)embed, tokens,
-                                                          (typename Acc<T>::type*)hidden, d);
-    return check_launch("embed_rows");
+    return launch_k(embed_kernel<T>, dim3(n_rows), dim3(256), 0, as_stream(stream), "embed_rows", (const T*)embed,
+                    tokens, (typename Acc<T>::type*)hidden, d);
   });
 }
 
@@ -686,9 +692,8 @@ int cc_logits_argmax(const void* hidden_rows, const float* norm_w, double eps, c
     if (smem > 48 * 1024)
       cudaFuncSetAttribute(logits_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int grid = std::min((vocab + 7) / 8, num_sms() * 8);
-    logits_kernel<T><<<grid, 256, smem, as_stream(stream)>>>((const A*)hidden_rows, norm_w, eps,
-                                                            (const T*)unembed, (A*)logits, m, d, vocab);
-    int rc = check_launch("logits");
+    int rc = launch_k(logits_kernel<T>, dim3(grid), dim3(256), smem, as_stream(stream), "logits",
+                      (const A*)hidden_rows, norm_w, eps, (const T*)unembed, (A*)logits, m, d, vocab);
     if (rc) return rc;
     if (argmax) {
       // partials live after the logits rows in a small static scratch
@@ -697,11 +702,11 @@ int cc_logits_argmax(const void* hidden_rows, const float* norm_w, double eps, c
       if (!scratch) return fail(CC_E_CUDA, "logits_argmax: scratch allocation failed");
       A* part_v = reinterpret_cast<A*>(scratch);
       int32_t* part_i = reinterpret_cast<int32_t*>(scratch + sizeof(A) * 8 * PARTS);
-      argmax_kernel<A><<<dim3(m, PARTS), 1024, 0, as_stream(stream)>>>((const A*)logits, argmax, vocab, part_v, part_i, 0);
-      rc = check_launch("argmax_partial");
+      rc = launch_k(argmax_kernel<A>, dim3(m, PARTS), dim3(1024), 0, as_stream(stream), "argmax_partial",
+                    (const A*)logits, argmax, vocab, part_v, part_i, 0);
       if (rc) return rc;
-      argmax_kernel<A><<<m, 64, 0, as_stream(stream)>>>((const A*)logits, argmax, vocab, part_v, part_i, PARTS);
-      return check_launch("argmax");
+      return launch_k(argmax_kernel<A>, dim3(m), dim3(64), 0, as_stream(stream), "argmax", (const A*)logits, argmax,
+                      vocab, part_v, part_i, PARTS);
     }
     return 0;
   });

@@ -139,6 +139,27 @@ def test_gemv_epilogues_vs_torch(cc, M, epi):
     assert torch.equal(C, C2)
 
 
+@pytest.mark.parametrize("epi", ["store", "swiglu"])
+def test_gemv_rmsnorm_equals_rmsnorm_then_gemv(cc, epi):
+    N = cc._native
+    K, Nn = 4096, (1536 if epi == "store" else 2048)
+    g = torch.Generator(device="cuda").manual_seed(7)
+    h = torch.randn((1, K), generator=g, device="cuda") * 3
+    w = torch.rand((K,), generator=g, device="cuda") + 0.5
+    W = (torch.randn((Nn, K), generator=g, device="cuda") / K ** 0.5).bfloat16()
+    code = N.EPI_STORE if epi == "store" else N.EPI_SWIGLU
+    out_n = Nn if epi == "store" else Nn // 2
+    C = torch.empty((1, out_n), device="cuda", dtype=torch.bfloat16)
+    N.call("cc_gemv_rmsnorm", N.ptr(h), K, N.ptr(w), 1e-5, N.ptr(W), K, N.ptr(C), out_n, 1, Nn, K, code,
+           N.stream_ptr())
+    xn = (h * torch.rsqrt((h * h).mean(dim=1, keepdim=True) + 1e-5) * w).bfloat16()
+    acc = xn.float() @ W.float().T
+    if epi == "swiglu":
+        a4 = acc.reshape(1, Nn // 128, 2, 64)
+        acc = (torch.nn.functional.silu(a4[:, :, 0]) * a4[:, :, 1]).reshape(1, Nn // 2)
+    torch.testing.assert_close(C.float(), acc, atol=2e-2, rtol=2e-2)
+
+
 @pytest.mark.parametrize("n_keys,G,pads", [(1, 4, False), (300, 4, True), (5153, 4, False), (777, 1, True)])
 def test_decode_attention_vs_torch(cc, n_keys, G, pads):
     N = cc._native
