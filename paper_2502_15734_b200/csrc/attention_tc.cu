@@ -121,7 +121,8 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                    const __grid_constant__ CUtensorMap tmV, const int32_t* __restrict__ q_slot,
                    const uint8_t* __restrict__ key_pad, __nv_bfloat16* __restrict__ ctx, float* __restrict__ lse,
-                   int n_q, int n_keys, int Hq, int G, float scale_log2, long long* __restrict__ trace) {
+                   int n_q, int n_keys, int Hq, int G, float scale_log2, long long* __restrict__ trace,
+                   int split_min, float* __restrict__ ws_o, float2* __restrict__ ws_ml, int* __restrict__ counters) {
   using SM = AtSmem<DH>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* base = smem_raw;
@@ -186,7 +187,16 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const int kmax = s_kmax;
-  const int n_tiles = kmax < 0 ? 0 : kmax / AT_BN + 1;
+  const int n_total = kmax < 0 ? 0 : kmax / AT_BN + 1;
+  // split-KV for the long CTAs (rows near the end of the prompt see every key):
+  // CTA z of a split pair takes key tiles [t0, t0 + n_tiles); the pair's
+  // partials are merged by whichever finishes last, in z order (deterministic)
+  const int z = blockIdx.z;
+  const bool split = gridDim.z > 1 && n_total >= split_min;
+  const int half0 = (n_total + 1) / 2;
+  const int t0 = (split && z) ? half0 : 0;
+  const int n_tiles = split ? (z ? n_total - half0 : half0) : (z ? 0 : n_total);
+  const bool owner = split || z == 0;  // writes (part of) the output
   const uint32_t t_s0 = tmem, t_o = tmem + 256, t_p = tmem + 384;  // S0 S1 | O | P0 P1
   const bool tracing = trace != nullptr;
   long long w0 = 0, w1 = 0, w2 = 0, w3 = 0, t_loop = 0;  // per-role stall cycles (trace only)
@@ -207,7 +217,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
         mbar_expect_tx(&k_full[st], SM::KV_BYTES);
 #pragma unroll
         for (int a = 0; a < SM::ATOMS; ++a)
-          tma_load_2d(sK + st * SM::KV_BYTES + a * AT_BN * 128, &tmK, &k_full[st], g * DH + a * 64, i * AT_BN);
+          tma_load_2d(sK + st * SM::KV_BYTES + a * AT_BN * 128, &tmK, &k_full[st], g * DH + a * 64, (t0 + i) * AT_BN);
       };
       load_k(0);
       for (int i = 0; i < n_tiles; ++i) {
@@ -217,7 +227,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
         mbar_expect_tx(&v_full[st], SM::KV_BYTES);
 #pragma unroll
         for (int a = 0; a < SM::ATOMS; ++a)
-          tma_load_2d(sV + st * SM::KV_BYTES + a * AT_BN * 128, &tmV, &v_full[st], g * DH + a * 64, i * AT_BN);
+          tma_load_2d(sV + st * SM::KV_BYTES + a * AT_BN * 128, &tmV, &v_full[st], g * DH + a * 64, (t0 + i) * AT_BN);
       }
     }
   } else if (warp == 1) {
@@ -300,7 +310,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
       }
       tc_fence_before();
       mbar_arrive(&s_empty[b]);
-      const int j0 = i * AT_BN;
+      const int j0 = (t0 + i) * AT_BN;
       // keys j0 + 64h + c visible iff c <= lim_rel (causal + bounds) and not a pad
       const int lim_rel = min(lim, n_keys - 1) - j0 - 64 * h;
       if (key_pad != nullptr) {
@@ -405,8 +415,69 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
       mbar_wait(&p_empty[(n_tiles - 1) & 1], ((n_tiles - 1) >> 1) & 1);
       tc_fence_after();
     }
-    const float inv = l_tot > 0.f ? 1.f / l_tot : 0.f;
     __nv_bfloat16* out = ctx + ((int64_t)row * Hq + head) * DH + h * (DH / 2);
+    if (split) {
+      // park this half's partial (unnormalised O, max in log2 units, sum) ...
+      const int pair = g * gridDim.y + blockIdx.y;
+      const float m_l2 = (m_run == -INFINITY) ? -INFINITY : m_run * scale_log2;
+      float* my_o = ws_o + ((int64_t)(pair * 2 + z) * 128 + m) * DH + h * (DH / 2);
+#pragma unroll 1
+      for (int c = 0; c < DH / 64; ++c) {
+        uint32_t r[32];
+        tmem_ld32(t_o + h * (DH / 2) + c * 32 + lane_off, r);
+        tmem_ld_wait();
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+          __stcg(reinterpret_cast<float4*>(my_o + c * 32) + e,
+                 make_float4(__uint_as_float(r[4 * e]), __uint_as_float(r[4 * e + 1]), __uint_as_float(r[4 * e + 2]),
+                             __uint_as_float(r[4 * e + 3])));
+      }
+      if (h == 0) __stcg(&ws_ml[(int64_t)(pair * 2 + z) * 128 + m], make_float2(m_l2, l_tot));
+      __threadfence();
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      if (warp == 2 && lane == 0) {
+        const int prev = atomicAdd(&counters[pair], 1);
+        padw[0] = prev;  // (pad words are no longer needed)
+        if (prev == 1) counters[pair] = 0;  // reset for the next launch
+      }
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      if (padw[0] == 1) {
+        // ... and the last of the pair merges both, in z order
+        __threadfence();
+        const float2 ml0 = __ldcg(&ws_ml[(int64_t)(pair * 2) * 128 + m]);
+        const float2 ml1 = __ldcg(&ws_ml[(int64_t)(pair * 2 + 1) * 128 + m]);
+        const float M = fmaxf(ml0.x, ml1.x);
+        const float w0 = ml0.x == -INFINITY ? 0.f : exp2f(ml0.x - M);
+        const float w1 = ml1.x == -INFINITY ? 0.f : exp2f(ml1.x - M);
+        const float lt = fmaf(ml0.y, w0, ml1.y * w1);
+        const float inv = lt > 0.f ? 1.f / lt : 0.f;
+        const float* o0 = ws_o + ((int64_t)(pair * 2) * 128 + m) * DH + h * (DH / 2);
+        const float* o1 = ws_o + ((int64_t)(pair * 2 + 1) * 128 + m) * DH + h * (DH / 2);
+        if (row < n_q) {
+#pragma unroll 1
+          for (int c = 0; c < DH / 16; ++c) {
+            float4 a0 = __ldcg(reinterpret_cast<const float4*>(o0 + c * 8));
+            float4 a1 = __ldcg(reinterpret_cast<const float4*>(o0 + c * 8) + 1);
+            float4 b0 = __ldcg(reinterpret_cast<const float4*>(o1 + c * 8));
+            float4 b1 = __ldcg(reinterpret_cast<const float4*>(o1 + c * 8) + 1);
+            float v[8] = {fmaf(a0.x, w0, b0.x * w1), fmaf(a0.y, w0, b0.y * w1), fmaf(a0.z, w0, b0.z * w1),
+                          fmaf(a0.w, w0, b0.w * w1), fmaf(a1.x, w0, b1.x * w1), fmaf(a1.y, w0, b1.y * w1),
+                          fmaf(a1.z, w0, b1.z * w1), fmaf(a1.w, w0, b1.w * w1)};
+            uint4 pk;
+            uint32_t* pw = reinterpret_cast<uint32_t*>(&pk);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              __nv_bfloat162 hv = __floats2bfloat162_rn(v[2 * e] * inv, v[2 * e + 1] * inv);
+              pw[e] = *reinterpret_cast<uint32_t*>(&hv);
+            }
+            *reinterpret_cast<uint4*>(out + c * 8) = pk;
+          }
+          if (h == 0)
+            lse[(int64_t)row * Hq + head] = lt > 0.f ? (M + log2f(lt)) * 0.6931471805599453f : -INFINITY;
+        }
+      }
+    } else if (owner) {
+    const float inv = l_tot > 0.f ? 1.f / l_tot : 0.f;
 #pragma unroll 1
     for (int c = 0; c < DH / 64; ++c) {
       uint32_t r[32];
@@ -427,9 +498,10 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
     }
     if (row < n_q && h == 0)
       lse[(int64_t)row * Hq + head] = l_tot > 0.f ? (m_run * scale_log2 + log2f(l_tot)) * 0.6931471805599453f : -INFINITY;
+    }
   }
   if (tracing) {
-    long long* tr = trace + 16 * ((int64_t)blockIdx.y * gridDim.x + blockIdx.x);
+    long long* tr = trace + 16 * (((int64_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x);
     if (threadIdx.x == 64) {
       long long t_end;
       asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_end));
@@ -452,6 +524,26 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
 }
 
 long long* g_attn_trace = nullptr;  // debug: per-CTA (n_tiles, start, end, sm, stalls)
+
+// zero-initialised pair counters of the split-KV merge, one array per stream
+// (the merging CTA resets its counter, so they stay zero between launches)
+int* split_counters(cudaStream_t st, int n) {
+  static std::mutex mu;
+  static std::unordered_map<uint64_t, std::pair<int*, int>> by_stream;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t key = (reinterpret_cast<uint64_t>(st) << 4) ^ (uint64_t)dev;
+  std::lock_guard<std::mutex> g(mu);
+  auto& e = by_stream[key];
+  if (e.second < n) {
+    if (e.first) cudaFree(e.first);
+    const int cap = n < 4096 ? 4096 : n;
+    if (cudaMalloc(&e.first, sizeof(int) * cap) != cudaSuccess) { e = {nullptr, 0}; return nullptr; }
+    cudaMemset(e.first, 0, sizeof(int) * cap);
+    e.second = cap;
+  }
+  return e.first;
+}
 
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -509,10 +601,31 @@ int launch(const void* q, const void* k, const void* v, const int32_t* q_slot, c
     cudaFuncSetAttribute(attn_tc_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)AtSmem<DH>::TOTAL);
     attr = true;
   }
-  dim3 grid(Hkv, (n_q + R - 1) / R);
+  const int row_tiles = (n_q + R - 1) / R;
+  // split the key range of CTAs that see more than half of the longest range
+  // (>= 8 tiles) when the grid leaves SMs idle (fewer CTAs than SMs).  With a
+  // fuller grid the extra CTA prologues cost more than the better balance
+  // (measured at config 2: 208 CTAs, 74.6 -> 81.6 us per launch when split).
+  const int max_tiles = (n_keys + AT_BN - 1) / AT_BN;
+  const int split_min = max(8, (max_tiles + 1) / 2);
+  const bool do_split = max_tiles >= 8 && Hkv * row_tiles < num_sms();
+  float* ws_o = nullptr;
+  float2* ws_ml = nullptr;
+  int* counters = nullptr;
+  if (do_split) {
+    const size_t pairs = (size_t)Hkv * row_tiles;
+    const size_t bytes = pairs * 2 * 128 * (DH * sizeof(float) + sizeof(float2));
+    uint8_t* scratch = (uint8_t*)stream_scratch(st, 3, bytes);
+    counters = split_counters(st, (int)pairs);
+    if (!scratch || !counters) return fail(CC_E_CUDA, "attention_tc: split workspace allocation failed");
+    ws_o = reinterpret_cast<float*>(scratch);
+    ws_ml = reinterpret_cast<float2*>(scratch + pairs * 2 * 128 * DH * sizeof(float));
+  }
+  dim3 grid(Hkv, row_tiles, do_split ? 2 : 1);
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)DH);
   attn_tc_kernel<DH><<<grid, AT_THREADS, AtSmem<DH>::TOTAL, st>>>(mq, mk, mv, q_slot, key_pad, (__nv_bfloat16*)ctx,
-                                                                  lse, n_q, n_keys, Hq, G, scale_log2, g_attn_trace);
+                                                                  lse, n_q, n_keys, Hq, G, scale_log2, g_attn_trace,
+                                                                  split_min, ws_o, ws_ml, counters);
   return check_launch("attention_tc");
 }
 

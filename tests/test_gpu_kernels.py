@@ -172,9 +172,10 @@ def _attn_ref(q, k, v, q_slot, pad, Hq, Hkv):
 
 
 @pytest.mark.parametrize("Hq,Hkv,dh,n", [(32, 8, 128, 700), (4, 4, 64, 700), (8, 1, 128, 700), (16, 2, 64, 700),
-                                          (32, 8, 128, 2100), (64, 8, 128, 300)])
+                                          (32, 8, 128, 2100), (64, 8, 128, 300), (32, 8, 128, 5152)])
 def test_attention_scattered_rows(N, Hq, Hkv, dh, n):
-    """impl 1 = tcgen05/TMEM kernel, 3 = mma.sync kernel, 2 = SIMT."""
+    """impl 1 = tcgen05/TMEM kernel (key range split in two for the long row
+    tiles when n >= 1024, merged in fixed order), 3 = mma.sync kernel, 2 = SIMT."""
     g = torch.Generator(device="cuda").manual_seed(Hq + dh)
     rows = torch.sort(torch.randperm(n, generator=g, device="cuda")[:150]).values.int()
     q = torch.randn((rows.numel(), Hq, dh), generator=g, device="cuda").bfloat16()
@@ -195,6 +196,11 @@ def test_attention_scattered_rows(N, Hq, Hkv, dh, n):
         ref, ref_lse = _attn_ref(q, k, v, rows, pad, Hq, Hkv)
         torch.testing.assert_close(ctx.float(), ref, atol=3e-2, rtol=3e-2)
         torch.testing.assert_close(lse, ref_lse, atol=2e-3, rtol=1e-3)
+        if impl == 1:  # deterministic (split merge order fixed)
+            ctx2 = torch.empty_like(ctx)
+            N.call("cc_attention", N.ptr(q), N.ptr(k), N.ptr(v), N.ptr(rows), N.ptr(pad), N.ptr(ctx2), N.ptr(lse),
+                   rows.numel(), n, Hq, Hkv, dh, N.BF16, impl, N.stream_ptr())
+            assert torch.equal(ctx, ctx2)
 
 
 def test_gather_rope_matches_torch(N):
