@@ -63,6 +63,8 @@ def parse():
     p.add_argument("--sweep", action="store_true", help="also report the recompute-ratio sweep 0..50%%")
     p.add_argument("--no-baselines", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--tp-peer", type=int, default=0,
+                   help="70b TP: fused push-GEMM + peer-memory reduction instead of NCCL all-reduce")
     p.add_argument("--tiers", type=int, default=1, help="time the host-tier (f2) variant of the fix-up; 0 skips")
     p.add_argument("--decode-steps", type=int, default=32,
                    help="greedy decode tokens timed after the fix-up (SURVEY f3); 0 skips")
@@ -194,7 +196,13 @@ def make_workload(args, rank):
         cfg = cc.ModelConfig.llama3_70b(n_layers=args.layers, dtype="bf16", seed=0)
         world = int(os.environ.get("WORLD_SIZE", "1"))
         if world > 1:
-            tp = parallel.TPContext(parallel.tp_slices(cfg.n_heads, cfg.kv_heads(), cfg.ff_dim(), rank, world))
+            peer = None
+            if getattr(args, "tp_peer", 0):
+                # fused push-GEMM + peer-memory reduction over NVLink (CUDA IPC buffers)
+                m_cap = -(-int(args.chunks * args.chunk_len * 0.2 + args.question + 128) // 128) * 128
+                peer = parallel.PeerComm.over_ipc(rank, world, cfg.d_model, m_cap, torch.device("cuda", rank))
+            tp = parallel.TPContext(parallel.tp_slices(cfg.n_heads, cfg.kv_heads(), cfg.ff_dim(), rank, world),
+                                    peer=peer)
         model = cc.build_model(cfg, tp=tp)
         r = np.random.default_rng(1000)  # every TP rank serves the same request
     else:

@@ -172,6 +172,35 @@ CC_API int cc_extract_to_pool(const void* kv_k, const void* kv_v, int64_t req_la
                        int64_t pool_layer_stride, int64_t pool_block_stride, int kv_width, int dtype,
                        void* stream);
 
+/* ---- tensor parallel: o_proj / down_proj all-reduce over peer memory ---- */
+
+/* Symmetric buffers of every TP rank (device pointers valid in the calling
+ * process: same-process, P2P or CUDA-IPC mapped).  Rank r owns columns
+ * [r*slice, (r+1)*slice) of the d-wide partial outputs. */
+typedef struct {
+  float* recv[8];     /* rank r: [world][m_cap][slice] f32 partials pushed to r   */
+  int32_t* flags[8];  /* rank r: [world][tiles of r's slice] arrival stamps       */
+  float* sum[8];      /* rank r: [m_cap][d] f32 reduced sums                      */
+  int32_t* done[8];   /* rank r: monotonic count of reduced tiles written to sum  */
+  int32_t rank, world, slice, m_cap, epoch;
+} cc_tp_peers;
+
+/* C_partial = A[M,K] B[N=d,K]^T of this rank with the reduce-scatter fused
+ * into the tcgen05 GEMM epilogue: each 128xBN fp32 tile is stored straight
+ * into its column owner's recv slab (NVLink P2P stores) and stamped with
+ * tab->epoch as soon as it is produced (model.py:417, :419 reductions). */
+CC_API int cc_tp_push_gemm(const void* A, int64_t lda, const void* B, int64_t ldb, int M, int N, int K,
+                           const cc_tp_peers* tab, void* stream);
+/* Owner side: wait for every rank's stamp of each owned tile, sum the world
+ * partials in rank order (deterministic, identical on all ranks) and store
+ * the sum into every rank's `sum` (the all-gather), then bump their `done`. */
+CC_API int cc_tp_reduce(const cc_tp_peers* tab, int M, int N, void* stream);
+/* Stream-ordered wait until this rank's `done` counter reaches `target`. */
+CC_API int cc_tp_wait(const cc_tp_peers* tab, int64_t target, void* stream);
+/* CUDA IPC: 64-byte handle of a device allocation / map a peer's handle. */
+CC_API int cc_ipc_get_handle(const void* dev_ptr, void* handle64);
+CC_API int cc_ipc_open_handle(const void* handle64, void** dev_ptr);
+
 /* dst[i] += src[i] over n f32 elements (the residual add after a tensor-
  * parallel all-reduce of the o_proj / down_proj partial outputs). */
 CC_API int cc_add_f32(float* dst, const float* src, int64_t n, void* stream);

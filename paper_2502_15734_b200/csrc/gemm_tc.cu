@@ -150,7 +150,7 @@ template <int EPI, int TC_BN, bool SPLIT>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, void* C,
                    int64_t ldc, int M, int N, int K, int t_dp, long long W, float* __restrict__ ws,
-                   int* __restrict__ flags, int epoch, long long* __restrict__ trace) {
+                   int* __restrict__ flags, int epoch, long long* __restrict__ trace, const PeerTab peer) {
   constexpr int TC_B_BYTES = TcCfg<TC_BN>::B_BYTES;
   constexpr int TC_STAGES = TcCfg<TC_BN>::STAGES;
   constexpr int TMEM_COLS = TcCfg<TC_BN>::TMEM_COLS;
@@ -328,7 +328,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             transpose32(stg, r, lane, v);
           }
           const int col = n0 + c * 32 + c4 * 4;
-          if constexpr (EPI == CC_EPI_RESID_ADD) {
+          if constexpr (EPI == CC_EPI_PEER_PUSH) {
+            // reduce-scatter push: this rank's fp32 partial of the tile goes
+            // straight into the owner's receive slab over NVLink (P2P stores),
+            // tile by tile as the GEMM produces it
+            const int owner = n0 / peer.slice;
+            float* dst = peer.recv[owner] + ((int64_t)peer.rank * peer.m_cap + rb) * peer.slice + (col - owner * peer.slice);
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+              if (ok[i]) *reinterpret_cast<float4*>(dst + (int64_t)4 * i * peer.slice) = v[i];
+          } else if constexpr (EPI == CC_EPI_RESID_ADD) {
             float* h = reinterpret_cast<float*>(C) + (int64_t)rb * ldc + col;
             if (split && !last) {
               fold8(slot(blockIdx.x, c * 32), 4 * TC_BN, ok, v, false, true);
@@ -366,6 +375,19 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       }
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
+      if constexpr (EPI == CC_EPI_PEER_PUSH) {
+        // all 128 epilogue threads' stores are visible system-wide before the
+        // owner sees this tile's stamp
+        __threadfence_system();
+        epi_bar();
+        if (et == 0) {
+          const int owner = n0 / peer.slice;
+          const int per = peer.slice / TC_BN;
+          const int local = mt * per + (nt - owner * per);
+          int* f = peer.flags[owner] + (int64_t)peer.rank * (((M + TC_BM - 1) / TC_BM) * per) + local;
+          asm volatile("st.release.sys.global.b32 [%0], %1;" ::"l"(f), "r"(peer.epoch) : "memory");
+        }
+      }
       if (split && !last) {
         __threadfence();
         epi_bar();
@@ -508,10 +530,10 @@ int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, void* C, int64_t ldc
     }
     sc.epoch = (sc.epoch + 1) & 0x3fffffff;
     gemm_tc_kernel<EPI, BN, true><<<tl.grid, TC_THREADS, TcCfg<BN>::SMEM, st>>>(ma, mb, C, ldc, M, N, K, tl.t_dp,
-                                                                               tl.W, sc.ws, sc.flags, sc.epoch, g_trace);
+                                                                               tl.W, sc.ws, sc.flags, sc.epoch, g_trace, PeerTab{});
   } else {
     gemm_tc_kernel<EPI, BN, false><<<tl.grid, TC_THREADS, TcCfg<BN>::SMEM, st>>>(ma, mb, C, ldc, M, N, K, tiles, 0,
-                                                                                nullptr, nullptr, 0, g_trace);
+                                                                                nullptr, nullptr, 0, g_trace, PeerTab{});
   }
   return check_launch("gemm_tc");
 }
@@ -618,6 +640,33 @@ int launch_epi(const void* A, int64_t lda, const void* B, int64_t ldb, void* C, 
 }  // namespace
 
 void gemm_tc_set_trace(void* p) { g_trace = reinterpret_cast<long long*>(p); }
+
+// o_proj / down_proj of a tensor-parallel rank with the reduce-scatter fused
+// into the epilogue (data-parallel schedule; BN must divide the owner slice)
+int gemm_tc_peer_push(const void* A, int64_t lda, const void* B, int64_t ldb, int M, int N, int K,
+                      const PeerTab& tab, cudaStream_t st) {
+  if (N % 128 != 0 || K % TC_BK != 0 || lda % 8 != 0 || ldb % 8 != 0 || tab.slice % 128 != 0 || N != tab.slice * tab.world)
+    return fail(CC_E_UNSUP, "gemm_tc_peer_push: needs N = slice * world, slice % 128 == 0, K % 64 == 0");
+  const int bn = tab.slice % 256 == 0 ? 256 : 128;
+  CUtensorMap ma, mb;
+  int rc = make_map(&ma, A, M, K, lda, TC_BM);
+  if (rc) return rc;
+  rc = make_map(&mb, B, N, K, ldb, bn);
+  if (rc) return rc;
+  Tiling tl = plan_dp(M, N, bn);
+  auto go = [&](auto kern, size_t smem) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attr = true;
+    }
+    kern<<<tl.grid, TC_THREADS, smem, st>>>(ma, mb, nullptr, 0, M, N, K, tl.t_dp, 0LL, nullptr, nullptr, 0, g_trace,
+                                            tab);
+    return check_launch("gemm_tc_peer_push");
+  };
+  if (bn == 256) return go(gemm_tc_kernel<CC_EPI_PEER_PUSH, 256, false>, TcCfg<256>::SMEM);
+  return go(gemm_tc_kernel<CC_EPI_PEER_PUSH, 128, false>, TcCfg<128>::SMEM);
+}
 
 int gemm_tc_bf16(const void* A, int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc, int M, int N, int K,
                  int epi, bool allow_split, cudaStream_t st) {

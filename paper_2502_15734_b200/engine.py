@@ -488,8 +488,25 @@ def execute(model: Model, plan: DevicePlan, ws: dict, *, record=False, record_va
 
 def _tp_partial_gemm(model, tp, a, lda, w, hidden, part, n_l, d, k, dt, gemm_impl, s):
     """Row-parallel projection: partial = a_local @ W_local^T on this rank,
-    summed over the TP group (NCCL all-reduce), then hidden += sum."""
+    summed over the TP group, then hidden += sum.  bf16 with a PeerComm: the
+    reduce-scatter is fused into the GEMM epilogue (P2P pushes) and the owner
+    reduction + all-gather runs over peer memory (csrc/tp_peer.cu); otherwise
+    an NCCL all-reduce of the partial."""
+    import ctypes
+
     P = N.ptr
+    peer = getattr(tp, "peer", None)
+    if peer is not None and dt == N.BF16 and n_l <= peer.m_cap and d == peer.d:
+        peer.epoch += 1
+        tab = peer.table()
+        addr = ctypes.addressof(tab)
+        N.call("cc_tp_push_gemm", P(a), lda, P(w), lda, n_l, d, k, addr, s)
+        N.call("cc_tp_reduce", addr, n_l, d, s)
+        bn = 256 if peer.slice % 256 == 0 else 128
+        peer.done_target += (-(-n_l // 128)) * (d // bn)
+        N.call("cc_tp_wait", addr, peer.done_target, s)
+        N.call("cc_add_f32", P(hidden), P(peer.local["sum"]), n_l * d, s)
+        return
     if dt == N.F64:
         part[:n_l].zero_()
         N.call("cc_gemm", P(a), lda, P(w), lda, P(part), d, n_l, d, k, N.EPI_RESID_ADD, dt, gemm_impl, s)

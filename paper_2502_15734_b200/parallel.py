@@ -16,6 +16,7 @@ CPU tests (oracle + gloo) both use it.
 
 from __future__ import annotations
 
+import ctypes
 import hashlib
 from dataclasses import dataclass
 
@@ -115,15 +116,106 @@ def local_config(cfg, sl: TPSlices):
                    d_head=cfg.head_dim())
 
 
+class _Peers(ctypes.Structure):
+    """cc_tp_peers (include/cachecraft_b200.h)."""
+
+    _fields_ = [("recv", ctypes.c_void_p * 8), ("flags", ctypes.c_void_p * 8), ("sum", ctypes.c_void_p * 8),
+                ("done", ctypes.c_void_p * 8), ("rank", ctypes.c_int32), ("world", ctypes.c_int32),
+                ("slice", ctypes.c_int32), ("m_cap", ctypes.c_int32), ("epoch", ctypes.c_int32)]
+
+
+class PeerComm:
+    """One rank's view of the symmetric buffers of the fused TP reduction
+    (csrc/tp_peer.cu): the o_proj / down_proj GEMM pushes each fp32 tile of
+    its partial output into the column owner's ``recv`` slab over NVLink as it
+    is produced (reduce-scatter fused into the epilogue); the owner sums the
+    world's partials in rank order and stores the sum into every rank's
+    ``sum`` (all-gather); each rank waits on its ``done`` counter and adds
+    ``sum`` to its residual.  Replaces the NCCL all-reduce of those two
+    reductions (model.py:417, :419) — NCCL stays for the small K8 masses."""
+
+    def __init__(self, rank: int, world: int, d: int, m_cap: int, local: dict, ptrs: list):
+        self.rank, self.world, self.d, self.m_cap = rank, world, d, m_cap
+        self.slice = d // world
+        self.local = local  # this rank's tensors (kept alive)
+        self.ptrs = ptrs  # per rank: (recv, flags, sum, done) device pointers valid here
+        self.epoch = 0
+        self.done_target = 0
+
+    @staticmethod
+    def alloc(device, world: int, d: int, m_cap: int) -> dict:
+        import torch
+
+        slice_ = d // world
+        n_m = -(-m_cap // 128)
+        return {
+            "recv": torch.zeros((world, m_cap, slice_), dtype=torch.float32, device=device),
+            "flags": torch.full((world * n_m * (slice_ // 128) + 8,), -1, dtype=torch.int32, device=device),
+            "sum": torch.zeros((m_cap, d), dtype=torch.float32, device=device),
+            "done": torch.zeros((8,), dtype=torch.int32, device=device),
+        }
+
+    @classmethod
+    def in_process(cls, world: int, d: int, m_cap: int, device) -> list:
+        """All ranks' buffers in one process (tests; one GPU or P2P peers)."""
+        if d % world or (d // world) % 128:
+            raise ConfigError("peer TP needs d / world to be a multiple of 128")
+        bufs = [cls.alloc(device, world, d, m_cap) for _ in range(world)]
+        ptrs = [tuple(b[k].data_ptr() for k in ("recv", "flags", "sum", "done")) for b in bufs]
+        return [cls(r, world, d, m_cap, bufs[r], ptrs) for r in range(world)]
+
+    @classmethod
+    def over_ipc(cls, rank: int, world: int, d: int, m_cap: int, device, group=None) -> "PeerComm":
+        """One process per GPU: exchange CUDA-IPC handles of the symmetric
+        buffers over torch.distributed and map every peer's buffers."""
+        import torch.distributed as dist
+
+        from . import _native as N
+
+        if d % world or (d // world) % 128:
+            raise ConfigError("peer TP needs d / world to be a multiple of 128")
+        local = cls.alloc(device, world, d, m_cap)
+        mine = []
+        for k in ("recv", "flags", "sum", "done"):
+            h = ctypes.create_string_buffer(64)
+            N.check(N.lib().cc_ipc_get_handle(ctypes.c_void_p(local[k].data_ptr()), h), "cc_ipc_get_handle")
+            mine.append(h.raw)
+        allh = [None] * world
+        dist.all_gather_object(allh, mine, group=group)
+        ptrs = []
+        for r in range(world):
+            if r == rank:
+                ptrs.append(tuple(local[k].data_ptr() for k in ("recv", "flags", "sum", "done")))
+                continue
+            row = []
+            for raw in allh[r]:
+                out = ctypes.c_void_p()
+                N.check(N.lib().cc_ipc_open_handle(ctypes.create_string_buffer(raw, 64), ctypes.byref(out)),
+                        "cc_ipc_open_handle")
+                row.append(out.value)
+            ptrs.append(tuple(row))
+        return cls(rank, world, d, m_cap, local, ptrs)
+
+    def table(self) -> _Peers:
+        t = _Peers()
+        for r, (rv, fl, sm, dn) in enumerate(self.ptrs):
+            t.recv[r], t.flags[r], t.sum[r], t.done[r] = rv, fl, sm, dn
+        t.rank, t.world, t.slice, t.m_cap, t.epoch = self.rank, self.world, self.slice, self.m_cap, self.epoch
+        return t
+
+
 class TPContext:
     """What the engine needs to run one rank of a TP group: the slices and an
     all-reduce (sum, in place) over the group.  The default all-reduce is
-    torch.distributed (NCCL on GPUs); tests inject their own."""
+    torch.distributed (NCCL on GPUs); tests inject their own.  With ``peer``
+    (a PeerComm) the o_proj / down_proj reductions of bf16 runs use the
+    fused push GEMM + peer reduction instead."""
 
-    def __init__(self, slices: TPSlices, allreduce=None, group=None):
+    def __init__(self, slices: TPSlices, allreduce=None, group=None, peer: "PeerComm | None" = None):
         self.slices = slices
         self.group = group
         self._allreduce = allreduce
+        self.peer = peer
 
     @property
     def world(self) -> int:

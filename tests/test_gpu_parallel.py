@@ -93,3 +93,46 @@ def test_two_rank_tensor_parallel_matches_unsharded(dtype, tol):
         k = np.concatenate([results[0][1][l], results[1][1][l]], axis=1)
         err = np.linalg.norm(k - ref["keys"][l]) / np.linalg.norm(ref["keys"][l])
         assert err < tol
+
+
+def test_peer_push_gemm_and_reduction_two_ranks():
+    """Fused TP reduction (csrc/tp_peer.cu) with two ranks' buffers on one
+    GPU, driven from one thread (no cross-rank spin can wait on an unlaunched
+    peer): each rank's GEMM pushes its fp32 tiles into the column owner's
+    slab, the owners reduce in rank order and all-gather; both ranks must hold
+    the same bits, equal to the fp32 sum of the partials."""
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import ctypes
+
+    from paper_2502_15734_b200 import _native as N
+    from paper_2502_15734_b200 import parallel
+
+    N.lib()
+    world, d, k, M = 2, 512, 256, 200
+    comms = parallel.PeerComm.in_process(world, d, 256, "cuda")
+    g = torch.Generator(device="cuda").manual_seed(11)
+    A = [torch.randn((M, k), generator=g, device="cuda").bfloat16() for _ in range(world)]
+    B = [(torch.randn((d, k), generator=g, device="cuda") / k ** 0.5).bfloat16() for _ in range(world)]
+    streams = [torch.cuda.Stream() for _ in range(world)]
+    for step in range(2):  # two calls: epochs and the monotonic done counter advance
+        tabs = []
+        for r in range(world):
+            comms[r].epoch += 1
+            tabs.append(comms[r].table())
+        torch.cuda.synchronize()
+        for r in range(world):
+            N.call("cc_tp_push_gemm", N.ptr(A[r]), k, N.ptr(B[r]), k, M, d, k, ctypes.addressof(tabs[r]),
+                   streams[r].cuda_stream)
+        for r in range(world):
+            N.call("cc_tp_reduce", ctypes.addressof(tabs[r]), M, d, streams[r].cuda_stream)
+        for r in range(world):
+            comms[r].done_target += (-(-M // 128)) * (d // 256)
+            N.call("cc_tp_wait", ctypes.addressof(tabs[r]), comms[r].done_target, streams[r].cuda_stream)
+        torch.cuda.synchronize()
+        ref = sum(a.float() @ b.float().T for a, b in zip(A, B))
+        s0 = comms[0].local["sum"][:M]
+        s1 = comms[1].local["sum"][:M]
+        assert torch.equal(s0, s1)
+        torch.testing.assert_close(s0, ref, atol=1e-3, rtol=1e-3)
+        A = [a.flip(0).contiguous() for a in A]

@@ -118,3 +118,14 @@ def _timing_worker(rank, world):
 
 def test_bench_timing_is_max_over_ranks():
     _run(2, _timing_worker)
+
+
+def test_peer_table_matches_c_layout():
+    """parallel._Peers mirrors cc_tp_peers (include/cachecraft_b200.h):
+    4 x 8 pointers then rank, world, slice, m_cap, epoch (int32)."""
+    import ctypes
+
+    from paper_2502_15734_b200.parallel import _Peers
+
+    assert ctypes.sizeof(_Peers) == 4 * 8 * 8 + 5 * 4 + 4  # 8-byte aligned tail
+    assert _Peers.rank.offset == 256 and _Peers.epoch.offset == 272
