@@ -168,7 +168,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int num_m = (M + TC_BM - 1) / TC_BM;
-  const int num_tiles = num_m * (N / TC_BN);
+  const int num_tiles = num_m * ((N + TC_BN - 1) / TC_BN);  // last N tile may be ragged (TMA zero-fills)
   const int num_kb = K / TC_BK;
   if (!SPLIT) { t_dp = num_tiles; W = 0; }
 
@@ -320,6 +320,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       } else {
 #pragma unroll 1
         for (int c = 0; c < TC_BN / 32; ++c) {
+          if (n0 + c * 32 >= N) break;  // ragged last tile (N % 32 == 0)
           float4 v[8];
           {
             uint32_t r[32];
@@ -493,6 +494,8 @@ SplitScratch& scratch(cudaStream_t st) {
 
 long long* g_trace = nullptr;  // debug: per-CTA unit timeline (cc_gemm_set_trace)
 
+inline int n_tiles_of(int N, int bn) { return (N + bn - 1) / bn; }
+
 // Tiling plan: tile width, how many tiles run data-parallel, the stream-K
 // k-block total and the persistent grid.
 struct Tiling {
@@ -513,7 +516,7 @@ int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, void* C, int64_t ldc
                          (int)TcCfg<BN>::SMEM);
     attr_set = true;
   }
-  const int tiles = ((M + TC_BM - 1) / TC_BM) * (N / BN);
+  const int tiles = ((M + TC_BM - 1) / TC_BM) * n_tiles_of(N, BN);
   SplitScratch& sc = scratch(st);
   if (tl.W > 0) {
     if (sc.flag_elems < tl.grid) {
@@ -538,14 +541,22 @@ int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, void* C, int64_t ldc
   return check_launch("gemm_tc");
 }
 
-// relative time of one k-block of a 128xBN tile (measured, BN = 256 / 192 / 128)
-constexpr double kKbCost[3] = {1.0, 0.75 / 0.97, 0.5 / 0.88};
+// tile widths: any multiple of 32 <= 256 (ragged last N tile); a width that
+// makes the tile count fit the SM count removes most of the wave
+// quantisation of M ~ 800 GEMMs (N = 4096: 7 x 19 tiles of 224 = one wave)
+constexpr int kBnCand[5] = {256, 224, 192, 160, 128};
+// relative time of one k-block of a 128xBN tile (measured efficiency per width)
+inline double kb_cost(int bn) {
+  const double eff = bn >= 256 ? 1.0 : bn >= 224 ? 0.985 : bn >= 192 ? 0.97 : bn >= 160 ? 0.93 : 0.88;
+  return bn / 256.0 / eff;
+}
+
 // exposed cost of a CTA's final stream-K fold (read the partials, in 128x256 k-blocks)
 constexpr double kFoldCost = 4.0;
 
 Tiling plan_dp(int M, int N, int bn) {
   Tiling t;
-  const int tiles = ((M + TC_BM - 1) / TC_BM) * (N / bn);
+  const int tiles = ((M + TC_BM - 1) / TC_BM) * n_tiles_of(N, bn);
   t.bn = bn;
   t.t_dp = tiles;
   t.grid = tiles < num_sms() ? tiles : num_sms();
@@ -558,7 +569,7 @@ Tiling plan_dp(int M, int N, int bn) {
 Tiling plan_sk(int M, int N, int K, int bn) {
   Tiling t;
   const int sms = num_sms(), nkb = K / TC_BK;
-  const int tiles = ((M + TC_BM - 1) / TC_BM) * (N / bn);
+  const int tiles = ((M + TC_BM - 1) / TC_BM) * n_tiles_of(N, bn);
   const int full = tiles / sms;
   t.bn = bn;
   t.t_dp = full >= 2 ? (full - 1) * sms : 0;
@@ -572,12 +583,12 @@ Tiling plan_sk(int M, int N, int K, int bn) {
 
 double model_time(const Tiling& t, int M, int N, int K) {
   const int nkb = K / TC_BK;
-  const int ci = t.bn == 256 ? 0 : (t.bn == 192 ? 1 : 2);
-  const int tiles = ((M + TC_BM - 1) / TC_BM) * (N / t.bn);
-  if (t.W == 0) return (double)((tiles + t.grid - 1) / t.grid) * nkb * kKbCost[ci];
+  const double kc = kb_cost(t.bn);
+  const int tiles = ((M + TC_BM - 1) / TC_BM) * n_tiles_of(N, t.bn);
+  if (t.W == 0) return (double)((tiles + t.grid - 1) / t.grid) * nkb * kc;
   const double per = (double)((t.W + t.grid - 1) / t.grid);
   const bool splits = (t.W / t.grid) % nkb != 0 || t.W / t.grid < nkb;
-  return ((double)(t.t_dp / t.grid) * nkb + per) * kKbCost[ci] + (splits ? kFoldCost * t.bn / 256.0 : 0.0);
+  return ((double)(t.t_dp / t.grid) * nkb + per) * kc + (splits ? kFoldCost * t.bn / 256.0 : 0.0);
 }
 
 // the tiling minimising the modelled time.  Stream-K is considered where it
@@ -586,14 +597,12 @@ double model_time(const Tiling& t, int M, int N, int K) {
 // the data-parallel schedule wins: stream-K's scattered k offsets defeat the
 // L2 sharing of the weight tiles across a wave's M tiles.
 Tiling pick_tiling(int M, int N, int K, int epi, bool allow_split) {
-  const int cand[3] = {256, 192, 128};
   const int sms = num_sms(), nkb = K / TC_BK;
   Tiling best;
   double best_t = 1e30;
-  for (int i = 0; i < 3; ++i) {
-    const int bn = cand[i];
-    if (N % bn) continue;
-    if (epi == CC_EPI_SWIGLU && bn != 256) continue;
+  for (int i = 0; i < 5; ++i) {
+    const int bn = kBnCand[i];
+    if (epi == CC_EPI_SWIGLU && (bn != 256 || N % 256)) continue;  // gate|up 64-column groups pair up per tile
     Tiling dp = plan_dp(M, N, bn);
     double t = model_time(dp, M, N, K);
     if (t < best_t - 1e-9) { best_t = t; best = dp; }
@@ -616,7 +625,7 @@ bool forced_tiling(int M, int N, int K, int epi, Tiling* out) {
     init = true;
     if (const char* e = getenv("CCB_GEMM_FORCE")) sscanf(e, "%d,%d", &fb, &fs);
   }
-  if (fb <= 0 || N % fb || (epi == CC_EPI_SWIGLU && fb != 256)) return false;
+  if (fb <= 0 || fb % 32 || fb > 256 || (epi == CC_EPI_SWIGLU && fb != 256)) return false;
   *out = fs == 1 ? plan_sk(M, N, K, fb) : plan_dp(M, N, fb);
   return true;
 }
@@ -632,9 +641,14 @@ int launch_epi(const void* A, int64_t lda, const void* B, int64_t ldb, void* C, 
   if (rc) return rc;
   rc = make_map(&mb, B, N, K, ldb, tl.bn);
   if (rc) return rc;
-  if (tl.bn == 256) return launch_tc<EPI, 256>(ma, mb, C, ldc, M, N, K, tl, st);
-  if (tl.bn == 192) return launch_tc<EPI, 192>(ma, mb, C, ldc, M, N, K, tl, st);
-  return launch_tc<EPI, 128>(ma, mb, C, ldc, M, N, K, tl, st);
+  switch (tl.bn) {
+    case 256: return launch_tc<EPI, 256>(ma, mb, C, ldc, M, N, K, tl, st);
+    case 224: return launch_tc<EPI, 224>(ma, mb, C, ldc, M, N, K, tl, st);
+    case 192: return launch_tc<EPI, 192>(ma, mb, C, ldc, M, N, K, tl, st);
+    case 160: return launch_tc<EPI, 160>(ma, mb, C, ldc, M, N, K, tl, st);
+    case 128: return launch_tc<EPI, 128>(ma, mb, C, ldc, M, N, K, tl, st);
+    default: return fail(CC_E_UNSUP, "gemm_tc: unsupported tile width");
+  }
 }
 
 }  // namespace

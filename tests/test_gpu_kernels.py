@@ -109,6 +109,37 @@ def test_gemm_tcgen05_epilogues(N, epi):
         torch.testing.assert_close(out.float(), ref, atol=2e-2, rtol=2e-2)
 
 
+@pytest.mark.parametrize("bn", [224, 160])
+@pytest.mark.parametrize("epi", ["store", "resid"])
+def test_gemm_ragged_tile_width(N, bn, epi, monkeypatch):
+    """Tile widths that do not divide N (ragged last tile, TMA zero fill,
+    masked epilogue) match the fp32 reference."""
+    import subprocess
+    import sys
+
+    code = f"""
+import torch, sys
+sys.path.insert(0, '.')
+from paper_2502_15734_b200 import _native as N
+M, Nn, K = 802, 4096, 1024
+g = torch.Generator(device='cuda').manual_seed(2)
+A = torch.randn((M, K), generator=g, device='cuda').bfloat16()
+B = (torch.randn((Nn, K), generator=g, device='cuda') / 32).bfloat16()
+acc = A.float() @ B.float().T
+if '{epi}' == 'resid':
+    C = torch.ones((M, Nn), device='cuda'); ref = acc + 1
+    N.call('cc_gemm', N.ptr(A), K, N.ptr(B), K, N.ptr(C), Nn, M, Nn, K, N.EPI_RESID_ADD, N.BF16, 1, N.stream_ptr())
+else:
+    C = torch.empty((M, Nn), device='cuda', dtype=torch.bfloat16); ref = acc
+    N.call('cc_gemm', N.ptr(A), K, N.ptr(B), K, N.ptr(C), Nn, M, Nn, K, N.EPI_STORE, N.BF16, 1, N.stream_ptr())
+torch.testing.assert_close(C.float(), ref, atol=2e-2, rtol=2e-2)
+print('ok')
+"""
+    env = dict(__import__("os").environ, CCB_GEMM_FORCE=f"{bn},0")
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=300)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
+
+
 @pytest.mark.parametrize("Nn", [512, 6144, 1536])
 def test_gemm_tcgen05_m_invariance(N, Nn):
     """A row's result does not depend on how many rows are active (also when
