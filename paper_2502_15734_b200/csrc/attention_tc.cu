@@ -37,7 +37,8 @@ constexpr int AT_BN = 128;      // keys per tile
 // operand (tcgen05.mma ... [a-tmem]); this frees the smem P buffers and 64 KiB
 // of smem traffic per tile, so the K/V ring gets a third stage.
 constexpr bool kPTmem = true;
-constexpr int AT_STAGES = kPTmem ? 3 : 2;    // K/V ring depth
+constexpr int AT_KST = 3;  // K ring depth
+constexpr int AT_VST = 2;  // V ring depth = P buffers: V slot i % 2 is released by PV_i's p_empty commit
 constexpr int AT_THREADS = 320;  // TMA warp, MMA warp, 2 x 4 softmax warps
 
 // MN-major operand (B = V: N = head dim contiguous, K = keys), 128B swizzle:
@@ -107,8 +108,8 @@ struct AtSmem {
   static constexpr int P_BYTES = 128 * AT_BN * 2;    // one P tile, 2 atoms of 64 keys (x2 buffers)
   static constexpr int Q_OFF = 0;
   static constexpr int K_OFF = Q_OFF + Q_BYTES;
-  static constexpr int V_OFF = K_OFF + AT_STAGES * KV_BYTES;
-  static constexpr int P_OFF = V_OFF + AT_STAGES * KV_BYTES;
+  static constexpr int V_OFF = K_OFF + AT_KST * KV_BYTES;
+  static constexpr int P_OFF = V_OFF + AT_VST * KV_BYTES;
   static constexpr int BAR_OFF = P_OFF + (kPTmem ? 0 : 2 * P_BYTES);
   static constexpr int X_OFF = BAR_OFF + 256;        // [2 parities][2 halves][128 rows] f32 exchange
   // no alignment slack: the kernel holds no static shared memory, so the
@@ -133,11 +134,10 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
   uint8_t* sP = base + SM::P_OFF;
   uint64_t* bars = reinterpret_cast<uint64_t*>(base + SM::BAR_OFF);
   uint64_t* q_full = bars + 0;
-  uint64_t* k_full = bars + 1;                 // [AT_STAGES]
-  uint64_t* v_full = k_full + AT_STAGES;       // [AT_STAGES]
-  uint64_t* k_empty = v_full + AT_STAGES;      // [AT_STAGES]
-  uint64_t* v_empty = k_empty + AT_STAGES;     // [AT_STAGES]
-  uint64_t* s_full = v_empty + AT_STAGES;      // [2]
+  uint64_t* k_full = bars + 1;                 // [AT_KST]
+  uint64_t* k_empty = k_full + AT_KST;         // [AT_KST] arrived by the softmax once S_i landed
+  uint64_t* v_full = k_empty + AT_KST;         // [AT_VST]
+  uint64_t* s_full = v_full + AT_VST;          // [2]
   uint64_t* s_empty = s_full + 2;              // [2]
   uint64_t* p_full = s_empty + 2;              // [2]
   uint64_t* p_empty = p_full + 2;              // [2]
@@ -159,12 +159,11 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
     tma_prefetch(&tmK);
     tma_prefetch(&tmV);
     mbar_init(q_full, 1);
-    for (int s = 0; s < AT_STAGES; ++s) {
+    for (int s = 0; s < AT_KST; ++s) {
       mbar_init(&k_full[s], 1);
-      mbar_init(&v_full[s], 1);
       mbar_init(&k_empty[s], 1);
-      mbar_init(&v_empty[s], 1);
     }
+    for (int s = 0; s < AT_VST; ++s) mbar_init(&v_full[s], 1);
     for (int b = 0; b < 2; ++b) {
       mbar_init(&s_full[b], 1);
       mbar_init(&s_empty[b], 256);
@@ -200,6 +199,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
   const uint32_t t_s0 = tmem, t_o = tmem + 256, t_p = tmem + 384;  // S0 S1 | O | P0 P1
   const bool tracing = trace != nullptr;
   long long w0 = 0, w1 = 0, w2 = 0, w3 = 0, t_loop = 0;  // per-role stall cycles (trace only)
+  long long t_s_issue = 0, t_s_commit = 0, t_p_issue = 0, t_p_commit = 0;
   long long t_begin = 0;
   if (trace != nullptr && threadIdx.x == 64) asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_begin));
 
@@ -212,8 +212,8 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
       // (early), V_i's when PV_{i-2} is done, so neither S nor PV waits on a
       // load issued after the previous PV
       auto load_k = [&](int i) {
-        const int st = i % AT_STAGES;
-        twait(&k_empty[st], ((i / AT_STAGES) & 1) ^ 1, tracing, w0);
+        const int st = i % AT_KST;
+        twait(&k_empty[st], ((i / AT_KST) & 1) ^ 1, tracing, w0);
         mbar_expect_tx(&k_full[st], SM::KV_BYTES);
 #pragma unroll
         for (int a = 0; a < SM::ATOMS; ++a)
@@ -222,8 +222,8 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
       load_k(0);
       for (int i = 0; i < n_tiles; ++i) {
         if (i + 1 < n_tiles) load_k(i + 1);
-        const int st = i % AT_STAGES;
-        twait(&v_empty[st], ((i / AT_STAGES) & 1) ^ 1, tracing, w1);
+        const int st = i % AT_VST;  // == P buffer of tile i: free once PV_{i-2} completed
+        twait(&p_empty[st], ((i / AT_VST) & 1) ^ 1, tracing, w1);
         mbar_expect_tx(&v_full[st], SM::KV_BYTES);
 #pragma unroll
         for (int a = 0; a < SM::ATOMS; ++a)
@@ -236,10 +236,11 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
       constexpr uint32_t id_o = idesc_bf16(128, DH, true);
       mbar_wait(q_full, 0);
       auto issue_s = [&](int i) {
-        const int st = i % AT_STAGES, b = i & 1;
-        twait(&k_full[st], (i / AT_STAGES) & 1, tracing, w0);
+        const int st = i % AT_KST, b = i & 1;
+        twait(&k_full[st], (i / AT_KST) & 1, tracing, w0);
         twait(&s_empty[b], ((i >> 1) & 1) ^ 1, tracing, w1);
         tc_fence_after();
+        const long long ts0 = tracing ? clock64() : 0;
 #pragma unroll
         for (int kk = 0; kk < DH / 16; ++kk) {
           const int a = kk >> 2, w = kk & 3;
@@ -247,16 +248,18 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
           uint64_t bd = desc_sw128(sK + st * SM::KV_BYTES + a * AT_BN * 128) + 2 * w;
           mma_bf16(t_s0 + b * AT_BN, ad, bd, id_s, kk > 0);
         }
-        mma_commit(&s_full[b]);
-        mma_commit(&k_empty[st]);
+        const long long ts1 = tracing ? clock64() : 0;
+        mma_commit(&s_full[b]);  // (K slot released by the softmax when it sees s_full)
+        if (tracing) { t_s_issue += ts1 - ts0; t_s_commit += clock64() - ts1; }
       };
       issue_s(0);
       for (int i = 0; i < n_tiles; ++i) {
         if (i + 1 < n_tiles) issue_s(i + 1);
-        const int st = i % AT_STAGES, pb = i & 1;
+        const int st = i % AT_VST, pb = i & 1;
         twait(&p_full[pb], (i >> 1) & 1, tracing, w2);
-        twait(&v_full[st], (i / AT_STAGES) & 1, tracing, w3);
+        twait(&v_full[st], (i / AT_VST) & 1, tracing, w3);
         tc_fence_after();
+        const long long tp0 = tracing ? clock64() : 0;
         const uint8_t* sPb = sP + pb * SM::P_BYTES;
 #pragma unroll
         for (int kk = 0; kk < AT_BN / 16; ++kk) {
@@ -269,8 +272,9 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
             mma_bf16(t_o, ad, bd, id_o, (i > 0 || kk > 0) ? 1u : 0u);
           }
         }
-        mma_commit(&p_empty[pb]);
-        mma_commit(&v_empty[st]);
+        const long long tp1 = tracing ? clock64() : 0;
+        mma_commit(&p_empty[pb]);  // P buffer and V slot pb
+        if (tracing) { t_p_issue += tp1 - tp0; t_p_commit += clock64() - tp1; }
       }
     }
   } else {
@@ -295,6 +299,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
       const int b = i & 1;
       twait(&s_full[b], (i >> 1) & 1, tracing, w0);
       tc_fence_after();
+      if (warp == 2 && lane == 0) mbar_arrive(&k_empty[i % AT_KST]);  // S_i done: K_i's slot is free
       float s[64];
       {
         uint32_t r0[32], r1[32];
@@ -511,8 +516,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
       tr[4] = w0; tr[5] = w1; tr[6] = w2; tr[7] = w3;  // softmax: s_full, p_empty(i-2), p_empty(grow)
     } else if (threadIdx.x == 32) {
       tr[8] = w0; tr[9] = w1; tr[10] = w2; tr[11] = w3;  // mma: k_full, s_empty, p_full, v_full
-    } else if (threadIdx.x == 0) {
-      tr[12] = w0; tr[13] = w1;  // tma: k_empty, v_empty
+      tr[12] = t_s_issue; tr[13] = t_s_commit; tr[14] = t_p_issue; tr[15] = t_p_commit;
     }
   }
   tc_fence_before();

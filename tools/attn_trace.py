@@ -37,8 +37,9 @@ for s_, d_ in zip(sm, dur):
     load[s_] = load.get(s_, 0) + d_
 print(f"SMs used {len(load)}  busiest SM {max(load.values()):.1f} us  mean SM busy {np.mean(list(load.values())):.1f} us")
 big = t[:, 0] >= 20
-names = ["sm:s_full", "sm:p_empty2", "sm:p_empty1", "-", "mma:k_full", "mma:s_empty", "mma:p_full", "mma:v_full", "tma:k_empty", "tma:v_empty"]
-cols = [4, 5, 6, 7, 8, 9, 10, 11, 12, 13]
+names = ["sm:s_full", "sm:p_empty2", "sm:p_empty1", "-", "mma:k_full", "mma:s_empty", "mma:p_full", "mma:v_full",
+         "mma:S issue", "mma:S commit", "mma:PV issue", "mma:PV commit"]
+cols = [4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15]
 per = {n: np.median(t[big, c] / t[big, 0]) for n, c in zip(names, cols)}
 print("stall cycles per tile (CTAs with >= 20 tiles):", {k: int(v) for k, v in per.items()})
 print("cycles per tile (clock64 ~ 1.9 GHz):", int(np.median(dur[big] / t[big, 0]) * 1900))
