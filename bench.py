@@ -667,6 +667,7 @@ def main():
         peaks = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
 
     cc, model, store, chunks, question = make_workload(args, rank)
+    model.l2_prefetch = not os.environ.get("CCB_NO_L2PF")
     plan, req, dplan, ws = resident_plan(cc, model, store, chunks, question, args.ratio)
     n_prompt = req.n_tokens
     n_recomputed = plan.tokens_recomputed()

@@ -253,6 +253,11 @@ CC_API int cc_decode_advance(int32_t* state, const int32_t* cur_token, int32_t* 
 CC_API int cc_rope_rows(const void* x, void* y, int64_t n_rows, int n, int width, const int32_t* positions,
                         const void* rope_table, int d_head, int dtype, void* stream);
 
+/* Pull a read-only device range (the next projection's weights) into L2 on a
+ * side stream while the SMs run other work (engine: o_proj weights during
+ * attention). */
+CC_API int cc_prefetch_l2(const void* p, size_t bytes, void* stream);
+
 /* L2 flush helper for benchmarks: writes `bytes` of scratch. */
 CC_API int cc_flush_l2(void* scratch, size_t bytes, void* stream);
 

@@ -47,6 +47,7 @@ _SIGS = {
     "cc_extract_to_pool": ([_vp, _vp, _i64, _i32, _i32, _i32, _vp, _i32, _vp, _i64, _i64, _i32, _i32, _vp], _i32),
     "cc_add_f32": ([_vp, _vp, _i64, _vp], _i32),
     "cc_flush_l2": ([_vp, _sz, _vp], _i32),
+    "cc_prefetch_l2": ([_vp, _sz, _vp], _i32),
     "cc_gemv": ([_vp, _i64, _vp, _i64, _vp, _i64, _i32, _i32, _i32, _i32, _vp], _i32),
     "cc_decode_attention": ([_vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _vp], _i32),
     "cc_rope_rows": ([_vp, _vp, _i64, _i32, _i32, _vp, _vp, _i32, _i32, _vp], _i32),

@@ -572,6 +572,15 @@ __global__ void add_f32_kernel(float4* __restrict__ dst, const float4* __restric
   }
 }
 
+// pull a read-only range (the next GEMM's weights) into L2 while other work
+// runs; 128-byte lines, evict_last so the streaming GEMM operands do not
+// displace it first
+__global__ void __launch_bounds__(256) prefetch_l2_kernel(const char* __restrict__ p, size_t bytes) {
+  const size_t lines = (bytes + 127) / 128;
+  for (size_t l = blockIdx.x * (size_t)blockDim.x + threadIdx.x; l < lines; l += (size_t)gridDim.x * blockDim.x)
+    asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(p + l * 128));
+}
+
 __global__ void flush_kernel(int4* p, size_t n, int seed) {
   for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
     p[i] = make_int4(seed, (int)i, seed, (int)i);
@@ -759,6 +768,12 @@ int cc_add_f32(float* dst, const float* src, int64_t n, void* stream) {
   const int grid = (int)std::min<int64_t>((n4 + 255) / 256, (int64_t)num_sms() * 8);
   add_f32_kernel<<<grid, 256, 0, as_stream(stream)>>>((float4*)dst, (const float4*)src, n4);
   return check_launch("add_f32");
+}
+
+int cc_prefetch_l2(const void* p, size_t bytes, void* stream) {
+  if (bytes == 0) return 0;
+  prefetch_l2_kernel<<<32, 256, 0, as_stream(stream)>>>(reinterpret_cast<const char*>(p), bytes);
+  return check_launch("prefetch_l2");
 }
 
 int cc_flush_l2(void* scratch, size_t bytes, void* stream) {

@@ -230,6 +230,7 @@ class Model:
         # tiers.calibrate_h2d measures it on this box
         self.h2d_bytes_per_s = 50e9
         self._copy_stream = None
+        self.l2_prefetch = False  # o_proj weights -> L2 during attention: measured -1% (noise level), off
         if tp is not None and tp.world > 1:
             from .parallel import local_config
 
