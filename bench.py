@@ -686,6 +686,7 @@ def main():
     summ = timer.summary()
 
     # ---- e2e: public API with host buffers ----------------------------------
+    # (a) TTFT: one request at a time, planning included, first token on host
     e2e_ms, ttft = [], []
     h2d = d2h = 0
     for i in range(args.warmup + args.steps):
@@ -701,9 +702,27 @@ def main():
             h2d = res.extras["plan"].h2d_bytes + sum(8 * len(np.asarray(cp.recompute)) + 64 for cp in p.chunks)
             d2h = 4 + sum(4 * len(cp.recompute) for cp in p.chunks if cp.recompute is not None)
         del res
-    e2e_mean = allreduce_max(statistics.mean(e2e_ms), world)
-    e2e_value = n_prompt * (1 if tp_mode else world) / (e2e_mean / 1e3)
     ttft_p50 = statistics.median(e2e_ms)
+    # (b) throughput: a request stream through the same API, pipelined the way
+    # a server runs it — request i+1 is planned (host scoring, K9 on the
+    # planning stream, layout, H2D) while request i computes; every request's
+    # copies and its first-token readback stay inside the timed region
+    barrier(world)
+    t_start = time.perf_counter()
+    p = cc.build_plan(chunks, question, store, alpha=1.0, cfo_override=args.ratio)
+    rq = cc.plan_to_request(p)
+    done = []
+    for i in range(args.warmup + args.steps):
+        res = cc.prefill(model, rq, record_attention=False, stats=False, first_token=True)
+        if i + 1 < args.warmup + args.steps:
+            p = cc.build_plan(chunks, question, store, alpha=1.0, cfo_override=args.ratio)
+            rq = cc.plan_to_request(p)
+        tok = res.first_token
+        done.append(time.perf_counter())
+        del res
+    per_req = (done[-1] - done[args.warmup - 1]) / args.steps if args.warmup > 0 else (done[-1] - t_start) / args.steps
+    e2e_mean = allreduce_max(per_req * 1e3, world)
+    e2e_value = n_prompt * (1 if tp_mode else world) / (e2e_mean / 1e3)
 
     # ---- decode continuation on the repaired KV (f3) ------------------------
     decode = None
@@ -786,7 +805,9 @@ def main():
                    "l2": "inputs larger than L2 (%s GB of weights streamed per step)" % ("140" if args.config == "70b" else "16")},
         "ttft_ms": {"p50_e2e": round(ttft_p50, 3), "device_mean": round(ms_step, 3)},
         "e2e": {"value": round(e2e_value, 1), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-                "d2h_bytes_per_step": int(d2h), "path": "build_plan -> plan_to_request -> prefill(first_token=True)"},
+                "d2h_bytes_per_step": int(d2h), "path": "build_plan -> plan_to_request -> prefill(first_token=True)",
+                "mode": "request stream, plan of request i+1 overlapped with compute of request i; "
+                        "serial TTFT in ttft_ms.p50_e2e"},
         "roofline": gemm_roof,
         "roofline_kernels": kernels,
         "kernel_time_share": share,

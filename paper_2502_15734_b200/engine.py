@@ -596,8 +596,7 @@ def run_prefill(model: Model, request, record_values: bool = False, record_atten
             raise PlanError("the question's last row is not computed through every layer")
         logits, tok = _logits_rows(model, ws["hidden"][r:r + 1])
         extras["logits_last"] = logits
-        extras["first_token_dev"] = tok
-        extras["first_token"] = int(tok.item())
+        extras["first_token_dev"] = tok  # read back lazily by PrefillResult.first_token
     L = cfg.n_layers
     attn = AttentionRecord(query_slots=[np.sort(plan.rows[:plan.n_act[l]]) for l in range(L)], _lazy=lazy)
     if lazy is None:

@@ -780,6 +780,10 @@ class PrefillResult:
 
     @property
     def first_token(self):
+        """Greedy first token; read back from the device on first access (so a
+        caller can plan the next request while this one computes)."""
+        if "first_token" not in self.extras and "first_token_dev" in self.extras:
+            self.extras["first_token"] = int(self.extras["first_token_dev"].item())
         return self.extras.get("first_token")
 
 
