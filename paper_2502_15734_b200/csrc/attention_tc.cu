@@ -4,18 +4,20 @@
 //
 // CTA = 128 "M-rows" = R query rows x G heads of one GQA group (G = Hq/Hkv,
 // R = 128/G), so one K/V tile in shared memory serves the whole group.
-//   warp 0     TMA: Q once (3-D map), K/V tiles of 128 keys (2-stage ring)
+//   warp 0     TMA: Q once (3-D map), K tiles of 128 keys (3-slot ring, one
+//              tile ahead of V), V tiles (2 slots tied to the P buffers)
 //   warp 1     MMA issuer: S_i = Q K_i^T (M128 N128 K16 x dh/16) into one of
-//              two TMEM S buffers, O += P_i V_i (A = P from smem, B = V
-//              MN-major) into the TMEM O accumulator
-//   warps 2-5  softmax / correction / epilogue: thread = M-row = TMEM lane.
-//              Reads its S row (tcgen05.ld), applies the causal+pad mask
-//              (key j visible iff j <= q_slot[row] and !pad[j]), online
-//              softmax in fp32 (exp2), rescales its own O row in TMEM when
-//              the running max grows, writes its P row (bf16, 128B-swizzled)
-//              to smem for the PV MMA.
+//              two TMEM S buffers, O += P_i V_i (A = P from TMEM, B = V
+//              MN-major from smem) into the TMEM O accumulator; two commits
+//              per tile (s_full, p_empty)
+//   warps 2-9  two softmax warpgroups: thread = (M-row, key half).  Reads
+//              its 64 S columns (tcgen05.ld), causal+pad mask (key j visible
+//              iff j <= q_slot[row] and !pad[j]), row-max exchange with the
+//              other half through smem, online softmax in fp32 (exp2, a
+//              quarter on the FMA pipe), lazy O rescale in TMEM, P packed to
+//              bf16 and stored to TMEM (tcgen05.st) for the PV MMA.
 // The PV MMA of tile i overlaps the S MMA of tile i+1 and the softmax of
-// tile i+1 (double-buffered S).
+// tile i+1 (double-buffered S and P).
 #include <math.h>
 #include <stdlib.h>
 
@@ -34,9 +36,8 @@ using namespace sm100;
 
 constexpr int AT_BN = 128;      // keys per tile
 // P (softmax output, bf16) lives in TMEM and feeds the PV MMA as its A
-// operand (tcgen05.mma ... [a-tmem]); this frees the smem P buffers and 64 KiB
-// of smem traffic per tile, so the K/V ring gets a third stage.
-constexpr bool kPTmem = true;
+// operand (tcgen05.mma ... [a-tmem]): no smem P buffers, 64 KiB less smem
+// traffic per tile, room for a third K stage.
 constexpr int AT_KST = 3;  // K ring depth
 constexpr int AT_VST = 2;  // V ring depth = P buffers: V slot i % 2 is released by PV_i's p_empty commit
 constexpr int AT_THREADS = 320;  // TMA warp, MMA warp, 2 x 4 softmax warps
@@ -82,12 +83,7 @@ __device__ __forceinline__ float ex2_poly(float x) {
   p = __int_as_float(__float_as_int(p) + e);
   return x < -125.f ? 0.f : p;
 }
-__device__ __forceinline__ void st_shared_v4(uint32_t addr, const uint32_t (&v)[4]) {
-  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3])
-               : "memory");
-}
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
-__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 // mbarrier wait that adds its stall cycles to acc when tracing (debug)
 __device__ __forceinline__ void twait(uint64_t* bar, uint32_t parity, bool tracing, long long& acc) {
@@ -105,12 +101,10 @@ struct AtSmem {
   static constexpr int ATOMS = DH / 64;              // 64-element (128 B) column atoms
   static constexpr int Q_BYTES = 128 * DH * 2;       // 128 M-rows
   static constexpr int KV_BYTES = AT_BN * DH * 2;    // one K (or V) tile
-  static constexpr int P_BYTES = 128 * AT_BN * 2;    // one P tile, 2 atoms of 64 keys (x2 buffers)
   static constexpr int Q_OFF = 0;
   static constexpr int K_OFF = Q_OFF + Q_BYTES;
   static constexpr int V_OFF = K_OFF + AT_KST * KV_BYTES;
-  static constexpr int P_OFF = V_OFF + AT_VST * KV_BYTES;
-  static constexpr int BAR_OFF = P_OFF + (kPTmem ? 0 : 2 * P_BYTES);
+  static constexpr int BAR_OFF = V_OFF + AT_VST * KV_BYTES;
   static constexpr int X_OFF = BAR_OFF + 256;        // [2 parities][2 halves][128 rows] f32 exchange
   // no alignment slack: the kernel holds no static shared memory, so the
   // dynamic window starts 1 KiB aligned (checked at run time)
@@ -131,7 +125,6 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
   uint8_t* sQ = base + SM::Q_OFF;
   uint8_t* sK = base + SM::K_OFF;
   uint8_t* sV = base + SM::V_OFF;
-  uint8_t* sP = base + SM::P_OFF;
   uint64_t* bars = reinterpret_cast<uint64_t*>(base + SM::BAR_OFF);
   uint64_t* q_full = bars + 0;
   uint64_t* k_full = bars + 1;                 // [AT_KST]
@@ -260,17 +253,11 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
         twait(&v_full[st], (i / AT_VST) & 1, tracing, w3);
         tc_fence_after();
         const long long tp0 = tracing ? clock64() : 0;
-        const uint8_t* sPb = sP + pb * SM::P_BYTES;
 #pragma unroll
         for (int kk = 0; kk < AT_BN / 16; ++kk) {
           uint64_t bd = desc_sw128_mn(sV + st * SM::KV_BYTES + kk * 16 * 128, AT_BN * 128);
-          if constexpr (kPTmem) {
-            // A = P in TMEM: row = lane, 2 bf16 keys per 32-bit column, 16 keys = 8 columns
-            mma_bf16_ts(t_o, t_p + pb * (AT_BN / 2) + kk * 8, bd, id_o, (i > 0 || kk > 0) ? 1u : 0u);
-          } else {
-            uint64_t ad = desc_sw128(sPb + (kk >> 2) * 128 * 128) + 2 * (kk & 3);
-            mma_bf16(t_o, ad, bd, id_o, (i > 0 || kk > 0) ? 1u : 0u);
-          }
+          // A = P in TMEM: row = lane, 2 bf16 keys per 32-bit column, 16 keys = 8 columns
+          mma_bf16_ts(t_o, t_p + pb * (AT_BN / 2) + kk * 8, bd, id_o, (i > 0 || kk > 0) ? 1u : 0u);
         }
         const long long tp1 = tracing ? clock64() : 0;
         mma_commit(&p_empty[pb]);  // P buffer and V slot pb
@@ -280,7 +267,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
   } else {
     // ---- softmax / correction / epilogue --------------------------------------
     // Two softmax warpgroups (warps 2-5, 6-9): thread = (M-row m, key half h);
-    // half h owns S columns [64h, 64h+64), P atom h and O columns
+    // half h owns S columns [64h, 64h+64), P columns [32h, 32h+32) and O columns
     // [DH/2 h, DH/2 (h+1)).  Per tile the pair exchanges its row max through
     // smem (one named barrier per TMEM lane quarter); the running sums stay
     // per half and are added once at the end.
@@ -292,7 +279,6 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
     const int lim = row < n_q ? q_slot[row] : -1;
     const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
     float m_run = -INFINITY, l_run = 0.f;
-    const uint32_t patom_s = smem_u32(sP + m * 128) + h * 128 * 128;  // row m of P atom h
     constexpr float kRescaleLog2 = 8.f;  // lazy rescale: keep the stale max while p <= 2^8
     auto pair_bar = [&]() { asm volatile("bar.sync %0, 64;" ::"r"(2 + q4) : "memory"); };
     for (int i = 0; i < n_tiles; ++i) {
@@ -361,11 +347,9 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
       if (m_run == -INFINITY) m_run = tmax;  // first visible keys: nothing accumulated yet
       const float base_l2 = (m_run == -INFINITY) ? 0.f : m_run * scale_log2;
       float ps[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-      const uint32_t patom = patom_s + pb * SM::P_BYTES;
       uint32_t pt[32];  // this half's 64 keys of P, packed bf16x2 (TMEM P)
 #pragma unroll
       for (int ch = 0; ch < 8; ++ch) {
-        uint32_t pk[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const int c = ch * 8 + e * 2;
@@ -378,16 +362,10 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
           ps[(2 * e) & 7] += p0;
           ps[(2 * e + 1) & 7] += p1;
           __nv_bfloat162 hv = __floats2bfloat162_rn(p0, p1);
-          pk[e] = *reinterpret_cast<uint32_t*>(&hv);
-        }
-        if constexpr (kPTmem) {
-#pragma unroll
-          for (int e = 0; e < 4; ++e) pt[ch * 4 + e] = pk[e];
-        } else {
-          st_shared_v4(patom + ((ch ^ (m & 7)) << 4), pk);
+          pt[ch * 4 + e] = *reinterpret_cast<uint32_t*>(&hv);
         }
       }
-      if constexpr (kPTmem) tmem_st32(t_p + pb * (AT_BN / 2) + h * 32 + lane_off, pt);
+      tmem_st32(t_p + pb * (AT_BN / 2) + h * 32 + lane_off, pt);
       l_run += ((ps[0] + ps[1]) + (ps[2] + ps[3])) + ((ps[4] + ps[5]) + (ps[6] + ps[7]));
       // O *= alpha (this half's columns) for rows whose max grew past the lazy
       // threshold.  tcgen05.ld/st are warp-collective: the whole warp joins,
@@ -407,7 +385,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
         }
         tmem_st_wait();
       }
-      if constexpr (kPTmem) tmem_st_wait(); else fence_async_smem();
+      tmem_st_wait();
       tc_fence_before();
       mbar_arrive(&p_full[pb]);
     }
