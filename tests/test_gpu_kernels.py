@@ -140,6 +140,42 @@ print('ok')
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
 
 
+@pytest.mark.parametrize("bnr", [208, 144, 256])
+@pytest.mark.parametrize("epi", ["store", "resid", "swiglu", "gelu"])
+def test_gemm_swap_ab(N, bnr, epi):
+    """Swap-AB tiles (weights as the MMA M side, activation rows as N with a
+    ragged last row tile) match the fp32 reference for every epilogue."""
+    import subprocess
+    import sys
+
+    code = f"""
+import torch, sys
+sys.path.insert(0, '.')
+from paper_2502_15734_b200 import _native as N
+M, Nn, K = 802, 1536, 1024
+g = torch.Generator(device='cuda').manual_seed(4)
+A = torch.randn((M, K), generator=g, device='cuda').bfloat16()
+B = (torch.randn((Nn, K), generator=g, device='cuda') / 32).bfloat16()
+acc = A.float() @ B.float().T
+epi = '{epi}'
+if epi == 'resid':
+    C = torch.ones((M, Nn), device='cuda'); ref = acc + 1; code = N.EPI_RESID_ADD
+elif epi == 'swiglu':
+    C = torch.empty((M, Nn // 2), device='cuda', dtype=torch.bfloat16); code = N.EPI_SWIGLU
+    a4 = acc.reshape(M, Nn // 128, 2, 64); ref = (torch.nn.functional.silu(a4[:, :, 0]) * a4[:, :, 1]).reshape(M, Nn // 2)
+else:
+    C = torch.empty((M, Nn), device='cuda', dtype=torch.bfloat16)
+    code = N.EPI_GELU if epi == 'gelu' else N.EPI_STORE
+    ref = torch.nn.functional.gelu(acc, approximate='tanh') if epi == 'gelu' else acc
+N.call('cc_gemm', N.ptr(A), K, N.ptr(B), K, N.ptr(C), C.shape[1], M, Nn, K, code, N.BF16, 1, N.stream_ptr())
+torch.testing.assert_close(C.float(), ref, atol=2e-2, rtol=2e-2)
+print('ok')
+"""
+    env = dict(__import__("os").environ, CCB_GEMM_FORCE=f"{bnr},2")
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=300)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
+
+
 @pytest.mark.parametrize("Nn", [512, 6144, 1536])
 def test_gemm_tcgen05_m_invariance(N, Nn):
     """A row's result does not depend on how many rows are active (also when
