@@ -34,11 +34,14 @@ constexpr int TC_THREADS = 192;
 template <int BN>
 struct TcCfg {
   static constexpr int B_BYTES = BN * TC_BK * 2;
-  static constexpr int STAGES = (200 * 1024) / (TC_A_BYTES + B_BYTES) > 6 ? 6 : (200 * 1024) / (TC_A_BYTES + B_BYTES);
+  // as many stages as fit next to the barriers and the 16 KiB transpose slabs
+  // (227 KiB per CTA): BN 256 -> 4, 208 / 192 / 160 -> 5, 128 -> 6
+  static constexpr int RING = 232448 - 1024 - 256 - 4 * 4096;
+  static constexpr int STAGES = RING / (TC_A_BYTES + B_BYTES) > 6 ? 6 : RING / (TC_A_BYTES + B_BYTES);
   static constexpr int TMEM_COLS = 2 * BN <= 256 ? 256 : 512;
   static constexpr int ACC_STRIDE = 2 * BN <= 256 ? BN : 256;  // TMEM column of accumulator 1
   // + 4 per-warp 4 KiB transpose slabs + 8 KiB gate/up exchange (swap SwiGLU)
-  static constexpr size_t SMEM = 1024 + STAGES * (TC_A_BYTES + B_BYTES) + 256 + 4 * 4096 + 8192;
+  static constexpr size_t SMEM = 1024 + STAGES * (TC_A_BYTES + B_BYTES) + 256 + 4 * 4096;
 };
 
 using namespace sm100;
@@ -250,7 +253,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const int et = threadIdx.x - 64;  // 0..127 within the epilogue warps
     const uint32_t stg = smem_u32(stg_base + (warp - 2) * 256);
-    const uint32_t xch = smem_u32(stg_base + 4 * 256);  // 8 KiB gate/up exchange (swap SwiGLU)
     int acc = 0;
     uint32_t acc_phase = 0;
     UnitIter it(num_kb, t_dp, W, gridDim.x, blockIdx.x);
@@ -306,27 +308,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           tmem_ld32(t0 + c * 32, r);
           tmem_ld_wait();
           const int jmax = min(32, min(TC_BN - c * 32, N - n0 - c * 32));  // rows of this chunk in tile and matrix
-          if constexpr (EPI == CC_EPI_SWIGLU) {
-            // weight tile = [gate 64 | up 64]: warps 0-1 hold gate features,
-            // warps 2-3 the matching up features -> exchange through smem
-            if (q >= 2) {
-#pragma unroll
-              for (int j = 0; j < 32; ++j)
-                asm volatile("st.shared.b32 [%0], %1;" ::"r"(xch + (((q - 2) * 32 + j) * 32 + lane) * 4), "r"(r[j])
-                             : "memory");
-            }
-            epi_bar();
-            if (q < 2) {
-              __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(C) + mt * 64 + q * 32 + lane;
-#pragma unroll
-              for (int j = 0; j < 32; ++j) {
-                float u;
-                asm volatile("ld.shared.f32 %0, [%1];" : "=f"(u) : "r"(xch + ((q * 32 + j) * 32 + lane) * 4) : "memory");
-                if (j < jmax)
-                  out[(int64_t)(n0 + c * 32 + j) * ldc] = __float2bfloat16_rn(silu(__uint_as_float(r[j])) * u);
-              }
-            }
-            epi_bar();  // slab reusable
+          static_assert(EPI != CC_EPI_SWIGLU, "swap-AB has no SwiGLU epilogue (measured slower; see pick_tiling)");
+          if constexpr (false) {
           } else if constexpr (EPI == CC_EPI_RESID_ADD) {
             float* h = reinterpret_cast<float*>(C) + (int64_t)(n0 + c * 32) * ldc + feat;
             float cv[32];
@@ -739,7 +722,7 @@ bool forced_tiling(int M, int N, int K, int epi, Tiling* out) {
     if (const char* e = getenv("CCB_GEMM_FORCE")) sscanf(e, "%d,%d", &fb, &fs);
   }
   if (fs == 2) {  // swap-AB with row tile fb
-    if (fb <= 0 || fb % 16 || fb > 256 || N % TC_BM) return false;
+    if (fb <= 0 || fb % 16 || fb > 256 || N % TC_BM || epi == CC_EPI_SWIGLU) return false;
     *out = plan_swap(M, N, fb);
     return true;
   }
@@ -754,7 +737,7 @@ int launch_epi(const void* A, int64_t lda, const void* B, int64_t ldb, void* C, 
   Tiling tl;
   if (!forced_tiling(M, N, K, EPI, &tl)) tl = pick_tiling(M, N, K, EPI, allow_split);
   if (tl.bn == 0) return fail(CC_E_UNSUP, "gemm_tc: N must be a multiple of 128 (SwiGLU: 256)");
-  if (tl.swap) {
+  if constexpr (EPI != CC_EPI_SWIGLU) if (tl.swap) {
     // A slot <- weights B [N][K] (128-row boxes), B slot <- activations A [M][K]
     CUtensorMap mw, mx;
     int rc = make_map(&mw, B, N, K, ldb, TC_BM);

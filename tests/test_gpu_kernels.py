@@ -141,7 +141,7 @@ print('ok')
 
 
 @pytest.mark.parametrize("bnr", [208, 144, 256])
-@pytest.mark.parametrize("epi", ["store", "resid", "swiglu", "gelu"])
+@pytest.mark.parametrize("epi", ["store", "resid", "gelu"])
 def test_gemm_swap_ab(N, bnr, epi):
     """Swap-AB tiles (weights as the MMA M side, activation rows as N with a
     ragged last row tile) match the fp32 reference for every epilogue."""
