@@ -52,7 +52,8 @@ __device__ __forceinline__ double gelu_tanh(double x) {
   const double k0 = 0.7978845608028654;
   return 0.5 * x * (1.0 + tanh(k0 * (x + 0.044715 * x * x * x)));
 }
-__device__ __forceinline__ float silu(float x) { return x / (1.f + __expf(-x)); }
+// (fast reciprocal division: the IEEE x / y slow path dominated the GEMM epilogues)
+__device__ __forceinline__ float silu(float x) { return __fdividef(x, 1.f + __expf(-x)); }
 __device__ __forceinline__ double silu(double x) { return x / (1.0 + exp(-x)); }
 
 // ---- dtype dispatch -------------------------------------------------------

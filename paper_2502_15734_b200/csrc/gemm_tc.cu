@@ -16,6 +16,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <mutex>
+#include <queue>
+#include <vector>
+#include <algorithm>
 #include <unordered_map>
 
 #include "common.cuh"
@@ -141,6 +144,8 @@ __device__ __forceinline__ void fold8(float* p, int64_t ld_rows4, const bool (&o
 }
 
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+// named barrier of epilogue warps q and q ^ 2 (ids 2, 3)
+__device__ __forceinline__ void pair_bar(int q) { asm volatile("bar.sync %0, 64;" ::"r"(2 + (q & 1)) : "memory"); }
 
 __device__ __forceinline__ int ld_acquire(const int* p) {
   int v;
@@ -456,6 +461,399 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   }
 }
 
+// ---- swap-AB with a host-planned unit table --------------------------------
+// The activation rows are the MMA N dimension, so a unit may cover any
+// multiple of 16 rows (<= 256) of one 128-feature weight tile.  The host cuts
+// every feature tile's rows into chunks and assigns the units to the
+// persistent CTAs longest-first (LPT), passed as a kernel parameter: at M ~ 800
+// the gate/up GEMM (224 feature tiles) runs ~5.0 tile-times per SM instead
+// of 6 whole waves of 128 x 256 tiles.  Every output element is still produced
+// by one unit with the full K reduction in order (no split, no workspace).
+constexpr int SW_MAXG = 160;   // >= SM count
+constexpr int SW_MAXU = 1792;  // units per launch
+struct SwTab {
+  uint16_t start[SW_MAXG + 1];  // CTA c runs units [start[c], start[c+1])
+  uint32_t unit[SW_MAXU];       // feature tile | (row0 / 16) << 14 | (rows / 16 - 1) << 25
+};
+__host__ __device__ constexpr uint32_t sw_pack(int ft, int r0, int n) {
+  return (uint32_t)ft | ((uint32_t)(r0 >> 4) << 14) | ((uint32_t)((n >> 4) - 1) << 25);
+}
+// activation rows per TMA box: a unit loads ceil(rows / box) boxes (rows past
+// the unit are other units' rows or zero fill, unused)
+inline int sw_box() {
+  static int b = [] {
+    const char* e = getenv("CCB_SW_BOX");
+    const int v = e ? atoi(e) : 64;
+    return (v == 32 || v == 64 || v == 128 || v == 256) ? v : 64;
+  }();
+  return b;
+}
+
+template <int EPI>
+__global__ void __launch_bounds__(TC_THREADS, 1)
+    gemm_sw_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX, void* C,
+                   int64_t ldc, int M, int K, int box, const __grid_constant__ SwTab tab) {
+  constexpr int B_BYTES = TcCfg<256>::B_BYTES;
+  constexpr int STAGES = TcCfg<256>::STAGES;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = base;
+  uint8_t* sB = base + STAGES * TC_A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  float4* stg_base = reinterpret_cast<float4*>(sB + STAGES * B_BYTES + 256);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int num_kb = K / TC_BK;
+  const int u_begin = tab.start[blockIdx.x], u_end = tab.start[blockIdx.x + 1];
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmW);
+    tma_prefetch(&tmX);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 128);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int u = u_begin; u < u_end; ++u) {
+        const uint32_t e = tab.unit[u];
+        const int ft = e & 0x3fff, r0 = ((e >> 14) & 0x7ff) * 16, n = (((e >> 25) & 0xf) + 1) * 16;
+        const int nbox = (n + box - 1) / box;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_expect_tx(&full[stage], TC_A_BYTES + nbox * box * TC_BK * 2);
+          tma_load_2d(sA + stage * TC_A_BYTES, &tmW, &full[stage], kb * TC_BK, ft * TC_BM);
+          for (int b = 0; b < nbox; ++b)
+            tma_load_2d(sB + stage * B_BYTES + b * box * TC_BK * 2, &tmX, &full[stage], kb * TC_BK, r0 + b * box);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int u = u_begin; u < u_end; ++u) {
+        const int n = (((tab.unit[u] >> 25) & 0xf) + 1) * 16;
+        const uint32_t idesc = idesc_bf16_f32(TC_BM, n);
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * 256;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint64_t ad = desc_sw128(sA + stage * TC_A_BYTES);
+          const uint64_t bd = desc_sw128(sB + stage * B_BYTES);
+#pragma unroll
+          for (int k = 0; k < TC_BK / 16; ++k) mma_bf16(d_tmem, ad + 2 * k, bd + 2 * k, idesc, (kb > 0 || k > 0) ? 1u : 0u);
+          mma_commit(&empty[stage]);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        mma_commit(&tfull[acc]);
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+  } else {
+    const int q = warp & 3;  // TMEM lane quarter = output features q*32 .. +31 of the tile
+    // per-warp 4 KiB slabs; SwiGLU: the up-feature warps (q = 2, 3) hand their
+    // accumulators to the gate-feature warps (q = 0, 1) through slab q - 2
+    const uint32_t xch = smem_u32(stg_base + (q >= 2 ? q - 2 : q) * 256);
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int u = u_begin; u < u_end; ++u) {
+      const uint32_t e = tab.unit[u];
+      const int ft = e & 0x3fff, r0 = ((e >> 14) & 0x7ff) * 16, n = (((e >> 25) & 0xf) + 1) * 16;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t t0 = tmem_base + acc * 256 + ((uint32_t)(q * 32) << 16);
+      const int feat = ft * TC_BM + q * 32 + lane;
+#pragma unroll 1
+      for (int c = 0; c * 32 < n; ++c) {
+        const int row = r0 + c * 32;
+        const int jmax = min(32, min(n - c * 32, M - row));  // rows of this chunk in unit and matrix
+        if (jmax <= 0) break;
+        uint32_t r[32];
+        tmem_ld32(t0 + c * 32, r);
+        tmem_ld_wait();
+        if constexpr (EPI == CC_EPI_SWIGLU) {
+          // weight tile = [gate 64 | up 64] -> outputs ft * 64 + 0..63
+          if (q >= 2) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              asm volatile("st.shared.b32 [%0], %1;" ::"r"(xch + (j * 32 + lane) * 4), "r"(r[j]) : "memory");
+          }
+          epi_bar();
+          if (q < 2) {
+            __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(C) + (int64_t)row * ldc + ft * 64 + q * 32 + lane;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              float up;
+              asm volatile("ld.shared.f32 %0, [%1];" : "=f"(up) : "r"(xch + (j * 32 + lane) * 4) : "memory");
+              if (j < jmax) out[(int64_t)j * ldc] = __float2bfloat16_rn(silu(__uint_as_float(r[j])) * up);
+            }
+          }
+          epi_bar();  // slab reusable
+        } else if constexpr (EPI == CC_EPI_RESID_ADD) {
+          float* h = reinterpret_cast<float*>(C) + (int64_t)row * ldc + feat;
+          float cv[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (j < jmax) cv[j] = h[(int64_t)j * ldc];
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (j < jmax) h[(int64_t)j * ldc] = cv[j] + __uint_as_float(r[j]);
+        } else {
+          __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(C) + (int64_t)row * ldc + feat;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            if (j >= jmax) continue;
+            float x = __uint_as_float(r[j]);
+            if constexpr (EPI == CC_EPI_GELU) x = gelu_tanh(x);
+            out[(int64_t)j * ldc] = __float2bfloat16_rn(x);
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem_base);
+  }
+}
+
+// ---- CTA-pair (cta_group::2) swap-AB with a unit table ----------------------
+// A 1-CTA 128 x 256 tile streams 48 KiB of operands into the SM per k-block,
+// and the SM ingests ~64 B/clk, so it runs at ~768 cycles per k-block where
+// the MMA needs 512: the kernels above are operand-feed bound.  A CTA pair
+// computes a 256-feature x n-row tile with one tcgen05.mma.cta_group::2: each
+// SM holds its 128 weight rows and HALF of the n activation rows (the MMA
+// reads the other half from the peer's smem), so the feed per SM for n = 256
+// is 32 KiB per k-block — matched to the MMA.  The leader CTA (rank 0) issues
+// the MMAs; both CTAs load through TMA onto the leader's full barrier, the
+// commits multicast to both CTAs' empty / accumulator-full barriers, and both
+// CTAs' epilogue warps release the accumulator to the leader's barrier.
+// Units (256-feature tile, row0, n rows; n % 32 == 0) come from the host LPT
+// table, one list per pair.
+constexpr int P2_STAGES = 6;                       // 6 x (16 + 16) KiB
+constexpr int P2_B_BYTES = 128 * TC_BK * 2;        // <= 128 activation rows per CTA
+// + 32 KiB epilogue staging: per epilogue warp two 4 KiB slabs (32 rows x 32
+// features, fp32 or bf16) drained by TMA stores / reduce-adds
+constexpr size_t P2_SMEM = 1024 + P2_STAGES * (TC_A_BYTES + P2_B_BYTES) + 256 + 8 * 4096;
+
+template <int EPI>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
+    gemm_pair_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX128,
+                     const __grid_constant__ CUtensorMap tmX64, const __grid_constant__ CUtensorMap tmX32,
+                     const __grid_constant__ CUtensorMap tmX16, const __grid_constant__ CUtensorMap tmC, int M,
+                     int K, int dbg, const __grid_constant__ SwTab tab) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = base;
+  uint8_t* sB = base + P2_STAGES * TC_A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + P2_STAGES * P2_B_BYTES);
+  uint64_t* empty = full + P2_STAGES;
+  uint64_t* tfull = empty + P2_STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint8_t* stg_base = sB + P2_STAGES * P2_B_BYTES + 256;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const int num_kb = K / TC_BK;
+  const int pair = blockIdx.x >> 1;
+  const int u_begin = tab.start[pair], u_end = tab.start[pair + 1];
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmW);
+    tma_prefetch(&tmX128);
+    for (int s = 0; s < P2_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 8);  // 4 epilogue warps x 2 CTAs (leader's copy is the one used)
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc_pair<512>(tmem_slot);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int u = u_begin; u < u_end; ++u) {
+        const uint32_t e = tab.unit[u];
+        const int fp = e & 0x3fff, r0 = ((e >> 14) & 0x7ff) * 16, n = (((e >> 25) & 0xf) + 1) * 16;
+        const int h = n / 2;  // rows per CTA (multiple of 16)
+        const int rows0 = r0 + (int)rank * h;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          if ((dbg & 2) && (u > u_begin || kb >= P2_STAGES)) {  // debug: MMA on stale tiles (no feed)
+            if (rank == 0) mbar_arrive(&full[stage]);
+            if (++stage == P2_STAGES) { stage = 0; phase ^= 1; }
+            continue;
+          }
+          const uint32_t fb = mapa_shared(smem_u32(&full[stage]), 0);
+          if (rank == 0) mbar_expect_tx(&full[stage], 2 * (TC_A_BYTES + h * TC_BK * 2));
+          tma_load_2d_pair(sA + stage * TC_A_BYTES, &tmW, fb, kb * TC_BK, fp * 2 * TC_BM + (int)rank * TC_BM);
+          uint8_t* dst = sB + stage * P2_B_BYTES;
+          int off = 0;
+          if (h & 128) { tma_load_2d_pair(dst, &tmX128, fb, kb * TC_BK, rows0); off += 128; }
+          if (h & 64) { tma_load_2d_pair(dst + off * 128, &tmX64, fb, kb * TC_BK, rows0 + off); off += 64; }
+          if (h & 32) { tma_load_2d_pair(dst + off * 128, &tmX32, fb, kb * TC_BK, rows0 + off); off += 32; }
+          if (h & 16) tma_load_2d_pair(dst + off * 128, &tmX16, fb, kb * TC_BK, rows0 + off);
+          if (++stage == P2_STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int u = u_begin; u < u_end; ++u) {
+        const int n = (((tab.unit[u] >> 25) & 0xf) + 1) * 16;
+        const uint32_t idesc = idesc_bf16_f32(2 * TC_BM, n);
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * 256;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint64_t ad = desc_sw128(sA + stage * TC_A_BYTES);
+          const uint64_t bd = desc_sw128(sB + stage * P2_B_BYTES);
+#pragma unroll
+          for (int k = 0; k < TC_BK / 16; ++k)
+            mma_bf16_pair(d_tmem, ad + 2 * k, bd + 2 * k, idesc, (kb > 0 || k > 0) ? 1u : 0u);
+          mma_commit_pair(&empty[stage], 0x3);
+          if (++stage == P2_STAGES) { stage = 0; phase ^= 1; }
+        }
+        mma_commit_pair(&tfull[acc], 0x3);
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+  } else {
+    const int q = warp & 3;  // TMEM lane quarter = features q*32 .. +31 of this CTA's 128
+    // staging: warp q owns two 4 KiB slabs at stg_base + q * 8 KiB (alternate
+    // chunks, so a chunk's TMA store drains while the next one is written);
+    // SwiGLU stages 16 x 32 bf16 per slab and swaps half chunks with warp q ^ 2
+    // through bytes 2048.. of its first slab
+    uint8_t* my_slab = stg_base + q * 8192;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    int nst = 0;  // TMA stores issued by this warp (slab parity)
+    for (int u = u_begin; u < u_end; ++u) {
+      const uint32_t e = tab.unit[u];
+      const int fp = e & 0x3fff, r0 = ((e >> 14) & 0x7ff) * 16, n = (((e >> 25) & 0xf) + 1) * 16;
+      const int ft = fp * 2 + (int)rank;  // this CTA's 128-feature tile
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t t0 = tmem_base + acc * 256 + ((uint32_t)(q * 32) << 16);
+#pragma unroll 1
+      for (int c = 0; c * 32 < n; ++c) {
+        const int row = r0 + c * 32;
+        if (row >= M) break;
+        uint32_t r[32];
+        tmem_ld32(t0 + c * 32, r);
+        tmem_ld_wait();
+        if (dbg & 1) continue;  // debug: no stores
+        uint8_t* slab = my_slab + (nst & 1) * 4096;
+        // the TMA store that last read this slab (two stores ago) is done reading
+        if (lane == 0) bulk_wait_read<1>();
+        __syncwarp();
+        if constexpr (EPI == CC_EPI_SWIGLU) {
+          // warps q (gate features) and q ^ 2 (the matching up features) swap
+          // half a chunk: the gate warp finishes rows 0-15, the up warp 16-31
+          const bool gate = q < 2;
+          const uint32_t out_x = smem_u32(my_slab) + 2048, in_x = smem_u32(stg_base + (q ^ 2) * 8192) + 2048;
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            asm volatile("st.shared.b32 [%0], %1;" ::"r"(out_x + (j * 32 + lane) * 4), "r"(r[gate ? 16 + j : j])
+                         : "memory");
+          pair_bar(q);
+          const uint32_t dst = smem_u32(slab) + lane * 2;
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            float other;
+            asm volatile("ld.shared.f32 %0, [%1];" : "=f"(other) : "r"(in_x + (j * 32 + lane) * 4) : "memory");
+            const float g = gate ? __uint_as_float(r[j]) : other, up = gate ? other : __uint_as_float(r[16 + j]);
+            const __nv_bfloat16 hv = __float2bfloat16_rn(silu(g) * up);
+            asm volatile("st.shared.b16 [%0], %1;" ::"r"(dst + j * 64), "h"(*reinterpret_cast<const uint16_t*>(&hv))
+                         : "memory");
+          }
+          pair_bar(q);  // exchange buffers reusable
+        } else if constexpr (EPI == CC_EPI_RESID_ADD) {
+          const uint32_t dst = smem_u32(slab) + lane * 4;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) asm volatile("st.shared.b32 [%0], %1;" ::"r"(dst + j * 128), "r"(r[j]) : "memory");
+        } else {
+          const uint32_t dst = smem_u32(slab) + lane * 2;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            float x = __uint_as_float(r[j]);
+            if constexpr (EPI == CC_EPI_GELU) x = gelu_tanh(x);
+            const __nv_bfloat16 hv = __float2bfloat16_rn(x);
+            asm volatile("st.shared.b16 [%0], %1;" ::"r"(dst + j * 64), "h"(*reinterpret_cast<const uint16_t*>(&hv))
+                         : "memory");
+          }
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0 && !(dbg & 8)) {
+          // rows >= M and columns past the matrix are clipped by the TMA unit
+          if constexpr (EPI == CC_EPI_RESID_ADD) tma_reduce_add_2d(&tmC, slab, ft * TC_BM + q * 32, row);
+          else if constexpr (EPI == CC_EPI_SWIGLU) tma_store_2d(&tmC, slab, ft * 64 + (q & 1) * 32, row + (q >> 1) * 16);
+          else tma_store_2d(&tmC, slab, ft * TC_BM + q * 32, row);
+          bulk_commit();
+        }
+        ++nst;
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), 0));
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+    if (lane == 0) bulk_wait_all();
+  }
+  tc_fence_before();
+  cluster_sync();  // the leader's last MMAs read this CTA's smem / write its TMEM
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc_pair<512>(tmem_base);
+  }
+}
+
 // ---- host: tensor maps ------------------------------------------------------
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -477,7 +875,7 @@ EncodeTiledFn get_encode_fn() {
 struct MapKey {
   const void* p;
   int64_t rows, cols, ld;
-  int box_rows;
+  int box_rows;  // < 0: output map, no swizzle: -1 bf16 32 x 32, -2 fp32 32 x 32, -3 bf16 32 cols x 16 rows
   bool operator==(const MapKey& o) const {
     return p == o.p && rows == o.rows && cols == o.cols && ld == o.ld && box_rows == o.box_rows;
   }
@@ -503,13 +901,15 @@ int make_map(CUtensorMap* out, const void* p, int64_t rows, int64_t cols, int64_
   }
   EncodeTiledFn enc = get_encode_fn();
   if (!enc) return fail(CC_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+  const bool outmap = box_rows < 0, f32 = box_rows == -2;
   cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)(ld * 2)};
-  cuuint32_t box[2] = {(cuuint32_t)TC_BK, (cuuint32_t)box_rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * (f32 ? 4 : 2))};
+  cuuint32_t box[2] = {(cuuint32_t)(outmap ? 32 : TC_BK), (cuuint32_t)(outmap ? (box_rows == -3 ? 16 : 32) : box_rows)};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(p), dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  CUresult r = enc(out, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                   const_cast<void*>(p), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   outmap ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(CC_E_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
   std::lock_guard<std::mutex> g(mu);
   if (cache.size() > 4096) cache.clear();
@@ -547,9 +947,12 @@ inline int n_tiles_of(int N, int bn) { return (N + bn - 1) / bn; }
 
 // Tiling plan: tile width, how many tiles run data-parallel, the stream-K
 // k-block total and the persistent grid.
+struct TabPlan;
 struct Tiling {
   int bn = 0;
   bool swap = false;  // swap-AB: bn = activation-row tile width, A slot = 128-row weight tiles
+  const TabPlan* tab = nullptr;  // swap-AB with a planned unit table (gemm_sw_kernel / gemm_pair_kernel)
+  bool pair = false;
   int t_dp = 0;
   long long W = 0;  // stream-K k-blocks (0: pure data-parallel)
   int grid = 0;
@@ -675,6 +1078,126 @@ double model_time(const Tiling& t, int M, int N, int K) {
   return ((double)(t.t_dp / t.grid) * nkb + per) * kc + (splits ? kFoldCost * t.bn / 256.0 : 0.0);
 }
 
+// ---- unit-table plans (gemm_sw_kernel / gemm_pair_kernel) -----------------
+// Time model in SM cycles per k-block (64-deep slice): the MMA (128 x n x 64
+// per SM: 2n cycles) against the operand feed at ~64 B/clk per SM (1-CTA:
+// 16 KiB weights + n rows; pair: 16 KiB + n/2 rows).  A 1-CTA 128 x 256 tile
+// is 768 cycles (feed bound, matches the measured ~430 ns per k-block); the
+// kb_cost() plans above are converted at that rate.
+constexpr double kKbCycles = 768.0;
+constexpr double kUnitOverhead = 2000.0;  // accumulator hand-off, pipeline turn (cycles)
+
+struct TabPlan {
+  SwTab tab;
+  int grid = 0;  // CTAs (pair plans: 2 per unit list)
+  double t = 1e30;  // modelled makespan, cycles
+};
+
+// measured: a pair k-block runs ~1.25x the ideal max(MMA, feed) (shared-memory
+// port: the MMA reads and the TMA writes of a k-block share it); calibrated on
+// the M = 802 / 2048 projection shapes against the 1-CTA plans
+constexpr double kPairFactor = 1.25;
+
+inline double unit_cycles(int n, int nkb, bool pair) {
+  const double mma = 2.0 * n, feed = pair ? 256.0 + n : 256.0 + 2.0 * n;
+  return ((mma > feed ? mma : feed) * nkb + kUnitOverhead) * (pair ? kPairFactor : 1.0);
+}
+
+// Cut each weight tile's (128 features; pair: 256) M rows into k chunks (j
+// chunks of 256 rows, the rest split evenly; granule 16 rows, pair 32), k
+// from ceil(M/256) to +3, assign the units longest-first to the least-loaded
+// CTA (pair), keep the smallest makespan.  Cached per shape.
+const TabPlan* plan_units(int M, int F, int K, bool pair) {
+  static std::mutex mu;
+  static std::unordered_map<uint64_t, TabPlan*> cache;
+  const uint64_t key = ((uint64_t)M << 44) ^ ((uint64_t)F << 20) ^ (uint64_t)K ^ (pair ? 1ull << 63 : 0);
+  std::lock_guard<std::mutex> g(mu);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  const int tile = pair ? 2 * TC_BM : TC_BM, gran = pair ? 32 : 16, maxb = 256 / gran;
+  const int ntile = F / tile, nkb = K / TC_BK;
+  int G = pair ? num_sms() / 2 : num_sms();
+  if (G > SW_MAXG) G = SW_MAXG;
+  const int nb = (M + gran - 1) / gran, kmin = (nb + maxb - 1) / maxb;
+  TabPlan* best = new TabPlan();
+  struct U {
+    double cost;
+    int ft, r0, n;
+  };
+  std::vector<U> units;
+  std::vector<std::vector<int>> lists(G);
+  std::vector<int> best_ch;
+  for (int k = kmin; k <= kmin + 3 && (long)ntile * k <= SW_MAXU; ++k) {
+    for (int j = 0; j < k; ++j) {
+      const int rem = nb - maxb * j, parts = k - j;
+      if (rem < parts) break;
+      if ((rem + parts - 1) / parts > maxb) continue;
+      std::vector<int> ch(j, maxb);
+      for (int i = 0; i < parts; ++i) ch.push_back(rem / parts + (i < rem % parts ? 1 : 0));
+      units.clear();
+      for (int ft = 0; ft < ntile; ++ft)
+        for (int ci = 0, r0 = 0; ci < (int)ch.size(); r0 += ch[ci] * gran, ++ci)
+          units.push_back({unit_cycles(ch[ci] * gran, nkb, pair), ft, r0, ch[ci] * gran});
+      // Units of one weight tile should run side by side (one HBM read of the
+      // weights, the rest from L2): list-schedule them in (tile, chunk) order
+      // onto the earliest-free CTA, except the last ~1.5 rounds of work, which
+      // go longest-first (LPT) to even out the finish.
+      double total = 0, maxc = 0;
+      for (auto& x : units) { total += x.cost; maxc = maxc > x.cost ? maxc : x.cost; }
+      size_t split = 0;
+      for (double pre = 0; split < units.size() && pre + units[split].cost <= total - 1.5 * G * maxc; ++split)
+        pre += units[split].cost;
+      std::stable_sort(units.begin() + split, units.end(), [](const U& a, const U& b) { return a.cost > b.cost; });
+      std::priority_queue<std::pair<double, int>, std::vector<std::pair<double, int>>, std::greater<>> heap;
+      for (int c = 0; c < G; ++c) heap.push({0.0, c});
+      for (auto& l : lists) l.clear();
+      double makespan = 0;
+      for (int i = 0; i < (int)units.size(); ++i) {
+        auto [load, c] = heap.top();
+        heap.pop();
+        load += units[i].cost;
+        if (load > makespan) makespan = load;
+        lists[c].push_back(i);
+        heap.push({load, c});
+      }
+      if (makespan < best->t - 1e-9) {
+        best->t = makespan;
+        best_ch = ch;
+        int nl = 0, pos = 0;
+        for (int c = 0; c < G; ++c) {
+          if (lists[c].empty()) continue;
+          best->tab.start[nl++] = (uint16_t)pos;
+          for (int i : lists[c]) best->tab.unit[pos++] = sw_pack(units[i].ft, units[i].r0, units[i].n);
+        }
+        best->tab.start[nl] = (uint16_t)pos;
+        best->grid = pair ? 2 * nl : nl;
+      }
+    }
+  }
+  if (getenv("CCB_SW_DEBUG")) {
+    fprintf(stderr, "[gemm_%s] M=%d F=%d K=%d makespan=%.0f cyc (%.2f x 768-cycle tiles) grid=%d chunks(x%d):",
+            pair ? "pair" : "sw", M, F, K, best->t, best->t / (kKbCycles * nkb), best->grid, gran);
+    for (int c : best_ch) fprintf(stderr, " %d", c);
+    fprintf(stderr, "\n");
+  }
+  if (best->grid == 0) {
+    delete best;
+    best = nullptr;
+  }
+  if (cache.size() > 1024) cache.clear();  // (plans of evicted shapes leak: bounded, rare)
+  cache.emplace(key, best);
+  return best;
+}
+
+// CCB_GEMM_PAIR=0 disables the CTA-pair plans (A/B measurements)
+inline bool pair_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("CCB_GEMM_PAIR");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 // the tiling minimising the modelled time.  Stream-K is considered where it
 // measured faster: small M (fewer than half a wave of tiles: weight
 // streaming) and long K with several waves (M ~ 5k down_proj).  At M ~ 800
@@ -709,6 +1232,17 @@ Tiling pick_tiling(int M, int N, int K, int epi, bool allow_split) {
       if (ts < 0.98 * best_t) { best_t = ts; best = sw; }
     }
   }
+  // CTA-pair unit table (any epilogue; SwiGLU: [gate 64 | up 64] per 128 rows)
+  if (M >= 64 && M <= 2048 && N % (2 * TC_BM) == 0 && pair_enabled()) {
+    const TabPlan* tp = plan_units(M, N, K, true);
+    if (tp && tp->t < 0.97 * best_t * kKbCycles) {
+      best = Tiling{};
+      best.bn = 256;
+      best.tab = tp;
+      best.pair = true;
+      best.grid = tp->grid;
+    }
+  }
   return best;
 }
 
@@ -720,6 +1254,17 @@ bool forced_tiling(int M, int N, int K, int epi, Tiling* out) {
   if (!init) {
     init = true;
     if (const char* e = getenv("CCB_GEMM_FORCE")) sscanf(e, "%d,%d", &fb, &fs);
+  }
+  if (fs == 3 || fs == 4) {  // planned unit table: 3 single CTAs, 4 CTA pairs
+    const bool pair = fs == 4;
+    const TabPlan* tp = M <= 4096 && N % (pair ? 2 * TC_BM : TC_BM) == 0 ? plan_units(M, N, K, pair) : nullptr;
+    if (!tp) return false;
+    *out = Tiling{};
+    out->bn = 256;
+    out->tab = tp;
+    out->pair = pair;
+    out->grid = tp->grid;
+    return true;
   }
   if (fs == 2) {  // swap-AB with row tile fb
     if (fb <= 0 || fb % 16 || fb > 256 || N % TC_BM || epi == CC_EPI_SWIGLU) return false;
@@ -737,6 +1282,40 @@ int launch_epi(const void* A, int64_t lda, const void* B, int64_t ldb, void* C, 
   Tiling tl;
   if (!forced_tiling(M, N, K, EPI, &tl)) tl = pick_tiling(M, N, K, EPI, allow_split);
   if (tl.bn == 0) return fail(CC_E_UNSUP, "gemm_tc: N must be a multiple of 128 (SwiGLU: 256)");
+  if (tl.tab && tl.pair) {
+    CUtensorMap mw, mx[4];
+    int rc = make_map(&mw, B, N, K, ldb, TC_BM);
+    for (int i = 0; i < 4 && !rc; ++i) rc = make_map(&mx[i], A, M, K, lda, 128 >> i);
+    if (rc) return rc;
+    CUtensorMap mc;  // output: [M][N] (SwiGLU [M][N/2]) with leading dim ldc
+    rc = make_map(&mc, C, M, EPI == CC_EPI_SWIGLU ? N / 2 : N, ldc,
+                  EPI == CC_EPI_RESID_ADD ? -2 : EPI == CC_EPI_SWIGLU ? -3 : -1);
+    if (rc) return rc;
+    static bool attr_set = false;
+    if (!attr_set) {
+      cudaFuncSetAttribute(gemm_pair_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P2_SMEM);
+      attr_set = true;
+    }
+    static const int dbg = getenv("CCB_PAIR_DBG") ? atoi(getenv("CCB_PAIR_DBG")) : 0;
+    gemm_pair_kernel<EPI><<<tl.grid, TC_THREADS, P2_SMEM, st>>>(mw, mx[0], mx[1], mx[2], mx[3], mc, M, K, dbg,
+                                                               tl.tab->tab);
+    return check_launch("gemm_pair");
+  }
+  if (tl.tab) {
+    CUtensorMap mw, mx;
+    int rc = make_map(&mw, B, N, K, ldb, TC_BM);
+    if (rc) return rc;
+    const int box = sw_box();
+    rc = make_map(&mx, A, M, K, lda, box);
+    if (rc) return rc;
+    static bool attr_set = false;
+    if (!attr_set) {
+      cudaFuncSetAttribute(gemm_sw_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TcCfg<256>::SMEM);
+      attr_set = true;
+    }
+    gemm_sw_kernel<EPI><<<tl.grid, TC_THREADS, TcCfg<256>::SMEM, st>>>(mw, mx, C, ldc, M, K, box, tl.tab->tab);
+    return check_launch("gemm_sw");
+  }
   if constexpr (EPI != CC_EPI_SWIGLU) if (tl.swap) {
     // A slot <- weights B [N][K] (128-row boxes), B slot <- activations A [M][K]
     CUtensorMap mw, mx;

@@ -176,6 +176,49 @@ print('ok')
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
 
 
+@pytest.mark.parametrize("M", [802, 300, 37])
+@pytest.mark.parametrize("epi", ["store", "resid", "swiglu", "gelu"])
+def test_gemm_cta_pair_unit_table(N, M, epi):
+    """CTA-pair (cta_group::2) swap-AB GEMM with the host-planned unit table
+    and TMA-store / TMA-reduce-add epilogues: matches the fp32 reference and
+    is bit-identical to the 1-CTA data-parallel tiling."""
+    import subprocess
+    import sys
+
+    code = f"""
+import math, torch, sys
+sys.path.insert(0, '.')
+from paper_2502_15734_b200 import _native as N
+M, Nn, K = {M}, 1536, 1024
+g = torch.Generator(device='cuda').manual_seed(6)
+A = torch.randn((M, K), generator=g, device='cuda').bfloat16()
+B = (torch.randn((Nn, K), generator=g, device='cuda') / 32).bfloat16()
+acc = A.float() @ B.float().T
+epi = '{epi}'
+code = dict(store=N.EPI_STORE, resid=N.EPI_RESID_ADD, swiglu=N.EPI_SWIGLU, gelu=N.EPI_GELU)[epi]
+if epi == 'resid':
+    C = torch.ones((M, Nn), device='cuda'); ref = acc + 1
+elif epi == 'swiglu':
+    C = torch.empty((M, Nn // 2), device='cuda', dtype=torch.bfloat16)
+    a4 = acc.reshape(M, Nn // 128, 2, 64); ref = (torch.nn.functional.silu(a4[:, :, 0]) * a4[:, :, 1]).reshape(M, Nn // 2)
+else:
+    C = torch.empty((M, Nn), device='cuda', dtype=torch.bfloat16)
+    ref = torch.nn.functional.gelu(acc, approximate='tanh') if epi == 'gelu' else acc
+N.call('cc_gemm', N.ptr(A), K, N.ptr(B), K, N.ptr(C), C.shape[1], M, Nn, K, code, N.BF16, 4, N.stream_ptr())
+torch.testing.assert_close(C.float(), ref, atol=2e-2, rtol=2e-2)
+torch.save(C.cpu(), sys.argv[1])
+print('ok')
+"""
+    outs = []
+    for i, force in enumerate(["0,4", "256,0"]):
+        path = f"/tmp/_pair_{epi}_{M}_{i}.pt"
+        env = dict(__import__("os").environ, CCB_GEMM_FORCE=force)
+        out = subprocess.run([sys.executable, "-c", code, path], capture_output=True, text=True, env=env, timeout=300)
+        assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
+        outs.append(torch.load(path))
+    assert torch.equal(outs[0], outs[1])
+
+
 @pytest.mark.parametrize("Nn", [512, 6144, 1536])
 def test_gemm_tcgen05_m_invariance(N, Nn):
     """A row's result does not depend on how many rows are active (also when

@@ -8,7 +8,7 @@ sys.path.insert(0, ".")
 from paper_2502_15734_b200 import _native as N
 
 M, Nn, K = (int(x) for x in sys.argv[1:4])
-epi = {"store": N.EPI_STORE, "resid": N.EPI_RESID_ADD, "swiglu": N.EPI_SWIGLU}[sys.argv[4]]
+epi = {"store": N.EPI_STORE, "resid": N.EPI_RESID_ADD, "swiglu": N.EPI_SWIGLU, "gelu": N.EPI_GELU}[sys.argv[4]]
 reps = int(sys.argv[5]) if len(sys.argv) > 5 else 3
 A = torch.randn((M, K), device="cuda").bfloat16()
 B = (torch.randn((Nn, K), device="cuda") / 64).bfloat16()
