@@ -169,6 +169,10 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
   }
   if (warp == 1) tmem_alloc<512>(tmem_slot);
   __syncthreads();
+  // PDL: the prologue above overlapped the predecessor's tail; its outputs
+  // (q_rot, k_rot, kv_v) are read from here on
+  pdl_trigger();
+  pdl_wait();
   // per-CTA key range: max causal limit over valid rows
   if (threadIdx.x < 128) {
     int r = row0 + threadIdx.x / G;
@@ -605,10 +609,9 @@ int launch(const void* q, const void* k, const void* v, const int32_t* q_slot, c
   }
   dim3 grid(Hkv, row_tiles, do_split ? 2 : 1);
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)DH);
-  attn_tc_kernel<DH><<<grid, AT_THREADS, AtSmem<DH>::TOTAL, st>>>(mq, mk, mv, q_slot, key_pad, (__nv_bfloat16*)ctx,
-                                                                  lse, n_q, n_keys, Hq, G, scale_log2, g_attn_trace,
-                                                                  split_min, ws_o, ws_ml, counters);
-  return check_launch("attention_tc");
+  return launch_k(attn_tc_kernel<DH>, grid, dim3(AT_THREADS), AtSmem<DH>::TOTAL, st, "attention_tc", mq, mk, mv, q_slot,
+                  key_pad, (__nv_bfloat16*)ctx, lse, n_q, n_keys, Hq, G, scale_log2, g_attn_trace, split_min, ws_o,
+                  ws_ml, counters);
 }
 
 }  // namespace

@@ -2,10 +2,18 @@
 // C[M,N] = A[M,K] B[N,K]^T, fp32 accumulation in TMEM, fused epilogues
 // (model.py:399-401 QKV, :417 o_proj + residual, :418-419 MLP).
 //
-// Persistent, warp-specialised, one CTA per SM:
-//   warp 0     TMA producer (A and B tiles, 128B swizzle, 4-stage ring)
-//   warp 1     MMA issuer (single thread, tcgen05.mma 128x256x16) + TMEM owner
+// Two kernels, both persistent and warp-specialised (one CTA per SM):
+//   gemm_tc_kernel    1-CTA 128 x BN tiles (data-parallel, stream-K tail, or
+//                     swap-AB with the activation rows as the MMA N side)
+//   gemm_pair_kernel  CTA pairs (cta_group::2), 256 weight rows x n activation
+//                     rows per unit from a host-planned unit table, TMA-store /
+//                     TMA-reduce-add epilogues; pick_tiling chooses per shape
+//   warp 0     TMA producer (A and B tiles, 128B swizzle, 4-6 stage ring)
+//   warp 1     MMA issuer (single thread, tcgen05.mma) + TMEM owner
 //   warps 2-5  epilogue (tcgen05.ld 32 lanes x 32 cols -> registers -> global)
+// Both launch with programmatic dependent launch when enabled (cc_set_pdl):
+// barrier init, TMEM allocation and the first weight tiles are issued before
+// griddepcontrol.wait.
 // Two TMEM accumulators (2 x 256 columns) let tile i's epilogue overlap tile
 // i+1's MMAs.  Tiles are walked M-fastest so the CTAs of one wave share the
 // weight tile through L2.  Wave quantisation (M ~ 800 gives 112-224 tiles on
@@ -205,6 +213,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_trigger();
+  if (warp != 0) pdl_wait();  // (the producer waits after issuing its first weight tiles)
 
   if (warp == 0) {
     if (lane == 0) {
@@ -212,15 +222,40 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       uint32_t phase = 0;
       UnitIter it(num_kb, t_dp, W, gridDim.x, blockIdx.x);
       Unit w;
-      while (it.next(w)) {
-        const int num_n = (N + TC_BN - 1) / TC_BN;
-        // (swap: row tiles fastest so a wave's CTAs share each weight tile)
-        const int mt = SWAP ? w.tile / num_n : w.tile % num_m, nt = SWAP ? w.tile % num_n : w.tile / num_m;
+      const int num_n = (N + TC_BN - 1) / TC_BN;
+      // (swap: row tiles fastest so a wave's CTAs share each weight tile)
+      auto tile_mn = [&](const Unit& x, int& mt, int& nt) {
+        mt = SWAP ? x.tile / num_n : x.tile % num_m;
+        nt = SWAP ? x.tile % num_n : x.tile / num_m;
+      };
+      bool have = it.next(w);
+      // PDL: the weight tiles of the first ring fill do not depend on the
+      // predecessor kernel -> issue them before griddepcontrol.wait
+      int pre = 0;
+      if (have) {
+        int mt, nt;
+        tile_mn(w, mt, nt);
+        pre = min(TC_STAGES, w.k1 - w.k0);
+        for (int i = 0; i < pre; ++i) {
+          mbar_expect_tx(&full[i], TC_A_BYTES + TC_B_BYTES);
+          if (SWAP) tma_load_2d(sA + i * TC_A_BYTES, &tmA, &full[i], (w.k0 + i) * TC_BK, mt * TC_BM);
+          else tma_load_2d(sB + i * TC_B_BYTES, &tmB, &full[i], (w.k0 + i) * TC_BK, nt * TC_BN);
+        }
+      }
+      pdl_wait();
+      for (bool first = true; have; first = false, have = it.next(w)) {
+        int mt, nt;
+        tile_mn(w, mt, nt);
         for (int kb = w.k0; kb < w.k1; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1);
-          mbar_expect_tx(&full[stage], TC_A_BYTES + TC_B_BYTES);
-          tma_load_2d(sA + stage * TC_A_BYTES, &tmA, &full[stage], kb * TC_BK, mt * TC_BM);
-          tma_load_2d(sB + stage * TC_B_BYTES, &tmB, &full[stage], kb * TC_BK, nt * TC_BN);
+          if (first && kb - w.k0 < pre) {  // weights already in flight: the activation tile only
+            if (SWAP) tma_load_2d(sB + stage * TC_B_BYTES, &tmB, &full[stage], kb * TC_BK, nt * TC_BN);
+            else tma_load_2d(sA + stage * TC_A_BYTES, &tmA, &full[stage], kb * TC_BK, mt * TC_BM);
+          } else {
+            mbar_wait(&empty[stage], phase ^ 1);
+            mbar_expect_tx(&full[stage], TC_A_BYTES + TC_B_BYTES);
+            tma_load_2d(sA + stage * TC_A_BYTES, &tmA, &full[stage], kb * TC_BK, mt * TC_BM);
+            tma_load_2d(sB + stage * TC_B_BYTES, &tmB, &full[stage], kb * TC_BK, nt * TC_BN);
+          }
           if (++stage == TC_STAGES) { stage = 0; phase ^= 1; }
         }
       }
@@ -461,16 +496,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   }
 }
 
-// ---- swap-AB with a host-planned unit table --------------------------------
-// The activation rows are the MMA N dimension, so a unit may cover any
-// multiple of 16 rows (<= 256) of one 128-feature weight tile.  The host cuts
-// every feature tile's rows into chunks and assigns the units to the
-// persistent CTAs longest-first (LPT), passed as a kernel parameter: at M ~ 800
-// the gate/up GEMM (224 feature tiles) runs ~5.0 tile-times per SM instead
-// of 6 whole waves of 128 x 256 tiles.  Every output element is still produced
-// by one unit with the full K reduction in order (no split, no workspace).
-constexpr int SW_MAXG = 160;   // >= SM count
-constexpr int SW_MAXU = 1792;  // units per launch
+// ---- unit table (host-planned work list of the CTA-pair kernel) -----------
+// With the activation rows as the MMA N dimension a unit may cover any
+// multiple of 32 rows (<= 256) of one 256-feature weight tile.  The host cuts
+// every weight tile's rows into chunks and assigns the units to the CTA pairs
+// (plan_units), passed as a kernel parameter.  Every output element is still
+// produced by one unit with the full K reduction in order (no split, no
+// workspace).
+constexpr int SW_MAXG = 80;    // CTA pairs (>= SM count / 2)
+constexpr int SW_MAXU = 4096;  // units per launch (the table rides in the kernel parameters: <= 32 KiB)
 struct SwTab {
   uint16_t start[SW_MAXG + 1];  // CTA c runs units [start[c], start[c+1])
   uint32_t unit[SW_MAXU];       // feature tile | (row0 / 16) << 14 | (rows / 16 - 1) << 25
@@ -478,182 +512,16 @@ struct SwTab {
 __host__ __device__ constexpr uint32_t sw_pack(int ft, int r0, int n) {
   return (uint32_t)ft | ((uint32_t)(r0 >> 4) << 14) | ((uint32_t)((n >> 4) - 1) << 25);
 }
-// activation rows per TMA box: a unit loads ceil(rows / box) boxes (rows past
-// the unit are other units' rows or zero fill, unused)
-inline int sw_box() {
-  static int b = [] {
-    const char* e = getenv("CCB_SW_BOX");
-    const int v = e ? atoi(e) : 64;
-    return (v == 32 || v == 64 || v == 128 || v == 256) ? v : 64;
-  }();
-  return b;
-}
-
-template <int EPI>
-__global__ void __launch_bounds__(TC_THREADS, 1)
-    gemm_sw_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX, void* C,
-                   int64_t ldc, int M, int K, int box, const __grid_constant__ SwTab tab) {
-  constexpr int B_BYTES = TcCfg<256>::B_BYTES;
-  constexpr int STAGES = TcCfg<256>::STAGES;
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sA = base;
-  uint8_t* sB = base + STAGES * TC_A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_BYTES);
-  uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;
-  uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  float4* stg_base = reinterpret_cast<float4*>(sB + STAGES * B_BYTES + 256);
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int num_kb = K / TC_BK;
-  const int u_begin = tab.start[blockIdx.x], u_end = tab.start[blockIdx.x + 1];
-
-  if (warp == 0 && lane == 0) {
-    tma_prefetch(&tmW);
-    tma_prefetch(&tmX);
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
-    }
-    for (int a = 0; a < 2; ++a) {
-      mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 128);
-    }
-    fence_barrier_init();
-  }
-  if (warp == 1) tmem_alloc<512>(tmem_slot);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem_base = *tmem_slot;
-
-  if (warp == 0) {
-    if (lane == 0) {
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int u = u_begin; u < u_end; ++u) {
-        const uint32_t e = tab.unit[u];
-        const int ft = e & 0x3fff, r0 = ((e >> 14) & 0x7ff) * 16, n = (((e >> 25) & 0xf) + 1) * 16;
-        const int nbox = (n + box - 1) / box;
-        for (int kb = 0; kb < num_kb; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1);
-          mbar_expect_tx(&full[stage], TC_A_BYTES + nbox * box * TC_BK * 2);
-          tma_load_2d(sA + stage * TC_A_BYTES, &tmW, &full[stage], kb * TC_BK, ft * TC_BM);
-          for (int b = 0; b < nbox; ++b)
-            tma_load_2d(sB + stage * B_BYTES + b * box * TC_BK * 2, &tmX, &full[stage], kb * TC_BK, r0 + b * box);
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
-        }
-      }
-    }
-  } else if (warp == 1) {
-    if (lane == 0) {
-      int stage = 0;
-      uint32_t phase = 0;
-      int acc = 0;
-      uint32_t acc_phase = 0;
-      for (int u = u_begin; u < u_end; ++u) {
-        const int n = (((tab.unit[u] >> 25) & 0xf) + 1) * 16;
-        const uint32_t idesc = idesc_bf16_f32(TC_BM, n);
-        mbar_wait(&tempty[acc], acc_phase ^ 1);
-        tc_fence_after();
-        const uint32_t d_tmem = tmem_base + acc * 256;
-        for (int kb = 0; kb < num_kb; ++kb) {
-          mbar_wait(&full[stage], phase);
-          tc_fence_after();
-          const uint64_t ad = desc_sw128(sA + stage * TC_A_BYTES);
-          const uint64_t bd = desc_sw128(sB + stage * B_BYTES);
-#pragma unroll
-          for (int k = 0; k < TC_BK / 16; ++k) mma_bf16(d_tmem, ad + 2 * k, bd + 2 * k, idesc, (kb > 0 || k > 0) ? 1u : 0u);
-          mma_commit(&empty[stage]);
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
-        }
-        mma_commit(&tfull[acc]);
-        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
-      }
-    }
-  } else {
-    const int q = warp & 3;  // TMEM lane quarter = output features q*32 .. +31 of the tile
-    // per-warp 4 KiB slabs; SwiGLU: the up-feature warps (q = 2, 3) hand their
-    // accumulators to the gate-feature warps (q = 0, 1) through slab q - 2
-    const uint32_t xch = smem_u32(stg_base + (q >= 2 ? q - 2 : q) * 256);
-    int acc = 0;
-    uint32_t acc_phase = 0;
-    for (int u = u_begin; u < u_end; ++u) {
-      const uint32_t e = tab.unit[u];
-      const int ft = e & 0x3fff, r0 = ((e >> 14) & 0x7ff) * 16, n = (((e >> 25) & 0xf) + 1) * 16;
-      mbar_wait(&tfull[acc], acc_phase);
-      tc_fence_after();
-      const uint32_t t0 = tmem_base + acc * 256 + ((uint32_t)(q * 32) << 16);
-      const int feat = ft * TC_BM + q * 32 + lane;
-#pragma unroll 1
-      for (int c = 0; c * 32 < n; ++c) {
-        const int row = r0 + c * 32;
-        const int jmax = min(32, min(n - c * 32, M - row));  // rows of this chunk in unit and matrix
-        if (jmax <= 0) break;
-        uint32_t r[32];
-        tmem_ld32(t0 + c * 32, r);
-        tmem_ld_wait();
-        if constexpr (EPI == CC_EPI_SWIGLU) {
-          // weight tile = [gate 64 | up 64] -> outputs ft * 64 + 0..63
-          if (q >= 2) {
-#pragma unroll
-            for (int j = 0; j < 32; ++j)
-              asm volatile("st.shared.b32 [%0], %1;" ::"r"(xch + (j * 32 + lane) * 4), "r"(r[j]) : "memory");
-          }
-          epi_bar();
-          if (q < 2) {
-            __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(C) + (int64_t)row * ldc + ft * 64 + q * 32 + lane;
-#pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              float up;
-              asm volatile("ld.shared.f32 %0, [%1];" : "=f"(up) : "r"(xch + (j * 32 + lane) * 4) : "memory");
-              if (j < jmax) out[(int64_t)j * ldc] = __float2bfloat16_rn(silu(__uint_as_float(r[j])) * up);
-            }
-          }
-          epi_bar();  // slab reusable
-        } else if constexpr (EPI == CC_EPI_RESID_ADD) {
-          float* h = reinterpret_cast<float*>(C) + (int64_t)row * ldc + feat;
-          float cv[32];
-#pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if (j < jmax) cv[j] = h[(int64_t)j * ldc];
-#pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if (j < jmax) h[(int64_t)j * ldc] = cv[j] + __uint_as_float(r[j]);
-        } else {
-          __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(C) + (int64_t)row * ldc + feat;
-#pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            if (j >= jmax) continue;
-            float x = __uint_as_float(r[j]);
-            if constexpr (EPI == CC_EPI_GELU) x = gelu_tanh(x);
-            out[(int64_t)j * ldc] = __float2bfloat16_rn(x);
-          }
-        }
-      }
-      tc_fence_before();
-      mbar_arrive(&tempty[acc]);
-      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 1) {
-    tc_fence_after();
-    tmem_dealloc<512>(tmem_base);
-  }
-}
 
 // ---- CTA-pair (cta_group::2) swap-AB with a unit table ----------------------
-// A 1-CTA 128 x 256 tile streams 48 KiB of operands into the SM per k-block,
-// and the SM ingests ~64 B/clk, so it runs at ~768 cycles per k-block where
-// the MMA needs 512: the kernels above are operand-feed bound.  A CTA pair
-// computes a 256-feature x n-row tile with one tcgen05.mma.cta_group::2: each
-// SM holds its 128 weight rows and HALF of the n activation rows (the MMA
-// reads the other half from the peer's smem), so the feed per SM for n = 256
-// is 32 KiB per k-block — matched to the MMA.  The leader CTA (rank 0) issues
+// A 1-CTA 128 x 256 tile moves 48 KiB into shared memory per k-block (TMA)
+// and the MMA reads the same 48 KiB back: ~768 cycles at the ~128 B/clk
+// shared-memory port where the MMA needs 512, so the kernel above is
+// operand-feed bound (measured ~430 ns per k-block).  A CTA pair computes a
+// 256-feature x n-row tile with one tcgen05.mma.cta_group::2: each SM holds
+// its 128 weight rows and HALF of the n activation rows (the pair's tensor
+// cores exchange the halves), so for n = 256 an SM moves 32 KiB in and 32 KiB
+// out per k-block — matched to the MMA's 512 cycles.  The leader CTA (rank 0) issues
 // the MMAs; both CTAs load through TMA onto the leader's full barrier, the
 // commits multicast to both CTAs' empty / accumulator-full barriers, and both
 // CTAs' epilogue warps release the accumulator to the leader's barrier.
@@ -706,26 +574,44 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_trigger();
+  if (warp != 0) pdl_wait();  // (the producer waits after issuing its first weight tiles)
 
   if (warp == 0) {
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
+      // PDL: the first ring fill's weight tiles do not depend on the predecessor
+      int pre = 0;
+      if (u_begin < u_end && !(dbg & 2)) {
+        const uint32_t e = tab.unit[u_begin];
+        const int fp = e & 0x3fff, n = (((e >> 25) & 0xf) + 1) * 16;
+        pre = min(P2_STAGES, num_kb);
+        for (int i = 0; i < pre; ++i) {
+          const uint32_t fb = mapa_shared(smem_u32(&full[i]), 0);
+          if (rank == 0) mbar_expect_tx(&full[i], 2 * (TC_A_BYTES + (n / 2) * TC_BK * 2));
+          tma_load_2d_pair(sA + i * TC_A_BYTES, &tmW, fb, i * TC_BK, fp * 2 * TC_BM + (int)rank * TC_BM);
+        }
+      }
+      pdl_wait();
       for (int u = u_begin; u < u_end; ++u) {
         const uint32_t e = tab.unit[u];
         const int fp = e & 0x3fff, r0 = ((e >> 14) & 0x7ff) * 16, n = (((e >> 25) & 0xf) + 1) * 16;
         const int h = n / 2;  // rows per CTA (multiple of 16)
         const int rows0 = r0 + (int)rank * h;
         for (int kb = 0; kb < num_kb; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1);
+          const bool prefetched = u == u_begin && kb < pre;
+          if (!prefetched) mbar_wait(&empty[stage], phase ^ 1);
           if ((dbg & 2) && (u > u_begin || kb >= P2_STAGES)) {  // debug: MMA on stale tiles (no feed)
             if (rank == 0) mbar_arrive(&full[stage]);
             if (++stage == P2_STAGES) { stage = 0; phase ^= 1; }
             continue;
           }
           const uint32_t fb = mapa_shared(smem_u32(&full[stage]), 0);
-          if (rank == 0) mbar_expect_tx(&full[stage], 2 * (TC_A_BYTES + h * TC_BK * 2));
-          tma_load_2d_pair(sA + stage * TC_A_BYTES, &tmW, fb, kb * TC_BK, fp * 2 * TC_BM + (int)rank * TC_BM);
+          if (!prefetched) {
+            if (rank == 0) mbar_expect_tx(&full[stage], 2 * (TC_A_BYTES + h * TC_BK * 2));
+            tma_load_2d_pair(sA + stage * TC_A_BYTES, &tmW, fb, kb * TC_BK, fp * 2 * TC_BM + (int)rank * TC_BM);
+          }
           uint8_t* dst = sB + stage * P2_B_BYTES;
           int off = 0;
           if (h & 128) { tma_load_2d_pair(dst, &tmX128, fb, kb * TC_BK, rows0); off += 128; }
@@ -951,8 +837,7 @@ struct TabPlan;
 struct Tiling {
   int bn = 0;
   bool swap = false;  // swap-AB: bn = activation-row tile width, A slot = 128-row weight tiles
-  const TabPlan* tab = nullptr;  // swap-AB with a planned unit table (gemm_sw_kernel / gemm_pair_kernel)
-  bool pair = false;
+  const TabPlan* tab = nullptr;  // CTA-pair swap-AB with a planned unit table (gemm_pair_kernel)
   int t_dp = 0;
   long long W = 0;  // stream-K k-blocks (0: pure data-parallel)
   int grid = 0;
@@ -985,13 +870,11 @@ int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, void* C, int64_t ldc
       if (cudaMalloc(&sc.ws, sizeof(float) * need) != cudaSuccess) return fail(CC_E_CUDA, "gemm_tc: workspace");
     }
     sc.epoch = (sc.epoch + 1) & 0x3fffffff;
-    gemm_tc_kernel<EPI, BN, true><<<tl.grid, TC_THREADS, TcCfg<BN>::SMEM, st>>>(ma, mb, C, ldc, M, N, K, tl.t_dp,
-                                                                               tl.W, sc.ws, sc.flags, sc.epoch, g_trace, PeerTab{});
-  } else {
-    gemm_tc_kernel<EPI, BN, false><<<tl.grid, TC_THREADS, TcCfg<BN>::SMEM, st>>>(ma, mb, C, ldc, M, N, K, tiles, 0,
-                                                                                nullptr, nullptr, 0, g_trace, PeerTab{});
+    return launch_k(gemm_tc_kernel<EPI, BN, true>, dim3(tl.grid), dim3(TC_THREADS), TcCfg<BN>::SMEM, st, "gemm_tc",
+                    ma, mb, C, ldc, M, N, K, tl.t_dp, tl.W, sc.ws, sc.flags, sc.epoch, g_trace, PeerTab{});
   }
-  return check_launch("gemm_tc");
+  return launch_k(gemm_tc_kernel<EPI, BN, false>, dim3(tl.grid), dim3(TC_THREADS), TcCfg<BN>::SMEM, st, "gemm_tc", ma,
+                  mb, C, ldc, M, N, K, tiles, 0LL, (float*)nullptr, (int*)nullptr, 0, g_trace, PeerTab{});
 }
 
 // tile widths: any multiple of 32 <= 256 (ragged last N tile); a width that
@@ -1010,9 +893,9 @@ int launch_swap(const CUtensorMap& mw, const CUtensorMap& mx, void* C, int64_t l
     attr_set = true;
   }
   const int tiles = ((N + TC_BM - 1) / TC_BM) * n_tiles_of(M, BNR);
-  gemm_tc_kernel<EPI, BNR, false, true><<<tl.grid, TC_THREADS, TcCfg<BNR>::SMEM, st>>>(
-      mw, mx, C, ldc, N, M, K, tiles, 0, nullptr, nullptr, 0, g_trace, PeerTab{});
-  return check_launch("gemm_tc_swap");
+  return launch_k(gemm_tc_kernel<EPI, BNR, false, true>, dim3(tl.grid), dim3(TC_THREADS), TcCfg<BNR>::SMEM, st,
+                  "gemm_tc_swap", mw, mx, C, ldc, N, M, K, tiles, 0LL, (float*)nullptr, (int*)nullptr, 0, g_trace,
+                  PeerTab{});
 }
 
 // relative time of one k-block of a 128xBN tile (measured efficiency per width)
@@ -1078,45 +961,45 @@ double model_time(const Tiling& t, int M, int N, int K) {
   return ((double)(t.t_dp / t.grid) * nkb + per) * kc + (splits ? kFoldCost * t.bn / 256.0 : 0.0);
 }
 
-// ---- unit-table plans (gemm_sw_kernel / gemm_pair_kernel) -----------------
-// Time model in SM cycles per k-block (64-deep slice): the MMA (128 x n x 64
-// per SM: 2n cycles) against the operand feed at ~64 B/clk per SM (1-CTA:
-// 16 KiB weights + n rows; pair: 16 KiB + n/2 rows).  A 1-CTA 128 x 256 tile
-// is 768 cycles (feed bound, matches the measured ~430 ns per k-block); the
-// kb_cost() plans above are converted at that rate.
+// ---- unit-table plans (gemm_pair_kernel) -----------------------------------
+// Time model in SM cycles per k-block (64-deep slice).  A 1-CTA 128 x 256
+// tile streams 48 KiB into shared memory and the MMA reads 48 KiB back: at
+// the ~128 B/clk shared-memory port that is 768 cycles (matches the measured
+// ~430 ns per k-block; the kb_cost() plans above are converted at that
+// rate).  A pair unit of n rows: max(MMA 2n, operand feed 256 + n) per SM,
+// times the measured kPairFactor.
 constexpr double kKbCycles = 768.0;
 constexpr double kUnitOverhead = 2000.0;  // accumulator hand-off, pipeline turn (cycles)
+// measured: a pair k-block runs ~1.25x the ideal (the MMA's operand reads and
+// the TMA writes share the port); calibrated on the M = 802 / 2048 projection
+// shapes against the 1-CTA plans
+constexpr double kPairFactor = 1.25;
 
 struct TabPlan {
   SwTab tab;
-  int grid = 0;  // CTAs (pair plans: 2 per unit list)
+  int grid = 0;     // CTAs (2 per unit list)
   double t = 1e30;  // modelled makespan, cycles
 };
 
-// measured: a pair k-block runs ~1.25x the ideal max(MMA, feed) (shared-memory
-// port: the MMA reads and the TMA writes of a k-block share it); calibrated on
-// the M = 802 / 2048 projection shapes against the 1-CTA plans
-constexpr double kPairFactor = 1.25;
-
-inline double unit_cycles(int n, int nkb, bool pair) {
-  const double mma = 2.0 * n, feed = pair ? 256.0 + n : 256.0 + 2.0 * n;
-  return ((mma > feed ? mma : feed) * nkb + kUnitOverhead) * (pair ? kPairFactor : 1.0);
+inline double unit_cycles(int n, int nkb) {
+  const double mma = 2.0 * n, feed = 256.0 + n;
+  return ((mma > feed ? mma : feed) * nkb + kUnitOverhead) * kPairFactor;
 }
 
-// Cut each weight tile's (128 features; pair: 256) M rows into k chunks (j
-// chunks of 256 rows, the rest split evenly; granule 16 rows, pair 32), k
-// from ceil(M/256) to +3, assign the units longest-first to the least-loaded
-// CTA (pair), keep the smallest makespan.  Cached per shape.
-const TabPlan* plan_units(int M, int F, int K, bool pair) {
+// Cut each 256-feature weight tile's M rows into k chunks (j chunks of 256
+// rows, the rest split evenly, 32-row granules), k from ceil(M/256) to +3,
+// schedule the units onto the CTA pairs, keep the smallest makespan.  Cached
+// per shape (evicted plans are leaked, not freed: a caller may still hold one).
+const TabPlan* plan_units(int M, int F, int K) {
   static std::mutex mu;
   static std::unordered_map<uint64_t, TabPlan*> cache;
-  const uint64_t key = ((uint64_t)M << 44) ^ ((uint64_t)F << 20) ^ (uint64_t)K ^ (pair ? 1ull << 63 : 0);
+  const uint64_t key = ((uint64_t)M << 44) ^ ((uint64_t)F << 20) ^ (uint64_t)K;
   std::lock_guard<std::mutex> g(mu);
   auto it = cache.find(key);
   if (it != cache.end()) return it->second;
-  const int tile = pair ? 2 * TC_BM : TC_BM, gran = pair ? 32 : 16, maxb = 256 / gran;
-  const int ntile = F / tile, nkb = K / TC_BK;
-  int G = pair ? num_sms() / 2 : num_sms();
+  constexpr int gran = 32, maxb = 256 / gran;
+  const int ntile = F / (2 * TC_BM), nkb = K / TC_BK;
+  int G = num_sms() / 2;
   if (G > SW_MAXG) G = SW_MAXG;
   const int nb = (M + gran - 1) / gran, kmin = (nb + maxb - 1) / maxb;
   TabPlan* best = new TabPlan();
@@ -1137,7 +1020,7 @@ const TabPlan* plan_units(int M, int F, int K, bool pair) {
       units.clear();
       for (int ft = 0; ft < ntile; ++ft)
         for (int ci = 0, r0 = 0; ci < (int)ch.size(); r0 += ch[ci] * gran, ++ci)
-          units.push_back({unit_cycles(ch[ci] * gran, nkb, pair), ft, r0, ch[ci] * gran});
+          units.push_back({unit_cycles(ch[ci] * gran, nkb), ft, r0, ch[ci] * gran});
       // Units of one weight tile should run side by side (one HBM read of the
       // weights, the rest from L2): list-schedule them in (tile, chunk) order
       // onto the earliest-free CTA, except the last ~1.5 rounds of work, which
@@ -1170,13 +1053,13 @@ const TabPlan* plan_units(int M, int F, int K, bool pair) {
           for (int i : lists[c]) best->tab.unit[pos++] = sw_pack(units[i].ft, units[i].r0, units[i].n);
         }
         best->tab.start[nl] = (uint16_t)pos;
-        best->grid = pair ? 2 * nl : nl;
+        best->grid = 2 * nl;
       }
     }
   }
   if (getenv("CCB_SW_DEBUG")) {
-    fprintf(stderr, "[gemm_%s] M=%d F=%d K=%d makespan=%.0f cyc (%.2f x 768-cycle tiles) grid=%d chunks(x%d):",
-            pair ? "pair" : "sw", M, F, K, best->t, best->t / (kKbCycles * nkb), best->grid, gran);
+    fprintf(stderr, "[gemm_pair] M=%d F=%d K=%d makespan=%.0f cyc (%.2f x 768-cycle tiles) grid=%d chunks(x%d):", M,
+            F, K, best->t, best->t / (kKbCycles * nkb), best->grid, gran);
     for (int c : best_ch) fprintf(stderr, " %d", c);
     fprintf(stderr, "\n");
   }
@@ -1233,13 +1116,12 @@ Tiling pick_tiling(int M, int N, int K, int epi, bool allow_split) {
     }
   }
   // CTA-pair unit table (any epilogue; SwiGLU: [gate 64 | up 64] per 128 rows)
-  if (M >= 64 && M <= 2048 && N % (2 * TC_BM) == 0 && pair_enabled()) {
-    const TabPlan* tp = plan_units(M, N, K, true);
+  if (M >= 64 && M <= 8192 && N % (2 * TC_BM) == 0 && pair_enabled()) {
+    const TabPlan* tp = plan_units(M, N, K);
     if (tp && tp->t < 0.97 * best_t * kKbCycles) {
       best = Tiling{};
       best.bn = 256;
       best.tab = tp;
-      best.pair = true;
       best.grid = tp->grid;
     }
   }
@@ -1255,14 +1137,12 @@ bool forced_tiling(int M, int N, int K, int epi, Tiling* out) {
     init = true;
     if (const char* e = getenv("CCB_GEMM_FORCE")) sscanf(e, "%d,%d", &fb, &fs);
   }
-  if (fs == 3 || fs == 4) {  // planned unit table: 3 single CTAs, 4 CTA pairs
-    const bool pair = fs == 4;
-    const TabPlan* tp = M <= 4096 && N % (pair ? 2 * TC_BM : TC_BM) == 0 ? plan_units(M, N, K, pair) : nullptr;
+  if (fs == 4) {  // CTA-pair unit table
+    const TabPlan* tp = M <= 8192 && N % (2 * TC_BM) == 0 ? plan_units(M, N, K) : nullptr;
     if (!tp) return false;
     *out = Tiling{};
     out->bn = 256;
     out->tab = tp;
-    out->pair = pair;
     out->grid = tp->grid;
     return true;
   }
@@ -1282,7 +1162,7 @@ int launch_epi(const void* A, int64_t lda, const void* B, int64_t ldb, void* C, 
   Tiling tl;
   if (!forced_tiling(M, N, K, EPI, &tl)) tl = pick_tiling(M, N, K, EPI, allow_split);
   if (tl.bn == 0) return fail(CC_E_UNSUP, "gemm_tc: N must be a multiple of 128 (SwiGLU: 256)");
-  if (tl.tab && tl.pair) {
+  if (tl.tab) {
     CUtensorMap mw, mx[4];
     int rc = make_map(&mw, B, N, K, ldb, TC_BM);
     for (int i = 0; i < 4 && !rc; ++i) rc = make_map(&mx[i], A, M, K, lda, 128 >> i);
@@ -1297,24 +1177,8 @@ int launch_epi(const void* A, int64_t lda, const void* B, int64_t ldb, void* C, 
       attr_set = true;
     }
     static const int dbg = getenv("CCB_PAIR_DBG") ? atoi(getenv("CCB_PAIR_DBG")) : 0;
-    gemm_pair_kernel<EPI><<<tl.grid, TC_THREADS, P2_SMEM, st>>>(mw, mx[0], mx[1], mx[2], mx[3], mc, M, K, dbg,
-                                                               tl.tab->tab);
-    return check_launch("gemm_pair");
-  }
-  if (tl.tab) {
-    CUtensorMap mw, mx;
-    int rc = make_map(&mw, B, N, K, ldb, TC_BM);
-    if (rc) return rc;
-    const int box = sw_box();
-    rc = make_map(&mx, A, M, K, lda, box);
-    if (rc) return rc;
-    static bool attr_set = false;
-    if (!attr_set) {
-      cudaFuncSetAttribute(gemm_sw_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TcCfg<256>::SMEM);
-      attr_set = true;
-    }
-    gemm_sw_kernel<EPI><<<tl.grid, TC_THREADS, TcCfg<256>::SMEM, st>>>(mw, mx, C, ldc, M, K, box, tl.tab->tab);
-    return check_launch("gemm_sw");
+    return launch_k(gemm_pair_kernel<EPI>, dim3(tl.grid), dim3(TC_THREADS), P2_SMEM, st, "gemm_pair", mw, mx[0], mx[1],
+                    mx[2], mx[3], mc, M, K, dbg, tl.tab->tab);
   }
   if constexpr (EPI != CC_EPI_SWIGLU) if (tl.swap) {
     // A slot <- weights B [N][K] (128-row boxes), B slot <- activations A [M][K]

@@ -94,6 +94,8 @@ __global__ void __launch_bounds__(256) gather_rope_kernel(
     int kvw, int dh) {
   using A = typename Acc<T>::type;
   using VT = Vec<T, V>;
+  pdl_trigger();
+  pdl_wait();
   const cc_gather_item it = items[blockIdx.x];
   const int l = l0 + blockIdx.y;
   const int half = dh / 2;
@@ -243,6 +245,8 @@ template <typename T, int NV>
 __global__ void __launch_bounds__(128) rmsnorm_vec_kernel(const float* __restrict__ h, T* __restrict__ out,
                                                           const float* __restrict__ w, int d, float eps) {
   __shared__ float red[4];
+  pdl_trigger();
+  pdl_wait();
   const float4* x = reinterpret_cast<const float4*>(h + (int64_t)blockIdx.x * d);
   float4 v[NV];
   float ss = 0.f;
@@ -626,11 +630,10 @@ int cc_gather_rope_kv(const void* pool, int64_t pool_layer_stride, int64_t pool_
     int vec = std::min(pick_vec<T>(d_head / 2), pick_vec<T>(kv_width));
     return CCB_DISPATCH_VEC(vec, V, [&] {
       dim3 grid(n_items, l1 - l0);
-      gather_rope_kernel<T, V><<<grid, 256, 0, as_stream(stream)>>>(
-          (const T*)pool, pool_layer_stride, pool_block_stride, items, l0, slot_pos, active_until,
-          (const typename CS<T>::type*)rope_table, (T*)kv_k, (T*)kv_v, (T*)k_rot, req_layer_stride, kv_width,
-          d_head);
-      return check_launch("gather_rope_kv");
+      return launch_k(gather_rope_kernel<T, V>, grid, dim3(256), 0, as_stream(stream), "gather_rope_kv",
+                      (const T*)pool, pool_layer_stride, pool_block_stride, items, l0, slot_pos, active_until,
+                      (const typename CS<T>::type*)rope_table, (T*)kv_k, (T*)kv_v, (T*)k_rot, req_layer_stride,
+                      kv_width, d_head);
     });
   });
 }
@@ -667,12 +670,10 @@ int cc_rmsnorm(const void* hidden, void* out, const float* weight, int n_rows, i
     auto go = [&](auto tag) -> int {
       constexpr int NV = decltype(tag)::value;
       if (dtype == CC_BF16)
-        rmsnorm_vec_kernel<__nv_bfloat16, NV><<<n_rows, 128, 0, as_stream(stream)>>>(
-            (const float*)hidden, (__nv_bfloat16*)out, weight, d, (float)eps);
-      else
-        rmsnorm_vec_kernel<float, NV><<<n_rows, 128, 0, as_stream(stream)>>>((const float*)hidden, (float*)out, weight,
-                                                                             d, (float)eps);
-      return check_launch("rmsnorm_vec");
+        return launch_k(rmsnorm_vec_kernel<__nv_bfloat16, NV>, dim3(n_rows), dim3(128), 0, as_stream(stream),
+                        "rmsnorm_vec", (const float*)hidden, (__nv_bfloat16*)out, weight, d, (float)eps);
+      return launch_k(rmsnorm_vec_kernel<float, NV>, dim3(n_rows), dim3(128), 0, as_stream(stream), "rmsnorm_vec",
+                      (const float*)hidden, (float*)out, weight, d, (float)eps);
     };
     switch (nv) {
       case 1: return go(std::integral_constant<int, 1>{});

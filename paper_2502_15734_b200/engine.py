@@ -382,8 +382,18 @@ def _apply_cut(model, plan, ws, slots, new_depth):
                plan.n * cfg.kv_width(), cfg.kv_width(), cfg.head_dim(), model.dtype_code, N.stream_ptr())
 
 
-def execute(model: Model, plan: DevicePlan, ws: dict, *, record=False, record_values=False, stats=False,
-            gemm_impl=0, attn_impl=0, timer=None, focus: OnlineFocus | None = None):
+def execute(model: Model, plan: DevicePlan, ws: dict, **kw):
+    """Launch the per-layer pipeline (see _execute) with programmatic dependent
+    launch enabled for its kernels when model.prefill_pdl."""
+    prev = N.lib().cc_set_pdl(1 if getattr(model, "prefill_pdl", False) else 0)
+    try:
+        return _execute(model, plan, ws, **kw)
+    finally:
+        N.lib().cc_set_pdl(prev)
+
+
+def _execute(model: Model, plan: DevicePlan, ws: dict, *, record=False, record_values=False, stats=False,
+             gemm_impl=0, attn_impl=0, timer=None, focus: OnlineFocus | None = None):
     """Launch the per-layer pipeline on the current stream.  Returns the
     LazyAttention (if recording), value trace list and stats masses.
     Under tensor parallelism (model.tp) the o_proj and down_proj GEMMs write

@@ -16,6 +16,7 @@ reference architecture): ``n_kv_heads`` (GQA), ``d_ff``, ``mlp``
 from __future__ import annotations
 
 import math
+import os
 import weakref
 from dataclasses import dataclass, field
 
@@ -231,6 +232,9 @@ class Model:
         self.h2d_bytes_per_s = 50e9
         self._copy_stream = None
         self.l2_prefetch = False  # o_proj weights -> L2 during attention: measured -1% (noise level), off
+        # programmatic dependent launch for the prefill chain: each kernel's
+        # prologue (barriers, TMEM, first weight tiles) overlaps its predecessor
+        self.prefill_pdl = os.environ.get("CCB_PDL", "1") != "0"
         if tp is not None and tp.world > 1:
             from .parallel import local_config
 
