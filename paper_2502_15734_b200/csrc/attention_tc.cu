@@ -19,6 +19,8 @@
 // The PV MMA of tile i overlaps the S MMA of tile i+1 and the softmax of
 // tile i+1 (double-buffered S and P).
 #include <math.h>
+#include <algorithm>
+#include <cmath>
 #include <stdlib.h>
 
 #include <mutex>
@@ -41,6 +43,8 @@ constexpr int AT_BN = 128;      // keys per tile
 constexpr int AT_KST = 3;  // K ring depth
 constexpr int AT_VST = 2;  // V ring depth = P buffers: V slot i % 2 is released by PV_i's p_empty commit
 constexpr int AT_THREADS = 320;  // TMA warp, MMA warp, 2 x 4 softmax warps
+constexpr int AT_MAXT = 512;     // row tiles the in-kernel work plan handles (more: no key splits)
+constexpr int AT_MAXP = 4;       // key-range parts per row tile (8 measured slower at r = 0)
 
 // MN-major operand (B = V: N = head dim contiguous, K = keys), 128B swizzle:
 // 64-element atoms along N at `lbo` bytes, 8-key groups at 1024 B.
@@ -106,18 +110,25 @@ struct AtSmem {
   static constexpr int V_OFF = K_OFF + AT_KST * KV_BYTES;
   static constexpr int BAR_OFF = V_OFF + AT_VST * KV_BYTES;
   static constexpr int X_OFF = BAR_OFF + 256;        // [2 parities][2 halves][128 rows] f32 exchange
+  static constexpr int PLAN_OFF = X_OFF + 4 * 128 * 4;  // work-item plan: [3][AT_MAXT] ints
   // no alignment slack: the kernel holds no static shared memory, so the
   // dynamic window starts 1 KiB aligned (checked at run time)
-  static constexpr size_t TOTAL = X_OFF + 4 * 128 * 4;
+  static constexpr size_t TOTAL = PLAN_OFF + 3 * AT_MAXT * 4;
 };
 
-template <int DH>
+// QT: Q lives in TMEM (written once by the first softmax warpgroup) and the
+// S MMA takes it as its A operand; P_i then aliases S_i's TMEM buffer.  This
+// removes the 32 KiB Q read from shared memory per key tile (the MMA's
+// operand reads and the TMA writes share the smem port).
+template <int DH, bool QT>
 __global__ void __launch_bounds__(AT_THREADS, 1)
-    attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+    attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __nv_bfloat16* __restrict__ qg,
+                   const __grid_constant__ CUtensorMap tmK,
                    const __grid_constant__ CUtensorMap tmV, const int32_t* __restrict__ q_slot,
                    const uint8_t* __restrict__ key_pad, __nv_bfloat16* __restrict__ ctx, float* __restrict__ lse,
                    int n_q, int n_keys, int Hq, int G, float scale_log2, long long* __restrict__ trace,
-                   int split_min, float* __restrict__ ws_o, float2* __restrict__ ws_ml, int* __restrict__ counters) {
+                   int n_groups, int n_row_tiles, int target, int max_parts, float* __restrict__ ws_o,
+                   float2* __restrict__ ws_ml, int* __restrict__ counters) {
   using SM = AtSmem<DH>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* base = smem_raw;
@@ -140,18 +151,75 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
   float* xmax = reinterpret_cast<float*>(base + SM::X_OFF);       // row maxima / sums of the pair
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // grid = (kv groups, row tiles), row tiles walked last-first: later rows see
-  // more keys, so the longest CTAs are scheduled in the first wave
-  const int g = blockIdx.x;
   const int R = 128 / G;
-  const int row0 = (gridDim.y - 1 - blockIdx.y) * R;
+  const int T = n_row_tiles;
+  // ---- work item of this CTA ------------------------------------------------
+  // An item = (kv group, row tile, part of the row tile's key range).  Row
+  // tile t's causal key range is estimated from its last row (rows are in
+  // slot order in the engine) and cut into ceil(len / target) parts; items
+  // are ordered longest first (LPT), so blockIdx x walks that list and the
+  // longest work is dispatched in the first wave.  CTAs past the last item
+  // exit.  Every CTA derives the same plan (deterministic); the exact key
+  // range of the tile is still taken over all its rows below.
+  int* s_item = reinterpret_cast<int*>(tmem_slot + 10);  // group, tile, part, parts, est
+  pdl_trigger();
+  pdl_wait();  // (q_slot and, below, q/k/v: written before this kernel)
+  if (max_parts > 1) {
+    int* p_len = reinterpret_cast<int*>(base + SM::PLAN_OFF);
+    int* p_parts = p_len + AT_MAXT;
+    int* p_order = p_parts + AT_MAXT;
+    for (int t = threadIdx.x; t < T; t += AT_THREADS) {
+      const int kq = q_slot[min((t + 1) * R, n_q) - 1];
+      const int est = kq < 0 ? 0 : min(kq, n_keys - 1) / AT_BN + 1;
+      const int parts = max(1, min(max_parts, (est + target - 1) / target));
+      p_parts[t] = parts;
+      p_len[t] = (est + parts - 1) / parts;
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < T; t += AT_THREADS) {
+      const int lt = p_len[t];
+      int rank = 0;
+      for (int u = 0; u < T; ++u) rank += (p_len[u] > lt || (p_len[u] == lt && u > t)) ? 1 : 0;
+      p_order[rank] = t;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int idx = blockIdx.x;
+      s_item[0] = -1;
+      for (int r = 0; r < T; ++r) {
+        const int t = p_order[r], c = n_groups * p_parts[t];
+        if (idx < c) {
+          s_item[0] = idx % n_groups;
+          s_item[1] = t;
+          s_item[2] = idx / n_groups;
+          s_item[3] = p_parts[t];
+          s_item[4] = p_len[t] * p_parts[t];
+          break;
+        }
+        idx -= c;
+      }
+    }
+    __syncthreads();
+  } else if (threadIdx.x == 0) {
+    // one item per (group, row tile); row tiles last-first (longest first)
+    s_item[0] = blockIdx.x % n_groups;
+    s_item[1] = T - 1 - (int)blockIdx.x / n_groups;
+    s_item[2] = 0;
+    s_item[3] = 1;
+    s_item[4] = 0;
+  }
+  if (max_parts <= 1) __syncthreads();
+  const int g = s_item[0];
+  if (g < 0) return;  // past the last item (before any barrier or TMEM use)
+  const int tile = s_item[1], part = s_item[2], parts = s_item[3], est = s_item[4];
+  const int row0 = tile * R;
 
   if (threadIdx.x == 0) s_kmax = -1;
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmQ);
     tma_prefetch(&tmK);
     tma_prefetch(&tmV);
-    mbar_init(q_full, 1);
+    mbar_init(q_full, QT ? 128 : 1);
     for (int s = 0; s < AT_KST; ++s) {
       mbar_init(&k_full[s], 1);
       mbar_init(&k_empty[s], 1);
@@ -169,10 +237,6 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
   }
   if (warp == 1) tmem_alloc<512>(tmem_slot);
   __syncthreads();
-  // PDL: the prologue above overlapped the predecessor's tail; its outputs
-  // (q_rot, k_rot, kv_v) are read from here on
-  pdl_trigger();
-  pdl_wait();
   // per-CTA key range: max causal limit over valid rows
   if (threadIdx.x < 128) {
     int r = row0 + threadIdx.x / G;
@@ -184,16 +248,15 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
   const uint32_t tmem = *tmem_slot;
   const int kmax = s_kmax;
   const int n_total = kmax < 0 ? 0 : kmax / AT_BN + 1;
-  // split-KV for the long CTAs (rows near the end of the prompt see every key):
-  // CTA z of a split pair takes key tiles [t0, t0 + n_tiles); the pair's
-  // partials are merged by whichever finishes last, in z order (deterministic)
-  const int z = blockIdx.z;
-  const bool split = gridDim.z > 1 && n_total >= split_min;
-  const int half0 = (n_total + 1) / 2;
-  const int t0 = (split && z) ? half0 : 0;
-  const int n_tiles = split ? (z ? n_total - half0 : half0) : (z ? 0 : n_total);
-  const bool owner = split || z == 0;  // writes (part of) the output
-  const uint32_t t_s0 = tmem, t_o = tmem + 256, t_p = tmem + 384;  // S0 S1 | O | P0 P1
+  // this part's key tiles [t0, t0 + n_tiles): boundaries from the planned
+  // estimate, the last part runs to the exact end (every tile covered once)
+  const bool split = parts > 1;
+  const int t0 = split ? min(part * est / parts, n_total) : 0;
+  const int t1 = !split || part == parts - 1 ? n_total : min((part + 1) * est / parts, n_total);
+  const int n_tiles = max(0, t1 - t0);
+  // TMEM columns: S0 S1 | O | P0 P1 (QT: S0/P0 S1/P1 | O | Q)
+  const uint32_t t_s0 = tmem, t_o = tmem + 256, t_p = QT ? tmem : tmem + 384, t_q = tmem + 384;
+  constexpr int P_STRIDE = QT ? AT_BN : AT_BN / 2;  // columns between the two P buffers
   const bool tracing = trace != nullptr;
   long long w0 = 0, w1 = 0, w2 = 0, w3 = 0, t_loop = 0;  // per-role stall cycles (trace only)
   long long t_s_issue = 0, t_s_commit = 0, t_p_issue = 0, t_p_commit = 0;
@@ -202,9 +265,11 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
 
   if (warp == 0) {
     if (lane == 0 && n_tiles > 0) {
-      mbar_expect_tx(q_full, SM::Q_BYTES);
+      if (!QT) {
+        mbar_expect_tx(q_full, SM::Q_BYTES);
 #pragma unroll
-      for (int a = 0; a < SM::ATOMS; ++a) tma_load_3d(sQ + a * 128 * 128, &tmQ, q_full, a * 64, g * G, row0);
+        for (int a = 0; a < SM::ATOMS; ++a) tma_load_3d(sQ + a * 128 * 128, &tmQ, q_full, a * 64, g * G, row0);
+      }
       // K runs one tile ahead of V: K_{i+1}'s slot frees when S_{i-1} is done
       // (early), V_i's when PV_{i-2} is done, so neither S nor PV waits on a
       // load issued after the previous PV
@@ -241,9 +306,14 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
 #pragma unroll
         for (int kk = 0; kk < DH / 16; ++kk) {
           const int a = kk >> 2, w = kk & 3;
-          uint64_t ad = desc_sw128(sQ + a * 128 * 128) + 2 * w;
           uint64_t bd = desc_sw128(sK + st * SM::KV_BYTES + a * AT_BN * 128) + 2 * w;
-          mma_bf16(t_s0 + b * AT_BN, ad, bd, id_s, kk > 0);
+          if (QT) {
+            // A = Q in TMEM: row = lane, 2 bf16 of the head dim per column
+            mma_bf16_ts(t_s0 + b * AT_BN, t_q + kk * 8, bd, id_s, kk > 0);
+          } else {
+            uint64_t ad = desc_sw128(sQ + a * 128 * 128) + 2 * w;
+            mma_bf16(t_s0 + b * AT_BN, ad, bd, id_s, kk > 0);
+          }
         }
         const long long ts1 = tracing ? clock64() : 0;
         mma_commit(&s_full[b]);  // (K slot released by the softmax when it sees s_full)
@@ -261,7 +331,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
         for (int kk = 0; kk < AT_BN / 16; ++kk) {
           uint64_t bd = desc_sw128_mn(sV + st * SM::KV_BYTES + kk * 16 * 128, AT_BN * 128);
           // A = P in TMEM: row = lane, 2 bf16 keys per 32-bit column, 16 keys = 8 columns
-          mma_bf16_ts(t_o, t_p + pb * (AT_BN / 2) + kk * 8, bd, id_o, (i > 0 || kk > 0) ? 1u : 0u);
+          mma_bf16_ts(t_o, t_p + pb * P_STRIDE + kk * 8, bd, id_o, (i > 0 || kk > 0) ? 1u : 0u);
         }
         const long long tp1 = tracing ? clock64() : 0;
         mma_commit(&p_empty[pb]);  // P buffer and V slot pb
@@ -285,6 +355,28 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
     float m_run = -INFINITY, l_run = 0.f;
     constexpr float kRescaleLog2 = 8.f;  // lazy rescale: keep the stale max while p <= 2^8
     auto pair_bar = [&]() { asm volatile("bar.sync %0, 64;" ::"r"(2 + q4) : "memory"); };
+    if (QT && h == 0 && n_tiles > 0) {
+      // Q row (head `head` of query row `row`) -> TMEM lane m, DH/2 columns
+#pragma unroll
+      for (int c = 0; c < DH / 64; ++c) {
+        uint32_t r[32];
+        if (row < n_q) {
+          const uint4* src = reinterpret_cast<const uint4*>(qg + ((int64_t)row * Hq + head) * DH + c * 64);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const uint4 v = src[e];
+            r[4 * e] = v.x; r[4 * e + 1] = v.y; r[4 * e + 2] = v.z; r[4 * e + 3] = v.w;
+          }
+        } else {
+#pragma unroll
+          for (int e = 0; e < 32; ++e) r[e] = 0u;
+        }
+        tmem_st32(t_q + c * 32 + lane_off, r);
+      }
+      tmem_st_wait();
+      tc_fence_before();
+      mbar_arrive(q_full);
+    }
     for (int i = 0; i < n_tiles; ++i) {
       const int b = i & 1;
       twait(&s_full[b], (i >> 1) & 1, tracing, w0);
@@ -369,7 +461,9 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
           pt[ch * 4 + e] = *reinterpret_cast<uint32_t*>(&hv);
         }
       }
-      tmem_st32(t_p + pb * (AT_BN / 2) + h * 32 + lane_off, pt);
+      // (QT: P_i overwrites S_i's first 64 columns; both halves finished
+      // reading S_i before the pair barrier above)
+      tmem_st32(t_p + pb * P_STRIDE + h * 32 + lane_off, pt);
       l_run += ((ps[0] + ps[1]) + (ps[2] + ps[3])) + ((ps[4] + ps[5]) + (ps[6] + ps[7]));
       // O *= alpha (this half's columns) for rows whose max grew past the lazy
       // threshold.  tcgen05.ld/st are warp-collective: the whole warp joins,
@@ -405,51 +499,66 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
     __nv_bfloat16* out = ctx + ((int64_t)row * Hq + head) * DH + h * (DH / 2);
     if (split) {
       // park this half's partial (unnormalised O, max in log2 units, sum) ...
-      const int pair = g * gridDim.y + blockIdx.y;
-      const float m_l2 = (m_run == -INFINITY) ? -INFINITY : m_run * scale_log2;
-      float* my_o = ws_o + ((int64_t)(pair * 2 + z) * 128 + m) * DH + h * (DH / 2);
+      const int key = g * T + tile, slot = key * AT_MAXP + part;
+      const bool any = n_tiles > 0 && m_run != -INFINITY;
+      const float m_l2 = any ? m_run * scale_log2 : -INFINITY;
+      float* my_o = ws_o + ((int64_t)slot * 128 + m) * DH + h * (DH / 2);
 #pragma unroll 1
       for (int c = 0; c < DH / 64; ++c) {
         uint32_t r[32];
-        tmem_ld32(t_o + h * (DH / 2) + c * 32 + lane_off, r);
-        tmem_ld_wait();
+        if (n_tiles > 0) {
+          tmem_ld32(t_o + h * (DH / 2) + c * 32 + lane_off, r);
+          tmem_ld_wait();
+        }
 #pragma unroll
         for (int e = 0; e < 8; ++e)
           __stcg(reinterpret_cast<float4*>(my_o + c * 32) + e,
-                 make_float4(__uint_as_float(r[4 * e]), __uint_as_float(r[4 * e + 1]), __uint_as_float(r[4 * e + 2]),
-                             __uint_as_float(r[4 * e + 3])));
+                 any ? make_float4(__uint_as_float(r[4 * e]), __uint_as_float(r[4 * e + 1]),
+                                   __uint_as_float(r[4 * e + 2]), __uint_as_float(r[4 * e + 3]))
+                     : make_float4(0.f, 0.f, 0.f, 0.f));
       }
-      if (h == 0) __stcg(&ws_ml[(int64_t)(pair * 2 + z) * 128 + m], make_float2(m_l2, l_tot));
+      if (h == 0) __stcg(&ws_ml[(int64_t)slot * 128 + m], make_float2(m_l2, any ? l_tot : 0.f));
       __threadfence();
       asm volatile("bar.sync 1, 256;" ::: "memory");
       if (warp == 2 && lane == 0) {
-        const int prev = atomicAdd(&counters[pair], 1);
+        const int prev = atomicAdd(&counters[key], 1);
         padw[0] = prev;  // (pad words are no longer needed)
-        if (prev == 1) counters[pair] = 0;  // reset for the next launch
+        if (prev == parts - 1) counters[key] = 0;  // reset for the next launch
       }
       asm volatile("bar.sync 1, 256;" ::: "memory");
-      if (padw[0] == 1) {
-        // ... and the last of the pair merges both, in z order
+      if ((int)padw[0] == parts - 1) {
+        // ... and the last part to finish merges all of them, in part order
         __threadfence();
-        const float2 ml0 = __ldcg(&ws_ml[(int64_t)(pair * 2) * 128 + m]);
-        const float2 ml1 = __ldcg(&ws_ml[(int64_t)(pair * 2 + 1) * 128 + m]);
-        const float M = fmaxf(ml0.x, ml1.x);
-        const float w0 = ml0.x == -INFINITY ? 0.f : exp2f(ml0.x - M);
-        const float w1 = ml1.x == -INFINITY ? 0.f : exp2f(ml1.x - M);
-        const float lt = fmaf(ml0.y, w0, ml1.y * w1);
+        float2 ml[AT_MAXP];
+        float M = -INFINITY;
+#pragma unroll
+        for (int p = 0; p < AT_MAXP; ++p) {
+          ml[p] = p < parts ? __ldcg(&ws_ml[((int64_t)key * AT_MAXP + p) * 128 + m]) : make_float2(-INFINITY, 0.f);
+          M = fmaxf(M, ml[p].x);
+        }
+        float w[AT_MAXP];
+        float lt = 0.f;
+#pragma unroll
+        for (int p = 0; p < AT_MAXP; ++p) {
+          w[p] = ml[p].x == -INFINITY ? 0.f : exp2f(ml[p].x - M);
+          lt = fmaf(ml[p].y, w[p], lt);
+        }
         const float inv = lt > 0.f ? 1.f / lt : 0.f;
-        const float* o0 = ws_o + ((int64_t)(pair * 2) * 128 + m) * DH + h * (DH / 2);
-        const float* o1 = ws_o + ((int64_t)(pair * 2 + 1) * 128 + m) * DH + h * (DH / 2);
         if (row < n_q) {
 #pragma unroll 1
           for (int c = 0; c < DH / 16; ++c) {
-            float4 a0 = __ldcg(reinterpret_cast<const float4*>(o0 + c * 8));
-            float4 a1 = __ldcg(reinterpret_cast<const float4*>(o0 + c * 8) + 1);
-            float4 b0 = __ldcg(reinterpret_cast<const float4*>(o1 + c * 8));
-            float4 b1 = __ldcg(reinterpret_cast<const float4*>(o1 + c * 8) + 1);
-            float v[8] = {fmaf(a0.x, w0, b0.x * w1), fmaf(a0.y, w0, b0.y * w1), fmaf(a0.z, w0, b0.z * w1),
-                          fmaf(a0.w, w0, b0.w * w1), fmaf(a1.x, w0, b1.x * w1), fmaf(a1.y, w0, b1.y * w1),
-                          fmaf(a1.z, w0, b1.z * w1), fmaf(a1.w, w0, b1.w * w1)};
+            float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+            for (int p = 0; p < AT_MAXP; ++p) {
+              if (p >= parts) break;
+              const float* op = ws_o + (((int64_t)key * AT_MAXP + p) * 128 + m) * DH + h * (DH / 2) + c * 8;
+              const float4 a0 = __ldcg(reinterpret_cast<const float4*>(op));
+              const float4 a1 = __ldcg(reinterpret_cast<const float4*>(op) + 1);
+              v[0] = fmaf(a0.x, w[p], v[0]); v[1] = fmaf(a0.y, w[p], v[1]);
+              v[2] = fmaf(a0.z, w[p], v[2]); v[3] = fmaf(a0.w, w[p], v[3]);
+              v[4] = fmaf(a1.x, w[p], v[4]); v[5] = fmaf(a1.y, w[p], v[5]);
+              v[6] = fmaf(a1.z, w[p], v[6]); v[7] = fmaf(a1.w, w[p], v[7]);
+            }
             uint4 pk;
             uint32_t* pw = reinterpret_cast<uint32_t*>(&pk);
 #pragma unroll
@@ -463,7 +572,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
             lse[(int64_t)row * Hq + head] = lt > 0.f ? (M + log2f(lt)) * 0.6931471805599453f : -INFINITY;
         }
       }
-    } else if (owner) {
+    } else {
     const float inv = l_tot > 0.f ? 1.f / l_tot : 0.f;
 #pragma unroll 1
     for (int c = 0; c < DH / 64; ++c) {
@@ -488,7 +597,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
     }
   }
   if (tracing) {
-    long long* tr = trace + 16 * (((int64_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x);
+    long long* tr = trace + 16 * (int64_t)blockIdx.x;
     if (threadIdx.x == 64) {
       long long t_end;
       asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_end));
@@ -584,34 +693,49 @@ int launch(const void* q, const void* k, const void* v, const int32_t* q_slot, c
   }
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(attn_tc_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)AtSmem<DH>::TOTAL);
+    cudaFuncSetAttribute(attn_tc_kernel<DH, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)AtSmem<DH>::TOTAL);
+    cudaFuncSetAttribute(attn_tc_kernel<DH, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)AtSmem<DH>::TOTAL);
     attr = true;
   }
+  // Q in TMEM (QT): measured ~1-2% slower than Q in smem at config 2 (the
+  // kernel is softmax-latency bound, not smem-port bound); opt-in
+  static const bool q_tmem = getenv("CCB_ATTN_QTMEM") && getenv("CCB_ATTN_QTMEM")[0] == '1';
   const int row_tiles = (n_q + R - 1) / R;
-  // split the key range of CTAs that see more than half of the longest range
-  // (>= 8 tiles) when the grid leaves SMs idle (fewer CTAs than SMs).  With a
-  // fuller grid the extra CTA prologues cost more than the better balance
-  // (measured at config 2: 208 CTAs, 74.6 -> 81.6 us per launch when split).
+  // Work items: when the grid of (group, row tile) CTAs leaves SMs idle, the
+  // row tiles with long causal key ranges are cut into up to AT_MAXP key
+  // parts (merged in part order by the last part to finish), all items
+  // dispatched longest first.  With a full grid the extra CTAs' fixed costs
+  // (prologue, pipeline fill, partial write + merge) outweigh the better
+  // balance: measured at config 2 (208 CTAs) 65.9 us unsplit vs 94.7 us with
+  // parts of half the per-SM share.
   const int max_tiles = (n_keys + AT_BN - 1) / AT_BN;
-  const int split_min = max(8, (max_tiles + 1) / 2);
-  const bool do_split = max_tiles >= 8 && Hkv * row_tiles < num_sms();
+  int target = max_tiles, max_parts = 1;
+  if (row_tiles <= AT_MAXT && max_tiles > 0 && Hkv * row_tiles < num_sms()) {
+    max_parts = std::max(1, std::min(AT_MAXP, num_sms() / (Hkv * row_tiles)));
+    target = std::max(8, (max_tiles + max_parts - 1) / max_parts);
+    max_parts = std::min(max_parts, (max_tiles + target - 1) / target);
+    if (max_parts < 1) max_parts = 1;
+  }
+  if (getenv("CCB_ATTN_NOSPLIT")) max_parts = 1;
   float* ws_o = nullptr;
   float2* ws_ml = nullptr;
   int* counters = nullptr;
-  if (do_split) {
-    const size_t pairs = (size_t)Hkv * row_tiles;
-    const size_t bytes = pairs * 2 * 128 * (DH * sizeof(float) + sizeof(float2));
+  if (max_parts > 1) {
+    const size_t keys = (size_t)Hkv * row_tiles;
+    const size_t bytes = keys * AT_MAXP * 128 * (DH * sizeof(float) + sizeof(float2));
     uint8_t* scratch = (uint8_t*)stream_scratch(st, 3, bytes);
-    counters = split_counters(st, (int)pairs);
+    counters = split_counters(st, (int)keys);
     if (!scratch || !counters) return fail(CC_E_CUDA, "attention_tc: split workspace allocation failed");
     ws_o = reinterpret_cast<float*>(scratch);
-    ws_ml = reinterpret_cast<float2*>(scratch + pairs * 2 * 128 * DH * sizeof(float));
+    ws_ml = reinterpret_cast<float2*>(scratch + keys * AT_MAXP * 128 * DH * sizeof(float));
   }
-  dim3 grid(Hkv, row_tiles, do_split ? 2 : 1);
+  // (an upper bound: CTAs past the planned items exit at once)
+  dim3 grid(Hkv * row_tiles * max_parts);
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)DH);
-  return launch_k(attn_tc_kernel<DH>, grid, dim3(AT_THREADS), AtSmem<DH>::TOTAL, st, "attention_tc", mq, mk, mv, q_slot,
-                  key_pad, (__nv_bfloat16*)ctx, lse, n_q, n_keys, Hq, G, scale_log2, g_attn_trace, split_min, ws_o,
-                  ws_ml, counters);
+  return launch_k(q_tmem ? attn_tc_kernel<DH, true> : attn_tc_kernel<DH, false>, grid, dim3(AT_THREADS),
+                  AtSmem<DH>::TOTAL, st, "attention_tc", mq, (const __nv_bfloat16*)q, mk, mv, q_slot, key_pad,
+                  (__nv_bfloat16*)ctx, lse, n_q, n_keys, Hq, G, scale_log2, g_attn_trace, Hkv, row_tiles, target,
+                  max_parts, ws_o, ws_ml, counters);
 }
 
 }  // namespace
