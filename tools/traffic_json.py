@@ -10,7 +10,8 @@ import csv
 import json
 import sys
 
-GROUPS = {"gemm": "gemm_tc_kernel", "attention": "attn_tc_kernel", "gather_rope": "gather_rope_kernel"}
+GROUPS = {"gemm": ("gemm_tc_kernel", "gemm_pair_kernel"), "attention": ("attn_tc_kernel",),
+          "gather_rope": ("gather_rope_kernel",)}
 
 rows = list(csv.reader(open(sys.argv[1])))
 i = [k for k, r in enumerate(rows) if "Kernel Name" in r][0]
@@ -26,7 +27,7 @@ for r in data:
     per[r[idi]][r[mi]] = v
 out = {"source": sys.argv[1].split("/")[-1], "how": __doc__.strip().splitlines()[0], "kernels": {}}
 for g, pat in GROUPS.items():
-    ls = [p for p in per.values() if pat in p["name"]]
+    ls = [p for p in per.values() if any(x in p["name"] for x in pat)]
     if not ls:
         continue
     tot = sum(p.get("dram__bytes_read.sum", 0) + p.get("dram__bytes_write.sum", 0) for p in ls)
