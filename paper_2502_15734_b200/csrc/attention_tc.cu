@@ -19,6 +19,7 @@
 // The PV MMA of tile i overlaps the S MMA of tile i+1 and the softmax of
 // tile i+1 (double-buffered S and P).
 #include <math.h>
+#include <stdio.h>
 #include <algorithm>
 #include <cmath>
 #include <stdlib.h>
@@ -717,6 +718,13 @@ int launch(const void* q, const void* k, const void* v, const int32_t* q_slot, c
     if (max_parts < 1) max_parts = 1;
   }
   if (getenv("CCB_ATTN_NOSPLIT")) max_parts = 1;
+  if (const char* e = getenv("CCB_ATTN_SPLIT")) {  // experiments: "target,max_parts"
+    int a = 0, b = 0;
+    if (sscanf(e, "%d,%d", &a, &b) == 2 && a > 0 && b >= 1 && b <= AT_MAXP && row_tiles <= AT_MAXT) {
+      target = a;
+      max_parts = b;
+    }
+  }
   float* ws_o = nullptr;
   float2* ws_ml = nullptr;
   int* counters = nullptr;

@@ -1,0 +1,10 @@
+for v in "CCB_ATTN_NOSPLIT=1" "CCB_ATTN_SPLIT=30,2" "CCB_ATTN_SPLIT=21,2" "CCB_ATTN_SPLIT=36,2"; do
+  env $v timeout 300 ncu --nvtx --nvtx-include "step/" --metrics gpu__time_duration.sum --clock-control none -k regex:attn --csv --log-file gpurun_out/sp.csv python tools/profile_step.py > /dev/null 2>&1
+  python - <<PY
+import csv
+rows=[r for r in csv.reader(open('gpurun_out/sp.csv')) if len(r)>10]
+h=rows[0]; vi=h.index('Metric Value')
+ts=[float(r[vi].replace(',','')) for r in rows[1:]]
+print('$v', 'attention avg us', round(sum(ts)/len(ts)/1e3,2), len(ts))
+PY
+done
