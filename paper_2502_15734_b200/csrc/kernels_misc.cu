@@ -153,7 +153,7 @@ __global__ void __launch_bounds__(256) gather_rope_kernel(
 // request KV (position-free k, rotated k for attention).  One CTA per row.
 // ---------------------------------------------------------------------------
 template <typename T, int V>
-__global__ void __launch_bounds__(128) rope_scatter_kernel(
+__global__ void __launch_bounds__(1024) rope_scatter_kernel(
     const T* __restrict__ qkv, int64_t ld, const int32_t* __restrict__ row_slot,
     const int32_t* __restrict__ row_pos, const typename CS<T>::type* __restrict__ table,
     T* __restrict__ q_rot, T* __restrict__ kv_k, T* __restrict__ kv_v, T* __restrict__ k_rot,
@@ -169,7 +169,15 @@ __global__ void __launch_bounds__(128) rope_scatter_kernel(
   const T* row = qkv + (int64_t)r * ld;
   const int kvw = Hkv * dh;
   const int rot_units = (Hq + Hkv) * hv;
-  for (int u = threadIdx.x; u < rot_units; u += blockDim.x) {
+  // one work unit per thread (the launch sizes the block to cover them): a
+  // rotated pair of V-vectors of a q or k head, or a V-vector of v
+  for (int u = threadIdx.x; u < rot_units + kvw / V; u += blockDim.x) {
+    if (u >= rot_units) {
+      const int c = u - rot_units;
+      const T* vrow = row + (int64_t)(Hq + Hkv) * dh;
+      *reinterpret_cast<VT*>(kv_v + (int64_t)slot * kvw + c * V) = *reinterpret_cast<const VT*>(vrow + c * V);
+      continue;
+    }
     int h = u / hv, jv = u % hv;
     bool is_q = h < Hq;
     int64_t off = (int64_t)h * dh + jv * V;  // q heads then k heads are contiguous in the row
@@ -199,11 +207,6 @@ __global__ void __launch_bounds__(128) rope_scatter_kernel(
       *reinterpret_cast<VT*>(k_rot + koff) = xr;
       *reinterpret_cast<VT*>(k_rot + koff + half) = yr;
     }
-  }
-  const T* vrow = row + (int64_t)(Hq + Hkv) * dh;
-  for (int c = threadIdx.x; c < kvw / V; c += blockDim.x) {
-    *reinterpret_cast<VT*>(kv_v + (int64_t)slot * kvw + c * V) =
-        *reinterpret_cast<const VT*>(vrow + c * V);
   }
 }
 
@@ -646,7 +649,10 @@ int cc_rope_scatter_qkv(const void* qkv, int64_t ld_qkv, int n_rows, const int32
   return CCB_DISPATCH_DTYPE(dtype, T, [&] {
     int vec = std::min(pick_vec<T>(d_head / 2), pick_vec<T>((int)ld_qkv));
     return CCB_DISPATCH_VEC(vec, V, [&] {
-      return launch_k(rope_scatter_kernel<T, V>, dim3(n_rows), dim3(128), 0, as_stream(stream), "rope_scatter_qkv",
+      // one thread per work unit (rotated q/k vector pairs + v vectors), <= 1024
+      const int units = (n_heads + n_kv_heads) * (d_head / 2 / V) + n_kv_heads * d_head / V;
+      const int threads = std::min(1024, std::max(128, (units + 31) / 32 * 32));
+      return launch_k(rope_scatter_kernel<T, V>, dim3(n_rows), dim3(threads), 0, as_stream(stream), "rope_scatter_qkv",
                       (const T*)qkv, ld_qkv, row_slot, row_pos, (const typename CS<T>::type*)rope_table, (T*)q_rot,
                       (T*)kv_k, (T*)kv_v, (T*)k_rot, n_heads, n_kv_heads, d_head);
     });
