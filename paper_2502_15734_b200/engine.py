@@ -606,7 +606,15 @@ def run_prefill(model: Model, request, record_values: bool = False, record_atten
             raise PlanError("the question's last row is not computed through every layer")
         logits, tok = _logits_rows(model, ws["hidden"][r:r + 1])
         extras["logits_last"] = logits
-        extras["first_token_dev"] = tok  # read back lazily by PrefillResult.first_token
+        extras["first_token_dev"] = tok
+        # asynchronous readback into pinned memory + an event right behind
+        # this request's kernels: PrefillResult.first_token waits for this
+        # request only, so a server can enqueue the next request first
+        host_tok = torch.empty(tok.numel(), dtype=tok.dtype, pin_memory=True)
+        host_tok.copy_(tok.reshape(-1), non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        extras["first_token_host"] = (host_tok, ev)
     L = cfg.n_layers
     attn = AttentionRecord(query_slots=[np.sort(plan.rows[:plan.n_act[l]]) for l in range(L)], _lazy=lazy)
     if lazy is None:

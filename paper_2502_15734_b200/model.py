@@ -786,7 +786,11 @@ class PrefillResult:
     def first_token(self):
         """Greedy first token; read back from the device on first access (so a
         caller can plan the next request while this one computes)."""
-        if "first_token" not in self.extras and "first_token_dev" in self.extras:
+        if "first_token" not in self.extras and "first_token_host" in self.extras:
+            host_tok, ev = self.extras["first_token_host"]
+            ev.synchronize()
+            self.extras["first_token"] = int(host_tok[0])
+        elif "first_token" not in self.extras and "first_token_dev" in self.extras:
             self.extras["first_token"] = int(self.extras["first_token_dev"].item())
         return self.extras.get("first_token")
 

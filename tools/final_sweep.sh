@@ -1,7 +1,7 @@
 # Round-end measurement set (one box): GPU tests, default bench (+ sweep), configs 3/4/5,
 # reference arm, launch list of the config-2 step with DRAM bytes.
 set -x
-timeout 1000 python -m pytest tests -m gpu -x -q 2>&1 | tail -3
+timeout 1000 python -m pytest tests -m gpu -x -q 2>&1 | tail -3 > gpurun_out/h_tests.log; cat gpurun_out/h_tests.log
 timeout 900 python bench.py --sweep > gpurun_out/h_main.json 2> gpurun_out/h_main.err; tail -c 400 gpurun_out/h_main.json
 timeout 600 python bench.py --config 8b-32k > gpurun_out/h_32k.json 2> gpurun_out/h_32k.err; tail -c 300 gpurun_out/h_32k.json
 timeout 900 python bench.py --config 70b --steps 3 > gpurun_out/h_70b.json 2> gpurun_out/h_70b.err; tail -c 300 gpurun_out/h_70b.json
