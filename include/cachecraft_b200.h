@@ -109,8 +109,10 @@ CC_API int cc_rmsnorm(const void* hidden, void* out, const float* weight, int n_
 /* C = A[M,K] B[N,K]^T with an epilogue (model.py:399-401, :417-419).  A is
  * the normed activations in dtype; B the weight in dtype; for
  * CC_EPI_RESID_ADD, C is the residual stream (f32/f64).  In CC_BF16 mode the
- * tcgen05/TMEM tensor-core kernel runs (impl 0 = auto, 1 = force tcgen05,
- * 2 = force SIMT reference kernel used by tests). */
+ * tcgen05/TMEM tensor-core kernels run, tiling chosen per shape (1-CTA tiles,
+ * swap-AB, or CTA-pair units; impl 0 = auto incl. the M <= 4 GEMV route,
+ * 1 = force tcgen05, 2 = force SIMT reference kernel used by tests,
+ * 4 = tcgen05 without K splits: a row's result independent of M). */
 CC_API int cc_gemm(const void* A, int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc, int M,
             int N, int K, int epilogue, int dtype, int impl, void* stream);
 
