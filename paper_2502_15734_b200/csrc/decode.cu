@@ -286,47 +286,47 @@ __global__ void __launch_bounds__(DA_KEYS) decode_attn_partial(const __nv_bfloat
 }
 
 // grid Hq, 128 threads: fold the chunks in index order
-__global__ void __launch_bounds__(DA_DH) decode_attn_combine(const float* __restrict__ part_o,
-                                                             const float2* __restrict__ part_ml, int n_chunks, int Hq,
-                                                             __nv_bfloat16* __restrict__ ctx, float* __restrict__ lse,
-                                                             const int32_t* __restrict__ n_keys_dev) {
-  const int head = blockIdx.x, t = threadIdx.x;
+// One warp per (head, 32 output columns): 4 x Hq CTAs instead of Hq, every
+// chunk partial a coalesced 128-byte row load.  Same arithmetic order as the
+// one-CTA-per-head form (weights and sum by lane-strided chunks + butterfly,
+// output in 4 fixed chains).
+__global__ void __launch_bounds__(32) decode_attn_combine(const float* __restrict__ part_o,
+                                                          const float2* __restrict__ part_ml, int n_chunks, int Hq,
+                                                          __nv_bfloat16* __restrict__ ctx, float* __restrict__ lse,
+                                                          const int32_t* __restrict__ n_keys_dev) {
+  const int head = blockIdx.x, lane = threadIdx.x, col = blockIdx.y * 32 + lane;
   pdl_trigger();
   pdl_wait();
   if (n_keys_dev != nullptr) n_chunks = (*n_keys_dev + DA_KEYS - 1) / DA_KEYS;
   __shared__ float w_s[DA_COMBINE_MAX];
-  __shared__ float ml_red[2];
-  // warp 0: global max and the chunk weights 2^(m_c - m), sum l (fixed order)
-  if (t < 32) {
-    float m = -INFINITY;
-    for (int c = t; c < n_chunks; c += 32) m = fmaxf(m, part_ml[(int64_t)c * Hq + head].x);
+  // global max and the chunk weights 2^(m_c - m), sum l (fixed order)
+  float m = -INFINITY;
+  for (int c = lane; c < n_chunks; c += 32) m = fmaxf(m, part_ml[(int64_t)c * Hq + head].x);
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
-    float l = 0.f;
-    for (int c = t; c < n_chunks; c += 32) {
-      const float2 ml = part_ml[(int64_t)c * Hq + head];
-      const float w = (m == -INFINITY || ml.x == -INFINITY) ? 0.f : exp2f(ml.x - m);
-      w_s[c] = w;
-      l = fmaf(ml.y, w, l);
-    }
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) l += __shfl_xor_sync(0xffffffffu, l, off);
-    if (t == 0) { ml_red[0] = m; ml_red[1] = l; }
+  for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
+  float l = 0.f;
+  for (int c = lane; c < n_chunks; c += 32) {
+    const float2 ml = part_ml[(int64_t)c * Hq + head];
+    const float w = (m == -INFINITY || ml.x == -INFINITY) ? 0.f : exp2f(ml.x - m);
+    w_s[c] = w;
+    l = fmaf(ml.y, w, l);
   }
-  __syncthreads();
-  const float m = ml_red[0], l = ml_red[1];
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) l += __shfl_xor_sync(0xffffffffu, l, off);
+  __syncwarp();
   float o0 = 0.f, o1 = 0.f, o2 = 0.f, o3 = 0.f;  // 4 independent chains
   int c = 0;
   for (; c + 3 < n_chunks; c += 4) {
-    o0 = fmaf(part_o[((int64_t)c * Hq + head) * DA_DH + t], w_s[c], o0);
-    o1 = fmaf(part_o[((int64_t)(c + 1) * Hq + head) * DA_DH + t], w_s[c + 1], o1);
-    o2 = fmaf(part_o[((int64_t)(c + 2) * Hq + head) * DA_DH + t], w_s[c + 2], o2);
-    o3 = fmaf(part_o[((int64_t)(c + 3) * Hq + head) * DA_DH + t], w_s[c + 3], o3);
+    o0 = fmaf(part_o[((int64_t)c * Hq + head) * DA_DH + col], w_s[c], o0);
+    o1 = fmaf(part_o[((int64_t)(c + 1) * Hq + head) * DA_DH + col], w_s[c + 1], o1);
+    o2 = fmaf(part_o[((int64_t)(c + 2) * Hq + head) * DA_DH + col], w_s[c + 2], o2);
+    o3 = fmaf(part_o[((int64_t)(c + 3) * Hq + head) * DA_DH + col], w_s[c + 3], o3);
   }
-  for (; c < n_chunks; ++c) o0 = fmaf(part_o[((int64_t)c * Hq + head) * DA_DH + t], w_s[c], o0);
+  for (; c < n_chunks; ++c) o0 = fmaf(part_o[((int64_t)c * Hq + head) * DA_DH + col], w_s[c], o0);
   const float o = (o0 + o1) + (o2 + o3);
-  ctx[(int64_t)head * DA_DH + t] = __float2bfloat16_rn(l > 0.f ? o / l : 0.f);
-  if (t == 0 && lse != nullptr) lse[head] = l > 0.f ? (m + log2f(l)) * 0.6931471805599453f : -INFINITY;
+  ctx[(int64_t)head * DA_DH + col] = __float2bfloat16_rn(l > 0.f ? o / l : 0.f);
+  if (blockIdx.y == 0 && lane == 0 && lse != nullptr)
+    lse[head] = l > 0.f ? (m + log2f(l)) * 0.6931471805599453f : -INFINITY;
 }
 
 // y[row] = RoPE(x[row], pos[row % n]) for rows of `width` = heads x d_head
@@ -448,7 +448,7 @@ int decode_attention_impl(const void* q, const void* k_rot, const void* v, const
     default: return fail(CC_E_UNSUP, "decode_attention: GQA group must be 1, 2, 4 or 8");
   }
   if (rc) return rc;
-  return launch_k(decode_attn_combine, dim3(n_heads), dim3(DA_DH), 0, st, "decode_attention_combine",
+  return launch_k(decode_attn_combine, dim3(n_heads, DA_DH / 32), dim3(32), 0, st, "decode_attention_combine",
                   (const float*)part_o, (const float2*)part_ml, n_chunks, n_heads, (__nv_bfloat16*)ctx, lse,
                   n_keys_dev);
 }
