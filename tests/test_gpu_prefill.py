@@ -253,3 +253,30 @@ def test_llama_shaped_fix_up_vs_oracle(cc, dtype, tol):
         assert rel(res.kv.keys[l], ref["keys"][l]) < max(tol, 1e-12)
         assert rel(res.kv.values[l], ref["values"][l]) < max(tol, 1e-12)
     assert res.first_token == O.greedy_token(w, ocfg, ref)
+
+
+def test_programmatic_dependent_launch_is_bit_identical(cc):
+    """The prefill chain launched with programmatic dependent launch
+    (griddepcontrol: prologues and first weight tiles before the wait) gives
+    the same bits as plain stream-ordered launches; the first token comes
+    back through the pinned-copy + event path either way."""
+    kw = dict(n_layers=3, n_heads=8, d_model=512, d_head=64, vocab_size=512, rpe_base=500000.0, seed=4,
+              n_kv_heads=2, d_ff=1024, mlp="swiglu", norm_weight=True, rms_eps=1e-5)
+    model = cc.build_model(cc.ModelConfig(dtype="bf16", **kw))
+    r = np.random.default_rng(12)
+    chunks = [r.integers(0, 512, n) for n in (160, 96, 200)]
+    q = r.integers(0, 512, 12)
+    req0 = cc.plain_request(*chunks, [])
+    res0 = cc.prefill(model, req0)
+    caches = [cc.extract_chunk_cache(res0, s, e) for s, e in req0.segment_slots]
+    masks = [r.uniform(size=c.size) < 0.2 for c in chunks]
+    segs = [cc.Segment(tokens=c, cache=k, recompute=m) for c, k, m in zip(chunks, caches, masks)]
+    outs = []
+    for pdl in (False, True):
+        model.prefill_pdl = pdl
+        res = cc.prefill(model, cc.build_request(segs, q), first_token=True)
+        outs.append((res.hidden.copy(), [k.copy() for k in res.kv.keys], res.first_token))
+    assert np.array_equal(outs[0][0], outs[1][0])
+    for a, b in zip(outs[0][1], outs[1][1]):
+        assert np.array_equal(a, b)
+    assert outs[0][2] == outs[1][2]
