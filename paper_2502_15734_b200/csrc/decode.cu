@@ -178,7 +178,7 @@ __global__ void __launch_bounds__(DA_KEYS) decode_attn_partial(const __nv_bfloat
   pdl_wait();
   if (n_keys_dev != nullptr) n_keys = *n_keys_dev;  // CUDA-graph replay: key count lives on the device
   if ((int)blockIdx.y * DA_KEYS >= n_keys) return;   // chunk beyond the live keys (grid sized for capacity)
-  __shared__ float qs[G][DA_DH];
+  __shared__ __align__(16) float qs[G][DA_DH];
   __shared__ float ps[G][DA_KEYS];
   __shared__ float2 ml_s[G];
   const int g = blockIdx.x, c = blockIdx.y, t = threadIdx.x;
@@ -210,11 +210,21 @@ __global__ void __launch_bounds__(DA_KEYS) decode_attn_partial(const __nv_bfloat
     for (int u = 0; u < DA_DH / 8; ++u) {
       const uint4 kk = kv16[u];
       const __nv_bfloat162* kb = reinterpret_cast<const __nv_bfloat162*>(&kk);
+      float kf[8];
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        const float2 kf = __bfloat1622float2(kb[e]);
+        const float2 f = __bfloat1622float2(kb[e]);
+        kf[2 * e] = f.x;
+        kf[2 * e + 1] = f.y;
+      }
 #pragma unroll
-        for (int h = 0; h < G; ++h) sc[h] = fmaf(kf.x, qs[h][u * 8 + 2 * e], fmaf(kf.y, qs[h][u * 8 + 2 * e + 1], sc[h]));
+      for (int h = 0; h < G; ++h) {
+        // q as two 16-byte shared loads per 8 products (same FMA order)
+        const float4 qa = *reinterpret_cast<const float4*>(&qs[h][u * 8]);
+        const float4 qb = *reinterpret_cast<const float4*>(&qs[h][u * 8 + 4]);
+        const float qv[8] = {qa.x, qa.y, qa.z, qa.w, qb.x, qb.y, qb.z, qb.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) sc[h] = fmaf(kf[2 * e], qv[2 * e], fmaf(kf[2 * e + 1], qv[2 * e + 1], sc[h]));
       }
     }
   }
@@ -316,6 +326,18 @@ __global__ void __launch_bounds__(32) decode_attn_combine(const float* __restric
   __syncwarp();
   float o0 = 0.f, o1 = 0.f, o2 = 0.f, o3 = 0.f;  // 4 independent chains
   int c = 0;
+  for (; c + 15 < n_chunks; c += 16) {  // 16 loads in flight, then the same 4-chain order
+    float v[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) v[k] = part_o[((int64_t)(c + k) * Hq + head) * DA_DH + col];
+#pragma unroll
+    for (int k = 0; k < 16; k += 4) {
+      o0 = fmaf(v[k], w_s[c + k], o0);
+      o1 = fmaf(v[k + 1], w_s[c + k + 1], o1);
+      o2 = fmaf(v[k + 2], w_s[c + k + 2], o2);
+      o3 = fmaf(v[k + 3], w_s[c + k + 3], o3);
+    }
+  }
   for (; c + 3 < n_chunks; c += 4) {
     o0 = fmaf(part_o[((int64_t)c * Hq + head) * DA_DH + col], w_s[c], o0);
     o1 = fmaf(part_o[((int64_t)(c + 1) * Hq + head) * DA_DH + col], w_s[c + 1], o1);
