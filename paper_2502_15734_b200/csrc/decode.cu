@@ -158,7 +158,7 @@ __global__ void __launch_bounds__(GV_WARPS * 32) gemv_kernel(const void* __restr
 }
 
 // ---- split-KV decode attention ------------------------------------------------
-constexpr int DA_KEYS = 128;  // keys per CTA (one per thread)
+constexpr int DA_KEYS = 128;  // keys per CTA (one per thread); 64 measured slower (14.7 vs 13.5 us + a longer combine)
 constexpr int DA_DH = 128;
 constexpr int DA_MAXG = 8;
 constexpr int DA_COMBINE_MAX = 4096;  // chunks of 128 keys: 512k keys
@@ -187,13 +187,14 @@ __global__ void __launch_bounds__(DA_KEYS) decode_attn_partial(const __nv_bfloat
   __syncthreads();
   // V rows of this thread's P.V role are loaded up front so their latency
   // overlaps the K loads and the score math (thread = 8 columns x 16 keys)
+  constexpr int NKG = DA_KEYS / 16;  // key groups of the P.V role (16 keys each)
   const int cg = t & 15, kg = t >> 4;
   const int jn = min(DA_KEYS, n_keys - c * DA_KEYS);
   const __nv_bfloat16* vbase = V + (int64_t)c * DA_KEYS * kvw + g * DA_DH + cg * 8;
-  uint4 vv[DA_KEYS / 8];
+  uint4 vv[16];
 #pragma unroll
-  for (int u = 0; u < DA_KEYS / 8; ++u) {
-    const int jj = kg + 8 * u;
+  for (int u = 0; u < 16; ++u) {
+    const int jj = kg + NKG * u;
     vv[u] = jj < jn ? *reinterpret_cast<const uint4*>(vbase + (int64_t)jj * kvw) : make_uint4(0, 0, 0, 0);
   }
   const int j = c * DA_KEYS + t;
@@ -234,9 +235,9 @@ __global__ void __launch_bounds__(DA_KEYS) decode_attn_partial(const __nv_bfloat
   // per head: max and exp-sum over the 128 keys (warp w handles heads w, w+4, ...)
   const int warp = t >> 5, lane = t & 31;
   for (int h = warp; h < G; h += DA_KEYS / 32) {
-    float v[4], m = -INFINITY;
+    float v[DA_KEYS / 32], m = -INFINITY;
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
+    for (int e = 0; e < DA_KEYS / 32; ++e) {
       v[e] = ps[h][lane + 32 * e];
       m = fmaxf(m, v[e]);
     }
@@ -244,7 +245,7 @@ __global__ void __launch_bounds__(DA_KEYS) decode_attn_partial(const __nv_bfloat
     for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
     float l = 0.f;
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
+    for (int e = 0; e < DA_KEYS / 32; ++e) {
       const float p = m == -INFINITY ? 0.f : exp2f(v[e] - m);
       ps[h][lane + 32 * e] = p;
       l += p;
@@ -263,8 +264,8 @@ __global__ void __launch_bounds__(DA_KEYS) decode_attn_partial(const __nv_bfloat
 #pragma unroll
     for (int e = 0; e < 8; ++e) o[h][e] = 0.f;
 #pragma unroll
-  for (int u = 0; u < DA_KEYS / 8; ++u) {
-    const int jj = kg + 8 * u;
+  for (int u = 0; u < 16; ++u) {
+    const int jj = kg + NKG * u;
     const __nv_bfloat162* vb = reinterpret_cast<const __nv_bfloat162*>(&vv[u]);
 #pragma unroll
     for (int h = 0; h < G; ++h) {
@@ -278,7 +279,7 @@ __global__ void __launch_bounds__(DA_KEYS) decode_attn_partial(const __nv_bfloat
     }
   }
   __syncthreads();  // ps no longer needed: reuse as [8 key groups][G][128] partials? (too small) -> red below
-  __shared__ float red[8][G][DA_DH];
+  __shared__ float red[NKG][G][DA_DH];
 #pragma unroll
   for (int h = 0; h < G; ++h)
 #pragma unroll
@@ -286,11 +287,13 @@ __global__ void __launch_bounds__(DA_KEYS) decode_attn_partial(const __nv_bfloat
   __syncthreads();
 #pragma unroll
   for (int h = 0; h < G; ++h) {
-    float acc = 0.f;
-#pragma unroll
-    for (int k2 = 0; k2 < 8; ++k2) acc += red[k2][h][t];
     const int head = g * G + h;
-    part_o[((int64_t)c * Hq + head) * DA_DH + t] = acc;
+    for (int col = t; col < DA_DH; col += DA_KEYS) {
+      float acc = 0.f;
+#pragma unroll
+      for (int k2 = 0; k2 < NKG; ++k2) acc += red[k2][h][col];
+      part_o[((int64_t)c * Hq + head) * DA_DH + col] = acc;
+    }
     if (t == 0) part_ml[(int64_t)c * Hq + head] = ml_s[h];
   }
 }
