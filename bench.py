@@ -676,9 +676,10 @@ def main():
     calls0 = sum(_native.calls.values())
     barrier(world)
     with Clocks(torch.cuda.current_device()) as clk:
-        # per-kernel CUDA events on the last two timed steps only (an event
-        # pair around every launch family costs ~0.8 ms over a whole step)
-        n_timed = min(2, args.steps)
+        # per-kernel CUDA events on the last timed step only (an event pair
+        # around every launch family costs ~0.8 ms over a whole step; one
+        # step still gives every family its 32 per-layer launches)
+        n_timed = 1
         ms, timer = time_device(model, dplan, ws, req, args.steps, args.warmup, world, timer_steps=n_timed)
     launches = (sum(_native.calls.values()) - calls0) // (args.steps + args.warmup)
     clocks = clk.summary()
