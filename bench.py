@@ -813,6 +813,9 @@ def main():
 
     if rank != 0:
         return
+    from paper_2502_15734_b200 import _native as N_
+
+    N_.assert_tensor_core_only()  # every bf16 GEMM / attention of the run ran on tcgen05
     gemm_roof = roofline_obj("gemm", summ, peaks, "tensor")
     kernels = [k for k in (roofline_obj("gather_rope", summ, peaks, "hbm"),
                            roofline_obj("attention", summ, peaks, "tensor")) if k]
@@ -839,6 +842,7 @@ def main():
         "roofline_kernels": kernels,
         "kernel_time_share": share,
         "gpu_launches": int(launches),
+        "bf16_simt_launches": N_.bf16_simt_launches(),
         "cpu_baseline": cpu,
         "baselines": baselines,
         "clocks": clocks,

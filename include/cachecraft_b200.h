@@ -67,6 +67,10 @@ typedef struct {
 CC_API int cc_abi_version(void);
 CC_API const char* cc_last_error(void);
 CC_API int cc_sm_count(int device);
+/* Number of SIMT (non-tensor-core) GEMM / attention / segment-mass kernel
+ * launches made with CC_BF16 data since load.  Only an explicit impl == 2
+ * test call reaches them in bf16: the bench and smoke assert it stays 0. */
+CC_API long long cc_bf16_simt_launches(void);
 
 /* RoPE cos/sin table [max_pos][half] of (cos, sin) pairs in the engine
  * dtype's float type (double2 for CC_F64, float2 otherwise), angles built in
@@ -110,7 +114,9 @@ CC_API int cc_rmsnorm(const void* hidden, void* out, const float* weight, int n_
  * the normed activations in dtype; B the weight in dtype; for
  * CC_EPI_RESID_ADD, C is the residual stream (f32/f64).  In CC_BF16 mode the
  * tcgen05/TMEM tensor-core kernels run, tiling chosen per shape (1-CTA tiles,
- * swap-AB, or CTA-pair units; impl 0 = auto incl. the M <= 4 GEMV route,
+ * swap-AB, or CTA-pair units; impl 0 = product path: bf16 runs the M <= 4
+ * GEMV route or the tcgen05 kernel and returns CC_E_UNSUP for a shape neither
+ * supports (no silent fallback), fp32/fp64 parity modes run SIMT;
  * 1 = force tcgen05, 2 = force SIMT reference kernel used by tests,
  * 4 = tcgen05 without K splits: a row's result independent of M). */
 CC_API int cc_gemm(const void* A, int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc, int M,
@@ -121,7 +127,9 @@ CC_API int cc_gemm(const void* A, int64_t lda, const void* B, int64_t ldb, void*
  * query row r sees keys j <= q_slot[r] with key_pad[j] == 0.  Writes
  * ctx [n_q][Hq*dh] and lse [n_q][Hq] (natural log of the softmax
  * denominator incl. the running max, scale applied; double in CC_F64 mode,
- * float otherwise). impl: 0 auto, 1 force tensor-core kernel, 2 force SIMT. */
+ * float otherwise). impl: 0 product path (bf16: the tcgen05 kernel only,
+ * CC_E_UNSUP for d_head not in {64, 128} or a GQA group not dividing 128;
+ * fp32/fp64: SIMT), 1 force tensor-core kernel, 2 force SIMT (tests). */
 CC_API int cc_attention(const void* q, const void* k_rot, const void* v, const int32_t* q_slot,
                  const uint8_t* key_pad, void* ctx, void* lse, int n_q, int n_keys, int n_heads,
                  int n_kv_heads, int d_head, int dtype, int impl, void* stream);

@@ -213,7 +213,8 @@ def layout(segments, question) -> dict:
 # --------------------------------------------------------------------------
 
 
-def prefill(w: dict, cfg: OracleConfig, lay: dict, caches, keep_weights=True, layers=None, tp=None) -> dict:
+def prefill(w: dict, cfg: OracleConfig, lay: dict, caches, keep_weights=True, layers=None, tp=None,
+            sample_rows=None) -> dict:
     """Partial prefill with injected position-free caches.
 
     ``caches`` is a list aligned with the segments: None for fresh text, else
@@ -230,6 +231,13 @@ def prefill(w: dict, cfg: OracleConfig, lay: dict, caches, keep_weights=True, la
     rank — its query/kv head columns and MLP columns — and ``allreduce``
     sums the o_proj and down_proj partial outputs over the ranks before the
     residual adds (the only two reductions of a layer, model.py:417, :419).
+
+    ``sample_rows`` (memory bound for the long-prompt parity tests): at the
+    LAST layer run, K/V are still projected for every active row, but the
+    attention, o_proj and MLP are evaluated only for the active rows whose
+    slot is in ``sample_rows`` (each row's output depends on its own
+    attention row only, so those rows are exact); other rows' hidden state
+    is left at its input value at that layer.
     """
     L = cfg.n_layers if layers is None else layers
     H, Hkv, dh = cfg.n_heads, cfg.hkv, cfg.dh
@@ -263,9 +271,12 @@ def prefill(w: dict, cfg: OracleConfig, lay: dict, caches, keep_weights=True, la
         if rows.size:
             x = hidden[rows]
             xn = rmsnorm(x, cfg.rms_eps, lw["attn_norm"] if nw else None)
-            q = xn @ lw["wq"][:, qc]
             K[rows] = xn @ lw["wk"][:, kc]
             V[rows] = xn @ lw["wv"][:, kc]
+            if sample_rows is not None and l == L - 1:
+                keep = np.isin(rows, np.asarray(sample_rows, dtype=np.int64))
+                rows, x, xn = rows[keep], x[keep], xn[keep]
+            q = xn @ lw["wq"][:, qc]
             qr = rope(q, pos[rows], cfg.rpe_base, dh).reshape(rows.size, H, dh)
             kr = rope(K, key_pos, cfg.rpe_base, dh).reshape(n, Hkv, dh)
             vv = V.reshape(n, Hkv, dh)

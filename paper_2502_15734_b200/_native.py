@@ -31,6 +31,7 @@ _SIGS = {
     "cc_abi_version": ([], _i32),
     "cc_last_error": ([], ctypes.c_char_p),
     "cc_sm_count": ([_i32], _i32),
+    "cc_bf16_simt_launches": ([], ctypes.c_longlong),
     "cc_rope_table": ([_vp, _vp, _i32, _i32, _i32, _vp], _i32),
     "cc_rope_apply_f64": ([_vp, _vp, _vp, _i32, _i32, _i32, _vp, _i32, _vp], _i32),
     "cc_gather_rope_kv": ([_vp, _i64, _i64, _vp, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i32, _i32, _i32, _vp], _i32),
@@ -117,6 +118,18 @@ def call(name: str, *args):
         2 if name in ("cc_decode_attention", "cc_decode_attention_dev") else 1)
     check(rc, name)
     return rc
+
+
+def bf16_simt_launches() -> int:
+    """SIMT kernel launches made on bf16 data (0 in the product path)."""
+    return int(lib().cc_bf16_simt_launches())
+
+
+def assert_tensor_core_only(before: int = 0):
+    """Fail loudly if any bf16 work since ``before`` ran on a SIMT kernel."""
+    n = bf16_simt_launches() - before
+    if n:
+        raise NativeError(f"{n} bf16 launches ran on SIMT kernels instead of tcgen05")
 
 
 def ptr(t) -> int | None:

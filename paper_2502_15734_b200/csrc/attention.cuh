@@ -3,8 +3,6 @@
 #include <stdint.h>
 
 namespace ccb {
-int attention_mma_bf16(const void* q, const void* k, const void* v, const int32_t* q_slot, const uint8_t* key_pad,
-                       void* ctx, float* lse, int n_q, int n_keys, int Hq, int Hkv, int dh, cudaStream_t st);
 int attention_tc_bf16(const void* q, const void* k, const void* v, const int32_t* q_slot, const uint8_t* key_pad,
                       void* ctx, float* lse, int n_q, int n_keys, int Hq, int Hkv, int dh, cudaStream_t st);
 int segment_mass_tc_bf16(const void* q, const void* k, const int32_t* q_slot, const uint8_t* key_pad,

@@ -155,6 +155,7 @@ __global__ void __launch_bounds__(256) segment_mass_kernel(
 int attention_simt(const void* q, const void* k, const void* v, const int32_t* q_slot, const uint8_t* key_pad,
                    void* ctx, void* lse, int n_q, int n_keys, int Hq, int Hkv, int dh, int dtype, cudaStream_t st) {
   CCB_REQUIRE(dh <= 256, "attention: d_head must be <= 256");
+  note_simt(dtype);
   dim3 grid(n_q, Hq);
   return CCB_DISPATCH_DTYPE(dtype, T, [&] {
     attn_simt_kernel<T><<<grid, 128, 0, st>>>((const T*)q, (const T*)k, (const T*)v, q_slot, key_pad, (T*)ctx,
@@ -176,17 +177,13 @@ int cc_attention(const void* q, const void* k_rot, const void* v, const int32_t*
   CCB_REQUIRE(d_head > 0 && d_head <= 256, "attention: bad d_head");
   if (n_q == 0) return 0;
   cudaStream_t st = as_stream(stream);
-  // impl: 0 auto (tcgen05 -> mma.sync -> SIMT), 1 tcgen05 only, 3 mma.sync only, 2 SIMT
-  if (dtype == CC_BF16 && (impl == 0 || impl == 1)) {
-    int rc = attention_tc_bf16(q, k_rot, v, q_slot, key_pad, ctx, (float*)lse, n_q, n_keys, n_heads, n_kv_heads,
-                               d_head, st);
-    if (rc != CC_E_UNSUP || impl == 1) return rc;
-  }
-  if (dtype == CC_BF16 && (impl == 0 || impl == 3)) {
-    int rc = attention_mma_bf16(q, k_rot, v, q_slot, key_pad, ctx, (float*)lse, n_q, n_keys, n_heads, n_kv_heads,
-                                d_head, st);
-    if (rc != CC_E_UNSUP || impl == 3) return rc;
-  }
+  // impl: 0 product path (bf16: the tcgen05 kernel only -- an unsupported
+  // shape is an error, never a silent slower kernel; fp32/fp64 parity modes:
+  // SIMT), 1 tcgen05, 2 SIMT reference (tests)
+  if (dtype == CC_BF16 && impl != 2)
+    return attention_tc_bf16(q, k_rot, v, q_slot, key_pad, ctx, (float*)lse, n_q, n_keys, n_heads, n_kv_heads,
+                             d_head, st);
+  if (impl == 1) return fail(CC_E_UNSUP, "attention: tcgen05 kernel requires bf16");
   return attention_simt(q, k_rot, v, q_slot, key_pad, ctx, lse, n_q, n_keys, n_heads, n_kv_heads, d_head, dtype, st);
 }
 
@@ -210,11 +207,10 @@ int cc_segment_mass(const void* q, const void* k_rot, const int32_t* q_slot, con
                     double* mass, int n_keys, int n_heads, int n_kv_heads, int d_head, int dtype, void* stream) {
   if (n_rows == 0) return 0;
   CCB_REQUIRE(d_head <= 256, "segment_mass: d_head must be <= 256");
-  if (dtype == CC_BF16) {
-    int rc = segment_mass_tc_bf16(q, k_rot, q_slot, key_pad, (const float*)lse, seg_lo, seg_hi, n_seg, rows, n_rows,
-                                  mass, n_keys, n_heads, n_kv_heads, d_head, as_stream(stream));
-    if (rc != CC_E_UNSUP) return rc;
-  }
+  if (dtype == CC_BF16)  // tcgen05 only: no silent SIMT fallback in the product path
+    return segment_mass_tc_bf16(q, k_rot, q_slot, key_pad, (const float*)lse, seg_lo, seg_hi, n_seg, rows, n_rows,
+                                mass, n_keys, n_heads, n_kv_heads, d_head, as_stream(stream));
+  note_simt(dtype);
   return CCB_DISPATCH_DTYPE(dtype, T, [&] {
     using A = typename Acc<T>::type;
     segment_mass_kernel<T><<<n_rows, 256, 0, as_stream(stream)>>>((const T*)q, (const T*)k_rot, q_slot, key_pad,

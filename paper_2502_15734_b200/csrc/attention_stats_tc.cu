@@ -282,14 +282,9 @@ int launch(const void* q, const void* k, const int32_t* q_slot, const uint8_t* k
           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return fail(CC_E_CUDA, "segment_mass_tc: tensor map encode failed");
   const int G = Hq / Hkv, R = 128 / G, W = n_seg + 1;
-  float* part = (float*)stream_scratch(st, 2, sizeof(float) * (size_t)n_rows * Hkv * W);
+  float* part = (float*)stream_scratch(st, SCR_SEGMASS, sizeof(float) * (size_t)n_rows * Hkv * W);
   if (!part) return fail(CC_E_CUDA, "segment_mass_tc: scratch allocation failed");
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(attn_stats_tc_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)StSmem<DH>::TOTAL);
-    attr = true;
-  }
+  if (int rc = ensure_smem(attn_stats_tc_kernel<DH>, StSmem<DH>::TOTAL)) return rc;
   dim3 grid(Hkv, (n_rows + R - 1) / R);
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)DH);
   attn_stats_tc_kernel<DH><<<grid, 192, StSmem<DH>::TOTAL, st>>>(mk, (const __nv_bfloat16*)q, rows, n_rows, q_slot,

@@ -692,12 +692,8 @@ int launch(const void* q, const void* k, const void* v, const int32_t* q_slot, c
     rc = encode(&mv, 2, v, dims, strides, box);
     if (rc) return rc;
   }
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(attn_tc_kernel<DH, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)AtSmem<DH>::TOTAL);
-    cudaFuncSetAttribute(attn_tc_kernel<DH, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)AtSmem<DH>::TOTAL);
-    attr = true;
-  }
+  if (int rc = ensure_smem(attn_tc_kernel<DH, true>, AtSmem<DH>::TOTAL)) return rc;
+  if (int rc = ensure_smem(attn_tc_kernel<DH, false>, AtSmem<DH>::TOTAL)) return rc;
   // Q in TMEM (QT): measured ~1-2% slower than Q in smem at config 2 (the
   // kernel is softmax-latency bound, not smem-port bound); opt-in
   static const bool q_tmem = getenv("CCB_ATTN_QTMEM") && getenv("CCB_ATTN_QTMEM")[0] == '1';
@@ -731,7 +727,7 @@ int launch(const void* q, const void* k, const void* v, const int32_t* q_slot, c
   if (max_parts > 1) {
     const size_t keys = (size_t)Hkv * row_tiles;
     const size_t bytes = keys * AT_MAXP * 128 * (DH * sizeof(float) + sizeof(float2));
-    uint8_t* scratch = (uint8_t*)stream_scratch(st, 3, bytes);
+    uint8_t* scratch = (uint8_t*)stream_scratch(st, SCR_ATTN, bytes);
     counters = split_counters(st, (int)keys);
     if (!scratch || !counters) return fail(CC_E_CUDA, "attention_tc: split workspace allocation failed");
     ws_o = reinterpret_cast<float*>(scratch);

@@ -1,7 +1,12 @@
 // Error plumbing and device queries of the C ABI (include/cachecraft_b200.h).
+#include <algorithm>
+#include <atomic>
 #include <mutex>
-#include <unordered_map>
+#include <set>
 #include <string>
+#include <tuple>
+#include <unordered_map>
+#include <vector>
 
 #include "common.cuh"
 
@@ -26,23 +31,51 @@ int check_launch(const char* what) {
 
 // Device scratch owned by the library, one buffer per (device, stream, tag):
 // kernels on different streams (e.g. tensor-parallel ranks in one process)
-// never share it.  Grows on demand; never freed (process lifetime).
+// never share it.  Grows on demand.  A grown-out buffer is retired, never
+// freed: a captured CUDA graph (DecodeSession) may still reference it, and
+// cudaFree would synchronise the device.
 void* stream_scratch(cudaStream_t st, int tag, size_t bytes) {
   static std::mutex mu;
   struct Buf { void* p = nullptr; size_t n = 0; };
   static std::unordered_map<uint64_t, Buf> bufs;
+  static std::vector<void*> retired;
   int dev = 0;
   cudaGetDevice(&dev);
   const uint64_t key = (reinterpret_cast<uint64_t>(st) * 1315423911ull) ^ ((uint64_t)dev << 56) ^ (uint64_t)tag;
   std::lock_guard<std::mutex> g(mu);
   Buf& b = bufs[key];
   if (b.n < bytes) {
-    if (b.p) cudaFree(b.p);
+    if (b.p) retired.push_back(b.p);
     b.p = nullptr;
-    if (cudaMalloc(&b.p, bytes) != cudaSuccess) { b.n = 0; return nullptr; }
-    b.n = bytes;
+    // grow geometrically so a slowly growing request retires few buffers
+    size_t want = std::max(bytes, b.n * 2);
+    if (cudaMalloc(&b.p, want) != cudaSuccess) {
+      b.p = nullptr;
+      if (cudaMalloc(&b.p, bytes) != cudaSuccess) { b.n = 0; return nullptr; }
+      want = bytes;
+    }
+    b.n = want;
   }
   return b.p;
+}
+
+int set_smem_attr(const void* fn, int bytes) {
+  static std::mutex mu;
+  static std::set<std::tuple<int, const void*, int>> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> g(mu);
+  auto key = std::make_tuple(dev, fn, bytes);
+  if (done.count(key)) return 0;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e != cudaSuccess) return fail(CC_E_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
+  done.insert(key);
+  return 0;
+}
+
+static std::atomic<long long> g_bf16_simt{0};
+void note_simt(int dtype) {
+  if (dtype == CC_BF16) g_bf16_simt.fetch_add(1, std::memory_order_relaxed);
 }
 
 int num_sms() {
@@ -71,6 +104,8 @@ int cc_set_pdl(int on) {
 }
 
 const char* cc_last_error(void) { return ccb::g_last_error.c_str(); }
+
+long long cc_bf16_simt_launches(void) { return ccb::g_bf16_simt.load(); }
 
 int cc_sm_count(int device) {
   int v = 0;

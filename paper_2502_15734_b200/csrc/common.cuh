@@ -70,7 +70,19 @@ __device__ __forceinline__ double silu(double x) { return x / (1.0 + exp(-x)); }
 inline size_t dtype_size(int dtype) { return dtype == CC_F64 ? 8 : (dtype == CC_F32 ? 4 : 2); }
 
 int num_sms();
+void note_simt(int dtype);  // counts bf16 SIMT launches (cc_bf16_simt_launches)
+// scratch tags: one per kernel family, so no two families share a buffer
+enum ScratchTag { SCR_LOGITS = 1, SCR_SEGMASS = 2, SCR_ATTN = 3, SCR_DECODE_ATTN = 4 };
 void* stream_scratch(cudaStream_t st, int tag, size_t bytes);
+
+// Dynamic shared-memory opt-in, once per (device, kernel): thread-safe, and
+// correct when one process drives several GPUs (a function attribute is
+// per-device state).
+int set_smem_attr(const void* fn, int bytes);
+template <typename... KArgs>
+inline int ensure_smem(void (*fn)(KArgs...), size_t bytes) {
+  return set_smem_attr(reinterpret_cast<const void*>(fn), (int)bytes);
+}
 
 // ---- programmatic dependent launch (PDL) ------------------------------------
 // Kernels of the decode chain call pdl_trigger() first (the next kernel may be

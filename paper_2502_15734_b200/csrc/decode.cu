@@ -394,14 +394,14 @@ int gemv_launch(const void* A, int64_t lda, const void* W, int64_t ldw, void* C,
   const int n_out = epi == CC_EPI_SWIGLU ? N / 2 : N;
   const size_t smem = (size_t)M * K * 2;
   int grid = (n_out + GV_WARPS - 1) / GV_WARPS;
-  static bool attr = false;  // (the instantiations share one function-pointer type)
-  if (!attr) {
-    auto set = [](auto k) { cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024); };
+  {
+    int rc = 0;
+    auto set = [&](auto k) { if (!rc) rc = ensure_smem(k, 96 * 1024); };
 #define CCB_GV_SET(E) set(gemv_kernel<E, false, 1>); set(gemv_kernel<E, true, 1>); \
     set(gemv_kernel<E, false, GV_MAXM>); set(gemv_kernel<E, true, GV_MAXM>);
     CCB_GV_SET(CC_EPI_STORE) CCB_GV_SET(CC_EPI_RESID_ADD) CCB_GV_SET(CC_EPI_SWIGLU) CCB_GV_SET(CC_EPI_GELU)
 #undef CCB_GV_SET
-    attr = true;
+    if (rc) return rc;
   }
   auto go = [&](auto kern) {
     return launch_k(kern, dim3(grid), dim3(GV_WARPS * 32), smem, st, "gemv", A, lda, (const __nv_bfloat16*)W, ldw,
@@ -453,7 +453,7 @@ int decode_attention_impl(const void* q, const void* k_rot, const void* v, const
   const int G = n_heads / n_kv_heads;
   const int n_chunks = (n_keys + DA_KEYS - 1) / DA_KEYS;
   const size_t bytes = (size_t)n_chunks * n_heads * (DA_DH * sizeof(float) + sizeof(float2));
-  uint8_t* scratch = (uint8_t*)stream_scratch(st, 2, bytes);
+  uint8_t* scratch = (uint8_t*)stream_scratch(st, SCR_DECODE_ATTN, bytes);
   if (!scratch) return fail(CC_E_CUDA, "decode_attention: scratch allocation failed");
   float* part_o = reinterpret_cast<float*>(scratch);
   float2* part_ml = reinterpret_cast<float2*>(scratch + (size_t)n_chunks * n_heads * DA_DH * sizeof(float));

@@ -85,6 +85,7 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(const T* __restrict__ A,
 int gemm_simt(const void* A, int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc, int M, int N, int K,
               int epi, int dtype, cudaStream_t st) {
   if (epi == CC_EPI_SWIGLU) CCB_REQUIRE(N % 128 == 0, "gemm: SWIGLU needs N % 128 == 0 (64-col gate|up groups)");
+  note_simt(dtype);
   int n_out = epi == CC_EPI_SWIGLU ? N / 2 : N;
   dim3 grid((n_out + SB_N - 1) / SB_N, (M + SB_M - 1) / SB_M);
   CCB_REQUIRE(grid.y <= 65535, "gemm: M too large");
@@ -108,16 +109,14 @@ extern "C" int cc_gemm(const void* A, int64_t lda, const void* B, int64_t ldb, v
   CCB_REQUIRE(M >= 0 && N > 0 && K > 0, "gemm: bad shape");
   if (M == 0) return 0;
   cudaStream_t st = as_stream(stream);
-  // impl: 0 auto (bf16: <= 4 rows -> weight-streaming GEMV, else tcgen05 with
-  // stream-K allowed; SIMT if unsupported), 1 tcgen05 with stream-K, 4 tcgen05
-  // without split (batch/M-invariant), 2 SIMT reference
+  // impl: 0 product path (bf16: <= 4 rows -> weight-streaming GEMV, else the
+  // tcgen05 kernel with stream-K allowed; an unsupported shape is an error,
+  // never a silent SIMT fallback; fp32/fp64 parity modes: SIMT),
+  // 1 tcgen05 with stream-K, 4 tcgen05 without split (batch/M-invariant),
+  // 2 SIMT reference (tests)
   if (dtype == CC_BF16 && impl == 0 && gemv_eligible(M, N, K, epilogue, A, lda, B, ldb))
     return gemv_bf16(A, lda, B, ldb, C, ldc, M, N, K, epilogue, st);
-  if (dtype == CC_BF16 && impl != 2) {
-    int rc = gemm_tc_bf16(A, lda, B, ldb, C, ldc, M, N, K, epilogue, impl != 4, st);
-    if (rc != CC_E_UNSUP || impl == 1 || impl == 4) return rc;
-  } else if (impl == 1 || impl == 4) {
-    return fail(CC_E_UNSUP, "gemm: tcgen05 kernel requires bf16");
-  }
+  if (dtype == CC_BF16 && impl != 2) return gemm_tc_bf16(A, lda, B, ldb, C, ldc, M, N, K, epilogue, impl != 4, st);
+  if (impl == 1 || impl == 4) return fail(CC_E_UNSUP, "gemm: tcgen05 kernel requires bf16");
   return gemm_simt(A, lda, B, ldb, C, ldc, M, N, K, epilogue, dtype, st);
 }

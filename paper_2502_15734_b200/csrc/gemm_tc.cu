@@ -846,14 +846,8 @@ struct Tiling {
 template <int EPI, int BN>
 int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, void* C, int64_t ldc, int M, int N, int K,
               const Tiling& tl, cudaStream_t st) {
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(gemm_tc_kernel<EPI, BN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)TcCfg<BN>::SMEM);
-    cudaFuncSetAttribute(gemm_tc_kernel<EPI, BN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)TcCfg<BN>::SMEM);
-    attr_set = true;
-  }
+  if (int rc = ensure_smem(gemm_tc_kernel<EPI, BN, false>, TcCfg<BN>::SMEM)) return rc;
+  if (int rc = ensure_smem(gemm_tc_kernel<EPI, BN, true>, TcCfg<BN>::SMEM)) return rc;
   const int tiles = ((M + TC_BM - 1) / TC_BM) * n_tiles_of(N, BN);
   SplitScratch& sc = scratch(st);
   if (tl.W > 0) {
@@ -886,12 +880,7 @@ constexpr int kBnCand[5] = {256, 224, 192, 160, 128};
 template <int EPI, int BNR>
 int launch_swap(const CUtensorMap& mw, const CUtensorMap& mx, void* C, int64_t ldc, int M, int N, int K,
                 const Tiling& tl, cudaStream_t st) {
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(gemm_tc_kernel<EPI, BNR, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)TcCfg<BNR>::SMEM);
-    attr_set = true;
-  }
+  if (int rc = ensure_smem(gemm_tc_kernel<EPI, BNR, false, true>, TcCfg<BNR>::SMEM)) return rc;
   const int tiles = ((N + TC_BM - 1) / TC_BM) * n_tiles_of(M, BNR);
   return launch_k(gemm_tc_kernel<EPI, BNR, false, true>, dim3(tl.grid), dim3(TC_THREADS), TcCfg<BNR>::SMEM, st,
                   "gemm_tc_swap", mw, mx, C, ldc, N, M, K, tiles, 0LL, (float*)nullptr, (int*)nullptr, 0, g_trace,
@@ -1171,11 +1160,7 @@ int launch_epi(const void* A, int64_t lda, const void* B, int64_t ldb, void* C, 
     rc = make_map(&mc, C, M, EPI == CC_EPI_SWIGLU ? N / 2 : N, ldc,
                   EPI == CC_EPI_RESID_ADD ? -2 : EPI == CC_EPI_SWIGLU ? -3 : -1);
     if (rc) return rc;
-    static bool attr_set = false;
-    if (!attr_set) {
-      cudaFuncSetAttribute(gemm_pair_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P2_SMEM);
-      attr_set = true;
-    }
+    if (int rc2 = ensure_smem(gemm_pair_kernel<EPI>, P2_SMEM)) return rc2;
     static const int dbg = getenv("CCB_PAIR_DBG") ? atoi(getenv("CCB_PAIR_DBG")) : 0;
     return launch_k(gemm_pair_kernel<EPI>, dim3(tl.grid), dim3(TC_THREADS), P2_SMEM, st, "gemm_pair", mw, mx[0], mx[1],
                     mx[2], mx[3], mc, M, K, dbg, tl.tab->tab);
@@ -1230,11 +1215,7 @@ int gemm_tc_peer_push(const void* A, int64_t lda, const void* B, int64_t ldb, in
   if (rc) return rc;
   Tiling tl = plan_dp(M, N, bn);
   auto go = [&](auto kern, size_t smem) {
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      attr = true;
-    }
+    if (int rc = ensure_smem(kern, smem)) return rc;
     kern<<<tl.grid, TC_THREADS, smem, st>>>(ma, mb, nullptr, 0, M, N, K, tl.t_dp, 0LL, nullptr, nullptr, 0, g_trace,
                                             tab);
     return check_launch("gemm_tc_peer_push");

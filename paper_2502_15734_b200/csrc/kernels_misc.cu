@@ -705,7 +705,7 @@ int cc_logits_argmax(const void* hidden_rows, const float* norm_w, double eps, c
     size_t smem = (size_t)m * d * sizeof(A);
     CCB_REQUIRE(smem <= 200 * 1024, "logits_argmax: rows too wide");
     if (smem > 48 * 1024)
-      cudaFuncSetAttribute(logits_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (int rc = ensure_smem(logits_kernel<T>, smem)) return rc;
     // 24 CTAs per SM (several waves of short CTAs): measured 198 us for the
     // 128256 x 4096 unembedding vs 217 (8 per SM), 207 (12), 208 (16), 204 (32)
     int grid = std::min((vocab + 7) / 8, num_sms() * 24);
@@ -715,7 +715,7 @@ int cc_logits_argmax(const void* hidden_rows, const float* norm_w, double eps, c
     if (argmax) {
       // partials live after the logits rows in a small static scratch
       constexpr int PARTS = 64;
-      uint8_t* scratch = (uint8_t*)stream_scratch(as_stream(stream), 1, (sizeof(A) + sizeof(int32_t)) * 8 * PARTS);
+      uint8_t* scratch = (uint8_t*)stream_scratch(as_stream(stream), SCR_LOGITS, (sizeof(A) + sizeof(int32_t)) * 8 * PARTS);
       if (!scratch) return fail(CC_E_CUDA, "logits_argmax: scratch allocation failed");
       A* part_v = reinterpret_cast<A*>(scratch);
       int32_t* part_i = reinterpret_cast<int32_t*>(scratch + sizeof(A) * 8 * PARTS);
@@ -737,7 +737,7 @@ int cc_topk_select(const double* scores, const int32_t* off, const int32_t* coun
   while (P < std::max(max_len, 1)) P <<= 1;
   size_t smem = (size_t)P * (sizeof(double) + sizeof(int) + 1);
   if (smem > 48 * 1024)
-    cudaFuncSetAttribute(topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (int rc = ensure_smem(topk_kernel, smem)) return rc;
   topk_kernel<<<n_chunks, 1024, smem, as_stream(stream)>>>(scores, off, count, off_out, out, P);
   return check_launch("topk_select");
 }

@@ -285,7 +285,7 @@ def _attn_ref(q, k, v, q_slot, pad, Hq, Hkv):
                                           (32, 8, 128, 2100), (64, 8, 128, 300), (32, 8, 128, 5152)])
 def test_attention_scattered_rows(N, Hq, Hkv, dh, n):
     """impl 1 = tcgen05/TMEM kernel (key range split in two for the long row
-    tiles when n >= 1024, merged in fixed order), 3 = mma.sync kernel, 2 = SIMT."""
+    tiles when n >= 1024, merged in fixed order), 2 = SIMT reference."""
     g = torch.Generator(device="cuda").manual_seed(Hq + dh)
     rows = torch.sort(torch.randperm(n, generator=g, device="cuda")[:150]).values.int()
     q = torch.randn((rows.numel(), Hq, dh), generator=g, device="cuda").bfloat16()
@@ -298,7 +298,7 @@ def test_attention_scattered_rows(N, Hq, Hkv, dh, n):
     q = q[: rows.numel()].contiguous()
     ctx = torch.empty((rows.numel(), Hq * dh), dtype=torch.bfloat16, device="cuda")
     lse = torch.empty((rows.numel(), Hq), dtype=torch.float32, device="cuda")
-    for impl in (1, 3, 2):
+    for impl in (1, 2):
         ctx.zero_()
         N.call("cc_attention", N.ptr(q), N.ptr(k), N.ptr(v), N.ptr(rows), N.ptr(pad), N.ptr(ctx), N.ptr(lse),
                rows.numel(), n, Hq, Hkv, dh, N.BF16, impl, N.stream_ptr())
@@ -404,3 +404,32 @@ def test_segment_mass_tensor_core_matches_simt(N, Hq, Hkv, dh):
            N.ptr(rows), rows.numel(), N.ptr(again), n, Hq, Hkv, dh, N.BF16, N.stream_ptr())
     torch.cuda.synchronize()
     assert torch.equal(again, out["tc"])  # deterministic
+
+
+def test_bf16_product_path_fails_loudly_on_unsupported_shapes(N):
+    """No silent fallback: in bf16 the product path (impl 0) runs the tcgen05
+    kernels (or the M <= 4 GEMV) only; a shape they do not support is an
+    error, and no SIMT kernel ever runs on bf16 data unless asked (impl 2)."""
+    from paper_2502_15734_b200.errors import NativeError
+
+    before = N.bf16_simt_launches()
+    A = torch.randn((64, 128), device="cuda").bfloat16()
+    B = torch.randn((100, 128), device="cuda").bfloat16()  # N % 128 != 0
+    C = torch.zeros((64, 100), dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(NativeError, match="gemm_tc"):
+        N.call("cc_gemm", N.ptr(A), 128, N.ptr(B), 128, N.ptr(C), 100, 64, 100, 128, N.EPI_STORE, N.BF16, 0,
+               N.stream_ptr())
+    q = torch.randn((8, 4, 32), device="cuda").bfloat16()  # d_head 32: no tcgen05 attention
+    kv = torch.randn((64, 4, 32), device="cuda").bfloat16()
+    rows = torch.arange(8, dtype=torch.int32, device="cuda")
+    ctx = torch.empty((8, 128), dtype=torch.bfloat16, device="cuda")
+    lse = torch.empty((8, 4), dtype=torch.float32, device="cuda")
+    with pytest.raises(NativeError, match="attention_tc"):
+        N.call("cc_attention", N.ptr(q), N.ptr(kv), N.ptr(kv), N.ptr(rows), None, N.ptr(ctx), N.ptr(lse), 8, 64, 4, 4,
+               32, N.BF16, 0, N.stream_ptr())
+    N.assert_tensor_core_only(before)
+    # the explicit SIMT reference is counted
+    N.call("cc_attention", N.ptr(q), N.ptr(kv), N.ptr(kv), N.ptr(rows), None, N.ptr(ctx), N.ptr(lse), 8, 64, 4, 4,
+           32, N.BF16, 2, N.stream_ptr())
+    torch.cuda.synchronize()
+    assert N.bf16_simt_launches() == before + 1

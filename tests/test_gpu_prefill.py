@@ -3,7 +3,7 @@ golden fixtures and the CPU oracle.
 
 Tolerances (north star): fp64 mode ~1e-9 absolute (the reference's own
 precision); fp32 mode 1e-3 relative; bf16 mode a bf16 tolerance (relative
-Frobenius error < 5e-2 on hidden/KV) plus an identical greedy next token.
+Frobenius error, BF16_TOY_TOL) plus an identical greedy next token.
 Selections and plan decisions are bit-exact."""
 import numpy as np
 import pytest
@@ -11,9 +11,17 @@ import pytest
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
-from ccb_helpers import golden_path  # noqa: E402
+from ccb_helpers import golden_path, record_measurement  # noqa: E402
 
 from oracle import cachecraft_oracle as O  # noqa: E402
+
+
+# bf16 mode against the float64 reference WITH UNROUNDED weights (the error
+# includes rounding the weights to bf16): ~3x the largest relative error
+# measured on the B200 over these small-model tests
+# (profiles/r2_parity_small.jsonl); the full-size tests in
+# test_gpu_parity_fullsize.py compare against the bf16-rounded weights
+BF16_TOY_TOL = 5e-2
 
 
 @pytest.fixture(scope="module")
@@ -69,13 +77,15 @@ def test_toy_fix_up_matches_reference_fp64(cc):
     np.testing.assert_allclose(model.logits(res.hidden[req.question_span[1] - 1])[0], g["logits_last"], atol=1e-9)
 
 
-@pytest.mark.parametrize("dtype,tol", [("fp32", 1e-3), ("bf16", 5e-2)])
+@pytest.mark.parametrize("dtype,tol", [("fp32", 1e-3), ("bf16", BF16_TOY_TOL)])
 def test_toy_fix_up_low_precision(cc, dtype, tol):
     g, model, req, res = toy_result(cc, dtype)
-    assert rel(res.hidden, g["hidden"]) < tol
-    for l in range(4):
-        assert rel(res.kv.keys[l], g[f"k{l}"]) < tol
-        assert rel(res.kv.values[l], g[f"v{l}"]) < tol
+    e = {"hidden": rel(res.hidden, g["hidden"]),
+         "keys": max(rel(res.kv.keys[l], g[f"k{l}"]) for l in range(4)),
+         "values": max(rel(res.kv.values[l], g[f"v{l}"]) for l in range(4))}
+    record_measurement("toy_fix_up", {"dtype": dtype, **e})
+    for k, v in e.items():
+        assert v < tol, (k, e)
     assert res.first_token == int(g["first_token"])
 
 
@@ -180,10 +190,13 @@ def config1_device(cc, dtype):
 @pytest.mark.parametrize("dtype", ["fp64", "fp32", "bf16"])
 def test_config1_creation_stats_and_selection(cc, dtype):
     g, model, caches, scores, meta = config1_device(cc, dtype)
-    tol = {"fp64": 1e-10, "fp32": 1e-3, "bf16": 5e-2}[dtype]
-    assert rel(np.stack(scores), g["scores"]) < tol
-    assert rel(np.array(meta)[:, :2], g["meta"][:, :2]) < tol
+    tol = {"fp64": 1e-10, "fp32": 1e-3, "bf16": BF16_TOY_TOL}[dtype]
+    e = {"scores": rel(np.stack(scores), g["scores"]), "meta": rel(np.array(meta)[:, :2], g["meta"][:, :2])}
     sel = [cc.select_tokens(s, 0.15) for s in scores]
+    flips = sum(len(set(a.tolist()) ^ set(b.tolist())) // 2 for a, b in zip(sel, g["selected"]))
+    record_measurement("config1_creation", {"dtype": dtype, **e, "flips": flips,
+                                            "selected": int(sum(len(s) for s in g["selected"]))})
+    assert e["scores"] < tol and e["meta"] < tol, e
     if dtype != "bf16":
         np.testing.assert_array_equal(np.stack(sel), g["selected"])
     else:
@@ -192,10 +205,10 @@ def test_config1_creation_stats_and_selection(cc, dtype):
             diff = set(got.tolist()) ^ set(want.tolist())
             if diff:
                 kth = np.sort(s_o)[::-1][len(want) - 1]
-                assert all(abs(s_o[i] - kth) < 5e-2 * abs(kth) for i in diff)
+                assert all(abs(s_o[i] - kth) < 3 * e["scores"] * abs(kth) for i in diff)
 
 
-@pytest.mark.parametrize("dtype,tol", [("fp64", 1e-9), ("fp32", 1e-3), ("bf16", 5e-2)])
+@pytest.mark.parametrize("dtype,tol", [("fp64", 1e-9), ("fp32", 1e-3), ("bf16", BF16_TOY_TOL)])
 def test_config1_fix_up_matches_reference(cc, dtype, tol):
     g, model, caches, _, _ = config1_device(cc, dtype)
     segs = []
@@ -206,14 +219,16 @@ def test_config1_fix_up_matches_reference(cc, dtype, tol):
     req = cc.build_request(segs, g["question"])
     res = cc.prefill(model, req, first_token=True)
     q0, q1 = req.question_span
+    rows = g["kv_rows"]
+    e = {"hidden_q": rel(res.hidden[q0:q1], g["hidden_q"]),
+         "keys": max(rel(res.kv.keys[l][rows], g[f"k{l}"]) for l in range(2)),
+         "values": max(rel(res.kv.values[l][rows], g[f"v{l}"]) for l in range(2))}
+    record_measurement("config1_fix_up", {"dtype": dtype, **e})
     if dtype == "fp64":
         np.testing.assert_allclose(res.hidden[q0:q1], g["hidden_q"], atol=tol)
     else:
-        assert rel(res.hidden[q0:q1], g["hidden_q"]) < tol
-    rows = g["kv_rows"]
-    for l in range(2):
-        assert rel(res.kv.keys[l][rows], g[f"k{l}"]) < max(tol, 1e-12)
-        assert rel(res.kv.values[l][rows], g[f"v{l}"]) < max(tol, 1e-12)
+        assert e["hidden_q"] < tol, e
+    assert e["keys"] < max(tol, 1e-12) and e["values"] < max(tol, 1e-12), e
     assert res.first_token == int(g["first_token"])
     assert res.active_per_layer == g["active_per_layer"].tolist()
 
@@ -223,7 +238,7 @@ def test_config1_fix_up_matches_reference(cc, dtype, tol):
 # ---------------------------------------------------------------------------
 
 
-@pytest.mark.parametrize("dtype,tol", [("fp64", 1e-9), ("fp32", 1e-3), ("bf16", 5e-2)])
+@pytest.mark.parametrize("dtype,tol", [("fp64", 1e-9), ("fp32", 1e-3), ("bf16", BF16_TOY_TOL)])
 def test_llama_shaped_fix_up_vs_oracle(cc, dtype, tol):
     kw = dict(n_layers=3, n_heads=8, d_model=512, d_head=64, vocab_size=512, rpe_base=500000.0, seed=4,
               n_kv_heads=2, d_ff=1024, mlp="swiglu", norm_weight=True, rms_eps=1e-5)
@@ -245,13 +260,15 @@ def test_llama_shaped_fix_up_vs_oracle(cc, dtype, tol):
     res = cc.prefill(model, cc.build_request(segs, q), first_token=True)
     lay = O.layout([{"tokens": c, "n_slots": c.size, "recompute": m} for c, m in zip(chunks, masks)], q)
     ref = O.prefill(w, ocfg, lay, ocaches)
+    e = {"hidden": rel(res.hidden, ref["hidden"]),
+         "keys": max(rel(res.kv.keys[l], ref["keys"][l]) for l in range(3)),
+         "values": max(rel(res.kv.values[l], ref["values"][l]) for l in range(3))}
+    record_measurement("llama_small_fix_up", {"dtype": dtype, **e})
     if dtype == "fp64":
         np.testing.assert_allclose(res.hidden, ref["hidden"], atol=tol)
     else:
-        assert rel(res.hidden, ref["hidden"]) < tol
-    for l in range(3):
-        assert rel(res.kv.keys[l], ref["keys"][l]) < max(tol, 1e-12)
-        assert rel(res.kv.values[l], ref["values"][l]) < max(tol, 1e-12)
+        assert e["hidden"] < tol, e
+    assert e["keys"] < max(tol, 1e-12) and e["values"] < max(tol, 1e-12), e
     assert res.first_token == O.greedy_token(w, ocfg, ref)
 
 
