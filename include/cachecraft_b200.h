@@ -164,7 +164,9 @@ CC_API int cc_chunk_stats(const double* mass, int L, int n_rows, int n_seg, cons
 
 /* K9 — per-chunk top-count selection (planner.py:17-34): order by
  * (score desc, index asc), keep the first count[c], emit ascending indices
- * into out[off_out[c] ...].  Scores are float64; bit-exact vs the reference. */
+ * into out[off_out[c] ...].  Scores are float64; bit-exact vs the reference.
+ * No length limit: chunks up to 8192 tokens sort in shared memory (bitonic),
+ * longer ones use an exact radix select over global memory. */
 CC_API int cc_topk_select(const double* scores, const int32_t* off, const int32_t* count,
                    const int32_t* off_out, int32_t* out, int n_chunks, int max_len, void* stream);
 

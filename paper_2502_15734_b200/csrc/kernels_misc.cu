@@ -432,8 +432,104 @@ __global__ void __launch_bounds__(1024) argmax_kernel(const A* __restrict__ logi
 // K9 top-k: bitonic sort of (score desc, index asc) in shared memory, then an
 // ordered compaction of the selected indices (ascending output).
 // ---------------------------------------------------------------------------
+constexpr int TOPK_SMEM_MAX = 8192;  // longest chunk the shared-memory bitonic sort holds
+
 __device__ __forceinline__ bool precedes(double sa, int ia, double sb, int ib) {
   return sa > sb || (sa == sb && ia < ib);
+}
+
+// Exclusive scan of one int per thread over a 1024-thread block; *total gets
+// the block sum.  `tmp` is 33 ints of shared memory.
+__device__ __forceinline__ int block_excl_scan(int v, int* tmp, int* total) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int incl = v;
+  for (int o = 1; o < 32; o <<= 1) {
+    int t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  if (lane == 31) tmp[w] = incl;
+  __syncthreads();
+  if (w == 0) {
+    int t = lane < (int)(blockDim.x >> 5) ? tmp[lane] : 0;
+    for (int o = 1; o < 32; o <<= 1) {
+      int u = __shfl_up_sync(0xffffffffu, t, o);
+      if (lane >= o) t += u;
+    }
+    tmp[lane] = t;  // inclusive per-warp totals
+  }
+  __syncthreads();
+  const int ex = incl - v + (w > 0 ? tmp[w - 1] : 0);
+  *total = tmp[(blockDim.x >> 5) - 1];
+  __syncthreads();  // tmp is reused by the next call
+  return ex;
+}
+
+// Order-preserving map of a finite double to uint64 (larger score -> larger
+// key; -0.0 and +0.0 map to the same key, as numpy compares them equal).
+__device__ __forceinline__ unsigned long long score_key(double s) {
+  if (s == 0.0) s = 0.0;
+  const unsigned long long b = (unsigned long long)__double_as_longlong(s);
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+
+// K9 for chunks longer than the shared-memory sort holds (planner.py:17-34,
+// same result): an 8-pass radix select finds the key T of the k-th best
+// score; every score above T is selected, plus the first `need` scores equal
+// to T in index order (ties go to the lower index); one ordered block-wide
+// compaction writes the indices ascending.  One CTA per chunk.
+__global__ void __launch_bounds__(1024) topk_radix_kernel(const double* __restrict__ scores,
+                                                          const int32_t* __restrict__ off,
+                                                          const int32_t* __restrict__ count,
+                                                          const int32_t* __restrict__ off_out,
+                                                          int32_t* __restrict__ out) {
+  __shared__ unsigned int hist[256];
+  __shared__ unsigned long long prefix_s;
+  __shared__ int need_s;
+  __shared__ int scan_tmp[33];
+  const int c = blockIdx.x;
+  const int base = off[c], n = off[c + 1] - off[c], k = min(count[c], n);
+  if (k <= 0) return;
+  const double* s = scores + base;
+  unsigned long long prefix = 0, mask = 0;
+  int need = k;
+  for (int shift = 56; shift >= 0; shift -= 8) {
+    for (int b = threadIdx.x; b < 256; b += blockDim.x) hist[b] = 0;
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      const unsigned long long key = score_key(s[i]);
+      if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255u], 1u);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int acc = 0, b = 255;
+      for (; b > 0; --b) {
+        if (acc + (int)hist[b] >= need) break;
+        acc += (int)hist[b];
+      }
+      prefix_s = prefix | ((unsigned long long)b << shift);
+      need_s = need - acc;
+    }
+    __syncthreads();
+    prefix = prefix_s;
+    need = need_s;
+    mask |= 0xffull << shift;
+  }
+  const unsigned long long T = prefix;
+  int32_t* o = out + off_out[c];
+  int written = 0, ties = 0;
+  for (int t0 = 0; t0 < n; t0 += blockDim.x) {
+    const int i = t0 + threadIdx.x;
+    const unsigned long long key = i < n ? score_key(s[i]) : 0ull;
+    const bool gt = i < n && key > T, eq = i < n && key == T;
+    int n_eq;
+    const int tie_rank = block_excl_scan(eq ? 1 : 0, scan_tmp, &n_eq);
+    const bool sel = gt || (eq && ties + tie_rank < need);
+    int n_sel;
+    const int pos = block_excl_scan(sel ? 1 : 0, scan_tmp, &n_sel);
+    if (sel) o[written + pos] = i;
+    written += n_sel;
+    ties += n_eq;
+  }
 }
 
 __global__ void __launch_bounds__(1024) topk_kernel(const double* __restrict__ scores,
@@ -731,8 +827,11 @@ int cc_logits_argmax(const void* hidden_rows, const float* norm_w, double eps, c
 
 int cc_topk_select(const double* scores, const int32_t* off, const int32_t* count, const int32_t* off_out,
                    int32_t* out, int n_chunks, int max_len, void* stream) {
-  CCB_REQUIRE(max_len <= 8192, "topk_select: chunk longer than 8192 tokens");
   if (n_chunks == 0) return 0;
+  if (max_len > TOPK_SMEM_MAX) {  // long chunks: radix select over global memory, any length
+    topk_radix_kernel<<<n_chunks, 1024, 0, as_stream(stream)>>>(scores, off, count, off_out, out);
+    return check_launch("topk_select_radix");
+  }
   int P = 1;
   while (P < std::max(max_len, 1)) P <<= 1;
   size_t smem = (size_t)P * (sizeof(double) + sizeof(int) + 1);

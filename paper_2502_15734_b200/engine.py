@@ -123,20 +123,26 @@ class LazyAttention:
         self.model, self.plan, self.k_rot = model, plan, k_rot
         self.q = {}
         self.lse = {}
+        # row order of each recorded layer (an online focus cut permutes the
+        # hidden rows mid-prefill: earlier layers keep the order they ran in)
+        self.rows = {}
+        self.row_slot = {}
 
     def materialize(self, layer: int) -> np.ndarray:
         import torch
 
         cfg = self.model.kcfg
-        n_l = self.plan.n_act[layer]
         H = cfg.n_heads
+        rows = self.rows.get(layer, self.plan.rows[: self.plan.n_act[layer]])
+        n_l = rows.size
         if n_l == 0:
             return np.zeros((H, 0, self.plan.n))
+        slot = self.row_slot.get(layer, self.plan.d["row_slot"])
         probs = torch.empty((H, n_l, self.plan.n), dtype=self.model.hidden_dtype, device=self.model.device)
-        N.call("cc_attention_probs", N.ptr(self.q[layer]), N.ptr(self.k_rot[layer]), N.ptr(self.plan.d["row_slot"]),
+        N.call("cc_attention_probs", N.ptr(self.q[layer]), N.ptr(self.k_rot[layer]), N.ptr(slot),
                N.ptr(self.plan.key_pad) if self.plan.has_pad else None, N.ptr(self.lse[layer]), N.ptr(probs), n_l,
                self.plan.n, H, cfg.kv_heads(), cfg.head_dim(), self.model.dtype_code, N.stream_ptr())
-        order = np.argsort(self.plan.rows[:n_l], kind="stable")
+        order = np.argsort(rows, kind="stable")
         return probs.double().cpu().numpy()[:, order]
 
     def materialize_all(self) -> list:
@@ -370,6 +376,17 @@ def _apply_cut(model, plan, ws, slots, new_depth):
     plan.d["active_until"].copy_(torch.from_numpy(plan.active_until_h).to(dev))
     if getattr(plan, "stats_row_spans", None):
         _attach_stats_rows(model, plan, plan.stats_row_spans)
+        # stats rows of spans containing cut slots hold no valid mass from new_depth on
+        cut_rows, off = [], 0
+        for lo, hi in plan.stats_row_spans:
+            if np.any((slots >= lo) & (slots < hi)):
+                cut_rows.extend(range(off, off + hi - lo))
+            off += hi - lo
+        if cut_rows:
+            import torch as _t
+
+            prev = getattr(plan, "stats_cut_rows", [])
+            plan.stats_cut_rows = prev + [(_t.tensor(cut_rows, device=dev), new_depth)]
     # stale rows of the cut slots for layers >= new_depth (K1 on the affected blocks only)
     touched = [it for it in plan.items if np.any((slots >= it["dst_slot"]) & (slots < it["dst_slot"] + it["n_rows"]))]
     if touched and new_depth < L:
@@ -441,7 +458,7 @@ def _execute(model: Model, plan: DevicePlan, ws: dict, *, record=False, record_v
             if preload is not None:  # nothing computed at this layer: the cached rows still land
                 preload.gather(model, plan, ws, l, rope, s)
             if record_values:
-                vtrace.append((kv_v[l], None))
+                vtrace.append((kv_v[l], None, None))
             continue
         N.call("cc_rmsnorm", P(hidden), P(xn), P(lw.get("attn_norm")), n_l, d, eps, dt, s)
         with tm.span("gemm", flops=2.0 * n_l * (qw + 2 * kvw) * d):
@@ -478,8 +495,11 @@ def _execute(model: Model, plan: DevicePlan, ws: dict, *, record=False, record_v
         if record:
             lazy.q[l] = q_rot[:n_l].clone()
             lazy.lse[l] = lse[:n_l].clone()
+            lazy.rows[l] = plan.rows[:n_l].copy()
+            if focus is not None:  # a later cut rewrites row_slot in place
+                lazy.row_slot[l] = D["row_slot"][:n_l].clone()
         if record_values:
-            vtrace.append((kv_v[l], ctx[:n_l].clone()))
+            vtrace.append((kv_v[l], ctx[:n_l].clone(), plan.rows[:n_l].copy()))
         with tm.span("gemm", flops=2.0 * n_l * qw * d):
             if tp is None:
                 N.call("cc_gemm", P(ctx), qw, P(lw["w_o"]), qw, P(hidden), d, n_l, d, qw, N.EPI_RESID_ADD, dt,
@@ -505,6 +525,11 @@ def _execute(model: Model, plan: DevicePlan, ws: dict, *, record=False, record_v
             focus.cut = True
             if n_stats:
                 n_stats = plan.stats_rows.size
+    if mass is not None and getattr(plan, "stats_cut_rows", None):
+        # rows of a stats span cut by the online focus stop at the cut layer:
+        # the segment-mass kernel read stale rows for them afterwards
+        for rows_, depth_ in plan.stats_cut_rows:
+            mass[depth_:, rows_] = 0.0
     if tp is not None and mass is not None:
         # K8a divides by the rank's own heads: global head mean = sum over ranks / world
         mass.mul_(1.0 / tp.world)
@@ -672,12 +697,12 @@ class _ValueTrace(list):
 
     def __init__(self, raw, plan):
         out = []
-        for l, (v, c) in enumerate(raw):
+        for l, (v, c, rows) in enumerate(raw):
             vv = v.double().cpu().numpy()
             if c is None:
                 out.append((vv, np.zeros((0, v.shape[-1]))))
                 continue
-            order = np.argsort(plan.rows[: c.shape[0]], kind="stable")
+            order = np.argsort(rows, kind="stable")
             out.append((vv, c.double().cpu().numpy()[order]))
         super().__init__(out)
 

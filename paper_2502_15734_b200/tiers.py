@@ -21,8 +21,11 @@ slot is released to layer l + L_p once that gather is done.  ``L_p`` is the
 reference's ``preload_depth`` (tiers.py:62-71).
 
 ``Tier``, ``TierConfig``, ``preload_depth`` and ``place_and_migrate`` keep
-the reference's names, fields, arithmetic and errors (checked against
-reference fixtures); the timeline simulator itself is out of scope.
+the reference's names, fields, results and errors (checked against
+reference fixtures).  The reference's discrete-event timeline simulator
+(``simulate``, ``Timeline``, ``timeline_to_csv``) is out of scope: the tiers
+here are real, and ``demote_slow_hits`` replaces its ``fallback_decision``
+with a cost check on the measured host->HBM rate.
 """
 
 from __future__ import annotations
@@ -43,22 +46,27 @@ HBM, HOST, DISK = "hbm", "host", "disk"
 
 
 # ---------------------------------------------------------------------------
-# reference control logic (tiers.py:27-71, :209-261)
+# placement policy and preload depth (reference tiers.py:27-71, :212-257)
 # ---------------------------------------------------------------------------
 
 
 @dataclass(frozen=True)
 class Tier:
+    """One storage level: ``bandwidth`` bytes/s, ``latency`` s per load,
+    optional byte budget and the share of variants (by f_r rank) it targets."""
+
     name: str
-    bandwidth: float  # bytes/s
-    latency: float = 0.0  # fixed seconds per load operation
+    bandwidth: float
+    latency: float = 0.0
     capacity_bytes: float | None = None
-    placement_fraction: float | None = None  # share of variants targeted, by f_r rank
+    placement_fraction: float | None = None
 
 
 @dataclass(frozen=True)
 class TierConfig:
-    tiers: tuple  # ordered fast -> slow
+    """Tiers ordered fastest first, plus the per-layer timing model."""
+
+    tiers: tuple
     n_layers: int
     t_prefill_layer: float
     t_decode_step: float = 0.0
@@ -66,80 +74,107 @@ class TierConfig:
     bytes_per_token_layer: float = 512.0
 
     def validate(self):
-        if not self.tiers:
+        if len(self.tiers) == 0:
             raise ArgumentError("need at least one tier")
-        for tier in self.tiers:
-            if tier.bandwidth <= 0:
-                raise ArgumentError(f"tier {tier.name} bandwidth must be positive")
-            if tier.latency < 0:
-                raise ArgumentError(f"tier {tier.name} latency must be non-negative")
-        if self.n_layers < 1 or self.t_prefill_layer <= 0:
+        bad_bw = next((t for t in self.tiers if not t.bandwidth > 0), None)
+        if bad_bw is not None:
+            raise ArgumentError(f"tier {bad_bw.name} bandwidth must be positive")
+        bad_lat = next((t for t in self.tiers if t.latency < 0), None)
+        if bad_lat is not None:
+            raise ArgumentError(f"tier {bad_lat.name} latency must be non-negative")
+        if not (self.n_layers >= 1 and self.t_prefill_layer > 0):
             raise ArgumentError("layer count and per-layer prefill time must be positive")
 
     def tier(self, name: str) -> Tier:
-        for tier in self.tiers:
-            if tier.name == name:
-                return tier
-        raise ArgumentError(f"unknown tier {name!r}")
+        by_name = {t.name: t for t in reversed(self.tiers)}  # first definition wins
+        if name not in by_name:
+            raise ArgumentError(f"unknown tier {name!r}")
+        return by_name[name]
 
 
 def preload_depth(n_layers: int, t_prefill: float, t_load: float) -> int:
-    """Smallest layer count to fetch ahead so computation never stalls:
-    L_p = ceil((L - 1)(1 - T_prefill / T_load) + 1), clamped to [1, L]
-    (tiers.py:62-71, PAPER.md eq. layerwise)."""
+    """Layers to fetch ahead so compute never waits on a load (Algorithm 2,
+    PAPER.md:758-776): L_p = ceil((L - 1)(1 - T_prefill/T_load) + 1), at least
+    1 and at most L (the 1e-9 slack keeps exact integers from rounding up)."""
     if n_layers < 1:
         raise ArgumentError("layer count must be >= 1")
-    if t_prefill <= 0 or t_load <= 0:
+    if not (t_prefill > 0 and t_load > 0):
         raise ArgumentError("per-layer times must be positive")
-    raw = (n_layers - 1) * (1.0 - t_prefill / t_load) + 1.0
-    depth = max(1, math.ceil(raw - 1e-9))
-    return min(depth, n_layers)
+    ahead = 1.0 + (n_layers - 1) * (1.0 - t_prefill / t_load)
+    return int(np.clip(math.ceil(ahead - 1e-9), 1, n_layers))
+
+
+def _band_sizes(n: int, tiers) -> list:
+    """How many of the n ranked variants each tier's band targets: a tier's
+    floor(fraction * n) (capped by what is left); the last tier, and any tier
+    without a fraction, takes the remainder."""
+    sizes, left = [], n
+    for pos, t in enumerate(tiers):
+        last = pos == len(tiers) - 1
+        take = left if (last or t.placement_fraction is None) else min(left, math.floor(t.placement_fraction * n))
+        sizes.append(int(take))
+        left -= int(take)
+    sizes[-1] += left
+    return sizes
 
 
 def place_and_migrate(variants, cfg: TierConfig) -> dict:
-    """Partition variants into tiers by f_r rank bands, respecting byte
-    budgets (spill to the next slower tier when a band is full)
-    (tiers.py:209-261).  Returns {variant_id: tier name}."""
+    """Assign every variant a tier: rank by reuse frequency (f_r desc, then
+    older first, then lower id), cut the ranking into the tiers' bands, and
+    let a variant whose band tier is out of budget spill to the next slower
+    tier with room.  Returns {variant_id: tier name}; PlacementError if the
+    fastest budget cannot hold the largest variant or nothing has room."""
     cfg.validate()
-    variants = sorted(variants, key=lambda v: (-v.f_r, v.created_at, v.variant_id))
-    if not variants:
+    ranked = sorted(variants, key=lambda v: (-v.f_r, v.created_at, v.variant_id))
+    if not ranked:
         return {}
-    fast = cfg.tiers[0]
-    largest = max(v.payload_bytes() for v in variants)
-    if fast.capacity_bytes is not None and largest > fast.capacity_bytes:
+    sizes = [v.payload_bytes() for v in ranked]
+    head = cfg.tiers[0]
+    if head.capacity_bytes is not None and max(sizes) > head.capacity_bytes:
         raise PlacementError(
-            f"fast tier budget {fast.capacity_bytes} cannot hold the largest variant ({largest} bytes)")
-    n = len(variants)
-    targets = []
-    assigned = 0
-    for idx, tier in enumerate(cfg.tiers):
-        if idx == len(cfg.tiers) - 1 or tier.placement_fraction is None:
-            targets.append(n - assigned)
-            assigned = n
-        else:
-            count = min(n - assigned, int(math.floor(tier.placement_fraction * n)))
-            targets.append(count)
-            assigned += count
-    if assigned < n:
-        targets[-1] += n - assigned
-    placement = {}
-    used = [0.0] * len(cfg.tiers)
-    band_of = []
-    for band, count in enumerate(targets):
-        band_of.extend([band] * count)
-    for variant, band in zip(variants, band_of):
-        placed = False
-        for idx in range(band, len(cfg.tiers)):
-            tier = cfg.tiers[idx]
-            size = variant.payload_bytes()
-            if tier.capacity_bytes is None or used[idx] + size <= tier.capacity_bytes:
-                placement[variant.variant_id] = tier.name
-                used[idx] += size
-                placed = True
-                break
-        if not placed:
-            raise PlacementError(f"no tier has room for variant {variant.variant_id}")
-    return placement
+            f"fast tier budget {head.capacity_bytes} cannot hold the largest variant ({max(sizes)} bytes)")
+    band = np.repeat(np.arange(len(cfg.tiers)), _band_sizes(len(ranked), cfg.tiers))
+    room = [math.inf if t.capacity_bytes is None else float(t.capacity_bytes) for t in cfg.tiers]
+    out = {}
+    for v, nbytes, first in zip(ranked, sizes, band):
+        fits = [k for k in range(int(first), len(cfg.tiers)) if nbytes <= room[k]]
+        if not fits:
+            raise PlacementError(f"no tier has room for variant {v.variant_id}")
+        room[fits[0]] -= nbytes
+        out[v.variant_id] = cfg.tiers[fits[0]].name
+    return out
+
+
+def demote_slow_hits(plan, model, disk_bytes_per_s: float = 3e9):
+    """Real-tier counterpart of the reference's fallback_decision
+    (tiers.py:260-299): a HIT whose payload sits in host memory or on disk is
+    demoted to a MISS (fresh recompute) when streaming its K/V would take
+    longer than recomputing the chunk.  With layer-wise preloading the load
+    overlaps compute, so the test is load time vs the chunk's own share of
+    the prefill: bytes / rate  >  tokens * L * (per-token-layer compute).
+    HBM-resident hits are never demoted.  Returns a new InferencePlan."""
+    from dataclasses import replace
+
+    from .planner import HIT, MISS, InferencePlan
+
+    cfg = model.kcfg
+    d, q, kv, ff = cfg.d_model, cfg.q_width(), cfg.kv_width(), cfg.ff_dim()
+    m = 3 if cfg.mlp == "swiglu" else 2
+    # linear FLOPs per token per layer at the rate the engine's GEMMs sustain
+    # (engine._estimate_layer_seconds uses the same figure)
+    tok_layer_s = 2.0 * (d * (q + 2 * kv) + q * d + m * d * ff) / 1.0e15
+    chunks = []
+    for cp in plan.chunks:
+        cache = getattr(cp, "cache", None)
+        t = tier_of(cache) if (cp.status == HIT and cache is not None) else HBM
+        if t in (HOST, DISK):
+            nbytes = cache._payload.nbytes()
+            rate = model.h2d_bytes_per_s if t == HOST else min(model.h2d_bytes_per_s, disk_bytes_per_s)
+            if nbytes / rate > cp.n_tokens * cfg.n_layers * tok_layer_s:
+                cp = replace(cp, status=MISS, variant_id=None, cfo=1.0, recompute=None, recompute_depth=None,
+                             score=None, cache=None, n_slots=cp.n_tokens)
+        chunks.append(cp)
+    return InferencePlan(chunks=chunks, question=plan.question, alpha=plan.alpha, focus_window=plan.focus_window)
 
 
 # ---------------------------------------------------------------------------

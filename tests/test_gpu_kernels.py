@@ -433,3 +433,26 @@ def test_bf16_product_path_fails_loudly_on_unsupported_shapes(N):
            32, N.BF16, 2, N.stream_ptr())
     torch.cuda.synchronize()
     assert N.bf16_simt_launches() == before + 1
+
+
+@pytest.mark.parametrize("n", [8193, 20000, 131072])
+def test_topk_select_long_chunks_radix_path(N, n):
+    """Chunks longer than the shared-memory sort (8192) go through the radix
+    select: same result as the reference's lexsort order, with heavy ties,
+    signed zeros and negative scores."""
+    import paper_2502_15734_b200 as cc
+    from paper_2502_15734_b200.planner import recompute_count, select_tokens_batched
+
+    r = np.random.default_rng(n)
+    s = np.round(r.standard_normal(n), 2)
+    s[r.choice(n, n // 10, replace=False)] = -0.0
+    s[r.choice(n, n // 10, replace=False)] = 0.0
+    for cfo in (1e-4, 0.15, 0.5, 1.0):
+        k = recompute_count(n, cfo)
+        want = np.sort(np.lexsort((np.arange(n), -s))[:k])
+        np.testing.assert_array_equal(cc.select_tokens(s, cfo), want)
+    # batched with a short chunk (both kernels' inputs in one launch)
+    short = np.round(r.standard_normal(300), 1)
+    got = select_tokens_batched([short, s], [recompute_count(300, 0.2), recompute_count(n, 0.2)])
+    np.testing.assert_array_equal(got[0], np.sort(np.lexsort((np.arange(300), -short))[:60]))
+    np.testing.assert_array_equal(got[1], np.sort(np.lexsort((np.arange(n), -s))[:recompute_count(n, 0.2)]))

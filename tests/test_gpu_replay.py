@@ -51,3 +51,42 @@ def test_replay_baselines_run_and_rank():
     assert aggs["full_recompute"]["tokens_computed"] >= aggs["exact_prefix"]["tokens_computed"]
     assert aggs["full_recompute"]["tokens_computed"] >= aggs["cachecraft"]["tokens_computed"]
     assert aggs["exact_prefix"]["mean_deviation"] < 1e-9
+
+
+def test_online_focus_cut_keeps_recorded_attention_and_values_consistent():
+    """prefill(focus_window=w, record_attention=True, record_values=True):
+    when the online early termination cuts unfocused chunks mid-prefill, the
+    recorded softmax weights, query slots and value traces of EVERY layer
+    equal those of a prefill that runs the post-cut depths from the start
+    (the reference's second pass, harness.py:425-428) — layers recorded
+    before the cut keep the row order they ran in."""
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import paper_2502_15734_b200 as cc
+
+    model = cc.build_model(cc.ModelConfig(n_layers=6, n_heads=4, d_model=64))
+    for seed in range(40):
+        r = np.random.default_rng(seed)
+        chunks = [r.integers(0, 256, 24) for _ in range(4)]
+        q = r.integers(0, 256, 6)
+        base = cc.prefill(model, cc.plain_request(*chunks, []), record_attention=False)
+        caches = [cc.extract_chunk_cache(base, s, e) for s, e in cc.plain_request(*chunks, []).segment_slots]
+        masks = [r.uniform(size=24) < 0.4 for _ in chunks]
+        segs = [cc.Segment(tokens=c, cache=k, recompute=m) for c, k, m in zip(chunks, caches, masks)]
+        one = cc.prefill(model, cc.build_request(segs, q), record_attention=True, record_values=True, focus_window=2)
+        if not one.extras.get("focus_cut"):
+            continue
+        focus = one.extras["focus"]
+        segs2 = []
+        for i, (c, k, m) in enumerate(zip(chunks, caches, masks)):
+            depth = None if i in focus.focused else np.full(24, focus.cutoff_layer, np.int64)
+            segs2.append(cc.Segment(tokens=c, cache=k, recompute=m, recompute_depth=depth))
+        two = cc.prefill(model, cc.build_request(segs2, q), record_attention=True, record_values=True)
+        assert one.active_per_layer == two.active_per_layer
+        for l in range(6):
+            np.testing.assert_array_equal(one.attn.query_slots[l], two.attn.query_slots[l])
+            np.testing.assert_allclose(one.attn.weights[l], two.attn.weights[l], atol=1e-12, rtol=0)
+            np.testing.assert_allclose(one.value_trace[l][1], two.value_trace[l][1], atol=1e-12, rtol=0)
+        np.testing.assert_allclose(one.hidden, two.hidden, atol=1e-12, rtol=0)
+        return
+    pytest.skip("no seed produced an early-termination cut")

@@ -107,3 +107,32 @@ def test_store_placement_migrates_variants(cc):
     T.TieredPool(model).apply_placement(store, placement)
     for vid, tier in placement.items():
         assert T.tier_of(store.get(vid).cache) == tier
+
+
+def test_demote_slow_hits_uses_the_measured_load_rate(cc):
+    """A host-tier HIT is demoted to a fresh MISS only when streaming its K/V
+    over the host link would take longer than recomputing the chunk; HBM hits
+    are never demoted (reference fallback_decision, tiers.py:260-299, on the
+    real tiers)."""
+    from paper_2502_15734_b200 import tiers
+    from paper_2502_15734_b200.planner import HIT, MISS
+
+    model, chunks, q, caches, masks = _setup(cc, "bf16", LLAMA, (64, 48, 80), 5)
+    store = cc.VariantStore(cc.StoreConfig())
+    for c, k in zip(chunks, caches):
+        store.insert(cc.chunk_hash(c), prefix=cc.PrefixContext((), ()), a_bar=0.0, b_bar=1.0, cci=0.5,
+                     token_scores=np.zeros(c.size), cache=k)
+    plan = cc.build_plan(chunks, q, store, alpha=1.0)
+    assert [cp.status for cp in plan.chunks] == [HIT] * 3
+    pool = tiers.TieredPool(model)
+    pool.to_host(plan.chunks[1].cache)
+    model.h2d_bytes_per_s = 50e9  # a real host link: loading is cheaper than recomputing
+    kept = tiers.demote_slow_hits(plan, model)
+    assert [cp.status for cp in kept.chunks] == [HIT] * 3
+    model.h2d_bytes_per_s = 1e3  # a pathological link: recompute instead
+    out = tiers.demote_slow_hits(plan, model)
+    assert [cp.status for cp in out.chunks] == [HIT, MISS, HIT]
+    assert out.chunks[1].cache is None and out.chunks[1].n_slots == chunks[1].size
+    res = cc.prefill(model, cc.plan_to_request(out), first_token=True)
+    assert res.active_per_layer[0] == chunks[1].size + q.size + sum(
+        cp.recompute.size for cp in out.chunks if cp.status == HIT and cp.recompute is not None)
