@@ -91,6 +91,27 @@ class ModelConfig:
             raise ConfigError("swiglu d_ff must be a multiple of 64 (gate|up column groups)")
         if self.dtype not in _DTYPES:
             raise ConfigError(f"dtype must be one of {sorted(_DTYPES)}")
+        if self.dtype == "bf16":
+            why = self.tensor_core_shape_error()
+            if why:
+                raise ConfigError(f"bf16 mode runs the tcgen05 kernels only (no fallback): {why}; "
+                                  "use dtype='fp32' or 'fp64' for this shape")
+
+    def tensor_core_shape_error(self) -> str | None:
+        """Why the bf16 tcgen05 GEMM / attention kernels cannot run this
+        shape (None if they can): d_head 64 or 128, a GQA group dividing
+        128, d_model / q width / ff multiples of 128 and a QKV width
+        multiple of 128 (the 128-row tiles and 64-deep k-blocks)."""
+        dh, g = self.head_dim(), self.n_heads // self.kv_heads()
+        if dh not in (64, 128):
+            return f"d_head {dh} not in (64, 128)"
+        if 128 % g:
+            return f"GQA group {g} does not divide 128"
+        for name, v in (("d_model", self.d_model), ("q width", self.q_width()), ("d_ff", self.ff_dim()),
+                        ("QKV width", self.q_width() + 2 * self.kv_width())):
+            if v % 128:
+                return f"{name} {v} is not a multiple of 128"
+        return None
 
     # Llama-3 shaped presets (random init; the reference has no such config)
     @classmethod

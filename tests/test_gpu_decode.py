@@ -43,7 +43,9 @@ def _toy_fixup(cc, g, dtype):
     return model, req, cc.prefill(model, req)
 
 
-@pytest.mark.parametrize("dtype,tol", [("fp64", 1e-9), ("fp32", 1e-3), ("bf16", 5e-2)])
+# (bf16 needs tensor-core shapes: the toy model is fp64/fp32 only; the bf16
+# decode path is checked on the GQA / d_head 128 model below)
+@pytest.mark.parametrize("dtype,tol", [("fp64", 1e-9), ("fp32", 1e-3)])
 def test_decode_continues_padded_fixup_like_reference(cc, dtype, tol):
     g = np.load(golden_path("decode_toy.npz"))
     model, req, res = _toy_fixup(cc, g, dtype)

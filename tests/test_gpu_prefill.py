@@ -77,7 +77,18 @@ def test_toy_fix_up_matches_reference_fp64(cc):
     np.testing.assert_allclose(model.logits(res.hidden[req.question_span[1] - 1])[0], g["logits_last"], atol=1e-9)
 
 
-@pytest.mark.parametrize("dtype,tol", [("fp32", 1e-3), ("bf16", BF16_TOY_TOL)])
+def test_bf16_mode_rejects_shapes_without_tensor_core_kernels(cc):
+    """The reference's toy model (d 64, d_head 16) has no tcgen05 tiling:
+    bf16 mode refuses it up front instead of silently running a slower
+    kernel; the parity modes run it."""
+    with pytest.raises(cc.ConfigError, match="tcgen05"):
+        cc.build_model(cc.ModelConfig(dtype="bf16"))
+    assert cc.ModelConfig(dtype="fp32").tensor_core_shape_error() == "d_head 16 not in (64, 128)"
+    assert cc.ModelConfig.llama3_8b(n_layers=1).tensor_core_shape_error() is None
+    assert cc.ModelConfig.llama3_70b(n_layers=1).tensor_core_shape_error() is None
+
+
+@pytest.mark.parametrize("dtype,tol", [("fp32", 1e-3)])
 def test_toy_fix_up_low_precision(cc, dtype, tol):
     g, model, req, res = toy_result(cc, dtype)
     e = {"hidden": rel(res.hidden, g["hidden"]),

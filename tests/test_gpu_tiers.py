@@ -126,7 +126,7 @@ def test_demote_slow_hits_uses_the_measured_load_rate(cc):
     assert [cp.status for cp in plan.chunks] == [HIT] * 3
     pool = tiers.TieredPool(model)
     pool.to_host(plan.chunks[1].cache)
-    model.h2d_bytes_per_s = 50e9  # a real host link: loading is cheaper than recomputing
+    model.h2d_bytes_per_s = 1e13  # a link fast enough that loading beats recomputing
     kept = tiers.demote_slow_hits(plan, model)
     assert [cp.status for cp in kept.chunks] == [HIT] * 3
     model.h2d_bytes_per_s = 1e3  # a pathological link: recompute instead

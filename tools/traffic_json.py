@@ -3,7 +3,7 @@ bench's roofline kernels from an ncu launch list of one config-2 step:
 
   ncu --nvtx --nvtx-include "step/" --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum \\
       --clock-control none --csv --log-file gpurun_out/launches.csv python tools/profile_step.py
-  python tools/traffic_json.py gpurun_out/launches.csv > profiles/traffic.json
+  python tools/traffic_json.py gpurun_out/launches.csv > profiles/traffic_<config>.json
 """
 import collections
 import csv
