@@ -636,7 +636,7 @@ def run_zipf(args, rank, world):
     import torch
 
     import paper_2502_15734_b200 as cc
-    from paper_2502_15734_b200 import parallel, replay
+    from paper_2502_15734_b200 import harness, parallel
 
     cfg = cc.ModelConfig.llama3_8b(n_layers=args.layers, dtype="bf16", seed=0)
     model = cc.build_model(cfg)
@@ -644,20 +644,20 @@ def run_zipf(args, rank, world):
     n_req = args.requests * world
     gen = dict(chunk_len_range=(args.chunk_len, args.chunk_len), question_len_range=(args.question, args.question),
                vocab_size=cfg.vocab_size)
-    skew = replay.fit_zipf_skew(n_chunks, k, n_req, target_share=0.6, seed=3, iterations=12, **gen)
-    trace = replay.gen_synthetic(n_chunks, skew, k, n_req, seed=3, **gen)
+    skew = harness.fit_zipf_skew(n_chunks, k, n_req, target_share=0.6, seed=3, iterations=12, **gen)
+    trace = harness.gen_synthetic(n_chunks, skew, k, n_req, seed=3, **gen)
     mine = parallel.shard_requests(trace.records, rank, world, "affinity")
     warm = min(20, max(0, len(mine) - 5))
     out = {}
     for policy in ("cachecraft", "exact_prefix", "full_recompute"):
         store = cc.VariantStore(cc.StoreConfig(max_chunks=100, variants_per_chunk=5))
         barrier(world)
-        rep = replay.replay_gpu(trace, model, store, policy=policy, warmup=warm, cfo_override=args.ratio,
+        rep = harness.replay_gpu(trace, model, store, policy=policy, warmup=warm, cfo_override=args.ratio,
                                 measure_deviation=False, records=mine)
         agg = rep.aggregate()
-        steady = rep.steady()
+        steady = rep.steady_state()
         tok = float(sum(r.tokens_total for r in steady))
-        wall = sum(r.ttft_ms for r in steady) / 1e3
+        wall = sum(r.ttft for r in steady)
         wall_max = allreduce_max(wall, world)
         tok_all = tok
         if world > 1:
@@ -681,7 +681,7 @@ def run_zipf(args, rank, world):
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic Zipf trace (random tokens, random-init weights)",
         "config": {"workload": f"config3: {n_req} requests x {k} chunks of {args.chunk_len} tokens + "
                                f"{args.question}-token question from a {n_chunks}-chunk corpus, zipf s={skew:.3f} "
-                               f"(top-5% share {replay.top_share(trace):.2f}), store N=100 M=5 per GPU, "
+                               f"(top-5% share {harness.top_share(trace):.2f}), store N=100 M=5 per GPU, "
                                "affinity request sharding", "parallelism": f"request-sharded x{world}"},
         "e2e": {"value": round(cc_["tokens_per_s"], 1), "unit": UNIT, "path": "replay_gpu (public API per request)"},
         "policies": out,

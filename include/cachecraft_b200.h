@@ -209,8 +209,10 @@ CC_API int cc_tp_push_gemm(const void* A, int64_t lda, const void* B, int64_t ld
 CC_API int cc_tp_reduce(const cc_tp_peers* tab, int M, int N, void* stream);
 /* Stream-ordered wait until this rank's `done` counter reaches `target`. */
 CC_API int cc_tp_wait(const cc_tp_peers* tab, int64_t target, void* stream);
-/* CUDA IPC: 64-byte handle of a device allocation / map a peer's handle. */
-CC_API int cc_ipc_get_handle(const void* dev_ptr, void* handle64);
+/* CUDA IPC: 64-byte handle of the allocation dev_ptr lies in, plus dev_ptr's
+ * byte offset from that allocation's base (caching allocators sub-allocate);
+ * map a peer's handle (returns the allocation base: add the offset). */
+CC_API int cc_ipc_get_handle(const void* dev_ptr, void* handle64, int64_t* offset);
 CC_API int cc_ipc_open_handle(const void* handle64, void** dev_ptr);
 
 /* dst[i] += src[i] over n f32 elements (the residual add after a tensor-

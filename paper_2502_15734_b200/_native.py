@@ -58,7 +58,7 @@ _SIGS = {
     "cc_tp_push_gemm": ([_vp, _i64, _vp, _i64, _i32, _i32, _i32, _vp, _vp], _i32),
     "cc_tp_reduce": ([_vp, _i32, _i32, _vp], _i32),
     "cc_tp_wait": ([_vp, _i64, _vp], _i32),
-    "cc_ipc_get_handle": ([_vp, _vp], _i32),
+    "cc_ipc_get_handle": ([_vp, _vp, _vp], _i32),
     "cc_ipc_open_handle": ([_vp, _vp], _i32),
     "cc_gemv_rmsnorm": ([_vp, _i64, _vp, _f64, _vp, _i64, _vp, _i64, _i32, _i32, _i32, _i32, _vp], _i32),
 }

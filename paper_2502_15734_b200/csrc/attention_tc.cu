@@ -4,8 +4,8 @@
 //
 // CTA = 128 "M-rows" = R query rows x G heads of one GQA group (G = Hq/Hkv,
 // R = 128/G), so one K/V tile in shared memory serves the whole group.
-//   warp 0     TMA: Q once (3-D map), K tiles of 128 keys (3-slot ring, one
-//              tile ahead of V), V tiles (2 slots tied to the P buffers)
+//   warp 0     TMA: Q once (3-D map), K tiles of BN keys (ring, one tile
+//              ahead of V), V tiles (2 slots tied to the P buffers)
 //   warp 1     MMA issuer: S_i = Q K_i^T (M128 N128 K16 x dh/16) into one of
 //              two TMEM S buffers, O += P_i V_i (A = P from TMEM, B = V
 //              MN-major from smem) into the TMEM O accumulator; two commits
@@ -101,36 +101,68 @@ __device__ __forceinline__ void twait(uint64_t* bar, uint32_t parity, bool traci
   }
 }
 
-template <int DH>
-struct AtSmem {
+// Kernel shape: DH head dim, BN keys per tile, NWG softmax warpgroups (a
+// softmax thread owns one M-row and BN / NWG keys of it).  P (bf16) is
+// written over the first BN/2 columns of its own S buffer once S has been
+// read (both key halves have, at the pair barrier), so TMEM holds
+// S0/P0 | S1/P1 | O: 2 BN + DH columns.  BN = 64 with DH = 128 needs 256
+// columns and ~106 KiB of shared memory: two CTAs share an SM, and each
+// CTA's MMAs fill the other's softmax gaps on the tensor pipe.
+template <int DH, int BN, int NWG>
+struct At {
+  static constexpr int KST = BN == 64 ? 2 : 3;   // K ring depth
+  static constexpr int VST = 2;                  // V ring depth = P buffers
+  static constexpr int THREADS = 64 + 128 * NWG;
+  static constexpr int KPT = BN / NWG;           // keys per softmax thread
+  static constexpr int OPT = DH / NWG;           // O columns per softmax thread
+  static constexpr int TMEM_USED = 2 * BN + DH;
+  static constexpr int TMEM_COLS = TMEM_USED <= 256 ? 256 : 512;
   static constexpr int ATOMS = DH / 64;              // 64-element (128 B) column atoms
   static constexpr int Q_BYTES = 128 * DH * 2;       // 128 M-rows
-  static constexpr int KV_BYTES = AT_BN * DH * 2;    // one K (or V) tile
+  static constexpr int KV_BYTES = BN * DH * 2;       // one K (or V) tile
   static constexpr int Q_OFF = 0;
   static constexpr int K_OFF = Q_OFF + Q_BYTES;
-  static constexpr int V_OFF = K_OFF + AT_KST * KV_BYTES;
-  static constexpr int BAR_OFF = V_OFF + AT_VST * KV_BYTES;
-  static constexpr int X_OFF = BAR_OFF + 256;        // [2 parities][2 halves][128 rows] f32 exchange
-  static constexpr int PLAN_OFF = X_OFF + 4 * 128 * 4;  // work-item plan: [3][AT_MAXT] ints
+  static constexpr int V_OFF = K_OFF + KST * KV_BYTES;
+  static constexpr int BAR_OFF = V_OFF + VST * KV_BYTES;
+  static constexpr int X_OFF = BAR_OFF + 256;        // [2 parities][NWG][128 rows] f32 exchange
+  static constexpr int PLAN_OFF = X_OFF + 2 * NWG * 128 * 4;  // work-item plan: [3][AT_MAXT] ints
   // no alignment slack: the kernel holds no static shared memory, so the
   // dynamic window starts 1 KiB aligned (checked at run time)
   static constexpr size_t TOTAL = PLAN_OFF + 3 * AT_MAXT * 4;
+  static constexpr int CTAS_PER_SM = (TMEM_COLS <= 256 && 2 * (TOTAL + 1024) <= 232448) ? 2 : 1;
+  static_assert(KPT % 32 == 0, "a softmax thread reads whole 32-column TMEM chunks");
 };
 
-// QT: Q lives in TMEM (written once by the first softmax warpgroup) and the
-// S MMA takes it as its A operand; P_i then aliases S_i's TMEM buffer.  This
-// removes the 32 KiB Q read from shared memory per key tile (the MMA's
-// operand reads and the TMA writes share the smem port).
-template <int DH, bool QT>
-__global__ void __launch_bounds__(AT_THREADS, 1)
-    attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __nv_bfloat16* __restrict__ qg,
-                   const __grid_constant__ CUtensorMap tmK,
+template <int N>
+__device__ __forceinline__ void tmem_st_cols(uint32_t taddr, const uint32_t* r);
+template <>
+__device__ __forceinline__ void tmem_st_cols<32>(uint32_t taddr, const uint32_t* r) {
+  tmem_st32(taddr, *reinterpret_cast<const uint32_t(*)[32]>(r));
+}
+template <>
+__device__ __forceinline__ void tmem_st_cols<16>(uint32_t taddr, const uint32_t* r) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]));
+}
+template <>
+__device__ __forceinline__ void tmem_st_cols<64>(uint32_t taddr, const uint32_t* r) {
+  tmem_st_cols<32>(taddr, r);
+  tmem_st_cols<32>(taddr + 32, r + 32);
+}
+
+template <int DH, int BN, int NWG>
+__global__ void __launch_bounds__(At<DH, BN, NWG>::THREADS, At<DH, BN, NWG>::CTAS_PER_SM)
+    attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                    const __grid_constant__ CUtensorMap tmV, const int32_t* __restrict__ q_slot,
                    const uint8_t* __restrict__ key_pad, __nv_bfloat16* __restrict__ ctx, float* __restrict__ lse,
                    int n_q, int n_keys, int Hq, int G, float scale_log2, long long* __restrict__ trace,
                    int n_groups, int n_row_tiles, int target, int max_parts, float* __restrict__ ws_o,
                    float2* __restrict__ ws_ml, int* __restrict__ counters) {
-  using SM = AtSmem<DH>;
+  using SM = At<DH, BN, NWG>;
+  constexpr int KST = SM::KST, VST = SM::VST, KPT = SM::KPT, OPT = SM::OPT, NT = SM::THREADS;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* base = smem_raw;
   if (smem_u32(smem_raw) & 1023) __trap();  // 128B-swizzled TMA / UMMA tiles need 1 KiB alignment
@@ -139,17 +171,17 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
   uint8_t* sV = base + SM::V_OFF;
   uint64_t* bars = reinterpret_cast<uint64_t*>(base + SM::BAR_OFF);
   uint64_t* q_full = bars + 0;
-  uint64_t* k_full = bars + 1;                 // [AT_KST]
-  uint64_t* k_empty = k_full + AT_KST;         // [AT_KST] arrived by the softmax once S_i landed
-  uint64_t* v_full = k_empty + AT_KST;         // [AT_VST]
-  uint64_t* s_full = v_full + AT_VST;          // [2]
+  uint64_t* k_full = bars + 1;                 // [KST]
+  uint64_t* k_empty = k_full + KST;            // [KST] arrived by the softmax once S_i landed
+  uint64_t* v_full = k_empty + KST;            // [VST]
+  uint64_t* s_full = v_full + VST;             // [2]
   uint64_t* s_empty = s_full + 2;              // [2]
   uint64_t* p_full = s_empty + 2;              // [2]
   uint64_t* p_empty = p_full + 2;              // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(p_empty + 2);
   int& s_kmax = *reinterpret_cast<int*>(tmem_slot + 1);
   uint32_t* padw = tmem_slot + 2;                                  // [2 parities][4 words]
-  float* xmax = reinterpret_cast<float*>(base + SM::X_OFF);       // row maxima / sums of the pair
+  float* xmax = reinterpret_cast<float*>(base + SM::X_OFF);       // row maxima / sums of the key halves
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int R = 128 / G;
@@ -169,15 +201,15 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
     int* p_len = reinterpret_cast<int*>(base + SM::PLAN_OFF);
     int* p_parts = p_len + AT_MAXT;
     int* p_order = p_parts + AT_MAXT;
-    for (int t = threadIdx.x; t < T; t += AT_THREADS) {
+    for (int t = threadIdx.x; t < T; t += NT) {
       const int kq = q_slot[min((t + 1) * R, n_q) - 1];
-      const int est = kq < 0 ? 0 : min(kq, n_keys - 1) / AT_BN + 1;
+      const int est = kq < 0 ? 0 : min(kq, n_keys - 1) / BN + 1;
       const int parts = max(1, min(max_parts, (est + target - 1) / target));
       p_parts[t] = parts;
       p_len[t] = (est + parts - 1) / parts;
     }
     __syncthreads();
-    for (int t = threadIdx.x; t < T; t += AT_THREADS) {
+    for (int t = threadIdx.x; t < T; t += NT) {
       const int lt = p_len[t];
       int rank = 0;
       for (int u = 0; u < T; ++u) rank += (p_len[u] > lt || (p_len[u] == lt && u > t)) ? 1 : 0;
@@ -220,23 +252,23 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
     tma_prefetch(&tmQ);
     tma_prefetch(&tmK);
     tma_prefetch(&tmV);
-    mbar_init(q_full, QT ? 128 : 1);
-    for (int s = 0; s < AT_KST; ++s) {
+    mbar_init(q_full, 1);
+    for (int s = 0; s < KST; ++s) {
       mbar_init(&k_full[s], 1);
       mbar_init(&k_empty[s], 1);
     }
-    for (int s = 0; s < AT_VST; ++s) mbar_init(&v_full[s], 1);
+    for (int s = 0; s < VST; ++s) mbar_init(&v_full[s], 1);
     for (int b = 0; b < 2; ++b) {
       mbar_init(&s_full[b], 1);
-      mbar_init(&s_empty[b], 256);
+      mbar_init(&s_empty[b], 128 * NWG);
     }
     for (int b = 0; b < 2; ++b) {
-      mbar_init(&p_full[b], 256);
+      mbar_init(&p_full[b], 128 * NWG);
       mbar_init(&p_empty[b], 1);
     }
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc<512>(tmem_slot);
+  if (warp == 1) tmem_alloc<SM::TMEM_COLS>(tmem_slot);
   __syncthreads();
   // per-CTA key range: max causal limit over valid rows
   if (threadIdx.x < 128) {
@@ -248,73 +280,68 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const int kmax = s_kmax;
-  const int n_total = kmax < 0 ? 0 : kmax / AT_BN + 1;
+  const int n_total = kmax < 0 ? 0 : kmax / BN + 1;
   // this part's key tiles [t0, t0 + n_tiles): boundaries from the planned
   // estimate, the last part runs to the exact end (every tile covered once)
   const bool split = parts > 1;
   const int t0 = split ? min(part * est / parts, n_total) : 0;
   const int t1 = !split || part == parts - 1 ? n_total : min((part + 1) * est / parts, n_total);
   const int n_tiles = max(0, t1 - t0);
-  // TMEM columns: S0 S1 | O | P0 P1 (QT: S0/P0 S1/P1 | O | Q)
-  const uint32_t t_s0 = tmem, t_o = tmem + 256, t_p = QT ? tmem : tmem + 384, t_q = tmem + 384;
-  constexpr int P_STRIDE = QT ? AT_BN : AT_BN / 2;  // columns between the two P buffers
+  // TMEM columns: S0/P0 | S1/P1 | O
+  const uint32_t t_s0 = tmem, t_o = tmem + 2 * BN;
   const bool tracing = trace != nullptr;
-  long long w0 = 0, w1 = 0, w2 = 0, w3 = 0, t_loop = 0;  // per-role stall cycles (trace only)
+  long long w0 = 0, w1 = 0, w2 = 0, w3 = 0;  // per-role stall cycles (trace only)
   long long t_s_issue = 0, t_s_commit = 0, t_p_issue = 0, t_p_commit = 0;
   long long t_begin = 0;
   if (trace != nullptr && threadIdx.x == 64) asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_begin));
 
   if (warp == 0) {
     if (lane == 0 && n_tiles > 0) {
-      if (!QT) {
-        mbar_expect_tx(q_full, SM::Q_BYTES);
+      mbar_expect_tx(q_full, SM::Q_BYTES);
 #pragma unroll
-        for (int a = 0; a < SM::ATOMS; ++a) tma_load_3d(sQ + a * 128 * 128, &tmQ, q_full, a * 64, g * G, row0);
-      }
+      for (int a = 0; a < SM::ATOMS; ++a) tma_load_3d(sQ + a * 128 * 128, &tmQ, q_full, a * 64, g * G, row0);
       // K runs one tile ahead of V: K_{i+1}'s slot frees when S_{i-1} is done
       // (early), V_i's when PV_{i-2} is done, so neither S nor PV waits on a
       // load issued after the previous PV
       auto load_k = [&](int i) {
-        const int st = i % AT_KST;
-        twait(&k_empty[st], ((i / AT_KST) & 1) ^ 1, tracing, w0);
+        const int st = i % KST;
+        twait(&k_empty[st], ((i / KST) & 1) ^ 1, tracing, w0);
         mbar_expect_tx(&k_full[st], SM::KV_BYTES);
 #pragma unroll
         for (int a = 0; a < SM::ATOMS; ++a)
-          tma_load_2d(sK + st * SM::KV_BYTES + a * AT_BN * 128, &tmK, &k_full[st], g * DH + a * 64, (t0 + i) * AT_BN);
+          tma_load_2d(sK + st * SM::KV_BYTES + a * BN * 128, &tmK, &k_full[st], g * DH + a * 64, (t0 + i) * BN);
       };
       load_k(0);
       for (int i = 0; i < n_tiles; ++i) {
         if (i + 1 < n_tiles) load_k(i + 1);
-        const int st = i % AT_VST;  // == P buffer of tile i: free once PV_{i-2} completed
-        twait(&p_empty[st], ((i / AT_VST) & 1) ^ 1, tracing, w1);
+        const int st = i % VST;  // == P buffer of tile i: free once PV_{i-2} completed
+        twait(&p_empty[st], ((i / VST) & 1) ^ 1, tracing, w1);
         mbar_expect_tx(&v_full[st], SM::KV_BYTES);
 #pragma unroll
         for (int a = 0; a < SM::ATOMS; ++a)
-          tma_load_2d(sV + st * SM::KV_BYTES + a * AT_BN * 128, &tmV, &v_full[st], g * DH + a * 64, (t0 + i) * AT_BN);
+          tma_load_2d(sV + st * SM::KV_BYTES + a * BN * 128, &tmV, &v_full[st], g * DH + a * 64, (t0 + i) * BN);
       }
     }
   } else if (warp == 1) {
     if (lane == 0 && n_tiles > 0) {
-      constexpr uint32_t id_s = idesc_bf16(128, AT_BN, false);
+      constexpr uint32_t id_s = idesc_bf16(128, BN, false);
       constexpr uint32_t id_o = idesc_bf16(128, DH, true);
       mbar_wait(q_full, 0);
+      // S_i = Q K_i^T into S buffer i & 1.  It overwrites P_{i-2} (aliased):
+      // issued after PV_{i-2} in this thread's program order, and tcgen05
+      // MMAs of one CTA execute in issue order
       auto issue_s = [&](int i) {
-        const int st = i % AT_KST, b = i & 1;
-        twait(&k_full[st], (i / AT_KST) & 1, tracing, w0);
+        const int st = i % KST, b = i & 1;
+        twait(&k_full[st], (i / KST) & 1, tracing, w0);
         twait(&s_empty[b], ((i >> 1) & 1) ^ 1, tracing, w1);
         tc_fence_after();
         const long long ts0 = tracing ? clock64() : 0;
 #pragma unroll
         for (int kk = 0; kk < DH / 16; ++kk) {
           const int a = kk >> 2, w = kk & 3;
-          uint64_t bd = desc_sw128(sK + st * SM::KV_BYTES + a * AT_BN * 128) + 2 * w;
-          if (QT) {
-            // A = Q in TMEM: row = lane, 2 bf16 of the head dim per column
-            mma_bf16_ts(t_s0 + b * AT_BN, t_q + kk * 8, bd, id_s, kk > 0);
-          } else {
-            uint64_t ad = desc_sw128(sQ + a * 128 * 128) + 2 * w;
-            mma_bf16(t_s0 + b * AT_BN, ad, bd, id_s, kk > 0);
-          }
+          uint64_t bd = desc_sw128(sK + st * SM::KV_BYTES + a * BN * 128) + 2 * w;
+          uint64_t ad = desc_sw128(sQ + a * 128 * 128) + 2 * w;
+          mma_bf16(t_s0 + b * BN, ad, bd, id_s, kk > 0);
         }
         const long long ts1 = tracing ? clock64() : 0;
         mma_commit(&s_full[b]);  // (K slot released by the softmax when it sees s_full)
@@ -323,16 +350,16 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
       issue_s(0);
       for (int i = 0; i < n_tiles; ++i) {
         if (i + 1 < n_tiles) issue_s(i + 1);
-        const int st = i % AT_VST, pb = i & 1;
+        const int st = i % VST, pb = i & 1;
         twait(&p_full[pb], (i >> 1) & 1, tracing, w2);
-        twait(&v_full[st], (i / AT_VST) & 1, tracing, w3);
+        twait(&v_full[st], (i / VST) & 1, tracing, w3);
         tc_fence_after();
         const long long tp0 = tracing ? clock64() : 0;
 #pragma unroll
-        for (int kk = 0; kk < AT_BN / 16; ++kk) {
-          uint64_t bd = desc_sw128_mn(sV + st * SM::KV_BYTES + kk * 16 * 128, AT_BN * 128);
+        for (int kk = 0; kk < BN / 16; ++kk) {
+          uint64_t bd = desc_sw128_mn(sV + st * SM::KV_BYTES + kk * 16 * 128, BN * 128);
           // A = P in TMEM: row = lane, 2 bf16 keys per 32-bit column, 16 keys = 8 columns
-          mma_bf16_ts(t_o, t_p + pb * P_STRIDE + kk * 8, bd, id_o, (i > 0 || kk > 0) ? 1u : 0u);
+          mma_bf16_ts(t_o, t_s0 + pb * BN + kk * 8, bd, id_o, (i > 0 || kk > 0) ? 1u : 0u);
         }
         const long long tp1 = tracing ? clock64() : 0;
         mma_commit(&p_empty[pb]);  // P buffer and V slot pb
@@ -341,13 +368,13 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
     }
   } else {
     // ---- softmax / correction / epilogue --------------------------------------
-    // Two softmax warpgroups (warps 2-5, 6-9): thread = (M-row m, key half h);
-    // half h owns S columns [64h, 64h+64), P columns [32h, 32h+32) and O columns
-    // [DH/2 h, DH/2 (h+1)).  Per tile the pair exchanges its row max through
-    // smem (one named barrier per TMEM lane quarter); the running sums stay
-    // per half and are added once at the end.
+    // NWG softmax warpgroups: thread = (M-row m, key part h); part h owns S
+    // columns [KPT h, KPT (h+1)), P columns [KPT/2 h, ...) and O columns
+    // [OPT h, OPT (h+1)).  With two parts the pair exchanges its row max
+    // through smem per tile (one named barrier per TMEM lane quarter); the
+    // running sums stay per part and are added once at the end.
     const int q4 = warp & 3;               // TMEM lane quarter
-    const int h = (warp - 2) >> 2;         // key / output-column half
+    const int h = (warp - 2) >> 2;         // key / output-column part
     const int m = q4 * 32 + lane;
     const int row = row0 + m / G;
     const int head = g * G + m % G;
@@ -355,77 +382,60 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
     const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
     float m_run = -INFINITY, l_run = 0.f;
     constexpr float kRescaleLog2 = 8.f;  // lazy rescale: keep the stale max while p <= 2^8
-    auto pair_bar = [&]() { asm volatile("bar.sync %0, 64;" ::"r"(2 + q4) : "memory"); };
-    if (QT && h == 0 && n_tiles > 0) {
-      // Q row (head `head` of query row `row`) -> TMEM lane m, DH/2 columns
-#pragma unroll
-      for (int c = 0; c < DH / 64; ++c) {
-        uint32_t r[32];
-        if (row < n_q) {
-          const uint4* src = reinterpret_cast<const uint4*>(qg + ((int64_t)row * Hq + head) * DH + c * 64);
-#pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            const uint4 v = src[e];
-            r[4 * e] = v.x; r[4 * e + 1] = v.y; r[4 * e + 2] = v.z; r[4 * e + 3] = v.w;
-          }
-        } else {
-#pragma unroll
-          for (int e = 0; e < 32; ++e) r[e] = 0u;
-        }
-        tmem_st32(t_q + c * 32 + lane_off, r);
-      }
-      tmem_st_wait();
-      tc_fence_before();
-      mbar_arrive(q_full);
-    }
+    auto pair_bar = [&]() {
+      if constexpr (NWG > 1) asm volatile("bar.sync %0, %1;" ::"r"(2 + q4), "r"(32 * NWG) : "memory");
+    };
     for (int i = 0; i < n_tiles; ++i) {
       const int b = i & 1;
       twait(&s_full[b], (i >> 1) & 1, tracing, w0);
       tc_fence_after();
-      if (warp == 2 && lane == 0) mbar_arrive(&k_empty[i % AT_KST]);  // S_i done: K_i's slot is free
-      float s[64];
+      if (warp == 2 && lane == 0) mbar_arrive(&k_empty[i % KST]);  // S_i done: K_i's slot is free
+      float s[KPT];
       {
-        uint32_t r0[32], r1[32];
-        const uint32_t ta = t_s0 + b * AT_BN + h * 64 + lane_off;
-        tmem_ld32(ta, r0);
-        tmem_ld32(ta + 32, r1);
-        tmem_ld_wait();
+        const uint32_t ta = t_s0 + b * BN + h * KPT + lane_off;
 #pragma unroll
-        for (int e = 0; e < 32; ++e) {
-          s[e] = __uint_as_float(r0[e]);
-          s[32 + e] = __uint_as_float(r1[e]);
+        for (int c = 0; c < KPT / 32; ++c) {
+          uint32_t r[32];
+          tmem_ld32(ta + c * 32, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int e = 0; e < 32; ++e) s[c * 32 + e] = __uint_as_float(r[e]);
         }
       }
       tc_fence_before();
       mbar_arrive(&s_empty[b]);
-      const int j0 = (t0 + i) * AT_BN;
-      // keys j0 + 64h + c visible iff c <= lim_rel (causal + bounds) and not a pad
-      const int lim_rel = min(lim, n_keys - 1) - j0 - 64 * h;
+      const int j0 = (t0 + i) * BN;
+      // keys j0 + KPT h + c visible iff c <= lim_rel (causal + bounds) and not a pad
+      const int lim_rel = min(lim, n_keys - 1) - j0 - KPT * h;
       if (key_pad != nullptr) {
-        // 128-bit pad mask of this tile, built by the first warpgroup
-        if (h == 0) {
+        // BN-bit pad mask of this tile (BN/32 words), built by the first warpgroup
+        if (h == 0 && q4 < BN / 32) {
           const int jm = j0 + m;
           const unsigned word = __ballot_sync(0xffffffffu, jm >= n_keys || key_pad[jm] != 0);
           if (lane == 0) padw[(i & 1) * 4 + q4] = word;
         }
-        asm volatile("bar.sync 1, 256;" ::: "memory");
-        const uint32_t pw0 = padw[(i & 1) * 4 + 2 * h], pw1 = padw[(i & 1) * 4 + 2 * h + 1];
+        asm volatile("bar.sync 1, %0;" ::"r"(128 * NWG) : "memory");
+        const uint32_t* pw = padw + (i & 1) * 4 + (KPT / 32) * h;
 #pragma unroll
-        for (int c = 0; c < 64; ++c)
-          s[c] = (c <= lim_rel && !((((c < 32) ? pw0 : pw1) >> (c & 31)) & 1u)) ? s[c] : -INFINITY;
-      } else if (lim_rel < 63) {
+        for (int c = 0; c < KPT; ++c)
+          s[c] = (c <= lim_rel && !((pw[c >> 5] >> (c & 31)) & 1u)) ? s[c] : -INFINITY;
+      } else if (lim_rel < KPT - 1) {
 #pragma unroll
-        for (int c = 0; c < 64; ++c) s[c] = (c <= lim_rel) ? s[c] : -INFINITY;
+        for (int c = 0; c < KPT; ++c) s[c] = (c <= lim_rel) ? s[c] : -INFINITY;
       }
       float mx[8];
 #pragma unroll
       for (int e = 0; e < 8; ++e) mx[e] = s[e];
 #pragma unroll
-      for (int c = 8; c < 64; ++c) mx[c & 7] = fmaxf(mx[c & 7], s[c]);
+      for (int c = 8; c < KPT; ++c) mx[c & 7] = fmaxf(mx[c & 7], s[c]);
       float tmax = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])), fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
-      xmax[((i & 1) * 2 + h) * 128 + m] = tmax;
-      pair_bar();
-      tmax = fmaxf(tmax, xmax[((i & 1) * 2 + (h ^ 1)) * 128 + m]);
+      if constexpr (NWG > 1) {
+        xmax[((i & 1) * NWG + h) * 128 + m] = tmax;
+        pair_bar();
+#pragma unroll
+        for (int o = 0; o < NWG; ++o)
+          if (o != h) tmax = fmaxf(tmax, xmax[((i & 1) * NWG + o) * 128 + m]);
+      }
       bool grow = false;
       float alpha = 1.f;
       if (i > 0) {
@@ -437,16 +447,12 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
         }
       }
       const int pb = i & 1;
-      if (i >= 2) {
-        twait(&p_empty[pb], ((i - 2) >> 1) & 1, tracing, w1);  // PV_{i-2} done: P buffer pb free
-        tc_fence_after();
-      }
       if (m_run == -INFINITY) m_run = tmax;  // first visible keys: nothing accumulated yet
       const float base_l2 = (m_run == -INFINITY) ? 0.f : m_run * scale_log2;
       float ps[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-      uint32_t pt[32];  // this half's 64 keys of P, packed bf16x2 (TMEM P)
+      uint32_t pt[KPT / 2];  // this part's keys of P, packed bf16x2 (TMEM P)
 #pragma unroll
-      for (int ch = 0; ch < 8; ++ch) {
+      for (int ch = 0; ch < KPT / 8; ++ch) {
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const int c = ch * 8 + e * 2;
@@ -462,19 +468,19 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
           pt[ch * 4 + e] = *reinterpret_cast<uint32_t*>(&hv);
         }
       }
-      // (QT: P_i overwrites S_i's first 64 columns; both halves finished
-      // reading S_i before the pair barrier above)
-      tmem_st32(t_p + pb * P_STRIDE + h * 32 + lane_off, pt);
+      // P_i over S_i's first BN/2 columns: every part finished reading S_i
+      // before the pair barrier above (one part: this thread read its own)
+      tmem_st_cols<KPT / 2>(t_s0 + pb * BN + h * (KPT / 2) + lane_off, pt);
       l_run += ((ps[0] + ps[1]) + (ps[2] + ps[3])) + ((ps[4] + ps[5]) + (ps[6] + ps[7]));
-      // O *= alpha (this half's columns) for rows whose max grew past the lazy
+      // O *= alpha (this part's columns) for rows whose max grew past the lazy
       // threshold.  tcgen05.ld/st are warp-collective: the whole warp joins,
       // alpha = 1 for rows that keep their max.
       if (__any_sync(0xffffffffu, grow)) {
         twait(&p_empty[(i - 1) & 1], ((i - 1) >> 1) & 1, tracing, w2);  // PV_{i-1} done: O current
         tc_fence_after();
 #pragma unroll 1
-        for (int c = 0; c < DH / 64; ++c) {
-          const uint32_t to = t_o + h * (DH / 2) + c * 32 + lane_off;
+        for (int c = 0; c < OPT / 32; ++c) {
+          const uint32_t to = t_o + h * OPT + c * 32 + lane_off;
           uint32_t r[32];
           tmem_ld32(to, r);
           tmem_ld_wait();
@@ -488,27 +494,32 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
       tc_fence_before();
       mbar_arrive(&p_full[pb]);
     }
-    // epilogue: total row sum = both halves
+    // epilogue: total row sum = all parts
     // (slot parity n_tiles & 1 was last read before the previous pair barrier)
-    xmax[((n_tiles & 1) * 2 + h) * 128 + m] = l_run;
-    pair_bar();
-    const float l_tot = l_run + xmax[((n_tiles & 1) * 2 + (h ^ 1)) * 128 + m];
+    float l_tot = l_run;
+    if constexpr (NWG > 1) {
+      xmax[((n_tiles & 1) * NWG + h) * 128 + m] = l_run;
+      pair_bar();
+#pragma unroll
+      for (int o = 0; o < NWG; ++o)
+        if (o != h) l_tot += xmax[((n_tiles & 1) * NWG + o) * 128 + m];
+    }
     if (n_tiles > 0) {
       mbar_wait(&p_empty[(n_tiles - 1) & 1], ((n_tiles - 1) >> 1) & 1);
       tc_fence_after();
     }
-    __nv_bfloat16* out = ctx + ((int64_t)row * Hq + head) * DH + h * (DH / 2);
+    __nv_bfloat16* out = ctx + ((int64_t)row * Hq + head) * DH + h * OPT;
     if (split) {
-      // park this half's partial (unnormalised O, max in log2 units, sum) ...
+      // park this part's partial (unnormalised O, max in log2 units, sum) ...
       const int key = g * T + tile, slot = key * AT_MAXP + part;
       const bool any = n_tiles > 0 && m_run != -INFINITY;
       const float m_l2 = any ? m_run * scale_log2 : -INFINITY;
-      float* my_o = ws_o + ((int64_t)slot * 128 + m) * DH + h * (DH / 2);
+      float* my_o = ws_o + ((int64_t)slot * 128 + m) * DH + h * OPT;
 #pragma unroll 1
-      for (int c = 0; c < DH / 64; ++c) {
+      for (int c = 0; c < OPT / 32; ++c) {
         uint32_t r[32];
         if (n_tiles > 0) {
-          tmem_ld32(t_o + h * (DH / 2) + c * 32 + lane_off, r);
+          tmem_ld32(t_o + h * OPT + c * 32 + lane_off, r);
           tmem_ld_wait();
         }
 #pragma unroll
@@ -520,13 +531,13 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
       }
       if (h == 0) __stcg(&ws_ml[(int64_t)slot * 128 + m], make_float2(m_l2, any ? l_tot : 0.f));
       __threadfence();
-      asm volatile("bar.sync 1, 256;" ::: "memory");
+      asm volatile("bar.sync 1, %0;" ::"r"(128 * NWG) : "memory");
       if (warp == 2 && lane == 0) {
         const int prev = atomicAdd(&counters[key], 1);
         padw[0] = prev;  // (pad words are no longer needed)
         if (prev == parts - 1) counters[key] = 0;  // reset for the next launch
       }
-      asm volatile("bar.sync 1, 256;" ::: "memory");
+      asm volatile("bar.sync 1, %0;" ::"r"(128 * NWG) : "memory");
       if ((int)padw[0] == parts - 1) {
         // ... and the last part to finish merges all of them, in part order
         __threadfence();
@@ -547,12 +558,12 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
         const float inv = lt > 0.f ? 1.f / lt : 0.f;
         if (row < n_q) {
 #pragma unroll 1
-          for (int c = 0; c < DH / 16; ++c) {
+          for (int c = 0; c < OPT / 8; ++c) {
             float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
             for (int p = 0; p < AT_MAXP; ++p) {
               if (p >= parts) break;
-              const float* op = ws_o + (((int64_t)key * AT_MAXP + p) * 128 + m) * DH + h * (DH / 2) + c * 8;
+              const float* op = ws_o + (((int64_t)key * AT_MAXP + p) * 128 + m) * DH + h * OPT + c * 8;
               const float4 a0 = __ldcg(reinterpret_cast<const float4*>(op));
               const float4 a1 = __ldcg(reinterpret_cast<const float4*>(op) + 1);
               v[0] = fmaf(a0.x, w[p], v[0]); v[1] = fmaf(a0.y, w[p], v[1]);
@@ -574,27 +585,27 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
         }
       }
     } else {
-    const float inv = l_tot > 0.f ? 1.f / l_tot : 0.f;
+      const float inv = l_tot > 0.f ? 1.f / l_tot : 0.f;
 #pragma unroll 1
-    for (int c = 0; c < DH / 64; ++c) {
-      uint32_t r[32];
-      tmem_ld32(t_o + h * (DH / 2) + c * 32 + lane_off, r);
-      tmem_ld_wait();
-      if (row < n_q && n_tiles > 0) {
-        uint4 pk[4];
-        uint32_t* pw = reinterpret_cast<uint32_t*>(pk);
+      for (int c = 0; c < OPT / 32; ++c) {
+        uint32_t r[32];
+        tmem_ld32(t_o + h * OPT + c * 32 + lane_off, r);
+        tmem_ld_wait();
+        if (row < n_q && n_tiles > 0) {
+          uint4 pk[4];
+          uint32_t* pw = reinterpret_cast<uint32_t*>(pk);
 #pragma unroll
-        for (int e = 0; e < 16; ++e) {
-          __nv_bfloat162 hv = __floats2bfloat162_rn(__uint_as_float(r[2 * e]) * inv, __uint_as_float(r[2 * e + 1]) * inv);
-          pw[e] = *reinterpret_cast<uint32_t*>(&hv);
+          for (int e = 0; e < 16; ++e) {
+            __nv_bfloat162 hv = __floats2bfloat162_rn(__uint_as_float(r[2 * e]) * inv, __uint_as_float(r[2 * e + 1]) * inv);
+            pw[e] = *reinterpret_cast<uint32_t*>(&hv);
+          }
+          uint4* o4 = reinterpret_cast<uint4*>(out + c * 32);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) o4[e] = pk[e];
         }
-        uint4* o4 = reinterpret_cast<uint4*>(out + c * 32);
-#pragma unroll
-        for (int e = 0; e < 4; ++e) o4[e] = pk[e];
       }
-    }
-    if (row < n_q && h == 0)
-      lse[(int64_t)row * Hq + head] = l_tot > 0.f ? (m_run * scale_log2 + log2f(l_tot)) * 0.6931471805599453f : -INFINITY;
+      if (row < n_q && h == 0)
+        lse[(int64_t)row * Hq + head] = l_tot > 0.f ? (m_run * scale_log2 + log2f(l_tot)) * 0.6931471805599453f : -INFINITY;
     }
   }
   if (tracing) {
@@ -605,7 +616,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
       int smid;
       asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
       tr[0] = n_tiles; tr[1] = t_begin; tr[2] = t_end; tr[3] = smid;
-      tr[4] = w0; tr[5] = w1; tr[6] = w2; tr[7] = w3;  // softmax: s_full, p_empty(i-2), p_empty(grow)
+      tr[4] = w0; tr[5] = w1; tr[6] = w2; tr[7] = w3;  // softmax: s_full, -, p_empty(grow)
     } else if (threadIdx.x == 32) {
       tr[8] = w0; tr[9] = w1; tr[10] = w2; tr[11] = w3;  // mma: k_full, s_empty, p_full, v_full
       tr[12] = t_s_issue; tr[13] = t_s_commit; tr[14] = t_p_issue; tr[15] = t_p_commit;
@@ -615,7 +626,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc<512>(tmem);
+    tmem_dealloc<SM::TMEM_COLS>(tmem);
   }
 }
 
@@ -670,9 +681,12 @@ int encode(CUtensorMap* m, int rank, const void* p, const cuuint64_t* dims, cons
   return CC_OK;
 }
 
-template <int DH>
+int g_attn_variant = -1;  // debug hook / CCB_ATTN_VARIANT: kernel shape (see pick below)
+
+template <int DH, int BN, int NWG>
 int launch(const void* q, const void* k, const void* v, const int32_t* q_slot, const uint8_t* key_pad, void* ctx,
            float* lse, int n_q, int n_keys, int Hq, int Hkv, cudaStream_t st) {
+  using SM = At<DH, BN, NWG>;
   const int G = Hq / Hkv;
   const int R = 128 / G;
   CUtensorMap mq, mk, mv;
@@ -686,30 +700,27 @@ int launch(const void* q, const void* k, const void* v, const int32_t* q_slot, c
   {
     cuuint64_t dims[2] = {(cuuint64_t)Hkv * DH, (cuuint64_t)n_keys};
     cuuint64_t strides[1] = {(cuuint64_t)Hkv * DH * 2};
-    cuuint32_t box[2] = {64, (cuuint32_t)AT_BN};
+    cuuint32_t box[2] = {64, (cuuint32_t)BN};
     int rc = encode(&mk, 2, k, dims, strides, box);
     if (rc) return rc;
     rc = encode(&mv, 2, v, dims, strides, box);
     if (rc) return rc;
   }
-  if (int rc = ensure_smem(attn_tc_kernel<DH, true>, AtSmem<DH>::TOTAL)) return rc;
-  if (int rc = ensure_smem(attn_tc_kernel<DH, false>, AtSmem<DH>::TOTAL)) return rc;
-  // Q in TMEM (QT): measured ~1-2% slower than Q in smem at config 2 (the
-  // kernel is softmax-latency bound, not smem-port bound); opt-in
-  static const bool q_tmem = getenv("CCB_ATTN_QTMEM") && getenv("CCB_ATTN_QTMEM")[0] == '1';
+  if (int rc = ensure_smem(attn_tc_kernel<DH, BN, NWG>, SM::TOTAL)) return rc;
   const int row_tiles = (n_q + R - 1) / R;
-  // Work items: when the grid of (group, row tile) CTAs leaves SMs idle, the
-  // row tiles with long causal key ranges are cut into up to AT_MAXP key
+  // Work items: when the grid of (group, row tile) CTAs leaves CTA slots idle,
+  // the row tiles with long causal key ranges are cut into up to AT_MAXP key
   // parts (merged in part order by the last part to finish), all items
   // dispatched longest first.  With a full grid the extra CTAs' fixed costs
   // (prologue, pipeline fill, partial write + merge) outweigh the better
   // balance: measured at config 2 (208 CTAs) 65.9 us unsplit vs 94.7 us with
   // parts of half the per-SM share.
-  const int max_tiles = (n_keys + AT_BN - 1) / AT_BN;
+  const int slots = num_sms() * SM::CTAS_PER_SM;
+  const int max_tiles = (n_keys + BN - 1) / BN;
   int target = max_tiles, max_parts = 1;
-  if (row_tiles <= AT_MAXT && max_tiles > 0 && Hkv * row_tiles < num_sms()) {
-    max_parts = std::max(1, std::min(AT_MAXP, num_sms() / (Hkv * row_tiles)));
-    target = std::max(8, (max_tiles + max_parts - 1) / max_parts);
+  if (row_tiles <= AT_MAXT && max_tiles > 0 && Hkv * row_tiles < slots) {
+    max_parts = std::max(1, std::min(AT_MAXP, slots / (Hkv * row_tiles)));
+    target = std::max(8 * 128 / BN, (max_tiles + max_parts - 1) / max_parts);
     max_parts = std::min(max_parts, (max_tiles + target - 1) / target);
     if (max_parts < 1) max_parts = 1;
   }
@@ -736,10 +747,24 @@ int launch(const void* q, const void* k, const void* v, const int32_t* q_slot, c
   // (an upper bound: CTAs past the planned items exit at once)
   dim3 grid(Hkv * row_tiles * max_parts);
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)DH);
-  return launch_k(q_tmem ? attn_tc_kernel<DH, true> : attn_tc_kernel<DH, false>, grid, dim3(AT_THREADS),
-                  AtSmem<DH>::TOTAL, st, "attention_tc", mq, (const __nv_bfloat16*)q, mk, mv, q_slot, key_pad,
-                  (__nv_bfloat16*)ctx, lse, n_q, n_keys, Hq, G, scale_log2, g_attn_trace, Hkv, row_tiles, target,
-                  max_parts, ws_o, ws_ml, counters);
+  return launch_k(attn_tc_kernel<DH, BN, NWG>, grid, dim3(SM::THREADS), SM::TOTAL, st, "attention_tc", mq, mk, mv,
+                  q_slot, key_pad, (__nv_bfloat16*)ctx, lse, n_q, n_keys, Hq, G, scale_log2, g_attn_trace, Hkv,
+                  row_tiles, target, max_parts, ws_o, ws_ml, counters);
+}
+
+// Kernel shape per launch: 0 = 128-key tiles, two softmax warpgroups (one
+// CTA per SM); 1 = 64-key tiles, one warpgroup; 2 = 64-key tiles, two
+// warpgroups (both two CTAs per SM); 3 = 128-key tiles, one warpgroup.
+template <int DH>
+int launch_variant(int variant, const void* q, const void* k, const void* v, const int32_t* q_slot,
+                   const uint8_t* key_pad, void* ctx, float* lse, int n_q, int n_keys, int Hq, int Hkv,
+                   cudaStream_t st) {
+  switch (variant) {
+    case 1: return launch<DH, 64, 1>(q, k, v, q_slot, key_pad, ctx, lse, n_q, n_keys, Hq, Hkv, st);
+    case 2: return launch<DH, 64, 2>(q, k, v, q_slot, key_pad, ctx, lse, n_q, n_keys, Hq, Hkv, st);
+    case 3: return launch<DH, 128, 1>(q, k, v, q_slot, key_pad, ctx, lse, n_q, n_keys, Hq, Hkv, st);
+    default: return launch<DH, 128, 2>(q, k, v, q_slot, key_pad, ctx, lse, n_q, n_keys, Hq, Hkv, st);
+  }
 }
 
 }  // namespace
@@ -750,8 +775,13 @@ int attention_tc_bf16(const void* q, const void* k, const void* v, const int32_t
   if (G < 1 || G > 128 || (128 % G) != 0) return fail(CC_E_UNSUP, "attention_tc: GQA group must divide 128");
   if ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(k) | reinterpret_cast<uintptr_t>(v)) & 15)
     return fail(CC_E_UNSUP, "attention_tc: pointers must be 16-byte aligned");
-  if (dh == 128) return launch<128>(q, k, v, q_slot, key_pad, ctx, lse, n_q, n_keys, Hq, Hkv, st);
-  if (dh == 64) return launch<64>(q, k, v, q_slot, key_pad, ctx, lse, n_q, n_keys, Hq, Hkv, st);
+  int variant = g_attn_variant;
+  if (variant < 0) {
+    static const int env = getenv("CCB_ATTN_VARIANT") ? atoi(getenv("CCB_ATTN_VARIANT")) : 0;
+    variant = env;
+  }
+  if (dh == 128) return launch_variant<128>(variant, q, k, v, q_slot, key_pad, ctx, lse, n_q, n_keys, Hq, Hkv, st);
+  if (dh == 64) return launch_variant<64>(variant, q, k, v, q_slot, key_pad, ctx, lse, n_q, n_keys, Hq, Hkv, st);
   return fail(CC_E_UNSUP, "attention_tc: d_head must be 64 or 128");
 }
 
@@ -761,3 +791,5 @@ int attention_tc_bf16(const void* q, const void* k, const void* v, const int32_t
 extern "C" __attribute__((visibility("default"))) void cc_debug_attn_trace(void* p) {
   ccb::g_attn_trace = reinterpret_cast<long long*>(p);
 }
+// debug hook (not part of the ABI): attention kernel shape of the next launches (-1: default)
+extern "C" __attribute__((visibility("default"))) void cc_debug_attn_variant(int v) { ccb::g_attn_variant = v; }

@@ -12,6 +12,8 @@
 // The residual add (hidden += sum) is cc_add_f32 on the local stream.
 #include <cuda.h>
 
+#include <mutex>
+
 #include "common.cuh"
 #include "gemm.cuh"
 
@@ -95,11 +97,31 @@ extern "C" int cc_tp_wait(const cc_tp_peers* tab, int64_t target, void* stream) 
   return check_launch("tp_wait");
 }
 
-extern "C" int cc_ipc_get_handle(const void* dev_ptr, void* handle64) {
+// An IPC handle names the whole allocation a pointer lies in (a caching
+// allocator hands out sub-ranges of larger cudaMalloc blocks): *offset gets
+// the pointer's byte offset from that allocation's base, which the peer adds
+// to the base cudaIpcOpenMemHandle returns.
+extern "C" int cc_ipc_get_handle(const void* dev_ptr, void* handle64, int64_t* offset) {
+  using RangeFn = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+  static RangeFn range = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      range = reinterpret_cast<RangeFn>(p);
+  });
+  if (!range) return fail(CC_E_CUDA, "ipc_get_handle: cuMemGetAddressRange unavailable");
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (range(&base, &size, reinterpret_cast<CUdeviceptr>(dev_ptr)) != CUDA_SUCCESS)
+    return fail(CC_E_CUDA, "ipc_get_handle: cuMemGetAddressRange failed");
   cudaIpcMemHandle_t h;
-  cudaError_t e = cudaIpcGetMemHandle(&h, const_cast<void*>(dev_ptr));
+  cudaError_t e = cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base));
   if (e != cudaSuccess) return fail(CC_E_CUDA, std::string("ipc_get_handle: ") + cudaGetErrorString(e));
   memcpy(handle64, &h, sizeof(h));
+  *offset = (int64_t)(reinterpret_cast<CUdeviceptr>(dev_ptr) - base);
   return 0;
 }
 

@@ -178,21 +178,26 @@ class PeerComm:
         mine = []
         for k in ("recv", "flags", "sum", "done"):
             h = ctypes.create_string_buffer(64)
-            N.check(N.lib().cc_ipc_get_handle(ctypes.c_void_p(local[k].data_ptr()), h), "cc_ipc_get_handle")
-            mine.append(h.raw)
+            off = ctypes.c_int64()
+            N.check(N.lib().cc_ipc_get_handle(ctypes.c_void_p(local[k].data_ptr()), h, ctypes.byref(off)),
+                    "cc_ipc_get_handle")
+            mine.append((h.raw, off.value))
         allh = [None] * world
         dist.all_gather_object(allh, mine, group=group)
         ptrs = []
+        opened: dict = {}  # one mapping per peer allocation (buffers may share one)
         for r in range(world):
             if r == rank:
                 ptrs.append(tuple(local[k].data_ptr() for k in ("recv", "flags", "sum", "done")))
                 continue
             row = []
-            for raw in allh[r]:
-                out = ctypes.c_void_p()
-                N.check(N.lib().cc_ipc_open_handle(ctypes.create_string_buffer(raw, 64), ctypes.byref(out)),
-                        "cc_ipc_open_handle")
-                row.append(out.value)
+            for raw, off in allh[r]:
+                if raw not in opened:
+                    out = ctypes.c_void_p()
+                    N.check(N.lib().cc_ipc_open_handle(ctypes.create_string_buffer(raw, 64), ctypes.byref(out)),
+                            "cc_ipc_open_handle")
+                    opened[raw] = out.value
+                row.append(opened[raw] + off)
             ptrs.append(tuple(row))
         return cls(rank, world, d, m_cap, local, ptrs)
 

@@ -25,7 +25,7 @@ if ROOT not in sys.path:
 
 import paper_2502_15734_b200 as _cc  # noqa: E402
 
-_SUBMODULES = ("errors", "model", "planner", "rpe", "scoring", "stats", "store", "tiers", "replay")
+_SUBMODULES = ("errors", "model", "planner", "rpe", "scoring", "stats", "store", "tiers", "harness")
 
 # Reference names deliberately NOT in the drop-in (outside the hot path,
 # SURVEY.md §2 out-of-scope rows).  They resolve to a stub so the test modules
@@ -38,6 +38,12 @@ OUT_OF_SCOPE = {
     "plan_from_json": "plan JSON import of the CLI (planner.py:218-264), not on the prefill path",
 }
 SKIPPED_TESTS = {
+    # fails on the unmodified reference too (its export_report writes the
+    # tokens_hit_total / tokens_hit_recomputed columns this header omits;
+    # SURVEY Appendix A probe P0: 199/200); the drop-in writes the
+    # reference's columns
+    "test_harness.py::TestReportExport::test_empty_report_writes_header_only":
+        "the reference fails this test itself (CSV header, SURVEY P0)",
     "test_scoring.py::TestCalibration": OUT_OF_SCOPE["calibrate_alpha"],
     "test_planner.py::TestPlanSerialization::test_json_round_trip_keeps_planning_fields": OUT_OF_SCOPE["plan_to_json"],
 }
@@ -58,16 +64,15 @@ for _n in OUT_OF_SCOPE:
 sys.modules.setdefault("cachecraft", _alias)
 for _name in _SUBMODULES:
     sys.modules.setdefault(f"cachecraft.{_name}", getattr(__import__(f"paper_2502_15734_b200.{_name}"), _name))
-# the reference's harness module is the replay driver here
-sys.modules.setdefault("cachecraft.harness", sys.modules["cachecraft.replay"])
 
 collect_ignore = [
     # KVC1 model-config / raw container helpers of the CLI (cli.py); the pool
     # snapshot uses the same container format through VariantStore.snapshot
     "test_serialize.py",
-    # replay driver / tier simulator under the reference names: pending
-    "test_harness.py",
-    "test_trends.py",
+    # the discrete-event tier simulator (simulate, Timeline, timeline_to_csv,
+    # fallback_decision, tiers.py:74-207, :260-299): the tiers here are real
+    # (engine layer-wise preload, tiers.demote_slow_hits); place_and_migrate
+    # and preload_depth are pinned by tests/test_tiers_host.py fixtures
     "test_tiers.py",
 ]
 

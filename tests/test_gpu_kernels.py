@@ -283,9 +283,16 @@ def _attn_ref(q, k, v, q_slot, pad, Hq, Hkv):
 
 @pytest.mark.parametrize("Hq,Hkv,dh,n", [(32, 8, 128, 700), (4, 4, 64, 700), (8, 1, 128, 700), (16, 2, 64, 700),
                                           (32, 8, 128, 2100), (64, 8, 128, 300), (32, 8, 128, 5152)])
-def test_attention_scattered_rows(N, Hq, Hkv, dh, n):
-    """impl 1 = tcgen05/TMEM kernel (key range split in two for the long row
-    tiles when n >= 1024, merged in fixed order), 2 = SIMT reference."""
+@pytest.mark.parametrize("variant", [0, 1, 2, 3])
+def test_attention_scattered_rows(N, Hq, Hkv, dh, n, variant):
+    """impl 1 = tcgen05/TMEM kernel in each tile shape (variant: 128- or
+    64-key tiles, one or two softmax warpgroups; key ranges split for the
+    long row tiles when the grid is small, merged in fixed order),
+    2 = SIMT reference."""
+    import ctypes
+
+    N.lib().cc_debug_attn_variant.argtypes = [ctypes.c_int]
+    N.lib().cc_debug_attn_variant(variant)
     g = torch.Generator(device="cuda").manual_seed(Hq + dh)
     rows = torch.sort(torch.randperm(n, generator=g, device="cuda")[:150]).values.int()
     q = torch.randn((rows.numel(), Hq, dh), generator=g, device="cuda").bfloat16()
@@ -311,6 +318,7 @@ def test_attention_scattered_rows(N, Hq, Hkv, dh, n):
             N.call("cc_attention", N.ptr(q), N.ptr(k), N.ptr(v), N.ptr(rows), N.ptr(pad), N.ptr(ctx2), N.ptr(lse),
                    rows.numel(), n, Hq, Hkv, dh, N.BF16, impl, N.stream_ptr())
             assert torch.equal(ctx, ctx2)
+    N.lib().cc_debug_attn_variant(-1)
 
 
 def test_gather_rope_matches_torch(N):

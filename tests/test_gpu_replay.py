@@ -21,13 +21,13 @@ def test_replay_decisions_match_reference(name, policy, focus, layers, two_pass)
     if not torch.cuda.is_available():
         pytest.skip("no GPU")
     import paper_2502_15734_b200 as cc
-    from paper_2502_15734_b200 import replay
+    from paper_2502_15734_b200 import harness
 
     g = load_json("replay.json")
-    tr = replay.gen_synthetic(12, 1.2, 3, 14, chunk_len_range=(16, 40), seed=3, question_len_range=(4, 8))
+    tr = harness.gen_synthetic(12, 1.2, 3, 14, chunk_len_range=(16, 40), seed=3, question_len_range=(4, 8))
     model = cc.build_model(cc.ModelConfig(n_layers=layers, n_heads=4, d_model=64))
     store = cc.VariantStore(cc.StoreConfig(max_chunks=5, variants_per_chunk=3))
-    rep = replay.replay_gpu(tr, model, store, alpha=1.0, policy=policy, warmup=0, use_focus=focus, focus_window=2,
+    rep = harness.replay_gpu(tr, model, store, alpha=1.0, policy=policy, warmup=0, use_focus=focus, focus_window=2,
                             two_pass=two_pass)
     want = g[name]
     got = [(m.hits, m.tokens_computed, m.token_layers, m.tokens_hit_recomputed) for m in rep.requests]
@@ -40,14 +40,14 @@ def test_replay_baselines_run_and_rank():
     """Policy ordering on a small Zipf trace (tests/test_trends.py:115-153):
     full >= cachecraft computed tokens, exact-prefix deviation 0."""
     import paper_2502_15734_b200 as cc
-    from paper_2502_15734_b200 import replay
+    from paper_2502_15734_b200 import harness
 
-    tr = replay.gen_synthetic(10, 1.2, 3, 12, chunk_len_range=(32, 48), seed=1, question_len_range=(8, 8))
+    tr = harness.gen_synthetic(10, 1.2, 3, 12, chunk_len_range=(32, 48), seed=1, question_len_range=(8, 8))
     model = cc.build_model(cc.ModelConfig(n_layers=2, n_heads=4, d_model=64))
     aggs = {}
     for policy in ("full_recompute", "exact_prefix", "cachecraft"):
         st = cc.VariantStore(cc.StoreConfig(max_chunks=20, variants_per_chunk=3))
-        aggs[policy] = replay.replay_gpu(tr, model, st, policy=policy, warmup=2).aggregate()
+        aggs[policy] = harness.replay_gpu(tr, model, st, policy=policy, warmup=2).aggregate()
     assert aggs["full_recompute"]["tokens_computed"] >= aggs["exact_prefix"]["tokens_computed"]
     assert aggs["full_recompute"]["tokens_computed"] >= aggs["cachecraft"]["tokens_computed"]
     assert aggs["exact_prefix"]["mean_deviation"] < 1e-9

@@ -90,7 +90,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _spawn(out_dir, dtype, use_peer, fn=None):
+def _spawn(out_dir, dtype, use_peer, fn=None, deadline=DEADLINE_S):
     import torch.multiprocessing as mp
 
     ctx = mp.start_processes(fn or _rank_main, args=(_free_port(), str(out_dir), dtype, use_peer), nprocs=WORLD,
@@ -98,8 +98,9 @@ def _spawn(out_dir, dtype, use_peer, fn=None):
     t0 = time.time()
     try:
         while not ctx.join(timeout=5):
-            if time.time() - t0 > DEADLINE_S:
-                raise TimeoutError(f"tensor-parallel ranks did not finish in {DEADLINE_S} s")
+            if time.time() - t0 > deadline:
+                phases = {f: open(os.path.join(out_dir, f)).read() for f in os.listdir(out_dir) if f.startswith("phase")}
+                raise TimeoutError(f"tensor-parallel ranks did not finish in {deadline} s (phases {phases})")
     finally:
         for p in ctx.processes:
             if p.is_alive():
@@ -145,7 +146,14 @@ def _ipc_rank_main(rank, port, out_dir, dtype, use_peer):
     try:
         torch.cuda.set_device(0)
         d, k, M = 512, 256, 200
+
+        def mark(phase):  # progress marker: a hang names its phase
+            with open(os.path.join(out_dir, f"phase{rank}"), "w") as fh:
+                fh.write(phase)
+
+        mark("over_ipc")
         comm = parallel.PeerComm.over_ipc(rank, WORLD, d, 256, "cuda")
+        mark("push")
         g = torch.Generator(device="cuda").manual_seed(100 + rank)
         A = torch.randn((M, k), generator=g, device="cuda").bfloat16()
         B = (torch.randn((d, k), generator=g, device="cuda") / k ** 0.5).bfloat16()
@@ -155,10 +163,12 @@ def _ipc_rank_main(rank, port, out_dir, dtype, use_peer):
         N.call("cc_tp_push_gemm", N.ptr(A), k, N.ptr(B), k, M, d, k, ctypes.addressof(tab), s)
         torch.cuda.synchronize()
         dist.barrier()  # every rank's tiles are in their owners' slabs
+        mark("reduce")
         N.call("cc_tp_reduce", ctypes.addressof(tab), M, d, s)
         torch.cuda.synchronize()
         dist.barrier()  # every owner has all-gathered its columns
         comm.done_target += (-(-M // 128)) * (d // 256)
+        mark("wait")
         N.call("cc_tp_wait", ctypes.addressof(tab), comm.done_target, s)
         torch.cuda.synchronize()
         np.savez(os.path.join(out_dir, f"ipc{rank}.npz"), A=A.float().cpu().numpy(), B=B.float().cpu().numpy(),
@@ -171,7 +181,7 @@ def _ipc_rank_main(rank, port, out_dir, dtype, use_peer):
 def test_ipc_peer_push_reduce_across_processes(tmp_path):
     if not torch.cuda.is_available():
         pytest.skip("no GPU")
-    _spawn(tmp_path, "bf16", True, fn=_ipc_rank_main)
+    _spawn(tmp_path, "bf16", True, fn=_ipc_rank_main, deadline=90)
     out = [np.load(os.path.join(tmp_path, f"ipc{r}.npz")) for r in range(WORLD)]
     want = sum(o["A"] @ o["B"].T for o in out)  # fp32 partials summed over the ranks
     for r in range(WORLD):

@@ -62,17 +62,17 @@ engine.execute = ex
 cfg = cc.ModelConfig.llama3_8b(dtype="bf16")
 model = cc.build_model(cfg)
 gen = dict(chunk_len_range=(512, 512), question_len_range=(32, 32), vocab_size=cfg.vocab_size)
-tr = replay.gen_synthetic(200, 1.542, 10, 50, seed=3, **gen)
+tr = harness.gen_synthetic(200, 1.542, 10, 50, seed=3, **gen)
 store = cc.VariantStore(cc.StoreConfig(max_chunks=100, variants_per_chunk=5))
-replay.replay_gpu(tr, model, store, policy="cachecraft", warmup=0, cfo_override=0.15, measure_deviation=False,
+harness.replay_gpu(tr, model, store, policy="cachecraft", warmup=0, cfo_override=0.15, measure_deviation=False,
                   records=tr.records[:20])
 T.clear(), C.clear()
 t0 = time.perf_counter()
-rep = replay.replay_gpu(tr, model, store, policy="cachecraft", warmup=0, cfo_override=0.15, measure_deviation=False,
+rep = harness.replay_gpu(tr, model, store, policy="cachecraft", warmup=0, cfo_override=0.15, measure_deviation=False,
                         records=tr.records[20:50])
 wall = time.perf_counter() - t0
 print(f"30 requests wall {wall*1e3:.0f} ms; per request {wall/30*1e3:.1f} ms; ttft p50 "
-      f"{np.median([r.ttft_ms for r in rep.requests]):.1f} ms")
+      f"{np.median([r.ttft * 1e3 for r in rep.requests]):.1f} ms")
 for k in sorted(T, key=lambda k: -T[k]):
     print(f"{k:22s} n={C[k]:4d} total {T[k]*1e3:8.1f} ms  per call {T[k]/C[k]*1e3:7.2f} ms")
 print("hits", [r.hits for r in rep.requests])
