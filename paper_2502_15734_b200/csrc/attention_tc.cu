@@ -160,7 +160,7 @@ __global__ void __launch_bounds__(At<DH, BN, NWG>::THREADS, At<DH, BN, NWG>::CTA
                    const uint8_t* __restrict__ key_pad, __nv_bfloat16* __restrict__ ctx, float* __restrict__ lse,
                    int n_q, int n_keys, int Hq, int G, float scale_log2, long long* __restrict__ trace,
                    int n_groups, int n_row_tiles, int target, int max_parts, float* __restrict__ ws_o,
-                   float2* __restrict__ ws_ml, int* __restrict__ counters) {
+                   float2* __restrict__ ws_ml, int* __restrict__ counters, int exp) {
   using SM = At<DH, BN, NWG>;
   constexpr int KST = SM::KST, VST = SM::VST, KPT = SM::KPT, OPT = SM::OPT, NT = SM::THREADS;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -336,12 +336,14 @@ __global__ void __launch_bounds__(At<DH, BN, NWG>::THREADS, At<DH, BN, NWG>::CTA
         twait(&s_empty[b], ((i >> 1) & 1) ^ 1, tracing, w1);
         tc_fence_after();
         const long long ts0 = tracing ? clock64() : 0;
+        if (exp != 3 && exp != 9) {  // (exp 3, timing experiment: no S MMA)
 #pragma unroll
-        for (int kk = 0; kk < DH / 16; ++kk) {
-          const int a = kk >> 2, w = kk & 3;
-          uint64_t bd = desc_sw128(sK + st * SM::KV_BYTES + a * BN * 128) + 2 * w;
-          uint64_t ad = desc_sw128(sQ + a * 128 * 128) + 2 * w;
-          mma_bf16(t_s0 + b * BN, ad, bd, id_s, kk > 0);
+          for (int kk = 0; kk < DH / 16; ++kk) {
+            const int a = kk >> 2, w = kk & 3;
+            uint64_t bd = desc_sw128(sK + st * SM::KV_BYTES + a * BN * 128) + 2 * w;
+            uint64_t ad = desc_sw128(sQ + a * 128 * 128) + 2 * w;
+            mma_bf16(t_s0 + b * BN, ad, bd, id_s, kk > 0);
+          }
         }
         const long long ts1 = tracing ? clock64() : 0;
         mma_commit(&s_full[b]);  // (K slot released by the softmax when it sees s_full)
@@ -355,11 +357,20 @@ __global__ void __launch_bounds__(At<DH, BN, NWG>::THREADS, At<DH, BN, NWG>::CTA
         twait(&v_full[st], (i / VST) & 1, tracing, w3);
         tc_fence_after();
         const long long tp0 = tracing ? clock64() : 0;
+        if (exp == 1) {  // timing experiment: V read as a K-major operand (wrong result)
+          constexpr uint32_t id_k = idesc_bf16(128, DH, false);
 #pragma unroll
-        for (int kk = 0; kk < BN / 16; ++kk) {
-          uint64_t bd = desc_sw128_mn(sV + st * SM::KV_BYTES + kk * 16 * 128, BN * 128);
-          // A = P in TMEM: row = lane, 2 bf16 keys per 32-bit column, 16 keys = 8 columns
-          mma_bf16_ts(t_o, t_s0 + pb * BN + kk * 8, bd, id_o, (i > 0 || kk > 0) ? 1u : 0u);
+          for (int kk = 0; kk < BN / 16; ++kk) {
+            uint64_t bd = desc_sw128(sV + st * SM::KV_BYTES + (kk >> 2) * DH * 128) + 2 * (kk & 3);
+            mma_bf16_ts(t_o, t_s0 + pb * BN + kk * 8, bd, id_k, (i > 0 || kk > 0) ? 1u : 0u);
+          }
+        } else if (exp != 2 && exp != 9) {  // (exp 2, timing experiment: no PV MMA)
+#pragma unroll
+          for (int kk = 0; kk < BN / 16; ++kk) {
+            uint64_t bd = desc_sw128_mn(sV + st * SM::KV_BYTES + kk * 16 * 128, BN * 128);
+            // A = P in TMEM: row = lane, 2 bf16 keys per 32-bit column, 16 keys = 8 columns
+            mma_bf16_ts(t_o, t_s0 + pb * BN + kk * 8, bd, id_o, (i > 0 || kk > 0) ? 1u : 0u);
+          }
         }
         const long long tp1 = tracing ? clock64() : 0;
         mma_commit(&p_empty[pb]);  // P buffer and V slot pb
@@ -393,17 +404,26 @@ __global__ void __launch_bounds__(At<DH, BN, NWG>::THREADS, At<DH, BN, NWG>::CTA
       float s[KPT];
       {
         const uint32_t ta = t_s0 + b * BN + h * KPT + lane_off;
+        if (exp == 7) {  // timing experiment: no S read
 #pragma unroll
-        for (int c = 0; c < KPT / 32; ++c) {
-          uint32_t r[32];
-          tmem_ld32(ta + c * 32, r);
-          tmem_ld_wait();
+          for (int c = 0; c < KPT; ++c) s[c] = 0.001f * c;
+        } else {
 #pragma unroll
-          for (int e = 0; e < 32; ++e) s[c * 32 + e] = __uint_as_float(r[e]);
+          for (int c = 0; c < KPT / 32; ++c) {
+            uint32_t r[32];
+            tmem_ld32(ta + c * 32, r);
+            tmem_ld_wait();
+#pragma unroll
+            for (int e = 0; e < 32; ++e) s[c * 32 + e] = __uint_as_float(r[e]);
+          }
         }
       }
       tc_fence_before();
       mbar_arrive(&s_empty[b]);
+      if (exp == 8 || exp == 9) {  // timing experiment: no softmax at all (barriers only)
+        mbar_arrive(&p_full[i & 1]);
+        continue;
+      }
       const int j0 = (t0 + i) * BN;
       // keys j0 + KPT h + c visible iff c <= lim_rel (causal + bounds) and not a pad
       const int lim_rel = min(lim, n_keys - 1) - j0 - KPT * h;
@@ -429,7 +449,7 @@ __global__ void __launch_bounds__(At<DH, BN, NWG>::THREADS, At<DH, BN, NWG>::CTA
 #pragma unroll
       for (int c = 8; c < KPT; ++c) mx[c & 7] = fmaxf(mx[c & 7], s[c]);
       float tmax = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])), fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
-      if constexpr (NWG > 1) {
+      if (NWG > 1 && exp != 6) {  // (exp 6, timing experiment: no max exchange)
         xmax[((i & 1) * NWG + h) * 128 + m] = tmax;
         pair_bar();
 #pragma unroll
@@ -460,8 +480,8 @@ __global__ void __launch_bounds__(At<DH, BN, NWG>::THREADS, At<DH, BN, NWG>::CTA
           // alone would take as long as the two MMAs of a tile)
           const bool poly = (ch & 3) == 3;
           const float x0 = fmaf(s[c], scale_log2, -base_l2), x1 = fmaf(s[c + 1], scale_log2, -base_l2);
-          const float p0 = poly ? ex2_poly(x0) : ex2_fast(x0);
-          const float p1 = poly ? ex2_poly(x1) : ex2_fast(x1);
+          const float p0 = exp == 4 ? x0 : (poly ? ex2_poly(x0) : ex2_fast(x0));
+          const float p1 = exp == 4 ? x1 : (poly ? ex2_poly(x1) : ex2_fast(x1));
           ps[(2 * e) & 7] += p0;
           ps[(2 * e + 1) & 7] += p1;
           __nv_bfloat162 hv = __floats2bfloat162_rn(p0, p1);
@@ -470,7 +490,7 @@ __global__ void __launch_bounds__(At<DH, BN, NWG>::THREADS, At<DH, BN, NWG>::CTA
       }
       // P_i over S_i's first BN/2 columns: every part finished reading S_i
       // before the pair barrier above (one part: this thread read its own)
-      tmem_st_cols<KPT / 2>(t_s0 + pb * BN + h * (KPT / 2) + lane_off, pt);
+      if (exp != 5) tmem_st_cols<KPT / 2>(t_s0 + pb * BN + h * (KPT / 2) + lane_off, pt);  // (5: no P store)
       l_run += ((ps[0] + ps[1]) + (ps[2] + ps[3])) + ((ps[4] + ps[5]) + (ps[6] + ps[7]));
       // O *= alpha (this part's columns) for rows whose max grew past the lazy
       // threshold.  tcgen05.ld/st are warp-collective: the whole warp joins,
@@ -683,6 +703,15 @@ int encode(CUtensorMap* m, int rank, const void* p, const cuuint64_t* dims, cons
 
 int g_attn_variant = -1;  // debug hook / CCB_ATTN_VARIANT: kernel shape (see pick below)
 
+// CCB_ATTN_EXP (timing experiments only, wrong results): 1 = V as a K-major
+// PV operand, 2 = no PV MMA, 3 = no S MMA, 4 = no softmax exponentials,
+// 5 = no P store, 6 = no max exchange, 7 = no S read, 8 = no softmax work,
+// 9 = 8 without the S and PV MMAs
+int attn_exp() {
+  const char* e = getenv("CCB_ATTN_EXP");
+  return e ? atoi(e) : 0;
+}
+
 template <int DH, int BN, int NWG>
 int launch(const void* q, const void* k, const void* v, const int32_t* q_slot, const uint8_t* key_pad, void* ctx,
            float* lse, int n_q, int n_keys, int Hq, int Hkv, cudaStream_t st) {
@@ -719,7 +748,8 @@ int launch(const void* q, const void* k, const void* v, const int32_t* q_slot, c
   const int max_tiles = (n_keys + BN - 1) / BN;
   int target = max_tiles, max_parts = 1;
   if (row_tiles <= AT_MAXT && max_tiles > 0 && Hkv * row_tiles < slots) {
-    max_parts = std::max(1, std::min(AT_MAXP, slots / (Hkv * row_tiles)));
+    // (rounded up: at r = 0.05, 80 items on 148 SMs, 2 parts measured 51.5 us vs 70 us unsplit)
+    max_parts = std::max(1, std::min(AT_MAXP, (slots + Hkv * row_tiles - 1) / (Hkv * row_tiles)));
     target = std::max(8 * 128 / BN, (max_tiles + max_parts - 1) / max_parts);
     max_parts = std::min(max_parts, (max_tiles + target - 1) / target);
     if (max_parts < 1) max_parts = 1;
@@ -749,7 +779,7 @@ int launch(const void* q, const void* k, const void* v, const int32_t* q_slot, c
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)DH);
   return launch_k(attn_tc_kernel<DH, BN, NWG>, grid, dim3(SM::THREADS), SM::TOTAL, st, "attention_tc", mq, mk, mv,
                   q_slot, key_pad, (__nv_bfloat16*)ctx, lse, n_q, n_keys, Hq, G, scale_log2, g_attn_trace, Hkv,
-                  row_tiles, target, max_parts, ws_o, ws_ml, counters);
+                  row_tiles, target, max_parts, ws_o, ws_ml, counters, attn_exp());
 }
 
 // Kernel shape per launch: 0 = 128-key tiles, two softmax warpgroups (one
@@ -777,8 +807,17 @@ int attention_tc_bf16(const void* q, const void* k, const void* v, const int32_t
     return fail(CC_E_UNSUP, "attention_tc: pointers must be 16-byte aligned");
   int variant = g_attn_variant;
   if (variant < 0) {
-    static const int env = getenv("CCB_ATTN_VARIANT") ? atoi(getenv("CCB_ATTN_VARIANT")) : 0;
+    static const int env = getenv("CCB_ATTN_VARIANT") ? atoi(getenv("CCB_ATTN_VARIANT")) : -1;
     variant = env;
+  }
+  if (variant < 0) {
+    // Two or more waves of (group, row tile) CTAs: 64-key tiles with two CTAs
+    // per SM (one CTA's MMAs fill the other's softmax gaps; measured full
+    // recompute 5152 rows: 221 vs 279 us, 32k prompt 1355 vs 1392 us).  One
+    // wave or less (config 2: 208 CTAs): 128-key tiles, one CTA per SM
+    // (72 vs 88 us) -- there the longest CTA sets the time.
+    const int items = Hkv * ((n_q + (128 / G) - 1) / (128 / G));
+    variant = items >= 2 * num_sms() ? 1 : 0;
   }
   if (dh == 128) return launch_variant<128>(variant, q, k, v, q_slot, key_pad, ctx, lse, n_q, n_keys, Hq, Hkv, st);
   if (dh == 64) return launch_variant<64>(variant, q, k, v, q_slot, key_pad, ctx, lse, n_q, n_keys, Hq, Hkv, st);

@@ -16,8 +16,7 @@ import torch  # noqa: E402
 
 from paper_2502_15734_b200 import _native as N  # noqa: E402
 
-variants = [int(x) for x in (sys.argv[1] if len(sys.argv) > 1 else "0,1,2").split(",")]
-iters = int(sys.argv[2]) if len(sys.argv) > 2 else 50
+# variant specs: "v" or "v@target/parts" (forced key split, CCB_ATTN_SPLIT)
 lib = N.lib()
 lib.cc_debug_attn_variant.argtypes = [ctypes.c_int]
 
@@ -67,37 +66,54 @@ def ref(args):
     return torch.cat(out)
 
 
-for name, (n_q, n, Hq, Hkv) in CASES.items():
-    args = make(n_q, n, Hq, Hkv)
-    keys_vis = (args[0].long() + 1).sum().item()
-    flop = 4.0 * Hq * 128 * keys_vis
-    ctx0 = None
-    want = ref(args) if n_q * n * Hq <= 6e9 else None
-    line = [f"{name:18s} flop {flop / 1e9:7.1f}G"]
-    for var in variants:
-        lib.cc_debug_attn_variant(var)
-        ctx = torch.empty((n_q, Hq * 128), dtype=torch.bfloat16, device="cuda")
-        lse = torch.empty((n_q, Hq), dtype=torch.float32, device="cuda")
-        for _ in range(3):
-            run(args, ctx, lse)
-        torch.cuda.synchronize()
-        ev = []
-        for _ in range(iters):
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record()
-            run(args, ctx, lse)
-            b.record()
-            ev.append((a, b))
-        torch.cuda.synchronize()
-        us = statistics.median(x.elapsed_time(y) for x, y in ev) * 1e3
-        err = ""
-        if want is not None:
-            e = ((ctx.float() - want).norm() / want.norm()).item()
-            err = f" err {e:.1e}"
-        if ctx0 is None:
-            ctx0 = ctx.clone()
-        else:
-            err += f" d0 {((ctx.float() - ctx0.float()).norm() / ctx0.float().norm()).item():.1e}"
-        line.append(f"v{var} {us:7.1f}us {flop / us / 1e6:6.0f}TF/s{err}")
-    lib.cc_debug_attn_variant(-1)
-    print(" | ".join(line), flush=True)
+def main():
+    variants = (sys.argv[1] if len(sys.argv) > 1 else "0,1,2").split(",")
+    iters = int(sys.argv[2]) if len(sys.argv) > 2 else 50
+    cases_sel = sys.argv[3].split(",") if len(sys.argv) > 3 else None
+    for name, (n_q, n, Hq, Hkv) in CASES.items():
+        if cases_sel and not any(c in name for c in cases_sel):
+            continue
+        args = make(n_q, n, Hq, Hkv)
+        keys_vis = (args[0].long() + 1).sum().item()
+        flop = 4.0 * Hq * 128 * keys_vis
+        ctx0 = None
+        want = ref(args) if n_q * n * Hq <= 6e9 else None
+        line = [f"{name:18s} flop {flop / 1e9:7.1f}G"]
+        for spec in variants:
+            # spec: "v", "vxE" (timing experiment E, CCB_ATTN_EXP), "...@target/parts" (CCB_ATTN_SPLIT)
+            os.environ.pop("CCB_ATTN_EXP", None)
+            os.environ.pop("CCB_ATTN_SPLIT", None)
+            head = spec.split("@")[0]
+            if "x" in head:
+                os.environ["CCB_ATTN_EXP"] = head.split("x")[1]
+            if "@" in spec:
+                os.environ["CCB_ATTN_SPLIT"] = spec.split("@")[1].replace("/", ",")
+            lib.cc_debug_attn_variant(int(head.split("x")[0]))
+            ctx = torch.empty((n_q, Hq * 128), dtype=torch.bfloat16, device="cuda")
+            lse = torch.empty((n_q, Hq), dtype=torch.float32, device="cuda")
+            for _ in range(3):
+                run(args, ctx, lse)
+            torch.cuda.synchronize()
+            ev = []
+            for _ in range(iters):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record()
+                run(args, ctx, lse)
+                b.record()
+                ev.append((a, b))
+            torch.cuda.synchronize()
+            us = statistics.median(x.elapsed_time(y) for x, y in ev) * 1e3
+            err = ""
+            if want is not None:
+                err = f" err {((ctx.float() - want).norm() / want.norm()).item():.1e}"
+            if ctx0 is None:
+                ctx0 = ctx.clone()
+            line.append(f"v{spec} {us:7.1f}us {flop / us / 1e6:6.0f}TF/s{err}")
+        lib.cc_debug_attn_variant(-1)
+        os.environ.pop("CCB_ATTN_EXP", None)
+        os.environ.pop("CCB_ATTN_SPLIT", None)
+        print(" | ".join(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

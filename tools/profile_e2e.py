@@ -40,3 +40,18 @@ t1 = time.perf_counter()
 torch.cuda.synchronize()
 t2 = time.perf_counter()
 print(f"execute enqueue {1e3 * (t1 - t0):.3f} ms, until done {1e3 * (t2 - t0):.3f} ms")
+
+# where the host time before the first kernel goes (cProfile, 5 requests)
+import cProfile  # noqa: E402
+import pstats  # noqa: E402
+
+pr = cProfile.Profile()
+for rep in range(5):
+    torch.cuda.synchronize()
+    pr.enable()
+    p = cc.build_plan(chunks, question, store, alpha=1.0, cfo_override=0.15)
+    rq = cc.plan_to_request(p)
+    res = cc.prefill(model, rq, record_attention=False, stats=False, first_token=True)
+    tok = res.first_token
+    pr.disable()
+pstats.Stats(pr).sort_stats("tottime").print_stats(25)
