@@ -904,7 +904,9 @@ def main():
     N_.assert_tensor_core_only()  # every bf16 GEMM / attention of the run ran on tcgen05
     gemm_roof = roofline_obj("gemm", summ, peaks, "tensor", args.config)
     kernels = [k for k in (roofline_obj("gather_rope", summ, peaks, "hbm", args.config),
-                           roofline_obj("attention", summ, peaks, "tensor", args.config)) if k]
+                           roofline_obj("attention", summ, peaks, "tensor", args.config),
+                           roofline_obj("rmsnorm", summ, peaks, "hbm", args.config),
+                           roofline_obj("rope_scatter", summ, peaks, "hbm", args.config)) if k]
     share = {k: round(v["ms_total"] / (sum(ms[-n_timed:]) or 1), 4) for k, v in summ.items()}
     line = {
         "metric": METRIC if args.config == "8b" else METRIC.replace("Llama-3-8B shapes, 10x512+32", {

@@ -460,12 +460,15 @@ def _execute(model: Model, plan: DevicePlan, ws: dict, *, record=False, record_v
             if record_values:
                 vtrace.append((kv_v[l], None, None))
             continue
-        N.call("cc_rmsnorm", P(hidden), P(xn), P(lw.get("attn_norm")), n_l, d, eps, dt, s)
+        with tm.span("rmsnorm", nbytes=n_l * d * (4 + esz)):
+            N.call("cc_rmsnorm", P(hidden), P(xn), P(lw.get("attn_norm")), n_l, d, eps, dt, s)
         with tm.span("gemm", flops=2.0 * n_l * (qw + 2 * kvw) * d):
             N.call("cc_gemm", P(xn), d, P(lw["w_qkv"]), d, P(qkv), qw + 2 * kvw, n_l, qw + 2 * kvw, d, N.EPI_STORE,
                    dt, gemm_impl, s)
-        N.call("cc_rope_scatter_qkv", P(qkv), qw + 2 * kvw, n_l, P(D["row_slot"]), P(D["row_pos"]), P(rope), P(q_rot),
-               P(kv_k[l]), P(kv_v[l]), P(k_rot[l]), H, Hkv, dh, dt, s)
+        # algorithmic bytes: read the qkv row, write q_rot and k, k_rot, v at the row slots
+        with tm.span("rope_scatter", nbytes=n_l * (qw + 2 * kvw + qw + 3 * kvw) * esz):
+            N.call("cc_rope_scatter_qkv", P(qkv), qw + 2 * kvw, n_l, P(D["row_slot"]), P(D["row_pos"]), P(rope),
+                   P(q_rot), P(kv_k[l]), P(kv_v[l]), P(k_rot[l]), H, Hkv, dh, dt, s)
         if preload is not None:
             preload.gather(model, plan, ws, l, rope, s)
         if l2pf is not None:  # o_proj weights -> L2 while attention runs (it reads K/V from L2 only)
@@ -506,7 +509,8 @@ def _execute(model: Model, plan: DevicePlan, ws: dict, *, record=False, record_v
                        gemm_impl, s)
             else:
                 _tp_partial_gemm(model, tp, ctx, qw, lw["w_o"], hidden, part, n_l, d, qw, dt, gemm_impl, s)
-        N.call("cc_rmsnorm", P(hidden), P(xn), P(lw.get("mlp_norm")), n_l, d, eps, dt, s)
+        with tm.span("rmsnorm", nbytes=n_l * d * (4 + esz)):
+            N.call("cc_rmsnorm", P(hidden), P(xn), P(lw.get("mlp_norm")), n_l, d, eps, dt, s)
         if cfg.mlp == "swiglu":
             with tm.span("gemm", flops=2.0 * n_l * 2 * ff * d):
                 N.call("cc_gemm", P(xn), d, P(lw["w_gu"]), d, P(act), ff, n_l, 2 * ff, d, N.EPI_SWIGLU, dt,
