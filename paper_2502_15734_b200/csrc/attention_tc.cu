@@ -108,10 +108,10 @@ __device__ __forceinline__ void twait(uint64_t* bar, uint32_t parity, bool traci
 // S0/P0 | S1/P1 | O: 2 BN + DH columns.  BN = 64 with DH = 128 needs 256
 // columns and ~106 KiB of shared memory: two CTAs share an SM, and each
 // CTA's MMAs fill the other's softmax gaps on the tensor pipe.
-template <int DH, int BN, int NWG>
+template <int DH, int BN, int NWG, int KST_ = (BN == 64 ? 2 : 3), int VST_ = 2>
 struct At {
-  static constexpr int KST = BN == 64 ? 2 : 3;   // K ring depth
-  static constexpr int VST = 2;                  // V ring depth = P buffers
+  static constexpr int KST = KST_;  // K ring depth
+  static constexpr int VST = VST_;  // V ring depth (>= 2: slot i % VST also names P buffer i % 2's release)
   static constexpr int THREADS = 64 + 128 * NWG;
   static constexpr int KPT = BN / NWG;           // keys per softmax thread
   static constexpr int OPT = DH / NWG;           // O columns per softmax thread
@@ -124,7 +124,7 @@ struct At {
   static constexpr int K_OFF = Q_OFF + Q_BYTES;
   static constexpr int V_OFF = K_OFF + KST * KV_BYTES;
   static constexpr int BAR_OFF = V_OFF + VST * KV_BYTES;
-  static constexpr int X_OFF = BAR_OFF + 256;        // [2 parities][NWG][128 rows] f32 exchange
+  static constexpr int X_OFF = BAR_OFF + 512;        // [2 parities][NWG][128 rows] f32 exchange
   static constexpr int PLAN_OFF = X_OFF + 2 * NWG * 128 * 4;  // work-item plan: [3][AT_MAXT] ints
   // no alignment slack: the kernel holds no static shared memory, so the
   // dynamic window starts 1 KiB aligned (checked at run time)
@@ -153,15 +153,15 @@ __device__ __forceinline__ void tmem_st_cols<64>(uint32_t taddr, const uint32_t*
   tmem_st_cols<32>(taddr + 32, r + 32);
 }
 
-template <int DH, int BN, int NWG>
-__global__ void __launch_bounds__(At<DH, BN, NWG>::THREADS, At<DH, BN, NWG>::CTAS_PER_SM)
+template <int DH, int BN, int NWG, int KST_, int VST_>
+__global__ void __launch_bounds__(At<DH, BN, NWG, KST_, VST_>::THREADS, At<DH, BN, NWG, KST_, VST_>::CTAS_PER_SM)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                    const __grid_constant__ CUtensorMap tmV, const int32_t* __restrict__ q_slot,
                    const uint8_t* __restrict__ key_pad, __nv_bfloat16* __restrict__ ctx, float* __restrict__ lse,
                    int n_q, int n_keys, int Hq, int G, float scale_log2, long long* __restrict__ trace,
                    int n_groups, int n_row_tiles, int target, int max_parts, float* __restrict__ ws_o,
                    float2* __restrict__ ws_ml, int* __restrict__ counters, int exp) {
-  using SM = At<DH, BN, NWG>;
+  using SM = At<DH, BN, NWG, KST_, VST_>;
   constexpr int KST = SM::KST, VST = SM::VST, KPT = SM::KPT, OPT = SM::OPT, NT = SM::THREADS;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* base = smem_raw;
@@ -174,7 +174,8 @@ __global__ void __launch_bounds__(At<DH, BN, NWG>::THREADS, At<DH, BN, NWG>::CTA
   uint64_t* k_full = bars + 1;                 // [KST]
   uint64_t* k_empty = k_full + KST;            // [KST] arrived by the softmax once S_i landed
   uint64_t* v_full = k_empty + KST;            // [VST]
-  uint64_t* s_full = v_full + VST;             // [2]
+  uint64_t* v_empty = v_full + VST;            // [VST] committed by the MMA thread after PV_i
+  uint64_t* s_full = v_empty + VST;            // [2]
   uint64_t* s_empty = s_full + 2;              // [2]
   uint64_t* p_full = s_empty + 2;              // [2]
   uint64_t* p_empty = p_full + 2;              // [2]
@@ -257,7 +258,10 @@ __global__ void __launch_bounds__(At<DH, BN, NWG>::THREADS, At<DH, BN, NWG>::CTA
       mbar_init(&k_full[s], 1);
       mbar_init(&k_empty[s], 1);
     }
-    for (int s = 0; s < VST; ++s) mbar_init(&v_full[s], 1);
+    for (int s = 0; s < VST; ++s) {
+      mbar_init(&v_full[s], 1);
+      mbar_init(&v_empty[s], 1);
+    }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&s_full[b], 1);
       mbar_init(&s_empty[b], 128 * NWG);
@@ -314,8 +318,8 @@ __global__ void __launch_bounds__(At<DH, BN, NWG>::THREADS, At<DH, BN, NWG>::CTA
       load_k(0);
       for (int i = 0; i < n_tiles; ++i) {
         if (i + 1 < n_tiles) load_k(i + 1);
-        const int st = i % VST;  // == P buffer of tile i: free once PV_{i-2} completed
-        twait(&p_empty[st], ((i / VST) & 1) ^ 1, tracing, w1);
+        const int st = i % VST;  // free once PV_{i-VST} completed
+        twait(&v_empty[st], ((i / VST) & 1) ^ 1, tracing, w1);
         mbar_expect_tx(&v_full[st], SM::KV_BYTES);
 #pragma unroll
         for (int a = 0; a < SM::ATOMS; ++a)
@@ -373,7 +377,8 @@ __global__ void __launch_bounds__(At<DH, BN, NWG>::THREADS, At<DH, BN, NWG>::CTA
           }
         }
         const long long tp1 = tracing ? clock64() : 0;
-        mma_commit(&p_empty[pb]);  // P buffer and V slot pb
+        mma_commit(&p_empty[pb]);       // P buffer pb (and O current through PV_i)
+        mma_commit(&v_empty[i % VST]);  // V slot of tile i
         if (tracing) { t_p_issue += tp1 - tp0; t_p_commit += clock64() - tp1; }
       }
     }
@@ -712,10 +717,10 @@ int attn_exp() {
   return e ? atoi(e) : 0;
 }
 
-template <int DH, int BN, int NWG>
+template <int DH, int BN, int NWG, int KST = (BN == 64 ? 2 : 3), int VST = 2>
 int launch(const void* q, const void* k, const void* v, const int32_t* q_slot, const uint8_t* key_pad, void* ctx,
            float* lse, int n_q, int n_keys, int Hq, int Hkv, cudaStream_t st) {
-  using SM = At<DH, BN, NWG>;
+  using SM = At<DH, BN, NWG, KST, VST>;
   const int G = Hq / Hkv;
   const int R = 128 / G;
   CUtensorMap mq, mk, mv;
@@ -735,7 +740,7 @@ int launch(const void* q, const void* k, const void* v, const int32_t* q_slot, c
     rc = encode(&mv, 2, v, dims, strides, box);
     if (rc) return rc;
   }
-  if (int rc = ensure_smem(attn_tc_kernel<DH, BN, NWG>, SM::TOTAL)) return rc;
+  if (int rc = ensure_smem(attn_tc_kernel<DH, BN, NWG, KST, VST>, SM::TOTAL)) return rc;
   const int row_tiles = (n_q + R - 1) / R;
   // Work items: when the grid of (group, row tile) CTAs leaves CTA slots idle,
   // the row tiles with long causal key ranges are cut into up to AT_MAXP key
@@ -777,7 +782,7 @@ int launch(const void* q, const void* k, const void* v, const int32_t* q_slot, c
   // (an upper bound: CTAs past the planned items exit at once)
   dim3 grid(Hkv * row_tiles * max_parts);
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)DH);
-  return launch_k(attn_tc_kernel<DH, BN, NWG>, grid, dim3(SM::THREADS), SM::TOTAL, st, "attention_tc", mq, mk, mv,
+  return launch_k(attn_tc_kernel<DH, BN, NWG, KST, VST>, grid, dim3(SM::THREADS), SM::TOTAL, st, "attention_tc", mq, mk, mv,
                   q_slot, key_pad, (__nv_bfloat16*)ctx, lse, n_q, n_keys, Hq, G, scale_log2, g_attn_trace, Hkv,
                   row_tiles, target, max_parts, ws_o, ws_ml, counters, attn_exp());
 }
