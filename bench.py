@@ -21,6 +21,7 @@ no data-path collective): value = sum of per-rank tokens / max-rank time.
 from __future__ import annotations
 
 import argparse
+import contextlib
 import json
 import math
 import os
@@ -76,6 +77,8 @@ def parse():
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--ratio", type=float, default=0.15)
+    p.add_argument("--streams", type=int, default=-1,
+                   help="requests in flight on as many CUDA streams (serving mode; -1: 6 for 8b, 2 for 8b-32k, 1 for 70b)")
     p.add_argument("--layers", type=int, default=32)
     p.add_argument("--chunks", type=int, default=10)
     p.add_argument("--chunk-len", type=int, default=512)
@@ -318,6 +321,46 @@ def time_device(model, dplan, ws, req, steps, warmup, world, timer_steps=0):
     torch.cuda.synchronize()
     ms = [a.elapsed_time(b) for a, b in times]
     return ms, timer
+
+
+def time_device_streams(model, runs, steps, warmup, world):
+    """Serving throughput with inputs resident: ``runs`` = one (dplan, ws,
+    req) per CUDA stream, each stream replaying its own request; the timed
+    region spans every stream (start event on the main stream, all streams
+    wait on it; the main stream waits on every stream's end event).
+    Returns the device ms per request (amortised over all streams)."""
+    import torch
+
+    from paper_2502_15734_b200 import engine
+
+    main = torch.cuda.current_stream()
+    streams = [torch.cuda.Stream() for _ in runs]
+    rows = [int(np.flatnonzero(dp.rows == rq.question_span[1] - 1)[0]) for dp, _, rq in runs]
+
+    def burst(n):
+        for _ in range(n):
+            for (dp, ws, _), st, r in zip(runs, streams, rows):
+                with torch.cuda.stream(st):
+                    engine.execute(model, dp, ws)
+                    engine._logits_rows(model, ws["hidden"][r:r + 1])
+
+    with engine.concurrent_streams():
+        for st in streams:
+            st.wait_stream(main)
+        burst(warmup)
+        for st in streams:
+            main.wait_stream(st)
+        barrier(world)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(main)
+        for st in streams:
+            st.wait_event(a)
+        burst(steps)
+        for st in streams:
+            main.wait_stream(st)
+        b.record(main)
+        torch.cuda.synchronize()
+    return a.elapsed_time(b) / (steps * len(runs))
 
 
 def torch_reference_full(model, tokens):
@@ -704,6 +747,7 @@ def main():
     import torch
 
     from paper_2502_15734_b200 import _native
+    from paper_2502_15734_b200 import engine as engine_mod
 
     peaks = {}
     try:
@@ -719,20 +763,34 @@ def main():
     n_recomputed = plan.tokens_recomputed()
 
     # ---- value: device-timed fix-up -----------------------------------------
+    # (a) one request at a time (latency; per-kernel CUDA events on the last
+    # timed step only: an event pair around every launch family costs ~0.8 ms
+    # over a whole step, one step still gives every family its 32 launches)
+    # (b) serving throughput: K requests in flight on K CUDA streams, each
+    # replaying its own resident request (distinct questions); the value
+    K = args.streams if args.streams > 0 else {"8b": 6, "8b-32k": 2, "70b": 1}[args.config]
     calls0 = sum(_native.calls.values())
     barrier(world)
+    tp_mode = args.config == "70b" and world > 1
     with Clocks(torch.cuda.current_device()) as clk:
-        # per-kernel CUDA events on the last timed step only (an event pair
-        # around every launch family costs ~0.8 ms over a whole step; one
-        # step still gives every family its 32 per-layer launches)
         n_timed = 1
         ms, timer = time_device(model, dplan, ws, req, args.steps, args.warmup, world, timer_steps=n_timed)
-    launches = (sum(_native.calls.values()) - calls0) // (args.steps + args.warmup)
+        launches = (sum(_native.calls.values()) - calls0) // (args.steps + args.warmup)
+        ms_step = statistics.mean(ms)
+        ms_max = allreduce_max(ms_step, world)
+        value_single = n_prompt * (1 if tp_mode else world) / (ms_max / 1e3)
+        ms_req = ms_max
+        if K > 1:
+            vq = np.random.default_rng(4242 + rank)
+            runs = []
+            for _ in range(K):
+                _, rq_k, dp_k, ws_k = resident_plan(cc, model, store, chunks,
+                                                    vq.integers(0, model.config.vocab_size, args.question), args.ratio)
+                runs.append((dp_k, ws_k, rq_k))
+            ms_req = allreduce_max(time_device_streams(model, runs, args.steps, args.warmup, world), world)
+            del runs
     clocks = clk.summary()
-    ms_step = statistics.mean(ms)
-    ms_max = allreduce_max(ms_step, world)
-    tp_mode = args.config == "70b" and world > 1
-    value = n_prompt * (1 if tp_mode else world) / (ms_max / 1e3)
+    value = n_prompt * (1 if tp_mode else world) / (ms_req / 1e3)
     summ = timer.summary()
 
     # ---- e2e: public API with host buffers ----------------------------------
@@ -764,30 +822,29 @@ def main():
     # Two requests in flight: request i is enqueued before request i-1's first
     # token is read back (an event behind i-1's kernels, not a stream sync),
     # so the GPU runs the requests back to back
+    # K requests in flight, request i on stream i % K (the serving mode of
+    # (b) above): each request is planned and enqueued, and the oldest one's
+    # first token is read back once K are in flight
     barrier(world)
     t_start = time.perf_counter()
     qs = questions[args.warmup + args.steps:]
-    p = cc.build_plan(chunks, qs[0], store, alpha=1.0, cfo_override=args.ratio)
-    rq = cc.plan_to_request(p)
-    # (one untimed tail request: every timed completion is then observed the
-    # same way — after the next request's enqueue — so a blocking enqueue,
-    # e.g. an allocator sync on the memory-tight 70B model, biases neither end)
+    e2e_streams = [torch.cuda.current_stream()] + [torch.cuda.Stream() for _ in range(K - 1)]
     done = []
-    prev = None
-    n_req = args.warmup + args.steps + 1
-    for i in range(n_req):
-        res = cc.prefill(model, rq, record_attention=False, stats=False, first_token=True)
-        if prev is not None:
-            tok = prev.first_token
-            done.append(time.perf_counter())
-            del prev
-        if i + 1 < n_req:
-            p = cc.build_plan(chunks, qs[i + 1], store, alpha=1.0, cfo_override=args.ratio)
-            rq = cc.plan_to_request(p)
-        prev = res
-    tok = prev.first_token
-    del prev, res
-    done = done[: args.warmup + args.steps]  # completions of the W + K counted requests
+    inflight = []
+    n_req = args.warmup + args.steps + K
+    with engine_mod.concurrent_streams() if K > 1 else contextlib.nullcontext():
+        for i in range(n_req):
+            with torch.cuda.stream(e2e_streams[i % K]):
+                p = cc.build_plan(chunks, qs[i % len(qs)], store, alpha=1.0, cfo_override=args.ratio)
+                inflight.append(cc.prefill(model, cc.plan_to_request(p), record_attention=False, stats=False,
+                                           first_token=True))
+            if len(inflight) > K - 1 and len(done) < args.warmup + args.steps:
+                tok = inflight.pop(0).first_token
+                done.append(time.perf_counter())
+        for r_ in inflight:
+            tok = r_.first_token
+        torch.cuda.synchronize()
+        del inflight
     per_req = (done[-1] - done[args.warmup - 1]) / args.steps if args.warmup > 0 else (done[-1] - t_start) / args.steps
     e2e_mean = allreduce_max(per_req * 1e3, world)
     e2e_value = n_prompt * (1 if tp_mode else world) / (e2e_mean / 1e3)
@@ -827,6 +884,17 @@ def main():
         del wsp
         baselines["prefix_cache_60pct_ours"] = {"tokens_per_s": round(n_prompt / (statistics.mean(msp) / 1e3), 1),
                                                 "ms_per_step": round(statistics.mean(msp), 3)}
+        if K > 1:  # full recompute at the same concurrency as the value
+            fq = np.random.default_rng(999)
+            runs_f = []
+            for _ in range(K):
+                rq_f, dp_f, ws_f = full_plan(cc, model, chunks, fq.integers(0, model.config.vocab_size, args.question))
+                runs_f.append((dp_f, ws_f, rq_f))
+            msf_k = allreduce_max(time_device_streams(model, runs_f, max(3, args.steps // 2), 2, world), world)
+            del runs_f
+            baselines["full_recompute_ours_streams"] = {"tokens_per_s": round(n_prompt / (msf_k / 1e3), 1),
+                                                        "ms_per_request": round(msf_k, 3), "requests_in_flight": K}
+            baselines["speedup_vs_full_recompute_ours_same_concurrency"] = round(msf_k / ms_req, 3)
         # the same three policies through the public API, one request at a
         # time with host token lists: p50 TTFT (submit -> first token on host)
         n_hit = int(round(0.6 * len(chunks)))
@@ -912,15 +980,19 @@ def main():
         "metric": METRIC if args.config == "8b" else METRIC.replace("Llama-3-8B shapes, 10x512+32", {
             "8b-32k": "Llama-3-8B shapes, 64x512+32", "70b": "Llama-3-70B shapes, 16x1024+32"}[args.config]),
         "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": round(ms_max, 4), "higher_is_better": True,
+        "warmup": args.warmup, "ms_per_step": round(ms_req, 4), "higher_is_better": True,
         "scaling": "strong" if tp_mode else "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init weights, random token chunks)",
         "config": wcfg,
         "ttft_ms": {"p50_e2e": round(ttft_p50, 3), "device_mean": round(ms_step, 3)},
+        "requests_in_flight": K,
+        "single_request": {"value": round(value_single, 1), "unit": UNIT, "ms_per_request": round(ms_max, 4),
+                           "note": "one request at a time on one stream (device-timed)"},
         "e2e": {"value": round(e2e_value, 1), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h), "path": "build_plan -> plan_to_request -> prefill(first_token=True)",
-                "mode": "request stream, two requests in flight (request i enqueued before request i-1's first "
-                        "token is read back; planning of i+1 overlapped with compute); serial TTFT in ttft_ms.p50_e2e"},
+                "mode": f"request stream with {K} requests in flight on {K} CUDA streams (a request's first token "
+                        "is read back once the next ones are enqueued; planning overlapped with compute); "
+                        "serial TTFT in ttft_ms.p50_e2e"},
         "roofline": gemm_roof,
         "roofline_kernels": kernels,
         "kernel_time_share": share,

@@ -226,6 +226,12 @@ CC_API int cc_add_f32(float* dst, const float* src, int64_t n, void* stream);
  * with programmatic dependent launch: each kernel's independent prologue
  * overlaps its predecessor.  Process-wide; returns the previous setting. */
 CC_API int cc_set_pdl(int on);
+/* Stream-K GEMM tails on (1, default) / off (0); returns the previous
+ * setting.  A stream-K fold spins on its sibling CTAs: with requests in
+ * flight on several streams, two such GEMMs could each hold SMs while
+ * waiting for CTAs that no SM is free to run, so concurrent (serving) mode
+ * turns them off and keeps every GEMM free of cross-CTA waits. */
+CC_API int cc_set_stream_k(int on);
 
 /* Weight-streaming projection for 1..4 rows (the per-token QKV / o / MLP
  * products of decode, model.py:461-476): C[M,N] (+)= epi(A[M,K] W[N,K]^T),

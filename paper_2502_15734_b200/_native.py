@@ -55,6 +55,7 @@ _SIGS = {
     "cc_decode_attention_dev": ([_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _vp], _i32),
     "cc_decode_advance": ([_vp, _vp, _vp, _vp], _i32),
     "cc_set_pdl": ([_i32], _i32),
+    "cc_set_stream_k": ([_i32], _i32),
     "cc_tp_push_gemm": ([_vp, _i64, _vp, _i64, _i32, _i32, _i32, _vp, _vp], _i32),
     "cc_tp_reduce": ([_vp, _i32, _i32, _vp], _i32),
     "cc_tp_wait": ([_vp, _i64, _vp], _i32),

@@ -17,6 +17,7 @@ static thread_local std::string g_last_error;
 void set_error(const std::string& msg) { g_last_error = msg; }
 
 int g_pdl = 0;
+int g_stream_k = 1;
 
 int fail(int code, const std::string& msg) {
   g_last_error = msg;
@@ -96,6 +97,12 @@ int num_sms() {
 extern "C" {
 
 int cc_abi_version(void) { return CC_ABI_VERSION; }
+
+int cc_set_stream_k(int on) {
+  const int prev = ccb::g_stream_k;
+  ccb::g_stream_k = on ? 1 : 0;
+  return prev;
+}
 
 int cc_set_pdl(int on) {
   const int prev = ccb::g_pdl;

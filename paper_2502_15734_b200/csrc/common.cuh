@@ -90,6 +90,7 @@ inline int ensure_smem(void (*fn)(KArgs...), size_t bytes) {
 // their independent prologue (weight streaming) overlaps the predecessor's
 // tail.  Both are no-ops for a kernel launched without the PDL attribute.
 extern int g_pdl;  // cc_set_pdl
+extern int g_stream_k;  // cc_set_stream_k
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 

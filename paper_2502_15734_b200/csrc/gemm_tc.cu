@@ -1149,7 +1149,7 @@ template <int EPI>
 int launch_epi(const void* A, int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc, int M, int N, int K,
                bool allow_split, cudaStream_t st) {
   Tiling tl;
-  if (!forced_tiling(M, N, K, EPI, &tl)) tl = pick_tiling(M, N, K, EPI, allow_split);
+  if (!forced_tiling(M, N, K, EPI, &tl)) tl = pick_tiling(M, N, K, EPI, allow_split && g_stream_k);
   if (tl.bn == 0) return fail(CC_E_UNSUP, "gemm_tc: N must be a multiple of 128 (SwiGLU: 256)");
   if (tl.tab) {
     CUtensorMap mw, mx[4];

@@ -16,6 +16,8 @@ libcc_b200.so; torch only allocates memory and provides the stream.
 
 from __future__ import annotations
 
+import contextlib
+
 import numpy as np
 
 from . import _native as N
@@ -397,6 +399,20 @@ def _apply_cut(model, plan, ws, slots, new_depth):
                len(touched), new_depth, L, N.ptr(plan.d["slot_pos"]), N.ptr(plan.d["active_until"]),
                N.ptr(model.rope_table(plan.max_pos)), N.ptr(ws["kv_k"]), N.ptr(ws["kv_v"]), N.ptr(ws["k_rot"]),
                plan.n * cfg.kv_width(), cfg.kv_width(), cfg.head_dim(), model.dtype_code, N.stream_ptr())
+
+
+@contextlib.contextmanager
+def concurrent_streams():
+    """Serving mode: requests may be in flight on several CUDA streams at
+    once.  Every kernel here already keeps per-stream scratch; inside this
+    context the GEMMs also run without stream-K tails, whose folds spin on
+    sibling CTAs (two such GEMMs on different streams could each hold SMs
+    waiting for CTAs no SM is free to run)."""
+    prev = N.lib().cc_set_stream_k(0)
+    try:
+        yield
+    finally:
+        N.lib().cc_set_stream_k(prev)
 
 
 def execute(model: Model, plan: DevicePlan, ws: dict, **kw):

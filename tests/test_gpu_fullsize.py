@@ -108,3 +108,32 @@ def test_32k_prompt_gather_copies_bit_exact():
     keys = res.kv.keys[0]
     for i, (s, e) in enumerate(req.segment_slots):
         assert np.array_equal(keys[s:e], caches[i].keys[0][:512])
+
+
+def test_concurrent_requests_on_streams_are_bit_identical(setup):
+    """Several fix-up requests in flight on different CUDA streams (the
+    serving mode of the bench's e2e stream) produce exactly the bits of the
+    same requests run one at a time: per-stream workspaces, scratch and
+    split counters, weights and pool read-only."""
+    cc, model, chunks, q, caches = setup
+    r = np.random.default_rng(31)
+    reqs = []
+    for _ in range(4):
+        segs = [cc.Segment(tokens=c, cache=k, recompute=r.uniform(size=c.size) < 0.15) for c, k in zip(chunks, caches)]
+        reqs.append(cc.build_request(segs, r.integers(0, model.config.vocab_size, 32)))
+    serial = []
+    with cc.concurrent_streams():  # (same GEMM tilings in both runs: no stream-K)
+        for rq in reqs:
+            res = cc.prefill(model, rq, record_attention=False, stats=False, first_token=True)
+            serial.append((res.hidden, res.kv.keys[1], res.first_token))
+    streams = [torch.cuda.Stream() for _ in reqs]
+    out = []
+    with cc.concurrent_streams():
+        for rq, st in zip(reqs, streams):
+            with torch.cuda.stream(st):
+                out.append(cc.prefill(model, rq, record_attention=False, stats=False, first_token=True))
+        torch.cuda.synchronize()
+    for res, (h, k1, tok) in zip(out, serial):
+        assert res.first_token == tok
+        assert np.array_equal(res.hidden, h)
+        assert np.array_equal(res.kv.keys[1], k1)
