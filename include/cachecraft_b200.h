@@ -122,6 +122,19 @@ CC_API int cc_rmsnorm(const void* hidden, void* out, const float* weight, int n_
 CC_API int cc_gemm(const void* A, int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc, int M,
             int N, int K, int epilogue, int dtype, int impl, void* stream);
 
+/* QKV projection with RoPE and the K/V scatter fused (K3, model.py:399-404;
+ * replaces cc_gemm(CC_EPI_STORE) + cc_rope_scatter_qkv): qkv = x W_qkv^T,
+ * q_rot[r] = RoPE(q, pos[r]); kv_k[slot[r]] = k; k_rot[slot[r]] = RoPE(k);
+ * kv_v[slot[r]] = v.  bf16, d_head 128, (Hq + 2 Hkv) 128 % 256 == 0 and
+ * 64 <= n_rows <= 8192: one tcgen05 CTA-pair kernel (epilogue does the
+ * rotation and scatter).  Other shapes / dtypes: the GEMM into qkv_scratch
+ * ([n_rows][(Hq + 2 Hkv) d_head], may be NULL when the fused kernel applies)
+ * followed by cc_rope_scatter_qkv -- bit-identical results in bf16. */
+CC_API int cc_gemm_qkv_rope(const void* x, int64_t ldx, const void* w_qkv, int64_t ldw, int n_rows, int d,
+                     const int32_t* row_slot, const int32_t* row_pos, const void* rope_table, void* q_rot,
+                     void* kv_k, void* kv_v, void* k_rot, void* qkv_scratch, int n_heads, int n_kv_heads,
+                     int d_head, int dtype, void* stream);
+
 /* K4 — causal attention of scattered query rows over all request keys
  * (model.py:406-416).  q [n_q][Hq][dh] rotated; k_rot/v [n_keys][Hkv][dh];
  * query row r sees keys j <= q_slot[r] with key_pad[j] == 0.  Writes

@@ -39,6 +39,8 @@ _SIGS = {
     "cc_embed_rows": ([_vp, _vp, _vp, _i32, _i32, _i32, _vp], _i32),
     "cc_rmsnorm": ([_vp, _vp, _vp, _i32, _i32, _f64, _i32, _vp], _i32),
     "cc_gemm": ([_vp, _i64, _vp, _i64, _vp, _i64, _i32, _i32, _i32, _i32, _i32, _i32, _vp], _i32),
+    "cc_gemm_qkv_rope": ([_vp, _i64, _vp, _i64, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32,
+                          _vp], _i32),
     "cc_attention": ([_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _vp], _i32),
     "cc_attention_probs": ([_vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _i32, _vp], _i32),
     "cc_segment_mass": ([_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _vp, _i32, _vp, _i32, _i32, _i32, _i32, _i32, _vp], _i32),

@@ -56,6 +56,14 @@ __device__ __forceinline__ double gelu_tanh(double x) {
 __device__ __forceinline__ float silu(float x) { return __fdividef(x, 1.f + __expf(-x)); }
 __device__ __forceinline__ double silu(double x) { return x / (1.0 + exp(-x)); }
 
+// RoPE rotation of one pair (x, y) by (cos, sin) in fp32 with a fixed FMA
+// order, shared by every kernel that rotates fresh rows (rope_scatter, the
+// fused QKV epilogue) so they produce the same bits
+__device__ __forceinline__ void rope_pair(float a, float b, float c, float s, float& xr, float& yr) {
+  xr = __fmaf_rn(a, c, -__fmul_rn(b, s));
+  yr = __fmaf_rn(a, s, __fmul_rn(b, c));
+}
+
 // ---- dtype dispatch -------------------------------------------------------
 #define CCB_DISPATCH_DTYPE(dtype, T, ...)                         \
   [&]() -> int {                                                  \

@@ -18,6 +18,9 @@ int gemm_tc_bf16(const void* A, int64_t lda, const void* B, int64_t ldb, void* C
                  int epi, bool allow_split, cudaStream_t st);
 int gemm_simt(const void* A, int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc, int M, int N, int K,
               int epi, int dtype, cudaStream_t st);
+int gemm_qkv_rope_bf16(const void* X, int64_t ldx, const void* Wqkv, int64_t ldw, int M, int K, int Hq, int Hkv,
+                       int d_head, const int32_t* row_slot, const int32_t* row_pos, const void* table, void* q_rot,
+                       void* kv_k, void* kv_v, void* k_rot, cudaStream_t st);
 bool gemv_eligible(int M, int N, int K, int epi, const void* A, int64_t lda, const void* W, int64_t ldw);
 int gemv_bf16(const void* A, int64_t lda, const void* W, int64_t ldw, void* C, int64_t ldc, int M, int N, int K,
               int epi, cudaStream_t st);

@@ -120,3 +120,32 @@ extern "C" int cc_gemm(const void* A, int64_t lda, const void* B, int64_t ldb, v
   if (impl == 1 || impl == 4) return fail(CC_E_UNSUP, "gemm: tcgen05 kernel requires bf16");
   return gemm_simt(A, lda, B, ldb, C, ldc, M, N, K, epilogue, dtype, st);
 }
+
+extern "C" int cc_rope_scatter_qkv(const void* qkv, int64_t ld_qkv, int n_rows, const int32_t* row_slot,
+                                   const int32_t* row_pos, const void* rope_table, void* q_rot, void* kv_k, void* kv_v,
+                                   void* k_rot, int n_heads, int n_kv_heads, int d_head, int dtype, void* stream);
+
+extern "C" int cc_gemm_qkv_rope(const void* x, int64_t ldx, const void* w_qkv, int64_t ldw, int n_rows, int d,
+                                const int32_t* row_slot, const int32_t* row_pos, const void* rope_table, void* q_rot,
+                                void* kv_k, void* kv_v, void* k_rot, void* qkv_scratch, int n_heads, int n_kv_heads,
+                                int d_head, int dtype, void* stream) {
+  using namespace ccb;
+  CCB_REQUIRE(n_rows >= 0 && d > 0 && n_heads > 0 && n_kv_heads > 0 && d_head > 0, "gemm_qkv_rope: bad shape");
+  if (n_rows == 0) return 0;
+  const int N = (n_heads + 2 * n_kv_heads) * d_head;
+  if (dtype == CC_BF16) {
+    const int rc = gemm_qkv_rope_bf16(x, ldx, w_qkv, ldw, n_rows, d, n_heads, n_kv_heads, d_head, row_slot, row_pos,
+                                      rope_table, q_rot, kv_k, kv_v, k_rot, as_stream(stream));
+    if (rc != CC_E_UNSUP) return rc;
+  }
+  // composition: the same GEMM into the qkv rows, then the RoPE / scatter pass
+  // (bit-identical to the fused epilogue in bf16)
+  CCB_REQUIRE(qkv_scratch != nullptr, "gemm_qkv_rope: shape needs the qkv scratch rows");
+  // (bf16, >= 64 rows: no K split, like the fused kernel -- a row's result
+  // does not depend on which of the two runs)
+  const int impl = dtype == CC_BF16 && n_rows >= 64 ? 4 : 0;
+  int rc = cc_gemm(x, ldx, w_qkv, ldw, qkv_scratch, N, n_rows, N, d, CC_EPI_STORE, dtype, impl, stream);
+  if (rc) return rc;
+  return cc_rope_scatter_qkv(qkv_scratch, N, n_rows, row_slot, row_pos, rope_table, q_rot, kv_k, kv_v, k_rot, n_heads,
+                             n_kv_heads, d_head, dtype, stream);
+}

@@ -533,12 +533,32 @@ constexpr int P2_B_BYTES = 128 * TC_BK * 2;        // <= 128 activation rows per
 // features, fp32 or bf16) drained by TMA stores / reduce-adds
 constexpr size_t P2_SMEM = 1024 + P2_STAGES * (TC_A_BYTES + P2_B_BYTES) + 256 + 8 * 4096;
 
+// QKV projection with RoPE and the K/V scatter in the epilogue (K3,
+// model.py:399-404): the 128 features of a CTA are one head (d_head 128) of
+// [q heads | k heads | v heads]; warps q and q ^ 2 hold the RoPE partners
+// (features i and i + 64) and swap their chunks through shared memory, so
+// each warp rotates its own 32 features for all 32 rows of a chunk.  q ->
+// q_rot[row] (32 x 32 TMA stores); k -> kv_k[slot] (as computed) and
+// k_rot[slot] (rotated); v -> kv_v[slot] (64-byte row segments).  Each value is rounded to bf16
+// before the rotation, so the results equal the unfused GEMM + rope_scatter.
+constexpr int EPI_ROPE_QKV = 5;  // (internal epilogue id, not part of the ABI enum)
+struct RopeQkv {
+  const int32_t* row_slot;
+  const int32_t* row_pos;
+  const float2* table;  // [max_pos][64] (cos, sin)
+  __nv_bfloat16* q_rot;
+  __nv_bfloat16* kv_k;
+  __nv_bfloat16* kv_v;
+  __nv_bfloat16* k_rot;
+  int Hq, Hkv;
+};
+
 template <int EPI>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
     gemm_pair_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX128,
                      const __grid_constant__ CUtensorMap tmX64, const __grid_constant__ CUtensorMap tmX32,
                      const __grid_constant__ CUtensorMap tmX16, const __grid_constant__ CUtensorMap tmC, int M,
-                     int K, int dbg, const __grid_constant__ SwTab tab) {
+                     int K, int dbg, const __grid_constant__ SwTab tab, const RopeQkv rq) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = base;
@@ -666,6 +686,112 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t t0 = tmem_base + acc * 256 + ((uint32_t)(q * 32) << 16);
+      if constexpr (EPI == EPI_ROPE_QKV) {
+        // warp slab (8 KiB): [0, 4K) this warp's fp32 chunk for the partner,
+        // [4K, 6K) / [6K, 8K) bf16 [32 rows][32 features] output staging.
+        // (Loading the next chunk's cos/sin during the current one measured
+        // slower: 61.1 vs 57.8 us at M = 802.)
+        const int kvw = rq.Hkv * 128;
+        const int kind = ft < rq.Hq ? 0 : ft < rq.Hq + rq.Hkv ? 1 : 2;  // q / k / v head
+        const int i = (q & 1) * 32 + lane;  // RoPE pair index (features i, i + 64)
+        const int nch = min((n + 31) / 32, (M - r0 + 31) / 32);
+        const uint32_t xo = smem_u32(my_slab), xi = smem_u32(stg_base + (q ^ 2) * 8192);
+        float2 cs[32];
+        int slot_c;
+        auto meta = [&](int c, float2 (&cc)[32], int& slot) {
+          const int row = r0 + c * 32, jmax = min(32, M - row);
+          slot = (kind > 0 && lane < jmax) ? rq.row_slot[row + lane] : 0;
+          if (kind < 2) {
+            const int pos = lane < jmax ? rq.row_pos[row + lane] : 0;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) cc[j] = rq.table[(int64_t)__shfl_sync(0xffffffffu, pos, j) * 64 + i];
+          }
+        };
+#pragma unroll 1
+        for (int c = 0; c < nch; ++c) {
+          const int row = r0 + c * 32, jmax = min(32, M - row);
+          uint32_t r[32];
+          tmem_ld32(t0 + c * 32, r);
+          meta(c, cs, slot_c);
+          tmem_ld_wait();
+          if (dbg & 1) continue;  // debug: no stores
+          // q heads alternate the two staging slabs (a chunk's TMA store drains
+          // while the next is written); k / v heads use both, read back here
+          const uint32_t ob0 = xo + 4096 + (kind == 0 ? (nst & 1) * 2048 : 0), ob1 = xo + 6144;
+          if (lane == 0) {
+            if (kind == 0) bulk_wait_read<1>();  // the store that last read this slab is done reading
+            else bulk_wait_read<0>();
+          }
+          __syncwarp();
+          if (kind < 2) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              asm volatile("st.shared.b32 [%0], %1;" ::"r"(xo + (j * 32 + lane) * 4), "r"(r[j]) : "memory");
+            pair_bar(q);
+            const bool xw = q < 2;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              float other;
+              asm volatile("ld.shared.f32 %0, [%1];" : "=f"(other) : "r"(xi + (j * 32 + lane) * 4) : "memory");
+              const __nv_bfloat16 ob = __float2bfloat16_rn(__uint_as_float(r[j]));
+              const float mine = __bfloat162float(ob), oth = __bfloat162float(__float2bfloat16_rn(other));
+              const float2 csj = cs[j];
+              float fx, fy;
+              rope_pair(xw ? mine : oth, xw ? oth : mine, csj.x, csj.y, fx, fy);
+              const __nv_bfloat16 rb = __float2bfloat16_rn(xw ? fx : fy);
+              if (kind == 0) {
+                asm volatile("st.shared.b16 [%0], %1;" ::"r"(ob0 + j * 64 + lane * 2),
+                             "h"(*reinterpret_cast<const uint16_t*>(&rb)) : "memory");
+              } else {
+                asm volatile("st.shared.b16 [%0], %1;" ::"r"(ob0 + j * 64 + lane * 2),
+                             "h"(*reinterpret_cast<const uint16_t*>(&ob)) : "memory");
+                asm volatile("st.shared.b16 [%0], %1;" ::"r"(ob1 + j * 64 + lane * 2),
+                             "h"(*reinterpret_cast<const uint16_t*>(&rb)) : "memory");
+              }
+            }
+            pair_bar(q);  // both warps have read the other's chunk
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const __nv_bfloat16 ob = __float2bfloat16_rn(__uint_as_float(r[j]));
+              asm volatile("st.shared.b16 [%0], %1;" ::"r"(ob0 + j * 64 + lane * 2),
+                           "h"(*reinterpret_cast<const uint16_t*>(&ob)) : "memory");
+            }
+          }
+          if (kind == 0) {  // q rows are contiguous: one TMA store of the 32 x 32 block
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_2d(&tmC, my_slab + 4096 + (nst & 1) * 2048, ft * TC_BM + q * 32, row);
+              bulk_commit();
+            }
+            ++nst;
+          } else {
+            // k / v rows go to their slots: two 64-byte rows per warp store
+            __syncwarp();
+            const int half = lane >> 4, c4 = lane & 15;
+            const int64_t col = (int64_t)(ft - rq.Hq - (kind == 2 ? rq.Hkv : 0)) * 128 + q * 32 + c4 * 2;
+            const int my_slot = slot_c;
+#pragma unroll 4
+            for (int it = 0; it < 16; ++it) {
+              const int rr = it * 2 + half;
+              const int sl = __shfl_sync(0xffffffffu, my_slot, rr);
+              if (rr >= jmax) continue;
+              uint32_t v0, v1 = 0;
+              asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v0) : "r"(ob0 + rr * 64 + c4 * 4) : "memory");
+              if (kind == 1)
+                asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v1) : "r"(ob1 + rr * 64 + c4 * 4) : "memory");
+              const int64_t o = (int64_t)sl * kvw + col;
+              if (kind == 1) {
+                *reinterpret_cast<uint32_t*>(rq.kv_k + o) = v0;
+                *reinterpret_cast<uint32_t*>(rq.k_rot + o) = v1;
+              } else {
+                *reinterpret_cast<uint32_t*>(rq.kv_v + o) = v0;
+              }
+            }
+          }
+        }
+      } else
 #pragma unroll 1
       for (int c = 0; c * 32 < n; ++c) {
         const int row = r0 + c * 32;
@@ -1163,7 +1289,7 @@ int launch_epi(const void* A, int64_t lda, const void* B, int64_t ldb, void* C, 
     if (int rc2 = ensure_smem(gemm_pair_kernel<EPI>, P2_SMEM)) return rc2;
     static const int dbg = getenv("CCB_PAIR_DBG") ? atoi(getenv("CCB_PAIR_DBG")) : 0;
     return launch_k(gemm_pair_kernel<EPI>, dim3(tl.grid), dim3(TC_THREADS), P2_SMEM, st, "gemm_pair", mw, mx[0], mx[1],
-                    mx[2], mx[3], mc, M, K, dbg, tl.tab->tab);
+                    mx[2], mx[3], mc, M, K, dbg, tl.tab->tab, RopeQkv{});
   }
   if constexpr (EPI != CC_EPI_SWIGLU) if (tl.swap) {
     // A slot <- weights B [N][K] (128-row boxes), B slot <- activations A [M][K]
@@ -1200,6 +1326,43 @@ int launch_epi(const void* A, int64_t lda, const void* B, int64_t ldb, void* C, 
 }  // namespace
 
 void gemm_tc_set_trace(void* p) { g_trace = reinterpret_cast<long long*>(p); }
+
+// QKV projection + RoPE + K/V scatter in one CTA-pair GEMM (see RopeQkv).
+// CC_E_UNSUP for shapes the fused epilogue does not cover (d_head != 128,
+// N not a multiple of 256, M > 8192): the caller then runs the GEMM and
+// rope_scatter separately.
+int gemm_qkv_rope_bf16(const void* X, int64_t ldx, const void* Wqkv, int64_t ldw, int M, int K, int Hq, int Hkv,
+                       int d_head, const int32_t* row_slot, const int32_t* row_pos, const void* table, void* q_rot,
+                       void* kv_k, void* kv_v, void* k_rot, cudaStream_t st) {
+  const int N = (Hq + 2 * Hkv) * d_head;
+  // The epilogue re-reads a row's cos/sin once per head (40x the table
+  // traffic of rope_scatter at Llama-3-8B widths) and the last unit's
+  // epilogue is exposed: measured (qkv_rope_ab.py, us, fused vs GEMM +
+  // rope_scatter) M = 290: 37.4 vs 51.7, 802: 57.8 vs 48.4, 1570: 86.6 vs
+  // 74.3, 5152: 208 vs 198 -- so the fused kernel runs for short activation
+  // matrices only (M <= CCB_QKV_FUSE_MAX, default 512).
+  static const int fuse_max = getenv("CCB_QKV_FUSE_MAX") ? atoi(getenv("CCB_QKV_FUSE_MAX")) : 512;
+  if (d_head != 128 || N % (2 * TC_BM) || M < 64 || M > fuse_max || M > 8192 || K % TC_BK || ldx % 8 || ldw % 8 ||
+      !pair_enabled())
+    return fail(CC_E_UNSUP, "gemm_qkv_rope: shape not covered by the fused epilogue");
+  if ((reinterpret_cast<uintptr_t>(X) | reinterpret_cast<uintptr_t>(Wqkv)) & 15)
+    return fail(CC_E_UNSUP, "gemm_qkv_rope: pointers must be 16-byte aligned");
+  const TabPlan* tp = plan_units(M, N, K);
+  if (!tp) return fail(CC_E_UNSUP, "gemm_qkv_rope: no unit plan");
+  CUtensorMap mw, mx[4];
+  int rc = make_map(&mw, Wqkv, N, K, ldw, TC_BM);
+  for (int i = 0; i < 4 && !rc; ++i) rc = make_map(&mx[i], X, M, K, ldx, 128 >> i);
+  if (rc) return rc;
+  CUtensorMap mq;  // q_rot [M][Hq * 128] bf16, 32 x 32 store boxes
+  rc = make_map(&mq, q_rot, M, (int64_t)Hq * 128, (int64_t)Hq * 128, -1);
+  if (rc) return rc;
+  if (int rc2 = ensure_smem(gemm_pair_kernel<EPI_ROPE_QKV>, P2_SMEM)) return rc2;
+  RopeQkv rq{row_slot, row_pos, reinterpret_cast<const float2*>(table), (__nv_bfloat16*)q_rot, (__nv_bfloat16*)kv_k,
+             (__nv_bfloat16*)kv_v, (__nv_bfloat16*)k_rot, Hq, Hkv};
+  static const int dbg = getenv("CCB_PAIR_DBG") ? atoi(getenv("CCB_PAIR_DBG")) : 0;
+  return launch_k(gemm_pair_kernel<EPI_ROPE_QKV>, dim3(tp->grid), dim3(TC_THREADS), P2_SMEM, st, "gemm_qkv_rope", mw,
+                  mx[0], mx[1], mx[2], mx[3], mq, M, K, dbg, tp->tab, rq);
+}
 
 // o_proj / down_proj of a tensor-parallel rank with the reduce-scatter fused
 // into the epilogue (data-parallel schedule; BN must divide the owner slice)

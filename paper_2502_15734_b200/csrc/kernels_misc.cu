@@ -191,8 +191,10 @@ __global__ void __launch_bounds__(1024) rope_scatter_kernel(
         xr.v[e] = from_d<T>(a * c - b * s);
         yr.v[e] = from_d<T>(a * s + b * c);
       } else {
-        xr.v[e] = from_f<T>(a * c - b * s);
-        yr.v[e] = from_f<T>(a * s + b * c);
+        float fx, fy;
+        rope_pair(a, b, c, s, fx, fy);
+        xr.v[e] = from_f<T>(fx);
+        yr.v[e] = from_f<T>(fy);
       }
     }
     if (is_q) {

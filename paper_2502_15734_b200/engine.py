@@ -478,13 +478,20 @@ def _execute(model: Model, plan: DevicePlan, ws: dict, *, record=False, record_v
             continue
         with tm.span("rmsnorm", nbytes=n_l * d * (4 + esz)):
             N.call("cc_rmsnorm", P(hidden), P(xn), P(lw.get("attn_norm")), n_l, d, eps, dt, s)
-        with tm.span("gemm", flops=2.0 * n_l * (qw + 2 * kvw) * d):
-            N.call("cc_gemm", P(xn), d, P(lw["w_qkv"]), d, P(qkv), qw + 2 * kvw, n_l, qw + 2 * kvw, d, N.EPI_STORE,
-                   dt, gemm_impl, s)
-        # algorithmic bytes: read the qkv row, write q_rot and k, k_rot, v at the row slots
-        with tm.span("rope_scatter", nbytes=n_l * (qw + 2 * kvw + qw + 3 * kvw) * esz):
-            N.call("cc_rope_scatter_qkv", P(qkv), qw + 2 * kvw, n_l, P(D["row_slot"]), P(D["row_pos"]), P(rope),
-                   P(q_rot), P(kv_k[l]), P(kv_v[l]), P(k_rot[l]), H, Hkv, dh, dt, s)
+        if gemm_impl == 0:
+            # QKV GEMM with RoPE and the K/V scatter in its epilogue (K3; bf16
+            # shapes it covers, else the same GEMM + rope_scatter, bit-identical)
+            with tm.span("gemm", flops=2.0 * n_l * (qw + 2 * kvw) * d):
+                N.call("cc_gemm_qkv_rope", P(xn), d, P(lw["w_qkv"]), d, n_l, d, P(D["row_slot"]), P(D["row_pos"]),
+                       P(rope), P(q_rot), P(kv_k[l]), P(kv_v[l]), P(k_rot[l]), P(qkv), H, Hkv, dh, dt, s)
+        else:
+            with tm.span("gemm", flops=2.0 * n_l * (qw + 2 * kvw) * d):
+                N.call("cc_gemm", P(xn), d, P(lw["w_qkv"]), d, P(qkv), qw + 2 * kvw, n_l, qw + 2 * kvw, d,
+                       N.EPI_STORE, dt, gemm_impl, s)
+            # algorithmic bytes: read the qkv row, write q_rot and k, k_rot, v at the row slots
+            with tm.span("rope_scatter", nbytes=n_l * (qw + 2 * kvw + qw + 3 * kvw) * esz):
+                N.call("cc_rope_scatter_qkv", P(qkv), qw + 2 * kvw, n_l, P(D["row_slot"]), P(D["row_pos"]), P(rope),
+                       P(q_rot), P(kv_k[l]), P(kv_v[l]), P(k_rot[l]), H, Hkv, dh, dt, s)
         if preload is not None:
             preload.gather(model, plan, ws, l, rope, s)
         if l2pf is not None:  # o_proj weights -> L2 while attention runs (it reads K/V from L2 only)

@@ -464,3 +464,58 @@ def test_topk_select_long_chunks_radix_path(N, n):
     got = select_tokens_batched([short, s], [recompute_count(300, 0.2), recompute_count(n, 0.2)])
     np.testing.assert_array_equal(got[0], np.sort(np.lexsort((np.arange(300), -short))[:60]))
     np.testing.assert_array_equal(got[1], np.sort(np.lexsort((np.arange(n), -s))[:recompute_count(n, 0.2)]))
+
+
+@pytest.mark.parametrize("M,Hq,Hkv,d,n_slots", [(802, 32, 8, 4096, 5152), (400, 32, 8, 4096, 5152), (150, 8, 2, 512, 700),
+                                                 (300, 8, 1, 1024, 900), (40, 8, 2, 512, 300)])
+def test_gemm_qkv_rope_fused_matches_unfused(N, M, Hq, Hkv, d, n_slots):
+    """K3: the QKV GEMM with RoPE + K/V scatter in its CTA-pair epilogue
+    (cc_gemm_qkv_rope) gives the same bits as the GEMM followed by
+    cc_rope_scatter_qkv, and matches a torch fp32 reference within bf16.
+    M = 40 and 802 are outside the fused kernel's range (64..512 rows): the
+    GEMM + rope_scatter composition runs there."""
+    dh = 128
+    g = torch.Generator(device="cuda").manual_seed(M + Hq)
+    NQ = (Hq + 2 * Hkv) * dh
+    x = (torch.randn((M, d), generator=g, device="cuda") * 0.5).bfloat16()
+    w = (torch.randn((NQ, d), generator=g, device="cuda") / d ** 0.5).bfloat16()
+    slots = torch.sort(torch.randperm(n_slots, generator=g, device="cuda")[:M]).values.int().contiguous()
+    pos = (slots + 7).int().contiguous()
+    inv = 1.0 / (500000.0 ** (torch.arange(0, dh // 2, dtype=torch.float64) * 2 / dh))
+    ang = torch.arange(n_slots + 8, dtype=torch.float64)[:, None] * inv[None, :]
+    table = torch.stack([torch.cos(ang), torch.sin(ang)], dim=-1).float().cuda().contiguous()
+    kvw = Hkv * dh
+
+    def bufs():
+        return (torch.zeros((M, Hq * dh), dtype=torch.bfloat16, device="cuda"),
+                *[torch.zeros((n_slots, kvw), dtype=torch.bfloat16, device="cuda") for _ in range(3)])
+
+    fq, fk, fv, fkr = bufs()
+    qkv = torch.empty((M, NQ), dtype=torch.bfloat16, device="cuda")
+    N.call("cc_gemm_qkv_rope", N.ptr(x), d, N.ptr(w), d, M, d, N.ptr(slots), N.ptr(pos), N.ptr(table), N.ptr(fq),
+           N.ptr(fk), N.ptr(fv), N.ptr(fkr), N.ptr(qkv), Hq, Hkv, dh, N.BF16, N.stream_ptr())
+    uq, uk, uv, ukr = bufs()
+    # (impl 4: no K split, as the fused kernel; below its range the composition runs impl 0)
+    N.call("cc_gemm", N.ptr(x), d, N.ptr(w), d, N.ptr(qkv), NQ, M, NQ, d, N.EPI_STORE, N.BF16, 4 if M >= 64 else 0,
+           N.stream_ptr())
+    N.call("cc_rope_scatter_qkv", N.ptr(qkv), NQ, M, N.ptr(slots), N.ptr(pos), N.ptr(table), N.ptr(uq), N.ptr(uk),
+           N.ptr(uv), N.ptr(ukr), Hq, Hkv, dh, N.BF16, N.stream_ptr())
+    torch.cuda.synchronize()
+    for a, b in ((fq, uq), (fk, uk), (fv, uv), (fkr, ukr)):
+        assert torch.equal(a, b)
+    # torch fp32 reference (rotate-half RoPE at pos)
+    ref = x.float() @ w.float().T
+    cs = table[pos.long()]  # [M][64][2]
+
+    def rot(t):  # t [M][h][128]
+        a, b = t[..., :64], t[..., 64:]
+        c, s = cs[:, None, :, 0], cs[:, None, :, 1]
+        return torch.cat([a * c - b * s, a * s + b * c], dim=-1)
+
+    q = rot(ref[:, : Hq * dh].view(M, Hq, dh)).reshape(M, -1)
+    k = ref[:, Hq * dh: Hq * dh + kvw]
+    kr = rot(k.view(M, Hkv, dh)).reshape(M, -1)
+    v = ref[:, Hq * dh + kvw:]
+    sl = slots.long()
+    for got, want in ((fq, q), (fk[sl], k), (fkr[sl], kr), (fv[sl], v)):
+        torch.testing.assert_close(got.float(), want, atol=2e-2, rtol=2e-2)

@@ -22,7 +22,7 @@ def declared_symbols():
 
 def test_header_declares_the_path():
     names = declared_symbols()
-    for must in ("cc_gather_rope_kv", "cc_gemm", "cc_attention", "cc_segment_mass", "cc_chunk_stats",
+    for must in ("cc_gather_rope_kv", "cc_gemm", "cc_gemm_qkv_rope", "cc_attention", "cc_segment_mass", "cc_chunk_stats",
                  "cc_topk_select", "cc_logits_argmax", "cc_extract_to_pool", "cc_rope_apply_f64"):
         assert must in names
 
