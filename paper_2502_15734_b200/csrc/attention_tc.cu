@@ -1455,7 +1455,11 @@ struct Pp {
   static_assert(2 * BN + 2 * DH <= TMEM_COLS, "TMEM budget");
 };
 
-template <int DH>
+// PF: exponentials per 8 key pairs computed as a polynomial on the FMA pipe
+// (A/B at config 2 / full / 32k / 70B rank, us: PF 2 63.9 / 221 / 1153 / 150,
+// PF 0 -- / 258 / 1585 / 181, PF 1 -- / 226 / 1280 / 154, PF 4 -- / 235 /
+// 1350 / 162)
+template <int DH, int PF = 2>
 __global__ void __launch_bounds__(384, 1)
     attn_pp_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                    const __grid_constant__ CUtensorMap tmV, const int32_t* __restrict__ q_slot,
@@ -1741,7 +1745,7 @@ __global__ void __launch_bounds__(384, 1)
           const int e = hh * (BN / 4) + e2;
           const uint64_t x2 = ffma2(f2_pack(s[2 * e], s[2 * e + 1]), sl2, nb2);
           uint64_t p2;
-          if ((e & 7) >= 6) {  // a quarter of the exponentials on the FMA pipe
+          if ((e & 7) >= 8 - PF) {  // PF / 8 of the exponentials on the FMA pipe
             p2 = ex2_poly2(x2);
           } else {
             float x0, x1;
@@ -1921,6 +1925,560 @@ __global__ void __launch_bounds__(384, 1)
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc<SM::TMEM_COLS>(tmem);
+  }
+}
+
+// ---- CTA-pair attention: cta_group::2 MMAs over four Q tiles per pair ---------
+//
+// A cluster of two CTAs (an SM pair) takes one work item: GQA group g, a
+// block of 4R query rows (each CTA: 2 Q tiles of 128 M-rows), a part of the
+// block's causal key range.  Every MMA is a pair MMA with M = 256 (the two
+// CTAs' Q tiles X): S_X = Q_X K^T (N = 64 keys: each CTA stages 32 of the
+// keys) and O_X += P_X V (N = 128 head columns: each CTA stages 64 of them, P
+// from each CTA's TMEM), issued by the leader CTA.  So an SM stages half of
+// each 64-key K/V tile and its shared-memory traffic per 64-key step is
+// S 80 KiB + PV 16 KiB + TMA 16 KiB -- below the port's ~128 B/clk at the
+// tensor pipe's 1024 cycles; the one-CTA ping-pong kernel needs a 128-key
+// S buffer per Q tile and serialises each softmax with its PV and next S.
+//   warp 0      TMA (both CTAs): Q tiles once, K halves (32 keys x 128
+//               columns) two tiles ahead of V halves (64 keys x 64 columns),
+//               6-deep rings; completion on the leader's barriers
+//   warp 1      leader only: MMA issuer.  Per Q tile X: S_X(0), S_X(1), then
+//               per 64-key tile j: PV_X(j), S_X(j+2) into the S buffer PV_X(j)
+//               just read -- S runs two tiles ahead, so both softmax
+//               warpgroups work back to back and concurrently
+//   warps 4-11  softmax of Q tile 0 / 1 (thread = M-row, 64 keys per tile,
+//               arithmetic as attn_pp_kernel), P over the second half of its
+//               S buffer; each warp releases P to the leader's p_full
+// TMEM per CTA: S_{X,b} at X 128 + b 64 (b = tile parity), O_X at 256 + X 128.
+template <int DH>
+struct Pr {
+  static constexpr int BN = 64;
+  static constexpr int KST = 6, VST = 6;
+  static constexpr int THREADS = 384;
+  static constexpr int Q_BYTES = 128 * DH * 2;    // one Q tile (128 M-rows)
+  static constexpr int K_HALF = 32 * DH * 2;      // 32 keys x DH columns
+  static constexpr int V_HALF = BN * (DH / 2) * 2;  // 64 keys x DH/2 columns
+  static constexpr int Q_OFF = 0;
+  static constexpr int K_OFF = 2 * Q_BYTES;
+  static constexpr int V_OFF = K_OFF + KST * K_HALF;
+  static constexpr int BAR_OFF = V_OFF + VST * V_HALF;
+  static constexpr int PLAN_OFF = BAR_OFF + 1024;
+  static constexpr size_t TOTAL = PLAN_OFF + 3 * AT_MAXT * 4;
+  static constexpr int TMEM_COLS = 512;
+  static_assert(DH == 128, "pair kernel: d_head 128");
+  static_assert(4 * BN + 2 * DH <= TMEM_COLS, "TMEM budget");
+};
+
+template <int DH>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
+    attn_pair_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                     const __grid_constant__ CUtensorMap tmV, const int32_t* __restrict__ q_slot,
+                     const uint8_t* __restrict__ key_pad, __nv_bfloat16* __restrict__ ctx, float* __restrict__ lse,
+                     int n_q, int n_keys, int Hq, int G, float scale_log2, int n_groups, int n_blocks, int target,
+                     int max_parts, float* __restrict__ ws_o, float2* __restrict__ ws_ml, int* __restrict__ counters,
+                     long long* __restrict__ trace, int exp) {
+  using SM = Pr<DH>;
+  constexpr int BN = SM::BN, KST = SM::KST, VST = SM::VST, NT = SM::THREADS;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* base = smem_raw;
+  if (smem_u32(smem_raw) & 1023) __trap();
+  uint8_t* sQ = base + SM::Q_OFF;
+  uint8_t* sK = base + SM::K_OFF;
+  uint8_t* sV = base + SM::V_OFF;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(base + SM::BAR_OFF);
+  uint64_t* q_full = bars + 0;        // leader: both CTAs' Q tiles
+  uint64_t* k_full = bars + 1;        // [KST] leader: both K halves
+  uint64_t* k_empty = k_full + KST;   // [KST] (both CTAs, multicast commit)
+  uint64_t* v_full = k_empty + KST;   // [VST] leader
+  uint64_t* v_empty = v_full + VST;   // [VST] both
+  uint64_t* s_full = v_empty + VST;   // [2 Q tiles][2 S buffers] both
+  uint64_t* p_full = s_full + 4;      // [2][2] leader: 4 softmax warps x 2 CTAs
+  uint64_t* pv_done = p_full + 4;     // [2] both: one phase per PV of the Q tile
+  uint64_t* o_done = pv_done + 2;     // [2] both: last PV completed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 2);
+  int* s_kmax = reinterpret_cast<int*>(tmem_slot + 1);  // [2]
+  int* s_item = s_kmax + 2;                             // group, block, part, parts, est
+  int* s_flag = s_item + 5;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const int R = 128 / G;  // query rows per Q tile
+  const int RB = 4 * R;   // query rows per pair block
+  const int T = n_blocks;
+  const int item_id = (int)blockIdx.x >> 1;  // one item per cluster
+  pdl_trigger();
+  pdl_wait();
+  if (max_parts > 1) {
+    // items (group, block, key part), longest first -- see attn_tc_kernel
+    int* p_len = reinterpret_cast<int*>(base + SM::PLAN_OFF);
+    int* p_parts = p_len + AT_MAXT;
+    int* p_order = p_parts + AT_MAXT;
+    for (int t = threadIdx.x; t < T; t += NT) {
+      const int kq = q_slot[min((t + 1) * RB, n_q) - 1];
+      const int est = kq < 0 ? 0 : min(kq, n_keys - 1) / BN + 1;
+      const int parts = max(1, min(max_parts, (est + target - 1) / target));
+      p_parts[t] = parts;
+      p_len[t] = (est + parts - 1) / parts;
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < T; t += NT) {
+      const int lt = p_len[t];
+      int rk = 0;
+      for (int u = 0; u < T; ++u) rk += (p_len[u] > lt || (p_len[u] == lt && u > t)) ? 1 : 0;
+      p_order[rk] = t;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int idx = item_id;
+      s_item[0] = -1;
+      for (int r = 0; r < T; ++r) {
+        const int t = p_order[r], c = n_groups * p_parts[t];
+        if (idx < c) {
+          s_item[0] = idx % n_groups;
+          s_item[1] = t;
+          s_item[2] = idx / n_groups;
+          s_item[3] = p_parts[t];
+          s_item[4] = p_len[t] * p_parts[t];
+          break;
+        }
+        idx -= c;
+      }
+    }
+  } else if (threadIdx.x == 0) {
+    s_item[0] = item_id % n_groups;
+    s_item[1] = T - 1 - item_id / n_groups;
+    s_item[2] = 0;
+    s_item[3] = 1;
+    s_item[4] = 0;
+  }
+  __syncthreads();
+  const int g = s_item[0];
+  if (g < 0) return;  // (both CTAs of the cluster: same item)
+  const int blk = s_item[1], part = s_item[2], parts = s_item[3], est = s_item[4];
+  const int row0 = blk * RB;
+
+  if (threadIdx.x < 2) s_kmax[threadIdx.x] = -1;
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmQ);
+    tma_prefetch(&tmK);
+    tma_prefetch(&tmV);
+    mbar_init(q_full, 1);
+    for (int s = 0; s < KST; ++s) {
+      mbar_init(&k_full[s], 1);
+      mbar_init(&k_empty[s], 1);
+    }
+    for (int s = 0; s < VST; ++s) {
+      mbar_init(&v_full[s], 1);
+      mbar_init(&v_empty[s], 1);
+    }
+    for (int i = 0; i < 4; ++i) {
+      mbar_init(&s_full[i], 1);
+      mbar_init(&p_full[i], 8);
+    }
+    for (int x = 0; x < 2; ++x) {
+      mbar_init(&pv_done[x], 1);
+      mbar_init(&o_done[x], 1);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc_pair<SM::TMEM_COLS>(tmem_slot);
+  __syncthreads();
+  // causal key range of Q tile X over both CTAs' rows (pair MMAs share it):
+  // row0 + t, t = rank' 2R + X R + i
+  if (threadIdx.x < RB) {
+    const int r = row0 + threadIdx.x;
+    if (r < n_q) atomicMax(&s_kmax[(threadIdx.x % (2 * R)) / R], min(q_slot[r], n_keys - 1));
+  }
+  tc_fence_before();
+  cluster_sync();  // barriers of both CTAs initialised, TMEM allocated, key ranges known
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int ntot0 = s_kmax[0] < 0 ? 0 : s_kmax[0] / BN + 1;
+  const int ntot1 = s_kmax[1] < 0 ? 0 : s_kmax[1] / BN + 1;
+  const int ntot = max(ntot0, ntot1);
+  const bool split = parts > 1;
+  const int t0 = split ? min(part * est / parts, ntot) : 0;
+  const int t1 = !split || part == parts - 1 ? ntot : min((part + 1) * est / parts, ntot);
+  const int n0 = max(0, min(t1, ntot0) - t0), n1 = max(0, min(t1, ntot1) - t0);
+  const int nmax = max(n0, n1);
+  const bool tracing = trace != nullptr;
+  long long tr_a = 0, tr_b = 0, tr_c = 0;
+  long long t_begin = 0;
+  if (tracing && threadIdx.x == 128) asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_begin));
+
+  if (warp == 0) {
+    if (lane == 0 && nmax > 0) {
+      const uint32_t qb = mapa_shared(smem_u32(q_full), 0);
+      if (rank == 0) mbar_expect_tx(q_full, 4 * SM::Q_BYTES);
+#pragma unroll
+      for (int x = 0; x < 2; ++x)
+#pragma unroll
+        for (int a = 0; a < DH / 64; ++a)
+          tma_load_3d_pair(sQ + x * SM::Q_BYTES + a * 128 * 128, &tmQ, qb, a * 64, g * G,
+                           row0 + (int)rank * 2 * R + x * R);
+      int kc = 0, vc = 0;
+      auto load_k = [&](int t) {
+        const int ks = kc % KST;
+        twait(&k_empty[ks], ((kc / KST) & 1) ^ 1, tracing, tr_a);
+        ++kc;
+        if (rank == 0) mbar_expect_tx(&k_full[ks], 2 * SM::K_HALF);
+        const uint32_t kb = mapa_shared(smem_u32(&k_full[ks]), 0);
+#pragma unroll
+        for (int a = 0; a < DH / 64; ++a)
+          tma_load_2d_pair(sK + ks * SM::K_HALF + a * 32 * 128, &tmK, kb, g * DH + a * 64,
+                           (t0 + t) * BN + (int)rank * 32);
+      };
+      load_k(0);
+      if (nmax > 1) load_k(1);
+      for (int t = 0; t < nmax; ++t) {
+        const int vs = vc % VST;
+        twait(&v_empty[vs], ((vc / VST) & 1) ^ 1, tracing, tr_b);
+        ++vc;
+        if (rank == 0) mbar_expect_tx(&v_full[vs], 2 * SM::V_HALF);
+        tma_load_2d_pair(sV + vs * SM::V_HALF, &tmV, mapa_shared(smem_u32(&v_full[vs]), 0),
+                         g * DH + (int)rank * (DH / 2), (t0 + t) * BN);
+        if (t + 2 < nmax) load_k(t + 2);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0 && nmax > 0) {
+      constexpr uint32_t id_s = idesc_bf16(256, BN, false);
+      constexpr uint32_t id_o = idesc_bf16(256, DH, true);
+      const int nx[2] = {n0, n1};
+      int kc = 0, vc = 0;
+      auto issue_s = [&](int x, int b, int ks) {
+        if (!(exp & 2))  // (timing experiment 2: no MMAs)
+#pragma unroll
+        for (int kk = 0; kk < DH / 16; ++kk) {
+          const int a = kk >> 2, w = kk & 3;
+          const uint64_t bd = desc_sw128(sK + ks * SM::K_HALF + a * 32 * 128) + 2 * w;
+          const uint64_t ad = desc_sw128(sQ + x * SM::Q_BYTES + a * 128 * 128) + 2 * w;
+          mma_bf16_pair(tmem + x * 2 * BN + b * BN, ad, bd, id_s, kk > 0);
+        }
+        mma_commit_pair(&s_full[x * 2 + b], 0x3);
+      };
+      twait(q_full, 0, tracing, tr_b);
+      for (int t = 0; t < min(2, nmax); ++t) {
+        const int ks = kc % KST;
+        twait(&k_full[ks], (kc / KST) & 1, tracing, tr_b);
+        tc_fence_after();
+#pragma unroll
+        for (int x = 0; x < 2; ++x)
+          if (t < nx[x]) issue_s(x, t & 1, ks);
+        mma_commit_pair(&k_empty[ks], 0x3);
+        ++kc;
+      }
+      for (int j = 0; j < nmax; ++j) {
+        const int vs = vc % VST;
+        bool v_ready = false, k_ready = false;
+#pragma unroll
+        for (int x = 0; x < 2; ++x) {
+          if (j >= nx[x]) continue;
+          const int b = j & 1;
+          twait(&p_full[x * 2 + b], (j >> 1) & 1, tracing, tr_a);
+          if (!v_ready) {
+            twait(&v_full[vs], (vc / VST) & 1, tracing, tr_b);
+            v_ready = true;
+          }
+          tc_fence_after();
+          const uint32_t t_o = tmem + 4 * BN + x * DH, t_p = tmem + x * 2 * BN + b * BN + BN / 2;
+          if (!(exp & 2))
+#pragma unroll
+          for (int kk = 0; kk < BN / 16; ++kk) {
+            // B = this CTA's DH/2 head columns of V (MN-major, one 64-element atom)
+            const uint64_t bd = desc_sw128_mn(sV + vs * SM::V_HALF + kk * 16 * 128, BN * 128);
+            mma_bf16_ts_pair(t_o, t_p + kk * 8, bd, id_o, (j > 0 || kk > 0) ? 1u : 0u);
+          }
+          mma_commit_pair(&pv_done[x], 0x3);
+          if (j + 2 < nx[x]) {
+            if (!k_ready) {
+              twait(&k_full[kc % KST], (kc / KST) & 1, tracing, tr_b);
+              tc_fence_after();
+              k_ready = true;
+            }
+            issue_s(x, b, kc % KST);
+          }
+          if (j == nx[x] - 1) mma_commit_pair(&o_done[x], 0x3);
+        }
+        mma_commit_pair(&v_empty[vs], 0x3);
+        ++vc;
+        if (k_ready) {
+          mma_commit_pair(&k_empty[kc % KST], 0x3);
+          ++kc;
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    // ---- softmax of Q tile X: thread = M-row m, 64 keys per tile ------------
+    const int X = (warp - 4) >> 2;
+    const int q4 = warp & 3;  // TMEM lane quarter
+    const int m = q4 * 32 + lane;
+    const int row = row0 + (int)rank * 2 * R + X * R + m / G;
+    const int head = g * G + m % G;
+    const int lim = row < n_q ? min(q_slot[row], n_keys - 1) : -1;
+    const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
+    const uint32_t t_s0 = tmem + X * 2 * BN + lane_off, t_o = tmem + 4 * BN + X * DH + lane_off;
+    const int nX = X == 0 ? n0 : n1;
+    const uint64_t sl2 = f2_pack(scale_log2, scale_log2);
+    float m_run = -INFINITY, l_run = 0.f;
+    constexpr float kRescaleLog2 = 8.f;
+    for (int j = 0; j < nX; ++j) {
+      const int b = j & 1;
+      const uint32_t t_s = t_s0 + b * BN;
+      twait(&s_full[X * 2 + b], (j >> 1) & 1, tracing, tr_a);
+      if (exp & 1) {  // (timing experiment 1: no softmax work)
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&p_full[X * 2 + b]), 0));
+        continue;
+      }
+      const long long tb0 = tracing ? clock64() : 0;
+      tc_fence_after();
+      float s[BN];
+      tmem_ld32(t_s, *reinterpret_cast<uint32_t(*)[32]>(&s[0]));
+      tmem_ld32(t_s + 32, *reinterpret_cast<uint32_t(*)[32]>(&s[32]));
+      tmem_ld_wait();
+      const int j0 = (t0 + j) * BN;
+      const int lim_rel = lim - j0;
+      if (key_pad != nullptr) {
+#pragma unroll
+        for (int u = 0; u < BN / 16; ++u) {
+          uint4 w = make_uint4(0u, 0u, 0u, 0u);
+          const int kb = j0 + u * 16;
+          if (kb + 16 <= n_keys) {
+            w = __ldg(reinterpret_cast<const uint4*>(key_pad + kb));
+          } else {
+            uint8_t* wb = reinterpret_cast<uint8_t*>(&w);
+            for (int e = 0; e < 16; ++e) wb[e] = kb + e < n_keys ? key_pad[kb + e] : 1;
+          }
+          const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            const int c = u * 16 + e;
+            const bool padded = ((ww[e >> 2] >> (8 * (e & 3))) & 0xffu) != 0u;
+            s[c] = (c <= lim_rel && !padded) ? s[c] : -INFINITY;
+          }
+        }
+      } else if (lim_rel < BN - 1) {
+#pragma unroll
+        for (int c = 0; c < BN; ++c) s[c] = (c <= lim_rel) ? s[c] : -INFINITY;
+      }
+      float mx[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) mx[e] = fmax3(s[e], s[8 + 2 * e], s[9 + 2 * e]);
+#pragma unroll
+      for (int c = 24; c < BN; c += 16) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) mx[e] = fmax3(mx[e], s[c + 2 * e], s[c + 2 * e + 1]);
+      }
+      const float tmax = fmax3(fmax3(mx[0], mx[1], mx[2]), fmax3(mx[3], mx[4], mx[5]), fmaxf(mx[6], mx[7]));
+      bool grow = false;
+      float alpha = 1.f;
+      if (m_run == -INFINITY) {
+        m_run = tmax;
+      } else if ((tmax - m_run) * scale_log2 > kRescaleLog2) {
+        grow = true;
+        alpha = ex2_fast((m_run - tmax) * scale_log2);
+        l_run *= alpha;
+        m_run = tmax;
+      }
+      const float nb = (m_run == -INFINITY) ? 0.f : -m_run * scale_log2;
+      const uint64_t nb2 = f2_pack(nb, nb);
+      uint64_t acc[4] = {0ull, 0ull, 0ull, 0ull};
+      uint32_t pt[BN / 2];
+#pragma unroll
+      for (int e = 0; e < BN / 2; ++e) {
+        const uint64_t x2 = ffma2(f2_pack(s[2 * e], s[2 * e + 1]), sl2, nb2);
+        uint64_t p2;
+        if ((e & 7) >= 6) {  // a quarter of the exponentials on the FMA pipe
+          p2 = ex2_poly2(x2);
+        } else {
+          float x0, x1;
+          f2_unpack(x2, x0, x1);
+          p2 = f2_pack(ex2_fast(x0), ex2_fast(x1));
+        }
+        acc[e & 3] = fadd2(acc[e & 3], p2);
+        float p0, p1;
+        f2_unpack(p2, p0, p1);
+        __nv_bfloat162 hv = __floats2bfloat162_rn(p0, p1);
+        pt[e] = *reinterpret_cast<uint32_t*>(&hv);
+      }
+      tmem_st_cols<BN / 2>(t_s + BN / 2, pt);  // P over the second half of this S buffer (read above)
+      if (__any_sync(0xffffffffu, grow)) {
+        // O_X *= alpha once PV_X(j-1) has completed (phase j - 1 of pv_done;
+        // PV_X(j-2) completed before S_X(j) was issued: the parity is exact)
+        twait(&pv_done[X], (j - 1) & 1, tracing, tr_c);
+        tc_fence_after();
+        const uint64_t a2 = f2_pack(alpha, alpha);
+#pragma unroll 1
+        for (int c = 0; c < DH / 32; ++c) {
+          uint32_t r[32];
+          tmem_ld32(t_o + c * 32, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            float o0, o1;
+            f2_unpack(fmul2(f2_pack(__uint_as_float(r[2 * e]), __uint_as_float(r[2 * e + 1])), a2), o0, o1);
+            r[2 * e] = __float_as_uint(o0);
+            r[2 * e + 1] = __float_as_uint(o1);
+          }
+          tmem_st32(t_o + c * 32, r);
+        }
+      }
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&p_full[X * 2 + b]), 0));
+      if (tracing) tr_b += clock64() - tb0;
+      const uint64_t a01 = fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3]));
+      float sa, sb;
+      f2_unpack(a01, sa, sb);
+      l_run += sa + sb;
+    }
+    if (nX > 0) {
+      mbar_wait(&o_done[X], 0);
+      tc_fence_after();
+    }
+    __nv_bfloat16* out = ctx + ((int64_t)row * Hq + head) * DH;
+    if (split) {
+      // park this part's partial ([part][column / 4][512 M-rows of the pair][4]);
+      // the last part of this CTA's rows to finish merges them in part order
+      const int key = g * T + blk, mm = (int)rank * 256 + X * 128 + m;
+      const bool any = nX > 0 && m_run != -INFINITY;
+      float4* my_o = reinterpret_cast<float4*>(ws_o) + ((int64_t)key * AT_MAXP + part) * (DH / 4) * 512 + mm;
+#pragma unroll 1
+      for (int c = 0; c < DH / 32; ++c) {
+        uint32_t r[32];
+        if (nX > 0) {
+          tmem_ld32(t_o + c * 32, r);
+          tmem_ld_wait();
+        }
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+          __stcg(my_o + (c * 8 + e) * 512,
+                 any ? make_float4(__uint_as_float(r[4 * e]), __uint_as_float(r[4 * e + 1]),
+                                   __uint_as_float(r[4 * e + 2]), __uint_as_float(r[4 * e + 3]))
+                     : make_float4(0.f, 0.f, 0.f, 0.f));
+      }
+      __stcg(&ws_ml[((int64_t)key * AT_MAXP + part) * 512 + mm],
+             make_float2(any ? m_run * scale_log2 : -INFINITY, any ? l_run : 0.f));
+      __threadfence();
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      if (warp == 4 && lane == 0) {
+        int* cnt = counters + 2 * key + (int)rank;
+        const int prev = atomicAdd(cnt, 1);
+        *s_flag = prev;
+        if (prev == parts - 1) *cnt = 0;  // reset for the next launch
+      }
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      if (*s_flag == parts - 1) {
+        __threadfence();
+        float mp[AT_MAXP], w[AT_MAXP], lp[AT_MAXP];
+        float M = -INFINITY;
+#pragma unroll
+        for (int p = 0; p < AT_MAXP; ++p) {
+          const float2 ml = p < parts ? __ldcg(&ws_ml[((int64_t)key * AT_MAXP + p) * 512 + mm])
+                                      : make_float2(-INFINITY, 0.f);
+          mp[p] = ml.x;
+          lp[p] = ml.y;
+          M = fmaxf(M, ml.x);
+        }
+        float lt = 0.f;
+#pragma unroll
+        for (int p = 0; p < AT_MAXP; ++p) {
+          w[p] = mp[p] == -INFINITY ? 0.f : exp2f(mp[p] - M);
+          lt = fmaf(lp[p], w[p], lt);
+        }
+        const float inv = lt > 0.f ? 1.f / lt : 0.f;
+        if (row < n_q) {
+#pragma unroll 1
+          for (int cg = 0; cg < DH / 32; ++cg) {
+            float v[32];
+#pragma unroll
+            for (int e = 0; e < 32; ++e) v[e] = 0.f;
+#pragma unroll
+            for (int p = 0; p < AT_MAXP; ++p) {
+              if (p < parts) {
+                const float4* op = reinterpret_cast<const float4*>(ws_o) +
+                                   ((int64_t)key * AT_MAXP + p) * (DH / 4) * 512 + (cg * 8) * 512 + mm;
+                float4 a[8];
+#pragma unroll
+                for (int e = 0; e < 8; ++e) a[e] = __ldcg(op + e * 512);
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                  v[4 * e] = fmaf(a[e].x, w[p], v[4 * e]);
+                  v[4 * e + 1] = fmaf(a[e].y, w[p], v[4 * e + 1]);
+                  v[4 * e + 2] = fmaf(a[e].z, w[p], v[4 * e + 2]);
+                  v[4 * e + 3] = fmaf(a[e].w, w[p], v[4 * e + 3]);
+                }
+              }
+            }
+            uint4 pk[4];
+            uint32_t* pw = reinterpret_cast<uint32_t*>(pk);
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+              __nv_bfloat162 hv = __floats2bfloat162_rn(v[2 * e] * inv, v[2 * e + 1] * inv);
+              pw[e] = *reinterpret_cast<uint32_t*>(&hv);
+            }
+            uint4* o4 = reinterpret_cast<uint4*>(out + cg * 32);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) o4[e] = pk[e];
+          }
+          lse[(int64_t)row * Hq + head] = lt > 0.f ? (M + log2f(lt)) * 0.6931471805599453f : -INFINITY;
+        }
+      }
+    } else {
+      const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
+#pragma unroll 1
+      for (int c = 0; c < DH / 32; ++c) {
+        uint32_t r[32];
+        if (nX > 0) {
+          tmem_ld32(t_o + c * 32, r);
+          tmem_ld_wait();
+        }
+        if (row < n_q) {
+          uint4 pk[4];
+          uint32_t* pw = reinterpret_cast<uint32_t*>(pk);
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            const float o0 = nX > 0 ? __uint_as_float(r[2 * e]) * inv : 0.f;
+            const float o1 = nX > 0 ? __uint_as_float(r[2 * e + 1]) * inv : 0.f;
+            __nv_bfloat162 hv = __floats2bfloat162_rn(o0, o1);
+            pw[e] = *reinterpret_cast<uint32_t*>(&hv);
+          }
+          uint4* o4 = reinterpret_cast<uint4*>(out + c * 32);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) o4[e] = pk[e];
+        }
+      }
+      if (row < n_q)
+        lse[(int64_t)row * Hq + head] =
+            l_run > 0.f ? (m_run * scale_log2 + log2f(l_run)) * 0.6931471805599453f : -INFINITY;
+    }
+  }
+  if (tracing) {
+    long long* tr = trace + 24 * (int64_t)blockIdx.x;
+    if (threadIdx.x == 128 || threadIdx.x == 256) {  // softmax X = 0 / 1: s_full wait, busy, pv wait
+      const int o = threadIdx.x == 128 ? 4 : 7;
+      tr[o] = tr_a; tr[o + 1] = tr_b; tr[o + 2] = tr_c;
+    }
+    if (threadIdx.x == 32) { tr[10] = tr_a; tr[11] = tr_b; }  // mma: p_full, k/v/q waits
+    if (threadIdx.x == 0) { tr[12] = tr_a; tr[13] = tr_b; }   // producer: k_empty, v_empty
+  }
+  tc_fence_before();
+  cluster_sync();  // the leader's last MMAs read this CTA's smem / write its TMEM
+  if (tracing && threadIdx.x == 128) {
+    long long* tr = trace + 24 * (int64_t)blockIdx.x;
+    long long t_end;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_end));
+    int smid;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+    tr[0] = nmax; tr[1] = t_begin; tr[2] = t_end; tr[3] = smid;
+  }
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc_pair<SM::TMEM_COLS>(tmem);
   }
 }
 
@@ -2107,7 +2665,7 @@ int launch_ps(const void* q, const void* k, const void* v, const int32_t* q_slot
                   ws_ml, counters, g_attn_trace, attn_exp());
 }
 
-template <int DH>
+template <int DH, int PF = 2>
 int launch_pp(const void* q, const void* k, const void* v, const int32_t* q_slot, const uint8_t* key_pad, void* ctx,
               float* lse, int n_q, int n_keys, int Hq, int Hkv, cudaStream_t st) {
   using SM = Pp<DH>;
@@ -2133,7 +2691,7 @@ int launch_pp(const void* q, const void* k, const void* v, const int32_t* q_slot
     rc = encode(&mv, 2, v, dims, strides, box);
     if (rc) return rc;
   }
-  if (int rc = ensure_smem(attn_pp_kernel<DH>, SM::TOTAL)) return rc;
+  if (int rc = ensure_smem(attn_pp_kernel<DH, PF>, SM::TOTAL)) return rc;
   const int blocks = (n_q + 2 * R - 1) / (2 * R);
   // key splits when the (group, block) grid leaves SMs idle (see launch<>)
   const int slots = num_sms();
@@ -2167,9 +2725,75 @@ int launch_pp(const void* q, const void* k, const void* v, const int32_t* q_slot
   }
   dim3 grid(Hkv * blocks * max_parts);
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)DH);
-  return launch_k(attn_pp_kernel<DH>, grid, dim3(SM::THREADS), SM::TOTAL, st, "attention_pp", mq, mk, mv, q_slot,
+  return launch_k(attn_pp_kernel<DH, PF>, grid, dim3(SM::THREADS), SM::TOTAL, st, "attention_pp", mq, mk, mv, q_slot,
                   key_pad, (__nv_bfloat16*)ctx, lse, n_q, n_keys, Hq, G, scale_log2, Hkv, blocks, target, max_parts,
                   ws_o, ws_ml, counters, g_attn_trace);
+}
+
+template <int DH>
+int launch_pair(const void* q, const void* k, const void* v, const int32_t* q_slot, const uint8_t* key_pad, void* ctx,
+                float* lse, int n_q, int n_keys, int Hq, int Hkv, cudaStream_t st) {
+  using SM = Pr<DH>;
+  constexpr int BN = SM::BN;
+  const int G = Hq / Hkv;
+  const int R = 128 / G;
+  if (key_pad != nullptr && (reinterpret_cast<uintptr_t>(key_pad) & 15))
+    return fail(CC_E_UNSUP, "attention_tc: key_pad must be 16-byte aligned");
+  CUtensorMap mq, mk, mv;
+  {
+    cuuint64_t dims[3] = {(cuuint64_t)DH, (cuuint64_t)Hq, (cuuint64_t)n_q};
+    cuuint64_t strides[2] = {(cuuint64_t)DH * 2, (cuuint64_t)Hq * DH * 2};
+    cuuint32_t box[3] = {64, (cuuint32_t)G, (cuuint32_t)R};
+    int rc = encode(&mq, 3, q, dims, strides, box);
+    if (rc) return rc;
+  }
+  {
+    cuuint64_t dims[2] = {(cuuint64_t)Hkv * DH, (cuuint64_t)n_keys};
+    cuuint64_t strides[1] = {(cuuint64_t)Hkv * DH * 2};
+    cuuint32_t kbox[2] = {64, 32};  // half a 64-key K tile per CTA
+    int rc = encode(&mk, 2, k, dims, strides, kbox);
+    if (rc) return rc;
+    cuuint32_t vbox[2] = {64, (cuuint32_t)BN};  // 64 keys x DH/2 columns per CTA
+    rc = encode(&mv, 2, v, dims, strides, vbox);
+    if (rc) return rc;
+  }
+  if (int rc = ensure_smem(attn_pair_kernel<DH>, SM::TOTAL)) return rc;
+  const int blocks = (n_q + 4 * R - 1) / (4 * R);
+  // key splits when the (group, block) pairs leave SM pairs idle (see launch<>)
+  const int slots = num_sms() / 2;
+  const int max_tiles = (n_keys + BN - 1) / BN;
+  int target = max_tiles, max_parts = 1;
+  if (blocks <= AT_MAXT && max_tiles > 0 && Hkv * blocks < slots) {
+    max_parts = std::max(1, std::min(AT_MAXP, (slots + Hkv * blocks - 1) / (Hkv * blocks)));
+    target = std::max(16, (max_tiles + max_parts - 1) / max_parts);
+    max_parts = std::min(max_parts, (max_tiles + target - 1) / target);
+    if (max_parts < 1) max_parts = 1;
+  }
+  if (getenv("CCB_ATTN_NOSPLIT")) max_parts = 1;
+  if (const char* e = getenv("CCB_ATTN_SPLIT")) {  // experiments: "target,max_parts"
+    int a = 0, b = 0;
+    if (sscanf(e, "%d,%d", &a, &b) == 2 && a > 0 && b >= 1 && b <= AT_MAXP && blocks <= AT_MAXT) {
+      target = a;
+      max_parts = b;
+    }
+  }
+  float* ws_o = nullptr;
+  float2* ws_ml = nullptr;
+  int* counters = nullptr;
+  if (max_parts > 1) {
+    const size_t keys = (size_t)Hkv * blocks;
+    const size_t bytes = keys * AT_MAXP * 512 * (DH * sizeof(float) + sizeof(float2));
+    uint8_t* scratch = (uint8_t*)stream_scratch(st, SCR_ATTN, bytes);
+    counters = split_counters(st, (int)(2 * keys));
+    if (!scratch || !counters) return fail(CC_E_CUDA, "attention_tc: split workspace allocation failed");
+    ws_o = reinterpret_cast<float*>(scratch);
+    ws_ml = reinterpret_cast<float2*>(scratch + keys * AT_MAXP * 512 * DH * sizeof(float));
+  }
+  dim3 grid(2 * Hkv * blocks * max_parts);
+  const float scale_log2 = 1.4426950408889634f / sqrtf((float)DH);
+  return launch_k(attn_pair_kernel<DH>, grid, dim3(SM::THREADS), SM::TOTAL, st, "attention_pair", mq, mk, mv, q_slot,
+                  key_pad, (__nv_bfloat16*)ctx, lse, n_q, n_keys, Hq, G, scale_log2, Hkv, blocks, target, max_parts,
+                  ws_o, ws_ml, counters, g_attn_trace, attn_exp());
 }
 
 // Kernel shape per launch: 0 = 128-key tiles, two softmax warpgroups (one
@@ -2185,6 +2809,10 @@ int launch_variant(int variant, const void* q, const void* k, const void* v, con
     case 3: return launch<DH, 128, 1>(q, k, v, q_slot, key_pad, ctx, lse, n_q, n_keys, Hq, Hkv, st);
     case 4: return launch_pp<DH>(q, k, v, q_slot, key_pad, ctx, lse, n_q, n_keys, Hq, Hkv, st);
     case 5: return launch_ps<DH>(q, k, v, q_slot, key_pad, ctx, lse, n_q, n_keys, Hq, Hkv, st);
+    case 6:
+      if constexpr (DH == 128) return launch_pair<DH>(q, k, v, q_slot, key_pad, ctx, lse, n_q, n_keys, Hq, Hkv, st);
+      return fail(CC_E_UNSUP, "attention_tc: the CTA-pair kernel needs d_head 128");
+
     default: return launch<DH, 128, 2>(q, k, v, q_slot, key_pad, ctx, lse, n_q, n_keys, Hq, Hkv, st);
   }
 }
