@@ -655,58 +655,6 @@ __global__ void __launch_bounds__(At<DH, BN, NWG, KST_, VST_>::THREADS, At<DH, B
   }
 }
 
-// ---- persistent ping-pong kernel: two Q tiles per CTA share every K/V tile ----
-//
-// Work: items (row block b of 2R query rows, GQA group g), each a sequence of
-// key tiles [0, len_b), len_b from the causal limit of the block's rows.  The
-// items are laid end to end (b ascending, g) into one sequence of W tile
-// pairs; CTA c of the grid (one per SM) takes the contiguous share
-// [c S, (c+1) S), S = max(ceil(W / grid), min_share) -- stream-K over the
-// attention: every SM gets the same number of tile pairs whatever the causal
-// ranges, and an item cut by a share boundary is finished by a fixed-order
-// merge of its parts (the last part to finish merges, in part order, so the
-// result does not depend on timing).  A CTA walks its segments in order;
-// barrier phases run on across segments, the next segment's Q load overlaps
-// the current segment's last softmax, and O is recycled once the epilogue
-// has read it.
-//
-// CTA = 2 Q tiles of 128 M-rows (R query rows x G heads each).
-//   warp 0      TMA: Q0 + Q1 per segment, K_j / V_j (2-deep rings); each K/V
-//               tile feeds both Q tiles (256 M-rows per L2 byte)
-//   warp 1      MMA issuer, per key tile j and Q tile X in turn:
-//                 O_X += P_X(j) V_j, then S_X(j+1) = Q_X K_{j+1}^T
-//               so while softmax X works on tile j the tensor pipe runs the
-//               other Q tile's PV and S (the two softmax warpgroups ping-pong)
-//   warps 4-7   softmax of Q tile 0, warps 8-11 of Q tile 1: thread = one
-//               M-row, all 128 keys of the tile (no cross-thread max
-//               exchange); fp32 online softmax with packed f32x2 math, exp2 on
-//               MUFU for three quarters and as a polynomial on the FMA pipe for
-//               one quarter, lazy O rescale in TMEM, P as bf16 over the second
-//               half of its own S buffer (the PV MMA's A operand)
-// TMEM: S0/P0 | S1/P1 | O0 | O1 (P_X over the second half of S_X).
-// S_X(j+1) overwrites P_X(j) only after
-// PV_X(j) (one MMA thread, in-order tensor pipe), and softmax X sees S_X(j+1)
-// only after PV_X(j) completed, so O_X is current whenever it is rescaled.
-template <int DH>
-struct Ps {
-  static constexpr int BN = 64;  // keys per tile
-  static constexpr int KST = 4, VST = 4;
-  static constexpr int THREADS = 384;
-  static constexpr int MAXB = 2048;  // row blocks the in-kernel plan handles
-  static constexpr int ATOMS = DH / 64;
-  static constexpr int Q_BYTES = 128 * DH * 2;  // one Q tile (128 M-rows)
-  static constexpr int KV_BYTES = BN * DH * 2;
-  static constexpr int Q_OFF = 0;
-  static constexpr int K_OFF = 2 * Q_BYTES;
-  static constexpr int V_OFF = K_OFF + KST * KV_BYTES;
-  static constexpr int BAR_OFF = V_OFF + VST * KV_BYTES;
-  static constexpr int PLAN_OFF = BAR_OFF + 1024;  // kmx[2][MAXB], pre[MAXB + 1]
-  static constexpr size_t TOTAL = PLAN_OFF + (3 * MAXB + 8) * 4;
-  // TMEM: S_{X,b} (b = tile parity) at X * 2 BN + b BN, O_X at 4 BN + X DH
-  static constexpr int TMEM_COLS = 512;
-  static_assert(4 * BN + 2 * DH <= TMEM_COLS, "TMEM budget");
-};
-
 __device__ __forceinline__ uint64_t f2_pack(float lo, float hi) {
   uint64_t r;
   asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
@@ -773,647 +721,6 @@ __device__ __forceinline__ void ld8_f4_cg_4k(const float4* p, float (&a)[32]) {
       : "l"(p)
       : "memory");
 }
-
-// one segment of a CTA's share: key tiles [ts, te) of item (b, g).  Items
-// occupy len + k0 positions of the sequence: k0 virtual tile pairs stand for
-// a segment's fixed cost (pipeline fill / drain, epilogue), so an SM given
-// many short items gets fewer tiles.  ts >= len: pos is in the virtual tail.
-struct PsSeg {
-  int b, g, ts, te, len, istart, ext;
-};
-__device__ __forceinline__ PsSeg ps_segment(int pos, int end, const int* pre, int T, int Hkv, int k0) {
-  int lo = 0, hi = T - 1;  // last block whose items start at or before pos
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (Hkv * pre[mid] <= pos) lo = mid; else hi = mid - 1;
-  }
-  PsSeg s;
-  s.b = lo;
-  s.ext = pre[lo + 1] - pre[lo];
-  s.len = s.ext - k0;
-  const int base = Hkv * pre[lo];
-  s.g = (pos - base) / s.ext;
-  s.istart = base + s.g * s.ext;
-  s.ts = pos - s.istart;
-  s.te = min(s.len, s.ts + (end - pos));
-  return s;
-}
-
-template <int DH>
-__global__ void __launch_bounds__(384, 1)
-    attn_ps_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-                   const __grid_constant__ CUtensorMap tmV, const int32_t* __restrict__ q_slot,
-                   const uint8_t* __restrict__ key_pad, __nv_bfloat16* __restrict__ ctx, float* __restrict__ lse,
-                   int n_q, int n_keys, int Hq, int G, float scale_log2, int Hkv, int T, int min_share, int k0,
-                   float* __restrict__ ws_o, float2* __restrict__ ws_ml, int* __restrict__ counters,
-                   long long* __restrict__ trace, int exp) {
-  using SM = Ps<DH>;
-  constexpr int BN = SM::BN, KST = SM::KST, VST = SM::VST, NT = SM::THREADS;
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* base = smem_raw;
-  if (smem_u32(smem_raw) & 1023) __trap();
-  uint8_t* sQ = base + SM::Q_OFF;
-  uint8_t* sK = base + SM::K_OFF;
-  uint8_t* sV = base + SM::V_OFF;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(base + SM::BAR_OFF);
-  uint64_t* q_full = bars + 0;
-  uint64_t* q_empty = bars + 1;       // committed after the segment's last S MMA
-  uint64_t* k_full = bars + 2;        // [KST]
-  uint64_t* k_empty = k_full + KST;   // [KST] committed after both S MMAs of the tile
-  uint64_t* v_full = k_empty + KST;   // [VST]
-  uint64_t* v_empty = v_full + VST;   // [VST] committed after both PV MMAs of the tile
-  uint64_t* s_full = v_empty + VST;   // [2 Q tiles][2 S buffers]
-  uint64_t* p_full = s_full + 4;      // [2][2] (128 softmax arrivals)
-  uint64_t* pv_done = p_full + 4;     // [2] one phase per PV MMA of the Q tile
-  uint64_t* o_done = pv_done + 2;     // [2] last PV of the segment completed
-  uint64_t* o_free = o_done + 2;      // [2] epilogue has read O (128 arrivals)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_free + 2);
-  int* s_flag = reinterpret_cast<int*>(tmem_slot + 1);  // [2] per Q tile: split-merge ticket
-  int* kmx = reinterpret_cast<int*>(base + SM::PLAN_OFF);  // [2][MAXB] causal limit per (Q tile, block)
-  int* pre = kmx + 2 * SM::MAXB;                            // [MAXB + 1] item extent prefix (tiles)
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int R = 128 / G;  // query rows per Q tile
-  const int RB = 2 * R;   // per block
-  pdl_trigger();
-  for (int i = threadIdx.x; i < 2 * T; i += NT) kmx[(i & 1) * SM::MAXB + (i >> 1)] = -1;
-  __syncthreads();
-  pdl_wait();  // q_slot and, below, q/k/v: written before this kernel
-  for (int r = threadIdx.x; r < min(T * RB, n_q); r += NT)  // row r -> block r / RB, Q tile (r % RB) / R
-    atomicMax(&kmx[((r % RB) / R) * SM::MAXB + r / RB], min(q_slot[r], n_keys - 1));
-  __syncthreads();
-  if (warp == 0) {  // exclusive prefix of the item extents (tiles + k0 per item)
-    const int per = (T + 31) / 32;
-    int sum = 0;
-    for (int b = lane * per; b < min(T, (lane + 1) * per); ++b) {
-      const int k = max(kmx[b], kmx[SM::MAXB + b]);
-      sum += k < 0 ? 0 : k / BN + 1 + k0;
-    }
-    int incl = sum;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int v = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += v;
-    }
-    int run = incl - sum;
-    for (int b = lane * per; b < min(T, (lane + 1) * per); ++b) {
-      pre[b] = run;
-      const int k = max(kmx[b], kmx[SM::MAXB + b]);
-      run += k < 0 ? 0 : k / BN + 1 + k0;
-    }
-    if (lane == 31) pre[T] = incl;
-  }
-  if (warp == 1 && lane == 0) {
-    tma_prefetch(&tmQ);
-    tma_prefetch(&tmK);
-    tma_prefetch(&tmV);
-    mbar_init(q_full, 1);
-    mbar_init(q_empty, 1);
-    for (int s = 0; s < KST; ++s) {
-      mbar_init(&k_full[s], 1);
-      mbar_init(&k_empty[s], 1);
-    }
-    for (int s = 0; s < VST; ++s) {
-      mbar_init(&v_full[s], 1);
-      mbar_init(&v_empty[s], 1);
-    }
-    for (int i = 0; i < 4; ++i) {
-      mbar_init(&s_full[i], 1);
-      mbar_init(&p_full[i], 128);
-    }
-    for (int x = 0; x < 2; ++x) {
-      mbar_init(&pv_done[x], 1);
-      mbar_init(&o_done[x], 1);
-      mbar_init(&o_free[x], 128);
-    }
-    fence_barrier_init();
-  }
-  __syncthreads();
-  const int W = Hkv * pre[T];
-  const int share = max((W + (int)gridDim.x - 1) / (int)gridDim.x, min_share);
-  const int c0 = (int)blockIdx.x * share, c1 = min(c0 + share, W);
-  if (c0 >= c1) return;  // no work for this CTA (before any TMEM use)
-  if (warp == 1) tmem_alloc<SM::TMEM_COLS>(tmem_slot);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-  const bool tracing = trace != nullptr;
-  long long tr_a = 0, tr_b = 0, tr_c = 0, tr_d = 0, tr_e = 0;
-  long long t_begin = 0;
-  if (tracing && threadIdx.x == 128) asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_begin));
-  // tiles of Q tile X in segment s: [ts, min(te, ntot_X))
-  auto seg_n = [&](const PsSeg& s, int x) {
-    const int k = kmx[x * SM::MAXB + s.b];
-    const int ntot = k < 0 ? 0 : k / BN + 1;
-    return max(0, min(s.te, ntot) - s.ts);
-  };
-
-  // every role ends here on its own (no control-flow join after the register
-  // split): trace, CTA barrier, TMEM release
-  auto finish = [&]() {
-    if (tracing) {
-      long long* tr = trace + 24 * (int64_t)blockIdx.x;
-      if (threadIdx.x == 128 || threadIdx.x == 256) {  // softmax X = 0 / 1, row 0: s_full wait, busy, epilogue
-        const int o = threadIdx.x == 128 ? 4 : 7;
-        tr[o] = tr_a; tr[o + 1] = tr_b; tr[o + 2] = tr_c;
-      }
-      if (threadIdx.x == 128) {  // softmax X = 0: o_done wait, split epilogue: all, ticket, park, merge, counts
-        tr[14] = tr_d; tr[15] = tr_e;
-      }
-      if (threadIdx.x == 32) { tr[10] = tr_a; tr[11] = tr_b; tr[16] = tr_c; tr[17] = tr_d; }  // mma: p_full, other waits, commits, issue
-      if (threadIdx.x == 0) { tr[12] = tr_a; tr[13] = tr_b; }   // producer: q_empty, k/v_empty
-    }
-    tc_fence_before();
-    asm volatile("bar.sync 15, 384;" ::: "memory");
-    if (tracing && threadIdx.x == 128) {
-      long long* tr = trace + 24 * (int64_t)blockIdx.x;
-      long long t_end;
-      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_end));
-      int smid;
-      asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
-      tr[0] = c1 - c0; tr[1] = t_begin; tr[2] = t_end; tr[3] = smid;
-    }
-    if (warp == 1) {
-      tc_fence_after();
-      tmem_dealloc<SM::TMEM_COLS>(tmem);
-    }
-  };
-  // registers: the TMA / MMA warpgroup needs few, a softmax thread more
-  // (REG_LO + 2 REG_HI per 128 threads <= 3 x 168), set at the top of each
-  // role (no role rejoins another: each ends in its own CTA barrier)
-#define PS_REG_LO "setmaxnreg.dec.sync.aligned.u32 120;"
-#define PS_REG_HI "setmaxnreg.inc.sync.aligned.u32 192;"
-  if (warp == 0) {
-    asm volatile(PS_REG_LO ::: "memory");
-    if (lane == 0) {
-      // Q per segment; K runs two tiles ahead of V (the MMA issues S two
-      // tiles ahead of PV): K0, K1, V0, K2, V1, K3, ...
-      int kc = 0, vc = 0, qc = 0;
-      for (int pos = c0; pos < c1;) {
-        const PsSeg sg = ps_segment(pos, c1, pre, T, Hkv, k0);
-        if (sg.ts >= sg.len) {  // virtual tail of an item
-          pos = sg.istart + sg.ext;
-          continue;
-        }
-        pos += sg.te - sg.ts;
-        const int nmax = sg.te - sg.ts;
-        twait(q_empty, (qc & 1) ^ 1, tracing, tr_a);
-        ++qc;
-        mbar_expect_tx(q_full, 2 * SM::Q_BYTES);
-#pragma unroll
-        for (int x = 0; x < 2; ++x)
-#pragma unroll
-          for (int a = 0; a < SM::ATOMS; ++a)
-            tma_load_3d(sQ + x * SM::Q_BYTES + a * 128 * 128, &tmQ, q_full, a * 64, sg.g * G, sg.b * RB + x * R);
-        auto load_k = [&](int t) {
-          const int ks = kc % KST;
-          twait(&k_empty[ks], ((kc / KST) & 1) ^ 1, tracing, tr_b);
-          ++kc;
-          mbar_expect_tx(&k_full[ks], SM::KV_BYTES);
-#pragma unroll
-          for (int a = 0; a < SM::ATOMS; ++a)
-            tma_load_2d(sK + ks * SM::KV_BYTES + a * BN * 128, &tmK, &k_full[ks], sg.g * DH + a * 64,
-                        (sg.ts + t) * BN);
-        };
-        load_k(0);
-        if (nmax > 1) load_k(1);
-        for (int t = 0; t < nmax; ++t) {
-          const int vs = vc % VST;
-          twait(&v_empty[vs], ((vc / VST) & 1) ^ 1, tracing, tr_b);
-          ++vc;
-          mbar_expect_tx(&v_full[vs], SM::KV_BYTES);
-#pragma unroll
-          for (int a = 0; a < SM::ATOMS; ++a)
-            tma_load_2d(sV + vs * SM::KV_BYTES + a * BN * 128, &tmV, &v_full[vs], sg.g * DH + a * 64,
-                        (sg.ts + t) * BN);
-          if (t + 2 < nmax) load_k(t + 2);
-        }
-      }
-    }
-    finish();
-    return;
-  } else if (warp == 1) {
-    asm volatile(PS_REG_LO ::: "memory");
-    if (lane == 0) {
-      // Per segment: S_X(0), S_X(1), then per tile j and Q tile X:
-      //   PV_X(j) (P from S buffer j & 1), then S_X(j+2) into the same buffer
-      // (in order after PV_X(j) has read its P).  The softmax of tile j+1
-      // finds S_X(j+1) long done, so the two softmax warpgroups run back to
-      // back and concurrently.  Buffer / phase of a Q tile's S and P follow
-      // its running tile count gj[X] across segments.
-      constexpr uint32_t id_s = idesc_bf16(128, BN, false);
-      constexpr uint32_t id_o = idesc_bf16(128, DH, true);
-      int kc = 0, vc = 0, qc = 0;
-      int gj[2] = {0, 0}, of[2] = {0, 0};
-      auto tcommit = [&](uint64_t* bar) {  // (trace: commit issue cycles in tr_c)
-        const long long t0 = tracing ? clock64() : 0;
-        mma_commit(bar);
-        if (tracing) tr_c += clock64() - t0;
-      };
-      auto issue_s = [&](int x, int b, int ks) {
-        const long long t0 = tracing ? clock64() : 0;
-        if (!(exp & 2))  // (timing experiment 2: no MMAs)
-#pragma unroll
-        for (int kk = 0; kk < DH / 16; ++kk) {
-          const int a = kk >> 2, w = kk & 3;
-          const uint64_t bd = desc_sw128(sK + ks * SM::KV_BYTES + a * BN * 128) + 2 * w;
-          const uint64_t ad = desc_sw128(sQ + x * SM::Q_BYTES + a * 128 * 128) + 2 * w;
-          mma_bf16(tmem + x * 2 * BN + b * BN, ad, bd, id_s, kk > 0);
-        }
-        if (tracing) tr_d += clock64() - t0;
-        tcommit(&s_full[x * 2 + b]);
-      };
-      for (int pos = c0; pos < c1;) {
-        const PsSeg sg = ps_segment(pos, c1, pre, T, Hkv, k0);
-        if (sg.ts >= sg.len) {  // virtual tail of an item
-          pos = sg.istart + sg.ext;
-          continue;
-        }
-        pos += sg.te - sg.ts;
-        const int nx[2] = {seg_n(sg, 0), seg_n(sg, 1)};
-        const int nmax = sg.te - sg.ts;
-        twait(q_full, qc & 1, tracing, tr_b);
-        ++qc;
-        for (int t = 0; t < min(2, nmax); ++t) {
-          const int ks = kc % KST;
-          twait(&k_full[ks], (kc / KST) & 1, tracing, tr_b);
-          tc_fence_after();
-#pragma unroll
-          for (int x = 0; x < 2; ++x)
-            if (t < nx[x]) issue_s(x, (gj[x] + t) & 1, ks);
-          tcommit(&k_empty[ks]);
-          ++kc;
-          if (t == nmax - 1) tcommit(q_empty);  // the segment's last S MMA is issued
-        }
-        for (int j = 0; j < nmax; ++j) {
-          const int vs = vc % VST;
-          bool v_ready = false, k_ready = false;
-#pragma unroll
-          for (int x = 0; x < 2; ++x) {
-            if (j >= nx[x]) continue;
-            const int g = gj[x] + j, b = g & 1;
-            twait(&p_full[x * 2 + b], (g >> 1) & 1, tracing, tr_a);
-            if (!v_ready) {
-              twait(&v_full[vs], (vc / VST) & 1, tracing, tr_b);
-              v_ready = true;
-            }
-            if (j == 0) {  // the previous segment's epilogue has read O_X
-              twait(&o_free[x], (of[x] & 1) ^ 1, tracing, tr_b);
-              ++of[x];
-            }
-            tc_fence_after();
-            // A = P over the second half of S buffer b (row = lane, 2 keys per column)
-            const uint32_t t_o = tmem + 4 * BN + x * DH, t_p = tmem + x * 2 * BN + b * BN + BN / 2;
-            const long long tp0 = tracing ? clock64() : 0;
-            if (!(exp & 2))
-#pragma unroll
-            for (int kk = 0; kk < BN / 16; ++kk) {
-              const uint64_t bd = desc_sw128_mn(sV + vs * SM::KV_BYTES + kk * 16 * 128, BN * 128);
-              mma_bf16_ts(t_o, t_p + kk * 8, bd, id_o, (j > 0 || kk > 0) ? 1u : 0u);
-            }
-            if (tracing) tr_d += clock64() - tp0;
-            tcommit(&pv_done[x]);
-            if (j + 2 < nx[x]) {
-              if (!k_ready) {
-                twait(&k_full[kc % KST], (kc / KST) & 1, tracing, tr_b);
-                tc_fence_after();
-                k_ready = true;
-              }
-              issue_s(x, b, kc % KST);
-            }
-            if (j == nx[x] - 1) tcommit(&o_done[x]);
-          }
-          tcommit(&v_empty[vs]);
-          ++vc;
-          if (k_ready) {
-            tcommit(&k_empty[kc % KST]);
-            ++kc;
-            if (j + 3 == nmax) tcommit(q_empty);  // the segment's last S MMA is issued
-          }
-        }
-        gj[0] += nx[0];
-        gj[1] += nx[1];
-      }
-    }
-    finish();
-    return;
-  } else if (warp >= 4) {
-    asm volatile(PS_REG_HI ::: "memory");
-    // ---- softmax + epilogue of Q tile X: thread = one M-row, all BN keys ------
-    const int X = (warp - 4) >> 2;
-    const int q4 = warp & 3;  // TMEM lane quarter
-    const int m = q4 * 32 + lane;
-    const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
-    const uint32_t t_s0 = tmem + X * 2 * BN + lane_off, t_o = tmem + 4 * BN + X * DH + lane_off;
-    const uint64_t sl2 = f2_pack(scale_log2, scale_log2);
-    constexpr float kRescaleLog2 = 8.f;
-    int gj = 0, oc = 0;
-    for (int pos = c0; pos < c1;) {
-      const PsSeg sg = ps_segment(pos, c1, pre, T, Hkv, k0);
-      if (sg.ts >= sg.len) {  // virtual tail of an item
-        pos = sg.istart + sg.ext;
-        continue;
-      }
-      const bool first_of_cta = pos == c0;
-      pos += sg.te - sg.ts;
-      const int nX = seg_n(sg, X);
-      const int row = sg.b * RB + X * R + m / G;
-      const int head = sg.g * G + m % G;
-      const int lim = row < n_q ? min(q_slot[row], n_keys - 1) : -1;
-      float m_run = -INFINITY, l_run = 0.f;
-      for (int j = 0; j < nX; ++j, ++gj) {
-        const int b = gj & 1;
-        const uint32_t t_s = t_s0 + b * BN;
-        twait(&s_full[X * 2 + b], (gj >> 1) & 1, tracing, tr_a);
-        if (exp & 1) {  // timing experiment 1: no softmax work (barriers only; wrong results)
-          tc_fence_before();
-          mbar_arrive(&p_full[X * 2 + b]);
-          continue;
-        }
-        const long long tb0 = tracing ? clock64() : 0;
-        tc_fence_after();
-        float s[BN];
-        tmem_ld32(t_s, *reinterpret_cast<uint32_t(*)[32]>(&s[0]));
-        tmem_ld32(t_s + 32, *reinterpret_cast<uint32_t(*)[32]>(&s[32]));
-        tmem_ld_wait();
-        const int j0 = (sg.ts + j) * BN;
-        const int lim_rel = lim - j0;
-        if (key_pad != nullptr) {
-#pragma unroll
-          for (int u = 0; u < BN / 16; ++u) {
-            uint4 w = make_uint4(0u, 0u, 0u, 0u);
-            const int kb = j0 + u * 16;
-            if (kb + 16 <= n_keys) {
-              w = __ldg(reinterpret_cast<const uint4*>(key_pad + kb));
-            } else {
-              uint8_t* wb = reinterpret_cast<uint8_t*>(&w);
-              for (int e = 0; e < 16; ++e) wb[e] = kb + e < n_keys ? key_pad[kb + e] : 1;
-            }
-            const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-            for (int e = 0; e < 16; ++e) {
-              const int c = u * 16 + e;
-              const bool padded = ((ww[e >> 2] >> (8 * (e & 3))) & 0xffu) != 0u;
-              s[c] = (c <= lim_rel && !padded) ? s[c] : -INFINITY;
-            }
-          }
-        } else if (lim_rel < BN - 1) {
-#pragma unroll
-          for (int c = 0; c < BN; ++c) s[c] = (c <= lim_rel) ? s[c] : -INFINITY;
-        }
-        float mx[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) mx[e] = fmax3(s[e], s[8 + 2 * e], s[9 + 2 * e]);
-#pragma unroll
-        for (int c = 24; c < BN; c += 16) {
-#pragma unroll
-          for (int e = 0; e < 8; ++e) mx[e] = fmax3(mx[e], s[c + 2 * e], s[c + 2 * e + 1]);
-        }
-        const float tmax = fmax3(fmax3(mx[0], mx[1], mx[2]), fmax3(mx[3], mx[4], mx[5]), fmaxf(mx[6], mx[7]));
-        bool grow = false;
-        float alpha = 1.f;
-        if (m_run == -INFINITY) {
-          m_run = tmax;
-        } else if ((tmax - m_run) * scale_log2 > kRescaleLog2) {
-          grow = true;
-          alpha = ex2_fast((m_run - tmax) * scale_log2);
-          l_run *= alpha;
-          m_run = tmax;
-        }
-        const float nb = (m_run == -INFINITY) ? 0.f : -m_run * scale_log2;
-        const uint64_t nb2 = f2_pack(nb, nb);
-        uint64_t acc[4] = {0ull, 0ull, 0ull, 0ull};
-        uint32_t pt[BN / 2];
-#pragma unroll
-        for (int e = 0; e < BN / 2; ++e) {
-          const uint64_t x2 = ffma2(f2_pack(s[2 * e], s[2 * e + 1]), sl2, nb2);
-          uint64_t p2;
-          if ((e & 7) >= 6) {  // a quarter of the exponentials on the FMA pipe
-            p2 = ex2_poly2(x2);
-          } else {
-            float x0, x1;
-            f2_unpack(x2, x0, x1);
-            p2 = f2_pack(ex2_fast(x0), ex2_fast(x1));
-          }
-          acc[e & 3] = fadd2(acc[e & 3], p2);
-          float p0, p1;
-          f2_unpack(p2, p0, p1);
-          __nv_bfloat162 hv = __floats2bfloat162_rn(p0, p1);
-          pt[e] = *reinterpret_cast<uint32_t*>(&hv);
-        }
-        // P over the second half of this S buffer (already read)
-        tmem_st_cols<BN / 2>(t_s + BN / 2, pt);
-        if (__any_sync(0xffffffffu, grow)) {
-          // O_X *= alpha once PV_X of the previous tile has completed (that PV
-          // is phase gj - 1 of pv_done[X]; every earlier one completed before
-          // S_X of this tile was issued, so the parity is unambiguous)
-          twait(&pv_done[X], (gj - 1) & 1, tracing, tr_d);
-          tc_fence_after();
-          const uint64_t a2 = f2_pack(alpha, alpha);
-#pragma unroll 1
-          for (int c = 0; c < DH / 32; ++c) {
-            uint32_t r[32];
-            tmem_ld32(t_o + c * 32, r);
-            tmem_ld_wait();
-#pragma unroll
-            for (int e = 0; e < 16; ++e) {
-              float o0, o1;
-              f2_unpack(fmul2(f2_pack(__uint_as_float(r[2 * e]), __uint_as_float(r[2 * e + 1])), a2), o0, o1);
-              r[2 * e] = __float_as_uint(o0);
-              r[2 * e + 1] = __float_as_uint(o1);
-            }
-            tmem_st32(t_o + c * 32, r);
-          }
-        }
-        tmem_st_wait();
-        tc_fence_before();
-        mbar_arrive(&p_full[X * 2 + b]);
-        if (tracing) tr_b += clock64() - tb0;
-        const uint64_t a01 = fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3]));
-        float sa, sb;
-        f2_unpack(a01, sa, sb);
-        l_run += sa + sb;
-      }
-      // ---- epilogue of the segment -------------------------------------------
-      const long long te0 = tracing ? clock64() : 0;
-      if (nX > 0) {
-        twait(&o_done[X], oc & 1, tracing, tr_d);
-        ++oc;
-        tc_fence_after();
-      }
-      // O_X, 32 columns at a time (o_free once all are read; the next
-      // segment's first PV_X waits for it)
-      __nv_bfloat16* out = ctx + ((int64_t)row * Hq + head) * DH;
-      const int q0 = sg.istart / share, q1 = (sg.istart + sg.len - 1) / share;  // CTAs sharing the item
-      if (q1 > q0) {
-        // Item cut by share boundaries: per Q tile X, the parts count in
-        // (atomic ticket); every part but the last parks its unnormalised O,
-        // max (log2 units) and sum in its CTA's slot (2c: the CTA's first
-        // segment, 2c+1: its last) and then signals `ready`; the last part
-        // waits for the others' signals and merges them with its own O (still
-        // in TMEM) in part order -- the same arithmetic whoever is last.
-        const int parts = q1 - q0 + 1, mypart = (int)blockIdx.x - q0;
-        const int item = sg.b * Hkv + sg.g, mm = X * 128 + m;
-        int* ticket = counters + 2 * (item * 2 + X);
-        int* ready = ticket + 1;
-        const bool any = nX > 0 && m_run != -INFINITY;
-        const float m_l2 = any ? m_run * scale_log2 : -INFINITY;
-        const float l_me = any ? l_run : 0.f;
-        const long long tm0 = tracing ? clock64() : 0;
-        auto xbar = [&]() { asm volatile("bar.sync %0, 128;" ::"r"(1 + X) : "memory"); };
-        xbar();  // (s_flag[X] of the previous split segment has been read by all)
-        if (q4 == 0 && lane == 0) s_flag[X] = atomicAdd(ticket, 1);
-        xbar();
-        const bool last = s_flag[X] == parts - 1;
-        if (!last) {
-          const int64_t slot = 2 * (int64_t)blockIdx.x + (first_of_cta ? 0 : 1);
-          // partial layout [slot][column / 4][256 M-rows][4]: a warp's
-          // 16-byte stores (and the merge's loads) cover 512 contiguous bytes
-          float4* my_o = reinterpret_cast<float4*>(ws_o) + slot * (DH / 4) * 256 + mm;
-#pragma unroll 1
-          for (int c = 0; c < DH / 32; ++c) {
-            uint32_t r[32];
-            if (nX > 0) {
-              tmem_ld32(t_o + c * 32, r);
-              tmem_ld_wait();
-            }
-#pragma unroll
-            for (int e = 0; e < 8; ++e)
-              __stcg(my_o + (c * 8 + e) * 256,
-                     any ? make_float4(__uint_as_float(r[4 * e]), __uint_as_float(r[4 * e + 1]),
-                                       __uint_as_float(r[4 * e + 2]), __uint_as_float(r[4 * e + 3]))
-                         : make_float4(0.f, 0.f, 0.f, 0.f));
-          }
-          if (nX > 0) {
-            tc_fence_before();
-            mbar_arrive(&o_free[X]);
-          }
-          __stcg(&ws_ml[slot * 256 + mm], make_float2(m_l2, l_me));
-          __threadfence();
-          xbar();
-          if (q4 == 0 && lane == 0) atomicAdd(ready, 1);
-        } else {
-          if (q4 == 0 && lane == 0) {
-            int seen;
-            do {
-              asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(seen) : "l"(ready) : "memory");
-            } while (seen < parts - 1);
-            *ready = 0;   // reset for the next launch (no part touches them again)
-            *ticket = 0;
-          }
-          xbar();
-          __threadfence();
-          int64_t sl[8];
-          float mp[8], lp[8];
-          float M = -INFINITY;
-#pragma unroll
-          for (int p = 0; p < 8; ++p) {
-            const int c = q0 + p;
-            sl[p] = 2 * (int64_t)c + (sg.istart <= c * share ? 0 : 1);
-            float2 ml = make_float2(-INFINITY, 0.f);
-            if (p == mypart) ml = make_float2(m_l2, l_me);
-            else if (p < parts) ml = __ldcg(&ws_ml[sl[p] * 256 + mm]);
-            mp[p] = ml.x;
-            lp[p] = ml.y;
-            M = fmaxf(M, ml.x);
-          }
-          float w[8];
-          float lt = 0.f;
-#pragma unroll
-          for (int p = 0; p < 8; ++p) {
-            w[p] = mp[p] == -INFINITY ? 0.f : exp2f(mp[p] - M);
-            lt = fmaf(lp[p], w[p], lt);
-          }
-          const float inv = lt > 0.f ? 1.f / lt : 0.f;
-#pragma unroll 1
-          for (int cg = 0; cg < DH / 32; ++cg) {
-            uint32_t r[32];
-            if (nX > 0) {
-              tmem_ld32(t_o + cg * 32, r);
-              tmem_ld_wait();
-            }
-            float v[32];
-#pragma unroll
-            for (int e = 0; e < 32; ++e) v[e] = 0.f;
-#pragma unroll
-            for (int p = 0; p < 8; ++p) {
-              if (p < parts) {
-                if (p == mypart) {
-#pragma unroll
-                  for (int e = 0; e < 32; ++e) v[e] = fmaf(any ? __uint_as_float(r[e]) : 0.f, w[p], v[e]);
-                } else {
-                  const float4* op = reinterpret_cast<const float4*>(ws_o) + sl[p] * (DH / 4) * 256 + (cg * 8) * 256 + mm;
-                  float a[32];
-                  ld8_f4_cg_4k(op, a);
-#pragma unroll
-                  for (int e = 0; e < 32; ++e) v[e] = fmaf(a[e], w[p], v[e]);
-                }
-              }
-            }
-            if (row < n_q) {
-              uint4 pk[4];
-              uint32_t* pw = reinterpret_cast<uint32_t*>(pk);
-#pragma unroll
-              for (int e = 0; e < 16; ++e) {
-                __nv_bfloat162 hv = __floats2bfloat162_rn(v[2 * e] * inv, v[2 * e + 1] * inv);
-                pw[e] = *reinterpret_cast<uint32_t*>(&hv);
-              }
-              uint4* o4 = reinterpret_cast<uint4*>(out + cg * 32);
-#pragma unroll
-              for (int e = 0; e < 4; ++e) o4[e] = pk[e];
-            }
-          }
-          if (nX > 0) {
-            tc_fence_before();
-            mbar_arrive(&o_free[X]);
-          }
-          if (row < n_q)
-            lse[(int64_t)row * Hq + head] = lt > 0.f ? (M + log2f(lt)) * 0.6931471805599453f : -INFINITY;
-        }
-        if (tracing) tr_e += clock64() - tm0;
-      } else {
-        const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
-#pragma unroll 1
-        for (int c = 0; c < DH / 32; ++c) {
-          uint32_t r[32];
-          if (nX > 0) {
-            tmem_ld32(t_o + c * 32, r);
-            tmem_ld_wait();
-          }
-          if (row < n_q) {
-            uint4 pk[4];
-            uint32_t* pw = reinterpret_cast<uint32_t*>(pk);
-#pragma unroll
-            for (int e = 0; e < 16; ++e) {
-              const float o0 = nX > 0 ? __uint_as_float(r[2 * e]) * inv : 0.f;
-              const float o1 = nX > 0 ? __uint_as_float(r[2 * e + 1]) * inv : 0.f;
-              __nv_bfloat162 hv = __floats2bfloat162_rn(o0, o1);
-              pw[e] = *reinterpret_cast<uint32_t*>(&hv);
-            }
-            uint4* o4 = reinterpret_cast<uint4*>(out + c * 32);
-#pragma unroll
-            for (int e = 0; e < 4; ++e) o4[e] = pk[e];
-          }
-        }
-        if (nX > 0) {
-          tc_fence_before();
-          mbar_arrive(&o_free[X]);
-        }
-        if (row < n_q)
-          lse[(int64_t)row * Hq + head] =
-              l_run > 0.f ? (m_run * scale_log2 + log2f(l_run)) * 0.6931471805599453f : -INFINITY;
-      }
-      if (tracing) tr_c += clock64() - te0;
-    }
-    finish();
-    return;
-  }
-  asm volatile(PS_REG_LO ::: "memory");
-  finish();  // warps 2-3
-}
-#undef PS_REG_LO
-#undef PS_REG_HI
 
 // ---- ping-pong kernel: two Q tiles per CTA share every K/V tile ---------------
 //
@@ -1928,562 +1235,7 @@ __global__ void __launch_bounds__(384, 1)
   }
 }
 
-// ---- CTA-pair attention: cta_group::2 MMAs over four Q tiles per pair ---------
-//
-// A cluster of two CTAs (an SM pair) takes one work item: GQA group g, a
-// block of 4R query rows (each CTA: 2 Q tiles of 128 M-rows), a part of the
-// block's causal key range.  Every MMA is a pair MMA with M = 256 (the two
-// CTAs' Q tiles X): S_X = Q_X K^T (N = 64 keys: each CTA stages 32 of the
-// keys) and O_X += P_X V (N = 128 head columns: each CTA stages 64 of them, P
-// from each CTA's TMEM), issued by the leader CTA.  So an SM stages half of
-// each 64-key K/V tile and its shared-memory traffic per 64-key step is
-// S 80 KiB + PV 16 KiB + TMA 16 KiB -- below the port's ~128 B/clk at the
-// tensor pipe's 1024 cycles; the one-CTA ping-pong kernel needs a 128-key
-// S buffer per Q tile and serialises each softmax with its PV and next S.
-//   warp 0      TMA (both CTAs): Q tiles once, K halves (32 keys x 128
-//               columns) two tiles ahead of V halves (64 keys x 64 columns),
-//               6-deep rings; completion on the leader's barriers
-//   warp 1      leader only: MMA issuer.  Per Q tile X: S_X(0), S_X(1), then
-//               per 64-key tile j: PV_X(j), S_X(j+2) into the S buffer PV_X(j)
-//               just read -- S runs two tiles ahead, so both softmax
-//               warpgroups work back to back and concurrently
-//   warps 4-11  softmax of Q tile 0 / 1 (thread = M-row, 64 keys per tile,
-//               arithmetic as attn_pp_kernel), P over the second half of its
-//               S buffer; each warp releases P to the leader's p_full
-// TMEM per CTA: S_{X,b} at X 128 + b 64 (b = tile parity), O_X at 256 + X 128.
-template <int DH>
-struct Pr {
-  static constexpr int BN = 64;
-  static constexpr int KST = 6, VST = 6;
-  static constexpr int THREADS = 384;
-  static constexpr int Q_BYTES = 128 * DH * 2;    // one Q tile (128 M-rows)
-  static constexpr int K_HALF = 32 * DH * 2;      // 32 keys x DH columns
-  static constexpr int V_HALF = BN * (DH / 2) * 2;  // 64 keys x DH/2 columns
-  static constexpr int Q_OFF = 0;
-  static constexpr int K_OFF = 2 * Q_BYTES;
-  static constexpr int V_OFF = K_OFF + KST * K_HALF;
-  static constexpr int BAR_OFF = V_OFF + VST * V_HALF;
-  static constexpr int PLAN_OFF = BAR_OFF + 1024;
-  static constexpr size_t TOTAL = PLAN_OFF + 3 * AT_MAXT * 4;
-  static constexpr int TMEM_COLS = 512;
-  static_assert(DH == 128, "pair kernel: d_head 128");
-  static_assert(4 * BN + 2 * DH <= TMEM_COLS, "TMEM budget");
-};
-
-template <int DH>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
-    attn_pair_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-                     const __grid_constant__ CUtensorMap tmV, const int32_t* __restrict__ q_slot,
-                     const uint8_t* __restrict__ key_pad, __nv_bfloat16* __restrict__ ctx, float* __restrict__ lse,
-                     int n_q, int n_keys, int Hq, int G, float scale_log2, int n_groups, int n_blocks, int target,
-                     int max_parts, float* __restrict__ ws_o, float2* __restrict__ ws_ml, int* __restrict__ counters,
-                     long long* __restrict__ trace, int exp) {
-  using SM = Pr<DH>;
-  constexpr int BN = SM::BN, KST = SM::KST, VST = SM::VST, NT = SM::THREADS;
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* base = smem_raw;
-  if (smem_u32(smem_raw) & 1023) __trap();
-  uint8_t* sQ = base + SM::Q_OFF;
-  uint8_t* sK = base + SM::K_OFF;
-  uint8_t* sV = base + SM::V_OFF;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(base + SM::BAR_OFF);
-  uint64_t* q_full = bars + 0;        // leader: both CTAs' Q tiles
-  uint64_t* k_full = bars + 1;        // [KST] leader: both K halves
-  uint64_t* k_empty = k_full + KST;   // [KST] (both CTAs, multicast commit)
-  uint64_t* v_full = k_empty + KST;   // [VST] leader
-  uint64_t* v_empty = v_full + VST;   // [VST] both
-  uint64_t* s_full = v_empty + VST;   // [2 Q tiles][2 S buffers] both
-  uint64_t* p_full = s_full + 4;      // [2][2] leader: 4 softmax warps x 2 CTAs
-  uint64_t* pv_done = p_full + 4;     // [2] both: one phase per PV of the Q tile
-  uint64_t* o_done = pv_done + 2;     // [2] both: last PV completed
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 2);
-  int* s_kmax = reinterpret_cast<int*>(tmem_slot + 1);  // [2]
-  int* s_item = s_kmax + 2;                             // group, block, part, parts, est
-  int* s_flag = s_item + 5;
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t rank = cluster_ctarank();
-  const int R = 128 / G;  // query rows per Q tile
-  const int RB = 4 * R;   // query rows per pair block
-  const int T = n_blocks;
-  const int item_id = (int)blockIdx.x >> 1;  // one item per cluster
-  pdl_trigger();
-  pdl_wait();
-  if (max_parts > 1) {
-    // items (group, block, key part), longest first -- see attn_tc_kernel
-    int* p_len = reinterpret_cast<int*>(base + SM::PLAN_OFF);
-    int* p_parts = p_len + AT_MAXT;
-    int* p_order = p_parts + AT_MAXT;
-    for (int t = threadIdx.x; t < T; t += NT) {
-      const int kq = q_slot[min((t + 1) * RB, n_q) - 1];
-      const int est = kq < 0 ? 0 : min(kq, n_keys - 1) / BN + 1;
-      const int parts = max(1, min(max_parts, (est + target - 1) / target));
-      p_parts[t] = parts;
-      p_len[t] = (est + parts - 1) / parts;
-    }
-    __syncthreads();
-    for (int t = threadIdx.x; t < T; t += NT) {
-      const int lt = p_len[t];
-      int rk = 0;
-      for (int u = 0; u < T; ++u) rk += (p_len[u] > lt || (p_len[u] == lt && u > t)) ? 1 : 0;
-      p_order[rk] = t;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      int idx = item_id;
-      s_item[0] = -1;
-      for (int r = 0; r < T; ++r) {
-        const int t = p_order[r], c = n_groups * p_parts[t];
-        if (idx < c) {
-          s_item[0] = idx % n_groups;
-          s_item[1] = t;
-          s_item[2] = idx / n_groups;
-          s_item[3] = p_parts[t];
-          s_item[4] = p_len[t] * p_parts[t];
-          break;
-        }
-        idx -= c;
-      }
-    }
-  } else if (threadIdx.x == 0) {
-    s_item[0] = item_id % n_groups;
-    s_item[1] = T - 1 - item_id / n_groups;
-    s_item[2] = 0;
-    s_item[3] = 1;
-    s_item[4] = 0;
-  }
-  __syncthreads();
-  const int g = s_item[0];
-  if (g < 0) return;  // (both CTAs of the cluster: same item)
-  const int blk = s_item[1], part = s_item[2], parts = s_item[3], est = s_item[4];
-  const int row0 = blk * RB;
-
-  if (threadIdx.x < 2) s_kmax[threadIdx.x] = -1;
-  if (warp == 0 && lane == 0) {
-    tma_prefetch(&tmQ);
-    tma_prefetch(&tmK);
-    tma_prefetch(&tmV);
-    mbar_init(q_full, 1);
-    for (int s = 0; s < KST; ++s) {
-      mbar_init(&k_full[s], 1);
-      mbar_init(&k_empty[s], 1);
-    }
-    for (int s = 0; s < VST; ++s) {
-      mbar_init(&v_full[s], 1);
-      mbar_init(&v_empty[s], 1);
-    }
-    for (int i = 0; i < 4; ++i) {
-      mbar_init(&s_full[i], 1);
-      mbar_init(&p_full[i], 8);
-    }
-    for (int x = 0; x < 2; ++x) {
-      mbar_init(&pv_done[x], 1);
-      mbar_init(&o_done[x], 1);
-    }
-    fence_barrier_init();
-  }
-  if (warp == 1) tmem_alloc_pair<SM::TMEM_COLS>(tmem_slot);
-  __syncthreads();
-  // causal key range of Q tile X over both CTAs' rows (pair MMAs share it):
-  // row0 + t, t = rank' 2R + X R + i
-  if (threadIdx.x < RB) {
-    const int r = row0 + threadIdx.x;
-    if (r < n_q) atomicMax(&s_kmax[(threadIdx.x % (2 * R)) / R], min(q_slot[r], n_keys - 1));
-  }
-  tc_fence_before();
-  cluster_sync();  // barriers of both CTAs initialised, TMEM allocated, key ranges known
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-  const int ntot0 = s_kmax[0] < 0 ? 0 : s_kmax[0] / BN + 1;
-  const int ntot1 = s_kmax[1] < 0 ? 0 : s_kmax[1] / BN + 1;
-  const int ntot = max(ntot0, ntot1);
-  const bool split = parts > 1;
-  const int t0 = split ? min(part * est / parts, ntot) : 0;
-  const int t1 = !split || part == parts - 1 ? ntot : min((part + 1) * est / parts, ntot);
-  const int n0 = max(0, min(t1, ntot0) - t0), n1 = max(0, min(t1, ntot1) - t0);
-  const int nmax = max(n0, n1);
-  const bool tracing = trace != nullptr;
-  long long tr_a = 0, tr_b = 0, tr_c = 0;
-  long long t_begin = 0;
-  if (tracing && threadIdx.x == 128) asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_begin));
-
-  if (warp == 0) {
-    if (lane == 0 && nmax > 0) {
-      const uint32_t qb = mapa_shared(smem_u32(q_full), 0);
-      if (rank == 0) mbar_expect_tx(q_full, 4 * SM::Q_BYTES);
-#pragma unroll
-      for (int x = 0; x < 2; ++x)
-#pragma unroll
-        for (int a = 0; a < DH / 64; ++a)
-          tma_load_3d_pair(sQ + x * SM::Q_BYTES + a * 128 * 128, &tmQ, qb, a * 64, g * G,
-                           row0 + (int)rank * 2 * R + x * R);
-      int kc = 0, vc = 0;
-      auto load_k = [&](int t) {
-        const int ks = kc % KST;
-        twait(&k_empty[ks], ((kc / KST) & 1) ^ 1, tracing, tr_a);
-        ++kc;
-        if (rank == 0) mbar_expect_tx(&k_full[ks], 2 * SM::K_HALF);
-        const uint32_t kb = mapa_shared(smem_u32(&k_full[ks]), 0);
-#pragma unroll
-        for (int a = 0; a < DH / 64; ++a)
-          tma_load_2d_pair(sK + ks * SM::K_HALF + a * 32 * 128, &tmK, kb, g * DH + a * 64,
-                           (t0 + t) * BN + (int)rank * 32);
-      };
-      load_k(0);
-      if (nmax > 1) load_k(1);
-      for (int t = 0; t < nmax; ++t) {
-        const int vs = vc % VST;
-        twait(&v_empty[vs], ((vc / VST) & 1) ^ 1, tracing, tr_b);
-        ++vc;
-        if (rank == 0) mbar_expect_tx(&v_full[vs], 2 * SM::V_HALF);
-        tma_load_2d_pair(sV + vs * SM::V_HALF, &tmV, mapa_shared(smem_u32(&v_full[vs]), 0),
-                         g * DH + (int)rank * (DH / 2), (t0 + t) * BN);
-        if (t + 2 < nmax) load_k(t + 2);
-      }
-    }
-  } else if (warp == 1) {
-    if (lane == 0 && rank == 0 && nmax > 0) {
-      constexpr uint32_t id_s = idesc_bf16(256, BN, false);
-      constexpr uint32_t id_o = idesc_bf16(256, DH, true);
-      const int nx[2] = {n0, n1};
-      int kc = 0, vc = 0;
-      auto issue_s = [&](int x, int b, int ks) {
-        if (!(exp & 2))  // (timing experiment 2: no MMAs)
-#pragma unroll
-        for (int kk = 0; kk < DH / 16; ++kk) {
-          const int a = kk >> 2, w = kk & 3;
-          const uint64_t bd = desc_sw128(sK + ks * SM::K_HALF + a * 32 * 128) + 2 * w;
-          const uint64_t ad = desc_sw128(sQ + x * SM::Q_BYTES + a * 128 * 128) + 2 * w;
-          mma_bf16_pair(tmem + x * 2 * BN + b * BN, ad, bd, id_s, kk > 0);
-        }
-        mma_commit_pair(&s_full[x * 2 + b], 0x3);
-      };
-      twait(q_full, 0, tracing, tr_b);
-      for (int t = 0; t < min(2, nmax); ++t) {
-        const int ks = kc % KST;
-        twait(&k_full[ks], (kc / KST) & 1, tracing, tr_b);
-        tc_fence_after();
-#pragma unroll
-        for (int x = 0; x < 2; ++x)
-          if (t < nx[x]) issue_s(x, t & 1, ks);
-        mma_commit_pair(&k_empty[ks], 0x3);
-        ++kc;
-      }
-      for (int j = 0; j < nmax; ++j) {
-        const int vs = vc % VST;
-        bool v_ready = false, k_ready = false;
-#pragma unroll
-        for (int x = 0; x < 2; ++x) {
-          if (j >= nx[x]) continue;
-          const int b = j & 1;
-          twait(&p_full[x * 2 + b], (j >> 1) & 1, tracing, tr_a);
-          if (!v_ready) {
-            twait(&v_full[vs], (vc / VST) & 1, tracing, tr_b);
-            v_ready = true;
-          }
-          tc_fence_after();
-          const uint32_t t_o = tmem + 4 * BN + x * DH, t_p = tmem + x * 2 * BN + b * BN + BN / 2;
-          if (!(exp & 2))
-#pragma unroll
-          for (int kk = 0; kk < BN / 16; ++kk) {
-            // B = this CTA's DH/2 head columns of V (MN-major, one 64-element atom)
-            const uint64_t bd = desc_sw128_mn(sV + vs * SM::V_HALF + kk * 16 * 128, BN * 128);
-            mma_bf16_ts_pair(t_o, t_p + kk * 8, bd, id_o, (j > 0 || kk > 0) ? 1u : 0u);
-          }
-          mma_commit_pair(&pv_done[x], 0x3);
-          if (j + 2 < nx[x]) {
-            if (!k_ready) {
-              twait(&k_full[kc % KST], (kc / KST) & 1, tracing, tr_b);
-              tc_fence_after();
-              k_ready = true;
-            }
-            issue_s(x, b, kc % KST);
-          }
-          if (j == nx[x] - 1) mma_commit_pair(&o_done[x], 0x3);
-        }
-        mma_commit_pair(&v_empty[vs], 0x3);
-        ++vc;
-        if (k_ready) {
-          mma_commit_pair(&k_empty[kc % KST], 0x3);
-          ++kc;
-        }
-      }
-    }
-  } else if (warp >= 4) {
-    // ---- softmax of Q tile X: thread = M-row m, 64 keys per tile ------------
-    const int X = (warp - 4) >> 2;
-    const int q4 = warp & 3;  // TMEM lane quarter
-    const int m = q4 * 32 + lane;
-    const int row = row0 + (int)rank * 2 * R + X * R + m / G;
-    const int head = g * G + m % G;
-    const int lim = row < n_q ? min(q_slot[row], n_keys - 1) : -1;
-    const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
-    const uint32_t t_s0 = tmem + X * 2 * BN + lane_off, t_o = tmem + 4 * BN + X * DH + lane_off;
-    const int nX = X == 0 ? n0 : n1;
-    const uint64_t sl2 = f2_pack(scale_log2, scale_log2);
-    float m_run = -INFINITY, l_run = 0.f;
-    constexpr float kRescaleLog2 = 8.f;
-    for (int j = 0; j < nX; ++j) {
-      const int b = j & 1;
-      const uint32_t t_s = t_s0 + b * BN;
-      twait(&s_full[X * 2 + b], (j >> 1) & 1, tracing, tr_a);
-      if (exp & 1) {  // (timing experiment 1: no softmax work)
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&p_full[X * 2 + b]), 0));
-        continue;
-      }
-      const long long tb0 = tracing ? clock64() : 0;
-      tc_fence_after();
-      float s[BN];
-      tmem_ld32(t_s, *reinterpret_cast<uint32_t(*)[32]>(&s[0]));
-      tmem_ld32(t_s + 32, *reinterpret_cast<uint32_t(*)[32]>(&s[32]));
-      tmem_ld_wait();
-      const int j0 = (t0 + j) * BN;
-      const int lim_rel = lim - j0;
-      if (key_pad != nullptr) {
-#pragma unroll
-        for (int u = 0; u < BN / 16; ++u) {
-          uint4 w = make_uint4(0u, 0u, 0u, 0u);
-          const int kb = j0 + u * 16;
-          if (kb + 16 <= n_keys) {
-            w = __ldg(reinterpret_cast<const uint4*>(key_pad + kb));
-          } else {
-            uint8_t* wb = reinterpret_cast<uint8_t*>(&w);
-            for (int e = 0; e < 16; ++e) wb[e] = kb + e < n_keys ? key_pad[kb + e] : 1;
-          }
-          const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-          for (int e = 0; e < 16; ++e) {
-            const int c = u * 16 + e;
-            const bool padded = ((ww[e >> 2] >> (8 * (e & 3))) & 0xffu) != 0u;
-            s[c] = (c <= lim_rel && !padded) ? s[c] : -INFINITY;
-          }
-        }
-      } else if (lim_rel < BN - 1) {
-#pragma unroll
-        for (int c = 0; c < BN; ++c) s[c] = (c <= lim_rel) ? s[c] : -INFINITY;
-      }
-      float mx[8];
-#pragma unroll
-      for (int e = 0; e < 8; ++e) mx[e] = fmax3(s[e], s[8 + 2 * e], s[9 + 2 * e]);
-#pragma unroll
-      for (int c = 24; c < BN; c += 16) {
-#pragma unroll
-        for (int e = 0; e < 8; ++e) mx[e] = fmax3(mx[e], s[c + 2 * e], s[c + 2 * e + 1]);
-      }
-      const float tmax = fmax3(fmax3(mx[0], mx[1], mx[2]), fmax3(mx[3], mx[4], mx[5]), fmaxf(mx[6], mx[7]));
-      bool grow = false;
-      float alpha = 1.f;
-      if (m_run == -INFINITY) {
-        m_run = tmax;
-      } else if ((tmax - m_run) * scale_log2 > kRescaleLog2) {
-        grow = true;
-        alpha = ex2_fast((m_run - tmax) * scale_log2);
-        l_run *= alpha;
-        m_run = tmax;
-      }
-      const float nb = (m_run == -INFINITY) ? 0.f : -m_run * scale_log2;
-      const uint64_t nb2 = f2_pack(nb, nb);
-      uint64_t acc[4] = {0ull, 0ull, 0ull, 0ull};
-      uint32_t pt[BN / 2];
-#pragma unroll
-      for (int e = 0; e < BN / 2; ++e) {
-        const uint64_t x2 = ffma2(f2_pack(s[2 * e], s[2 * e + 1]), sl2, nb2);
-        uint64_t p2;
-        if ((e & 7) >= 6) {  // a quarter of the exponentials on the FMA pipe
-          p2 = ex2_poly2(x2);
-        } else {
-          float x0, x1;
-          f2_unpack(x2, x0, x1);
-          p2 = f2_pack(ex2_fast(x0), ex2_fast(x1));
-        }
-        acc[e & 3] = fadd2(acc[e & 3], p2);
-        float p0, p1;
-        f2_unpack(p2, p0, p1);
-        __nv_bfloat162 hv = __floats2bfloat162_rn(p0, p1);
-        pt[e] = *reinterpret_cast<uint32_t*>(&hv);
-      }
-      tmem_st_cols<BN / 2>(t_s + BN / 2, pt);  // P over the second half of this S buffer (read above)
-      if (__any_sync(0xffffffffu, grow)) {
-        // O_X *= alpha once PV_X(j-1) has completed (phase j - 1 of pv_done;
-        // PV_X(j-2) completed before S_X(j) was issued: the parity is exact)
-        twait(&pv_done[X], (j - 1) & 1, tracing, tr_c);
-        tc_fence_after();
-        const uint64_t a2 = f2_pack(alpha, alpha);
-#pragma unroll 1
-        for (int c = 0; c < DH / 32; ++c) {
-          uint32_t r[32];
-          tmem_ld32(t_o + c * 32, r);
-          tmem_ld_wait();
-#pragma unroll
-          for (int e = 0; e < 16; ++e) {
-            float o0, o1;
-            f2_unpack(fmul2(f2_pack(__uint_as_float(r[2 * e]), __uint_as_float(r[2 * e + 1])), a2), o0, o1);
-            r[2 * e] = __float_as_uint(o0);
-            r[2 * e + 1] = __float_as_uint(o1);
-          }
-          tmem_st32(t_o + c * 32, r);
-        }
-      }
-      tmem_st_wait();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&p_full[X * 2 + b]), 0));
-      if (tracing) tr_b += clock64() - tb0;
-      const uint64_t a01 = fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3]));
-      float sa, sb;
-      f2_unpack(a01, sa, sb);
-      l_run += sa + sb;
-    }
-    if (nX > 0) {
-      mbar_wait(&o_done[X], 0);
-      tc_fence_after();
-    }
-    __nv_bfloat16* out = ctx + ((int64_t)row * Hq + head) * DH;
-    if (split) {
-      // park this part's partial ([part][column / 4][512 M-rows of the pair][4]);
-      // the last part of this CTA's rows to finish merges them in part order
-      const int key = g * T + blk, mm = (int)rank * 256 + X * 128 + m;
-      const bool any = nX > 0 && m_run != -INFINITY;
-      float4* my_o = reinterpret_cast<float4*>(ws_o) + ((int64_t)key * AT_MAXP + part) * (DH / 4) * 512 + mm;
-#pragma unroll 1
-      for (int c = 0; c < DH / 32; ++c) {
-        uint32_t r[32];
-        if (nX > 0) {
-          tmem_ld32(t_o + c * 32, r);
-          tmem_ld_wait();
-        }
-#pragma unroll
-        for (int e = 0; e < 8; ++e)
-          __stcg(my_o + (c * 8 + e) * 512,
-                 any ? make_float4(__uint_as_float(r[4 * e]), __uint_as_float(r[4 * e + 1]),
-                                   __uint_as_float(r[4 * e + 2]), __uint_as_float(r[4 * e + 3]))
-                     : make_float4(0.f, 0.f, 0.f, 0.f));
-      }
-      __stcg(&ws_ml[((int64_t)key * AT_MAXP + part) * 512 + mm],
-             make_float2(any ? m_run * scale_log2 : -INFINITY, any ? l_run : 0.f));
-      __threadfence();
-      asm volatile("bar.sync 1, 256;" ::: "memory");
-      if (warp == 4 && lane == 0) {
-        int* cnt = counters + 2 * key + (int)rank;
-        const int prev = atomicAdd(cnt, 1);
-        *s_flag = prev;
-        if (prev == parts - 1) *cnt = 0;  // reset for the next launch
-      }
-      asm volatile("bar.sync 1, 256;" ::: "memory");
-      if (*s_flag == parts - 1) {
-        __threadfence();
-        float mp[AT_MAXP], w[AT_MAXP], lp[AT_MAXP];
-        float M = -INFINITY;
-#pragma unroll
-        for (int p = 0; p < AT_MAXP; ++p) {
-          const float2 ml = p < parts ? __ldcg(&ws_ml[((int64_t)key * AT_MAXP + p) * 512 + mm])
-                                      : make_float2(-INFINITY, 0.f);
-          mp[p] = ml.x;
-          lp[p] = ml.y;
-          M = fmaxf(M, ml.x);
-        }
-        float lt = 0.f;
-#pragma unroll
-        for (int p = 0; p < AT_MAXP; ++p) {
-          w[p] = mp[p] == -INFINITY ? 0.f : exp2f(mp[p] - M);
-          lt = fmaf(lp[p], w[p], lt);
-        }
-        const float inv = lt > 0.f ? 1.f / lt : 0.f;
-        if (row < n_q) {
-#pragma unroll 1
-          for (int cg = 0; cg < DH / 32; ++cg) {
-            float v[32];
-#pragma unroll
-            for (int e = 0; e < 32; ++e) v[e] = 0.f;
-#pragma unroll
-            for (int p = 0; p < AT_MAXP; ++p) {
-              if (p < parts) {
-                const float4* op = reinterpret_cast<const float4*>(ws_o) +
-                                   ((int64_t)key * AT_MAXP + p) * (DH / 4) * 512 + (cg * 8) * 512 + mm;
-                float4 a[8];
-#pragma unroll
-                for (int e = 0; e < 8; ++e) a[e] = __ldcg(op + e * 512);
-#pragma unroll
-                for (int e = 0; e < 8; ++e) {
-                  v[4 * e] = fmaf(a[e].x, w[p], v[4 * e]);
-                  v[4 * e + 1] = fmaf(a[e].y, w[p], v[4 * e + 1]);
-                  v[4 * e + 2] = fmaf(a[e].z, w[p], v[4 * e + 2]);
-                  v[4 * e + 3] = fmaf(a[e].w, w[p], v[4 * e + 3]);
-                }
-              }
-            }
-            uint4 pk[4];
-            uint32_t* pw = reinterpret_cast<uint32_t*>(pk);
-#pragma unroll
-            for (int e = 0; e < 16; ++e) {
-              __nv_bfloat162 hv = __floats2bfloat162_rn(v[2 * e] * inv, v[2 * e + 1] * inv);
-              pw[e] = *reinterpret_cast<uint32_t*>(&hv);
-            }
-            uint4* o4 = reinterpret_cast<uint4*>(out + cg * 32);
-#pragma unroll
-            for (int e = 0; e < 4; ++e) o4[e] = pk[e];
-          }
-          lse[(int64_t)row * Hq + head] = lt > 0.f ? (M + log2f(lt)) * 0.6931471805599453f : -INFINITY;
-        }
-      }
-    } else {
-      const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
-#pragma unroll 1
-      for (int c = 0; c < DH / 32; ++c) {
-        uint32_t r[32];
-        if (nX > 0) {
-          tmem_ld32(t_o + c * 32, r);
-          tmem_ld_wait();
-        }
-        if (row < n_q) {
-          uint4 pk[4];
-          uint32_t* pw = reinterpret_cast<uint32_t*>(pk);
-#pragma unroll
-          for (int e = 0; e < 16; ++e) {
-            const float o0 = nX > 0 ? __uint_as_float(r[2 * e]) * inv : 0.f;
-            const float o1 = nX > 0 ? __uint_as_float(r[2 * e + 1]) * inv : 0.f;
-            __nv_bfloat162 hv = __floats2bfloat162_rn(o0, o1);
-            pw[e] = *reinterpret_cast<uint32_t*>(&hv);
-          }
-          uint4* o4 = reinterpret_cast<uint4*>(out + c * 32);
-#pragma unroll
-          for (int e = 0; e < 4; ++e) o4[e] = pk[e];
-        }
-      }
-      if (row < n_q)
-        lse[(int64_t)row * Hq + head] =
-            l_run > 0.f ? (m_run * scale_log2 + log2f(l_run)) * 0.6931471805599453f : -INFINITY;
-    }
-  }
-  if (tracing) {
-    long long* tr = trace + 24 * (int64_t)blockIdx.x;
-    if (threadIdx.x == 128 || threadIdx.x == 256) {  // softmax X = 0 / 1: s_full wait, busy, pv wait
-      const int o = threadIdx.x == 128 ? 4 : 7;
-      tr[o] = tr_a; tr[o + 1] = tr_b; tr[o + 2] = tr_c;
-    }
-    if (threadIdx.x == 32) { tr[10] = tr_a; tr[11] = tr_b; }  // mma: p_full, k/v/q waits
-    if (threadIdx.x == 0) { tr[12] = tr_a; tr[13] = tr_b; }   // producer: k_empty, v_empty
-  }
-  tc_fence_before();
-  cluster_sync();  // the leader's last MMAs read this CTA's smem / write its TMEM
-  if (tracing && threadIdx.x == 128) {
-    long long* tr = trace + 24 * (int64_t)blockIdx.x;
-    long long t_end;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_end));
-    int smid;
-    asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
-    tr[0] = nmax; tr[1] = t_begin; tr[2] = t_end; tr[3] = smid;
-  }
-  if (warp == 1) {
-    tc_fence_after();
-    tmem_dealloc_pair<SM::TMEM_COLS>(tmem);
-  }
-}
-
 long long* g_attn_trace = nullptr;  // debug: per-CTA (n_tiles, start, end, sm, stalls)
-int g_ps_min_share = 12;            // CCB_ATTN_MINSHARE: smallest share of tile pairs per CTA (persistent kernel)
 
 // zero-initialised pair counters of the split-KV merge, one array per stream
 // (the merging CTA resets its counter, so they stay zero between launches)
@@ -2615,56 +1367,6 @@ int launch(const void* q, const void* k, const void* v, const int32_t* q_slot, c
                   row_tiles, target, max_parts, ws_o, ws_ml, counters, attn_exp());
 }
 
-template <int DH>
-int launch_ps(const void* q, const void* k, const void* v, const int32_t* q_slot, const uint8_t* key_pad, void* ctx,
-              float* lse, int n_q, int n_keys, int Hq, int Hkv, cudaStream_t st) {
-  using SM = Ps<DH>;
-  constexpr int BN = SM::BN;
-  const int G = Hq / Hkv;
-  const int R = 128 / G;
-  if (key_pad != nullptr && (reinterpret_cast<uintptr_t>(key_pad) & 15))
-    return fail(CC_E_UNSUP, "attention_tc: key_pad must be 16-byte aligned");
-  const int blocks = (n_q + 2 * R - 1) / (2 * R);
-  if (blocks > SM::MAXB) return fail(CC_E_UNSUP, "attention_tc: too many query rows for the persistent plan");
-  CUtensorMap mq, mk, mv;
-  {
-    cuuint64_t dims[3] = {(cuuint64_t)DH, (cuuint64_t)Hq, (cuuint64_t)n_q};
-    cuuint64_t strides[2] = {(cuuint64_t)DH * 2, (cuuint64_t)Hq * DH * 2};
-    cuuint32_t box[3] = {64, (cuuint32_t)G, (cuuint32_t)R};
-    int rc = encode(&mq, 3, q, dims, strides, box);
-    if (rc) return rc;
-  }
-  {
-    cuuint64_t dims[2] = {(cuuint64_t)Hkv * DH, (cuuint64_t)n_keys};
-    cuuint64_t strides[1] = {(cuuint64_t)Hkv * DH * 2};
-    cuuint32_t box[2] = {64, (cuuint32_t)BN};
-    int rc = encode(&mk, 2, k, dims, strides, box);
-    if (rc) return rc;
-    rc = encode(&mv, 2, v, dims, strides, box);
-    if (rc) return rc;
-  }
-  if (int rc = ensure_smem(attn_ps_kernel<DH>, SM::TOTAL)) return rc;
-  const int grid = num_sms();
-  // shares of at least min_share tile pairs, and at least 1/8 of the longest
-  // item (a split item merges at most 8 parts)
-  const int max_len = (n_keys + BN - 1) / BN;
-  static const int env_share = getenv("CCB_ATTN_MINSHARE") ? atoi(getenv("CCB_ATTN_MINSHARE")) : 0;
-  int min_share = std::max(env_share > 0 ? env_share : g_ps_min_share, (max_len + 6) / 7);
-  const size_t items = (size_t)Hkv * blocks;
-  const size_t bytes = (size_t)2 * grid * 256 * (DH * sizeof(float) + sizeof(float2));
-  uint8_t* scratch = (uint8_t*)stream_scratch(st, SCR_ATTN, bytes);
-  int* counters = split_counters(st, (int)(4 * items));  // per (item, Q tile): ticket, ready
-  if (!scratch || !counters) return fail(CC_E_CUDA, "attention_tc: split workspace allocation failed");
-  float* ws_o = reinterpret_cast<float*>(scratch);
-  float2* ws_ml = reinterpret_cast<float2*>(scratch + (size_t)2 * grid * 256 * DH * sizeof(float));
-  const float scale_log2 = 1.4426950408889634f / sqrtf((float)DH);
-  static const int env_k0 = getenv("CCB_ATTN_SEGCOST") ? atoi(getenv("CCB_ATTN_SEGCOST")) : -1;
-  const int k0 = env_k0 >= 0 ? env_k0 : 1;  // fixed cost of a segment, in tile pairs
-  return launch_k(attn_ps_kernel<DH>, dim3(grid), dim3(SM::THREADS), SM::TOTAL, st, "attention_ps", mq, mk, mv, q_slot,
-                  key_pad, (__nv_bfloat16*)ctx, lse, n_q, n_keys, Hq, G, scale_log2, Hkv, blocks, min_share, k0, ws_o,
-                  ws_ml, counters, g_attn_trace, attn_exp());
-}
-
 template <int DH, int PF = 2>
 int launch_pp(const void* q, const void* k, const void* v, const int32_t* q_slot, const uint8_t* key_pad, void* ctx,
               float* lse, int n_q, int n_keys, int Hq, int Hkv, cudaStream_t st) {
@@ -2730,72 +1432,6 @@ int launch_pp(const void* q, const void* k, const void* v, const int32_t* q_slot
                   ws_o, ws_ml, counters, g_attn_trace);
 }
 
-template <int DH>
-int launch_pair(const void* q, const void* k, const void* v, const int32_t* q_slot, const uint8_t* key_pad, void* ctx,
-                float* lse, int n_q, int n_keys, int Hq, int Hkv, cudaStream_t st) {
-  using SM = Pr<DH>;
-  constexpr int BN = SM::BN;
-  const int G = Hq / Hkv;
-  const int R = 128 / G;
-  if (key_pad != nullptr && (reinterpret_cast<uintptr_t>(key_pad) & 15))
-    return fail(CC_E_UNSUP, "attention_tc: key_pad must be 16-byte aligned");
-  CUtensorMap mq, mk, mv;
-  {
-    cuuint64_t dims[3] = {(cuuint64_t)DH, (cuuint64_t)Hq, (cuuint64_t)n_q};
-    cuuint64_t strides[2] = {(cuuint64_t)DH * 2, (cuuint64_t)Hq * DH * 2};
-    cuuint32_t box[3] = {64, (cuuint32_t)G, (cuuint32_t)R};
-    int rc = encode(&mq, 3, q, dims, strides, box);
-    if (rc) return rc;
-  }
-  {
-    cuuint64_t dims[2] = {(cuuint64_t)Hkv * DH, (cuuint64_t)n_keys};
-    cuuint64_t strides[1] = {(cuuint64_t)Hkv * DH * 2};
-    cuuint32_t kbox[2] = {64, 32};  // half a 64-key K tile per CTA
-    int rc = encode(&mk, 2, k, dims, strides, kbox);
-    if (rc) return rc;
-    cuuint32_t vbox[2] = {64, (cuuint32_t)BN};  // 64 keys x DH/2 columns per CTA
-    rc = encode(&mv, 2, v, dims, strides, vbox);
-    if (rc) return rc;
-  }
-  if (int rc = ensure_smem(attn_pair_kernel<DH>, SM::TOTAL)) return rc;
-  const int blocks = (n_q + 4 * R - 1) / (4 * R);
-  // key splits when the (group, block) pairs leave SM pairs idle (see launch<>)
-  const int slots = num_sms() / 2;
-  const int max_tiles = (n_keys + BN - 1) / BN;
-  int target = max_tiles, max_parts = 1;
-  if (blocks <= AT_MAXT && max_tiles > 0 && Hkv * blocks < slots) {
-    max_parts = std::max(1, std::min(AT_MAXP, (slots + Hkv * blocks - 1) / (Hkv * blocks)));
-    target = std::max(16, (max_tiles + max_parts - 1) / max_parts);
-    max_parts = std::min(max_parts, (max_tiles + target - 1) / target);
-    if (max_parts < 1) max_parts = 1;
-  }
-  if (getenv("CCB_ATTN_NOSPLIT")) max_parts = 1;
-  if (const char* e = getenv("CCB_ATTN_SPLIT")) {  // experiments: "target,max_parts"
-    int a = 0, b = 0;
-    if (sscanf(e, "%d,%d", &a, &b) == 2 && a > 0 && b >= 1 && b <= AT_MAXP && blocks <= AT_MAXT) {
-      target = a;
-      max_parts = b;
-    }
-  }
-  float* ws_o = nullptr;
-  float2* ws_ml = nullptr;
-  int* counters = nullptr;
-  if (max_parts > 1) {
-    const size_t keys = (size_t)Hkv * blocks;
-    const size_t bytes = keys * AT_MAXP * 512 * (DH * sizeof(float) + sizeof(float2));
-    uint8_t* scratch = (uint8_t*)stream_scratch(st, SCR_ATTN, bytes);
-    counters = split_counters(st, (int)(2 * keys));
-    if (!scratch || !counters) return fail(CC_E_CUDA, "attention_tc: split workspace allocation failed");
-    ws_o = reinterpret_cast<float*>(scratch);
-    ws_ml = reinterpret_cast<float2*>(scratch + keys * AT_MAXP * 512 * DH * sizeof(float));
-  }
-  dim3 grid(2 * Hkv * blocks * max_parts);
-  const float scale_log2 = 1.4426950408889634f / sqrtf((float)DH);
-  return launch_k(attn_pair_kernel<DH>, grid, dim3(SM::THREADS), SM::TOTAL, st, "attention_pair", mq, mk, mv, q_slot,
-                  key_pad, (__nv_bfloat16*)ctx, lse, n_q, n_keys, Hq, G, scale_log2, Hkv, blocks, target, max_parts,
-                  ws_o, ws_ml, counters, g_attn_trace, attn_exp());
-}
-
 // Kernel shape per launch: 0 = 128-key tiles, two softmax warpgroups (one
 // CTA per SM); 1 = 64-key tiles, one warpgroup; 2 = 64-key tiles, two
 // warpgroups (both two CTAs per SM); 3 = 128-key tiles, one warpgroup.
@@ -2808,10 +1444,7 @@ int launch_variant(int variant, const void* q, const void* k, const void* v, con
     case 2: return launch<DH, 64, 2>(q, k, v, q_slot, key_pad, ctx, lse, n_q, n_keys, Hq, Hkv, st);
     case 3: return launch<DH, 128, 1>(q, k, v, q_slot, key_pad, ctx, lse, n_q, n_keys, Hq, Hkv, st);
     case 4: return launch_pp<DH>(q, k, v, q_slot, key_pad, ctx, lse, n_q, n_keys, Hq, Hkv, st);
-    case 5: return launch_ps<DH>(q, k, v, q_slot, key_pad, ctx, lse, n_q, n_keys, Hq, Hkv, st);
-    case 6:
-      if constexpr (DH == 128) return launch_pair<DH>(q, k, v, q_slot, key_pad, ctx, lse, n_q, n_keys, Hq, Hkv, st);
-      return fail(CC_E_UNSUP, "attention_tc: the CTA-pair kernel needs d_head 128");
+
 
     default: return launch<DH, 128, 2>(q, k, v, q_slot, key_pad, ctx, lse, n_q, n_keys, Hq, Hkv, st);
   }
