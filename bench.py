@@ -412,9 +412,10 @@ def torch_reference_full(model, tokens):
             o = attn(q, k, v).reshape(n, H * dh)
             h = h + (o @ lw["w_o"].T).float()
             x = F.rms_norm(h, (d,), lw["mlp_norm"], cfg.rms_eps).bfloat16()
-            gu = (x @ lw["w_gu"].T).view(n, ff // 64, 2, 64)
-            a = (F.silu(gu[:, :, 0].float()) * gu[:, :, 1].float()).bfloat16().reshape(n, ff)
-            h = h + (a @ lw["w_down"].T).float()
+            for i0 in range(0, n, 4096):  # (row blocks: the 70B full-recompute temporaries fit beside 140 GB of weights)
+                gu = (x[i0:i0 + 4096] @ lw["w_gu"].T).view(-1, ff // 64, 2, 64)
+                a = (F.silu(gu[:, :, 0].float()) * gu[:, :, 1].float()).bfloat16().reshape(-1, ff)
+                h[i0:i0 + 4096] += (a @ lw["w_down"].T).float()
         last = F.rms_norm(h[-1:], (d,), model.w["final_norm"], cfg.rms_eps).bfloat16()
         return (last @ model.w["unembed_t"].T).argmax()
 
