@@ -929,6 +929,28 @@ def main():
         api["speedup_ttft_vs_prefix_cache"] = round(api["prefix_cache_60pct"]["ttft_p50_ms"]
                                                     / api["fix_up_15pct"]["ttft_p50_ms"], 3)
         baselines["public_api_ttft"] = api
+        # K8 on the MISS path (harness.py:331-354): a store miss prefills its
+        # chunks fresh WITH creation statistics (cc_segment_mass: per-row mass
+        # per key segment, recomputed from q / lse; cc_chunk_stats) so the new
+        # variants can be scored.  Same 10 x 512 + 32 request, all chunks new.
+        miss = {}
+        for name, st in (("no_stats", False), ("with_creation_stats", True)):
+            ts = []
+            for i in range(args.warmup + 3):
+                barrier(world)
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                res = cc.prefill(model, full_req(i), record_attention=False, stats=st)
+                if st:
+                    cc.creation_stats(res, list(range(len(chunks) + 1)), list(range(len(chunks))))
+                torch.cuda.synchronize()
+                if i >= args.warmup:
+                    ts.append((time.perf_counter() - t0) * 1e3)
+                del res
+            miss[name + "_ms"] = round(statistics.median(ts), 3)
+        miss["k8_cost_ms"] = round(miss["with_creation_stats_ms"] - miss["no_stats_ms"], 3)
+        miss["k8_share"] = round(miss["k8_cost_ms"] / miss["with_creation_stats_ms"], 4)
+        baselines["miss_path_full_prefill"] = miss
     if not args.no_baselines and not tp_mode:
         toks = torch.from_numpy(np.concatenate(chunks + [question]).astype(np.int64)).cuda()
         run, attn_name = torch_reference_full(model, toks)
