@@ -766,7 +766,11 @@ struct Pp {
 // (A/B at config 2 / full / 32k / 70B rank, us: PF 2 63.9 / 221 / 1153 / 150,
 // PF 0 -- / 258 / 1585 / 181, PF 1 -- / 226 / 1280 / 154, PF 4 -- / 235 /
 // 1350 / 162)
-template <int DH, int PF = 2>
+// RH: registers per softmax thread (setmaxnreg; the TMA/MMA warpgroup keeps
+// 504 - 2 RH).  A/B (us, config 2 / full / 32k / 70B rank): RH 224 62.0 /
+// 205.5 / 1101 / 154, RH 200 61.8 / 209.4 / 1254 / 158, RH 168 (no split)
+// 64.1 / 214.6 / 1236 / 158.
+template <int DH, int PF = 2, int RH = 224>
 __global__ void __launch_bounds__(384, 1)
     attn_pp_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                    const __grid_constant__ CUtensorMap tmV, const int32_t* __restrict__ q_slot,
@@ -896,7 +900,38 @@ __global__ void __launch_bounds__(384, 1)
   long long t_begin = 0;
   if (tracing && threadIdx.x == 128) asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_begin));
 
+  // Each role ends on its own (no control-flow join after the per-role
+  // register allocation below): trace, CTA barrier, TMEM release.
+  auto finish = [&]() {
+    if (tracing) {
+      long long* tr = trace + 24 * (int64_t)blockIdx.x;
+      if (threadIdx.x == 128 || threadIdx.x == 256) {  // softmax X = 0 / 1: s_full wait, busy, epilogue
+        const int o = threadIdx.x == 128 ? 4 : 7;
+        tr[o] = tr_a; tr[o + 1] = tr_b; tr[o + 2] = tr_c;
+      }
+      if (threadIdx.x == 32) { tr[10] = tr_a; tr[11] = tr_b; }  // mma: p_full, k/v/q waits
+      if (threadIdx.x == 0) { tr[12] = tr_a; tr[13] = tr_b; }   // producer: k_empty, v_empty
+    }
+    tc_fence_before();
+    asm volatile("bar.sync 15, 384;" ::: "memory");
+    if (tracing && threadIdx.x == 128) {
+      long long* tr = trace + 24 * (int64_t)blockIdx.x;
+      long long t_end;
+      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_end));
+      int smid;
+      asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+      tr[0] = nmax; tr[1] = t_begin; tr[2] = t_end; tr[3] = smid;
+    }
+    if (warp == 1) {
+      tc_fence_after();
+      tmem_dealloc<SM::TMEM_COLS>(tmem);
+    }
+  };
+  // registers: the TMA / MMA warpgroup needs few, a softmax thread holds a
+  // 128-key S row ((504 - 2 RH) + 2 RH per 128 threads = 3 x 168)
+#define PP_REG_LO "setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(504 - 2 * RH)
   if (warp == 0) {
+    asm volatile(PP_REG_LO : "memory");
     if (lane == 0 && nmax > 0) {
       mbar_expect_tx(q_full, 2 * SM::Q_BYTES);
 #pragma unroll
@@ -919,7 +954,10 @@ __global__ void __launch_bounds__(384, 1)
           tma_load_2d(sV + vs * SM::KV_BYTES + a * BN * 128, &tmV, &v_full[vs], g * DH + a * 64, (t0 + j) * BN);
       }
     }
+    finish();
+    return;
   } else if (warp == 1) {
+    asm volatile(PP_REG_LO : "memory");
     if (lane == 0 && nmax > 0) {
       constexpr uint32_t id_s = idesc_bf16(128, BN, false);
       constexpr uint32_t id_o = idesc_bf16(128, DH, true);
@@ -974,7 +1012,10 @@ __global__ void __launch_bounds__(384, 1)
         if (k_ready) mma_commit(&k_empty[(j + 1) % KST]);
       }
     }
+    finish();
+    return;
   } else if (warp >= 4) {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(RH) : "memory");
     // ---- softmax of Q tile X: thread = M-row m, all BN keys -------------------
     const int X = (warp - 4) >> 2;
     const int q4 = warp & 3;  // TMEM lane quarter
@@ -1209,31 +1250,13 @@ __global__ void __launch_bounds__(384, 1)
             l_run > 0.f ? (m_run * scale_log2 + log2f(l_run)) * 0.6931471805599453f : -INFINITY;
     }
     if (tracing) tr_c += clock64() - te0;
+    finish();
+    return;
   }
-  if (tracing) {
-    long long* tr = trace + 24 * (int64_t)blockIdx.x;
-    if (threadIdx.x == 128 || threadIdx.x == 256) {  // softmax X = 0 / 1: s_full wait, busy, epilogue
-      const int o = threadIdx.x == 128 ? 4 : 7;
-      tr[o] = tr_a; tr[o + 1] = tr_b; tr[o + 2] = tr_c;
-    }
-    if (threadIdx.x == 32) { tr[10] = tr_a; tr[11] = tr_b; }  // mma: p_full, k/v/q waits
-    if (threadIdx.x == 0) { tr[12] = tr_a; tr[13] = tr_b; }   // producer: k_empty, v_empty
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (tracing && threadIdx.x == 128) {
-    long long* tr = trace + 24 * (int64_t)blockIdx.x;
-    long long t_end;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_end));
-    int smid;
-    asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
-    tr[0] = nmax; tr[1] = t_begin; tr[2] = t_end; tr[3] = smid;
-  }
-  if (warp == 1) {
-    tc_fence_after();
-    tmem_dealloc<SM::TMEM_COLS>(tmem);
-  }
+  asm volatile(PP_REG_LO : "memory");
+  finish();  // warps 2-3
 }
+#undef PP_REG_LO
 
 long long* g_attn_trace = nullptr;  // debug: per-CTA (n_tiles, start, end, sm, stalls)
 
@@ -1367,7 +1390,7 @@ int launch(const void* q, const void* k, const void* v, const int32_t* q_slot, c
                   row_tiles, target, max_parts, ws_o, ws_ml, counters, attn_exp());
 }
 
-template <int DH, int PF = 2>
+template <int DH, int PF = 2, int RH = 224>
 int launch_pp(const void* q, const void* k, const void* v, const int32_t* q_slot, const uint8_t* key_pad, void* ctx,
               float* lse, int n_q, int n_keys, int Hq, int Hkv, cudaStream_t st) {
   using SM = Pp<DH>;
@@ -1393,7 +1416,7 @@ int launch_pp(const void* q, const void* k, const void* v, const int32_t* q_slot
     rc = encode(&mv, 2, v, dims, strides, box);
     if (rc) return rc;
   }
-  if (int rc = ensure_smem(attn_pp_kernel<DH, PF>, SM::TOTAL)) return rc;
+  if (int rc = ensure_smem(attn_pp_kernel<DH, PF, RH>, SM::TOTAL)) return rc;
   const int blocks = (n_q + 2 * R - 1) / (2 * R);
   // key splits when the (group, block) grid leaves SMs idle (see launch<>)
   const int slots = num_sms();
@@ -1427,7 +1450,7 @@ int launch_pp(const void* q, const void* k, const void* v, const int32_t* q_slot
   }
   dim3 grid(Hkv * blocks * max_parts);
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)DH);
-  return launch_k(attn_pp_kernel<DH, PF>, grid, dim3(SM::THREADS), SM::TOTAL, st, "attention_pp", mq, mk, mv, q_slot,
+  return launch_k(attn_pp_kernel<DH, PF, RH>, grid, dim3(SM::THREADS), SM::TOTAL, st, "attention_pp", mq, mk, mv, q_slot,
                   key_pad, (__nv_bfloat16*)ctx, lse, n_q, n_keys, Hq, G, scale_log2, Hkv, blocks, target, max_parts,
                   ws_o, ws_ml, counters, g_attn_trace);
 }
@@ -1444,6 +1467,7 @@ int launch_variant(int variant, const void* q, const void* k, const void* v, con
     case 2: return launch<DH, 64, 2>(q, k, v, q_slot, key_pad, ctx, lse, n_q, n_keys, Hq, Hkv, st);
     case 3: return launch<DH, 128, 1>(q, k, v, q_slot, key_pad, ctx, lse, n_q, n_keys, Hq, Hkv, st);
     case 4: return launch_pp<DH>(q, k, v, q_slot, key_pad, ctx, lse, n_q, n_keys, Hq, Hkv, st);
+
 
 
     default: return launch<DH, 128, 2>(q, k, v, q_slot, key_pad, ctx, lse, n_q, n_keys, Hq, Hkv, st);
