@@ -5,12 +5,17 @@
 //   warp 0     TMA K tiles (128 keys, 2-stage ring)
 //   warp 1     tcgen05.mma S = Q K^T into one of two TMEM buffers
 //   warps 2-5  load the CTA's Q rows (gathered by index, written 128B-swizzled
-//              into smem), then per tile: tcgen05.ld S, p = exp2(s*c - lse*log2e)
-//              masked by the causal limit and pads, accumulated per key segment
-//              with a warp-uniform run-length walk over the tile's segment map.
-// Partial sums per (row, kv group) are folded over the G heads of the CTA in
-// fixed order; a second kernel folds the kv groups in fixed order and divides
-// by Hq.  No atomics: run-to-run bit-identical.
+//              into smem), then take the EVEN key tiles, warps 6-9 the ODD
+//              ones (each warpgroup owns one of the two TMEM S buffers):
+//              tcgen05.ld S, p = exp2(s*c - lse*log2e) masked by the causal
+//              limit and pads, accumulated per key segment (a tile inside one
+//              segment: one sum; a tile across boundaries: a warp-uniform walk
+//              over the segments it overlaps) into the warpgroup's own
+//              per-row accumulators.
+// The two warpgroups' sums and the G heads of the CTA are folded in fixed
+// order; a second kernel folds the kv groups in fixed order and divides by
+// Hq.  No atomics: run-to-run bit-identical.  (One warpgroup for all tiles
+// measured latency-bound: the K8 pass cost 16% of a fresh 8B prefill.)
 #include <math.h>
 
 #include "attention.cuh"
@@ -25,7 +30,7 @@ using namespace sm100;
 
 constexpr int ST_BN = 128;
 constexpr int ST_STAGES = 2;
-constexpr int ST_MAXSEG = 128;  // n_seg + 1 (diagonal) <= 128
+constexpr int ST_MAXSEG = 112;  // n_seg + 1 (diagonal) <= 112 (two warpgroups' accumulators in smem)
 
 __host__ __device__ constexpr uint32_t idesc_s(int M, int N) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
@@ -43,25 +48,25 @@ struct StSmem {
   static constexpr int K_BYTES = ST_BN * DH * 2;
   static constexpr int Q_OFF = 0;
   static constexpr int K_OFF = Q_BYTES;
-  static constexpr int ACC_OFF = K_OFF + ST_STAGES * K_BYTES;            // float [128][ST_MAXSEG]
-  static constexpr int SEG_OFF = ACC_OFF + 128 * (ST_MAXSEG + 1) * 4;     // int seg_lo[128], seg_hi[128]
-  static constexpr int BAR_OFF = SEG_OFF + 2 * ST_BN * 4;
-  static constexpr size_t TOTAL = 1024 + BAR_OFF + 256;
+  static constexpr int SEG_OFF = K_OFF + ST_STAGES * K_BYTES;  // int seg_lo[ST_MAXSEG], seg_hi[ST_MAXSEG]
+  static constexpr int BAR_OFF = SEG_OFF + 2 * ST_MAXSEG * 4;
+  static constexpr int ACC_OFF = BAR_OFF + 256;  // float [2 warpgroups][128][stride], stride odd >= n_seg + 1
+  static size_t total(int stride) { return 1024 + ACC_OFF + (size_t)2 * 128 * stride * 4; }
 };
 
 template <int DH>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(320, 1)
     attn_stats_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __nv_bfloat16* __restrict__ q,
                          const int32_t* __restrict__ rows, int n_rows, const int32_t* __restrict__ q_slot,
                          const uint8_t* __restrict__ key_pad, const float* __restrict__ lse,
                          const int32_t* __restrict__ seg_lo, const int32_t* __restrict__ seg_hi, int n_seg,
-                         float* __restrict__ part, int n_keys, int Hq, int Hkv, int G, float scale_log2) {
+                         float* __restrict__ part, int n_keys, int Hq, int Hkv, int G, float scale_log2, int stride) {
   using SM = StSmem<DH>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = base + SM::Q_OFF;
   uint8_t* sK = base + SM::K_OFF;
-  float* acc = reinterpret_cast<float*>(base + SM::ACC_OFF);
+  float* acc = reinterpret_cast<float*>(base + SM::ACC_OFF);  // [2][128][stride]
   int* segmap = reinterpret_cast<int*>(base + SM::SEG_OFF);
   uint64_t* bars = reinterpret_cast<uint64_t*>(base + SM::BAR_OFF);
   uint64_t* q_full = bars;
@@ -71,7 +76,7 @@ __global__ void __launch_bounds__(192, 1)
   uint64_t* s_empty = s_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_empty + 2);
   __shared__ int s_kmax;
-  __shared__ uint32_t padw[8];
+  __shared__ uint32_t padw[2][8];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = blockIdx.x;
@@ -89,7 +94,7 @@ __global__ void __launch_bounds__(192, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&s_full[b], 1);
-      mbar_init(&s_empty[b], 128);
+      mbar_init(&s_empty[b], 128);  // the warpgroup that owns buffer b
     }
     fence_barrier_init();
   }
@@ -99,6 +104,7 @@ __global__ void __launch_bounds__(192, 1)
     const int sr = r0 + threadIdx.x / G;
     if (sr < n_rows) atomicMax(&s_kmax, q_slot[rows[sr]]);
   }
+  (void)SM::ACC_OFF;
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -138,17 +144,18 @@ __global__ void __launch_bounds__(192, 1)
       }
     }
   } else {
+    const int wg = (warp - 2) >> 2;  // 0: even key tiles (S buffer 0), 1: odd tiles (buffer 1)
     const int q4 = warp & 3;
     const int m = q4 * 32 + lane;
-    const int et = threadIdx.x - 64;
+    const int et = threadIdx.x - 64;  // 0..255
     const int sr = r0 + m / G;
     const int head = g * G + m % G;
     const bool valid = sr < n_rows;
     const int qrow = valid ? rows[sr] : 0;
     const int lim = valid ? q_slot[qrow] : -1;
     const float base_l2 = valid ? lse[(int64_t)qrow * Hq + head] * 1.4426950408889634f : 0.f;
-    // gather this M-row's q (dh bf16) into the 128B-swizzled K-major tile
-    {
+    if (wg == 0) {
+      // gather this M-row's q (dh bf16) into the 128B-swizzled K-major tile
       const uint4* src = reinterpret_cast<const uint4*>(q + ((int64_t)qrow * Hq + head) * DH);
 #pragma unroll
       for (int ch = 0; ch < DH / 8; ++ch) {
@@ -159,29 +166,29 @@ __global__ void __launch_bounds__(192, 1)
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mbar_arrive(q_full);
     }
-    float* my = acc + m * (ST_MAXSEG + 1);  // padded stride: no bank conflicts
+    float* my = acc + ((int64_t)wg * 128 + m) * stride;  // odd stride: no bank conflicts
     for (int sg = 0; sg < W; ++sg) my[sg] = 0.f;
     // segment bounds in shared memory (segments are sorted, disjoint slot ranges)
     int* s_lo = segmap;
     int* s_hi = segmap + ST_MAXSEG;
-    for (int sg = et; sg < n_seg; sg += 128) {
+    for (int sg = et; sg < n_seg; sg += 256) {
       s_lo[sg] = seg_lo[sg];
       s_hi[sg] = seg_hi[sg];
     }
-    asm volatile("bar.sync 1, 128;" ::: "memory");
+    asm volatile("bar.sync 1, 256;" ::: "memory");
     float diag = 0.f;
-    for (int i = 0; i < n_tiles; ++i) {
-      const int b = i & 1;
+    for (int i = wg; i < n_tiles; i += 2) {
+      const int b = wg;  // this warpgroup's S buffer
       const int j0 = i * ST_BN;
       uint32_t pw[4] = {0u, 0u, 0u, 0u};
       if (key_pad != nullptr) {
-        // 128-bit pad mask of the tile, built by the 128 threads (double-buffered)
+        // 128-bit pad mask of the tile, built by this warpgroup's 128 threads
         const int jm = j0 + m;  // word q4 of the mask covers keys [32*q4, 32*q4+32)
         const unsigned word = __ballot_sync(0xffffffffu, jm >= n_keys || key_pad[jm] != 0);
-        if (lane == 0) padw[(b << 2) + q4] = word;
-        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (lane == 0) padw[wg][((i >> 1) & 1) * 4 + q4] = word;
+        asm volatile("bar.sync %0, 128;" ::"r"(2 + wg) : "memory");
 #pragma unroll
-        for (int w = 0; w < 4; ++w) pw[w] = padw[(b << 2) + w];
+        for (int w = 0; w < 4; ++w) pw[w] = padw[wg][((i >> 1) & 1) * 4 + w];
       }
       mbar_wait(&s_full[b], (i >> 1) & 1);
       tc_fence_after();
@@ -215,24 +222,31 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll
         for (int c = 0; c < ST_BN; ++c) diag += (c == lim_rel) ? p[c] : 0.f;
       }
-      // each segment overlapping the tile: predicated 8-way-ILP sum over its columns
+      // each segment overlapping the tile: a tile inside one segment is one
+      // 8-way sum; otherwise a predicated sum per overlapping segment
       for (int sg = 0; sg < n_seg; ++sg) {
         const int lo = s_lo[sg] - j0, hi = s_hi[sg] - j0;  // warp-uniform
         if (hi <= 0 || lo >= ST_BN) continue;
         float a8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        if (lo <= 0 && hi >= ST_BN) {
 #pragma unroll
-        for (int c = 0; c < ST_BN; ++c) a8[c & 7] += (c >= lo && c < hi) ? p[c] : 0.f;
+          for (int c = 0; c < ST_BN; ++c) a8[c & 7] += p[c];
+        } else {
+#pragma unroll
+          for (int c = 0; c < ST_BN; ++c) a8[c & 7] += (c >= lo && c < hi) ? p[c] : 0.f;
+        }
         my[sg] += ((a8[0] + a8[1]) + (a8[2] + a8[3])) + ((a8[4] + a8[5]) + (a8[6] + a8[7]));
       }
     }
     my[n_seg] = diag;
-    asm volatile("bar.sync 1, 128;" ::: "memory");
-    // fold the G heads of each row in fixed order -> part[sr][g][W]
-    for (int t = et; t < R * W; t += 128) {
+    asm volatile("bar.sync 1, 256;" ::: "memory");
+    // fold the two warpgroups and the G heads of each row in fixed order -> part[sr][g][W]
+    for (int t = et; t < R * W; t += 256) {
       const int rr = t / W, sg = t % W;
       if (r0 + rr < n_rows) {
         float v = 0.f;
-        for (int h = 0; h < G; ++h) v += acc[(rr * G + h) * (ST_MAXSEG + 1) + sg];
+        for (int h = 0; h < G; ++h)
+          v += acc[(int64_t)(rr * G + h) * stride + sg] + acc[((int64_t)128 + rr * G + h) * stride + sg];
         part[((int64_t)(r0 + rr) * Hkv + g) * W + sg] = v;
       }
     }
@@ -284,12 +298,14 @@ int launch(const void* q, const void* k, const int32_t* q_slot, const uint8_t* k
   const int G = Hq / Hkv, R = 128 / G, W = n_seg + 1;
   float* part = (float*)stream_scratch(st, SCR_SEGMASS, sizeof(float) * (size_t)n_rows * Hkv * W);
   if (!part) return fail(CC_E_CUDA, "segment_mass_tc: scratch allocation failed");
-  if (int rc = ensure_smem(attn_stats_tc_kernel<DH>, StSmem<DH>::TOTAL)) return rc;
+  const int stride = W | 1;  // odd: the rows' accumulators fall in distinct banks
+  const size_t smem = StSmem<DH>::total(stride);
+  if (int rc = ensure_smem(attn_stats_tc_kernel<DH>, StSmem<DH>::total(ST_MAXSEG | 1))) return rc;
   dim3 grid(Hkv, (n_rows + R - 1) / R);
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)DH);
-  attn_stats_tc_kernel<DH><<<grid, 192, StSmem<DH>::TOTAL, st>>>(mk, (const __nv_bfloat16*)q, rows, n_rows, q_slot,
-                                                                   key_pad, lse, seg_lo, seg_hi, n_seg, part, n_keys,
-                                                                   Hq, Hkv, G, scale_log2);
+  attn_stats_tc_kernel<DH><<<grid, 320, smem, st>>>(mk, (const __nv_bfloat16*)q, rows, n_rows, q_slot, key_pad, lse,
+                                                    seg_lo, seg_hi, n_seg, part, n_keys, Hq, Hkv, G, scale_log2,
+                                                    stride);
   int rc = check_launch("segment_mass_tc");
   if (rc) return rc;
   const int64_t total = (int64_t)n_rows * W;
