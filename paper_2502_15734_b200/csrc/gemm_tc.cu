@@ -1212,7 +1212,11 @@ Tiling pick_tiling(int M, int N, int K, int epi, bool allow_split) {
     double t = model_time(dp, M, N, K);
     if (t < best_t - 1e-9) { best_t = t; best = dp; }
     const int tiles = dp.t_dp;
-    if (allow_split && (2 * tiles <= sms || (tiles >= 2 * sms && nkb >= 128))) {
+    // stream-K: weight-streaming shapes (under half a wave of tiles) only
+    // below 128 rows -- at M = 290 it measured 44.0 / 38.4 / 70.6 us for
+    // QKV / o_proj / down against the CTA-pair plans' 26.6 / 26.5 / 67.9
+    // (tools/smallm_force.sh) -- and long-K multi-wave shapes
+    if (allow_split && ((2 * tiles <= sms && M < 128) || (tiles >= 2 * sms && nkb >= 128))) {
       Tiling sk = plan_sk(M, N, K, bn);
       double ts = model_time(sk, M, N, K);
       if (ts < 0.97 * best_t) { best_t = ts; best = sk; }
