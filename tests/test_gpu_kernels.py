@@ -519,3 +519,33 @@ def test_gemm_qkv_rope_fused_matches_unfused(N, M, Hq, Hkv, d, n_slots):
     sl = slots.long()
     for got, want in ((fq, q), (fk[sl], k), (fkr[sl], kr), (fv[sl], v)):
         torch.testing.assert_close(got.float(), want, atol=2e-2, rtol=2e-2)
+
+
+@pytest.mark.parametrize("Hq,Hkv,dh,n,n_rows", [(32, 8, 128, 3001, 1200), (16, 2, 64, 2013, 900), (8, 1, 128, 4099, 2000)])
+def test_attention_many_rows_and_ragged_keys(N, Hq, Hkv, dh, n, n_rows):
+    """The default (ping-pong) attention kernel on grids of more than one
+    wave (no key splits), key counts that are not a multiple of 16 and pads in
+    several places, against torch fp32; and run-to-run bit-identical."""
+    g = torch.Generator(device="cuda").manual_seed(n + dh)
+    rows = torch.sort(torch.randperm(n, generator=g, device="cuda")[:n_rows]).values.int()
+    q = torch.randn((n_rows, Hq, dh), generator=g, device="cuda").bfloat16()
+    k = torch.randn((n, Hkv, dh), generator=g, device="cuda").bfloat16()
+    v = torch.randn((n, Hkv, dh), generator=g, device="cuda").bfloat16()
+    pad = torch.zeros(n, dtype=torch.uint8, device="cuda")
+    pad[7:9] = 1
+    pad[1000:1013] = 1
+    pad[n - 5: n - 1] = 1
+    rows = rows[pad[rows.long()] == 0].contiguous()
+    q = q[: rows.numel()].contiguous()
+    outs = []
+    for _ in range(2):
+        ctx = torch.empty((rows.numel(), Hq * dh), dtype=torch.bfloat16, device="cuda")
+        lse = torch.empty((rows.numel(), Hq), dtype=torch.float32, device="cuda")
+        N.call("cc_attention", N.ptr(q), N.ptr(k), N.ptr(v), N.ptr(rows), N.ptr(pad), N.ptr(ctx), N.ptr(lse),
+               rows.numel(), n, Hq, Hkv, dh, N.BF16, 0, N.stream_ptr())
+        torch.cuda.synchronize()
+        outs.append((ctx, lse))
+    ref, ref_lse = _attn_ref(q, k, v, rows, pad, Hq, Hkv)
+    torch.testing.assert_close(outs[0][0].float(), ref, atol=3e-2, rtol=3e-2)
+    torch.testing.assert_close(outs[0][1], ref_lse, atol=2e-3, rtol=1e-3)
+    assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
