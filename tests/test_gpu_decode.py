@@ -2,7 +2,7 @@
 against the reference fixture and the CPU oracle.
 
 Tolerances as for prefill: fp64 ~1e-9 absolute vs the reference; fp32 1e-3
-relative; bf16 relative Frobenius < 5e-2 on the appended K/V plus identical
+relative; bf16 relative Frobenius < 1.3e-2 (3x measured) on the appended K/V plus identical
 greedy tokens.  Kernel tests compare with a plain torch fp32 reference."""
 import numpy as np
 import pytest
@@ -12,6 +12,7 @@ pytestmark = pytest.mark.gpu
 
 from ccb_helpers import golden_path  # noqa: E402
 
+from ccb_helpers import record_measurement  # noqa: E402
 from oracle import cachecraft_oracle as O  # noqa: E402
 
 
@@ -78,7 +79,7 @@ def test_decode_zero_steps_and_chaining(cc):
     assert kv.n_slots == int(g["n0"]) + 3
 
 
-@pytest.mark.parametrize("dtype,tol", [("fp64", 1e-9), ("bf16", 5e-2)])
+@pytest.mark.parametrize("dtype,tol", [("fp64", 1e-9), ("bf16", 1.3e-2)])  # bf16: 3x measured (4.2e-3)
 def test_decode_llama_shaped_vs_oracle(cc, dtype, tol):
     """GQA 8/2, d_head 128 (bf16: GEMV projections + split-KV decode attention),
     SwiGLU, norm weights, theta 5e5."""
@@ -100,12 +101,14 @@ def test_decode_llama_shaped_vs_oracle(cc, dtype, tol):
     kv = res.kv
     got = cc.decode(model, kv, res.hidden[last], 5)
     assert got == want
+    e = {"keys": max(rel(kv.keys[l][n0:], k2[l][n0:]) for l in range(2)),
+         "values": max(rel(kv.values[l][n0:], v2[l][n0:]) for l in range(2))}
+    record_measurement("decode_llama_shaped", {"dtype": dtype, **e})
     for l in range(2):
         if dtype == "fp64":
             np.testing.assert_allclose(kv.keys[l][n0:], k2[l][n0:], atol=tol)
-        else:
-            assert rel(kv.keys[l][n0:], k2[l][n0:]) < tol
-            assert rel(kv.values[l][n0:], v2[l][n0:]) < tol
+    if dtype != "fp64":
+        assert e["keys"] < tol and e["values"] < tol, e
 
 
 # ---------------------------------------------------------------------------

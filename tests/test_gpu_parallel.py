@@ -11,6 +11,7 @@ import pytest
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
+from ccb_helpers import record_measurement  # noqa: E402
 from oracle import cachecraft_oracle as O  # noqa: E402
 
 
@@ -35,7 +36,7 @@ class ThreadGroup:
         return ar
 
 
-@pytest.mark.parametrize("dtype,tol", [("fp64", 1e-9), ("bf16", 5e-2)])
+@pytest.mark.parametrize("dtype,tol", [("fp64", 1e-9), ("bf16", 1.2e-2)])  # bf16: 3x measured (4.0e-3)
 def test_two_rank_tensor_parallel_matches_unsharded(dtype, tol):
     if not torch.cuda.is_available():
         pytest.skip("no GPU")
@@ -84,15 +85,19 @@ def test_two_rank_tensor_parallel_matches_unsharded(dtype, tol):
     for t in th:
         t.join(timeout=300)
     assert not errors, errors
+    errs = {"hidden": 0.0, "keys": 0.0}
     for rank in range(2):
         h, keys, tok = results[rank]
         err = np.linalg.norm(h - ref["hidden"]) / np.linalg.norm(ref["hidden"])
+        errs["hidden"] = max(errs["hidden"], float(err))
         assert err < tol, (rank, err)
         assert tok == O.greedy_token(w, ocfg, ref)
     for l in range(2):
         k = np.concatenate([results[0][1][l], results[1][1][l]], axis=1)
         err = np.linalg.norm(k - ref["keys"][l]) / np.linalg.norm(ref["keys"][l])
+        errs["keys"] = max(errs["keys"], float(err))
         assert err < tol
+    record_measurement("tp2_in_process", {"dtype": dtype, **errs})
 
 
 def test_peer_push_gemm_and_reduction_two_ranks():

@@ -2,8 +2,9 @@
 golden fixtures and the CPU oracle.
 
 Tolerances (north star): fp64 mode ~1e-9 absolute (the reference's own
-precision); fp32 mode 1e-3 relative; bf16 mode a bf16 tolerance (relative
-Frobenius error, BF16_TOY_TOL) plus an identical greedy next token.
+precision); fp32 mode 1e-3 relative; bf16 mode relative Frobenius error
+below BF16_TOY_TOL (3x the measured error) plus an identical greedy next
+token.
 Selections and plan decisions are bit-exact."""
 import numpy as np
 import pytest
@@ -19,9 +20,13 @@ from oracle import cachecraft_oracle as O  # noqa: E402
 # bf16 mode against the float64 reference WITH UNROUNDED weights (the error
 # includes rounding the weights to bf16): ~3x the largest relative error
 # measured on the B200 over these small-model tests
-# (profiles/r2_parity_small.jsonl); the full-size tests in
-# test_gpu_parity_fullsize.py compare against the bf16-rounded weights
-BF16_TOY_TOL = 5e-2
+# (profiles/r2_parity_small.jsonl: hidden / K / V 3.1e-3 - 5.1e-3); the
+# full-size tests in test_gpu_parity_fullsize.py compare against the
+# bf16-rounded weights
+BF16_TOY_TOL = 1.5e-2
+# creation statistics in bf16 (measured: token scores 1.0e-4, a/b means
+# 3.6e-5 relative)
+BF16_SCORE_TOL = 5e-4
 
 
 @pytest.fixture(scope="module")
@@ -201,7 +206,7 @@ def config1_device(cc, dtype):
 @pytest.mark.parametrize("dtype", ["fp64", "fp32", "bf16"])
 def test_config1_creation_stats_and_selection(cc, dtype):
     g, model, caches, scores, meta = config1_device(cc, dtype)
-    tol = {"fp64": 1e-10, "fp32": 1e-3, "bf16": BF16_TOY_TOL}[dtype]
+    tol = {"fp64": 1e-10, "fp32": 1e-3, "bf16": BF16_SCORE_TOL}[dtype]
     e = {"scores": rel(np.stack(scores), g["scores"]), "meta": rel(np.array(meta)[:, :2], g["meta"][:, :2])}
     sel = [cc.select_tokens(s, 0.15) for s in scores]
     flips = sum(len(set(a.tolist()) ^ set(b.tolist())) // 2 for a, b in zip(sel, g["selected"]))
