@@ -10,7 +10,7 @@ import csv
 import json
 import sys
 
-GROUPS = {"gemm": ("gemm_tc_kernel", "gemm_pair_kernel"), "attention": ("attn_tc_kernel", "attn_pp_kernel", "attn_ps_kernel"),
+GROUPS = {"gemm": ("gemm_tc_kernel", "gemm_pair_kernel"), "attention": ("attn_tc_kernel", "attn_pp_kernel"),
           "gather_rope": ("gather_rope_kernel",)}
 
 rows = list(csv.reader(open(sys.argv[1])))
