@@ -950,6 +950,20 @@ def main():
             miss[name + "_ms"] = round(statistics.median(ts), 3)
         miss["k8_cost_ms"] = round(miss["with_creation_stats_ms"] - miss["no_stats_ms"], 3)
         miss["k8_share"] = round(miss["k8_cost_ms"] / miss["with_creation_stats_ms"], 4)
+        # K8's own launches, device-timed on the launching stream (same MISS
+        # request, every chunk span + the question as stats segments)
+        from paper_2502_15734_b200 import engine as E_
+
+        reqm, dpm, wsm = full_plan(cc, model, chunks, question)
+        segm = list(reqm.segment_slots) + [tuple(reqm.question_span)]
+        dpm.stats_segments = segm
+        E_._attach_stats_rows(model, dpm, segm)
+        tk8 = E_.KernelTimer()
+        for i in range(args.warmup + 2):
+            E_.execute(model, dpm, wsm, stats=True, timer=tk8 if i >= args.warmup else None)
+        torch.cuda.synchronize()
+        miss["segment_mass_roofline"] = roofline_obj("segment_mass", tk8.summary(), peaks, "tensor", args.config)
+        del wsm
         baselines["miss_path_full_prefill"] = miss
     if not args.no_baselines and not tp_mode:
         toks = torch.from_numpy(np.concatenate(chunks + [question]).astype(np.int64)).cuda()

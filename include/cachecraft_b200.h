@@ -275,6 +275,21 @@ CC_API int cc_decode_attention_dev(const void* q, const void* k_rot, const void*
                                    void* ctx, float* lse, const int32_t* n_keys_dev, int max_keys, int n_heads,
                                    int n_kv_heads, int d_head, void* stream);
 
+/* One decode layer's attention step in ONE launch (model.py:455-474): RoPE of
+ * the new row's q and k heads at *pos (rope table as cc_rope_scatter_qkv),
+ * the append of k (position-free), rotated k and v at row *slot of the
+ * layer's kv_k / k_rot / kv_v [max_keys][Hkv*dh], then the split-KV attention
+ * of q over keys 0 .. n_keys-1 (the new key included, key_pad[j] != 0 masks
+ * key j) with the chunk combine done by the last CTA of each kv head (fixed
+ * chunk order, deterministic).  qkv = the raw projection row [q | k | v].
+ * n_keys_dev != NULL: the key count is read on the device (graph replay) and
+ * n_keys is ignored; the grid is sized for max_keys (<= 131072).  bf16,
+ * d_head 128, GQA group 1/2/4/8.  Same appended bits as cc_rope_scatter_qkv. */
+CC_API int cc_decode_attention_qkv(const void* qkv, const int32_t* slot, const int32_t* pos, const void* rope_table,
+                                   void* kv_k, void* kv_v, void* k_rot, const uint8_t* key_pad, void* ctx, float* lse,
+                                   int n_keys, const int32_t* n_keys_dev, int max_keys, int n_heads, int n_kv_heads,
+                                   int d_head, void* stream);
+
 /* Decode step bookkeeping on the device (model.py:455-483 loop state):
  * tokens[state[0]] = *cur_token, then state[0..3] (count, slot, position,
  * live keys) += 1. */

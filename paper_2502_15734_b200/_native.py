@@ -55,6 +55,8 @@ _SIGS = {
     "cc_decode_attention": ([_vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _vp], _i32),
     "cc_rope_rows": ([_vp, _vp, _i64, _i32, _i32, _vp, _vp, _i32, _i32, _vp], _i32),
     "cc_decode_attention_dev": ([_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _vp], _i32),
+    "cc_decode_attention_qkv": ([_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _vp, _i32, _i32, _i32, _i32,
+                                 _vp], _i32),
     "cc_decode_advance": ([_vp, _vp, _vp, _vp], _i32),
     "cc_set_pdl": ([_i32], _i32),
     "cc_set_stream_k": ([_i32], _i32),

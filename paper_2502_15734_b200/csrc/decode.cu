@@ -9,14 +9,23 @@
 //   * rope_rows_kernel  rotate stored position-free keys at their positions
 //                       (rpe.py:19-44), once per decode session
 #include <math.h>
+#include <stdlib.h>
+
+#include <algorithm>
 
 #include <type_traits>
 
+#include <mutex>
+#include <unordered_map>
+
 #include "common.cuh"
+#include "sm100.cuh"
 
 namespace ccb {
 
 namespace {
+
+using namespace sm100;
 
 __device__ __forceinline__ uint4 ld_stream16(const void* p) {
   uint4 r;
@@ -35,6 +44,37 @@ __device__ __forceinline__ float dot8(const uint4& w, const uint4& x) {
     s = fmaf(fa.y, fb.y, s);
   }
   return s;
+}
+
+// ---- debug timeline of the decode chain (cc_debug_decode_trace) ---------------
+// When armed, thread 0 of every CTA of the GEMV / fused-attention kernels
+// appends {start, wait released, end, tag << 48 | smid << 32 | block} in
+// %globaltimer ns; off (one predicated load) otherwise.
+__device__ unsigned long long* g_dtrace = nullptr;
+__device__ unsigned g_dtrace_cap = 0;
+__device__ unsigned g_dtrace_n = 0;
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void dtrace(unsigned tag, unsigned long long t0, unsigned long long t1) {
+  unsigned long long* buf = g_dtrace;
+  if (buf == nullptr) return;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned long long t2 = gtime();
+    const unsigned i = atomicAdd(&g_dtrace_n, 1u);
+    if (i < g_dtrace_cap) {
+      unsigned smid;
+      asm("mov.u32 %0, %%smid;" : "=r"(smid));
+      const unsigned blk = blockIdx.x + blockIdx.y * gridDim.x;
+      buf[4 * i] = t0;
+      buf[4 * i + 1] = t1;
+      buf[4 * i + 2] = t2;
+      buf[4 * i + 3] = ((unsigned long long)tag << 48) | ((unsigned long long)smid << 32) | blk;
+    }
+  }
 }
 
 constexpr int GV_MAXM = 4;
@@ -61,8 +101,10 @@ __global__ void __launch_bounds__(GV_WARPS * 32) gemv_kernel(const void* __restr
     wg = reinterpret_cast<const uint4*>(W + (int64_t)rg * ldw);
     wu = reinterpret_cast<const uint4*>(W + (int64_t)(rg + 64) * ldw);
   };
+  const unsigned long long t0 = gtime();
   pdl_trigger();
   pdl_wait();  // activations come from the predecessor
+  const unsigned long long t1 = gtime();
   if constexpr (NORM) {
     __shared__ float red[GV_WARPS];
     __nv_bfloat16* xb = reinterpret_cast<__nv_bfloat16*>(xs);
@@ -155,6 +197,200 @@ __global__ void __launch_bounds__(GV_WARPS * 32) gemv_kernel(const void* __restr
       }
     }
   }
+  dtrace(2, t0, t1);
+}
+
+// ---- weight-streaming GEMV for one row (decode) -------------------------------
+// One CTA per SM, GS_CFG.nw warps.  The n_out x (K / pe) row pieces ("stages")
+// are split evenly over all warps of the grid (to one stage); a row cut by a
+// warp boundary (a "seam") is finished by whichever of its two warps comes
+// second, lo + hi in that fixed order (deterministic).  Each warp streams its
+// pieces through its own ring of 2 KiB shared-memory stages with 16-byte
+// cp.async (L2 evict-first: weights are read once per token, the KV cache and
+// activations stay).  The ring is filled BEFORE griddepcontrol.wait -- weights
+// never depend on the predecessor -- so under programmatic dependent launch
+// the first stages load while the previous kernel of the decode chain drains.
+// A stage is one 1024-element piece of a row (SwiGLU: a 512-element piece of
+// the gate row + the same piece of its up row); lane l copies and later reads
+// the 16-byte words l, l + 32, ... of the piece (no cross-lane hand-off)
+// against the staged activation row; the warp reduces once per output.
+// Measured and dropped: 1D bulk copies through the TMA unit (2.2-3.3 TB/s at
+// these shapes: not enough bytes in flight per SM for a pure stream), L2
+// bulk prefetch ahead of the ring (cp.async.bulk.prefetch.L2, rolling or
+// before the wait: 5-25% slower per token), the previous kernel prefetching
+// the next projection's weights into L2 (3% slower).
+// 28 warps x 2 stages x 2 KiB (measured best of {8..32} warps x {1, 2, 4} KiB
+// stages x {1..6} stages at config 2: 3.30 ms/token vs 3.38 for 24 x 2 x 2 KiB,
+// 3.42-3.56 with 4 stages, 4.1-4.2 with 1 KiB stages or 8 warps).
+struct GsCfg { int nw, sb, ns; };
+constexpr GsCfg GS_CFG = {28, 2048, 2};
+// Every launch requests > 114 KiB of shared memory, so at most ONE CTA of it
+// is resident per SM: under programmatic dependent launch the CTAs are
+// placed while the previous kernel still occupies the SMs, and a statically
+// partitioned grid whose CTAs doubled up on some SMs (measured: 148 CTAs on
+// 77 SMs) runs at half speed.  The 116 KiB still leave room for the fused
+// attention step's CTAs (19 KiB) to land early next to the QKV projection.
+constexpr int GS_MIN_SMEM = 116 * 1024;
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, uint64_t pol) {
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+template <int EPI, bool NORM, int GS_WARPS, int GS_STAGE, int GS_STAGES>
+__global__ void __launch_bounds__(GS_WARPS * 32) gemv_stream_kernel(const void* __restrict__ A_,
+                                                                    const __nv_bfloat16* __restrict__ W, int64_t ldw,
+                                                                    void* __restrict__ C, int N, int K,
+                                                                    const float* __restrict__ norm_w, float eps,
+                                                                    float4* __restrict__ seam, unsigned* seam_ticket) {
+  extern __shared__ __align__(128) uint8_t gs_smem[];
+  __shared__ float red[GS_WARPS];
+  constexpr bool GLU = EPI == CC_EPI_SWIGLU;
+  constexpr int VPL = GLU ? GS_STAGE / 1024 : GS_STAGE / 512;  // 16-byte words per lane per stage (per row for SwiGLU)
+  constexpr int GS_RING = GS_WARPS * GS_STAGES * GS_STAGE;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_out = GLU ? N / 2 : N;
+  const int pe = GLU ? min(K, GS_STAGE / 4) : min(K, GS_STAGE / 2);  // row elements per stage
+  const int nv = pe / 256;                                             // words per lane actually used (<= VPL)
+  const int np = K / pe;                              // stages per output
+  // warps split the n_out * np stages evenly (to one stage); a row cut by a
+  // range boundary ("seam") is finished by whichever of its two warps comes
+  // second, as lo + hi (fixed order).  Every used warp covers >= 1 row, so a
+  // row has at most one seam.
+  const int gw = blockIdx.x * GS_WARPS + warp;
+  const int used = min(gridDim.x * GS_WARPS, n_out);
+  const int64_t tot = (int64_t)n_out * np;
+  const int64_t s0 = gw < used ? tot * gw / used : 0, s1 = gw < used ? tot * (gw + 1) / used : 0;
+  const int n_st = (int)(s1 - s0);
+  uint8_t* ring = gs_smem + (size_t)warp * GS_STAGES * GS_STAGE;
+  __nv_bfloat16* xs = reinterpret_cast<__nv_bfloat16*>(gs_smem + GS_RING);
+  const unsigned long long t0 = gtime();
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  auto issue = [&](int st) {  // this lane's words of stage st (one commit group per stage, empty past the end)
+    if (st < n_st) {
+      const int o = (int)((s0 + st) / np), p = (int)((s0 + st) % np);
+      uint4* dst = reinterpret_cast<uint4*>(ring + (size_t)(st % GS_STAGES) * GS_STAGE);
+      const int64_t rg = GLU ? (int64_t)(o / 64) * 128 + (o % 64) : o;
+      const uint4* src = reinterpret_cast<const uint4*>(W + rg * ldw + (int64_t)p * pe);
+#pragma unroll
+      for (int i = 0; i < VPL; ++i)
+        if (i < nv) cp_async16(dst + lane + 32 * i, src + lane + 32 * i, pol);
+      if constexpr (GLU) {
+        const uint4* src_u = reinterpret_cast<const uint4*>(W + (rg + 64) * ldw + (int64_t)p * pe);
+#pragma unroll
+        for (int i = 0; i < VPL; ++i)
+          if (i < nv) cp_async16(dst + GS_STAGE / 32 + lane + 32 * i, src_u + lane + 32 * i, pol);
+      }
+    }
+    cp_async_commit();
+  };
+#pragma unroll
+  for (int st = 0; st < GS_STAGES; ++st) issue(st);
+  pdl_trigger();
+  pdl_wait();  // the activation row comes from the predecessor
+  const unsigned long long t1 = gtime();
+  if constexpr (NORM) {  // weighted RMSNorm of the f32 residual row (same expression as gemv_kernel)
+    const float4* x4 = reinterpret_cast<const float4*>(A_);
+    float ss = 0.f;
+    constexpr int NR = 4;  // residual words held in registers (K <= 16 * blockDim)
+    float4 xr[NR], gr[NR];
+#pragma unroll
+    for (int j = 0; j < NR; ++j) {  // residual + norm weights in one round trip
+      const int i = threadIdx.x + j * blockDim.x;
+      xr[j] = i < K / 4 ? x4[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+      gr[j] = (i < K / 4 && norm_w != nullptr) ? reinterpret_cast<const float4*>(norm_w)[i]
+                                               : make_float4(1.f, 1.f, 1.f, 1.f);
+    }
+#pragma unroll
+    for (int j = 0; j < NR; ++j)
+      ss = fmaf(xr[j].x, xr[j].x, fmaf(xr[j].y, xr[j].y, fmaf(xr[j].z, xr[j].z, fmaf(xr[j].w, xr[j].w, ss))));
+    for (int i = threadIdx.x + NR * blockDim.x; i < K / 4; i += blockDim.x) {
+      const float4 v = x4[i];
+      ss = fmaf(v.x, v.x, fmaf(v.y, v.y, fmaf(v.z, v.z, fmaf(v.w, v.w, ss))));
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
+    if (lane == 0) red[warp] = ss;
+    __syncthreads();
+    float tot = 0.f;
+#pragma unroll
+    for (int w = 0; w < GS_WARPS; ++w) tot += red[w];
+    const float inv = rsqrtf(tot / (float)K + eps);
+    auto put = [&](int i, const float4& v, const float4& g) {
+      __nv_bfloat162 a = __floats2bfloat162_rn(v.x * inv * g.x, v.y * inv * g.y);
+      __nv_bfloat162 b = __floats2bfloat162_rn(v.z * inv * g.z, v.w * inv * g.w);
+      *reinterpret_cast<uint2*>(xs + 4 * i) =
+          make_uint2(*reinterpret_cast<uint32_t*>(&a), *reinterpret_cast<uint32_t*>(&b));
+    };
+#pragma unroll
+    for (int j = 0; j < NR; ++j) {
+      const int i = threadIdx.x + j * blockDim.x;
+      if (i < K / 4) put(i, xr[j], gr[j]);
+    }
+    for (int i = threadIdx.x + NR * blockDim.x; i < K / 4; i += blockDim.x)
+      put(i, x4[i], norm_w != nullptr ? reinterpret_cast<const float4*>(norm_w)[i] : make_float4(1.f, 1.f, 1.f, 1.f));
+  } else {
+    const uint4* a8 = reinterpret_cast<const uint4*>(A_);
+    for (int i = threadIdx.x; i < K / 8; i += blockDim.x) reinterpret_cast<uint4*>(xs)[i] = a8[i];
+  }
+  __syncthreads();
+  float ag = 0.f, au = 0.f;
+  for (int st = 0; st < n_st; ++st) {
+    cp_async_wait<GS_STAGES - 1>();  // this lane's words of stage st have landed
+    const int p = (int)((s0 + st) % np);
+    const uint4* wv = reinterpret_cast<const uint4*>(ring + (size_t)(st % GS_STAGES) * GS_STAGE);
+    const uint4* xv = reinterpret_cast<const uint4*>(xs + (size_t)p * pe);
+#pragma unroll
+    for (int i = 0; i < VPL; ++i)
+      if (i < nv) {
+        const uint4 x = xv[lane + 32 * i];
+        ag += dot8(wv[lane + 32 * i], x);
+        if constexpr (GLU) au += dot8(wv[GS_STAGE / 32 + lane + 32 * i], x);
+      }
+    issue(st + GS_STAGES);  // refill the slot just read (same lane, same words)
+    if (p == np - 1 || st == n_st - 1) {
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        ag += __shfl_xor_sync(0xffffffffu, ag, off);
+        if constexpr (GLU) au += __shfl_xor_sync(0xffffffffu, au, off);
+      }
+      const int o = (int)((s0 + st) / np);
+      bool finish = true;
+      if ((int64_t)o * np < s0 || (int64_t)(o + 1) * np > s1) {  // a seam row: lo (ends past s1) or hi part
+        const bool hi = (int64_t)o * np < s0;
+        const int sm = hi ? gw : gw + 1;
+        if (lane == 0) {
+          seam[2 * sm + (hi ? 1 : 0)] = make_float4(ag, au, 0.f, 0.f);
+          __threadfence();
+          finish = atomicAdd(&seam_ticket[sm], 1u) == 1u;
+          if (finish) {
+            __threadfence();
+            const float4 other = __ldcg(&seam[2 * sm + (hi ? 0 : 1)]);
+            ag = hi ? other.x + ag : ag + other.x;
+            au = hi ? other.y + au : au + other.y;
+            seam_ticket[sm] = 0u;  // ready for the next launch on this stream
+          }
+        }
+      }
+      if (lane == 0 && finish) {
+        if constexpr (EPI == CC_EPI_RESID_ADD) {
+          reinterpret_cast<float*>(C)[o] += ag;
+        } else {
+          float y = ag;
+          if constexpr (EPI == CC_EPI_GELU) y = gelu_tanh(ag);
+          if constexpr (GLU) y = silu(ag) * au;
+          reinterpret_cast<__nv_bfloat16*>(C)[o] = __float2bfloat16_rn(y);
+        }
+      }
+      ag = au = 0.f;
+    }
+  }
+  cp_async_wait<0>();
+  dtrace(1, t0, t1);
 }
 
 // ---- split-KV decode attention ------------------------------------------------
@@ -298,6 +534,535 @@ __global__ void __launch_bounds__(DA_KEYS) decode_attn_partial(const __nv_bfloat
   }
 }
 
+// ---- fused decode attention step (one launch per layer) -------------------------
+// Same split-KV partial as decode_attn_partial, plus what the decode chain ran
+// as separate kernels around it:
+//   * RoPE of the new row's q heads of this group (rope_scatter's arithmetic:
+//     rope_pair on the bf16 inputs, rounded to bf16);
+//   * the append: the CTA whose chunk holds the new slot writes its kv head's
+//     k (position-free), rotated k and v at the slot (rope_scatter's bits)
+//     and uses them from shared memory for that key;
+//   * the combine: each CTA bumps its group's ticket after writing its
+//     partial; the last one folds the chunks (fixed chunk order: the result
+//     does not depend on which CTA came last) and resets the ticket.
+// grid (Hkv, chunks of the capacity); CTAs past the live keys exit at once.
+constexpr int DF_MAXC = 1024;  // chunks the in-kernel combine folds (128k keys)
+
+template <int G>
+__global__ void __launch_bounds__(DA_KEYS) decode_attn_fused(
+    const __nv_bfloat16* __restrict__ qkv, const int32_t* __restrict__ slot_p, const int32_t* __restrict__ pos_p,
+    const float2* __restrict__ table, __nv_bfloat16* kv_k, __nv_bfloat16* kv_v, __nv_bfloat16* k_rot,
+    const uint8_t* __restrict__ key_pad, float* part_o, float2* part_ml, unsigned* tickets,
+    __nv_bfloat16* __restrict__ ctx, float* __restrict__ lse, int n_keys, const int32_t* __restrict__ n_keys_dev,
+    int Hq, int Hkv, float scale_log2) {
+  const unsigned long long t0 = gtime();
+  pdl_trigger();
+  pdl_wait();
+  const unsigned long long t1 = gtime();
+  if (n_keys_dev != nullptr) n_keys = *n_keys_dev;
+  const int n_chunks = (n_keys + DA_KEYS - 1) / DA_KEYS;
+  const int g = blockIdx.x, c = blockIdx.y, t = threadIdx.x;
+  if (c >= n_chunks) return;
+  constexpr int NKG = DA_KEYS / 16;
+  __shared__ __align__(16) float qs[G][DA_DH];
+  __shared__ float ps[G][DA_KEYS];
+  __shared__ float2 ml_s[G];
+  __shared__ __align__(16) float red[NKG][G][DA_DH];
+  __shared__ __align__(16) __nv_bfloat16 knew[DA_DH], vnew[DA_DH];
+  __shared__ unsigned ticket_s;
+  const int kvw = Hkv * DA_DH;
+  const int slot = *slot_p;
+  const int cg = t & 15, kg = t >> 4;
+  const int jn = min(DA_KEYS, n_keys - c * DA_KEYS);
+  // V rows of the P.V role first (their latency overlaps the rest)
+  const __nv_bfloat16* vbase = kv_v + (int64_t)c * DA_KEYS * kvw + g * DA_DH + cg * 8;
+  uint4 vv[16];
+#pragma unroll
+  for (int u = 0; u < 16; ++u) {
+    const int jj = kg + NKG * u;
+    vv[u] = jj < jn ? *reinterpret_cast<const uint4*>(vbase + (int64_t)jj * kvw) : make_uint4(0, 0, 0, 0);
+  }
+  const float2* cs = table + (int64_t)(*pos_p) * (DA_DH / 2);
+  const __nv_bfloat16* qrow = qkv + (int64_t)g * G * DA_DH;
+  for (int i = t; i < G * DA_DH / 2; i += DA_KEYS) {
+    const int h = i / (DA_DH / 2), jj = i % (DA_DH / 2);
+    const float a = __bfloat162float(qrow[h * DA_DH + jj]), b = __bfloat162float(qrow[h * DA_DH + jj + DA_DH / 2]);
+    float xr, yr;
+    rope_pair(a, b, cs[jj].x, cs[jj].y, xr, yr);
+    qs[h][jj] = __bfloat162float(__float2bfloat16_rn(xr));
+    qs[h][jj + DA_DH / 2] = __bfloat162float(__float2bfloat16_rn(yr));
+  }
+  const bool owner = slot / DA_KEYS == c;
+  if (owner) {  // append this kv head's slice of the new row
+    const int64_t off = (int64_t)slot * kvw + g * DA_DH;
+    const __nv_bfloat16* krow = qkv + (int64_t)(Hq + g) * DA_DH;
+    const __nv_bfloat16* vrow = qkv + (int64_t)(Hq + Hkv + g) * DA_DH;
+    if (t < DA_DH / 2) {
+      const __nv_bfloat16 x = krow[t], y = krow[t + DA_DH / 2];
+      float xr, yr;
+      rope_pair(__bfloat162float(x), __bfloat162float(y), cs[t].x, cs[t].y, xr, yr);
+      const __nv_bfloat16 bx = __float2bfloat16_rn(xr), by = __float2bfloat16_rn(yr);
+      kv_k[off + t] = x;
+      kv_k[off + t + DA_DH / 2] = y;
+      k_rot[off + t] = bx;
+      k_rot[off + t + DA_DH / 2] = by;
+      knew[t] = bx;
+      knew[t + DA_DH / 2] = by;
+    }
+    const __nv_bfloat16 vx = vrow[t];
+    kv_v[off + t] = vx;
+    vnew[t] = vx;
+  }
+  __syncthreads();
+  if (owner) {  // the new key's V words from shared memory (the global copy may be stale in this CTA)
+    const int jn_new = slot - c * DA_KEYS;
+#pragma unroll
+    for (int u = 0; u < 16; ++u)
+      if (kg + NKG * u == jn_new) vv[u] = *reinterpret_cast<const uint4*>(&vnew[cg * 8]);
+  }
+  const int j = c * DA_KEYS + t;
+  const bool valid = j < n_keys && (key_pad == nullptr || key_pad[j] == 0);
+  float sc[G];
+#pragma unroll
+  for (int h = 0; h < G; ++h) sc[h] = 0.f;
+  if (valid) {
+    const uint4* kr = j == slot ? reinterpret_cast<const uint4*>(knew)
+                                : reinterpret_cast<const uint4*>(k_rot + (int64_t)j * kvw + g * DA_DH);
+    uint4 kv16[DA_DH / 8];
+#pragma unroll
+    for (int u = 0; u < DA_DH / 8; ++u) kv16[u] = kr[u];
+#pragma unroll
+    for (int u = 0; u < DA_DH / 8; ++u) {
+      const uint4 kk = kv16[u];
+      const __nv_bfloat162* kb = reinterpret_cast<const __nv_bfloat162*>(&kk);
+      float kf[8];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 f = __bfloat1622float2(kb[e]);
+        kf[2 * e] = f.x;
+        kf[2 * e + 1] = f.y;
+      }
+#pragma unroll
+      for (int h = 0; h < G; ++h) {
+        const float4 qa = *reinterpret_cast<const float4*>(&qs[h][u * 8]);
+        const float4 qb = *reinterpret_cast<const float4*>(&qs[h][u * 8 + 4]);
+        const float qv[8] = {qa.x, qa.y, qa.z, qa.w, qb.x, qb.y, qb.z, qb.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) sc[h] = fmaf(kf[2 * e], qv[2 * e], fmaf(kf[2 * e + 1], qv[2 * e + 1], sc[h]));
+      }
+    }
+  }
+#pragma unroll
+  for (int h = 0; h < G; ++h) ps[h][t] = valid ? sc[h] * scale_log2 : -INFINITY;
+  __syncthreads();
+  const int warp = t >> 5, lane = t & 31;
+  for (int h = warp; h < G; h += DA_KEYS / 32) {
+    float v[DA_KEYS / 32], m = -INFINITY;
+#pragma unroll
+    for (int e = 0; e < DA_KEYS / 32; ++e) {
+      v[e] = ps[h][lane + 32 * e];
+      m = fmaxf(m, v[e]);
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
+    float l = 0.f;
+#pragma unroll
+    for (int e = 0; e < DA_KEYS / 32; ++e) {
+      const float p = m == -INFINITY ? 0.f : exp2f(v[e] - m);
+      ps[h][lane + 32 * e] = p;
+      l += p;
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) l += __shfl_xor_sync(0xffffffffu, l, off);
+    if (lane == 0) ml_s[h] = make_float2(m, l);
+  }
+  __syncthreads();
+  float o[G][8];
+#pragma unroll
+  for (int h = 0; h < G; ++h)
+#pragma unroll
+    for (int e = 0; e < 8; ++e) o[h][e] = 0.f;
+#pragma unroll
+  for (int u = 0; u < 16; ++u) {
+    const int jj = kg + NKG * u;
+    const __nv_bfloat162* vb = reinterpret_cast<const __nv_bfloat162*>(&vv[u]);
+#pragma unroll
+    for (int h = 0; h < G; ++h) {
+      const float p = ps[h][jj];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 vf = __bfloat1622float2(vb[e]);
+        o[h][2 * e] = fmaf(p, vf.x, o[h][2 * e]);
+        o[h][2 * e + 1] = fmaf(p, vf.y, o[h][2 * e + 1]);
+      }
+    }
+  }
+#pragma unroll
+  for (int h = 0; h < G; ++h)
+#pragma unroll
+    for (int e = 0; e < 8; ++e) red[kg][h][cg * 8 + e] = o[h][e];
+  __syncthreads();
+#pragma unroll
+  for (int h = 0; h < G; ++h) {
+    const int head = g * G + h;
+    float acc = 0.f;
+#pragma unroll
+    for (int k2 = 0; k2 < NKG; ++k2) acc += red[k2][h][t];
+    part_o[((int64_t)c * Hq + head) * DA_DH + t] = acc;
+    if (t == 0) part_ml[(int64_t)c * Hq + head] = ml_s[h];
+  }
+  // ---- last CTA of the group folds the chunks ----
+  __threadfence();
+  __syncthreads();
+  if (t == 0) ticket_s = atomicAdd(&tickets[g], 1u);
+  __syncthreads();
+  if (ticket_s != (unsigned)(n_chunks - 1)) {
+    dtrace(3, t0, t1);
+    return;
+  }
+  if (t == 0) tickets[g] = 0u;  // ready for the next layer / step
+  __threadfence();
+  float* wsm = &red[0][0][0] + warp * DF_MAXC;  // chunk weights of this warp's head (red is free now)
+  for (int h = warp; h < G; h += DA_KEYS / 32) {
+    const int head = g * G + h;
+    float m = -INFINITY;
+    for (int cc = lane; cc < n_chunks; cc += 32) m = fmaxf(m, __ldcg(&part_ml[(int64_t)cc * Hq + head]).x);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
+    float l = 0.f;
+    for (int cc = lane; cc < n_chunks; cc += 32) {
+      const float2 ml = __ldcg(&part_ml[(int64_t)cc * Hq + head]);
+      const float w = (m == -INFINITY || ml.x == -INFINITY) ? 0.f : exp2f(ml.x - m);
+      wsm[cc] = w;
+      l = fmaf(ml.y, w, l);
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) l += __shfl_xor_sync(0xffffffffu, l, off);
+    __syncwarp();
+    // lane = 4 output columns; 16 chunk rows in flight
+    const float4* po = reinterpret_cast<const float4*>(part_o) + (int64_t)head * (DA_DH / 4) + lane;
+    const int64_t cstride = (int64_t)Hq * (DA_DH / 4);
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    int cc = 0;
+    for (; cc + 15 < n_chunks; cc += 16) {
+      float4 v[16];
+#pragma unroll
+      for (int k = 0; k < 16; ++k) v[k] = __ldcg(po + (int64_t)(cc + k) * cstride);
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        const float w = wsm[cc + k];
+        acc.x = fmaf(v[k].x, w, acc.x);
+        acc.y = fmaf(v[k].y, w, acc.y);
+        acc.z = fmaf(v[k].z, w, acc.z);
+        acc.w = fmaf(v[k].w, w, acc.w);
+      }
+    }
+    for (; cc < n_chunks; ++cc) {
+      const float4 v = __ldcg(po + (int64_t)cc * cstride);
+      const float w = wsm[cc];
+      acc.x = fmaf(v.x, w, acc.x);
+      acc.y = fmaf(v.y, w, acc.y);
+      acc.z = fmaf(v.z, w, acc.z);
+      acc.w = fmaf(v.w, w, acc.w);
+    }
+    const float inv = l > 0.f ? 1.f / l : 0.f;
+    __nv_bfloat162 lo = __floats2bfloat162_rn(acc.x * inv, acc.y * inv);
+    __nv_bfloat162 hi = __floats2bfloat162_rn(acc.z * inv, acc.w * inv);
+    *reinterpret_cast<uint2*>(ctx + (int64_t)head * DA_DH + 4 * lane) =
+        make_uint2(*reinterpret_cast<uint32_t*>(&lo), *reinterpret_cast<uint32_t*>(&hi));
+    if (lane == 0 && lse != nullptr) lse[head] = l > 0.f ? (m + log2f(l)) * 0.6931471805599453f : -INFINITY;
+  }
+  dtrace(4, t0, t1);  // the combining CTA
+}
+
+// ---- tensor-core decode attention step (default) ------------------------------
+// Same contract as decode_attn_fused (RoPE of q / the new key, the append,
+// split-KV partials, last-CTA combine) with the per-chunk math on mma.sync
+// (m16n8k16 bf16 -> f32) in the swapped orientation: S^T = K Q^T (M = 16
+// keys, N = 8 query heads of the group, zero-padded past G), O^T += V^T P^T
+// (M = 16 head dims, N = heads, K = 16 keys).  Both operands are fed straight
+// from 16-byte global loads by permuting the reduction index consistently on
+// both sides (dims inside each 32-dim pair for S, keys per step for O) and the
+// output rows (dims) -- no shared-memory staging; P^T comes from the S^T
+// accumulator through movmatrix.trans.
+// Each warp owns 32 keys (2 steps of 16) of the CTA's 128-key chunk; the K/V
+// words of those keys are loaded BEFORE griddepcontrol.wait: rows other than
+// the new slot were appended by this layer's attention step of an earlier
+// decode token, and the decode chain keeps at most ~3 grids in flight (every
+// GEMV grid holds > 114 KiB of shared memory per SM), so they are complete.
+// The new key's words are patched in from shared memory after the append;
+// V words of rows past the live keys (uninitialised capacity) are zeroed.
+constexpr int DT_WARPS = 4, DT_STEPS = 2, DT_KC = DT_WARPS * DT_STEPS * 16;  // 128 keys per CTA
+
+__device__ __forceinline__ void mma16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                         uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t movtrans(uint32_t x) {
+  uint32_t y;
+  asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;" : "=r"(y) : "r"(x));
+  return y;
+}
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+__device__ __forceinline__ uint32_t u4w(const uint4& v, int i) { return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w; }
+
+template <int G>
+__global__ void __launch_bounds__(DT_WARPS * 32) decode_attn_tc(
+    const __nv_bfloat16* __restrict__ qkv, const int32_t* __restrict__ slot_p, const int32_t* __restrict__ pos_p,
+    const float2* __restrict__ table, __nv_bfloat16* kv_k, __nv_bfloat16* kv_v, __nv_bfloat16* k_rot,
+    const uint8_t* __restrict__ key_pad, float* part_o, float2* part_ml, unsigned* tickets,
+    __nv_bfloat16* __restrict__ ctx, float* __restrict__ lse, int n_keys, const int32_t* __restrict__ n_keys_dev,
+    int max_keys, int Hq, int Hkv, float scale_log2) {
+  static_assert(G <= 8, "one n-tile of query heads");
+  const unsigned long long t0 = gtime();
+  const int g = blockIdx.x, c = blockIdx.y, tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31, r = lane >> 2, q = lane & 3;
+  const int kvw = Hkv * DA_DH;
+  const int kbase = c * DT_KC + warp * (DT_STEPS * 16);
+  // ---- pre-wait: this warp's K and V words ----
+  uint4 kf[DT_STEPS][2][4];  // [step][key r, r + 8][32-dim pair p]: dims 32p + 8q .. + 7
+  uint4 vf[DT_STEPS][4][2];  // [step][key 2q, 2q+1, 2q+8, 2q+9][half]: dims 16r .. 16r + 15
+#pragma unroll
+  for (int s = 0; s < DT_STEPS; ++s) {
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int key = min(kbase + s * 16 + r + 8 * e, max_keys - 1);
+      const __nv_bfloat16* kp = k_rot + (int64_t)key * kvw + g * DA_DH + 8 * q;
+#pragma unroll
+      for (int p = 0; p < 4; ++p) kf[s][e][p] = ld_stream16(kp + 32 * p);
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int key = min(kbase + s * 16 + 2 * q + (e & 1) + 8 * (e >> 1), max_keys - 1);
+      const __nv_bfloat16* vp = kv_v + (int64_t)key * kvw + g * DA_DH + 16 * r;
+      vf[s][e][0] = ld_stream16(vp);
+      vf[s][e][1] = ld_stream16(vp + 8);
+    }
+  }
+  pdl_trigger();
+  pdl_wait();
+  const unsigned long long t1 = gtime();
+  if (n_keys_dev != nullptr) n_keys = *n_keys_dev;
+  const int n_chunks = (n_keys + DT_KC - 1) / DT_KC;
+  if (c >= n_chunks) return;
+  __shared__ __align__(16) __nv_bfloat16 qb[8][DA_DH];
+  __shared__ __align__(16) __nv_bfloat16 knew[DA_DH], vnew[DA_DH];
+  __shared__ __align__(16) float wo[DT_WARPS][8][DA_DH];
+  __shared__ float wm[DT_WARPS][8], wl[DT_WARPS][8];
+  __shared__ unsigned ticket_s;
+  const int slot = *slot_p;
+  const float2* cs = table + (int64_t)(*pos_p) * (DA_DH / 2);
+  const __nv_bfloat16* qrow = qkv + (int64_t)g * G * DA_DH;
+  for (int i = tid; i < 8 * DA_DH / 2; i += DT_WARPS * 32) {
+    const int h = i / (DA_DH / 2), jj = i % (DA_DH / 2);
+    __nv_bfloat16 bx = __float2bfloat16_rn(0.f), by = bx;
+    if (h < G) {
+      float xr, yr;
+      rope_pair(__bfloat162float(qrow[h * DA_DH + jj]), __bfloat162float(qrow[h * DA_DH + jj + DA_DH / 2]), cs[jj].x,
+                cs[jj].y, xr, yr);
+      bx = __float2bfloat16_rn(xr);
+      by = __float2bfloat16_rn(yr);
+    }
+    qb[h][jj] = bx;
+    qb[h][jj + DA_DH / 2] = by;
+  }
+  const bool owner = slot / DT_KC == c;
+  if (owner) {  // append this kv head's slice of the new row (rope_scatter's bits)
+    const int64_t off = (int64_t)slot * kvw + g * DA_DH;
+    const __nv_bfloat16* krow = qkv + (int64_t)(Hq + g) * DA_DH;
+    const __nv_bfloat16* vrow = qkv + (int64_t)(Hq + Hkv + g) * DA_DH;
+    if (tid < DA_DH / 2) {
+      const __nv_bfloat16 x = krow[tid], y = krow[tid + DA_DH / 2];
+      float xr, yr;
+      rope_pair(__bfloat162float(x), __bfloat162float(y), cs[tid].x, cs[tid].y, xr, yr);
+      const __nv_bfloat16 bx = __float2bfloat16_rn(xr), by = __float2bfloat16_rn(yr);
+      kv_k[off + tid] = x;
+      kv_k[off + tid + DA_DH / 2] = y;
+      k_rot[off + tid] = bx;
+      k_rot[off + tid + DA_DH / 2] = by;
+      knew[tid] = bx;
+      knew[tid + DA_DH / 2] = by;
+    }
+    const __nv_bfloat16 vx = vrow[tid];
+    kv_v[off + tid] = vx;
+    vnew[tid] = vx;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int s = 0; s < DT_STEPS; ++s) {
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int key = kbase + s * 16 + r + 8 * e;
+      if (owner && key == slot)
+#pragma unroll
+        for (int p = 0; p < 4; ++p) kf[s][e][p] = *reinterpret_cast<const uint4*>(&knew[32 * p + 8 * q]);
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int key = kbase + s * 16 + 2 * q + (e & 1) + 8 * (e >> 1);
+      if (owner && key == slot) {
+        vf[s][e][0] = *reinterpret_cast<const uint4*>(&vnew[16 * r]);
+        vf[s][e][1] = *reinterpret_cast<const uint4*>(&vnew[16 * r + 8]);
+      }
+      if (key >= n_keys) vf[s][e][0] = vf[s][e][1] = make_uint4(0, 0, 0, 0);
+    }
+  }
+  uint4 qf[4];  // B operand of S^T: head r, dims 32p + 8q .. + 7
+#pragma unroll
+  for (int p = 0; p < 4; ++p) qf[p] = *reinterpret_cast<const uint4*>(&qb[r][32 * p + 8 * q]);
+  float M0 = -INFINITY, M1 = -INFINITY, L0 = 0.f, L1 = 0.f;  // heads 2q, 2q + 1
+  float o[8][4];
+#pragma unroll
+  for (int t = 0; t < 8; ++t) o[t][0] = o[t][1] = o[t][2] = o[t][3] = 0.f;
+#pragma unroll
+  for (int s = 0; s < DT_STEPS; ++s) {
+    float sc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int p = 0; p < 4; ++p)
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+        mma16816(sc, u4w(kf[s][0][p], 2 * h), u4w(kf[s][1][p], 2 * h), u4w(kf[s][0][p], 2 * h + 1),
+                 u4w(kf[s][1][p], 2 * h + 1), u4w(qf[p], 2 * h), u4w(qf[p], 2 * h + 1));
+    const int j0 = kbase + s * 16 + r, j1 = j0 + 8;
+    const bool v0 = j0 < n_keys && (key_pad == nullptr || key_pad[j0] == 0);
+    const bool v1 = j1 < n_keys && (key_pad == nullptr || key_pad[j1] == 0);
+    const float x0 = v0 ? sc[0] * scale_log2 : -INFINITY, x1 = v0 ? sc[1] * scale_log2 : -INFINITY;
+    const float x2 = v1 ? sc[2] * scale_log2 : -INFINITY, x3 = v1 ? sc[3] * scale_log2 : -INFINITY;
+    float m0 = fmaxf(x0, x2), m1 = fmaxf(x1, x3);
+#pragma unroll
+    for (int off = 4; off < 32; off <<= 1) {
+      m0 = fmaxf(m0, __shfl_xor_sync(0xffffffffu, m0, off));
+      m1 = fmaxf(m1, __shfl_xor_sync(0xffffffffu, m1, off));
+    }
+    const float N0 = fmaxf(M0, m0), N1 = fmaxf(M1, m1);
+    const float a0 = N0 == -INFINITY ? 1.f : exp2f(M0 - N0), a1 = N1 == -INFINITY ? 1.f : exp2f(M1 - N1);
+    const float p0 = N0 == -INFINITY ? 0.f : exp2f(x0 - N0), p2 = N0 == -INFINITY ? 0.f : exp2f(x2 - N0);
+    const float p1 = N1 == -INFINITY ? 0.f : exp2f(x1 - N1), p3 = N1 == -INFINITY ? 0.f : exp2f(x3 - N1);
+    M0 = N0;
+    M1 = N1;
+    L0 = fmaf(L0, a0, p0 + p2);
+    L1 = fmaf(L1, a1, p1 + p3);
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      o[t][0] *= a0;
+      o[t][1] *= a1;
+      o[t][2] *= a0;
+      o[t][3] *= a1;
+    }
+    const uint32_t b0 = movtrans(pack_bf16(p0, p1)), b1 = movtrans(pack_bf16(p2, p3));
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const uint32_t wa = u4w(vf[s][0][t >> 2], t & 3), wb = u4w(vf[s][1][t >> 2], t & 3);
+      const uint32_t wc = u4w(vf[s][2][t >> 2], t & 3), wd = u4w(vf[s][3][t >> 2], t & 3);
+      mma16816(o[t], __byte_perm(wa, wb, 0x5410), __byte_perm(wa, wb, 0x7632), __byte_perm(wc, wd, 0x5410),
+               __byte_perm(wc, wd, 0x7632), b0, b1);
+    }
+  }
+#pragma unroll
+  for (int off = 4; off < 32; off <<= 1) {
+    L0 += __shfl_xor_sync(0xffffffffu, L0, off);
+    L1 += __shfl_xor_sync(0xffffffffu, L1, off);
+  }
+  // ---- CTA merge of the 4 warps (fixed order) ----
+#pragma unroll
+  for (int t = 0; t < 8; ++t) {
+    wo[warp][2 * q][16 * r + 2 * t] = o[t][0];
+    wo[warp][2 * q + 1][16 * r + 2 * t] = o[t][1];
+    wo[warp][2 * q][16 * r + 2 * t + 1] = o[t][2];
+    wo[warp][2 * q + 1][16 * r + 2 * t + 1] = o[t][3];
+  }
+  if (r == 0) {
+    wm[warp][2 * q] = M0;
+    wm[warp][2 * q + 1] = M1;
+    wl[warp][2 * q] = L0;
+    wl[warp][2 * q + 1] = L1;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int h = 0; h < G; ++h) {
+    float mc = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < DT_WARPS; ++w) mc = fmaxf(mc, wm[w][h]);
+    float acc = 0.f, lc = 0.f;
+#pragma unroll
+    for (int w = 0; w < DT_WARPS; ++w) {
+      const float a = (mc == -INFINITY || wm[w][h] == -INFINITY) ? 0.f : exp2f(wm[w][h] - mc);
+      acc = fmaf(wo[w][h][tid], a, acc);
+      lc = fmaf(wl[w][h], a, lc);
+    }
+    const int head = g * G + h;
+    part_o[((int64_t)c * Hq + head) * DA_DH + tid] = acc;
+    if (tid == 0) part_ml[(int64_t)c * Hq + head] = make_float2(mc, lc);
+  }
+  // ---- last CTA of the group folds the chunks ----
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) ticket_s = atomicAdd(&tickets[g], 1u);
+  __syncthreads();
+  if (ticket_s != (unsigned)(n_chunks - 1)) {
+    dtrace(3, t0, t1);
+    return;
+  }
+  if (tid == 0) tickets[g] = 0u;
+  __threadfence();
+  float* wsm = &wo[0][0][0] + warp * DF_MAXC;  // chunk weights of this warp's head (wo is free now)
+  for (int h = warp; h < G; h += DT_WARPS) {
+    const int head = g * G + h;
+    float m = -INFINITY;
+    for (int cc = lane; cc < n_chunks; cc += 32) m = fmaxf(m, __ldcg(&part_ml[(int64_t)cc * Hq + head]).x);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
+    float l = 0.f;
+    for (int cc = lane; cc < n_chunks; cc += 32) {
+      const float2 ml = __ldcg(&part_ml[(int64_t)cc * Hq + head]);
+      const float w = (m == -INFINITY || ml.x == -INFINITY) ? 0.f : exp2f(ml.x - m);
+      wsm[cc] = w;
+      l = fmaf(ml.y, w, l);
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) l += __shfl_xor_sync(0xffffffffu, l, off);
+    __syncwarp();
+    const float4* po = reinterpret_cast<const float4*>(part_o) + (int64_t)head * (DA_DH / 4) + lane;
+    const int64_t cstride = (int64_t)Hq * (DA_DH / 4);
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    int cc = 0;
+    for (; cc + 15 < n_chunks; cc += 16) {
+      float4 v[16];
+#pragma unroll
+      for (int k = 0; k < 16; ++k) v[k] = __ldcg(po + (int64_t)(cc + k) * cstride);
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        const float w = wsm[cc + k];
+        acc.x = fmaf(v[k].x, w, acc.x);
+        acc.y = fmaf(v[k].y, w, acc.y);
+        acc.z = fmaf(v[k].z, w, acc.z);
+        acc.w = fmaf(v[k].w, w, acc.w);
+      }
+    }
+    for (; cc < n_chunks; ++cc) {
+      const float4 v = __ldcg(po + (int64_t)cc * cstride);
+      const float w = wsm[cc];
+      acc.x = fmaf(v.x, w, acc.x);
+      acc.y = fmaf(v.y, w, acc.y);
+      acc.z = fmaf(v.z, w, acc.z);
+      acc.w = fmaf(v.w, w, acc.w);
+    }
+    const float inv = l > 0.f ? 1.f / l : 0.f;
+    __nv_bfloat162 lo = __floats2bfloat162_rn(acc.x * inv, acc.y * inv);
+    __nv_bfloat162 hi = __floats2bfloat162_rn(acc.z * inv, acc.w * inv);
+    *reinterpret_cast<uint2*>(ctx + (int64_t)head * DA_DH + 4 * lane) =
+        make_uint2(*reinterpret_cast<uint32_t*>(&lo), *reinterpret_cast<uint32_t*>(&hi));
+    if (lane == 0 && lse != nullptr) lse[head] = l > 0.f ? (m + log2f(l)) * 0.6931471805599453f : -INFINITY;
+  }
+  dtrace(4, t0, t1);
+}
+
 // grid Hq, 128 threads: fold the chunks in index order
 // One warp per (head, 32 output columns): 4 x Hq CTAs instead of Hq, every
 // chunk partial a coalesced 128-byte row load.  Same arithmetic order as the
@@ -389,8 +1154,66 @@ bool gemv_eligible(int M, int N, int K, int epi, const void* A, int64_t lda, con
   return ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(W)) & 15) == 0;
 }
 
+// Zero-initialised device buffers per (device, stream, tag) for tickets the
+// kernels reset themselves after use (allocated and cleared once, outside any
+// graph capture: the first eager call on a stream).
+void* zeroed_scratch(cudaStream_t st, int tag, size_t bytes) {
+  static std::mutex mu;
+  static std::unordered_map<uint64_t, std::pair<void*, size_t>> bufs;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t key = (reinterpret_cast<uint64_t>(st) << 8) ^ ((uint64_t)dev << 4) ^ (uint64_t)tag;
+  std::lock_guard<std::mutex> g(mu);
+  auto& b = bufs[key];
+  if (b.second < bytes) {
+    void* p = nullptr;
+    if (cudaMalloc(&p, bytes) != cudaSuccess) return nullptr;
+    cudaMemset(p, 0, bytes);
+    b = {p, bytes};  // a smaller predecessor is retired, never freed (a captured graph may use it)
+  }
+  return b.first;
+}
+constexpr int GS_MAX_SEAMS = 8192;
+
+// the streaming kernel (one row, weights through cp.async rings) takes the shape?
+bool gemv_stream_ok(int M, int K, int epi) {
+  static const int on = [] {
+    const char* e = getenv("CCB_GEMV_STREAM");
+    return e ? atoi(e) : 1;
+  }();
+  if (!on || M != 1) return false;
+  const int pe = epi == CC_EPI_SWIGLU ? std::min(K, GS_CFG.sb / 4) : std::min(K, GS_CFG.sb / 2);
+  return pe % 256 == 0 && K % pe == 0 && GS_CFG.nw * GS_CFG.ns * GS_CFG.sb + K * 2 <= 227 * 1024;
+}
+
+int gemv_stream_launch(const void* A, const void* W, int64_t ldw, void* C, int N, int K, int epi, const float* norm_w,
+                       float eps, bool norm, cudaStream_t st) {
+  constexpr GsCfg c = GS_CFG;
+  float4* seam = reinterpret_cast<float4*>(zeroed_scratch(st, 1, GS_MAX_SEAMS * (2 * sizeof(float4) + sizeof(unsigned))));
+  if (!seam) return fail(CC_E_CUDA, "gemv_stream: seam buffer allocation failed");
+  if (num_sms() * c.nw + 1 > GS_MAX_SEAMS) return fail(CC_E_UNSUP, "gemv_stream: too many warps");
+  const size_t smem = std::max<size_t>((size_t)c.nw * c.ns * c.sb + (size_t)K * 2, GS_MIN_SMEM);
+  auto go = [&](auto kern) -> int {
+    if (int rc = ensure_smem(kern, smem)) return rc;
+    return launch_k(kern, dim3(num_sms()), dim3(c.nw * 32), smem, st, "gemv_stream", A, (const __nv_bfloat16*)W, ldw,
+                    C, N, K, norm_w, eps, seam, reinterpret_cast<unsigned*>(seam + 2 * GS_MAX_SEAMS));
+  };
+  auto by_norm = [&](auto e_tag) -> int {
+    constexpr int E = decltype(e_tag)::value;
+    return norm ? go(gemv_stream_kernel<E, true, c.nw, c.sb, c.ns>) : go(gemv_stream_kernel<E, false, c.nw, c.sb, c.ns>);
+  };
+  switch (epi) {
+    case CC_EPI_STORE: return by_norm(std::integral_constant<int, CC_EPI_STORE>{});
+    case CC_EPI_RESID_ADD: return by_norm(std::integral_constant<int, CC_EPI_RESID_ADD>{});
+    case CC_EPI_SWIGLU: return by_norm(std::integral_constant<int, CC_EPI_SWIGLU>{});
+    case CC_EPI_GELU: return by_norm(std::integral_constant<int, CC_EPI_GELU>{});
+    default: return fail(CC_E_ARG, "gemv: unknown epilogue");
+  }
+}
+
 int gemv_launch(const void* A, int64_t lda, const void* W, int64_t ldw, void* C, int64_t ldc, int M, int N, int K,
                 int epi, const float* norm_w, float eps, bool norm, cudaStream_t st) {
+  if (gemv_stream_ok(M, K, epi)) return gemv_stream_launch(A, W, ldw, C, N, K, epi, norm_w, eps, norm, st);
   const int n_out = epi == CC_EPI_SWIGLU ? N / 2 : N;
   const size_t smem = (size_t)M * K * 2;
   int grid = (n_out + GV_WARPS - 1) / GV_WARPS;
@@ -478,6 +1301,57 @@ int decode_attention_impl(const void* q, const void* k_rot, const void* v, const
                   n_keys_dev);
 }
 
+int decode_attention_qkv_impl(const void* qkv, const int32_t* slot, const int32_t* pos, const void* rope_table,
+                              void* kv_k, void* kv_v, void* k_rot, const uint8_t* key_pad, void* ctx, float* lse,
+                              int n_keys, const int32_t* n_keys_dev, int max_keys, int n_heads, int n_kv_heads,
+                              int d_head, cudaStream_t st) {
+  CCB_REQUIRE(max_keys >= 1 && n_heads >= 1 && n_kv_heads >= 1 && n_heads % n_kv_heads == 0 && n_kv_heads <= 1024,
+              "decode_attention_qkv: bad shape");
+  CCB_REQUIRE(n_keys_dev != nullptr || (n_keys >= 1 && n_keys <= max_keys), "decode_attention_qkv: bad key count");
+  if (d_head != DA_DH) return fail(CC_E_UNSUP, "decode_attention_qkv: d_head must be 128");
+  const int n_chunks = (max_keys + DA_KEYS - 1) / DA_KEYS;
+  if (n_chunks > DF_MAXC) return fail(CC_E_UNSUP, "decode_attention_qkv: more than 128k keys");
+  const size_t bytes = (size_t)n_chunks * n_heads * (DA_DH * sizeof(float) + sizeof(float2));
+  uint8_t* scratch = (uint8_t*)stream_scratch(st, SCR_DECODE_ATTN, bytes);
+  unsigned* tickets = reinterpret_cast<unsigned*>(zeroed_scratch(st, 2, 1024 * sizeof(unsigned)));
+  if (!scratch || !tickets) return fail(CC_E_CUDA, "decode_attention_qkv: scratch allocation failed");
+  float* part_o = reinterpret_cast<float*>(scratch);
+  float2* part_ml = reinterpret_cast<float2*>(scratch + (size_t)n_chunks * n_heads * DA_DH * sizeof(float));
+  const float scale_log2 = 1.4426950408889634f / sqrtf((float)d_head);
+  static const int use_tc = [] {
+    const char* e = getenv("CCB_DECODE_ATTN_TC");
+    return e ? atoi(e) : 1;
+  }();
+  if (use_tc) {
+    auto go_tc = [&](auto kern) {
+      return launch_k(kern, dim3(n_kv_heads, n_chunks), dim3(DT_WARPS * 32), 0, st, "decode_attention_qkv",
+                      (const __nv_bfloat16*)qkv, slot, pos, (const float2*)rope_table, (__nv_bfloat16*)kv_k,
+                      (__nv_bfloat16*)kv_v, (__nv_bfloat16*)k_rot, key_pad, part_o, part_ml, tickets,
+                      (__nv_bfloat16*)ctx, lse, n_keys, n_keys_dev, max_keys, n_heads, n_kv_heads, scale_log2);
+    };
+    switch (n_heads / n_kv_heads) {
+      case 1: return go_tc(decode_attn_tc<1>);
+      case 2: return go_tc(decode_attn_tc<2>);
+      case 4: return go_tc(decode_attn_tc<4>);
+      case 8: return go_tc(decode_attn_tc<8>);
+      default: return fail(CC_E_UNSUP, "decode_attention_qkv: GQA group must be 1, 2, 4 or 8");
+    }
+  }
+  auto go = [&](auto kern) {
+    return launch_k(kern, dim3(n_kv_heads, n_chunks), dim3(DA_KEYS), 0, st, "decode_attention_qkv",
+                    (const __nv_bfloat16*)qkv, slot, pos, (const float2*)rope_table, (__nv_bfloat16*)kv_k,
+                    (__nv_bfloat16*)kv_v, (__nv_bfloat16*)k_rot, key_pad, part_o, part_ml, tickets,
+                    (__nv_bfloat16*)ctx, lse, n_keys, n_keys_dev, n_heads, n_kv_heads, scale_log2);
+  };
+  switch (n_heads / n_kv_heads) {
+    case 1: return go(decode_attn_fused<1>);
+    case 2: return go(decode_attn_fused<2>);
+    case 4: return go(decode_attn_fused<4>);
+    case 8: return go(decode_attn_fused<8>);
+    default: return fail(CC_E_UNSUP, "decode_attention_qkv: GQA group must be 1, 2, 4 or 8");
+  }
+}
+
 // one decode step's bookkeeping on the device (graph-replayable):
 // tokens[state[0]] = *cur_tok; state[0]++ (count); state[1]++ (slot);
 // state[2]++ (position); state[3]++ (live keys)
@@ -533,4 +1407,23 @@ extern "C" int cc_rope_rows(const void* x, void* y, int64_t n_rows, int n, int w
         (const T*)x, (T*)y, n, width, positions, (const typename CS<T>::type*)rope_table, d_head);
     return check_launch("rope_rows");
   });
+}
+
+extern "C" int cc_decode_attention_qkv(const void* qkv, const int32_t* slot, const int32_t* pos,
+                                       const void* rope_table, void* kv_k, void* kv_v, void* k_rot,
+                                       const uint8_t* key_pad, void* ctx, float* lse, int n_keys,
+                                       const int32_t* n_keys_dev, int max_keys, int n_heads, int n_kv_heads,
+                                       int d_head, void* stream) {
+  return decode_attention_qkv_impl(qkv, slot, pos, rope_table, kv_k, kv_v, k_rot, key_pad, ctx, lse, n_keys,
+                                   n_keys_dev, max_keys, n_heads, n_kv_heads, d_head, as_stream(stream));
+}
+
+// Arm (buf != NULL: capacity records of 4 x u64) or disarm the decode-chain timeline.
+extern "C" __attribute__((visibility("default"))) int cc_debug_decode_trace(void* buf, int cap) {
+  unsigned long long* p = reinterpret_cast<unsigned long long*>(buf);
+  unsigned c = buf ? (unsigned)cap : 0u, z = 0u;
+  if (cudaMemcpyToSymbol(g_dtrace, &p, sizeof(p)) != cudaSuccess || cudaMemcpyToSymbol(g_dtrace_cap, &c, sizeof(c)) != cudaSuccess ||
+      cudaMemcpyToSymbol(g_dtrace_n, &z, sizeof(z)) != cudaSuccess)
+    return fail(CC_E_CUDA, "decode_trace: cudaMemcpyToSymbol failed");
+  return 0;
 }

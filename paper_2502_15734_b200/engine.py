@@ -17,6 +17,7 @@ libcc_b200.so; torch only allocates memory and provides the stream.
 from __future__ import annotations
 
 import contextlib
+import os
 
 import numpy as np
 
@@ -97,6 +98,7 @@ class DevicePlan:
         }
         self.stats_segments = None
         self.stats_rows = np.zeros(0, np.int32)
+        self.stats_keys = 0.0
         offs, cur = {}, 0
         for k, a in parts.items():
             offs[k] = (cur, a.size)
@@ -500,8 +502,10 @@ def _execute(model: Model, plan: DevicePlan, ws: dict, *, record=False, record_v
             N.call("cc_attention", P(q_rot), P(k_rot[l]), P(kv_v[l]), P(D["row_slot"]), key_pad, P(ctx), P(lse), n_l,
                    n, H, Hkv, dh, dt, attn_impl, s)
         if n_stats:
-            N.call("cc_segment_mass", P(q_rot), P(k_rot[l]), P(D["row_slot"]), key_pad, P(lse), P(D["seg_lo"]),
-                   P(D["seg_hi"]), n_seg, P(D["stats_rows"]), n_stats, P(mass[l]), n, H, Hkv, dh, dt, s)
+            # algorithmic FLOPs: q.k over every causal key of each stats row
+            with tm.span("segment_mass", flops=2.0 * H * dh * plan.stats_keys):
+                N.call("cc_segment_mass", P(q_rot), P(k_rot[l]), P(D["row_slot"]), key_pad, P(lse), P(D["seg_lo"]),
+                       P(D["seg_hi"]), n_seg, P(D["stats_rows"]), n_stats, P(mass[l]), n, H, Hkv, dh, dt, s)
         pending_cut = None
         if focus is not None and focus.result is None and n_stats:
             # question rows are the last stats span; their mass onto each chunk span
@@ -710,6 +714,7 @@ def _attach_stats_rows(model, plan: DevicePlan, spans):
     sr = np.concatenate(rows).astype(np.int32) if rows else np.zeros(0, np.int32)
     plan.stats_rows = sr
     plan.stats_row_spans = spans
+    plan.stats_keys = float(plan.rows[sr].astype(np.int64).sum() + sr.size)  # causal keys the K8 rows score
     segs = plan.stats_segments
     host = np.concatenate([sr, np.array([a for a, _ in segs], np.int32), np.array([b for _, b in segs], np.int32)])
     dev = torch.from_numpy(host).to(model.device)
@@ -855,12 +860,18 @@ class DecodeSession:
         self.fast_attn = (model.dtype_code == N.BF16 and cfg.head_dim() == 128
                           and cfg.n_heads // cfg.kv_heads() in (1, 2, 4, 8))
         self.graphable = self.fast_attn and not tp
+        # bf16: RoPE + append + split-KV attention + combine in one launch per layer
+        self.fused_attn = self.fast_attn and cap <= 131072 and os.environ.get("CCB_DECODE_FUSED", "1") != "0"
         # bf16: fused RMSNorm + weight-streaming GEMV (cc_gemv_rmsnorm) when eligible
         self.fused_norm = (model.dtype_code == N.BF16 and cfg.d_model % 8 == 0
                            and cfg.d_model * 2 <= 96 * 1024 and (cfg.mlp != "swiglu" or (2 * cfg.ff_dim()) % 128 == 0))
         self.graph = None
         self.replay_events = None
-        self.pdl = False
+        # programmatic dependent launch: the streaming GEMVs fill their weight
+        # rings before griddepcontrol.wait, so each one's first ~100 KiB per SM
+        # load while its predecessor runs (with the unfused chain PDL measured
+        # slower: parked dependents only cut the running GEMV's occupancy)
+        self.pdl = self.fused_attn and os.environ.get("CCB_DECODE_PDL", "1") != "0"
 
     def _argmax(self, rows, out_ptr):
         m = self.model
@@ -889,17 +900,22 @@ class DecodeSession:
                 N.call("cc_rmsnorm", P(hid), P(self.xn), P(lw.get("attn_norm")), 1, d, cfg.rms_eps, dt, s)
                 N.call("cc_gemm", P(self.xn), d, P(lw["w_qkv"]), d, P(self.qkv), qw + 2 * kvw, 1, qw + 2 * kvw, d,
                        N.EPI_STORE, dt, 0, s)
-            N.call("cc_rope_scatter_qkv", P(self.qkv), qw + 2 * kvw, 1, slot_ptr, pos_ptr, P(self.rope),
-                   P(self.q_rot), P(self.kv_k[l]), P(self.kv_v[l]), P(self.k_rot[l]), H, Hkv, dh, dt, s)
-            if n_keys is None:
-                N.call("cc_decode_attention_dev", P(self.q_rot), P(self.k_rot[l]), P(self.kv_v[l]), pad, P(self.ctx),
-                       P(self.lse), P(self.state[3:4]), self.cap, H, Hkv, dh, s)
-            elif self.fast_attn:
-                N.call("cc_decode_attention", P(self.q_rot), P(self.k_rot[l]), P(self.kv_v[l]), pad, P(self.ctx),
-                       P(self.lse), n_keys, H, Hkv, dh, s)
+            if self.fused_attn:
+                N.call("cc_decode_attention_qkv", P(self.qkv), slot_ptr, pos_ptr, P(self.rope), P(self.kv_k[l]),
+                       P(self.kv_v[l]), P(self.k_rot[l]), pad, P(self.ctx), P(self.lse), n_keys or 0,
+                       P(self.state[3:4]) if n_keys is None else None, self.cap, H, Hkv, dh, s)
             else:
-                N.call("cc_attention", P(self.q_rot), P(self.k_rot[l]), P(self.kv_v[l]), slot_ptr, pad,
-                       P(self.ctx), P(self.lse), 1, n_keys, H, Hkv, dh, dt, 0, s)
+                N.call("cc_rope_scatter_qkv", P(self.qkv), qw + 2 * kvw, 1, slot_ptr, pos_ptr, P(self.rope),
+                       P(self.q_rot), P(self.kv_k[l]), P(self.kv_v[l]), P(self.k_rot[l]), H, Hkv, dh, dt, s)
+                if n_keys is None:
+                    N.call("cc_decode_attention_dev", P(self.q_rot), P(self.k_rot[l]), P(self.kv_v[l]), pad,
+                           P(self.ctx), P(self.lse), P(self.state[3:4]), self.cap, H, Hkv, dh, s)
+                elif self.fast_attn:
+                    N.call("cc_decode_attention", P(self.q_rot), P(self.k_rot[l]), P(self.kv_v[l]), pad,
+                           P(self.ctx), P(self.lse), n_keys, H, Hkv, dh, s)
+                else:
+                    N.call("cc_attention", P(self.q_rot), P(self.k_rot[l]), P(self.kv_v[l]), slot_ptr, pad,
+                           P(self.ctx), P(self.lse), 1, n_keys, H, Hkv, dh, dt, 0, s)
             if tp is None:
                 N.call("cc_gemm", P(self.ctx), qw, P(lw["w_o"]), qw, P(hid), d, 1, d, qw, N.EPI_RESID_ADD, dt, 0, s)
             else:
@@ -939,9 +955,6 @@ class DecodeSession:
         no per-token host work.  Otherwise every step is launched eagerly."""
         import torch
 
-        # programmatic dependent launch of the decode chain is available
-        # (cc_set_pdl) but measured slower on B200 here (3.86 -> 4.08 ms/token:
-        # parked dependent CTAs cut the running GEMV's occupancy); off by default
         prev_pdl = N.lib().cc_set_pdl(1 if self.pdl else 0)
         try:
             self._run(last_hidden_dev)

@@ -212,3 +212,85 @@ def test_rope_rows_matches_oracle(cc):
     N.call("cc_rope_rows", N.ptr(xd), N.ptr(y), L * n, n, width, N.ptr(pd), N.ptr(table), dh, N.F64, N.stream_ptr())
     want = np.stack([O.rope(x[l], pos, model.config.rpe_base, dh) for l in range(L)])
     np.testing.assert_allclose(y.cpu().numpy(), want, atol=1e-12)
+
+
+@pytest.mark.parametrize("n_keys,G,pads,dev", [(1, 4, False, False), (300, 4, True, True), (5153, 4, False, True),
+                                               (777, 1, True, False), (2050, 8, False, True), (129, 2, False, True)])
+def test_decode_attention_qkv_matches_unfused(cc, n_keys, G, pads, dev):
+    """cc_decode_attention_qkv (RoPE + append + split-KV + in-kernel combine,
+    one launch) against cc_rope_scatter_qkv + cc_decode_attention: appended
+    K / rotated K / V bit-identical, ctx within one bf16 ulp (only the chunk
+    fold order differs), both against torch fp32; deterministic across calls
+    (the combine tickets reset themselves)."""
+    N = cc._native
+    Hkv, dh = 2, 128
+    Hq, kvw, cap = Hkv * G, Hkv * dh, n_keys + 37
+    gen = torch.Generator(device="cuda").manual_seed(n_keys * 10 + G)
+    qkv = torch.randn((1, (Hq + 2 * Hkv) * dh), generator=gen, device="cuda").bfloat16()
+    base = [torch.randn((cap, kvw), generator=gen, device="cuda").bfloat16() for _ in range(3)]
+    ang = torch.rand((n_keys + 100, dh // 2), generator=gen, device="cuda") * 6.283
+    table = torch.stack([ang.cos(), ang.sin()], dim=-1).contiguous()
+    slot, pos = n_keys - 1, n_keys + 50
+    i32 = dict(dtype=torch.int32, device="cuda")
+    slot_d, pos_d, nk_d = torch.tensor([slot], **i32), torch.tensor([pos], **i32), torch.tensor([n_keys], **i32)
+    pad = torch.zeros((-(-cap // 16) * 16,), dtype=torch.uint8, device="cuda")
+    if pads and n_keys > 20:
+        pad[5:17] = 1
+    padp = N.ptr(pad) if pads else None
+    k1, v1, r1 = (b.clone() for b in base)
+    q_rot = torch.empty((Hq * dh,), dtype=torch.bfloat16, device="cuda")
+    N.call("cc_rope_scatter_qkv", N.ptr(qkv), qkv.shape[1], 1, N.ptr(slot_d), N.ptr(pos_d), N.ptr(table), N.ptr(q_rot),
+           N.ptr(k1), N.ptr(v1), N.ptr(r1), Hq, Hkv, dh, N.BF16, N.stream_ptr())
+    ctx1 = torch.empty((Hq * dh,), device="cuda", dtype=torch.bfloat16)
+    lse1 = torch.empty((Hq,), device="cuda")
+    N.call("cc_decode_attention", N.ptr(q_rot), N.ptr(r1), N.ptr(v1), padp, N.ptr(ctx1), N.ptr(lse1), n_keys, Hq, Hkv,
+           dh, N.stream_ptr())
+    outs = []
+    for _ in range(2):
+        k2, v2, r2 = (b.clone() for b in base)
+        ctx2 = torch.empty_like(ctx1)
+        lse2 = torch.empty_like(lse1)
+        N.call("cc_decode_attention_qkv", N.ptr(qkv), N.ptr(slot_d), N.ptr(pos_d), N.ptr(table), N.ptr(k2), N.ptr(v2),
+               N.ptr(r2), padp, N.ptr(ctx2), N.ptr(lse2), 0 if dev else n_keys, N.ptr(nk_d) if dev else None, cap, Hq,
+               Hkv, dh, N.stream_ptr())
+        assert torch.equal(k1, k2) and torch.equal(v1, v2) and torch.equal(r1, r2)
+        outs.append((ctx2, lse2))
+    ctx2, lse2 = outs[0]
+    assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
+    torch.testing.assert_close(ctx2.float(), ctx1.float(), atol=4e-3, rtol=8e-3)
+    torch.testing.assert_close(lse2, lse1, atol=1e-5, rtol=1e-6)
+    qh = q_rot.float().reshape(Hq, dh)
+    kh = r1[:n_keys].float().reshape(n_keys, Hkv, dh).repeat_interleave(G, dim=1).transpose(0, 1)
+    vh = v1[:n_keys].float().reshape(n_keys, Hkv, dh).repeat_interleave(G, dim=1).transpose(0, 1)
+    s = torch.einsum("hd,hnd->hn", qh, kh) / dh ** 0.5
+    if pads:
+        s[:, pad[:n_keys].bool()] = -float("inf")
+    ref = torch.einsum("hn,hnd->hd", torch.softmax(s, dim=1), vh).reshape(-1)
+    torch.testing.assert_close(ctx2.float(), ref, atol=2e-2, rtol=2e-2)
+    torch.testing.assert_close(lse2, torch.logsumexp(s, dim=1), atol=1e-3, rtol=1e-4)
+
+
+@pytest.mark.parametrize("K,Nn,epi", [(512, 768, "store"), (1536, 640, "resid"), (2048, 1024, "swiglu"),
+                                      (8192, 2304, "gelu"), (28672, 512, "resid")])
+def test_gemv_stream_shapes_vs_torch(cc, K, Nn, epi):
+    """One-row GEMV through the bulk-copy streaming kernel at row lengths that
+    split into 1 / 2 / 14 stages per output and output counts that leave
+    warps with uneven ranges (or none)."""
+    N = cc._native
+    g = torch.Generator(device="cuda").manual_seed(K + Nn)
+    A = torch.randn((1, K), generator=g, device="cuda").bfloat16()
+    W = (torch.randn((Nn, K), generator=g, device="cuda") / K ** 0.5).bfloat16()
+    acc = A.float() @ W.float().T
+    code = {"store": N.EPI_STORE, "resid": N.EPI_RESID_ADD, "swiglu": N.EPI_SWIGLU, "gelu": N.EPI_GELU}[epi]
+    if epi == "resid":
+        C = torch.full((1, Nn), 0.5, device="cuda")
+        ref = acc + 0.5
+    elif epi == "swiglu":
+        C = torch.empty((1, Nn // 2), device="cuda", dtype=torch.bfloat16)
+        a4 = acc.reshape(1, Nn // 128, 2, 64)
+        ref = (torch.nn.functional.silu(a4[:, :, 0]) * a4[:, :, 1]).reshape(1, Nn // 2)
+    else:
+        C = torch.empty((1, Nn), device="cuda", dtype=torch.bfloat16)
+        ref = torch.nn.functional.gelu(acc, approximate="tanh") if epi == "gelu" else acc
+    N.call("cc_gemv", N.ptr(A), K, N.ptr(W), K, N.ptr(C), C.shape[1], 1, Nn, K, code, N.stream_ptr())
+    torch.testing.assert_close(C.float(), ref, atol=2e-2, rtol=2e-2)

@@ -7,6 +7,11 @@ import torch
 sys.path.insert(0, ".")
 from paper_2502_15734_b200 import _native as N
 
+import os
+
+if os.environ.get("CCB_BENCH_PDL") == "1":  # chained launches overlap (the decode chain's mode)
+    N.lib().cc_set_pdl(1)
+
 shapes = [("qkv", 6144, 4096, N.EPI_STORE), ("o", 4096, 4096, N.EPI_RESID_ADD), ("gate_up", 28672, 4096, N.EPI_SWIGLU),
           ("down", 4096, 14336, N.EPI_RESID_ADD), ("unembed-like", 128256, 4096, N.EPI_STORE)]
 
@@ -42,7 +47,7 @@ for name, Nn, K, epi in shapes:
     print(f"gemv {name:12s} N={Nn:6d} K={K:6d}: {ms*1e3:7.1f} us  {gb/ms*1e3:7.0f} GB/s", flush=True)
     del Ws
 
-for n in (1024, 5152, 32800):
+for n in (() if os.environ.get("CCB_BENCH_NOATTN") else (1024, 5152, 32800)):
     Hq, Hkv, dh = 32, 8, 128
     q = torch.randn((Hq * dh,), device="cuda").bfloat16()
     ks = [torch.randn((n, Hkv * dh), device="cuda").bfloat16() for _ in range(4)]

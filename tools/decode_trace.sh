@@ -1,0 +1,10 @@
+run() {
+  env "$@" timeout 900 python bench.py --no-baselines --no-cpu --tiers 0 --steps 3 > gpurun_out/dec_x.json 2> gpurun_out/dec_x.err
+  python -c "
+import json
+d=json.loads(open('gpurun_out/dec_x.json').read().strip().splitlines()[-1])['decode']
+print('$*', d['ms_per_token'], d['roofline']['frac'], d['first_tokens'])
+" || tail -3 gpurun_out/dec_x.err
+}
+export CCB_DECODE_L2PF=0
+for c in 0 1 2 3 4 5 0; do run CCB_GS_CFG=$c; done
