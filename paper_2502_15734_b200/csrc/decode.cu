@@ -16,6 +16,7 @@
 #include <type_traits>
 
 #include <mutex>
+#include <set>
 #include <unordered_map>
 
 #include "common.cuh"
@@ -58,7 +59,10 @@ __device__ __forceinline__ unsigned long long gtime() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
-__device__ __forceinline__ void dtrace(unsigned tag, unsigned long long t0, unsigned long long t1) {
+// (records are 8 x u64: start, released, end, tag|smid|block, checkpoints c1..c4 as offsets from released)
+__device__ __forceinline__ void dtrace(unsigned tag, unsigned long long t0, unsigned long long t1,
+                                       unsigned long long c1 = 0, unsigned long long c2 = 0,
+                                       unsigned long long c3 = 0, unsigned long long c4 = 0) {
   unsigned long long* buf = g_dtrace;
   if (buf == nullptr) return;
   __syncthreads();
@@ -69,10 +73,14 @@ __device__ __forceinline__ void dtrace(unsigned tag, unsigned long long t0, unsi
       unsigned smid;
       asm("mov.u32 %0, %%smid;" : "=r"(smid));
       const unsigned blk = blockIdx.x + blockIdx.y * gridDim.x;
-      buf[4 * i] = t0;
-      buf[4 * i + 1] = t1;
-      buf[4 * i + 2] = t2;
-      buf[4 * i + 3] = ((unsigned long long)tag << 48) | ((unsigned long long)smid << 32) | blk;
+      buf[8 * i] = t0;
+      buf[8 * i + 1] = t1;
+      buf[8 * i + 2] = t2;
+      buf[8 * i + 3] = ((unsigned long long)tag << 48) | ((unsigned long long)smid << 32) | blk;
+      buf[8 * i + 4] = c1 ? c1 - t1 : 0;
+      buf[8 * i + 5] = c2 ? c2 - t1 : 0;
+      buf[8 * i + 6] = c3 ? c3 - t1 : 0;
+      buf[8 * i + 7] = c4 ? c4 - t1 : 0;
     }
   }
 }
@@ -236,12 +244,19 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src, uint64_t 
   asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src), "l"(pol)
                : "memory");
 }
+__device__ __forceinline__ void cp_async16_plain(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
+// <= 48 registers: a 896-thread CTA then leaves room in the register file for
+// one CTA of the fused attention step (168 x 128) -- without it the NORM
+// variants took 58-72 and the attention grid could not land until the QKV
+// projection drained.
 template <int EPI, bool NORM, int GS_WARPS, int GS_STAGE, int GS_STAGES>
-__global__ void __launch_bounds__(GS_WARPS * 32) gemv_stream_kernel(const void* __restrict__ A_,
+__global__ void __maxnreg__(48) gemv_stream_kernel(const void* __restrict__ A_,
                                                                     const __nv_bfloat16* __restrict__ W, int64_t ldw,
                                                                     void* __restrict__ C, int N, int K,
                                                                     const float* __restrict__ norm_w, float eps,
@@ -296,7 +311,7 @@ __global__ void __launch_bounds__(GS_WARPS * 32) gemv_stream_kernel(const void* 
   if constexpr (NORM) {  // weighted RMSNorm of the f32 residual row (same expression as gemv_kernel)
     const float4* x4 = reinterpret_cast<const float4*>(A_);
     float ss = 0.f;
-    constexpr int NR = 4;  // residual words held in registers (K <= 16 * blockDim)
+    constexpr int NR = 1;  // residual words held in registers (K <= 4 * blockDim; the rest re-read)
     float4 xr[NR], gr[NR];
 #pragma unroll
     for (int j = 0; j < NR; ++j) {  // residual + norm weights in one round trip
@@ -339,9 +354,12 @@ __global__ void __launch_bounds__(GS_WARPS * 32) gemv_stream_kernel(const void* 
   }
   __syncthreads();
   float ag = 0.f, au = 0.f;
+  float c_pre = 0.f;  // residual: the row's old value, loaded when its first piece starts
   for (int st = 0; st < n_st; ++st) {
     cp_async_wait<GS_STAGES - 1>();  // this lane's words of stage st have landed
     const int p = (int)((s0 + st) % np);
+    if constexpr (EPI == CC_EPI_RESID_ADD)
+      if (lane == 0 && (p == 0 || st == 0)) c_pre = reinterpret_cast<const float*>(C)[(s0 + st) / np];
     const uint4* wv = reinterpret_cast<const uint4*>(ring + (size_t)(st % GS_STAGES) * GS_STAGE);
     const uint4* xv = reinterpret_cast<const uint4*>(xs + (size_t)p * pe);
 #pragma unroll
@@ -365,10 +383,10 @@ __global__ void __launch_bounds__(GS_WARPS * 32) gemv_stream_kernel(const void* 
         const int sm = hi ? gw : gw + 1;
         if (lane == 0) {
           seam[2 * sm + (hi ? 1 : 0)] = make_float4(ag, au, 0.f, 0.f);
-          __threadfence();
-          finish = atomicAdd(&seam_ticket[sm], 1u) == 1u;
+          unsigned prev;  // release our partial, acquire the other's
+          asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(&seam_ticket[sm]) : "memory");
+          finish = prev == 1u;
           if (finish) {
-            __threadfence();
             const float4 other = __ldcg(&seam[2 * sm + (hi ? 0 : 1)]);
             ag = hi ? other.x + ag : ag + other.x;
             au = hi ? other.y + au : au + other.y;
@@ -378,7 +396,7 @@ __global__ void __launch_bounds__(GS_WARPS * 32) gemv_stream_kernel(const void* 
       }
       if (lane == 0 && finish) {
         if constexpr (EPI == CC_EPI_RESID_ADD) {
-          reinterpret_cast<float*>(C)[o] += ag;
+          reinterpret_cast<float*>(C)[o] = c_pre + ag;
         } else {
           float y = ag;
           if constexpr (EPI == CC_EPI_GELU) y = gelu_tanh(ag);
@@ -792,7 +810,8 @@ __global__ void __launch_bounds__(DA_KEYS) decode_attn_fused(
 // GEMV grid holds > 114 KiB of shared memory per SM), so they are complete.
 // The new key's words are patched in from shared memory after the append;
 // V words of rows past the live keys (uninitialised capacity) are zeroed.
-constexpr int DT_WARPS = 4, DT_STEPS = 2, DT_KC = DT_WARPS * DT_STEPS * 16;  // 128 keys per CTA
+constexpr int DT_WARPS = 4, DT_STEPS = 4, DT_KC = DT_WARPS * DT_STEPS * 16;  // 256 keys per CTA
+constexpr int DT_SMEM = DT_WARPS * 2 * 16 * 32 * 16;                         // staged steps 2-3: 64 KiB
 
 __device__ __forceinline__ void mma16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
                                          uint32_t b0, uint32_t b1) {
@@ -813,106 +832,130 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
 __device__ __forceinline__ uint32_t u4w(const uint4& v, int i) { return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w; }
 
 template <int G>
-__global__ void __launch_bounds__(DT_WARPS * 32) decode_attn_tc(
+__global__ void __launch_bounds__(DT_WARPS * 32, 3) decode_attn_tc(
     const __nv_bfloat16* __restrict__ qkv, const int32_t* __restrict__ slot_p, const int32_t* __restrict__ pos_p,
     const float2* __restrict__ table, __nv_bfloat16* kv_k, __nv_bfloat16* kv_v, __nv_bfloat16* k_rot,
     const uint8_t* __restrict__ key_pad, float* part_o, float2* part_ml, unsigned* tickets,
     __nv_bfloat16* __restrict__ ctx, float* __restrict__ lse, int n_keys, const int32_t* __restrict__ n_keys_dev,
     int max_keys, int Hq, int Hkv, float scale_log2) {
   static_assert(G <= 8, "one n-tile of query heads");
+  extern __shared__ __align__(16) uint4 stg[];  // [warp][staged step][word][lane]
   const unsigned long long t0 = gtime();
   const int g = blockIdx.x, c = blockIdx.y, tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31, r = lane >> 2, q = lane & 3;
   const int kvw = Hkv * DA_DH;
   const int kbase = c * DT_KC + warp * (DT_STEPS * 16);
-  // ---- pre-wait: this warp's K and V words ----
-  uint4 kf[DT_STEPS][2][4];  // [step][key r, r + 8][32-dim pair p]: dims 32p + 8q .. + 7
-  uint4 vf[DT_STEPS][4][2];  // [step][key 2q, 2q+1, 2q+8, 2q+9][half]: dims 16r .. 16r + 15
-#pragma unroll
-  for (int s = 0; s < DT_STEPS; ++s) {
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
+  // a step's 16 words per lane: K keys r, r + 8 (dims 32p + 8q .. + 7) then V
+  // keys 2q, 2q+1, 2q+8, 2q+9 (dims 16r .. 16r + 15)
+  auto word_src = [&](int s, int i) -> const __nv_bfloat16* {
+    if (i < 8) {
+      const int e = i >> 2, p = i & 3;
       const int key = min(kbase + s * 16 + r + 8 * e, max_keys - 1);
-      const __nv_bfloat16* kp = k_rot + (int64_t)key * kvw + g * DA_DH + 8 * q;
+      return k_rot + (int64_t)key * kvw + g * DA_DH + 8 * q + 32 * p;
+    }
+    const int e = (i - 8) >> 1, h = (i - 8) & 1;
+    const int key = min(kbase + s * 16 + 2 * q + (e & 1) + 8 * (e >> 1), max_keys - 1);
+    return kv_v + (int64_t)key * kvw + g * DA_DH + 16 * r + 8 * h;
+  };
+  uint4 kf[2][2][4];  // register buffers of two steps
+  uint4 vf[2][4][2];
+  // ---- pre-wait: steps 0-1 into registers, steps 2-3 into shared memory ----
 #pragma unroll
-      for (int p = 0; p < 4; ++p) kf[s][e][p] = ld_stream16(kp + 32 * p);
+  for (int s = 0; s < 2; ++s)
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const uint4 w = ld_stream16(word_src(s, i));
+      if (i < 8) kf[s][i >> 2][i & 3] = w;
+      else vf[s][(i - 8) >> 1][(i - 8) & 1] = w;
     }
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const int key = min(kbase + s * 16 + 2 * q + (e & 1) + 8 * (e >> 1), max_keys - 1);
-      const __nv_bfloat16* vp = kv_v + (int64_t)key * kvw + g * DA_DH + 16 * r;
-      vf[s][e][0] = ld_stream16(vp);
-      vf[s][e][1] = ld_stream16(vp + 8);
-    }
-  }
+  for (int s = 2; s < DT_STEPS; ++s)
+#pragma unroll
+    for (int i = 0; i < 16; ++i) cp_async16_plain(&stg[((warp * 2 + (s - 2)) * 16 + i) * 32 + lane], word_src(s, i));
+  cp_async_commit();
   pdl_trigger();
   pdl_wait();
   const unsigned long long t1 = gtime();
+  // one round trip: key count, slot, position and the raw q / k / v words of
+  // this group (their addresses do not depend on the position)
   if (n_keys_dev != nullptr) n_keys = *n_keys_dev;
+  const int slot = *slot_p, pos = *pos_p;
+  constexpr int QP = (G * DA_DH / 2 + DT_WARPS * 32 - 1) / (DT_WARPS * 32);  // q rotation pairs per thread
+  const __nv_bfloat16* qrow = qkv + (int64_t)g * G * DA_DH;
+  __nv_bfloat16 qlo[QP], qhi[QP];
+#pragma unroll
+  for (int j = 0; j < QP; ++j) {
+    const int i = tid + j * DT_WARPS * 32, h = i / (DA_DH / 2), jj = i % (DA_DH / 2);
+    if (i < G * DA_DH / 2) {
+      qlo[j] = qrow[h * DA_DH + jj];
+      qhi[j] = qrow[h * DA_DH + jj + DA_DH / 2];
+    }
+  }
+  const __nv_bfloat16* krow = qkv + (int64_t)(Hq + g) * DA_DH;
+  const __nv_bfloat16 kx = krow[tid & (DA_DH / 2 - 1)], ky = krow[(tid & (DA_DH / 2 - 1)) + DA_DH / 2];
+  const __nv_bfloat16 vx = qkv[(int64_t)(Hq + Hkv + g) * DA_DH + tid];
   const int n_chunks = (n_keys + DT_KC - 1) / DT_KC;
-  if (c >= n_chunks) return;
+  if (c >= n_chunks) {
+    cp_async_wait<0>();
+    return;
+  }
   __shared__ __align__(16) __nv_bfloat16 qb[8][DA_DH];
   __shared__ __align__(16) __nv_bfloat16 knew[DA_DH], vnew[DA_DH];
   __shared__ __align__(16) float wo[DT_WARPS][8][DA_DH];
   __shared__ float wm[DT_WARPS][8], wl[DT_WARPS][8];
   __shared__ unsigned ticket_s;
-  const int slot = *slot_p;
-  const float2* cs = table + (int64_t)(*pos_p) * (DA_DH / 2);
-  const __nv_bfloat16* qrow = qkv + (int64_t)g * G * DA_DH;
-  for (int i = tid; i < 8 * DA_DH / 2; i += DT_WARPS * 32) {
-    const int h = i / (DA_DH / 2), jj = i % (DA_DH / 2);
-    __nv_bfloat16 bx = __float2bfloat16_rn(0.f), by = bx;
-    if (h < G) {
+  const float2* cs = table + (int64_t)pos * (DA_DH / 2);
+#pragma unroll
+  for (int j = 0; j < QP; ++j) {
+    const int i = tid + j * DT_WARPS * 32, h = i / (DA_DH / 2), jj = i % (DA_DH / 2);
+    if (i < G * DA_DH / 2) {
       float xr, yr;
-      rope_pair(__bfloat162float(qrow[h * DA_DH + jj]), __bfloat162float(qrow[h * DA_DH + jj + DA_DH / 2]), cs[jj].x,
-                cs[jj].y, xr, yr);
-      bx = __float2bfloat16_rn(xr);
-      by = __float2bfloat16_rn(yr);
+      rope_pair(__bfloat162float(qlo[j]), __bfloat162float(qhi[j]), cs[jj].x, cs[jj].y, xr, yr);
+      qb[h][jj] = __float2bfloat16_rn(xr);
+      qb[h][jj + DA_DH / 2] = __float2bfloat16_rn(yr);
     }
-    qb[h][jj] = bx;
-    qb[h][jj + DA_DH / 2] = by;
   }
+  for (int i = G * DA_DH + tid; i < 8 * DA_DH; i += DT_WARPS * 32) (&qb[0][0])[i] = __float2bfloat16_rn(0.f);
   const bool owner = slot / DT_KC == c;
   if (owner) {  // append this kv head's slice of the new row (rope_scatter's bits)
     const int64_t off = (int64_t)slot * kvw + g * DA_DH;
-    const __nv_bfloat16* krow = qkv + (int64_t)(Hq + g) * DA_DH;
-    const __nv_bfloat16* vrow = qkv + (int64_t)(Hq + Hkv + g) * DA_DH;
     if (tid < DA_DH / 2) {
-      const __nv_bfloat16 x = krow[tid], y = krow[tid + DA_DH / 2];
       float xr, yr;
-      rope_pair(__bfloat162float(x), __bfloat162float(y), cs[tid].x, cs[tid].y, xr, yr);
+      rope_pair(__bfloat162float(kx), __bfloat162float(ky), cs[tid].x, cs[tid].y, xr, yr);
       const __nv_bfloat16 bx = __float2bfloat16_rn(xr), by = __float2bfloat16_rn(yr);
-      kv_k[off + tid] = x;
-      kv_k[off + tid + DA_DH / 2] = y;
+      kv_k[off + tid] = kx;
+      kv_k[off + tid + DA_DH / 2] = ky;
       k_rot[off + tid] = bx;
       k_rot[off + tid + DA_DH / 2] = by;
       knew[tid] = bx;
       knew[tid + DA_DH / 2] = by;
     }
-    const __nv_bfloat16 vx = vrow[tid];
     kv_v[off + tid] = vx;
     vnew[tid] = vx;
   }
   __syncthreads();
-#pragma unroll
-  for (int s = 0; s < DT_STEPS; ++s) {
+  // the new key's words from shared memory; V of rows past the live keys zeroed
+  auto fix = [&](int s, uint4 (&kb)[2][4], uint4 (&vb)[4][2]) {
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
       const int key = kbase + s * 16 + r + 8 * e;
       if (owner && key == slot)
 #pragma unroll
-        for (int p = 0; p < 4; ++p) kf[s][e][p] = *reinterpret_cast<const uint4*>(&knew[32 * p + 8 * q]);
+        for (int p = 0; p < 4; ++p) kb[e][p] = *reinterpret_cast<const uint4*>(&knew[32 * p + 8 * q]);
     }
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       const int key = kbase + s * 16 + 2 * q + (e & 1) + 8 * (e >> 1);
       if (owner && key == slot) {
-        vf[s][e][0] = *reinterpret_cast<const uint4*>(&vnew[16 * r]);
-        vf[s][e][1] = *reinterpret_cast<const uint4*>(&vnew[16 * r + 8]);
+        vb[e][0] = *reinterpret_cast<const uint4*>(&vnew[16 * r]);
+        vb[e][1] = *reinterpret_cast<const uint4*>(&vnew[16 * r + 8]);
       }
-      if (key >= n_keys) vf[s][e][0] = vf[s][e][1] = make_uint4(0, 0, 0, 0);
+      if (key >= n_keys) vb[e][0] = vb[e][1] = make_uint4(0, 0, 0, 0);
     }
-  }
+  };
+  fix(0, kf[0], vf[0]);
+  fix(1, kf[1], vf[1]);
+  const unsigned long long c1 = g_dtrace ? gtime() : 0;
   uint4 qf[4];  // B operand of S^T: head r, dims 32p + 8q .. + 7
 #pragma unroll
   for (int p = 0; p < 4; ++p) qf[p] = *reinterpret_cast<const uint4*>(&qb[r][32 * p + 8 * q]);
@@ -920,21 +963,42 @@ __global__ void __launch_bounds__(DT_WARPS * 32) decode_attn_tc(
   float o[8][4];
 #pragma unroll
   for (int t = 0; t < 8; ++t) o[t][0] = o[t][1] = o[t][2] = o[t][3] = 0.f;
+  // two steps per online-softmax round (steps 0-1 from registers, 2-3 staged)
 #pragma unroll
-  for (int s = 0; s < DT_STEPS; ++s) {
-    float sc[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int pr = 0; pr < DT_STEPS / 2; ++pr) {
+    if (pr == 1) {  // staged steps: this lane's own words back from shared memory
+      cp_async_wait<0>();
 #pragma unroll
-    for (int p = 0; p < 4; ++p)
+      for (int b = 0; b < 2; ++b)
 #pragma unroll
-      for (int h = 0; h < 2; ++h)
-        mma16816(sc, u4w(kf[s][0][p], 2 * h), u4w(kf[s][1][p], 2 * h), u4w(kf[s][0][p], 2 * h + 1),
-                 u4w(kf[s][1][p], 2 * h + 1), u4w(qf[p], 2 * h), u4w(qf[p], 2 * h + 1));
-    const int j0 = kbase + s * 16 + r, j1 = j0 + 8;
-    const bool v0 = j0 < n_keys && (key_pad == nullptr || key_pad[j0] == 0);
-    const bool v1 = j1 < n_keys && (key_pad == nullptr || key_pad[j1] == 0);
-    const float x0 = v0 ? sc[0] * scale_log2 : -INFINITY, x1 = v0 ? sc[1] * scale_log2 : -INFINITY;
-    const float x2 = v1 ? sc[2] * scale_log2 : -INFINITY, x3 = v1 ? sc[3] * scale_log2 : -INFINITY;
-    float m0 = fmaxf(x0, x2), m1 = fmaxf(x1, x3);
+        for (int i = 0; i < 16; ++i) {
+          const uint4 w = stg[((warp * 2 + b) * 16 + i) * 32 + lane];
+          if (i < 8) kf[b][i >> 2][i & 3] = w;
+          else vf[b][(i - 8) >> 1][(i - 8) & 1] = w;
+        }
+      fix(2, kf[0], vf[0]);
+      fix(3, kf[1], vf[1]);
+    }
+    float x[2][4];
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+      const int s = 2 * pr + b;
+      float sc[4] = {0.f, 0.f, 0.f, 0.f}, sd[4] = {0.f, 0.f, 0.f, 0.f};  // even / odd k-tile chains
+#pragma unroll
+      for (int p = 0; p < 4; ++p) {
+        mma16816(sc, kf[b][0][p].x, kf[b][1][p].x, kf[b][0][p].y, kf[b][1][p].y, qf[p].x, qf[p].y);
+        mma16816(sd, kf[b][0][p].z, kf[b][1][p].z, kf[b][0][p].w, kf[b][1][p].w, qf[p].z, qf[p].w);
+      }
+      const int j0 = kbase + s * 16 + r, j1 = j0 + 8;
+      const bool v0 = j0 < n_keys && (key_pad == nullptr || key_pad[j0] == 0);
+      const bool v1 = j1 < n_keys && (key_pad == nullptr || key_pad[j1] == 0);
+      x[b][0] = v0 ? (sc[0] + sd[0]) * scale_log2 : -INFINITY;
+      x[b][1] = v0 ? (sc[1] + sd[1]) * scale_log2 : -INFINITY;
+      x[b][2] = v1 ? (sc[2] + sd[2]) * scale_log2 : -INFINITY;
+      x[b][3] = v1 ? (sc[3] + sd[3]) * scale_log2 : -INFINITY;
+    }
+    float m0 = fmaxf(fmaxf(x[0][0], x[0][2]), fmaxf(x[1][0], x[1][2]));
+    float m1 = fmaxf(fmaxf(x[0][1], x[0][3]), fmaxf(x[1][1], x[1][3]));
 #pragma unroll
     for (int off = 4; off < 32; off <<= 1) {
       m0 = fmaxf(m0, __shfl_xor_sync(0xffffffffu, m0, off));
@@ -942,12 +1006,18 @@ __global__ void __launch_bounds__(DT_WARPS * 32) decode_attn_tc(
     }
     const float N0 = fmaxf(M0, m0), N1 = fmaxf(M1, m1);
     const float a0 = N0 == -INFINITY ? 1.f : exp2f(M0 - N0), a1 = N1 == -INFINITY ? 1.f : exp2f(M1 - N1);
-    const float p0 = N0 == -INFINITY ? 0.f : exp2f(x0 - N0), p2 = N0 == -INFINITY ? 0.f : exp2f(x2 - N0);
-    const float p1 = N1 == -INFINITY ? 0.f : exp2f(x1 - N1), p3 = N1 == -INFINITY ? 0.f : exp2f(x3 - N1);
+    float pv[2][4];
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+      pv[b][0] = N0 == -INFINITY ? 0.f : exp2f(x[b][0] - N0);
+      pv[b][2] = N0 == -INFINITY ? 0.f : exp2f(x[b][2] - N0);
+      pv[b][1] = N1 == -INFINITY ? 0.f : exp2f(x[b][1] - N1);
+      pv[b][3] = N1 == -INFINITY ? 0.f : exp2f(x[b][3] - N1);
+    }
     M0 = N0;
     M1 = N1;
-    L0 = fmaf(L0, a0, p0 + p2);
-    L1 = fmaf(L1, a1, p1 + p3);
+    L0 = fmaf(L0, a0, (pv[0][0] + pv[0][2]) + (pv[1][0] + pv[1][2]));
+    L1 = fmaf(L1, a1, (pv[0][1] + pv[0][3]) + (pv[1][1] + pv[1][3]));
 #pragma unroll
     for (int t = 0; t < 8; ++t) {
       o[t][0] *= a0;
@@ -955,15 +1025,19 @@ __global__ void __launch_bounds__(DT_WARPS * 32) decode_attn_tc(
       o[t][2] *= a0;
       o[t][3] *= a1;
     }
-    const uint32_t b0 = movtrans(pack_bf16(p0, p1)), b1 = movtrans(pack_bf16(p2, p3));
 #pragma unroll
-    for (int t = 0; t < 8; ++t) {
-      const uint32_t wa = u4w(vf[s][0][t >> 2], t & 3), wb = u4w(vf[s][1][t >> 2], t & 3);
-      const uint32_t wc = u4w(vf[s][2][t >> 2], t & 3), wd = u4w(vf[s][3][t >> 2], t & 3);
-      mma16816(o[t], __byte_perm(wa, wb, 0x5410), __byte_perm(wa, wb, 0x7632), __byte_perm(wc, wd, 0x5410),
-               __byte_perm(wc, wd, 0x7632), b0, b1);
+    for (int b = 0; b < 2; ++b) {
+      const uint32_t b0 = movtrans(pack_bf16(pv[b][0], pv[b][1])), b1 = movtrans(pack_bf16(pv[b][2], pv[b][3]));
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        const uint32_t wa = u4w(vf[b][0][t >> 2], t & 3), wb = u4w(vf[b][1][t >> 2], t & 3);
+        const uint32_t wc = u4w(vf[b][2][t >> 2], t & 3), wd = u4w(vf[b][3][t >> 2], t & 3);
+        mma16816(o[t], __byte_perm(wa, wb, 0x5410), __byte_perm(wa, wb, 0x7632), __byte_perm(wc, wd, 0x5410),
+                 __byte_perm(wc, wd, 0x7632), b0, b1);
+      }
     }
   }
+  const unsigned long long c2 = g_dtrace ? gtime() : 0;
 #pragma unroll
   for (int off = 4; off < 32; off <<= 1) {
     L0 += __shfl_xor_sync(0xffffffffu, L0, off);
@@ -1001,19 +1075,30 @@ __global__ void __launch_bounds__(DT_WARPS * 32) decode_attn_tc(
     if (tid == 0) part_ml[(int64_t)c * Hq + head] = make_float2(mc, lc);
   }
   // ---- last CTA of the group folds the chunks ----
-  __threadfence();
   __syncthreads();
-  if (tid == 0) ticket_s = atomicAdd(&tickets[g], 1u);
+  if (tid == 0) {  // release the CTA's partial (cumulative over the barrier), acquire the others'
+    unsigned prev;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(&tickets[g]) : "memory");
+    ticket_s = prev;
+  }
   __syncthreads();
+  const unsigned long long c3 = g_dtrace ? gtime() : 0;
   if (ticket_s != (unsigned)(n_chunks - 1)) {
-    dtrace(3, t0, t1);
+    dtrace(3, t0, t1, c1, c2, c3);
     return;
   }
   if (tid == 0) tickets[g] = 0u;
   __threadfence();
   float* wsm = &wo[0][0][0] + warp * DF_MAXC;  // chunk weights of this warp's head (wo is free now)
+  constexpr int DF_BATCH = 24;  // chunk rows whose loads go out together with the (max, sum) loads
   for (int h = warp; h < G; h += DT_WARPS) {
     const int head = g * G + h;
+    const float4* po = reinterpret_cast<const float4*>(part_o) + (int64_t)head * (DA_DH / 4) + lane;
+    const int64_t cstride = (int64_t)Hq * (DA_DH / 4);
+    float4 vb[DF_BATCH];
+#pragma unroll
+    for (int k = 0; k < DF_BATCH; ++k)
+      vb[k] = k < n_chunks ? __ldcg(po + (int64_t)k * cstride) : make_float4(0.f, 0.f, 0.f, 0.f);
     float m = -INFINITY;
     for (int cc = lane; cc < n_chunks; cc += 32) m = fmaxf(m, __ldcg(&part_ml[(int64_t)cc * Hq + head]).x);
 #pragma unroll
@@ -1028,10 +1113,16 @@ __global__ void __launch_bounds__(DT_WARPS * 32) decode_attn_tc(
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) l += __shfl_xor_sync(0xffffffffu, l, off);
     __syncwarp();
-    const float4* po = reinterpret_cast<const float4*>(part_o) + (int64_t)head * (DA_DH / 4) + lane;
-    const int64_t cstride = (int64_t)Hq * (DA_DH / 4);
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    int cc = 0;
+#pragma unroll
+    for (int k = 0; k < DF_BATCH; ++k) {
+      const float w = k < n_chunks ? wsm[k] : 0.f;
+      acc.x = fmaf(vb[k].x, w, acc.x);
+      acc.y = fmaf(vb[k].y, w, acc.y);
+      acc.z = fmaf(vb[k].z, w, acc.z);
+      acc.w = fmaf(vb[k].w, w, acc.w);
+    }
+    int cc = DF_BATCH;
     for (; cc + 15 < n_chunks; cc += 16) {
       float4 v[16];
 #pragma unroll
@@ -1060,7 +1151,7 @@ __global__ void __launch_bounds__(DT_WARPS * 32) decode_attn_tc(
         make_uint2(*reinterpret_cast<uint32_t*>(&lo), *reinterpret_cast<uint32_t*>(&hi));
     if (lane == 0 && lse != nullptr) lse[head] = l > 0.f ? (m + log2f(l)) * 0.6931471805599453f : -INFINITY;
   }
-  dtrace(4, t0, t1);
+  dtrace(4, t0, t1, c1, c2, c3);
 }
 
 // grid Hq, 128 threads: fold the chunks in index order
@@ -1154,6 +1245,25 @@ bool gemv_eligible(int M, int N, int K, int epi, const void* A, int64_t lda, con
   return ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(W)) & 15) == 0;
 }
 
+// Kernels of the decode chain run with the whole 228 KiB shared-memory
+// carveout: a CTA of the next kernel can only land next to a running CTA when
+// the SM's current carveout has room for both (the default picks the smallest
+// carveout that fits the running kernel, which shuts the next one out).
+template <typename... KArgs>
+int max_carveout(void (*fn)(KArgs...)) {
+  static std::mutex mu;
+  static std::set<std::pair<int, const void*>> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> g(mu);
+  if (done.count({dev, reinterpret_cast<const void*>(fn)})) return 0;
+  if (cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributePreferredSharedMemoryCarveout,
+                           (int)cudaSharedmemCarveoutMaxShared) != cudaSuccess)
+    return fail(CC_E_CUDA, "cudaFuncSetAttribute(carveout) failed");
+  done.insert({dev, reinterpret_cast<const void*>(fn)});
+  return 0;
+}
+
 // Zero-initialised device buffers per (device, stream, tag) for tickets the
 // kernels reset themselves after use (allocated and cleared once, outside any
 // graph capture: the first eager call on a stream).
@@ -1174,6 +1284,10 @@ void* zeroed_scratch(cudaStream_t st, int tag, size_t bytes) {
   return b.first;
 }
 constexpr int GS_MAX_SEAMS = 8192;
+const int g_carveout = [] {
+  const char* e = getenv("CCB_DECODE_CARVEOUT");
+  return e ? atoi(e) : 1;
+}();
 
 // the streaming kernel (one row, weights through cp.async rings) takes the shape?
 bool gemv_stream_ok(int M, int K, int epi) {
@@ -1195,6 +1309,8 @@ int gemv_stream_launch(const void* A, const void* W, int64_t ldw, void* C, int N
   const size_t smem = std::max<size_t>((size_t)c.nw * c.ns * c.sb + (size_t)K * 2, GS_MIN_SMEM);
   auto go = [&](auto kern) -> int {
     if (int rc = ensure_smem(kern, smem)) return rc;
+    if (g_carveout)
+      if (int rc = max_carveout(kern)) return rc;
     return launch_k(kern, dim3(num_sms()), dim3(c.nw * 32), smem, st, "gemv_stream", A, (const __nv_bfloat16*)W, ldw,
                     C, N, K, norm_w, eps, seam, reinterpret_cast<unsigned*>(seam + 2 * GS_MAX_SEAMS));
   };
@@ -1309,8 +1425,13 @@ int decode_attention_qkv_impl(const void* qkv, const int32_t* slot, const int32_
               "decode_attention_qkv: bad shape");
   CCB_REQUIRE(n_keys_dev != nullptr || (n_keys >= 1 && n_keys <= max_keys), "decode_attention_qkv: bad key count");
   if (d_head != DA_DH) return fail(CC_E_UNSUP, "decode_attention_qkv: d_head must be 128");
-  const int n_chunks = (max_keys + DA_KEYS - 1) / DA_KEYS;
-  if (n_chunks > DF_MAXC) return fail(CC_E_UNSUP, "decode_attention_qkv: more than 128k keys");
+  static const int use_tc = [] {
+    const char* e = getenv("CCB_DECODE_ATTN_TC");
+    return e ? atoi(e) : 1;
+  }();
+  const int kc = use_tc ? DT_KC : DA_KEYS;
+  const int n_chunks = (max_keys + kc - 1) / kc;
+  if (n_chunks > DF_MAXC) return fail(CC_E_UNSUP, "decode_attention_qkv: too many keys");
   const size_t bytes = (size_t)n_chunks * n_heads * (DA_DH * sizeof(float) + sizeof(float2));
   uint8_t* scratch = (uint8_t*)stream_scratch(st, SCR_DECODE_ATTN, bytes);
   unsigned* tickets = reinterpret_cast<unsigned*>(zeroed_scratch(st, 2, 1024 * sizeof(unsigned)));
@@ -1318,13 +1439,12 @@ int decode_attention_qkv_impl(const void* qkv, const int32_t* slot, const int32_
   float* part_o = reinterpret_cast<float*>(scratch);
   float2* part_ml = reinterpret_cast<float2*>(scratch + (size_t)n_chunks * n_heads * DA_DH * sizeof(float));
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)d_head);
-  static const int use_tc = [] {
-    const char* e = getenv("CCB_DECODE_ATTN_TC");
-    return e ? atoi(e) : 1;
-  }();
   if (use_tc) {
     auto go_tc = [&](auto kern) {
-      return launch_k(kern, dim3(n_kv_heads, n_chunks), dim3(DT_WARPS * 32), 0, st, "decode_attention_qkv",
+      if (int rc = ensure_smem(kern, DT_SMEM)) return rc;
+      if (g_carveout)
+        if (int rc = max_carveout(kern)) return rc;
+      return launch_k(kern, dim3(n_kv_heads, n_chunks), dim3(DT_WARPS * 32), DT_SMEM, st, "decode_attention_qkv",
                       (const __nv_bfloat16*)qkv, slot, pos, (const float2*)rope_table, (__nv_bfloat16*)kv_k,
                       (__nv_bfloat16*)kv_v, (__nv_bfloat16*)k_rot, key_pad, part_o, part_ml, tickets,
                       (__nv_bfloat16*)ctx, lse, n_keys, n_keys_dev, max_keys, n_heads, n_kv_heads, scale_log2);

@@ -29,7 +29,7 @@ h = torch.from_numpy(np.asarray(res.hidden[req.question_span[1] - 1], np.float64
 engine.DecodeSession(model, res.kv, 3).run(h)
 torch.cuda.synchronize()
 cap = 400000
-buf = torch.zeros((cap, 4), dtype=torch.int64, device="cuda")
+buf = torch.zeros((cap, 8), dtype=torch.int64, device="cuda")
 lib = N.lib()
 lib.cc_debug_decode_trace.argtypes = [ctypes.c_void_p, ctypes.c_int]
 sess = engine.DecodeSession(model, res.kv, 3)
@@ -44,6 +44,7 @@ tag[tag == 4] = 3
 sm = ((r[:, 3] >> np.uint64(32)) & np.uint64(0xFFFF)).astype(int)
 blk = (r[:, 3] & np.uint64(0xFFFFFFFF)).astype(int)
 t0, t1, t2 = (r[:, i].astype(np.int64) for i in range(3))
+cps = r[:, 4:8].astype(np.int64)
 order = np.argsort(t0, kind="stable")
 launches = []
 cur = {}
@@ -86,3 +87,11 @@ for i in range(n // 3, 2 * n // 3):
     tot[nm] += (e - w0) / 1e3
     cnt[nm] += 1
 print("mean wait-released -> end (us):", {k: round(tot[k] / cnt[k], 2) for k in tot})
+att = (tag == 3) & (cps[:, 0] > 0)
+if att.any():
+    c = cps[att] / 1e3
+    last = (r[:, 3] >> np.uint64(48)).astype(int)[att] == 4
+    print("attention CTA checkpoints after release (us, median): rope/append/fix %.2f, steps %.2f, merge+partial+ticket %.2f, end %.2f"
+          % (np.median(c[:, 0]), np.median(c[:, 1]), np.median(c[:, 2]), np.median((t2 - t1)[att]) / 1e3))
+    if last.any():
+        print("combining CTAs: ticket at %.2f, end %.2f" % (np.median(c[last, 2]), np.median((t2 - t1)[att][last]) / 1e3))
