@@ -251,6 +251,23 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
+constexpr int GS_EPI_LOGITS = 16;  // internal epilogue: K7 logits (f32 normed row, f32 out)
+__device__ __forceinline__ float dot8f(const uint4& w, const float4& x0, const float4& x1) {
+  const __nv_bfloat162* a = reinterpret_cast<const __nv_bfloat162*>(&w);
+  float2 f0 = __bfloat1622float2(a[0]), f1 = __bfloat1622float2(a[1]), f2 = __bfloat1622float2(a[2]),
+         f3 = __bfloat1622float2(a[3]);
+  float s = 0.f;
+  s = fmaf(f0.x, x0.x, s);
+  s = fmaf(f0.y, x0.y, s);
+  s = fmaf(f1.x, x0.z, s);
+  s = fmaf(f1.y, x0.w, s);
+  s = fmaf(f2.x, x1.x, s);
+  s = fmaf(f2.y, x1.y, s);
+  s = fmaf(f3.x, x1.z, s);
+  s = fmaf(f3.y, x1.w, s);
+  return s;
+}
+
 // <= 48 registers: a 896-thread CTA then leaves room in the register file for
 // one CTA of the fused attention step (168 x 128) -- without it the NORM
 // variants took 58-72 and the attention grid could not land until the QKV
@@ -264,6 +281,7 @@ __global__ void __maxnreg__(48) gemv_stream_kernel(const void* __restrict__ A_,
   extern __shared__ __align__(128) uint8_t gs_smem[];
   __shared__ float red[GS_WARPS];
   constexpr bool GLU = EPI == CC_EPI_SWIGLU;
+  constexpr bool F32X = EPI == GS_EPI_LOGITS;  // f32 activations (unrounded normed row), f32 output
   constexpr int VPL = GLU ? GS_STAGE / 1024 : GS_STAGE / 512;  // 16-byte words per lane per stage (per row for SwiGLU)
   constexpr int GS_RING = GS_WARPS * GS_STAGES * GS_STAGE;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -282,6 +300,7 @@ __global__ void __maxnreg__(48) gemv_stream_kernel(const void* __restrict__ A_,
   const int n_st = (int)(s1 - s0);
   uint8_t* ring = gs_smem + (size_t)warp * GS_STAGES * GS_STAGE;
   __nv_bfloat16* xs = reinterpret_cast<__nv_bfloat16*>(gs_smem + GS_RING);
+  float* xsf = reinterpret_cast<float*>(gs_smem + GS_RING);
   const unsigned long long t0 = gtime();
   uint64_t pol;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
@@ -336,6 +355,11 @@ __global__ void __maxnreg__(48) gemv_stream_kernel(const void* __restrict__ A_,
     for (int w = 0; w < GS_WARPS; ++w) tot += red[w];
     const float inv = rsqrtf(tot / (float)K + eps);
     auto put = [&](int i, const float4& v, const float4& g) {
+      if constexpr (F32X) {
+        *reinterpret_cast<float4*>(xsf + 4 * i) =
+            make_float4(v.x * inv * g.x, v.y * inv * g.y, v.z * inv * g.z, v.w * inv * g.w);
+        return;
+      }
       __nv_bfloat162 a = __floats2bfloat162_rn(v.x * inv * g.x, v.y * inv * g.y);
       __nv_bfloat162 b = __floats2bfloat162_rn(v.z * inv * g.z, v.w * inv * g.w);
       *reinterpret_cast<uint2*>(xs + 4 * i) =
@@ -362,12 +386,17 @@ __global__ void __maxnreg__(48) gemv_stream_kernel(const void* __restrict__ A_,
       if (lane == 0 && (p == 0 || st == 0)) c_pre = reinterpret_cast<const float*>(C)[(s0 + st) / np];
     const uint4* wv = reinterpret_cast<const uint4*>(ring + (size_t)(st % GS_STAGES) * GS_STAGE);
     const uint4* xv = reinterpret_cast<const uint4*>(xs + (size_t)p * pe);
+    const float4* xf = reinterpret_cast<const float4*>(xsf + (size_t)p * pe);
 #pragma unroll
     for (int i = 0; i < VPL; ++i)
       if (i < nv) {
-        const uint4 x = xv[lane + 32 * i];
-        ag += dot8(wv[lane + 32 * i], x);
-        if constexpr (GLU) au += dot8(wv[GS_STAGE / 32 + lane + 32 * i], x);
+        if constexpr (F32X) {
+          ag += dot8f(wv[lane + 32 * i], xf[2 * (lane + 32 * i)], xf[2 * (lane + 32 * i) + 1]);
+        } else {
+          const uint4 x = xv[lane + 32 * i];
+          ag += dot8(wv[lane + 32 * i], x);
+          if constexpr (GLU) au += dot8(wv[GS_STAGE / 32 + lane + 32 * i], x);
+        }
       }
     issue(st + GS_STAGES);  // refill the slot just read (same lane, same words)
     if (p == np - 1 || st == n_st - 1) {
@@ -397,6 +426,8 @@ __global__ void __maxnreg__(48) gemv_stream_kernel(const void* __restrict__ A_,
       if (lane == 0 && finish) {
         if constexpr (EPI == CC_EPI_RESID_ADD) {
           reinterpret_cast<float*>(C)[o] = c_pre + ag;
+        } else if constexpr (F32X) {
+          reinterpret_cast<float*>(C)[o] = ag;
         } else {
           float y = ag;
           if constexpr (EPI == CC_EPI_GELU) y = gelu_tanh(ag);
@@ -1325,6 +1356,28 @@ int gemv_stream_launch(const void* A, const void* W, int64_t ldw, void* C, int N
     case CC_EPI_GELU: return by_norm(std::integral_constant<int, CC_EPI_GELU>{});
     default: return fail(CC_E_ARG, "gemv: unknown epilogue");
   }
+}
+
+// K7 logits of one row through the streaming kernel (RMSNorm prologue in f32,
+// f32 logits); CC_E_UNSUP when the shape does not fit
+int logits_stream_bf16(const float* hidden, const float* norm_w, float eps, const void* U, float* logits, int d,
+                       int vocab, cudaStream_t st) {
+  static const int on = [] {
+    const char* e = getenv("CCB_LOGITS_STREAM");
+    return e ? atoi(e) : 1;
+  }();
+  const int pe = std::min(d, GS_CFG.sb / 2);
+  const size_t smem = std::max<size_t>((size_t)GS_CFG.nw * GS_CFG.ns * GS_CFG.sb + (size_t)d * 4, GS_MIN_SMEM);
+  if (!on || pe % 256 || d % pe || smem > 227 * 1024 || (reinterpret_cast<uintptr_t>(hidden) & 15) ||
+      (reinterpret_cast<uintptr_t>(norm_w) & 15) || (reinterpret_cast<uintptr_t>(U) & 15))
+    return CC_E_UNSUP;
+  float4* seam = reinterpret_cast<float4*>(zeroed_scratch(st, 1, GS_MAX_SEAMS * (2 * sizeof(float4) + sizeof(unsigned))));
+  if (!seam) return fail(CC_E_CUDA, "logits: seam buffer allocation failed");
+  auto kern = gemv_stream_kernel<GS_EPI_LOGITS, true, GS_CFG.nw, GS_CFG.sb, GS_CFG.ns>;
+  if (int rc = ensure_smem(kern, smem)) return rc;
+  return launch_k(kern, dim3(num_sms()), dim3(GS_CFG.nw * 32), smem, st, "logits_stream", (const void*)hidden,
+                  (const __nv_bfloat16*)U, (int64_t)d, (void*)logits, vocab, d, norm_w, eps, seam,
+                  reinterpret_cast<unsigned*>(seam + 2 * GS_MAX_SEAMS));
 }
 
 int gemv_launch(const void* A, int64_t lda, const void* W, int64_t ldw, void* C, int64_t ldc, int M, int N, int K,

@@ -14,6 +14,7 @@
 #include <type_traits>
 
 #include "common.cuh"
+#include "gemm.cuh"
 
 namespace ccb {
 
@@ -807,8 +808,13 @@ int cc_logits_argmax(const void* hidden_rows, const float* norm_w, double eps, c
     // 24 CTAs per SM (several waves of short CTAs): measured 198 us for the
     // 128256 x 4096 unembedding vs 217 (8 per SM), 207 (12), 208 (16), 204 (32)
     int grid = std::min((vocab + 7) / 8, num_sms() * 24);
-    int rc = launch_k(logits_kernel<T>, dim3(grid), dim3(256), smem, as_stream(stream), "logits",
-                      (const A*)hidden_rows, norm_w, eps, (const T*)unembed, (A*)logits, m, d, vocab);
+    int rc = CC_E_UNSUP;
+    if constexpr (std::is_same<T, __nv_bfloat16>::value)  // one row: the weight-streaming GEMV (decode.cu)
+      if (m == 1) rc = logits_stream_bf16((const float*)hidden_rows, norm_w, (float)eps, unembed, (float*)logits, d,
+                                          vocab, as_stream(stream));
+    if (rc == CC_E_UNSUP)
+      rc = launch_k(logits_kernel<T>, dim3(grid), dim3(256), smem, as_stream(stream), "logits",
+                    (const A*)hidden_rows, norm_w, eps, (const T*)unembed, (A*)logits, m, d, vocab);
     if (rc) return rc;
     if (argmax) {
       // partials live after the logits rows in a small static scratch
