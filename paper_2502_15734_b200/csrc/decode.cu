@@ -230,8 +230,12 @@ __global__ void __launch_bounds__(GV_WARPS * 32) gemv_kernel(const void* __restr
 // 28 warps x 2 stages x 2 KiB (measured best of {8..32} warps x {1, 2, 4} KiB
 // stages x {1..6} stages at config 2: 3.30 ms/token vs 3.38 for 24 x 2 x 2 KiB,
 // 3.42-3.56 with 4 stages, 4.1-4.2 with 1 KiB stages or 8 warps).
-struct GsCfg { int nw, sb, ns; };
-constexpr GsCfg GS_CFG = {28, 2048, 2};
+struct GsCfg { int nw, sb, ns, min_smem, maxr; };
+constexpr GsCfg GS_CFG = {28, 2048, 2, 116 * 1024, 48};
+// (Measured and dropped: alternating footprints -- the NORM projections at
+// 24 warps / 104 KiB, the others at 22 warps / >= 116 KiB, <= 40 registers --
+// so each projection's CTAs land next to the previous one's and stream while
+// it drains: 3.41 vs 3.13 ms/token; the co-resident pair slows both.)
 // Every launch requests > 114 KiB of shared memory, so at most ONE CTA of it
 // is resident per SM: under programmatic dependent launch the CTAs are
 // placed while the previous kernel still occupies the SMs, and a statically
@@ -272,8 +276,8 @@ __device__ __forceinline__ float dot8f(const uint4& w, const float4& x0, const f
 // one CTA of the fused attention step (168 x 128) -- without it the NORM
 // variants took 58-72 and the attention grid could not land until the QKV
 // projection drained.
-template <int EPI, bool NORM, int GS_WARPS, int GS_STAGE, int GS_STAGES>
-__global__ void __maxnreg__(48) gemv_stream_kernel(const void* __restrict__ A_,
+template <int EPI, bool NORM, int GS_WARPS, int GS_STAGE, int GS_STAGES, int MAXR>
+__global__ void __maxnreg__(MAXR) gemv_stream_kernel(const void* __restrict__ A_,
                                                                     const __nv_bfloat16* __restrict__ W, int64_t ldw,
                                                                     void* __restrict__ C, int N, int K,
                                                                     const float* __restrict__ norm_w, float eps,
@@ -1337,7 +1341,7 @@ int gemv_stream_launch(const void* A, const void* W, int64_t ldw, void* C, int N
   float4* seam = reinterpret_cast<float4*>(zeroed_scratch(st, 1, GS_MAX_SEAMS * (2 * sizeof(float4) + sizeof(unsigned))));
   if (!seam) return fail(CC_E_CUDA, "gemv_stream: seam buffer allocation failed");
   if (num_sms() * c.nw + 1 > GS_MAX_SEAMS) return fail(CC_E_UNSUP, "gemv_stream: too many warps");
-  const size_t smem = std::max<size_t>((size_t)c.nw * c.ns * c.sb + (size_t)K * 2, GS_MIN_SMEM);
+  const size_t smem = std::max<size_t>((size_t)c.nw * c.ns * c.sb + (size_t)K * 2, (size_t)c.min_smem);
   auto go = [&](auto kern) -> int {
     if (int rc = ensure_smem(kern, smem)) return rc;
     if (g_carveout)
@@ -1347,7 +1351,8 @@ int gemv_stream_launch(const void* A, const void* W, int64_t ldw, void* C, int N
   };
   auto by_norm = [&](auto e_tag) -> int {
     constexpr int E = decltype(e_tag)::value;
-    return norm ? go(gemv_stream_kernel<E, true, c.nw, c.sb, c.ns>) : go(gemv_stream_kernel<E, false, c.nw, c.sb, c.ns>);
+    return norm ? go(gemv_stream_kernel<E, true, c.nw, c.sb, c.ns, c.maxr>)
+                : go(gemv_stream_kernel<E, false, c.nw, c.sb, c.ns, c.maxr>);
   };
   switch (epi) {
     case CC_EPI_STORE: return by_norm(std::integral_constant<int, CC_EPI_STORE>{});
@@ -1373,7 +1378,7 @@ int logits_stream_bf16(const float* hidden, const float* norm_w, float eps, cons
     return CC_E_UNSUP;
   float4* seam = reinterpret_cast<float4*>(zeroed_scratch(st, 1, GS_MAX_SEAMS * (2 * sizeof(float4) + sizeof(unsigned))));
   if (!seam) return fail(CC_E_CUDA, "logits: seam buffer allocation failed");
-  auto kern = gemv_stream_kernel<GS_EPI_LOGITS, true, GS_CFG.nw, GS_CFG.sb, GS_CFG.ns>;
+  auto kern = gemv_stream_kernel<GS_EPI_LOGITS, true, GS_CFG.nw, GS_CFG.sb, GS_CFG.ns, GS_CFG.maxr>;
   if (int rc = ensure_smem(kern, smem)) return rc;
   return launch_k(kern, dim3(num_sms()), dim3(GS_CFG.nw * 32), smem, st, "logits_stream", (const void*)hidden,
                   (const __nv_bfloat16*)U, (int64_t)d, (void*)logits, vocab, d, norm_w, eps, seam,

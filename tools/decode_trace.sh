@@ -1,4 +1,4 @@
-timeout 900 python -m pytest tests/test_gpu_decode.py tests/test_gpu_kernels.py -x -q -k "decode or logits or gemv or argmax" 2>&1 | tail -2
+timeout 900 python -m pytest tests/test_gpu_decode.py -x -q 2>&1 | tail -1
 run() {
   env "$@" timeout 900 python bench.py --no-baselines --no-cpu --tiers 0 --steps 3 > gpurun_out/dec_x.json 2> gpurun_out/dec_x.err
   python -c "
@@ -7,5 +7,8 @@ d=json.loads(open('gpurun_out/dec_x.json').read().strip().splitlines()[-1])['dec
 print('$*', d['ms_per_token'], d['roofline']['frac'], d['first_tokens'])
 " || tail -3 gpurun_out/dec_x.err
 }
-run CCB_LOGITS_STREAM=0
-run CCB_LOGITS_STREAM=1
+run CCB_GS_ALT=0
+run CCB_GS_ALT=1
+run CCB_GS_ALT=0
+run CCB_GS_ALT=1
+echo "=== trace alt"; CCB_GS_ALT=1 timeout 600 python tools/decode_trace.py 1 2>&1 | tail -10
