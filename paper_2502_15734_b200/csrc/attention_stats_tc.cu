@@ -17,10 +17,14 @@
 // Hq.  No atomics: run-to-run bit-identical.  (One warpgroup for all tiles
 // measured latency-bound: the K8 pass cost 16% of a fresh 8B prefill.)
 #include <math.h>
+#include <stdlib.h>
+
+#include <type_traits>
 
 #include "attention.cuh"
 #include "common.cuh"
 #include "sm100.cuh"
+#include "f32x2.cuh"
 
 namespace ccb {
 
@@ -29,7 +33,7 @@ namespace {
 using namespace sm100;
 
 constexpr int ST_BN = 128;
-constexpr int ST_STAGES = 2;
+constexpr int ST_MAXSTAGES = 4;
 constexpr int ST_MAXSEG = 112;  // n_seg + 1 (diagonal) <= 112 (two warpgroups' accumulators in smem)
 
 __host__ __device__ constexpr uint32_t idesc_s(int M, int N) {
@@ -42,7 +46,7 @@ __device__ __forceinline__ float ex2f(float x) {
   return y;
 }
 
-template <int DH>
+template <int DH, int ST_STAGES>
 struct StSmem {
   static constexpr int Q_BYTES = 128 * DH * 2;
   static constexpr int K_BYTES = ST_BN * DH * 2;
@@ -54,14 +58,14 @@ struct StSmem {
   static size_t total(int stride) { return 1024 + ACC_OFF + (size_t)2 * 128 * stride * 4; }
 };
 
-template <int DH>
+template <int DH, int ST_STAGES, int PF>
 __global__ void __launch_bounds__(320, 1)
     attn_stats_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __nv_bfloat16* __restrict__ q,
                          const int32_t* __restrict__ rows, int n_rows, const int32_t* __restrict__ q_slot,
                          const uint8_t* __restrict__ key_pad, const float* __restrict__ lse,
                          const int32_t* __restrict__ seg_lo, const int32_t* __restrict__ seg_hi, int n_seg,
                          float* __restrict__ part, int n_keys, int Hq, int Hkv, int G, float scale_log2, int stride) {
-  using SM = StSmem<DH>;
+  using SM = StSmem<DH, ST_STAGES>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = base + SM::Q_OFF;
@@ -81,7 +85,9 @@ __global__ void __launch_bounds__(320, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = blockIdx.x;
   const int R = 128 / G;
-  const int r0 = blockIdx.y * R;  // first stats row of this CTA
+  // row blocks in reverse: with causal limits the last rows see the most key
+  // tiles, so the longest CTAs start first instead of forming the tail wave
+  const int r0 = (gridDim.y - 1 - blockIdx.y) * R;  // first stats row of this CTA
   const int W = n_seg + 1;
 
   if (threadIdx.x == 0) s_kmax = -1;
@@ -212,6 +218,39 @@ __global__ void __launch_bounds__(320, 1)
       tc_fence_before();
       mbar_arrive(&s_empty[b]);
       const int lim_rel = lim - j0;
+      // fast path: every key of the tile visible to this row and the tile
+      // inside one segment (the common case: segments are chunk spans) --
+      // packed f32x2 arithmetic, a quarter of the exponentials on the FMA
+      // pipe, summed straight into four packed accumulators
+      int one_seg = -1;
+      if (lim_rel >= ST_BN && (pw[0] | pw[1] | pw[2] | pw[3]) == 0)  // (the diagonal tile: general path)
+        for (int sg = 0; sg < n_seg; ++sg)
+          if (s_lo[sg] <= j0 && s_hi[sg] >= j0 + ST_BN) {
+            one_seg = sg;
+            break;
+          }
+      if (__all_sync(0xffffffffu, one_seg >= 0) && one_seg == __shfl_sync(0xffffffffu, one_seg, 0)) {
+        const uint64_t sc2 = f2_pack(scale_log2, scale_log2), nb2 = f2_pack(-base_l2, -base_l2);
+        uint64_t a2[4] = {0ull, 0ull, 0ull, 0ull};
+#pragma unroll
+        for (int c2 = 0; c2 < ST_BN / 2; ++c2) {
+          const uint64_t x2 = ffma2(f2_pack(p[2 * c2], p[2 * c2 + 1]), sc2, nb2);
+          uint64_t e2;
+          if ((c2 & 7) >= 8 - PF) {
+            e2 = ex2_poly2(x2);
+          } else {
+            float x0, x1;
+            f2_unpack(x2, x0, x1);
+            e2 = f2_pack(ex2f(x0), ex2f(x1));
+          }
+          a2[c2 & 3] = fadd2(a2[c2 & 3], e2);
+        }
+        const uint64_t t2 = fadd2(fadd2(a2[0], a2[1]), fadd2(a2[2], a2[3]));
+        float t0, t1;
+        f2_unpack(t2, t0, t1);
+        my[one_seg] += t0 + t1;
+        continue;
+      }
       // all probabilities first (independent -> full ILP); masked keys give 0
 #pragma unroll
       for (int c = 0; c < ST_BN; ++c) {
@@ -299,14 +338,31 @@ int launch(const void* q, const void* k, const int32_t* q_slot, const uint8_t* k
   float* part = (float*)stream_scratch(st, SCR_SEGMASS, sizeof(float) * (size_t)n_rows * Hkv * W);
   if (!part) return fail(CC_E_CUDA, "segment_mass_tc: scratch allocation failed");
   const int stride = W | 1;  // odd: the rows' accumulators fall in distinct banks
-  const size_t smem = StSmem<DH>::total(stride);
-  if (int rc = ensure_smem(attn_stats_tc_kernel<DH>, StSmem<DH>::total(ST_MAXSEG | 1))) return rc;
   dim3 grid(Hkv, (n_rows + R - 1) / R);
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)DH);
-  attn_stats_tc_kernel<DH><<<grid, 320, smem, st>>>(mk, (const __nv_bfloat16*)q, rows, n_rows, q_slot, key_pad, lse,
-                                                    seg_lo, seg_hi, n_seg, part, n_keys, Hq, Hkv, G, scale_log2,
-                                                    stride);
-  int rc = check_launch("segment_mass_tc");
+  static const int stages = [] {
+    const char* e = getenv("CCB_K8_STAGES");
+    return e ? atoi(e) : 4;
+  }();
+  static const int k8_pf = [] {  // exponential pairs (of 8) on the FMA pipe in the fast path
+    const char* e = getenv("CCB_K8_PF");
+    return e ? atoi(e) : 2;
+  }();
+  auto go = [&](auto tag) -> int {
+    constexpr int S = decltype(tag)::value;
+    const size_t smem = StSmem<DH, S>::total(stride);
+    auto kern = k8_pf == 0 ? attn_stats_tc_kernel<DH, S, 0>
+                : k8_pf == 3 ? attn_stats_tc_kernel<DH, S, 3>
+                : k8_pf == 4 ? attn_stats_tc_kernel<DH, S, 4> : attn_stats_tc_kernel<DH, S, 2>;
+    if (int rc = ensure_smem(kern, smem)) return rc;
+    kern<<<grid, 320, smem, st>>>(mk, (const __nv_bfloat16*)q, rows, n_rows, q_slot, key_pad,
+                                                          lse, seg_lo, seg_hi, n_seg, part, n_keys, Hq, Hkv, G,
+                                                          scale_log2, stride);
+    return check_launch("segment_mass_tc");
+  };
+  // a 4-deep K ring while the per-row segment accumulators leave room (<= ~60 segments)
+  const bool deep = stages != 2 && StSmem<DH, 4>::total(stride) <= 227 * 1024;
+  int rc = deep ? go(std::integral_constant<int, 4>{}) : go(std::integral_constant<int, 2>{});
   if (rc) return rc;
   const int64_t total = (int64_t)n_rows * W;
   seg_mass_fold_kernel<<<(int)((total + 255) / 256), 256, 0, st>>>(part, mass, n_rows, Hkv, W, Hq);
