@@ -248,6 +248,13 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src, uint64_t 
   asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src), "l"(pol)
                : "memory");
 }
+__device__ __forceinline__ float4 ld_f4_hint(const float4* p, uint64_t pol) {
+  float4 r;
+  asm volatile("ld.global.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+               : "l"(p), "l"(pol));
+  return r;
+}
 __device__ __forceinline__ void cp_async16_plain(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
@@ -326,34 +333,48 @@ __global__ void __maxnreg__(MAXR) gemv_stream_kernel(const void* __restrict__ A_
     }
     cp_async_commit();
   };
+  // RMSNorm weights are weights: loaded before the ring fills and before the
+  // wait (issued after the predecessor they would queue behind ~20 MB of
+  // streaming loads: measured 3.3-5.5 us for the prologue)
+  constexpr int TAILMAX = 256;  // words past one per thread, kept in shared memory (K / 4 <= threads + 256)
+  __shared__ float4 xt[NORM ? TAILMAX : 1], gt[NORM ? TAILMAX : 1];
+  float4 gr = make_float4(1.f, 1.f, 1.f, 1.f);
+  if constexpr (NORM) {
+    const float4* g4 = reinterpret_cast<const float4*>(norm_w);
+    if (norm_w != nullptr) {  // L2 evict-last: 32 KiB per layer that every CTA reads, kept across tokens
+      uint64_t keep;
+      asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(keep));
+      if ((int)threadIdx.x < K / 4) gr = ld_f4_hint(g4 + threadIdx.x, keep);
+      for (int j = threadIdx.x + blockDim.x; j < K / 4 && j - (int)blockDim.x < TAILMAX; j += blockDim.x)
+        gt[j - blockDim.x] = ld_f4_hint(g4 + j, keep);
+    } else {
+      for (int j = threadIdx.x; j < TAILMAX; j += blockDim.x) gt[j] = make_float4(1.f, 1.f, 1.f, 1.f);
+    }
+  }
 #pragma unroll
-  for (int st = 0; st < GS_STAGES; ++st) issue(st);
+  for (int st = 0; st < GS_STAGES; ++st) issue(st);  // the ring fills before the wait
   pdl_trigger();
   pdl_wait();  // the activation row comes from the predecessor
   const unsigned long long t1 = gtime();
+  unsigned long long c_x = 0, c_r = 0;
   if constexpr (NORM) {  // weighted RMSNorm of the f32 residual row (same expression as gemv_kernel)
     const float4* x4 = reinterpret_cast<const float4*>(A_);
-    float ss = 0.f;
-    constexpr int NR = 1;  // residual words held in registers (K <= 4 * blockDim; the rest re-read)
-    float4 xr[NR], gr[NR];
-#pragma unroll
-    for (int j = 0; j < NR; ++j) {  // residual + norm weights in one round trip
-      const int i = threadIdx.x + j * blockDim.x;
-      xr[j] = i < K / 4 ? x4[i] : make_float4(0.f, 0.f, 0.f, 0.f);
-      gr[j] = (i < K / 4 && norm_w != nullptr) ? reinterpret_cast<const float4*>(norm_w)[i]
-                                               : make_float4(1.f, 1.f, 1.f, 1.f);
-    }
-#pragma unroll
-    for (int j = 0; j < NR; ++j)
-      ss = fmaf(xr[j].x, xr[j].x, fmaf(xr[j].y, xr[j].y, fmaf(xr[j].z, xr[j].z, fmaf(xr[j].w, xr[j].w, ss))));
-    for (int i = threadIdx.x + NR * blockDim.x; i < K / 4; i += blockDim.x) {
+    const float4* g4 = reinterpret_cast<const float4*>(norm_w);
+    // one round trip (L2: the predecessor just wrote the row)
+    const int i0 = threadIdx.x;
+    const float4 xr = i0 < K / 4 ? x4[i0] : make_float4(0.f, 0.f, 0.f, 0.f);
+    float ss = fmaf(xr.x, xr.x, fmaf(xr.y, xr.y, fmaf(xr.z, xr.z, fmaf(xr.w, xr.w, 0.f))));
+    for (int i = i0 + blockDim.x; i < K / 4; i += blockDim.x) {
       const float4 v = x4[i];
       ss = fmaf(v.x, v.x, fmaf(v.y, v.y, fmaf(v.z, v.z, fmaf(v.w, v.w, ss))));
+      if (i - (int)blockDim.x < TAILMAX) xt[i - blockDim.x] = v;
     }
+    if (g_dtrace && threadIdx.x == 0 && ss != 12345.f) c_x = gtime();  // (timeline: the row has landed)
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
     if (lane == 0) red[warp] = ss;
     __syncthreads();
+    if (g_dtrace && threadIdx.x == 0) c_r = gtime();
     float tot = 0.f;
 #pragma unroll
     for (int w = 0; w < GS_WARPS; ++w) tot += red[w];
@@ -369,18 +390,18 @@ __global__ void __maxnreg__(MAXR) gemv_stream_kernel(const void* __restrict__ A_
       *reinterpret_cast<uint2*>(xs + 4 * i) =
           make_uint2(*reinterpret_cast<uint32_t*>(&a), *reinterpret_cast<uint32_t*>(&b));
     };
-#pragma unroll
-    for (int j = 0; j < NR; ++j) {
-      const int i = threadIdx.x + j * blockDim.x;
-      if (i < K / 4) put(i, xr[j], gr[j]);
+    if (i0 < K / 4) put(i0, xr, gr);
+    for (int i = i0 + blockDim.x; i < K / 4; i += blockDim.x) {
+      const int t = i - blockDim.x;  // (own words: no barrier needed)
+      if (t < TAILMAX) put(i, xt[t], gt[t]);
+      else put(i, x4[i], norm_w != nullptr ? g4[i] : make_float4(1.f, 1.f, 1.f, 1.f));
     }
-    for (int i = threadIdx.x + NR * blockDim.x; i < K / 4; i += blockDim.x)
-      put(i, x4[i], norm_w != nullptr ? reinterpret_cast<const float4*>(norm_w)[i] : make_float4(1.f, 1.f, 1.f, 1.f));
   } else {
     const uint4* a8 = reinterpret_cast<const uint4*>(A_);
     for (int i = threadIdx.x; i < K / 8; i += blockDim.x) reinterpret_cast<uint4*>(xs)[i] = a8[i];
   }
   __syncthreads();
+  const unsigned long long c1 = g_dtrace ? gtime() : 0;
   float ag = 0.f, au = 0.f;
   float c_pre = 0.f;  // residual: the row's old value, loaded when its first piece starts
   for (int st = 0; st < n_st; ++st) {
@@ -443,7 +464,7 @@ __global__ void __maxnreg__(MAXR) gemv_stream_kernel(const void* __restrict__ A_
     }
   }
   cp_async_wait<0>();
-  dtrace(1, t0, t1);
+  dtrace(1, t0, t1, c1, g_dtrace ? gtime() : 0, c_x, c_r);
 }
 
 // ---- split-KV decode attention ------------------------------------------------
@@ -872,7 +893,7 @@ __global__ void __launch_bounds__(DT_WARPS * 32, 3) decode_attn_tc(
     const float2* __restrict__ table, __nv_bfloat16* kv_k, __nv_bfloat16* kv_v, __nv_bfloat16* k_rot,
     const uint8_t* __restrict__ key_pad, float* part_o, float2* part_ml, unsigned* tickets,
     __nv_bfloat16* __restrict__ ctx, float* __restrict__ lse, int n_keys, const int32_t* __restrict__ n_keys_dev,
-    int max_keys, int Hq, int Hkv, float scale_log2) {
+    int max_keys, int Hq, int Hkv, float scale_log2, int stage_pre) {
   static_assert(G <= 8, "one n-tile of query heads");
   extern __shared__ __align__(16) uint4 stg[];  // [warp][staged step][word][lane]
   const unsigned long long t0 = gtime();
@@ -895,21 +916,29 @@ __global__ void __launch_bounds__(DT_WARPS * 32, 3) decode_attn_tc(
   uint4 kf[2][2][4];  // register buffers of two steps
   uint4 vf[2][4][2];
   // ---- pre-wait: steps 0-1 into registers, steps 2-3 into shared memory ----
+  auto preload = [&]() {
 #pragma unroll
-  for (int s = 0; s < 2; ++s)
+    for (int s = 0; s < 2; ++s)
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      const uint4 w = ld_stream16(word_src(s, i));
-      if (i < 8) kf[s][i >> 2][i & 3] = w;
-      else vf[s][(i - 8) >> 1][(i - 8) & 1] = w;
-    }
+      for (int i = 0; i < 16; ++i) {
+        const uint4 w = ld_stream16(word_src(s, i));
+        if (i < 8) kf[s][i >> 2][i & 3] = w;
+        else vf[s][(i - 8) >> 1][(i - 8) & 1] = w;
+      }
+  };
+  if (stage_pre & 2) preload();
+  auto stage = [&]() {
 #pragma unroll
-  for (int s = 2; s < DT_STEPS; ++s)
+    for (int s = 2; s < DT_STEPS; ++s)
 #pragma unroll
-    for (int i = 0; i < 16; ++i) cp_async16_plain(&stg[((warp * 2 + (s - 2)) * 16 + i) * 32 + lane], word_src(s, i));
-  cp_async_commit();
+      for (int i = 0; i < 16; ++i) cp_async16_plain(&stg[((warp * 2 + (s - 2)) * 16 + i) * 32 + lane], word_src(s, i));
+    cp_async_commit();
+  };
+  if (stage_pre & 1) stage();
   pdl_trigger();
   pdl_wait();
+  if (!(stage_pre & 2)) preload();
+  if (!(stage_pre & 1)) stage();
   const unsigned long long t1 = gtime();
   // one round trip: key count, slot, position and the raw q / k / v words of
   // this group (their addresses do not depend on the position)
@@ -1319,6 +1348,12 @@ void* zeroed_scratch(cudaStream_t st, int tag, size_t bytes) {
   return b.first;
 }
 constexpr int GS_MAX_SEAMS = 8192;
+// attention: which K/V words load before the wait -- bit 0 the shared-memory
+// staged steps, bit 1 the register steps (3 measured best: 3.20 vs 3.28 / 3.31 / 3.33)
+const int g_dt_stage_pre = [] {
+  const char* e = getenv("CCB_DT_STAGE_PRE");
+  return e ? atoi(e) : 3;
+}();
 const int g_carveout = [] {
   const char* e = getenv("CCB_DECODE_CARVEOUT");
   return e ? atoi(e) : 1;
@@ -1505,7 +1540,8 @@ int decode_attention_qkv_impl(const void* qkv, const int32_t* slot, const int32_
       return launch_k(kern, dim3(n_kv_heads, n_chunks), dim3(DT_WARPS * 32), DT_SMEM, st, "decode_attention_qkv",
                       (const __nv_bfloat16*)qkv, slot, pos, (const float2*)rope_table, (__nv_bfloat16*)kv_k,
                       (__nv_bfloat16*)kv_v, (__nv_bfloat16*)k_rot, key_pad, part_o, part_ml, tickets,
-                      (__nv_bfloat16*)ctx, lse, n_keys, n_keys_dev, max_keys, n_heads, n_kv_heads, scale_log2);
+                      (__nv_bfloat16*)ctx, lse, n_keys, n_keys_dev, max_keys, n_heads, n_kv_heads, scale_log2,
+                      g_dt_stage_pre);
     };
     switch (n_heads / n_kv_heads) {
       case 1: return go_tc(decode_attn_tc<1>);

@@ -87,6 +87,17 @@ for i in range(n // 3, 2 * n // 3):
     tot[nm] += (e - w0) / 1e3
     cnt[nm] += 1
 print("mean wait-released -> end (us):", {k: round(tot[k] / cnt[k], 2) for k in tot})
+# streaming GEMV checkpoints per launch in the middle third: prologue (x staged), loop end (before the CTA barrier)
+gl = [L for L in launches if L["tag"] == 1]
+if gl:
+    k = len(gl) // 2
+    for L in gl[k:k + 4]:
+        ix = np.array(L["idx"])
+        c = cps[ix] / 1e3
+        print("gemv_stream launch: row landed %.2f, reduced %.2f, x staged %.2f, loop done %.2f (median), %.2f (max), "
+              "CTA end %.2f (median) us after release"
+              % (np.median(c[:, 2]), np.median(c[:, 3]), np.median(c[:, 0]), np.median(c[:, 1]), c[:, 1].max(),
+                 np.median((t2 - t1)[ix]) / 1e3))
 att = (tag == 3) & (cps[:, 0] > 0)
 if att.any():
     c = cps[att] / 1e3

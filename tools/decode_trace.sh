@@ -1,4 +1,3 @@
-timeout 900 python -m pytest tests/test_gpu_decode.py -x -q 2>&1 | tail -1
 run() {
   env "$@" timeout 900 python bench.py --no-baselines --no-cpu --tiers 0 --steps 3 > gpurun_out/dec_x.json 2> gpurun_out/dec_x.err
   python -c "
@@ -7,8 +6,5 @@ d=json.loads(open('gpurun_out/dec_x.json').read().strip().splitlines()[-1])['dec
 print('$*', d['ms_per_token'], d['roofline']['frac'], d['first_tokens'])
 " || tail -3 gpurun_out/dec_x.err
 }
-run CCB_GS_ALT=0
-run CCB_GS_ALT=1
-run CCB_GS_ALT=0
-run CCB_GS_ALT=1
-echo "=== trace alt"; CCB_GS_ALT=1 timeout 600 python tools/decode_trace.py 1 2>&1 | tail -10
+for sp in 3 2 3 2; do run CCB_DT_STAGE_PRE=$sp; done
+echo "=== trace"; CCB_DT_STAGE_PRE=2 timeout 600 python tools/decode_trace.py 1 2>&1 | tail -7
