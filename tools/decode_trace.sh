@@ -6,5 +6,5 @@ d=json.loads(open('gpurun_out/dec_x.json').read().strip().splitlines()[-1])['dec
 print('$*', d['ms_per_token'], d['roofline']['frac'], d['first_tokens'])
 " || tail -3 gpurun_out/dec_x.err
 }
-for sp in 3 2 3 2; do run CCB_DT_STAGE_PRE=$sp; done
-echo "=== trace"; CCB_DT_STAGE_PRE=2 timeout 600 python tools/decode_trace.py 1 2>&1 | tail -7
+for t in 0 1 0 1; do run CCB_GS_TRIGGER=$t; done
+echo "=== trace late"; timeout 600 python tools/decode_trace.py 1 2>&1 | tail -13
