@@ -57,6 +57,7 @@ __device__ unsigned g_dtrace_n = 0;
 // streaming GEMV: griddepcontrol.launch_dependents after the activation
 // prologue (1, default) or right after the ring fills (0); CCB_GS_TRIGGER
 __device__ int g_trigger_late = 1;
+
 __device__ __forceinline__ unsigned long long gtime() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -1380,11 +1381,11 @@ bool gemv_stream_ok(int M, int K, int epi) {
 void set_trigger_mode() {
   static std::once_flag once;
   std::call_once(once, [] {
-    const char* e = getenv("CCB_GS_TRIGGER");
-    if (e) {
+    if (const char* e = getenv("CCB_GS_TRIGGER")) {
       int v = atoi(e);
       cudaMemcpyToSymbol(g_trigger_late, &v, sizeof(v));
     }
+
   });
 }
 
