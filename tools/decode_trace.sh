@@ -6,5 +6,4 @@ d=json.loads(open('gpurun_out/dec_x.json').read().strip().splitlines()[-1])['dec
 print('$*', d['ms_per_token'], d['roofline']['frac'], d['first_tokens'])
 " || tail -3 gpurun_out/dec_x.err
 }
-for t in 0 8 0 8; do run CCB_GS_L2SHORT=$t; done
-echo "=== trace"; timeout 600 python tools/decode_trace.py 1 2>&1 | tail -7
+for t in 0 1 0 1 0 1; do run CCB_DECODE_CARVEOUT=$t; done
