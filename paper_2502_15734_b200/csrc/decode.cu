@@ -235,7 +235,7 @@ __global__ void __launch_bounds__(GV_WARPS * 32) gemv_kernel(const void* __restr
 // stages x {1..6} stages at config 2: 3.30 ms/token vs 3.38 for 24 x 2 x 2 KiB,
 // 3.42-3.56 with 4 stages, 4.1-4.2 with 1 KiB stages or 8 warps).
 struct GsCfg { int nw, sb, ns, min_smem, maxr; };
-constexpr GsCfg GS_CFG = {28, 2048, 2, 116 * 1024, 48};
+constexpr GsCfg GS_CFG = {28, 2048, 2, 116 * 1024, 80};
 // (Measured and dropped: alternating footprints -- the NORM projections at
 // 24 warps / 104 KiB, the others at 22 warps / >= 116 KiB, <= 40 registers --
 // so each projection's CTAs land next to the previous one's and stream while
@@ -283,10 +283,10 @@ __device__ __forceinline__ float dot8f(const uint4& w, const float4& x0, const f
   return s;
 }
 
-// <= 48 registers: a 896-thread CTA then leaves room in the register file for
-// one CTA of the fused attention step (168 x 128) -- without it the NORM
-// variants took 58-72 and the attention grid could not land until the QKV
-// projection drained.
+// Register cap per configuration (MAXR): 80 (48 kept a 896-thread CTA small
+// enough for an attention CTA to land next to the QKV projection, which only
+// pays with the maximum shared-memory carveout -- measured: 48 / 64 / 80 / 128
+// registers 3.23 / 3.11 / 3.10 / 3.10 ms per token with the driver's carveout).
 template <int EPI, bool NORM, int GS_WARPS, int GS_STAGE, int GS_STAGES, int MAXR>
 __global__ void __maxnreg__(MAXR) gemv_stream_kernel(const void* __restrict__ A_,
                                                                     const __nv_bfloat16* __restrict__ W, int64_t ldw,

@@ -6,4 +6,9 @@ d=json.loads(open('gpurun_out/dec_x.json').read().strip().splitlines()[-1])['dec
 print('$*', d['ms_per_token'], d['roofline']['frac'], d['first_tokens'])
 " || tail -3 gpurun_out/dec_x.err
 }
-for t in 0 1 0 1 0 1; do run CCB_DECODE_CARVEOUT=$t; done
+cp paper_2502_15734_b200/_lib/libcc_b200.so /tmp/lib_base.so
+for i in 1 2; do
+  cp /tmp/lib_base.so paper_2502_15734_b200/_lib/libcc_b200.so; run CFG=28x2048x2
+  for c in 2820483 3220482 2420483 2020484; do cp tools/lib_c$c.so paper_2502_15734_b200/_lib/libcc_b200.so; run CFG=$c; done
+done
+cp /tmp/lib_base.so paper_2502_15734_b200/_lib/libcc_b200.so
