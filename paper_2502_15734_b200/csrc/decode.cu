@@ -896,7 +896,7 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
 __device__ __forceinline__ uint32_t u4w(const uint4& v, int i) { return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w; }
 
 template <int G>
-__global__ void __launch_bounds__(DT_WARPS * 32, 3) decode_attn_tc(
+__global__ void __launch_bounds__(DT_WARPS * 32, 2) decode_attn_tc(
     const __nv_bfloat16* __restrict__ qkv, const int32_t* __restrict__ slot_p, const int32_t* __restrict__ pos_p,
     const float2* __restrict__ table, __nv_bfloat16* kv_k, __nv_bfloat16* kv_v, __nv_bfloat16* k_rot,
     const uint8_t* __restrict__ key_pad, float* part_o, float2* part_ml, unsigned* tickets,

@@ -8,7 +8,7 @@ print('$*', d['ms_per_token'], d['roofline']['frac'], d['first_tokens'])
 }
 cp paper_2502_15734_b200/_lib/libcc_b200.so /tmp/lib_base.so
 for i in 1 2; do
-  cp /tmp/lib_base.so paper_2502_15734_b200/_lib/libcc_b200.so; run CFG=28x2048x2
-  for c in 2820483 3220482 2420483 2020484; do cp tools/lib_c$c.so paper_2502_15734_b200/_lib/libcc_b200.so; run CFG=$c; done
+  cp /tmp/lib_base.so paper_2502_15734_b200/_lib/libcc_b200.so; run ATTN_LB=3; run ATTN_LB=3 CCB_DT_STAGE_PRE=2; run ATTN_LB=3 CCB_DT_STAGE_PRE=0
+  cp tools/lib_a2.so paper_2502_15734_b200/_lib/libcc_b200.so; run ATTN_LB=2
 done
 cp /tmp/lib_base.so paper_2502_15734_b200/_lib/libcc_b200.so
