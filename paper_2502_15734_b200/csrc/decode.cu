@@ -1163,8 +1163,7 @@ __global__ void __launch_bounds__(DT_WARPS * 32, 2) decode_attn_tc(
     dtrace(3, t0, t1, c1, c2, c3);
     return;
   }
-  if (tid == 0) tickets[g] = 0u;
-  __threadfence();
+  if (tid == 0) tickets[g] = 0u;  // (thread 0's acquire + the barrier order the loads below)
   float* wsm = &wo[0][0][0] + warp * DF_MAXC;  // chunk weights of this warp's head (wo is free now)
   constexpr int DF_BATCH = 24;  // chunk rows whose loads go out together with the (max, sum) loads
   for (int h = warp; h < G; h += DT_WARPS) {
