@@ -1,6 +1,7 @@
 // Error plumbing and device queries of the C ABI (include/cachecraft_b200.h).
 #include <algorithm>
 #include <atomic>
+#include <map>
 #include <mutex>
 #include <set>
 #include <string>
@@ -62,15 +63,17 @@ void* stream_scratch(cudaStream_t st, int tag, size_t bytes) {
 
 int set_smem_attr(const void* fn, int bytes) {
   static std::mutex mu;
-  static std::set<std::tuple<int, const void*, int>> done;
+  // the attribute is an upper bound: only ever raised, so a kernel launched
+  // with several shared-memory sizes keeps the largest one requested
+  static std::map<std::pair<int, const void*>, int> done;
   int dev = 0;
   cudaGetDevice(&dev);
   std::lock_guard<std::mutex> g(mu);
-  auto key = std::make_tuple(dev, fn, bytes);
-  if (done.count(key)) return 0;
+  int& cur = done[std::make_pair(dev, fn)];
+  if (bytes <= cur) return 0;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   if (e != cudaSuccess) return fail(CC_E_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
-  done.insert(key);
+  cur = bytes;
   return 0;
 }
 

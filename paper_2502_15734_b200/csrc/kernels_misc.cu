@@ -11,10 +11,12 @@
 #include <math.h>
 
 #include <algorithm>
+#include <atomic>
 #include <type_traits>
 
 #include "common.cuh"
 #include "gemm.cuh"
+#include "sm100.cuh"
 
 namespace ccb {
 
@@ -147,6 +149,138 @@ __global__ void __launch_bounds__(256) gather_rope_kernel(
     VT x = *reinterpret_cast<const VT*>(srcV + (int64_t)r * kvw + c * V);
     *reinterpret_cast<VT*>(kv_v + lofs + (int64_t)slot * kvw + c * V) = x;
   }
+}
+
+// ---------------------------------------------------------------------------
+// K1, TMA-staged (the default): one CTA per (gather item, column chunk,
+// layer), three per SM.  Warp 0 stages the block's live K and V rows into
+// shared memory with bulk copies (cp.async.bulk completing on one mbarrier)
+// and sends them straight back out to kv_k / kv_v with bulk stores; a run of
+// consecutive live rows is one contiguous segment on both sides when the
+// chunk spans the full row (the block's rows land on consecutive request
+// slots), so a fully live 16-row block is 2 loads + 2 stores -- the TMA unit
+// costs ~50 ns per bulk operation whatever its size, per-row copies would be
+// operation-bound.  While the copies are in flight every thread fetches the
+// (cos, sin) coefficients of its rotation units; then the CTA rotates K out
+// of shared memory into k_rot with 16-byte stores.  Rows recomputed at the
+// layer (active_until[slot] > l) are neither loaded nor stored.  Same
+// arithmetic as gather_rope_kernel (bit-identical output).
+// ---------------------------------------------------------------------------
+template <typename T, int V>
+__global__ void __launch_bounds__(256, 3) gather_rope_bulk_kernel(
+    const T* __restrict__ pool, int64_t pool_layer_stride, int64_t pool_block_stride,
+    const cc_gather_item* __restrict__ items, int l0, const int32_t* __restrict__ slot_pos,
+    const int32_t* __restrict__ active_until, const typename CS<T>::type* __restrict__ table,
+    T* __restrict__ kv_k, T* __restrict__ kv_v, T* __restrict__ k_rot, int64_t req_layer_stride,
+    int kvw, int dh, int cols, int stg) {
+  using namespace sm100;
+  using A = typename Acc<T>::type;
+  using VT = Vec<T, V>;
+  using C2 = typename CS<T>::type;
+  constexpr int UPT = 4;  // rotation units per thread per round (coefficients held in registers)
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  T* sK = reinterpret_cast<T*>(smem_raw);
+  T* sV = sK + 16 * cols;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sV + 16 * cols);
+  __shared__ uint32_t s_mask;
+  pdl_trigger();
+  pdl_wait();
+  const int nchunk = kvw / cols;
+  const cc_gather_item it = items[blockIdx.x / nchunk];
+  const int c0 = (blockIdx.x % nchunk) * cols;
+  const int l = l0 + blockIdx.y;
+  const int tid = threadIdx.x;
+  const uint32_t row_bytes = (uint32_t)cols * sizeof(T);
+  const int64_t lofs = (int64_t)l * req_layer_stride;
+  int len = 0;  // warp 0: the run of live rows starting at row tid
+  if (tid < 32) {
+    const bool live = tid < it.n_rows && active_until[it.dst_slot + tid] <= l;
+    const uint32_t m = __ballot_sync(0xffffffffu, live);
+    if (live) len = cols < kvw ? 1 : (tid > 0 && ((m >> (tid - 1)) & 1u)) ? 0 : __ffs(~(m >> tid)) - 1;
+    if (tid == 0) {
+      s_mask = m;
+      mbar_init(bar, 1);
+      fence_proxy_async_smem();  // the init is visible to the async proxy
+      if (m) mbar_expect_tx(bar, 2u * __popc(m) * row_bytes);
+    }
+    __syncwarp();
+    if (len) {
+      const T* src = pool + (int64_t)l * pool_layer_stride + (int64_t)it.src_block * pool_block_stride +
+                     (int64_t)tid * kvw + c0;
+      bulk_load_1d(sK + tid * cols, src, len * row_bytes, bar);
+      bulk_load_1d(sV + tid * cols, src + 16 * (int64_t)kvw, len * row_bytes, bar);
+    }
+  }
+  __syncthreads();
+  const uint32_t m = s_mask;
+  if (!m) return;
+  const int half = dh / 2, hv = half / V, nh = cols / dh;
+  const int units = 16 * nh * hv;
+  // the staged rows have landed: K and V leave for kv_k / kv_v
+  auto stage_out = [&]() {
+    mbar_wait(bar, 0);
+    if (stg) {  // (experiment) position-free K and V written by the threads
+      const int vpr = cols / V;
+      for (int w = tid; w < 16 * vpr; w += 256) {
+        const int r = w / vpr, c = w % vpr;
+        if (!((m >> r) & 1u)) continue;
+        const int64_t doff = lofs + (int64_t)(it.dst_slot + r) * kvw + c0 + c * V;
+        *reinterpret_cast<VT*>(kv_k + doff) = *reinterpret_cast<const VT*>(sK + r * cols + c * V);
+        *reinterpret_cast<VT*>(kv_v + doff) = *reinterpret_cast<const VT*>(sV + r * cols + c * V);
+      }
+    } else if (len) {  // position-free K and V leave as loaded
+      const int64_t doff = lofs + (int64_t)(it.dst_slot + tid) * kvw + c0;
+      bulk_store_1d(kv_k + doff, sK + tid * cols, len * row_bytes);
+      bulk_store_1d(kv_v + doff, sV + tid * cols, len * row_bytes);
+      bulk_commit();
+    }
+  };
+  bool staged = false;
+  for (int base = tid; base < units; base += UPT * 256) {
+    C2 cs[UPT][V];
+#pragma unroll
+    for (int k = 0; k < UPT; ++k) {
+      const int w = base + k * 256;
+      const int r = w / (nh * hv), jv = (w % (nh * hv)) % hv;
+      if (w < units && ((m >> r) & 1u)) {
+        const C2* t = table + (int64_t)slot_pos[it.dst_slot + r] * half + jv * V;
+#pragma unroll
+        for (int e = 0; e < V; ++e) cs[k][e] = t[e];
+      }
+    }
+    if (!staged) {
+      stage_out();
+      staged = true;
+    }
+#pragma unroll
+    for (int k = 0; k < UPT; ++k) {
+      const int w = base + k * 256;
+      const int r = w / (nh * hv), rem = w % (nh * hv);
+      if (w >= units || !((m >> r) & 1u)) continue;
+      const int h = rem / hv, jv = rem % hv;
+      const int off = r * cols + h * dh + jv * V;
+      const VT x = *reinterpret_cast<const VT*>(sK + off);
+      const VT y = *reinterpret_cast<const VT*>(sK + off + half);
+      VT xr, yr;
+#pragma unroll
+      for (int e = 0; e < V; ++e) {
+        A c = (A)cs[k][e].x, s = (A)cs[k][e].y;
+        A a = (A)to_f(x.v[e]), b = (A)to_f(y.v[e]);
+        if constexpr (sizeof(A) == 8) {
+          xr.v[e] = from_d<T>(a * c - b * s);
+          yr.v[e] = from_d<T>(a * s + b * c);
+        } else {
+          xr.v[e] = from_f<T>(a * c - b * s);
+          yr.v[e] = from_f<T>(a * s + b * c);
+        }
+      }
+      const int64_t doff = lofs + (int64_t)(it.dst_slot + r) * kvw + c0 + h * dh + jv * V;
+      *reinterpret_cast<VT*>(k_rot + doff) = xr;
+      *reinterpret_cast<VT*>(k_rot + doff + half) = yr;
+    }
+  }
+  if (!staged) stage_out();  // (threads without rotation units)
+  if (len && !stg) bulk_wait_read<0>();  // shared memory stays valid until the stores have read it
 }
 
 // ---------------------------------------------------------------------------
@@ -719,6 +853,13 @@ int cc_rope_apply_f64(const double* x, double* y, const int64_t* positions, int 
   return check_launch("rope_apply_f64");
 }
 
+// K1 kernel choice for experiments and tests (< 0: the environment's)
+static std::atomic<int> g_k1_ldg{-1}, g_k1_cols{-1};
+extern "C" __attribute__((visibility("default"))) void cc_debug_k1(int ldg, int cols) {
+  g_k1_ldg = ldg;
+  g_k1_cols = cols;
+}
+
 int cc_gather_rope_kv(const void* pool, int64_t pool_layer_stride, int64_t pool_block_stride,
                       const cc_gather_item* items, int n_items, int l0, int l1, const int32_t* slot_pos,
                       const int32_t* active_until, const void* rope_table, void* kv_k, void* kv_v, void* k_rot,
@@ -727,9 +868,39 @@ int cc_gather_rope_kv(const void* pool, int64_t pool_layer_stride, int64_t pool_
   CCB_REQUIRE(l1 >= l0 && l0 >= 0, "gather_rope_kv: bad layer range");
   if (n_items == 0 || l1 == l0) return 0;
   CCB_REQUIRE(n_items <= 0x7fffffff && (l1 - l0) <= 65535, "gather_rope_kv: grid too large");
+  // CCB_K1_LDG=1: the register-path kernel (A/B experiments); CCB_K1_COLS:
+  // column chunk of the TMA-staged kernel (default: the widest multiple of
+  // d_head dividing kv_width with 16 rows x cols <= 32 KiB)
+  // (cc_debug_k1 overrides both at run time)
+  static const int env_ldg = getenv("CCB_K1_LDG") ? atoi(getenv("CCB_K1_LDG")) : 0;
+  static const int env_cols = getenv("CCB_K1_COLS") ? atoi(getenv("CCB_K1_COLS")) : 0;
+  const int gl = g_k1_ldg.load(), gc = g_k1_cols.load();
+  const int k1_ldg = gl >= 0 ? gl : env_ldg, k1_cols = gc >= 0 ? gc : env_cols;
   return CCB_DISPATCH_DTYPE(dtype, T, [&] {
     int vec = std::min(pick_vec<T>(d_head / 2), pick_vec<T>(kv_width));
     return CCB_DISPATCH_VEC(vec, V, [&] {
+      if (k1_ldg != 1) {
+        int cols = d_head;
+        for (int c = kv_width; c >= d_head; c -= d_head)
+          if (kv_width % c == 0 && (k1_cols > 0 ? c <= k1_cols : 16 * c * (int)sizeof(T) <= 32768)) {
+            cols = c;
+            break;
+          }
+        const auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+        CCB_REQUIRE((cols * sizeof(T)) % 16 == 0 && (kv_width * sizeof(T)) % 16 == 0 &&
+                        (pool_layer_stride * sizeof(T)) % 16 == 0 && (pool_block_stride * sizeof(T)) % 16 == 0 &&
+                        (req_layer_stride * sizeof(T)) % 16 == 0 && al(pool) && al(kv_k) && al(kv_v) && al(k_rot),
+                    "gather_rope_kv: rows and buffers must be 16-byte aligned");
+        const size_t smem = 2 * 16 * (size_t)cols * sizeof(T) + 16;
+        auto kern = gather_rope_bulk_kernel<T, V>;
+        if (int e = ensure_smem(kern, smem)) return e;
+        const int64_t nx = (int64_t)n_items * (kv_width / cols);
+        CCB_REQUIRE(nx <= 0x7fffffff, "gather_rope_kv: grid too large");
+        return launch_k(kern, dim3((unsigned)nx, l1 - l0), dim3(256), smem, as_stream(stream), "gather_rope_kv",
+                        (const T*)pool, pool_layer_stride, pool_block_stride, items, l0, slot_pos, active_until,
+                        (const typename CS<T>::type*)rope_table, (T*)kv_k, (T*)kv_v, (T*)k_rot, req_layer_stride,
+                        kv_width, d_head, cols, k1_ldg == 2 ? 1 : 0);
+      }
       dim3 grid(n_items, l1 - l0);
       return launch_k(gather_rope_kernel<T, V>, grid, dim3(256), 0, as_stream(stream), "gather_rope_kv",
                       (const T*)pool, pool_layer_stride, pool_block_stride, items, l0, slot_pos, active_until,

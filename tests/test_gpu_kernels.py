@@ -357,6 +357,41 @@ def test_gather_rope_matches_torch(N):
                 np.testing.assert_allclose(k_rot[l, s].double().numpy(force=True), want, atol=2e-2, rtol=1e-2)
 
 
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+def test_gather_rope_bulk_matches_register_path(N, dtype):
+    """The TMA-staged K1 (bulk copies through shared memory, column chunks)
+    writes exactly the bytes of the register-path kernel, including partial
+    blocks and slots skipped at some layers."""
+    L, kvw, dh = 4, 512, 128
+    tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    code = N.BF16 if dtype == "bf16" else N.F32
+    g = torch.Generator(device="cuda").manual_seed(5)
+    pool = torch.randn((L, 9, 2, 16, kvw), device="cuda", generator=g).to(tdt)
+    items = np.array([(3, 0, 16, 0), (7, 16, 16, 0), (1, 32, 10, 0), (5, 42, 1, 0), (0, 43, 16, 0)], dtype=np.int32)
+    n = 59
+    slot_pos = torch.randperm(200, device="cuda", generator=g)[:n].to(torch.int32)
+    active = torch.zeros(n, dtype=torch.int32, device="cuda")
+    active[[2, 17, 18, 42, 50]] = torch.tensor([1, 4, 2, 3, 1], dtype=torch.int32, device="cuda")
+    half = dh // 2
+    inv = torch.from_numpy(500000.0 ** (-2.0 * np.arange(half) / dh)).cuda()
+    tab = torch.empty((256, half, 2), dtype=torch.float32, device="cuda")
+    N.call("cc_rope_table", N.ptr(tab), N.ptr(inv), 256, half, code, N.stream_ptr())
+    it = torch.from_numpy(items.reshape(-1)).cuda()
+    outs = {}
+    for mode in ((1, 0), (0, 0), (0, 128), (0, 256), (2, 0), (2, 128)):
+        N.lib().cc_debug_k1(*mode)
+        bufs = [torch.full((L, n, kvw), 7.0, dtype=tdt, device="cuda") for _ in range(3)]
+        N.call("cc_gather_rope_kv", N.ptr(pool), pool.stride(0), pool.stride(1), N.ptr(it), len(items), 0, L,
+               N.ptr(slot_pos), N.ptr(active), N.ptr(tab), *(N.ptr(b) for b in bufs), n * kvw, kvw, dh,
+               code, N.stream_ptr())
+        torch.cuda.synchronize()
+        outs[mode] = bufs
+    N.lib().cc_debug_k1(-1, -1)
+    for mode, bufs in outs.items():
+        for a, b in zip(bufs, outs[(1, 0)]):
+            assert torch.equal(a, b), mode
+
+
 def test_logits_argmax_first_max_wins(N):
     d, vocab = 64, 1000
     U = torch.zeros((vocab, d), dtype=torch.float32, device="cuda")

@@ -11,7 +11,7 @@ import json
 import sys
 
 GROUPS = {"gemm": ("gemm_tc_kernel", "gemm_pair_kernel"), "attention": ("attn_tc_kernel", "attn_pp_kernel"),
-          "gather_rope": ("gather_rope_kernel",)}
+          "gather_rope": ("gather_rope_kernel", "gather_rope_bulk_kernel")}
 
 rows = list(csv.reader(open(sys.argv[1])))
 i = [k for k, r in enumerate(rows) if "Kernel Name" in r][0]
