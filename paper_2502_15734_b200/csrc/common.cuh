@@ -80,7 +80,10 @@ inline size_t dtype_size(int dtype) { return dtype == CC_F64 ? 8 : (dtype == CC_
 int num_sms();
 void note_simt(int dtype);  // counts bf16 SIMT launches (cc_bf16_simt_launches)
 // scratch tags: one per kernel family, so no two families share a buffer
-enum ScratchTag { SCR_LOGITS = 1, SCR_SEGMASS = 2, SCR_ATTN = 3, SCR_DECODE_ATTN = 4 };
+enum ScratchTag { SCR_LOGITS = 1, SCR_SEGMASS = 2, SCR_ATTN = 3, SCR_DECODE_ATTN = 4, SCR_PAIR_KSPLIT = 5 };
+// zero-initialised buffers (decode.cu): tickets the kernels reset themselves
+enum ZeroedTag { ZSCR_GEMV_SEAMS = 1, ZSCR_DECODE_TICKETS = 2, ZSCR_PAIR_TICKETS = 3 };
+void* zeroed_scratch(cudaStream_t st, int tag, size_t bytes);
 void* stream_scratch(cudaStream_t st, int tag, size_t bytes);
 
 // Dynamic shared-memory opt-in, once per (device, kernel): thread-safe, and

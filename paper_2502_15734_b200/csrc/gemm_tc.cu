@@ -508,6 +508,18 @@ constexpr int SW_MAXU = 4096;  // units per launch (the table rides in the kerne
 struct SwTab {
   uint16_t start[SW_MAXG + 1];  // CTA c runs units [start[c], start[c+1])
   uint32_t unit[SW_MAXU];       // feature tile | (row0 / 16) << 14 | (rows / 16 - 1) << 25
+  uint8_t ks[SW_MAXU];          // K split: slice s << 4 | (slices - 1); 0 = the whole K
+};
+// K-split units (small M: too few (tile, row chunk) units for the CTA pairs):
+// slice s of S covers k-blocks [s * nkb / S, (s + 1) * nkb / S).  Each CTA
+// parks its fp32 partial in ws[s][feature][row] (row stride Mpad), bumps the
+// (tile, chunk, CTA rank) ticket, and the CTA that draws the last ticket sums
+// the S partials in slice order (its own from TMEM) before the normal
+// epilogue -- deterministic whichever CTA finishes last.
+struct KSplit {
+  float* ws;         // [S_max][F][Mpad] fp32
+  unsigned* ticket;  // [F / 128][Mpad / 32], zero between launches
+  int Mpad, F;
 };
 __host__ __device__ constexpr uint32_t sw_pack(int ft, int r0, int n) {
   return (uint32_t)ft | ((uint32_t)(r0 >> 4) << 14) | ((uint32_t)((n >> 4) - 1) << 25);
@@ -558,7 +570,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
     gemm_pair_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX128,
                      const __grid_constant__ CUtensorMap tmX64, const __grid_constant__ CUtensorMap tmX32,
                      const __grid_constant__ CUtensorMap tmX16, const __grid_constant__ CUtensorMap tmC, int M,
-                     int K, int dbg, const __grid_constant__ SwTab tab, const RopeQkv rq) {
+                     int K, int dbg, const __grid_constant__ SwTab tab, const RopeQkv rq, const KSplit ksp) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = base;
@@ -569,6 +581,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   uint8_t* stg_base = sB + P2_STAGES * P2_B_BYTES + 256;
+  __shared__ bool ks_last_s;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();
@@ -606,11 +619,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
       if (u_begin < u_end && !(dbg & 2)) {
         const uint32_t e = tab.unit[u_begin];
         const int fp = e & 0x3fff, n = (((e >> 25) & 0xf) + 1) * 16;
-        pre = min(P2_STAGES, num_kb);
+        const int ks = tab.ks[u_begin], kb0 = (ks >> 4) * num_kb / ((ks & 15) + 1);
+        const int kb1 = ((ks >> 4) + 1) * num_kb / ((ks & 15) + 1);
+        pre = min(P2_STAGES, kb1 - kb0);
         for (int i = 0; i < pre; ++i) {
           const uint32_t fb = mapa_shared(smem_u32(&full[i]), 0);
           if (rank == 0) mbar_expect_tx(&full[i], 2 * (TC_A_BYTES + (n / 2) * TC_BK * 2));
-          tma_load_2d_pair(sA + i * TC_A_BYTES, &tmW, fb, i * TC_BK, fp * 2 * TC_BM + (int)rank * TC_BM);
+          tma_load_2d_pair(sA + i * TC_A_BYTES, &tmW, fb, (kb0 + i) * TC_BK, fp * 2 * TC_BM + (int)rank * TC_BM);
         }
       }
       pdl_wait();
@@ -619,10 +634,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
         const int fp = e & 0x3fff, r0 = ((e >> 14) & 0x7ff) * 16, n = (((e >> 25) & 0xf) + 1) * 16;
         const int h = n / 2;  // rows per CTA (multiple of 16)
         const int rows0 = r0 + (int)rank * h;
-        for (int kb = 0; kb < num_kb; ++kb) {
-          const bool prefetched = u == u_begin && kb < pre;
+        const int ks = tab.ks[u], kb0 = (ks >> 4) * num_kb / ((ks & 15) + 1);
+        const int kb1 = ((ks >> 4) + 1) * num_kb / ((ks & 15) + 1);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          const bool prefetched = u == u_begin && kb - kb0 < pre;
           if (!prefetched) mbar_wait(&empty[stage], phase ^ 1);
-          if ((dbg & 2) && (u > u_begin || kb >= P2_STAGES)) {  // debug: MMA on stale tiles (no feed)
+          if ((dbg & 2) && (u > u_begin || kb - kb0 >= P2_STAGES)) {  // debug: MMA on stale tiles (no feed)
             if (rank == 0) mbar_arrive(&full[stage]);
             if (++stage == P2_STAGES) { stage = 0; phase ^= 1; }
             continue;
@@ -654,14 +671,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * 256;
-        for (int kb = 0; kb < num_kb; ++kb) {
+        const int ks = tab.ks[u], kb0 = (ks >> 4) * num_kb / ((ks & 15) + 1);
+        const int kb1 = ((ks >> 4) + 1) * num_kb / ((ks & 15) + 1);
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint64_t ad = desc_sw128(sA + stage * TC_A_BYTES);
           const uint64_t bd = desc_sw128(sB + stage * P2_B_BYTES);
 #pragma unroll
           for (int k = 0; k < TC_BK / 16; ++k)
-            mma_bf16_pair(d_tmem, ad + 2 * k, bd + 2 * k, idesc, (kb > 0 || k > 0) ? 1u : 0u);
+            mma_bf16_pair(d_tmem, ad + 2 * k, bd + 2 * k, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
           mma_commit_pair(&empty[stage], 0x3);
           if (++stage == P2_STAGES) { stage = 0; phase ^= 1; }
         }
@@ -686,6 +705,65 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t t0 = tmem_base + acc * 256 + ((uint32_t)(q * 32) << 16);
+      const int ks = tab.ks[u], ns = (ks & 15) + 1, my_s = ks >> 4;
+      const int feat = ft * TC_BM + q * 32 + lane;  // this thread's feature (TMEM lane)
+      if (ns > 1) {
+        // park this slice's partial: ws[my_s][feat][r0 .. r0 + n), 32 rows per chunk
+        float* dst = ksp.ws + ((int64_t)my_s * ksp.F + feat) * ksp.Mpad + r0;
+#pragma unroll 1
+        for (int c = 0; c * 32 < n; ++c) {
+          uint32_t r[32];
+          tmem_ld32(t0 + c * 32, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 32; j += 4)
+            __stcg(reinterpret_cast<float4*>(dst + c * 32 + j),
+                   make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]), __uint_as_float(r[j + 2]),
+                               __uint_as_float(r[j + 3])));
+        }
+        __threadfence();
+        epi_bar();
+        unsigned* tk = ksp.ticket + (int64_t)ft * (ksp.Mpad / 32) + r0 / 32;
+        if (threadIdx.x == 64) {  // (first epilogue thread) release the partials, acquire the others'
+          unsigned prev;
+          asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(tk) : "memory");
+          ks_last_s = prev == (unsigned)(ns - 1);
+          if (ks_last_s) *tk = 0u;  // ready for the next launch on this stream
+        }
+        epi_bar();
+        if (!ks_last_s) {  // another slice's CTA finishes this unit
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), 0));
+          if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+          continue;
+        }
+      }
+      // r[j] (row r0 + 32 c + j of this thread's feature) = the slices summed in order
+      auto fold = [&](int c, uint32_t (&r)[32]) {
+        if (ns == 1) return;
+        float a[32];
+#pragma unroll 1
+        for (int s2 = 0; s2 < ns; ++s2) {
+          if (s2 == my_s) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) a[j] = s2 == 0 ? __uint_as_float(r[j]) : a[j] + __uint_as_float(r[j]);
+          } else {
+            const float* src = ksp.ws + ((int64_t)s2 * ksp.F + feat) * ksp.Mpad + r0 + c * 32;
+#pragma unroll
+            for (int j = 0; j < 32; j += 4) {
+              const float4 v = __ldcg(reinterpret_cast<const float4*>(src + j));
+              if (s2 == 0) {
+                a[j] = v.x; a[j + 1] = v.y; a[j + 2] = v.z; a[j + 3] = v.w;
+              } else {
+                a[j] += v.x; a[j + 1] += v.y; a[j + 2] += v.z; a[j + 3] += v.w;
+              }
+            }
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(a[j]);
+      };
       if constexpr (EPI == EPI_ROPE_QKV) {
         // warp slab (8 KiB): [0, 4K) this warp's fp32 chunk for the partner,
         // [4K, 6K) / [6K, 8K) bf16 [32 rows][32 features] output staging.
@@ -714,6 +792,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
           tmem_ld32(t0 + c * 32, r);
           meta(c, cs, slot_c);
           tmem_ld_wait();
+          fold(c, r);
           if (dbg & 1) continue;  // debug: no stores
           // q heads alternate the two staging slabs (a chunk's TMA store drains
           // while the next is written); k / v heads use both, read back here
@@ -799,6 +878,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
         uint32_t r[32];
         tmem_ld32(t0 + c * 32, r);
         tmem_ld_wait();
+        fold(c, r);
         if (dbg & 1) continue;  // debug: no stores
         uint8_t* slab = my_slab + (nst & 1) * 4096;
         // the TMA store that last read this slab (two stores ago) is done reading
@@ -1094,7 +1174,15 @@ struct TabPlan {
   SwTab tab;
   int grid = 0;     // CTAs (2 per unit list)
   double t = 1e30;  // modelled makespan, cycles
+  int slices = 1;   // K split (1: none)
 };
+// K-split cost per unit on top of its k-blocks: park the n x 128 fp32 partial,
+// the ticket round trip, and (amortised over the slices) the last CTA's reads
+// of the other slices' partials, in cycles per row
+constexpr double kSplitFixed = 2500.0, kSplitPerRow = 12.0;
+// K splits considered for short activation matrices only (few units per pair)
+constexpr int kSplitMaxM = 1024;
+constexpr int kSplitCand[5] = {1, 2, 3, 4, 6};
 
 inline double unit_cycles(int n, int nkb) {
   const double mma = 2.0 * n, feed = 256.0 + n;
@@ -1105,10 +1193,10 @@ inline double unit_cycles(int n, int nkb) {
 // rows, the rest split evenly, 32-row granules), k from ceil(M/256) to +3,
 // schedule the units onto the CTA pairs, keep the smallest makespan.  Cached
 // per shape (evicted plans are leaked, not freed: a caller may still hold one).
-const TabPlan* plan_units(int M, int F, int K) {
+const TabPlan* plan_units(int M, int F, int K, bool ksplit, int force_s = 0) {
   static std::mutex mu;
   static std::unordered_map<uint64_t, TabPlan*> cache;
-  const uint64_t key = ((uint64_t)M << 44) ^ ((uint64_t)F << 20) ^ (uint64_t)K;
+  const uint64_t key = ((uint64_t)M << 44) ^ ((uint64_t)F << 20) ^ (uint64_t)K ^ (ksplit ? 1ull << 63 : 0ull) ^ ((uint64_t)force_s << 58);
   std::lock_guard<std::mutex> g(mu);
   auto it = cache.find(key);
   if (it != cache.end()) return it->second;
@@ -1120,12 +1208,16 @@ const TabPlan* plan_units(int M, int F, int K) {
   TabPlan* best = new TabPlan();
   struct U {
     double cost;
-    int ft, r0, n;
+    int ft, r0, n, ks;
   };
   std::vector<U> units;
   std::vector<std::vector<int>> lists(G);
   std::vector<int> best_ch;
-  for (int k = kmin; k <= kmin + 3 && (long)ntile * k <= SW_MAXU; ++k) {
+  const int Mpad = nb * gran;
+  for (int S : kSplitCand)
+  for (int k = kmin; k <= kmin + 3 && (long)ntile * k * S <= SW_MAXU; ++k) {
+    if (force_s > 0 ? S != force_s : S > 1 && (!ksplit || M > kSplitMaxM)) break;
+    if (S > 1 && (nkb / S < 8 || (double)S * F * Mpad * 4.0 > 256.0 * (1 << 20))) break;
     for (int j = 0; j < k; ++j) {
       const int rem = nb - maxb * j, parts = k - j;
       if (rem < parts) break;
@@ -1135,7 +1227,11 @@ const TabPlan* plan_units(int M, int F, int K) {
       units.clear();
       for (int ft = 0; ft < ntile; ++ft)
         for (int ci = 0, r0 = 0; ci < (int)ch.size(); r0 += ch[ci] * gran, ++ci)
-          units.push_back({unit_cycles(ch[ci] * gran, nkb), ft, r0, ch[ci] * gran});
+          for (int sl = 0; sl < S; ++sl) {
+            const int n = ch[ci] * gran, kbs = (sl + 1) * nkb / S - sl * nkb / S;
+            const double c = unit_cycles(n, kbs) + (S > 1 ? kSplitFixed + kSplitPerRow * n : 0.0);
+            units.push_back({c, ft, r0, n, S > 1 ? (sl << 4) | (S - 1) : 0});
+          }
       // Units of one weight tile should run side by side (one HBM read of the
       // weights, the rest from L2): list-schedule them in (tile, chunk) order
       // onto the earliest-free CTA, except the last ~1.5 rounds of work, which
@@ -1160,12 +1256,16 @@ const TabPlan* plan_units(int M, int F, int K) {
       }
       if (makespan < best->t - 1e-9) {
         best->t = makespan;
+        best->slices = S;
         best_ch = ch;
         int nl = 0, pos = 0;
         for (int c = 0; c < G; ++c) {
           if (lists[c].empty()) continue;
           best->tab.start[nl++] = (uint16_t)pos;
-          for (int i : lists[c]) best->tab.unit[pos++] = sw_pack(units[i].ft, units[i].r0, units[i].n);
+          for (int i : lists[c]) {
+            best->tab.ks[pos] = (uint8_t)units[i].ks;
+            best->tab.unit[pos++] = sw_pack(units[i].ft, units[i].r0, units[i].n);
+          }
         }
         best->tab.start[nl] = (uint16_t)pos;
         best->grid = 2 * nl;
@@ -1173,8 +1273,8 @@ const TabPlan* plan_units(int M, int F, int K) {
     }
   }
   if (getenv("CCB_SW_DEBUG")) {
-    fprintf(stderr, "[gemm_pair] M=%d F=%d K=%d makespan=%.0f cyc (%.2f x 768-cycle tiles) grid=%d chunks(x%d):", M,
-            F, K, best->t, best->t / (kKbCycles * nkb), best->grid, gran);
+    fprintf(stderr, "[gemm_pair] M=%d F=%d K=%d makespan=%.0f cyc (%.2f x 768-cycle tiles) grid=%d slices=%d chunks(x%d):",
+            M, F, K, best->t, best->t / (kKbCycles * nkb), best->grid, best->slices, gran);
     for (int c : best_ch) fprintf(stderr, " %d", c);
     fprintf(stderr, "\n");
   }
@@ -1185,6 +1285,32 @@ const TabPlan* plan_units(int M, int F, int K) {
   if (cache.size() > 1024) cache.clear();  // (plans of evicted shapes leak: bounded, rare)
   cache.emplace(key, best);
   return best;
+}
+
+// CCB_PAIR_KSPLIT=1 lets the planner pick K-split unit plans.  Off by
+// default: measured slower than the unsplit plans at every shape tried
+// (tools/ksplit_check.sh, us, split vs unsplit: M = 290 o_proj 31.5 vs 21.0,
+// down 55.1 vs 58.2; M = 545 down 111 vs 60; M = 96 down 50 vs 44), far
+// above the modelled cost of parking and folding the partials.
+inline bool ksplit_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("CCB_PAIR_KSPLIT");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
+// workspace + tickets of a K-split plan, per (device, stream)
+int ksplit_buffers(const TabPlan* tp, int M, int F, cudaStream_t st, KSplit* out) {
+  if (tp->slices <= 1) return 0;
+  const int Mpad = (M + 31) / 32 * 32;
+  out->Mpad = Mpad;
+  out->F = F;
+  out->ws = reinterpret_cast<float*>(stream_scratch(st, SCR_PAIR_KSPLIT, (size_t)tp->slices * F * Mpad * sizeof(float)));
+  out->ticket = reinterpret_cast<unsigned*>(
+      zeroed_scratch(st, ZSCR_PAIR_TICKETS, (size_t)(F / TC_BM) * (Mpad / 32) * sizeof(unsigned)));
+  if (!out->ws || !out->ticket) return fail(CC_E_CUDA, "gemm_pair: K-split workspace allocation failed");
+  return 0;
 }
 
 // CCB_GEMM_PAIR=0 disables the CTA-pair plans (A/B measurements)
@@ -1236,7 +1362,7 @@ Tiling pick_tiling(int M, int N, int K, int epi, bool allow_split) {
   }
   // CTA-pair unit table (any epilogue; SwiGLU: [gate 64 | up 64] per 128 rows)
   if (M >= 64 && M <= 8192 && N % (2 * TC_BM) == 0 && pair_enabled()) {
-    const TabPlan* tp = plan_units(M, N, K);
+    const TabPlan* tp = plan_units(M, N, K, allow_split && ksplit_enabled());
     if (tp && tp->t < 0.97 * best_t * kKbCycles) {
       best = Tiling{};
       best.bn = 256;
@@ -1256,8 +1382,8 @@ bool forced_tiling(int M, int N, int K, int epi, Tiling* out) {
     init = true;
     if (const char* e = getenv("CCB_GEMM_FORCE")) sscanf(e, "%d,%d", &fb, &fs);
   }
-  if (fs == 4) {  // CTA-pair unit table
-    const TabPlan* tp = M <= 8192 && N % (2 * TC_BM) == 0 ? plan_units(M, N, K) : nullptr;
+  if (fs == 4 || fs == 5) {  // CTA-pair unit table (5: with fb K slices)
+    const TabPlan* tp = M <= 8192 && N % (2 * TC_BM) == 0 ? plan_units(M, N, K, false, fs == 5 ? fb : 0) : nullptr;
     if (!tp) return false;
     *out = Tiling{};
     out->bn = 256;
@@ -1291,9 +1417,11 @@ int launch_epi(const void* A, int64_t lda, const void* B, int64_t ldb, void* C, 
                   EPI == CC_EPI_RESID_ADD ? -2 : EPI == CC_EPI_SWIGLU ? -3 : -1);
     if (rc) return rc;
     if (int rc2 = ensure_smem(gemm_pair_kernel<EPI>, P2_SMEM)) return rc2;
+    KSplit ksp{};
+    if (int rc2 = ksplit_buffers(tl.tab, M, N, st, &ksp)) return rc2;
     static const int dbg = getenv("CCB_PAIR_DBG") ? atoi(getenv("CCB_PAIR_DBG")) : 0;
     return launch_k(gemm_pair_kernel<EPI>, dim3(tl.grid), dim3(TC_THREADS), P2_SMEM, st, "gemm_pair", mw, mx[0], mx[1],
-                    mx[2], mx[3], mc, M, K, dbg, tl.tab->tab, RopeQkv{});
+                    mx[2], mx[3], mc, M, K, dbg, tl.tab->tab, RopeQkv{}, ksp);
   }
   if constexpr (EPI != CC_EPI_SWIGLU) if (tl.swap) {
     // A slot <- weights B [N][K] (128-row boxes), B slot <- activations A [M][K]
@@ -1351,8 +1479,10 @@ int gemm_qkv_rope_bf16(const void* X, int64_t ldx, const void* Wqkv, int64_t ldw
     return fail(CC_E_UNSUP, "gemm_qkv_rope: shape not covered by the fused epilogue");
   if ((reinterpret_cast<uintptr_t>(X) | reinterpret_cast<uintptr_t>(Wqkv)) & 15)
     return fail(CC_E_UNSUP, "gemm_qkv_rope: pointers must be 16-byte aligned");
-  const TabPlan* tp = plan_units(M, N, K);
+  const TabPlan* tp = plan_units(M, N, K, false);  // (no K split: the same bits as impl 4 + rope_scatter)
   if (!tp) return fail(CC_E_UNSUP, "gemm_qkv_rope: no unit plan");
+  KSplit ksp{};
+  if (int rc = ksplit_buffers(tp, M, N, st, &ksp)) return rc;
   CUtensorMap mw, mx[4];
   int rc = make_map(&mw, Wqkv, N, K, ldw, TC_BM);
   for (int i = 0; i < 4 && !rc; ++i) rc = make_map(&mx[i], X, M, K, ldx, 128 >> i);
@@ -1365,7 +1495,7 @@ int gemm_qkv_rope_bf16(const void* X, int64_t ldx, const void* Wqkv, int64_t ldw
              (__nv_bfloat16*)kv_v, (__nv_bfloat16*)k_rot, Hq, Hkv};
   static const int dbg = getenv("CCB_PAIR_DBG") ? atoi(getenv("CCB_PAIR_DBG")) : 0;
   return launch_k(gemm_pair_kernel<EPI_ROPE_QKV>, dim3(tp->grid), dim3(TC_THREADS), P2_SMEM, st, "gemm_qkv_rope", mw,
-                  mx[0], mx[1], mx[2], mx[3], mq, M, K, dbg, tp->tab, rq);
+                  mx[0], mx[1], mx[2], mx[3], mq, M, K, dbg, tp->tab, rq, ksp);
 }
 
 // o_proj / down_proj of a tensor-parallel rank with the reduce-scatter fused

@@ -219,6 +219,63 @@ print('ok')
     assert torch.equal(outs[0], outs[1])
 
 
+@pytest.mark.parametrize("M,S", [(96, 2), (290, 3), (290, 4), (545, 6)])
+@pytest.mark.parametrize("epi", ["store", "resid", "swiglu", "gelu"])
+def test_gemm_cta_pair_k_split(N, M, S, epi):
+    """CTA-pair units with the K dimension split into S slices (small M):
+    each slice's CTA parks an fp32 partial, the last to finish a unit sums
+    them in slice order and runs the epilogue.  Matches the fp32 reference,
+    equals the unsplit pair plan within fp32 re-association, and is
+    bit-identical from run to run (whichever CTA finishes last)."""
+    import subprocess
+    import sys
+
+    code = f"""
+import torch, sys
+sys.path.insert(0, '.')
+from paper_2502_15734_b200 import _native as N
+M, Nn, K = {M}, 1536, 4096
+g = torch.Generator(device='cuda').manual_seed(7)
+A = torch.randn((M, K), generator=g, device='cuda').bfloat16()
+B = (torch.randn((Nn, K), generator=g, device='cuda') / 64).bfloat16()
+acc = A.float() @ B.float().T
+epi = '{epi}'
+code = dict(store=N.EPI_STORE, resid=N.EPI_RESID_ADD, swiglu=N.EPI_SWIGLU, gelu=N.EPI_GELU)[epi]
+def run():
+    if epi == 'resid':
+        C = torch.ones((M, Nn), device='cuda')
+    elif epi == 'swiglu':
+        C = torch.empty((M, Nn // 2), device='cuda', dtype=torch.bfloat16)
+    else:
+        C = torch.empty((M, Nn), device='cuda', dtype=torch.bfloat16)
+    N.call('cc_gemm', N.ptr(A), K, N.ptr(B), K, N.ptr(C), C.shape[1], M, Nn, K, code, N.BF16, 1, N.stream_ptr())
+    torch.cuda.synchronize()
+    return C
+if epi == 'resid':
+    ref = acc + 1
+elif epi == 'swiglu':
+    a4 = acc.reshape(M, Nn // 128, 2, 64); ref = (torch.nn.functional.silu(a4[:, :, 0]) * a4[:, :, 1]).reshape(M, Nn // 2)
+else:
+    ref = torch.nn.functional.gelu(acc, approximate='tanh') if epi == 'gelu' else acc
+outs = [run() for _ in range(3)]
+torch.testing.assert_close(outs[0].float(), ref, atol=2e-2, rtol=2e-2)
+assert all(torch.equal(outs[0], o) for o in outs[1:])
+torch.save(outs[0].cpu(), sys.argv[1])
+print('ok')
+"""
+    outs = []
+    for i, force in enumerate([f"{S},5", "0,4"]):
+        path = f"/tmp/_ksplit_{epi}_{M}_{S}_{i}.pt"
+        env = dict(__import__("os").environ, CCB_GEMM_FORCE=force, CCB_SW_DEBUG="1")
+        out = subprocess.run([sys.executable, "-c", code, path], capture_output=True, text=True, env=env, timeout=300)
+        assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
+        if i == 0:
+            assert f"slices={S}" in out.stderr, out.stderr[-500:]
+        outs.append(torch.load(path).float())
+    # slices re-associate the fp32 sum: the unsplit result within a bf16 ulp or two
+    torch.testing.assert_close(outs[0], outs[1], atol=1e-2, rtol=1e-2)
+
+
 @pytest.mark.parametrize("Nn", [512, 6144, 1536])
 def test_gemm_tcgen05_m_invariance(N, Nn):
     """A row's result does not depend on how many rows are active (also when
