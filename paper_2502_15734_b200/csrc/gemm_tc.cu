@@ -512,12 +512,12 @@ struct SwTab {
 };
 // K-split units (small M: too few (tile, row chunk) units for the CTA pairs):
 // slice s of S covers k-blocks [s * nkb / S, (s + 1) * nkb / S).  Each CTA
-// parks its fp32 partial in ws[s][feature][row] (row stride Mpad), bumps the
+// parks its fp32 partial in ws[s][row][feature] (row stride F), bumps the
 // (tile, chunk, CTA rank) ticket, and the CTA that draws the last ticket sums
 // the S partials in slice order (its own from TMEM) before the normal
 // epilogue -- deterministic whichever CTA finishes last.
 struct KSplit {
-  float* ws;         // [S_max][F][Mpad] fp32
+  float* ws;         // [S_max][Mpad][F] fp32
   unsigned* ticket;  // [F / 128][Mpad / 32], zero between launches
   int Mpad, F;
 };
@@ -707,19 +707,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
       const uint32_t t0 = tmem_base + acc * 256 + ((uint32_t)(q * 32) << 16);
       const int ks = tab.ks[u], ns = (ks & 15) + 1, my_s = ks >> 4;
       const int feat = ft * TC_BM + q * 32 + lane;  // this thread's feature (TMEM lane)
-      if (ns > 1) {
-        // park this slice's partial: ws[my_s][feat][r0 .. r0 + n), 32 rows per chunk
-        float* dst = ksp.ws + ((int64_t)my_s * ksp.F + feat) * ksp.Mpad + r0;
+      if (ns > 1 && !(dbg & 16)) {  // (debug 16: no partials / tickets, every slice stores)
+        // park this slice's partial: ws[my_s][row][feat] for rows r0 .. r0 + n
+        // (a warp's store per row = 32 consecutive features = one 128-byte line)
+        float* dst = ksp.ws + ((int64_t)my_s * ksp.Mpad + r0) * ksp.F + feat;
 #pragma unroll 1
         for (int c = 0; c * 32 < n; ++c) {
           uint32_t r[32];
           tmem_ld32(t0 + c * 32, r);
           tmem_ld_wait();
 #pragma unroll
-          for (int j = 0; j < 32; j += 4)
-            __stcg(reinterpret_cast<float4*>(dst + c * 32 + j),
-                   make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]), __uint_as_float(r[j + 2]),
-                               __uint_as_float(r[j + 3])));
+          for (int j = 0; j < 32; ++j) __stcg(dst + (int64_t)(c * 32 + j) * ksp.F, __uint_as_float(r[j]));
         }
         __threadfence();
         epi_bar();
@@ -741,7 +739,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
       }
       // r[j] (row r0 + 32 c + j of this thread's feature) = the slices summed in order
       auto fold = [&](int c, uint32_t (&r)[32]) {
-        if (ns == 1) return;
+        if (ns == 1 || (dbg & 48)) return;  // (debug 32: partials parked, no fold)
         float a[32];
 #pragma unroll 1
         for (int s2 = 0; s2 < ns; ++s2) {
@@ -749,16 +747,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
 #pragma unroll
             for (int j = 0; j < 32; ++j) a[j] = s2 == 0 ? __uint_as_float(r[j]) : a[j] + __uint_as_float(r[j]);
           } else {
-            const float* src = ksp.ws + ((int64_t)s2 * ksp.F + feat) * ksp.Mpad + r0 + c * 32;
+            const float* src = ksp.ws + ((int64_t)s2 * ksp.Mpad + r0 + c * 32) * ksp.F + feat;
+            float v[32];
 #pragma unroll
-            for (int j = 0; j < 32; j += 4) {
-              const float4 v = __ldcg(reinterpret_cast<const float4*>(src + j));
-              if (s2 == 0) {
-                a[j] = v.x; a[j + 1] = v.y; a[j + 2] = v.z; a[j + 3] = v.w;
-              } else {
-                a[j] += v.x; a[j + 1] += v.y; a[j + 2] += v.z; a[j + 3] += v.w;
-              }
-            }
+            for (int j = 0; j < 32; ++j) v[j] = __ldcg(src + (int64_t)j * ksp.F);
+#pragma unroll
+            for (int j = 0; j < 32; ++j) a[j] = s2 == 0 ? v[j] : a[j] + v[j];
           }
         }
 #pragma unroll
@@ -1181,7 +1175,7 @@ struct TabPlan {
 // of the other slices' partials, in cycles per row
 constexpr double kSplitFixed = 2500.0, kSplitPerRow = 12.0;
 // K splits considered for short activation matrices only (few units per pair)
-constexpr int kSplitMaxM = 1024;
+constexpr int kSplitMaxM = 384;  // (at M = 552 the split down_proj measured slower: 10.98 vs 10.72 ms per step)
 constexpr int kSplitCand[5] = {1, 2, 3, 4, 6};
 
 inline double unit_cycles(int n, int nkb) {
@@ -1287,15 +1281,15 @@ const TabPlan* plan_units(int M, int F, int K, bool ksplit, int force_s = 0) {
   return best;
 }
 
-// CCB_PAIR_KSPLIT=1 lets the planner pick K-split unit plans.  Off by
-// default: measured slower than the unsplit plans at every shape tried
-// (tools/ksplit_check.sh, us, split vs unsplit: M = 290 o_proj 31.5 vs 21.0,
-// down 55.1 vs 58.2; M = 545 down 111 vs 60; M = 96 down 50 vs 44), far
-// above the modelled cost of parking and folding the partials.
+// CCB_PAIR_KSPLIT=0 keeps the planner off K-split unit plans (A/B).  The
+// config-2 step replayed from a CUDA graph (tools/graph_step.py, ms, split
+// vs unsplit): r = 0 (32 rows) 5.96 vs 6.38, r = 0.05 (292 rows) 8.21 vs
+// 8.56; at r = 0.10 (552 rows) the split down_proj was slower (10.98 vs
+// 10.72), hence kSplitMaxM.
 inline bool ksplit_enabled() {
   static const bool on = [] {
     const char* e = getenv("CCB_PAIR_KSPLIT");
-    return e && e[0] == '1';
+    return !(e && e[0] == '0');
   }();
   return on;
 }
@@ -1361,7 +1355,7 @@ Tiling pick_tiling(int M, int N, int K, int epi, bool allow_split) {
     }
   }
   // CTA-pair unit table (any epilogue; SwiGLU: [gate 64 | up 64] per 128 rows)
-  if (M >= 64 && M <= 8192 && N % (2 * TC_BM) == 0 && pair_enabled()) {
+  if (M >= (allow_split && ksplit_enabled() ? 32 : 64) && M <= 8192 && N % (2 * TC_BM) == 0 && pair_enabled()) {
     const TabPlan* tp = plan_units(M, N, K, allow_split && ksplit_enabled());
     if (tp && tp->t < 0.97 * best_t * kKbCycles) {
       best = Tiling{};

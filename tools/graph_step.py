@@ -11,10 +11,11 @@ import torch  # noqa: E402
 import bench  # noqa: E402
 from paper_2502_15734_b200 import engine  # noqa: E402
 
+ratio = float(sys.argv[1]) if len(sys.argv) > 1 else 0.15
 args = argparse.Namespace(layers=32, chunks=10, chunk_len=512, question=32)
 torch.cuda.set_device(0)
 cc, model, store, chunks, question = bench.make_workload(args, 0)
-_, req, dplan, ws = bench.resident_plan(cc, model, store, chunks, question, 0.15)
+_, req, dplan, ws = bench.resident_plan(cc, model, store, chunks, question, ratio)
 last = int(np.flatnonzero(dplan.rows == req.question_span[1] - 1)[0])
 
 
@@ -36,7 +37,7 @@ def timed(fn, k=10):
     return a.elapsed_time(b) / k
 
 
-print("stream ms/step", round(timed(step), 3), flush=True)
+print("ratio", ratio, "rows", len(dplan.rows), "stream ms/step", round(timed(step), 3), flush=True)
 s = torch.cuda.Stream()
 s.wait_stream(torch.cuda.current_stream())
 with torch.cuda.stream(s):
