@@ -276,6 +276,36 @@ print('ok')
     torch.testing.assert_close(outs[0], outs[1], atol=1e-2, rtol=1e-2)
 
 
+def test_gemm_k_split_concurrent_streams(N):
+    """K-split units on several CUDA streams at once (the serving mode runs
+    requests on separate streams): each stream has its own partial workspace
+    and tickets, so concurrent launches give the single-stream bits."""
+    M, Nn, K = 96, 4096, 14336
+    g = torch.Generator(device="cuda").manual_seed(11)
+    A = [torch.randn((M, K), generator=g, device="cuda").bfloat16() for _ in range(4)]
+    B = (torch.randn((Nn, K), generator=g, device="cuda") / 64).bfloat16()
+
+    def run(i, stream):
+        C = torch.ones((M, Nn), device="cuda")
+        stream.wait_stream(torch.cuda.current_stream())  # (C is filled on the current stream)
+        N.call("cc_gemm", N.ptr(A[i]), K, N.ptr(B), K, N.ptr(C), Nn, M, Nn, K, N.EPI_RESID_ADD, N.BF16, 0,
+               N.stream_ptr(stream))
+        return C
+
+    base = []
+    for i in range(4):
+        base.append(run(i, torch.cuda.current_stream()))
+    torch.cuda.synchronize()
+    streams = [torch.cuda.Stream() for _ in range(4)]
+    for rep in range(3):
+        outs = [run(i, streams[i]) for i in range(4)]
+        torch.cuda.synchronize()
+        for i in range(4):
+            assert torch.equal(outs[i], base[i]), (rep, i)
+    ref = A[0].float() @ B.float().T + 1
+    torch.testing.assert_close(base[0], ref, atol=2e-2, rtol=2e-2)
+
+
 @pytest.mark.parametrize("Nn", [512, 6144, 1536])
 def test_gemm_tcgen05_m_invariance(N, Nn):
     """A row's result does not depend on how many rows are active (also when
