@@ -887,19 +887,23 @@ int cc_gather_rope_kv(const void* pool, int64_t pool_layer_stride, int64_t pool_
             break;
           }
         const auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
-        CCB_REQUIRE((cols * sizeof(T)) % 16 == 0 && (kv_width * sizeof(T)) % 16 == 0 &&
-                        (pool_layer_stride * sizeof(T)) % 16 == 0 && (pool_block_stride * sizeof(T)) % 16 == 0 &&
-                        (req_layer_stride * sizeof(T)) % 16 == 0 && al(pool) && al(kv_k) && al(kv_v) && al(k_rot),
-                    "gather_rope_kv: rows and buffers must be 16-byte aligned");
-        const size_t smem = 2 * 16 * (size_t)cols * sizeof(T) + 16;
-        auto kern = gather_rope_bulk_kernel<T, V>;
-        if (int e = ensure_smem(kern, smem)) return e;
-        const int64_t nx = (int64_t)n_items * (kv_width / cols);
-        CCB_REQUIRE(nx <= 0x7fffffff, "gather_rope_kv: grid too large");
-        return launch_k(kern, dim3((unsigned)nx, l1 - l0), dim3(256), smem, as_stream(stream), "gather_rope_kv",
-                        (const T*)pool, pool_layer_stride, pool_block_stride, items, l0, slot_pos, active_until,
-                        (const typename CS<T>::type*)rope_table, (T*)kv_k, (T*)kv_v, (T*)k_rot, req_layer_stride,
-                        kv_width, d_head, cols, k1_ldg == 2 ? 1 : 0);
+        // bulk copies need 16-byte aligned rows and buffers; other layouts (none
+        // in the engine) take the register-path kernel below (the same bits)
+        const bool bulk_ok = (cols * sizeof(T)) % 16 == 0 && (kv_width * sizeof(T)) % 16 == 0 &&
+                             (pool_layer_stride * sizeof(T)) % 16 == 0 && (pool_block_stride * sizeof(T)) % 16 == 0 &&
+                             (req_layer_stride * sizeof(T)) % 16 == 0 && al(pool) && al(kv_k) && al(kv_v) &&
+                             al(k_rot) && 2 * 16 * (size_t)cols * sizeof(T) <= 200 * 1024;
+        if (bulk_ok) {
+          const size_t smem = 2 * 16 * (size_t)cols * sizeof(T) + 16;
+          auto kern = gather_rope_bulk_kernel<T, V>;
+          if (int e = ensure_smem(kern, smem)) return e;
+          const int64_t nx = (int64_t)n_items * (kv_width / cols);
+          CCB_REQUIRE(nx <= 0x7fffffff, "gather_rope_kv: grid too large");
+          return launch_k(kern, dim3((unsigned)nx, l1 - l0), dim3(256), smem, as_stream(stream), "gather_rope_kv",
+                          (const T*)pool, pool_layer_stride, pool_block_stride, items, l0, slot_pos, active_until,
+                          (const typename CS<T>::type*)rope_table, (T*)kv_k, (T*)kv_v, (T*)k_rot, req_layer_stride,
+                          kv_width, d_head, cols, k1_ldg == 2 ? 1 : 0);
+        }
       }
       dim3 grid(n_items, l1 - l0);
       return launch_k(gather_rope_kernel<T, V>, grid, dim3(256), 0, as_stream(stream), "gather_rope_kv",
