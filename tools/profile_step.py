@@ -18,8 +18,13 @@ from paper_2502_15734_b200 import engine  # noqa: E402
 p = argparse.ArgumentParser()
 p.add_argument("--ratio", type=float, default=0.15)
 p.add_argument("--full", action="store_true", help="profile the full-recompute baseline step instead")
+p.add_argument("--config", default="8b", choices=["8b", "8b-32k", "70b"])
 a = p.parse_args()
-args = argparse.Namespace(layers=32, chunks=10, chunk_len=512, question=32)
+args = argparse.Namespace(layers=32, chunks=10, chunk_len=512, question=32, config=a.config, tp_peer=0)
+if a.config == "8b-32k":
+    args.chunks = 64
+elif a.config == "70b":
+    args.chunks, args.chunk_len, args.layers = 16, 1024, 80
 torch.cuda.set_device(0)
 cc, model, store, chunks, question = bench.make_workload(args, 0)
 if a.full:
