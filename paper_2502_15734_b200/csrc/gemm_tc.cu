@@ -1357,7 +1357,11 @@ Tiling pick_tiling(int M, int N, int K, int epi, bool allow_split) {
   // CTA-pair unit table (any epilogue; SwiGLU: [gate 64 | up 64] per 128 rows)
   if (M >= (allow_split && ksplit_enabled() ? 32 : 64) && M <= 8192 && N % (2 * TC_BM) == 0 && pair_enabled()) {
     const TabPlan* tp = plan_units(M, N, K, allow_split && ksplit_enabled());
-    if (tp && tp->t < 0.97 * best_t * kKbCycles) {
+    // below 64 rows the 1-CTA stream-K tiles measured far slower than their
+    // model (r = 0 step: o_proj 29 us for 33.5 MB, QKV 29 us for 50 MB, i.e.
+    // 1.2-1.8 TB/s) while the K-split pair units stream at 3.7 TB/s (down):
+    // take the pair plan there whenever one exists
+    if (tp && ((M < 64 && tp->slices > 1) || tp->t < 0.97 * best_t * kKbCycles)) {
       best = Tiling{};
       best.bn = 256;
       best.tab = tp;
