@@ -51,7 +51,9 @@ constexpr int AT_KST = 3;  // K ring depth
 constexpr int AT_VST = 2;  // V ring depth = P buffers: V slot i % 2 is released by PV_i's p_empty commit
 constexpr int AT_THREADS = 320;  // TMA warp, MMA warp, 2 x 4 softmax warps
 constexpr int AT_MAXT = 512;     // row tiles the in-kernel work plan handles (more: no key splits)
-constexpr int AT_MAXP = 4;       // key-range parts per row tile (8 measured slower at r = 0)
+constexpr int AT_MAXP = 4;       // key-range parts per row tile, merged by the last part (8 measured slower at r = 0)
+constexpr int AT_MAXP_EXT = 16;  // key parts with the separate merge kernel (ping-pong kernel, few items)
+constexpr int kExtMaxItems = 16; // (group, block) items up to which the ping-pong kernel uses it
 
 // MN-major operand (B = V: N = head dim contiguous, K = keys), 128B swizzle:
 // 64-element atoms along N at `lbo` bytes, 8-key groups at 1024 B.
@@ -736,7 +738,7 @@ __global__ void __launch_bounds__(384, 1)
                    const uint8_t* __restrict__ key_pad, __nv_bfloat16* __restrict__ ctx, float* __restrict__ lse,
                    int n_q, int n_keys, int Hq, int G, float scale_log2, int n_groups, int n_blocks, int target,
                    int max_parts, float* __restrict__ ws_o, float2* __restrict__ ws_ml, int* __restrict__ counters,
-                   long long* __restrict__ trace) {
+                   int pstride, int ext, long long* __restrict__ trace) {
   using SM = Pp<DH>;
   constexpr int BN = SM::BN, KST = SM::KST, VST = SM::VST, NT = SM::THREADS;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -1105,7 +1107,7 @@ __global__ void __launch_bounds__(384, 1)
       // the block to finish merges all of them in part order
       const int key = g * T + blk, mm = X * 128 + m;
       const bool any = nX > 0 && m_run != -INFINITY;
-      float4* my_o = reinterpret_cast<float4*>(ws_o) + ((int64_t)key * AT_MAXP + part) * (DH / 4) * 256 + mm;
+      float4* my_o = reinterpret_cast<float4*>(ws_o) + ((int64_t)key * pstride + part) * (DH / 4) * 256 + mm;
 #pragma unroll 1
       for (int c = 0; c < DH / 32; ++c) {
         uint32_t r[32];
@@ -1120,8 +1122,9 @@ __global__ void __launch_bounds__(384, 1)
                                    __uint_as_float(r[4 * e + 2]), __uint_as_float(r[4 * e + 3]))
                      : make_float4(0.f, 0.f, 0.f, 0.f));
       }
-      __stcg(&ws_ml[((int64_t)key * AT_MAXP + part) * 256 + mm],
+      __stcg(&ws_ml[((int64_t)key * pstride + part) * 256 + mm],
              make_float2(any ? m_run * scale_log2 : -INFINITY, any ? l_run : 0.f));
+      if (!ext) {  // (ext: the merge kernel attn_pp_merge folds the parts)
       __threadfence();
       asm volatile("bar.sync 1, 256;" ::: "memory");
       if (warp == 4 && lane == 0) {
@@ -1136,7 +1139,7 @@ __global__ void __launch_bounds__(384, 1)
         float M = -INFINITY;
 #pragma unroll
         for (int p = 0; p < AT_MAXP; ++p) {
-          const float2 ml = p < parts ? __ldcg(&ws_ml[((int64_t)key * AT_MAXP + p) * 256 + mm])
+          const float2 ml = p < parts ? __ldcg(&ws_ml[((int64_t)key * pstride + p) * 256 + mm])
                                       : make_float2(-INFINITY, 0.f);
           mp[p] = ml.x;
           lp[p] = ml.y;
@@ -1159,7 +1162,7 @@ __global__ void __launch_bounds__(384, 1)
             for (int p = 0; p < AT_MAXP; ++p) {
               if (p < parts) {
                 const float4* op =
-                    reinterpret_cast<const float4*>(ws_o) + ((int64_t)key * AT_MAXP + p) * (DH / 4) * 256 + (cg * 8) * 256 + mm;
+                    reinterpret_cast<const float4*>(ws_o) + ((int64_t)key * pstride + p) * (DH / 4) * 256 + (cg * 8) * 256 + mm;
                 float a[32];
                 ld8_f4_cg_4k(op, a);
 #pragma unroll
@@ -1179,6 +1182,7 @@ __global__ void __launch_bounds__(384, 1)
           }
           lse[(int64_t)row * Hq + head] = lt > 0.f ? (M + log2f(lt)) * 0.6931471805599453f : -INFINITY;
         }
+      }
       }
     } else {
       const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
@@ -1357,11 +1361,12 @@ int launch(const void* q, const void* k, const void* v, const int32_t* q_slot, c
 // scheduled longest-first onto the SMs (the kernel's own order).  Measured at
 // the 70B rank shape: 102.8 us (16/3) vs 135.5 us for the old rule (65/2);
 // config 2 (21/2) and r = 0.05 (11/4) keep their plans.  Cached per shape.
-std::pair<int, int> pp_split_plan(int T, int groups, int max_tiles, int slots) {
+std::pair<int, int> pp_split_plan(int T, int groups, int max_tiles, int slots, int maxp_cap = AT_MAXP,
+                                  double merge_cost = 2.0) {
   static std::mutex mu;
   static std::map<std::tuple<int, int, int, int>, std::pair<int, int>> cache;
   std::lock_guard<std::mutex> g(mu);
-  const auto key = std::make_tuple(T, groups, max_tiles, slots);
+  const auto key = std::make_tuple(T, groups, max_tiles, slots * 64 + maxp_cap);
   auto it = cache.find(key);
   if (it != cache.end()) return it->second;
   double best = 1e30;
@@ -1369,13 +1374,13 @@ std::pair<int, int> pp_split_plan(int T, int groups, int max_tiles, int slots) {
   std::pair<int, int> plan{max_tiles, 1};
   std::vector<double> ctas;
   std::vector<double> load(slots);
-  for (int maxp = 1; maxp <= AT_MAXP; ++maxp)
+  for (int maxp = 1; maxp <= maxp_cap; ++maxp)
     for (int target = std::max(1, std::min(8, max_tiles)); target <= max_tiles; ++target) {
       ctas.clear();
       for (int t = 0; t < T; ++t) {
         const int est = (int)(((int64_t)max_tiles * (t + 1) + T - 1) / T);
         const int parts = std::max(1, std::min(maxp, (est + target - 1) / target));
-        const double c = (est + parts - 1) / parts + 3.0 + (parts > 1 ? 2.0 : 0.0);
+        const double c = (est + parts - 1) / parts + 3.0 + (parts > 1 ? merge_cost : 0.0);
         for (int k = 0; k < groups * parts; ++k) ctas.push_back(c);
       }
       std::sort(ctas.begin(), ctas.end(), std::greater<double>());
@@ -1396,6 +1401,77 @@ std::pair<int, int> pp_split_plan(int T, int groups, int max_tiles, int slots) {
     }
   cache[key] = plan;
   return plan;
+}
+
+// Key-part merge for the ping-pong kernel's "ext" mode (few (group, block)
+// items, many key parts): the parts only park their partials; this kernel
+// folds them, one CTA per (item, 32 output columns), one thread per M-row,
+// in part order (the same arithmetic as the in-kernel merge).  Items whose
+// block was not split were written by the attention kernel itself.
+template <int DH>
+__global__ void __launch_bounds__(256) attn_pp_merge(const float* __restrict__ ws_o, const float2* __restrict__ ws_ml,
+                                                     const int32_t* __restrict__ q_slot, __nv_bfloat16* __restrict__ ctx,
+                                                     float* __restrict__ lse, int n_q, int n_keys, int Hq, int G,
+                                                     int n_blocks, int target, int max_parts, int pstride) {
+  constexpr int BN = Pp<DH>::BN;
+  pdl_trigger();
+  pdl_wait();
+  const int key = blockIdx.x, cg = blockIdx.y, mm = threadIdx.x;
+  const int g = key / n_blocks, blk = key % n_blocks;
+  const int RB = 2 * (128 / G);
+  const int kq = q_slot[min((blk + 1) * RB, n_q) - 1];
+  const int est = kq < 0 ? 0 : min(kq, n_keys - 1) / BN + 1;
+  const int parts = max(1, min(max_parts, (est + target - 1) / target));
+  if (parts <= 1) return;
+  const int row = blk * RB + mm / G, head = g * G + mm % G;
+  if (row >= n_q) return;
+  // all (max, sum) pairs in one round trip, then the partial rows four parts
+  // per round trip (the loads of a group go out together)
+  float mp[AT_MAXP_EXT], lp[AT_MAXP_EXT];
+  float M = -INFINITY;
+#pragma unroll
+  for (int p = 0; p < AT_MAXP_EXT; ++p) {
+    const float2 ml = p < parts ? __ldcg(&ws_ml[((int64_t)key * pstride + p) * 256 + mm]) : make_float2(-INFINITY, 0.f);
+    mp[p] = ml.x;
+    lp[p] = ml.y;
+  }
+#pragma unroll
+  for (int p = 0; p < AT_MAXP_EXT; ++p) M = fmaxf(M, mp[p]);
+  float lt = 0.f;
+  float v[32];
+#pragma unroll
+  for (int e = 0; e < 32; ++e) v[e] = 0.f;
+#pragma unroll
+  for (int p0 = 0; p0 < AT_MAXP_EXT; p0 += 4) {
+    if (p0 >= parts) break;
+    float a[4][32];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (p0 + i < parts)
+        ld8_f4_cg_4k(reinterpret_cast<const float4*>(ws_o) + ((int64_t)key * pstride + p0 + i) * (DH / 4) * 256 +
+                         (cg * 8) * 256 + mm,
+                     a[i]);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      if (p0 + i >= parts) break;
+      const float w = mp[p0 + i] == -INFINITY ? 0.f : exp2f(mp[p0 + i] - M);
+      lt = fmaf(lp[p0 + i], w, lt);
+#pragma unroll
+      for (int e = 0; e < 32; ++e) v[e] = fmaf(a[i][e], w, v[e]);
+    }
+  }
+  const float inv = lt > 0.f ? 1.f / lt : 0.f;
+  uint4 pk[4];
+  uint32_t* pw = reinterpret_cast<uint32_t*>(pk);
+#pragma unroll
+  for (int e = 0; e < 16; ++e) {
+    __nv_bfloat162 hv = __floats2bfloat162_rn(v[2 * e] * inv, v[2 * e + 1] * inv);
+    pw[e] = *reinterpret_cast<uint32_t*>(&hv);
+  }
+  uint4* o4 = reinterpret_cast<uint4*>(ctx + ((int64_t)row * Hq + head) * DH + cg * 32);
+#pragma unroll
+  for (int e = 0; e < 4; ++e) o4[e] = pk[e];
+  if (cg == 0) lse[(int64_t)row * Hq + head] = lt > 0.f ? (M + log2f(lt)) * 0.6931471805599453f : -INFINITY;
 }
 
 template <int DH, int PF = 2, int RH = 224>
@@ -1430,8 +1506,13 @@ int launch_pp(const void* q, const void* k, const void* v, const int32_t* q_slot
   const int slots = num_sms();
   const int max_tiles = (n_keys + BN - 1) / BN;
   int target = max_tiles, max_parts = 1;
+  // few (group, block) items: up to AT_MAXP_EXT key parts, merged by a
+  // second kernel (attn_pp_merge) instead of the last part
+  static const int ext_env = getenv("CCB_ATTN_EXT") ? atoi(getenv("CCB_ATTN_EXT")) : -1;
+  const bool ext = ext_env >= 0 ? ext_env > 0 : Hkv * blocks <= kExtMaxItems;
   if (blocks <= AT_MAXT && max_tiles > 0 && Hkv * blocks < slots) {
-    const std::pair<int, int> plan = pp_split_plan(blocks, Hkv, max_tiles, slots);
+    const std::pair<int, int> plan =
+        ext ? pp_split_plan(blocks, Hkv, max_tiles, slots, AT_MAXP_EXT, 1.0) : pp_split_plan(blocks, Hkv, max_tiles, slots);
     target = plan.first;
     max_parts = std::min(plan.second, (max_tiles + target - 1) / target);
     if (max_parts < 1) max_parts = 1;
@@ -1439,28 +1520,35 @@ int launch_pp(const void* q, const void* k, const void* v, const int32_t* q_slot
   if (getenv("CCB_ATTN_NOSPLIT")) max_parts = 1;
   if (const char* e = getenv("CCB_ATTN_SPLIT")) {  // experiments: "target,max_parts"
     int a = 0, b = 0;
-    if (sscanf(e, "%d,%d", &a, &b) == 2 && a > 0 && b >= 1 && b <= AT_MAXP && blocks <= AT_MAXT) {
+    if (sscanf(e, "%d,%d", &a, &b) == 2 && a > 0 && b >= 1 && b <= (ext ? AT_MAXP_EXT : AT_MAXP) &&
+        blocks <= AT_MAXT) {
       target = a;
       max_parts = b;
     }
   }
+  const int pstride = ext ? max_parts : AT_MAXP;
   float* ws_o = nullptr;
   float2* ws_ml = nullptr;
   int* counters = nullptr;
   if (max_parts > 1) {
     const size_t keys = (size_t)Hkv * blocks;
-    const size_t bytes = keys * AT_MAXP * 256 * (DH * sizeof(float) + sizeof(float2));
+    const size_t bytes = keys * pstride * 256 * (DH * sizeof(float) + sizeof(float2));
     uint8_t* scratch = (uint8_t*)stream_scratch(st, SCR_ATTN, bytes);
     counters = split_counters(st, (int)keys);
     if (!scratch || !counters) return fail(CC_E_CUDA, "attention_tc: split workspace allocation failed");
     ws_o = reinterpret_cast<float*>(scratch);
-    ws_ml = reinterpret_cast<float2*>(scratch + keys * AT_MAXP * 256 * DH * sizeof(float));
+    ws_ml = reinterpret_cast<float2*>(scratch + keys * pstride * 256 * DH * sizeof(float));
   }
+  const bool ext_merge = ext && max_parts > 1;
   dim3 grid(Hkv * blocks * max_parts);
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)DH);
-  return launch_k(attn_pp_kernel<DH, PF, RH>, grid, dim3(SM::THREADS), SM::TOTAL, st, "attention_pp", mq, mk, mv, q_slot,
-                  key_pad, (__nv_bfloat16*)ctx, lse, n_q, n_keys, Hq, G, scale_log2, Hkv, blocks, target, max_parts,
-                  ws_o, ws_ml, counters, g_attn_trace);
+  int rc = launch_k(attn_pp_kernel<DH, PF, RH>, grid, dim3(SM::THREADS), SM::TOTAL, st, "attention_pp", mq, mk, mv,
+                    q_slot, key_pad, (__nv_bfloat16*)ctx, lse, n_q, n_keys, Hq, G, scale_log2, Hkv, blocks, target,
+                    max_parts, ws_o, ws_ml, counters, pstride, ext_merge ? 1 : 0, g_attn_trace);
+  if (rc || !ext_merge) return rc;
+  return launch_k(attn_pp_merge<DH>, dim3(Hkv * blocks, DH / 32), dim3(256), 0, st, "attention_pp_merge",
+                  (const float*)ws_o, (const float2*)ws_ml, q_slot, (__nv_bfloat16*)ctx, lse, n_q, n_keys, Hq, G,
+                  blocks, target, max_parts, pstride);
 }
 
 // Kernel shape per launch: 0 = 128-key tiles, two softmax warpgroups (one
