@@ -1405,7 +1405,7 @@ std::pair<int, int> pp_split_plan(int T, int groups, int max_tiles, int slots, i
 
 // Key-part merge for the ping-pong kernel's "ext" mode (few (group, block)
 // items, many key parts): the parts only park their partials; this kernel
-// folds them, one CTA per (item, 32 output columns), one thread per M-row,
+// folds them, one CTA per (item, 16 output columns), one thread per M-row,
 // in part order (the same arithmetic as the in-kernel merge).  Items whose
 // block was not split were written by the attention kernel itself.
 template <int DH>
@@ -1425,8 +1425,8 @@ __global__ void __launch_bounds__(256) attn_pp_merge(const float* __restrict__ w
   if (parts <= 1) return;
   const int row = blk * RB + mm / G, head = g * G + mm % G;
   if (row >= n_q) return;
-  // all (max, sum) pairs in one round trip, then the partial rows four parts
-  // per round trip (the loads of a group go out together)
+  // all (max, sum) pairs in one round trip, then this CTA's 16 columns of the
+  // partial rows eight parts per round trip (the loads of a group go out together)
   float mp[AT_MAXP_EXT], lp[AT_MAXP_EXT];
   float M = -INFINITY;
 #pragma unroll
@@ -1438,39 +1438,46 @@ __global__ void __launch_bounds__(256) attn_pp_merge(const float* __restrict__ w
 #pragma unroll
   for (int p = 0; p < AT_MAXP_EXT; ++p) M = fmaxf(M, mp[p]);
   float lt = 0.f;
-  float v[32];
+  float v[16];
 #pragma unroll
-  for (int e = 0; e < 32; ++e) v[e] = 0.f;
+  for (int e = 0; e < 16; ++e) v[e] = 0.f;
 #pragma unroll
-  for (int p0 = 0; p0 < AT_MAXP_EXT; p0 += 4) {
+  for (int p0 = 0; p0 < AT_MAXP_EXT; p0 += 8) {
     if (p0 >= parts) break;
-    float a[4][32];
+    float4 a[8][4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
-      if (p0 + i < parts)
-        ld8_f4_cg_4k(reinterpret_cast<const float4*>(ws_o) + ((int64_t)key * pstride + p0 + i) * (DH / 4) * 256 +
-                         (cg * 8) * 256 + mm,
-                     a[i]);
+    for (int i = 0; i < 8; ++i)
+      if (p0 + i < parts) {
+        const float4* op = reinterpret_cast<const float4*>(ws_o) + ((int64_t)key * pstride + p0 + i) * (DH / 4) * 256 +
+                           (cg * 4) * 256 + mm;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
+        for (int c = 0; c < 4; ++c) a[i][c] = __ldcg(op + c * 256);
+      }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
       if (p0 + i >= parts) break;
       const float w = mp[p0 + i] == -INFINITY ? 0.f : exp2f(mp[p0 + i] - M);
       lt = fmaf(lp[p0 + i], w, lt);
 #pragma unroll
-      for (int e = 0; e < 32; ++e) v[e] = fmaf(a[i][e], w, v[e]);
+      for (int c = 0; c < 4; ++c) {
+        v[4 * c] = fmaf(a[i][c].x, w, v[4 * c]);
+        v[4 * c + 1] = fmaf(a[i][c].y, w, v[4 * c + 1]);
+        v[4 * c + 2] = fmaf(a[i][c].z, w, v[4 * c + 2]);
+        v[4 * c + 3] = fmaf(a[i][c].w, w, v[4 * c + 3]);
+      }
     }
   }
   const float inv = lt > 0.f ? 1.f / lt : 0.f;
-  uint4 pk[4];
+  uint4 pk[2];
   uint32_t* pw = reinterpret_cast<uint32_t*>(pk);
 #pragma unroll
-  for (int e = 0; e < 16; ++e) {
+  for (int e = 0; e < 8; ++e) {
     __nv_bfloat162 hv = __floats2bfloat162_rn(v[2 * e] * inv, v[2 * e + 1] * inv);
     pw[e] = *reinterpret_cast<uint32_t*>(&hv);
   }
-  uint4* o4 = reinterpret_cast<uint4*>(ctx + ((int64_t)row * Hq + head) * DH + cg * 32);
+  uint4* o4 = reinterpret_cast<uint4*>(ctx + ((int64_t)row * Hq + head) * DH + cg * 16);
 #pragma unroll
-  for (int e = 0; e < 4; ++e) o4[e] = pk[e];
+  for (int e = 0; e < 2; ++e) o4[e] = pk[e];
   if (cg == 0) lse[(int64_t)row * Hq + head] = lt > 0.f ? (M + log2f(lt)) * 0.6931471805599453f : -INFINITY;
 }
 
@@ -1546,7 +1553,7 @@ int launch_pp(const void* q, const void* k, const void* v, const int32_t* q_slot
                     q_slot, key_pad, (__nv_bfloat16*)ctx, lse, n_q, n_keys, Hq, G, scale_log2, Hkv, blocks, target,
                     max_parts, ws_o, ws_ml, counters, pstride, ext_merge ? 1 : 0, g_attn_trace);
   if (rc || !ext_merge) return rc;
-  return launch_k(attn_pp_merge<DH>, dim3(Hkv * blocks, DH / 32), dim3(256), 0, st, "attention_pp_merge",
+  return launch_k(attn_pp_merge<DH>, dim3(Hkv * blocks, DH / 16), dim3(256), 0, st, "attention_pp_merge",
                   (const float*)ws_o, (const float2*)ws_ml, q_slot, (__nv_bfloat16*)ctx, lse, n_q, n_keys, Hq, G,
                   blocks, target, max_parts, pstride);
 }
