@@ -368,6 +368,52 @@ def _attn_ref(q, k, v, q_slot, pad, Hq, Hkv):
     return torch.einsum("hqk,khd->qhd", p, vv).reshape(q.shape[0], Hq * dh), torch.logsumexp(s, dim=-1).T
 
 
+@pytest.mark.parametrize("ext", ["0", "1"])
+@pytest.mark.parametrize("n_rows,n", [(32, 5152), (150, 2100), (300, 5152)])
+def test_attention_key_part_merge_modes(N, ext, n_rows, n):
+    """The ping-pong kernel's key parts merged by the last part (CCB_ATTN_EXT=0)
+    or by the separate attn_pp_merge kernel (=1, up to 16 parts; the default
+    for <= 16 items): both match torch fp32 and are deterministic."""
+    import subprocess
+    import sys
+
+    code = f"""
+import math, sys, torch
+sys.path.insert(0, '.')
+sys.path.insert(0, 'tests')
+from paper_2502_15734_b200 import _native as N
+from test_gpu_kernels import _attn_ref
+Hq, Hkv, dh, n = 32, 8, 128, {n}
+g = torch.Generator(device='cuda').manual_seed(3)
+rows = torch.sort(torch.randperm(n, generator=g, device='cuda')[:{n_rows}]).values.int()
+rows[-1] = n - 1
+rows = torch.unique(rows).int().contiguous()
+q = torch.randn((rows.numel(), Hq, dh), generator=g, device='cuda').bfloat16()
+k = torch.randn((n, Hkv, dh), generator=g, device='cuda').bfloat16()
+v = torch.randn((n, Hkv, dh), generator=g, device='cuda').bfloat16()
+pad = torch.zeros(n, dtype=torch.uint8, device='cuda')
+pad[40:52] = 1
+rows = rows[pad[rows.long()] == 0].contiguous()
+q = q[: rows.numel()].contiguous()
+outs = []
+for _ in range(2):
+    ctx = torch.zeros((rows.numel(), Hq * dh), dtype=torch.bfloat16, device='cuda')
+    lse = torch.zeros((rows.numel(), Hq), dtype=torch.float32, device='cuda')
+    N.call('cc_attention', N.ptr(q), N.ptr(k), N.ptr(v), N.ptr(rows), N.ptr(pad), N.ptr(ctx), N.ptr(lse),
+           rows.numel(), n, Hq, Hkv, dh, N.BF16, 1, N.stream_ptr())
+    torch.cuda.synchronize()
+    outs.append((ctx, lse))
+ref, ref_lse = _attn_ref(q, k, v, rows, pad, Hq, Hkv)
+torch.testing.assert_close(outs[0][0].float(), ref, atol=3e-2, rtol=3e-2)
+torch.testing.assert_close(outs[0][1], ref_lse, atol=2e-3, rtol=1e-3)
+assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
+print('ok')
+"""
+    env = dict(__import__("os").environ, CCB_ATTN_EXT=ext)
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=300)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
+
+
 @pytest.mark.parametrize("Hq,Hkv,dh,n", [(32, 8, 128, 700), (4, 4, 64, 700), (8, 1, 128, 700), (16, 2, 64, 700),
                                           (32, 8, 128, 2100), (64, 8, 128, 300), (32, 8, 128, 5152)])
 @pytest.mark.parametrize("variant", [0, 1, 2, 3, 4])
