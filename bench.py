@@ -622,7 +622,9 @@ def run_reference_arm(args, rank, world):
             f"{n_prompt}-token fix-up request per step (same chunks, question and K9 recompute rows; seeded "
             f"weights and caches), extrapolated x{args.layers}")
     line = {"impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
+            "steps": args.steps, "warmup": args.warmup,
+            # (extrapolated: one full request through all layers at the measured rate)
+            "ms_per_step": round(n_prompt / value * 1e3, 3), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": workload_config(args, world),
             "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": ncores, "kind": "port", "sample": desc},
